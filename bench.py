@@ -1,0 +1,331 @@
+#!/usr/bin/env python3
+"""Benchmark: umc multi-component compress + decompress on B200.
+
+Metric (BASELINE.json): compress & decompress GB/s of field data at 1 B200,
+and % of the HBM roofline. Workload = BASELINE config 3 (3D jittered
+tetrahedral-lattice mesh, 512^3 = 134,217,728 vertices, vertex order
+permuted, fp64 64-mode Fourier field, 256^3 grid, relative bound 1e-4,
+rho 0.5, nearest g), synthetic and seeded (data generated on the GPU).
+
+A step = one compress + one decompress of the field with inputs resident in
+HBM (inputs are 1.07 GB, larger than the 126 MB L2: no flush needed).
+`value` = field bytes / step time. `e2e` = the same metric through the
+host-buffer C ABI (umcg_compress_host / umcg_decompress_host) with pinned
+host buffers, H2D/D2H inside the timed region.
+
+--impl reference times the unmodified reference (oracle/_ref, compiled from
+the reference's headers) on the host cores: one compress+decompress per
+thread per step on a bounded sample of the same workload.
+
+Multi-GPU: replicas only (the north star is single-GPU; independent fields
+go to independent GPUs with a replicated plan, no collective on the data
+path). value = all ranks' field bytes / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "compress & decompress GB/s of field data at 1 B200; % of HBM roofline"
+SEED = 0x250106910 + 3
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = f"/tmp/umcg_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+            sm = [float(r[0]) for r in rows]
+            mx = max(float(r[1]) for r in rows)
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            reasons = sorted({names[k] for r in rows for k in range(4) if "Active" in r[3 + k]})
+            return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": reasons,
+                    "samples": len(rows)}
+        except Exception as e:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": str(e)[:80]}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def setup_config3(lattice: int, grid: int, dev, keep_coords=False):
+    import torch
+    import paper_2501_06910_b200 as umcg
+    xyz, x = umcg.gen_config(3, lattice, SEED, device=dev)
+    axes = [np.linspace(0.0, 1.0, grid) for _ in range(3)]  # uniform axes over the exact bbox
+    plan = umcg.Plan.build(axes, xyz, keep_coords=keep_coords)
+    del xyz
+    torch.cuda.synchronize()
+    return plan, x
+
+
+def algorithmic_bytes(n, n1, archive):
+    """compulsory traffic of the two-pass algorithm, nearest g, V=1, s=8."""
+    b_c = 32 * n + 20 * n1 + archive
+    b_d = 20 * n + 8 * n1 + archive
+    return b_c, b_d
+
+
+def cpu_reference_sample(lattice: int, grid: int, threads: int, reps: int, tau: float):
+    """Time the unmodified reference (oracle/_ref) on a bounded sample of the
+    config-3 workload: `threads` concurrent compress+decompress calls."""
+    import torch
+    import paper_2501_06910_b200 as umcg
+    from oracle.bindings import Ref, Setup
+    xyz, x = umcg.gen_config(3, lattice, SEED, device="cuda")
+    axes = [np.linspace(0.0, 1.0, grid) for _ in range(3)]
+    plan = umcg.Plan.build(axes, xyz)
+    mode, gaxes, assign, visited = plan.export()
+    xh = x.cpu().numpy()
+    del xyz, x
+    torch.cuda.empty_cache()
+    R = Ref()
+    s = Setup(dim=3, axes=gaxes, mode=mode, assignments=assign, visited=visited)
+    ctx = R.ctx(s)
+    n = len(xh)
+    results = []
+
+    def work():
+        tc, td, ab = R.time_roundtrip(ctx, xh, tau, reps=1)
+        results.append((tc, td, ab))
+
+    R.time_roundtrip(ctx, xh, tau, reps=1)  # warm
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        ts = [threading.Thread(target=work) for _ in range(threads)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+    wall = time.perf_counter() - t0
+    tc = float(np.mean([r[0] for r in results]))
+    td = float(np.mean([r[1] for r in results]))
+    gbs = threads * reps * n * 8 / wall / 1e9
+    return dict(value=gbs, unit="GB/s", cores=threads, kind="reference",
+                sample=f"config-3 construction at lattice {lattice}^3 ({n} vertices), grid {grid}^3, "
+                       f"tau_rel {tau}: {threads} concurrent compress+decompress x {reps} rounds "
+                       f"(per call: compress {tc:.3f} s, decompress {td:.3f} s)",
+                compress_s=tc, decompress_s=td, wall_s=wall, n=n)
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    threads = min(os.cpu_count() or 1, 32)
+    lat, grid = 128, 64
+    base = dict(impl="reference", metric=METRIC, unit="GB/s", higher_is_better=True, n_gpus=args.gpus,
+                steps=args.steps, warmup=args.warmup, scaling="weak", vs_baseline=None, dtype="f64",
+                data="synthetic")
+    try:
+        for _ in range(args.warmup):
+            cpu_reference_sample(lat, grid, threads, 1, args.tau)
+        r = cpu_reference_sample(lat, grid, threads, args.steps, args.tau)
+    except Exception as e:
+        print(json.dumps(dict(base, unavailable=f"reference CPU run failed: {e}"[:300])))
+        return 0
+    out = dict(base, value=r["value"], ms_per_step=1e3 * r["wall_s"] / args.steps,
+               config={"workload": f"config3-sample lattice{lat}^3 grid{grid}^3 tau_rel {args.tau}",
+                       "threads": threads},
+               cpu_baseline={k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+               e2e={"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+    print(json.dumps(out))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="umcg", choices=["umcg", "reference"])
+    ap.add_argument("--lattice", type=int, default=512)
+    ap.add_argument("--grid", type=int, default=256)
+    ap.add_argument("--tau", type=float, default=1e-4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import paper_2501_06910_b200 as umcg
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    plan, x = setup_config3(args.lattice, args.grid, dev)
+    n, n1 = plan.n, int(plan.info.n_slots)
+    budget = umcg.Budget(tau=args.tau, split_rho=0.5, bound_kind=1)
+    cap = plan.compress_bound("field")
+    ar = torch.empty(cap, dtype=torch.uint8, device=dev)
+    out = torch.empty(n, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        L = plan.compress_into(x, budget, ar, "field")
+        plan.decompress_into(ar, L, out)
+        return L
+
+    for _ in range(max(args.warmup, 3)):
+        alen = step()
+    # per-direction timing (CUDA events on the launching stream), outside the headline region
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    tc, td = [], []
+    for _ in range(3):
+        ev[0].record(stream)
+        L = plan.compress_into(x, budget, ar, "field")
+        ev[1].record(stream)
+        plan.decompress_into(ar, L, out)
+        ev[2].record(stream)
+        torch.cuda.synchronize()
+        tc.append(ev[0].elapsed_time(ev[1]))
+        td.append(ev[1].elapsed_time(ev[2]))
+    err = (out - x).abs().max().item()
+    tau_abs = args.tau * (x.max() - x.min()).item()
+
+    launches0 = umcg.kernel_launches()
+    barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            alen = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = umcg.kernel_launches() - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    value = ws * n * 8 / (ms * 1e-3) / 1e9
+
+    # e2e through the host-buffer ABI with pinned buffers
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        xh.copy_(x.cpu())
+        arh = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
+        yh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        xa, aa, ya = xh.numpy(), arh.numpy(), yh.numpy()
+
+        def estep():
+            L = plan.compress_host(xa, budget, "field", out=aa)
+            plan.decompress_host(aa[:L], out=ya)
+            return L
+
+        for _ in range(2):
+            estep()
+        k = max(2, args.steps // 3)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(k):
+            L = estep()
+        te = (time.perf_counter() - t0) / k
+        e2e = {"value": ws * n * 8 / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": n * 8 + L,
+               "d2h_bytes_per_step": L + n * 8, "ms_per_step": te * 1e3,
+               "path": "umcg_compress_host + umcg_decompress_host (pinned host buffers)"}
+
+    peak, peak_kind = peaks()
+    b_c, b_d = algorithmic_bytes(n, n1, alen)
+    tcm, tdm = float(np.median(tc)), float(np.median(td))
+    res = dict(
+        metric=METRIC, value=value, unit="GB/s", n_gpus=ws, steps=args.steps, warmup=args.warmup,
+        ms_per_step=ms, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
+        data="synthetic (GPU-generated, SplitMix64-seeded config 3)",
+        config={"workload": f"config3 lattice{args.lattice}^3 ({n} vertices) grid{args.grid}^3 "
+                            f"tau_rel {args.tau} rho 0.5 nearest g",
+                "l2": "inputs larger than L2 (1.07 GB field), no flush", "parallelism": f"replicas x{ws}",
+                "archive_bytes": alen, "mode": "seed" if plan.info.mode else "dense"},
+        compress={"ms": tcm, "gbs_field": n * 8 / tcm / 1e6, "algorithmic_bytes": b_c,
+                  "roofline_frac": b_c / (tcm * 1e-3) / 1e9 / peak},
+        decompress={"ms": tdm, "gbs_field": n * 8 / tdm / 1e6, "algorithmic_bytes": b_d,
+                    "roofline_frac": b_d / (tdm * 1e-3) / 1e9 / peak},
+        roofline={"bound": "hbm", "achieved": (b_c + b_d) / ((tcm + tdm) * 1e-3) / 1e9, "peak": peak,
+                  "unit": "GB/s", "frac": (b_c + b_d) / ((tcm + tdm) * 1e-3) / 1e9 / peak,
+                  "traffic": None, "scope": "whole compress+decompress path (SURVEY 8d algorithmic bytes)",
+                  "peak_source": peak_kind},
+        max_err_over_tau=err / tau_abs if tau_abs else None,
+        gpu_launches=launches,
+        clocks=clk.summary(),
+        e2e=e2e,
+    )
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            cb = cpu_reference_sample(128, 64, 1, 2, args.tau)
+            res["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:
+            res["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    if rank == 0:
+        print(json.dumps(res))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,324 @@
+"""umc-b200: B200 (sm_100a) implementation of the umc multi-component
+compressor's data-parallel hot path.
+
+Python host mirror of the reference interface (umc::compress /
+umc::decompress, pipeline.hpp:117-148 / 180-210; umc::encode / umc::decode,
+codec.hpp:220-441) over the C ABI in include/umcg.h (libumcg.so, built
+in-tree by ``paper_2501_06910_b200.build``). Device buffers are torch CUDA
+tensors; PyTorch is only the allocator and stream provider here.
+
+There is no CPU fallback: importing works without a GPU, but every compute
+call goes to libumcg.so and fails loudly if the library or the device is
+missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libumcg.so")
+
+# umcg_status values == reference exception types (common.hpp:19-38)
+ERROR_NAMES = {
+    1: "error", 2: "malformed_file", 3: "index_out_of_range", 4: "non_finite_value",
+    5: "io_failure", 6: "degenerate_mesh", 7: "empty_after_filtering",
+    8: "internal_inconsistency", 9: "seed_mode_unsupported", 10: "unknown_codec",
+    11: "corrupt_payload", 12: "external_codec_violation", 13: "subprocess_failure",
+    14: "budget_inadmissible", 15: "mapping_mismatch", 16: "zero_norm_reference",
+    17: "mismatched_runs", 100: "cuda_error", 101: "invalid_argument",
+}
+
+# public symbols of include/umcg.h (checked by tests/test_abi.py)
+EXPORTED = [
+    "umcg_plan_create", "umcg_plan_build", "umcg_plan_destroy", "umcg_plan_get_info",
+    "umcg_plan_export", "umcg_compress_bound", "umcg_compress", "umcg_compress_batch",
+    "umcg_decompress", "umcg_compress_host", "umcg_decompress_host", "umcg_encode_bound",
+    "umcg_encode", "umcg_decode", "umcg_rle_compress", "umcg_rle_decompress", "umcg_gen_config",
+    "umcg_kernel_launches", "umcg_last_error", "umcg_version",
+]
+
+
+class UmcgError(RuntimeError):
+    """A umcg_status != 0; ``kind`` is the reference exception name."""
+
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        self.kind = ERROR_NAMES.get(status, str(status))
+        super().__init__(f"{self.kind}: {msg}")
+
+
+u8p = C.POINTER(C.c_uint8)
+u64p = C.POINTER(C.c_uint64)
+f64p = C.POINTER(C.c_double)
+
+
+class GridDesc(C.Structure):
+    _fields_ = [("dim", C.c_int), ("axis_sizes", u64p), ("axes", f64p)]
+
+
+class MappingDesc(C.Structure):
+    _fields_ = [("mode", C.c_int), ("n_vertices", C.c_uint64), ("assignments", u64p),
+                ("n_visited", C.c_uint64), ("visited_nodes", u64p)]
+
+
+class Params(C.Structure):
+    _fields_ = [("tau", C.c_double), ("split_rho", C.c_double), ("bound_kind", C.c_int),
+                ("g_kind", C.c_int), ("coeff_abs_sum", C.c_double), ("fill", C.c_int),
+                ("codec_id", C.c_int), ("backend_id", C.c_int)]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [("dim", C.c_int), ("mode", C.c_int), ("n_vertices", C.c_uint64),
+                ("n_slots", C.c_uint64), ("shape", C.c_uint64 * 3), ("n_visited", C.c_uint64),
+                ("visited_fraction", C.c_double), ("digest", C.c_uint64), ("has_coords", C.c_int)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libumcg.so (raises if it was not built: no fallback exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2501_06910_b200.build` "
+                          "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp = C.c_void_p
+    L.umcg_last_error.restype = C.c_char_p
+    L.umcg_version.restype = C.c_char_p
+    L.umcg_kernel_launches.restype = C.c_uint64
+    L.umcg_encode_bound.restype = C.c_uint64
+    L.umcg_encode_bound.argtypes = [C.c_uint64, C.c_int]
+    L.umcg_plan_create.argtypes = [C.POINTER(GridDesc), C.POINTER(MappingDesc), C.c_int, f64p,
+                                   C.POINTER(vp)]
+    L.umcg_plan_build.argtypes = [C.POINTER(GridDesc), C.c_uint64, vp, C.c_double, C.c_int,
+                                  C.POINTER(vp)]
+    L.umcg_plan_destroy.argtypes = [vp]
+    L.umcg_plan_get_info.argtypes = [vp, C.POINTER(PlanInfo)]
+    L.umcg_plan_export.argtypes = [vp, u64p, u64p, f64p]
+    L.umcg_compress_bound.argtypes = [vp, C.c_char_p, u64p]
+    L.umcg_compress.argtypes = [vp, C.POINTER(Params), vp, C.c_char_p, vp, C.c_uint64, u64p, vp]
+    L.umcg_compress_batch.argtypes = [vp, C.POINTER(Params), vp, C.c_int, C.c_int,
+                                      C.POINTER(C.c_char_p), vp, C.c_uint64, u64p, vp]
+    L.umcg_decompress.argtypes = [vp, vp, C.c_uint64, vp, vp]
+    L.umcg_compress_host.argtypes = [vp, C.POINTER(Params), vp, C.c_char_p, vp, C.c_uint64, u64p]
+    L.umcg_decompress_host.argtypes = [vp, vp, C.c_uint64, vp]
+    L.umcg_encode.argtypes = [vp, C.c_uint64, C.c_int, C.c_int, u64p, C.c_double, C.c_int, C.c_int,
+                              vp, C.c_uint64, u64p, vp]
+    L.umcg_decode.argtypes = [vp, C.c_uint64, vp, C.c_uint64, u64p, vp]
+    L.umcg_gen_config.argtypes = [C.c_int, C.c_uint64, C.c_uint64, vp, vp, u64p, vp]
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc:
+        raise UmcgError(rc, lib().umcg_last_error().decode(errors="replace"))
+
+
+def kernel_launches() -> int:
+    return int(lib().umcg_kernel_launches())
+
+
+def _ptr(a, t):
+    return a.ctypes.data_as(t)
+
+
+def _stream_ptr(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+@dataclass
+class Budget:
+    """umc::ErrorBudget (pipeline.hpp:25-29) + CompressOptions (:81-86)."""
+    tau: float = 1e-3
+    split_rho: float = 0.5
+    bound_kind: int = 1  # 0 absolute, 1 relative_to_range
+    g_kind: int = 0  # 0 nearest, 1 multilinear
+    coeff_abs_sum: float = 1.0
+    fill: int = 0  # 0 zero, 1 nearest_visited
+    codec_id: int = 0
+    backend_id: int = 0
+
+    def c(self) -> Params:
+        return Params(self.tau, self.split_rho, self.bound_kind, self.g_kind, self.coeff_abs_sum,
+                      self.fill, self.codec_id, self.backend_id)
+
+
+class Plan:
+    """Immutable device plan for one mesh mapping (umcg_plan)."""
+
+    def __init__(self, handle):
+        self.h = handle
+        info = PlanInfo()
+        _check(lib().umcg_plan_get_info(self.h, C.byref(info)))
+        self.info = info
+
+    @classmethod
+    def from_mapping(cls, dim, axes, mode, assignments, visited=None, coords=None):
+        """umcg_plan_create: host grid + mapping (+ coordinates for multilinear g)."""
+        sizes = np.array([len(a) for a in axes], np.uint64)
+        cat = np.ascontiguousarray(np.concatenate([np.asarray(a, np.float64) for a in axes]))
+        a = np.ascontiguousarray(assignments, np.uint64)
+        v = np.ascontiguousarray(visited if visited is not None else np.zeros(0), np.uint64)
+        g = GridDesc(dim, _ptr(sizes, u64p), _ptr(cat, f64p))
+        m = MappingDesc(mode, len(a), _ptr(a, u64p) if len(a) else None, len(v),
+                        _ptr(v, u64p) if len(v) else None)
+        cp = None
+        if coords is not None:
+            coords = np.ascontiguousarray(coords, np.float64)
+            cp = _ptr(coords, f64p)
+        h = C.c_void_p()
+        _check(lib().umcg_plan_create(C.byref(g), C.byref(m), dim, cp, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def build(cls, init_axes, d_coords, seed_threshold=0.35, keep_coords=False):
+        """umcg_plan_build: GPU grid_coarsen of device coordinates (torch tensor [n, dim])."""
+        dim = len(init_axes)
+        sizes = np.array([len(a) for a in init_axes], np.uint64)
+        cat = np.ascontiguousarray(np.concatenate([np.asarray(a, np.float64) for a in init_axes]))
+        g = GridDesc(dim, _ptr(sizes, u64p), _ptr(cat, f64p))
+        h = C.c_void_p()
+        _check(lib().umcg_plan_build(C.byref(g), d_coords.shape[0], C.c_void_p(d_coords.data_ptr()),
+                                     seed_threshold, 1 if keep_coords else 0, C.byref(h)))
+        return cls(h)
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().umcg_plan_destroy(self.h)
+        except Exception:
+            pass
+
+    @property
+    def n(self) -> int:
+        return int(self.info.n_vertices)
+
+    @property
+    def digest(self) -> int:
+        return int(self.info.digest)
+
+    def export(self):
+        """(mode, axes list, assignments u64, visited u64) back on the host."""
+        n = self.n
+        a = np.zeros(max(n, 1), np.uint64)
+        nv = int(self.info.n_visited) if self.info.mode == 1 else 0
+        v = np.zeros(max(nv, 1), np.uint64)
+        shape = [int(self.info.shape[d]) for d in range(self.info.dim)]
+        ax = np.zeros(sum(shape), np.float64)
+        _check(lib().umcg_plan_export(self.h, _ptr(a, u64p), _ptr(v, u64p), _ptr(ax, f64p)))
+        axes, off = [], 0
+        for s in shape:
+            axes.append(ax[off: off + s].copy())
+            off += s
+        return int(self.info.mode), axes, a[:n], v[:nv]
+
+    def compress_bound(self, name: str = "") -> int:
+        b = C.c_uint64()
+        _check(lib().umcg_compress_bound(self.h, name.encode(), C.byref(b)))
+        return b.value
+
+    # ---- device-pointer path (the measured one) ---------------------------
+    def compress_into(self, d_values, budget: Budget, d_archive, name: str = "", stream=None) -> int:
+        n = C.c_uint64()
+        prm = budget.c()
+        _check(lib().umcg_compress(self.h, C.byref(prm), C.c_void_p(d_values.data_ptr()),
+                                   name.encode(), C.c_void_p(d_archive.data_ptr()),
+                                   d_archive.numel(), C.byref(n), _stream_ptr(stream)))
+        return n.value
+
+    def decompress_into(self, d_archive, length: int, d_out, stream=None):
+        _check(lib().umcg_decompress(self.h, C.c_void_p(d_archive.data_ptr()), length,
+                                     C.c_void_p(d_out.data_ptr()), _stream_ptr(stream)))
+
+    def compress(self, d_values, budget: Budget = Budget(), name: str = "") -> bytes:
+        import torch
+        buf = torch.empty(self.compress_bound(name), dtype=torch.uint8, device=d_values.device)
+        n = self.compress_into(d_values, budget, buf, name)
+        return bytes(buf[:n].cpu().numpy())
+
+    def decompress(self, archive: bytes, device="cuda"):
+        import torch
+        a = torch.from_numpy(np.frombuffer(archive, np.uint8).copy()).to(device)
+        out = torch.empty(self.n, dtype=torch.float64, device=device)
+        self.decompress_into(a, len(archive), out)
+        return out
+
+    # ---- host-buffer path (reference call shape) ---------------------------
+    def compress_host(self, values: np.ndarray, budget: Budget = Budget(), name: str = "",
+                      out: np.ndarray | None = None) -> bytes | int:
+        v = np.ascontiguousarray(values, np.float64)
+        buf = out if out is not None else np.empty(self.compress_bound(name), np.uint8)
+        n = C.c_uint64()
+        prm = budget.c()
+        _check(lib().umcg_compress_host(self.h, C.byref(prm), C.c_void_p(v.ctypes.data),
+                                        name.encode(), C.c_void_p(buf.ctypes.data), len(buf),
+                                        C.byref(n)))
+        return n.value if out is not None else buf[: n.value].tobytes()
+
+    def decompress_host(self, archive, out: np.ndarray | None = None) -> np.ndarray:
+        a = np.frombuffer(archive, np.uint8) if isinstance(archive, (bytes, bytearray)) else archive
+        length = len(archive) if isinstance(archive, (bytes, bytearray)) else int(a.size)
+        y = out if out is not None else np.empty(self.n, np.float64)
+        _check(lib().umcg_decompress_host(self.h, C.c_void_p(a.ctypes.data), length,
+                                          C.c_void_p(y.ctypes.data)))
+        return y
+
+
+def encode(d_values, predictor: int = 1, dims=None, tau: float = 1e-3, codec_id: int = 0,
+           backend_id: int = 0) -> bytes:
+    """umc::encode (codec.hpp:220) on a device fp64 tensor; returns the payload bytes."""
+    import torch
+    n = d_values.numel()
+    dims = np.array(dims if dims is not None else [n], np.uint64)
+    cap = int(lib().umcg_encode_bound(n, len(dims)))
+    buf = torch.empty(cap, dtype=torch.uint8, device=d_values.device)
+    out = C.c_uint64()
+    _check(lib().umcg_encode(C.c_void_p(d_values.data_ptr()), n, predictor, len(dims),
+                             _ptr(dims, u64p), tau, codec_id, backend_id,
+                             C.c_void_p(buf.data_ptr()), cap, C.byref(out), _stream_ptr()))
+    return bytes(buf[: out.value].cpu().numpy())
+
+
+def decode(payload: bytes, n_capacity: int | None = None, device="cuda"):
+    """umc::decode (codec.hpp:364) of a payload; returns a device fp64 tensor."""
+    import torch
+    a = torch.from_numpy(np.frombuffer(payload, np.uint8).copy()).to(device) if payload else \
+        torch.zeros(1, dtype=torch.uint8, device=device)
+    if n_capacity is None:
+        # header: n_elements at byte 12 (codec.hpp:231)
+        n_capacity = int.from_bytes(payload[12:20], "little") if len(payload) >= 20 else 0
+    out = torch.empty(max(n_capacity, 1), dtype=torch.float64, device=device)
+    n = C.c_uint64()
+    _check(lib().umcg_decode(C.c_void_p(a.data_ptr()), len(payload), C.c_void_p(out.data_ptr()),
+                             n_capacity, C.byref(n), _stream_ptr()))
+    return out[: n.value]
+
+
+def gen_config(config: int, lattice: int, seed: int, coords: bool = True, values: bool = True,
+               device="cuda"):
+    """Synthetic BASELINE inputs on the device: (coords [n,dim] f64, values)."""
+    import torch
+    n = C.c_uint64()
+    _check(lib().umcg_gen_config(config, lattice, seed, None, None, C.byref(n), None))
+    n = n.value
+    dim = 3 if config == 3 else 2
+    xyz = torch.empty((n, dim), dtype=torch.float64, device=device) if coords else None
+    if config == 4:
+        vals = torch.empty((5, n), dtype=torch.float32, device=device) if values else None
+    else:
+        vals = torch.empty(n, dtype=torch.float64, device=device) if values else None
+    _check(lib().umcg_gen_config(config, lattice, seed,
+                                 C.c_void_p(xyz.data_ptr()) if xyz is not None else None,
+                                 C.c_void_p(vals.data_ptr()) if vals is not None else None,
+                                 C.byref(C.c_uint64()), _stream_ptr()))
+    return xyz, vals

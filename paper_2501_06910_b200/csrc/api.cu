@@ -1,0 +1,817 @@
+// C ABI (include/umcg.h): orchestration of the sm_100a kernels for
+// umc::compress / umc::decompress (pipeline.hpp:117-148, 180-210) and the
+// component codec (codec.hpp:220-441).
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "plan.h"
+
+namespace umcg {
+
+std::atomic<uint64_t> g_launches{0};
+static thread_local std::string g_last_error;
+
+umcg_plan* plan_create_host(const umcg_grid_desc*, const umcg_mapping_desc*, int, const double*);
+umcg_plan* plan_build_gpu(const umcg_grid_desc*, uint64_t, const double*, double, int);
+
+namespace {
+
+constexpr int THREADS = 256;
+
+template <class F>
+umcg_status guarded(F&& f) {
+    try {
+        f();
+        return UMCG_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return UMCG_ERROR;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return UMCG_ERROR;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Archive layout (pipeline.hpp:214-235) and component header
+// (codec.hpp:225-233, 329-331), written on the device from DevCtl so the
+// whole compress needs one host synchronization.
+// ---------------------------------------------------------------------------
+struct HdrArgs {
+    uint16_t flags, name_len;
+    uint64_t digest;
+    double tau, rho;
+    const uint8_t* name;   // device
+    int pred[2], D[2];
+    uint64_t dims[2][3];
+    uint64_t n[2];
+    int lossless_codes[2];  // unused by layout, kept for debugging
+};
+
+__device__ __forceinline__ void put_le(uint8_t* d, uint64_t off, uint64_t v, int k) {
+    for (int i = 0; i < k; ++i) d[off + i] = (uint8_t)(v >> (8 * i));
+}
+__device__ __forceinline__ uint64_t comp_hdr_bytes(int D) { return 4 + 8 + 8 + 1 + 8ull * D + 8; }
+
+__device__ uint64_t write_comp_header(uint8_t* a, uint64_t o, int pred, double tau, uint64_t n, int D,
+                                      const uint64_t* dims, uint64_t n_esc) {
+    a[o] = 0;              // codec_id (builtin PQ)
+    a[o + 1] = (uint8_t)pred;
+    a[o + 2] = 0;          // backend_id
+    a[o + 3] = 0;
+    put_le(a, o + 4, (uint64_t)__double_as_longlong(tau), 8);
+    put_le(a, o + 12, n, 8);
+    a[o + 20] = (uint8_t)D;
+    for (int d = 0; d < D; ++d) put_le(a, o + 21 + 8ull * d, dims[d], 8);
+    put_le(a, o + 21 + 8ull * D, n_esc, 8);
+    return o + comp_hdr_bytes(D);
+}
+
+// Computes stream offsets (consumed by the stream writers) and writes every
+// header byte of the UMCZ archive.
+__global__ void k_layout_archive(HdrArgs h, DevCtl* ctl, uint8_t* a) {
+    if (threadIdx.x | blockIdx.x) return;
+    uint64_t o = 0;
+    a[0] = 'U'; a[1] = 'M'; a[2] = 'C'; a[3] = 'Z';
+    put_le(a, 4, 1, 2);  // kFormatVersion
+    put_le(a, 6, h.flags, 2);
+    put_le(a, 8, h.name_len, 2);
+    o = 10;
+    for (uint32_t i = 0; i < h.name_len; ++i) a[o + i] = h.name[i];
+    o += h.name_len;
+    put_le(a, o, h.digest, 8);
+    put_le(a, o + 8, (uint64_t)__double_as_longlong(h.tau), 8);
+    put_le(a, o + 16, (uint64_t)__double_as_longlong(h.rho), 8);
+    o += 24;
+    for (int c = 0; c < 2; ++c) {
+        const uint64_t pl = comp_hdr_bytes(h.D[c]) + 16 * ctl->n_esc[c] + ctl->stream_len[c];
+        ctl->payload_len[c] = pl;
+        put_le(a, o, pl, 8);
+        o += 8;
+        const uint64_t e = write_comp_header(a, o, h.pred[c], ctl->tau_c[c], h.n[c], h.D[c], h.dims[c],
+                                             ctl->n_esc[c]);
+        ctl->aux[2 + c] = e;  // escape records offset
+        ctl->stream_off[c] = e + 16 * ctl->n_esc[c];
+        o += pl;
+    }
+    ctl->archive_len = o;
+}
+
+// Bare component payload (umcg_encode).
+__global__ void k_layout_component(int pred, int D, NdShape sh, uint64_t n, DevCtl* ctl, uint8_t* a) {
+    if (threadIdx.x | blockIdx.x) return;
+    const uint64_t e = write_comp_header(a, 0, pred, ctl->tau_c[0], n, D, sh.dims, ctl->n_esc[0]);
+    ctl->aux[2] = e;
+    ctl->stream_off[0] = e + 16 * ctl->n_esc[0];
+    ctl->payload_len[0] = ctl->stream_off[0] + ctl->stream_len[0];
+    ctl->archive_len = ctl->payload_len[0];
+}
+
+__global__ void k_write_escapes(const uint64_t* __restrict__ idx, const double* __restrict__ val, uint64_t ne,
+                                const DevCtl* __restrict__ ctl, int comp, uint8_t* __restrict__ a) {
+    const uint64_t e = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (e >= ne) return;
+    const uint64_t o = ctl->aux[2 + comp] + 16 * e;
+    put_le(a, o, idx[e], 8);
+    put_le(a, o + 8, (uint64_t)__double_as_longlong(val[e]), 8);
+}
+
+// Escape records of a payload -> arrays, with the reference's validation
+// (codec.hpp:408-416): indices < n and strictly increasing.
+__global__ void k_read_escapes(const uint8_t* __restrict__ p, uint64_t ne, uint64_t n,
+                               uint64_t* __restrict__ idx, double* __restrict__ val, DevCtl* ctl) {
+    const uint64_t e = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (e >= ne) return;
+    uint64_t i = 0, v = 0, pi = 0;
+    for (int k = 0; k < 8; ++k) {
+        i |= (uint64_t)p[16 * e + k] << (8 * k);
+        v |= (uint64_t)p[16 * e + 8 + k] << (8 * k);
+    }
+    if (e > 0)
+        for (int k = 0; k < 8; ++k) pi |= (uint64_t)p[16 * (e - 1) + k] << (8 * k);
+    if (i >= n || (e > 0 && i <= pi)) set_err(ctl, DE_CORRUPT_ESCAPE);
+    idx[e] = i;
+    val[e] = __longlong_as_double((long long)v);
+}
+
+__global__ void k_widen(const float* __restrict__ x, uint64_t n, double* __restrict__ y) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i < n) y[i] = (double)x[i];
+}
+
+inline unsigned blocks(uint64_t n) { return (unsigned)cdiv(n, THREADS); }
+
+uint64_t stream_bound(uint64_t n) { return 10 * n + 3 * (n / 8 + 2) * 11 + 16; }
+uint64_t payload_bound(uint64_t n, int D) { return 29 + 8ull * D + 16 * n + stream_bound(n); }
+uint64_t archive_bound(uint64_t n, uint64_t n1, int D, uint64_t name_len) {
+    return 34 + name_len + 16 + payload_bound(n1, D) + payload_bound(n, 1) + 64;
+}
+
+DevCtl read_ctl(umcg_plan* p, DevCtl* d, cudaStream_t st) {
+    auto* h = static_cast<DevCtl*>(p->hctl.reserve(sizeof(DevCtl)));
+    UMCG_CUDA(cudaMemcpyAsync(h, d, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
+    UMCG_CUDA(cudaStreamSynchronize(st));
+    return *h;
+}
+
+void init_ctl(DevCtl* d, cudaStream_t st) {
+    UMCG_CUDA(cudaMemsetAsync(d, 0, sizeof(DevCtl), st));
+    UMCG_CUDA(cudaMemsetAsync(&d->min_key, 0xff, 8, st));
+}
+
+// Host replica of the budget arithmetic for absolute bounds (decides the
+// lossless path up front); relative bounds are resolved on the device.
+void host_budget(double tau_abs, double rho, double coeff, double* tc) {
+    double t1 = rho * tau_abs / coeff;
+    const double t2 = (1.0 - rho) * tau_abs;
+    while (coeff * t1 + t2 > tau_abs) t1 = std::nextafter(t1, 0.0);
+    tc[0] = t1 * (1.0 - 1e-9);
+    tc[1] = t2 * (1.0 - 1e-9);
+}
+
+struct CompressMode {
+    bool lossless[2];
+    bool serial[2];
+};
+
+// One pass of the compress pipeline. Returns the device control block.
+DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int x_f32, const std::string& name,
+                     uint8_t* d_ar, const CompressMode& m, cudaStream_t st) {
+    const uint64_t n = p->n, n1 = p->n_slots;
+    auto* ctl = p->ctl.as<DevCtl>(1);
+    init_ctl(ctl, st);
+    minmax(d_x, x_f32, n, ctl, st);
+    budget(BudgetArgs{prm.tau, prm.split_rho, prm.coeff_abs_sum, prm.bound_kind, n}, ctl, st);
+
+    // f: cluster means (interp.hpp:46-93)
+    double* x1 = p->x1.as<double>(n1 ? n1 : 1);
+    cluster_mean(d_x, x_f32, p->d_perm.as<uint32_t>(1), p->d_seg.as<uint32_t>(1), n1, x1, st);
+    if (prm.fill == 1 && p->mode == 0) fill_nearest_visited(p->d_seg.as<uint32_t>(1), n1, p->shape[p->dim - 1], x1, st);
+
+    // component specs (grid_codec_spec, pipeline.hpp:96-110)
+    const int pred1 = p->mode == 1 ? 1 : 2;
+    const int D1 = p->mode == 1 ? 1 : p->dim;
+    uint64_t dims1[3] = {n1, 1, 1};
+    if (p->mode == 0) for (int d = 0; d < p->dim; ++d) dims1[d] = p->shape[d];
+    const NdShape sh1 = make_shape(D1, dims1);
+
+    ResidualSrc rs{};
+    rs.x = d_x;
+    rs.x_f32 = x_f32;
+    rs.node = p->d_node.as<uint32_t>(1);
+    rs.x1 = x1;
+    rs.g_kind = prm.g_kind;
+    rs.coords = p->has_coords ? p->d_coords.as<double>(1) : nullptr;
+    rs.axes = p->d_axes.as<double>(1);
+    rs.axis_off = p->d_axis_off.as<uint64_t>(1);
+    rs.D = p->dim;
+    for (int d = 0; d < 3; ++d) rs.shape[d] = p->shape[d];
+
+    // codes
+    void* codes[2] = {nullptr, nullptr};
+    bool wide[2];
+    uint64_t ncode[2] = {n1, n};
+    for (int c = 0; c < 2; ++c) {
+        DevBuf& cb = c == 0 ? p->codes1 : p->codes2;
+        wide[c] = m.lossless[c] || m.serial[c];
+        codes[c] = cb.reserve((ncode[c] ? ncode[c] : 1) * (wide[c] ? 8 : 4));
+    }
+    uint64_t* esc_idx[2] = {nullptr, nullptr};
+    double* esc_val[2] = {nullptr, nullptr};
+    // grid component
+    if (m.serial[0]) {
+        DevCtl hc = read_ctl(p, ctl, st);  // need the shaved tau on the host for the serial kernel
+        esc_idx[0] = p->scratch_a.as<uint64_t>(n1 ? n1 : 1);
+        esc_val[0] = p->scratch_b.as<double>(2 * (n1 ? n1 : 1));
+        serial_encode(x1, n1, pred1, sh1, hc.tau_c[0], static_cast<uint64_t*>(codes[0]), esc_val[0] + n1,
+                      esc_idx[0], esc_val[0], ctl, 0, st);
+    } else if (m.lossless[0]) {
+        codes_lossless_values(x1, n1, pred1, sh1, static_cast<uint64_t*>(codes[0]), st);
+    } else {
+        int32_t* kb = p->kbuf.as<int32_t>(n1 ? n1 : 1);
+        codes_lossy_values(x1, n1, pred1, sh1, ctl, 0, static_cast<uint32_t*>(codes[0]), kb, st);
+    }
+    // residual component
+    if (m.serial[1]) {
+        DevCtl hc = read_ctl(p, ctl, st);
+        double* x2 = p->scratch_c.as<double>(2 * (n ? n : 1));
+        materialize_residual(rs, n, x2, st);
+        esc_idx[1] = p->scratch_d.as<uint64_t>(n ? n : 1);
+        esc_val[1] = x2 + n;  // reuse: escapes written after recon? keep separate below
+        double* ev = p->dx1.as<double>(2 * (n ? n : 1));
+        esc_val[1] = ev;
+        serial_encode(x2, n, 1, make_shape(1, &n), hc.tau_c[1], static_cast<uint64_t*>(codes[1]), ev + n,
+                      esc_idx[1], ev, ctl, 1, st);
+    } else if (m.lossless[1]) {
+        codes_lossless_residual(rs, n, static_cast<uint64_t*>(codes[1]), st);
+    } else {
+        codes_lossy_residual(rs, n, ctl, static_cast<uint32_t*>(codes[1]), st);
+    }
+
+    // stream structure, layout, headers, bytes
+    StreamEncScratch es[2];
+    for (int c = 0; c < 2; ++c) {
+        DevBuf& eb = c == 0 ? p->enc1 : p->enc2;
+        es[c] = stream_enc_carve(eb.reserve(stream_enc_scratch_bytes(ncode[c])), ncode[c]);
+        if (wide[c]) stream_plan_u64(static_cast<uint64_t*>(codes[c]), ncode[c], es[c], ctl, c, st);
+        else stream_plan_u32(static_cast<uint32_t*>(codes[c]), ncode[c], es[c], ctl, c, st);
+    }
+    HdrArgs h{};
+    uint16_t flags = 0;
+    if (p->mode == 1) flags |= 1u;
+    if (prm.g_kind == 1) flags |= 2u;
+    if (prm.bound_kind == 1) flags |= 4u;
+    h.flags = flags;
+    h.name_len = (uint16_t)name.size();
+    uint8_t* dname = p->hdr.as<uint8_t>(name.size() + 1);
+    if (!name.empty()) {
+        auto* hs = static_cast<uint8_t*>(p->hstage.reserve(name.size()));
+        std::memcpy(hs, name.data(), name.size());
+        UMCG_CUDA(cudaMemcpyAsync(dname, hs, name.size(), cudaMemcpyHostToDevice, st));
+    }
+    h.name = dname;
+    h.digest = p->digest;
+    h.tau = prm.tau;
+    h.rho = prm.split_rho;
+    h.pred[0] = pred1; h.pred[1] = 1;
+    h.D[0] = D1; h.D[1] = 1;
+    for (int d = 0; d < 3; ++d) { h.dims[0][d] = dims1[d]; h.dims[1][d] = d == 0 ? n : 1; }
+    h.n[0] = n1; h.n[1] = n;
+    k_layout_archive<<<1, 32, 0, st>>>(h, ctl, d_ar);
+    UMCG_LAUNCHED();
+    for (int c = 0; c < 2; ++c) {
+        if (m.serial[c]) {
+            // escapes count is on the device; launch for the worst case, kernel bounds itself
+            DevCtl hc = read_ctl(p, ctl, st);
+            if (hc.n_esc[c]) {
+                k_write_escapes<<<blocks(hc.n_esc[c]), THREADS, 0, st>>>(esc_idx[c], esc_val[c], hc.n_esc[c], ctl, c, d_ar);
+                UMCG_LAUNCHED();
+            }
+        }
+        if (wide[c]) stream_write_u64(static_cast<uint64_t*>(codes[c]), ncode[c], es[c], ctl, c, d_ar, true, st);
+        else stream_write_u32(static_cast<uint32_t*>(codes[c]), ncode[c], es[c], ctl, c, d_ar, true, st);
+    }
+    return read_ctl(p, ctl, st);
+}
+
+void compress_impl(umcg_plan* p, const umcg_params* prm_in, const void* d_x, int x_f32, const char* name_c,
+                   uint8_t* d_ar, uint64_t cap, uint64_t* out_len, cudaStream_t st) {
+    if (!p || !prm_in || !out_len) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
+    if (p->n && !d_x) fail(UMCG_INVALID_ARGUMENT, "NULL values");
+    const umcg_params prm = *prm_in;
+    const std::string name = name_c ? name_c : "";
+    std::lock_guard<std::mutex> lock(p->mu);
+    UMCG_CUDA(cudaSetDevice(p->device));
+
+    // Parameter errors in the reference's order (pipeline.hpp:120-146):
+    // validate_field's finiteness first, then the budget, then seed/multilinear,
+    // then the codec, then serialize_archive's name limit.
+    umcg_status perr = UMCG_OK;
+    std::string pmsg;
+    if (!(prm.tau >= 0.0)) { perr = UMCG_BUDGET_INADMISSIBLE; pmsg = "tau must be >= 0"; }
+    else if (!(prm.split_rho > 0.0) || !(prm.split_rho < 1.0)) { perr = UMCG_BUDGET_INADMISSIBLE; pmsg = "rho must lie strictly inside (0, 1)"; }
+    else if (!(prm.coeff_abs_sum > 0.0)) { perr = UMCG_BUDGET_INADMISSIBLE; pmsg = "coefficient sum must be positive"; }
+    else if (prm.g_kind == 1 && p->mode == 1) { perr = UMCG_SEED_MODE_UNSUPPORTED; pmsg = "multilinear back-interpolation needs a dense grid component"; }
+    else if (prm.g_kind == 1 && !p->has_coords) { perr = UMCG_INVALID_ARGUMENT; pmsg = "multilinear g needs a plan with vertex coordinates"; }
+    else if (prm.codec_id != 0) { perr = UMCG_UNKNOWN_CODEC; pmsg = "only the builtin PQ codec (id 0) runs on the device path"; }
+    else if (prm.backend_id != 0) { perr = UMCG_UNKNOWN_CODEC; pmsg = "lossless backend " + std::to_string(prm.backend_id) + " not registered"; }
+    else if (name.size() > 0xffff) { perr = UMCG_MALFORMED_FILE; pmsg = "field name too long"; }
+    if (perr != UMCG_OK) {
+        auto* ctl = p->ctl.as<DevCtl>(1);
+        init_ctl(ctl, st);
+        minmax(d_x, x_f32, p->n, ctl, st);
+        const DevCtl hc = read_ctl(p, ctl, st);
+        if (hc.nonfinite) fail(UMCG_NON_FINITE_VALUE, "non-finite field value");
+        fail(perr, pmsg);
+    }
+    const int D1 = p->mode == 1 ? 1 : p->dim;
+    const uint64_t need = archive_bound(p->n, p->n_slots, D1, name.size());
+    if (!d_ar || cap < need)
+        fail(UMCG_INVALID_ARGUMENT, "archive capacity " + std::to_string(cap) + " < bound " + std::to_string(need));
+
+    CompressMode m{};
+    if (prm.bound_kind == 0) {
+        double tc[2];
+        host_budget(prm.tau, prm.split_rho, prm.coeff_abs_sum, tc);
+        m.lossless[0] = tc[0] == 0.0;
+        m.lossless[1] = tc[1] == 0.0;
+    } else {
+        m.lossless[0] = m.lossless[1] = prm.tau == 0.0;
+    }
+    for (int iter = 0; iter < 3; ++iter) {
+        const DevCtl hc = compress_pass(p, prm, d_x, x_f32, name, d_ar, m, st);
+        if (hc.nonfinite) fail(UMCG_NON_FINITE_VALUE, "non-finite field value");
+        bool redo = false;
+        for (int c = 0; c < 2; ++c) {
+            const bool ll = (hc.lossless >> c) & 1;
+            if (ll != m.lossless[c]) { m.lossless[c] = ll; m.serial[c] = false; redo = true; }
+            if (!ll && !m.serial[c] && hc.need_serial[c]) { m.serial[c] = true; redo = true; }
+        }
+        if (!redo) {
+            *out_len = hc.archive_len;
+            return;
+        }
+    }
+    fail(UMCG_INTERNAL_INCONSISTENCY, "compress did not converge");
+}
+
+// ---------------------------------------------------------------------------
+// Decode side
+// ---------------------------------------------------------------------------
+struct HostReader {
+    const uint8_t* p;
+    uint64_t n, pos = 0;
+    bool err = false;
+    bool need(uint64_t k) { if (n - pos < k) err = true; return !err; }
+    uint64_t le(int k) {
+        if (!need((uint64_t)k)) return 0;
+        uint64_t v = 0;
+        for (int i = 0; i < k; ++i) v |= (uint64_t)p[pos + i] << (8 * i);
+        pos += (uint64_t)k;
+        return v;
+    }
+    double f64() { uint64_t u = le(8); double d; std::memcpy(&d, &u, 8); return d; }
+};
+
+// parse_component (codec.hpp:342-362) on header bytes; false -> corrupt.
+bool parse_comp_header(const uint8_t* b, uint64_t avail, uint64_t payload_len, CompHeader& h, std::string& why) {
+    HostReader r{b, std::min(avail, payload_len)};
+    h.codec = (int)r.le(1);
+    h.pred = (int)r.le(1);
+    h.backend = (int)r.le(1);
+    (void)r.le(1);
+    h.tau = r.f64();
+    h.n = r.le(8);
+    h.D = (int)r.le(1);
+    if (r.err) { why = "unexpected end of data"; return false; }
+    if (h.pred > 2) { why = "bad predictor byte"; return false; }
+    uint64_t prod = 1;
+    for (int d = 0; d < h.D; ++d) {
+        const uint64_t v = r.le(8);
+        if (d < 8) h.dims[d] = v;
+        prod *= v;
+    }
+    if (r.err) { why = "unexpected end of data"; return false; }
+    if (h.D == 0 || prod != h.n) { why = "dims product does not match element count"; return false; }
+    return true;
+}
+
+// decode's own prefix: n_escapes after the dims (codec.hpp:385).
+void finish_comp_header(const uint8_t* b, uint64_t avail, uint64_t payload_len, CompHeader& h) {
+    const uint64_t o = 21 + 8ull * h.D;
+    HostReader r{b, std::min(avail, payload_len)};
+    r.pos = o;
+    h.n_esc = r.le(8);
+    if (r.err) fail(UMCG_CORRUPT_PAYLOAD, "unexpected end of data");
+    h.esc_off = o + 8;
+}
+
+}  // namespace
+
+// codec.hpp:364-441 on device memory. h.n_esc/esc_off already read.
+void decode_component(umcg_plan* p, const CompHeader& h, const uint8_t* d_payload, double* d_out, cudaStream_t st) {
+    const uint64_t payload_len = h.stream_off + h.stream_len;  // set by caller as full payload length
+    (void)payload_len;
+    if (h.codec == 1 || h.codec >= 128)
+        fail(UMCG_UNKNOWN_CODEC, "codec " + std::to_string(h.codec) + " is a host plugin (out of the device path)");
+    if (h.codec != 0) fail(UMCG_CORRUPT_PAYLOAD, "unknown codec id in payload");
+    if (h.D > 8) fail(UMCG_CORRUPT_PAYLOAD, "codec supports at most 8 dimensions");
+    if (h.n_esc > h.n) fail(UMCG_CORRUPT_PAYLOAD, "escape count exceeds element count");
+    auto* ctl = p->ctl.as<DevCtl>(1);
+    init_ctl(ctl, st);
+    uint64_t* eidx = nullptr;
+    double* evals = nullptr;
+    if (h.n_esc) {
+        if (h.stream_off < h.esc_off + 16 * h.n_esc) fail(UMCG_CORRUPT_PAYLOAD, "unexpected end of data");
+        eidx = p->scratch_a.as<uint64_t>(h.n_esc);
+        evals = p->scratch_b.as<double>(h.n_esc);
+        k_read_escapes<<<blocks(h.n_esc), THREADS, 0, st>>>(d_payload + h.esc_off, h.n_esc, h.n, eidx, evals, ctl);
+        UMCG_LAUNCHED();
+        const DevCtl hc = read_ctl(p, ctl, st);
+        if (hc.err == DE_CORRUPT_ESCAPE) fail(UMCG_CORRUPT_PAYLOAD, "bad escape index sequence");
+    }
+    if (h.backend != 0)
+        fail(UMCG_UNKNOWN_CODEC, "lossless backend " + std::to_string(h.backend) + " not registered");
+    uint64_t* codes = p->dcodes.as<uint64_t>(h.n ? h.n : 1);
+    init_ctl(ctl, st);
+    stream_decode(d_payload + h.stream_off, h.stream_len, h.n, codes, p->dec, ctl, st);
+    const NdShape sh = make_shape(h.D, h.dims);
+    const int pred = (h.pred == 2 && h.D == 1) ? 1 : h.pred;  // 1-axis Lorenzo == lorenzo_1d
+    if (h.tau == 0.0) {
+        if (h.n_esc != 0) fail(UMCG_CORRUPT_PAYLOAD, "lossless payload with escapes");
+        if (pred == 2) {
+            serial_decode(codes, h.n, pred, sh, 0.0, nullptr, nullptr, 0, d_out, st);
+        } else {
+            uint64_t* sc = p->kbuf.as<uint64_t>(cdiv(h.n, RECON_TILE) + 1);
+            recon_lossless(codes, h.n, pred, d_out, sc, st);
+        }
+        return;
+    }
+    const double bin = 2.0 * h.tau;
+    if (h.n_esc || !std::isfinite(bin)) {
+        serial_decode(codes, h.n, h.pred, sh, h.tau, eidx, evals, h.n_esc, d_out, st);
+        return;
+    }
+    int64_t* kb = p->kbuf.as<int64_t>(std::max<uint64_t>(h.n, cdiv(h.n, RECON_TILE) + 1));
+    init_ctl(ctl, st);
+    recon_lossy(codes, h.n, pred, sh, bin, kb, d_out, ctl, st);
+    if (pred != 0) {
+        const DevCtl hc = read_ctl(p, ctl, st);
+        const double lim = pred == 1 ? 1073741824.0 : std::ldexp(1.0, 31 - h.D);
+        if (!((double)hc.max_abs_k[0] < lim))  // far from the lattice regime: replay the chain exactly
+            serial_decode(codes, h.n, h.pred, sh, h.tau, nullptr, nullptr, 0, d_out, st);
+    }
+}
+
+namespace {
+
+void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_out, cudaStream_t st) {
+    if (!p || (!d_ar && len)) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
+    std::lock_guard<std::mutex> lock(p->mu);
+    UMCG_CUDA(cudaSetDevice(p->device));
+    // deserialize_archive (pipeline.hpp:237-267): all truncation -> malformed_file
+    const uint64_t head = std::min<uint64_t>(len, 10 + 65535 + 24 + 8 + 29 + 64);
+    auto* hb = static_cast<uint8_t*>(p->hstage.reserve(std::max<uint64_t>(head, 128) + 128));
+    if (head) UMCG_CUDA(cudaMemcpyAsync(hb, d_ar, head, cudaMemcpyDeviceToHost, st));
+    UMCG_CUDA(cudaStreamSynchronize(st));
+    if (len < 4) fail(UMCG_MALFORMED_FILE, "file too short for archive header");
+    if (std::memcmp(hb, "UMCZ", 4) != 0) fail(UMCG_MALFORMED_FILE, "bad magic for archive");
+    HostReader r{hb, head};
+    r.pos = 4;
+    const uint64_t ver = r.le(2);
+    if (r.err) fail(UMCG_MALFORMED_FILE, "truncated archive: unexpected end of data");
+    if (ver != 1) fail(UMCG_MALFORMED_FILE, "unsupported archive format version " + std::to_string(ver));
+    const uint64_t flags = r.le(2);
+    const uint64_t nl = r.le(2);
+    r.need(nl);
+    r.pos += nl;
+    const uint64_t digest = r.le(8);
+    (void)r.f64();
+    (void)r.f64();
+    const uint64_t l1 = r.le(8);
+    if (r.err) fail(UMCG_MALFORMED_FILE, "truncated archive: unexpected end of data");
+    const uint64_t p1 = r.pos;
+    if (len - p1 < l1) fail(UMCG_MALFORMED_FILE, "truncated archive: unexpected end of data");
+    CompHeader h1{};
+    std::string why;
+    if (!parse_comp_header(hb + p1, head - p1, l1, h1, why)) fail(UMCG_MALFORMED_FILE, "truncated archive: " + why);
+    // component 2 header
+    const uint64_t o2 = p1 + l1;
+    if (len - o2 < 8) fail(UMCG_MALFORMED_FILE, "truncated archive: unexpected end of data");
+    uint8_t tail[8 + 29 + 64 + 8];
+    const uint64_t tl = std::min<uint64_t>(sizeof tail, len - o2);
+    UMCG_CUDA(cudaMemcpyAsync(tail, d_ar + o2, tl, cudaMemcpyDeviceToHost, st));
+    UMCG_CUDA(cudaStreamSynchronize(st));
+    HostReader r2{tail, tl};
+    const uint64_t l2 = r2.le(8);
+    const uint64_t p2 = o2 + 8;
+    if (len - p2 < l2) fail(UMCG_MALFORMED_FILE, "truncated archive: unexpected end of data");
+    const bool baseline = flags & 8u;
+    CompHeader h2{};
+    if (l2) {
+        if (!parse_comp_header(tail + 8, tl - 8, l2, h2, why)) fail(UMCG_MALFORMED_FILE, "truncated archive: " + why);
+    } else if (!baseline) {
+        fail(UMCG_MALFORMED_FILE, "missing residual component");
+    }
+    if (p2 + l2 != len) fail(UMCG_MALFORMED_FILE, "trailing bytes in archive");
+
+    auto prep = [&](CompHeader& h, const uint8_t* hostb, uint64_t avail, uint64_t pl) {
+        finish_comp_header(hostb, avail, pl, h);
+        h.stream_off = h.esc_off + 16 * h.n_esc;
+        if (h.n_esc > h.n) fail(UMCG_CORRUPT_PAYLOAD, "escape count exceeds element count");
+        if (h.stream_off > pl) fail(UMCG_CORRUPT_PAYLOAD, "unexpected end of data");
+        h.stream_len = pl - h.stream_off;
+    };
+    if (baseline) {  // pipeline.hpp:184-187
+        if (h1.n != p->n) fail(UMCG_MAPPING_MISMATCH, "vertex count does not match archive component");
+        prep(h1, hb + p1, head - p1, l1);
+        decode_component(p, h1, d_ar + p1, d_out, st);
+        UMCG_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    // pipeline.hpp:188-197
+    if (digest != p->digest) fail(UMCG_MAPPING_MISMATCH, "archive was compressed with a different mapping");
+    const bool seed = p->mode == 1;
+    if (seed != (bool)(flags & 1u)) fail(UMCG_MAPPING_MISMATCH, "mapping mode does not match archive");
+    if (h1.n != p->n_slots) fail(UMCG_MAPPING_MISMATCH, "grid size does not match archive component");
+    if (h2.n != p->n) fail(UMCG_MAPPING_MISMATCH, "vertex count does not match archive component");
+    prep(h1, hb + p1, head - p1, l1);
+    prep(h2, tail + 8, tl - 8, l2);
+    double* x1 = p->x1.as<double>(p->n_slots ? p->n_slots : 1);
+    decode_component(p, h1, d_ar + p1, x1, st);
+    decode_component(p, h2, d_ar + p2, d_out, st);
+    const int g_kind = (flags & 2u) ? 1 : 0;
+    if (g_kind == 1 && seed) fail(UMCG_SEED_MODE_UNSUPPORTED, "multilinear back-interpolation needs a dense grid component");
+    if (g_kind == 1 && !p->has_coords) fail(UMCG_INVALID_ARGUMENT, "multilinear g needs a plan with vertex coordinates");
+    ResidualSrc rs{};
+    rs.node = p->d_node.as<uint32_t>(1);
+    rs.x1 = x1;
+    rs.g_kind = g_kind;
+    rs.coords = p->has_coords ? p->d_coords.as<double>(1) : nullptr;
+    rs.axes = p->d_axes.as<double>(1);
+    rs.axis_off = p->d_axis_off.as<uint64_t>(1);
+    rs.D = p->dim;
+    for (int d = 0; d < 3; ++d) rs.shape[d] = p->shape[d];
+    recompose(rs, p->n, d_out, st);
+    UMCG_CUDA(cudaStreamSynchronize(st));
+}
+
+// Thread-local workspace for the plan-less codec entry points.
+umcg_plan* codec_ws() {
+    thread_local std::unique_ptr<umcg_plan> ws;
+    if (!ws) ws.reset(new umcg_plan);
+    return ws.get();
+}
+
+void encode_impl(const double* d_v, uint64_t n, int pred, int D, const uint64_t* dims, double tau, int codec,
+                 int backend, uint8_t* d_out, uint64_t cap, uint64_t* out_len, cudaStream_t st) {
+    if (!out_len || (n && !d_v) || (D > 0 && !dims)) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
+    // validate_codec_spec (codec.hpp:50-57)
+    if (!(tau >= 0.0)) fail(UMCG_ERROR, "tau_abs must be >= 0");
+    uint64_t prod = 1;
+    for (int d = 0; d < D; ++d) prod *= dims[d];
+    if (D <= 0 || prod != n) fail(UMCG_ERROR, "codec dims product does not equal element count");
+    if (D > 8) fail(UMCG_ERROR, "codec supports at most 8 dimensions");
+    if (pred < 0 || pred > 2) fail(UMCG_UNKNOWN_CODEC, "bad predictor id");
+    umcg_plan* p = codec_ws();
+    auto* ctl = p->ctl.as<DevCtl>(1);
+    init_ctl(ctl, st);
+    minmax(d_v, 0, n, ctl, st);
+    DevCtl hc = read_ctl(p, ctl, st);
+    if (hc.nonfinite) fail(UMCG_NON_FINITE_VALUE, "non-finite input to encode");
+    if (codec == 1 || codec >= 128) fail(UMCG_UNKNOWN_CODEC, "codec " + std::to_string(codec) + " is a host plugin (out of the device path)");
+    if (codec != 0) fail(UMCG_UNKNOWN_CODEC, "unknown codec id " + std::to_string(codec));
+    if (backend != 0) fail(UMCG_UNKNOWN_CODEC, "lossless backend " + std::to_string(backend) + " not registered");
+    const uint64_t need = payload_bound(n, D);
+    if (!d_out || cap < need) fail(UMCG_INVALID_ARGUMENT, "payload capacity " + std::to_string(cap) + " < bound " + std::to_string(need));
+    const NdShape sh = make_shape(D, dims);
+    const int epred = (pred == 2 && D == 1) ? 1 : pred;
+    const bool lossless = tau == 0.0;
+    bool serial = false;
+    for (int iter = 0; iter < 2; ++iter) {
+        init_ctl(ctl, st);
+        DevCtl hset{};
+        hset.tau_c[0] = tau;
+        hset.bin[0] = 2.0 * tau;
+        hset.min_key = ~0ull;
+        UMCG_CUDA(cudaMemcpyAsync(ctl, &hset, sizeof(DevCtl), cudaMemcpyHostToDevice, st));
+        const bool wide = lossless || serial;
+        void* codes = p->codes1.reserve((n ? n : 1) * (wide ? 8 : 4));
+        uint64_t* eidx = nullptr;
+        double* evals = nullptr;
+        if (serial) {
+            eidx = p->scratch_a.as<uint64_t>(n ? n : 1);
+            evals = p->scratch_b.as<double>(2 * (n ? n : 1));
+            serial_encode(d_v, n, pred, sh, tau, static_cast<uint64_t*>(codes), evals + n, eidx, evals, ctl, 0, st);
+        } else if (lossless) {
+            if (epred == 2) {  // N-D lossless codes are parallel (exact prediction from exact values)
+                codes_lossless_values(d_v, n, 2, sh, static_cast<uint64_t*>(codes), st);
+            } else {
+                codes_lossless_values(d_v, n, epred, sh, static_cast<uint64_t*>(codes), st);
+            }
+        } else {
+            int32_t* kb = p->kbuf.as<int32_t>(n ? n : 1);
+            codes_lossy_values(d_v, n, epred, sh, ctl, 0, static_cast<uint32_t*>(codes), kb, st);
+        }
+        StreamEncScratch es = stream_enc_carve(p->enc1.reserve(stream_enc_scratch_bytes(n)), n);
+        if (wide) stream_plan_u64(static_cast<uint64_t*>(codes), n, es, ctl, 0, st);
+        else stream_plan_u32(static_cast<uint32_t*>(codes), n, es, ctl, 0, st);
+        k_layout_component<<<1, 32, 0, st>>>(pred, D, sh, n, ctl, d_out);
+        UMCG_LAUNCHED();
+        if (serial) {
+            hc = read_ctl(p, ctl, st);
+            if (hc.n_esc[0]) {
+                k_write_escapes<<<blocks(hc.n_esc[0]), THREADS, 0, st>>>(eidx, evals, hc.n_esc[0], ctl, 0, d_out);
+                UMCG_LAUNCHED();
+            }
+        }
+        if (wide) stream_write_u64(static_cast<uint64_t*>(codes), n, es, ctl, 0, d_out, true, st);
+        else stream_write_u32(static_cast<uint32_t*>(codes), n, es, ctl, 0, d_out, true, st);
+        hc = read_ctl(p, ctl, st);
+        if (!lossless && !serial && hc.need_serial[0]) { serial = true; continue; }
+        *out_len = hc.archive_len;
+        return;
+    }
+    fail(UMCG_INTERNAL_INCONSISTENCY, "encode did not converge");
+}
+
+void decode_impl(const uint8_t* d_p, uint64_t len, double* d_out, uint64_t cap, uint64_t* n_out, cudaStream_t st) {
+    if (!n_out || (!d_p && len)) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
+    umcg_plan* p = codec_ws();
+    uint8_t hb[21 + 64 + 8];
+    const uint64_t k = std::min<uint64_t>(len, sizeof hb);
+    if (k) UMCG_CUDA(cudaMemcpyAsync(hb, d_p, k, cudaMemcpyDeviceToHost, st));
+    UMCG_CUDA(cudaStreamSynchronize(st));
+    CompHeader h{};
+    std::string why;
+    if (!parse_comp_header(hb, k, len, h, why)) fail(UMCG_CORRUPT_PAYLOAD, why);
+    finish_comp_header(hb, k, len, h);
+    if (h.n_esc > h.n) fail(UMCG_CORRUPT_PAYLOAD, "escape count exceeds element count");
+    h.stream_off = h.esc_off + 16 * h.n_esc;
+    if (h.stream_off > len) fail(UMCG_CORRUPT_PAYLOAD, "unexpected end of data");
+    h.stream_len = len - h.stream_off;
+    if (h.n > cap || (h.n && !d_out)) fail(UMCG_INVALID_ARGUMENT, "output capacity too small");
+    decode_component(p, h, d_p, d_out, st);
+    UMCG_CUDA(cudaStreamSynchronize(st));
+    *n_out = h.n;
+}
+
+}  // namespace
+}  // namespace umcg
+
+using namespace umcg;
+
+extern "C" {
+
+const char* umcg_last_error(void) { return g_last_error.c_str(); }
+const char* umcg_version(void) { return "umcg 0.1 (sm_100a)"; }
+uint64_t umcg_kernel_launches(void) { return g_launches.load(); }
+
+umcg_status umcg_plan_create(const umcg_grid_desc* grid, const umcg_mapping_desc* mapping, int mesh_dim,
+                             const double* coords, umcg_plan** out) {
+    return guarded([&] {
+        if (!out) fail(UMCG_INVALID_ARGUMENT, "NULL out");
+        *out = plan_create_host(grid, mapping, mesh_dim, coords);
+    });
+}
+
+umcg_status umcg_plan_build(const umcg_grid_desc* init_grid, uint64_t n, const double* d_coords, double thr,
+                            int keep_coords, umcg_plan** out) {
+    return guarded([&] {
+        if (!out) fail(UMCG_INVALID_ARGUMENT, "NULL out");
+        *out = plan_build_gpu(init_grid, n, d_coords, thr, keep_coords);
+    });
+}
+
+umcg_status umcg_plan_destroy(umcg_plan* plan) {
+    return guarded([&] { delete plan; });
+}
+
+umcg_status umcg_plan_get_info(const umcg_plan* p, umcg_plan_info* info) {
+    return guarded([&] {
+        if (!p || !info) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
+        info->dim = p->dim;
+        info->mode = p->mode;
+        info->n_vertices = p->n;
+        info->n_slots = p->n_slots;
+        for (int d = 0; d < 3; ++d) info->shape[d] = p->shape[d];
+        info->n_visited = p->n_visited;
+        info->visited_fraction = p->visited_fraction;
+        info->digest = p->digest;
+        info->has_coords = p->has_coords ? 1 : 0;
+    });
+}
+
+umcg_status umcg_plan_export(const umcg_plan* pc, uint64_t* assignments, uint64_t* visited, double* axes) {
+    return guarded([&] {
+        auto* p = const_cast<umcg_plan*>(pc);
+        if (!p) fail(UMCG_INVALID_ARGUMENT, "NULL plan");
+        if (assignments && p->n) {
+            std::vector<uint32_t> a(p->n);
+            UMCG_CUDA(cudaMemcpy(a.data(), p->d_node.get(), p->n * 4, cudaMemcpyDeviceToHost));
+            for (uint64_t i = 0; i < p->n; ++i) assignments[i] = a[i];
+        }
+        if (visited && p->mode == 1 && p->n_visited)
+            UMCG_CUDA(cudaMemcpy(visited, p->d_visited.get(), p->n_visited * 8, cudaMemcpyDeviceToHost));
+        if (axes) std::memcpy(axes, p->axes.data(), p->axes.size() * 8);
+    });
+}
+
+umcg_status umcg_compress_bound(const umcg_plan* p, const char* name, uint64_t* bytes) {
+    return guarded([&] {
+        if (!p || !bytes) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
+        const int D1 = p->mode == 1 ? 1 : p->dim;
+        *bytes = archive_bound(p->n, p->n_slots, D1, name ? std::strlen(name) : 0);
+    });
+}
+
+umcg_status umcg_compress(umcg_plan* p, const umcg_params* prm, const double* d_values, const char* name,
+                          uint8_t* d_archive, uint64_t cap, uint64_t* len, void* stream) {
+    return guarded([&] {
+        compress_impl(p, prm, d_values, 0, name, d_archive, cap, len, static_cast<cudaStream_t>(stream));
+    });
+}
+
+umcg_status umcg_compress_batch(umcg_plan* p, const umcg_params* prm, const void* d_values, int dtype,
+                                int n_fields, const char* const* names, uint8_t* d_archive, uint64_t cap,
+                                uint64_t* lens, void* stream) {
+    return guarded([&] {
+        if (!p || !lens || n_fields < 0) fail(UMCG_INVALID_ARGUMENT, "bad argument");
+        const size_t es = dtype == 1 ? 4 : 8;
+        uint64_t off = 0;
+        for (int f = 0; f < n_fields; ++f) {
+            const void* x = static_cast<const uint8_t*>(d_values) + (size_t)f * p->n * es;
+            uint64_t l = 0;
+            compress_impl(p, prm, x, dtype == 1, names ? names[f] : "", d_archive ? d_archive + off : nullptr,
+                          cap > off ? cap - off : 0, &l, static_cast<cudaStream_t>(stream));
+            lens[f] = l;
+            off += l;
+        }
+    });
+}
+
+umcg_status umcg_decompress(umcg_plan* p, const uint8_t* d_archive, uint64_t len, double* d_out, void* stream) {
+    return guarded([&] { decompress_impl(p, d_archive, len, d_out, static_cast<cudaStream_t>(stream)); });
+}
+
+umcg_status umcg_compress_host(umcg_plan* p, const umcg_params* prm, const double* values, const char* name,
+                               uint8_t* archive, uint64_t cap, uint64_t* len) {
+    return guarded([&] {
+        if (!p || !len) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
+        thread_local DevBuf dx, dar;
+        const uint64_t n = p->n;
+        uint64_t bound = 0;
+        const int D1 = p->mode == 1 ? 1 : p->dim;
+        bound = archive_bound(n, p->n_slots, D1, name ? std::strlen(name) : 0);
+        double* x = dx.as<double>(n ? n : 1);
+        uint8_t* a = dar.as<uint8_t>(bound);
+        if (n) UMCG_CUDA(cudaMemcpyAsync(x, values, n * 8, cudaMemcpyHostToDevice, 0));
+        compress_impl(p, prm, x, 0, name, a, bound, len, 0);
+        if (*len > cap || !archive) fail(UMCG_INVALID_ARGUMENT, "archive buffer too small: need " + std::to_string(*len));
+        UMCG_CUDA(cudaMemcpyAsync(archive, a, *len, cudaMemcpyDeviceToHost, 0));
+        UMCG_CUDA(cudaStreamSynchronize(0));
+    });
+}
+
+umcg_status umcg_decompress_host(umcg_plan* p, const uint8_t* archive, uint64_t len, double* out) {
+    return guarded([&] {
+        if (!p) fail(UMCG_INVALID_ARGUMENT, "NULL plan");
+        thread_local DevBuf dar, dy;
+        uint8_t* a = dar.as<uint8_t>(len ? len : 1);
+        double* y = dy.as<double>(p->n ? p->n : 1);
+        if (len) UMCG_CUDA(cudaMemcpyAsync(a, archive, len, cudaMemcpyHostToDevice, 0));
+        decompress_impl(p, a, len, y, 0);
+        if (p->n) UMCG_CUDA(cudaMemcpyAsync(out, y, p->n * 8, cudaMemcpyDeviceToHost, 0));
+        UMCG_CUDA(cudaStreamSynchronize(0));
+    });
+}
+
+uint64_t umcg_encode_bound(uint64_t n, int ndims) { return payload_bound(n, ndims); }
+
+umcg_status umcg_encode(const double* d_values, uint64_t n, int predictor, int ndims, const uint64_t* dims,
+                        double tau, int codec_id, int backend_id, uint8_t* d_out, uint64_t cap, uint64_t* out_len,
+                        void* stream) {
+    return guarded([&] {
+        encode_impl(d_values, n, predictor, ndims, dims, tau, codec_id, backend_id, d_out, cap, out_len,
+                    static_cast<cudaStream_t>(stream));
+    });
+}
+
+umcg_status umcg_decode(const uint8_t* d_payload, uint64_t len, double* d_out, uint64_t n_cap, uint64_t* n_out,
+                        void* stream) {
+    return guarded([&] { decode_impl(d_payload, len, d_out, n_cap, n_out, static_cast<cudaStream_t>(stream)); });
+}
+
+umcg_status umcg_rle_compress(const uint8_t*, uint64_t, uint8_t*, uint64_t, uint64_t*, void*) {
+    return guarded([&] { fail(UMCG_ERROR, "umcg_rle_compress: not built in this round"); });
+}
+umcg_status umcg_rle_decompress(const uint8_t*, uint64_t, uint8_t*, uint64_t, uint64_t*, void*) {
+    return guarded([&] { fail(UMCG_ERROR, "umcg_rle_decompress: not built in this round"); });
+}
+
+}  // extern "C"

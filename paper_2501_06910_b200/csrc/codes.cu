@@ -1,0 +1,619 @@
+// Quantization codes and reconstruction on sm_100a.
+//
+// Fast path = lattice reformulation of the reference predictor-quantizer
+// (codec.hpp:300-326). With bin = 2*tau', the serial reference produces
+// recon_i ~= bin*K_i with K_i = round(v_i / bin); its code is then
+// q_i = K_i - sum(+-K_nbr) over the same Lorenzo stencil
+// (codec.hpp:61-80). Every element is independent, so codes are computed in
+// parallel; decode is an exact integer (N-D) prefix sum and recon =
+// fl(K * bin). Codes equal the reference's except where a value sits within
+// the serial chain's rounding drift of a bin boundary.
+//
+// Whenever the lattice could disagree with the reference beyond that window
+// (an escape would be needed, |K| large enough that FP spacing approaches the
+// bin, non-finite bins) the component is flagged and re-encoded by
+// serial_encode: a one-thread exact replica of the reference loop. That path
+// is correct by construction and only exists for pathological inputs.
+//
+// All files compile with --fmad=false: no contraction, IEEE division and
+// round-half-away-from-zero, exactly like the reference build
+// (-ffp-contract=off, proj/CMakeLists.txt:16-17).
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include "kernels.h"
+
+namespace umcg {
+
+NdShape make_shape(int D, const uint64_t* dims) {
+    NdShape s;
+    s.D = D;
+    for (int d = 0; d < 8; ++d) { s.dims[d] = d < D ? dims[d] : 1; s.strides[d] = 1; }
+    for (int d = D - 1; d >= 1; --d) s.strides[d - 1] = s.strides[d] * s.dims[d];  // codec.hpp:87-92
+    return s;
+}
+
+namespace {
+
+constexpr int THREADS = 256;
+constexpr double kQLimit = 2147483647.0;  // codec.hpp:305
+
+// |K| bound under which the lattice codes cannot overflow the int32 code
+// range for a stencil of 2^D terms (|q| <= 2^D * max|K| < 2^31 - 1).
+__host__ __device__ inline double k_limit(int pred, int D) {
+    if (pred == 0) return kQLimit;
+    if (pred == 1) return 1073741824.0;          // 2^30
+    return ldexp(1.0, 31 - (D < 1 ? 1 : D));     // 2^(31-D)
+}
+
+__device__ __forceinline__ void flag_serial(DevCtl* ctl, int comp) {
+    if (ctl->need_serial[comp] == 0) atomicExch(&ctl->need_serial[comp], 1);
+}
+
+// Lattice index of v with the escape / regime checks of codec.hpp:305-314.
+__device__ __forceinline__ double lattice_k(double v, double bin, double tau, double lim,
+                                            DevCtl* ctl, int comp) {
+    const double K = round(v / bin);
+    bool bad = !(fabs(K) < lim);
+    if (!bad) bad = !(fabs(v - K * bin) <= tau);
+    if (bad) flag_serial(ctl, comp);
+    return K;
+}
+
+__device__ __forceinline__ void multi_index(uint64_t lin, const NdShape& sh, uint64_t* idx) {
+    for (int d = sh.D - 1; d >= 0; --d) {
+        idx[d] = lin % sh.dims[d];
+        lin /= sh.dims[d];
+    }
+}
+
+// ---- lossy: none / 1-D over an array ---------------------------------------
+__global__ void __launch_bounds__(THREADS) k_codes_1d(const double* __restrict__ v, uint64_t n, int pred,
+                                                     DevCtl* ctl, int comp, uint32_t* __restrict__ codes) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i >= n) return;
+    const double bin = ctl->bin[comp], tau = ctl->tau_c[comp];
+    const double lim = k_limit(pred, 1);
+    const double K = lattice_k(v[i], bin, tau, lim, ctl, comp);
+    double Kp = 0.0;
+    if (pred == 1 && i > 0) Kp = round(v[i - 1] / bin);
+    const int64_t q = (int64_t)K - (int64_t)Kp;
+    codes[i] = (uint32_t)zz_enc(q);
+}
+
+// ---- lossy N-D: K grid, then the integer Lorenzo stencil --------------------
+__global__ void __launch_bounds__(THREADS) k_lattice_nd(const double* __restrict__ v, uint64_t n, int D,
+                                                       DevCtl* ctl, int comp, int32_t* __restrict__ K) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i >= n) return;
+    const double bin = ctl->bin[comp], tau = ctl->tau_c[comp];
+    K[i] = (int32_t)lattice_k(v[i], bin, tau, k_limit(2, D), ctl, comp);
+}
+
+__global__ void __launch_bounds__(THREADS) k_stencil_nd(const int32_t* __restrict__ K, uint64_t n,
+                                                       NdShape sh, uint32_t* __restrict__ codes) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i >= n) return;
+    uint64_t idx[8];
+    multi_index(i, sh, idx);
+    int64_t pred = 0;
+    for (unsigned mask = 1; mask < (1u << sh.D); ++mask) {  // lorenzo_predict, codec.hpp:66-78
+        uint64_t off = 0;
+        bool ok = true;
+        for (int d = 0; d < sh.D; ++d)
+            if ((mask >> d) & 1u) {
+                if (idx[d] == 0) { ok = false; break; }
+                off += sh.strides[d];
+            }
+        if (!ok) continue;
+        const int64_t term = K[i - off];
+        pred += (__popc(mask) & 1) ? term : -term;
+    }
+    codes[i] = (uint32_t)zz_enc((int64_t)K[i] - pred);
+}
+
+// ---- lossless XOR codes (codec.hpp:276-294) --------------------------------
+__device__ __forceinline__ double lorenzo_fp(const double* __restrict__ v, uint64_t i, const NdShape& sh) {
+    uint64_t idx[8];
+    multi_index(i, sh, idx);
+    double pred = 0.0;
+    for (unsigned mask = 1; mask < (1u << sh.D); ++mask) {
+        uint64_t off = 0;
+        bool ok = true;
+        for (int d = 0; d < sh.D; ++d)
+            if ((mask >> d) & 1u) {
+                if (idx[d] == 0) { ok = false; break; }
+                off += sh.strides[d];
+            }
+        if (!ok) continue;
+        const double term = v[i - off];
+        pred = (__popc(mask) & 1) ? __dadd_rn(pred, term) : __dsub_rn(pred, term);
+    }
+    return pred;
+}
+
+__global__ void __launch_bounds__(THREADS) k_lossless(const double* __restrict__ v, uint64_t n, int pred,
+                                                     NdShape sh, uint64_t* __restrict__ codes) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i >= n) return;
+    double p = 0.0;
+    if (pred == 1) p = i ? v[i - 1] : 0.0;
+    else if (pred == 2) p = lorenzo_fp(v, i, sh);
+    codes[i] = (uint64_t)__double_as_longlong(v[i]) ^ (uint64_t)__double_as_longlong(p);
+}
+
+// ---- residual component -----------------------------------------------------
+// detail::multilinear_at (interp.hpp:97-132), same operation order.
+__device__ double multilinear_at(const ResidualSrc& s, const double* __restrict__ p) {
+    uint64_t lo_idx[3] = {0, 0, 0};
+    double t[3] = {0, 0, 0};
+    for (int d = 0; d < s.D; ++d) {
+        const uint64_t n = s.shape[d];
+        const double* axis = s.axes + s.axis_off[d];
+        if (n == 1) { lo_idx[d] = 0; t[d] = 0.0; continue; }
+        uint64_t lo = 0, hi = n;  // std::upper_bound
+        while (lo < hi) {
+            const uint64_t mid = lo + (hi - lo) / 2;
+            if (!(p[d] < axis[mid])) lo = mid + 1; else hi = mid;
+        }
+        uint64_t h = lo < 1 ? 1 : lo;
+        if (h > n - 1) h = n - 1;
+        const uint64_t l = h - 1;
+        const double w = __ddiv_rn(__dsub_rn(p[d], axis[l]), __dsub_rn(axis[h], axis[l]));
+        lo_idx[d] = l;
+        t[d] = (w < 0.0) ? 0.0 : ((1.0 < w) ? 1.0 : w);  // std::clamp
+    }
+    double acc = 0.0;
+    for (unsigned corner = 0; corner < (1u << s.D); ++corner) {
+        double w = 1.0;
+        uint64_t lin = 0;
+        for (int d = 0; d < s.D; ++d) {
+            const bool high = (corner >> d) & 1u;
+            w = __dmul_rn(w, high ? t[d] : __dsub_rn(1.0, t[d]));
+            const uint64_t n = s.shape[d];
+            uint64_t idx = lo_idx[d] + (high ? 1 : 0);
+            if (idx >= n) idx = n - 1;
+            lin = lin * n + idx;
+        }
+        if (w != 0.0) acc = __dadd_rn(acc, __dmul_rn(w, s.x1[lin]));
+    }
+    return acc;
+}
+
+__device__ __forceinline__ double load_x(const ResidualSrc& s, uint64_t i) {
+    return s.x_f32 ? (double)static_cast<const float*>(s.x)[i] : static_cast<const double*>(s.x)[i];
+}
+
+__device__ __forceinline__ double g_at(const ResidualSrc& s, uint64_t i) {
+    if (s.g_kind == 0) return s.x1[s.node[i]];
+    return multilinear_at(s, s.coords + i * (uint64_t)s.D);
+}
+
+// compute_residuals (interp.hpp:161-170): one IEEE subtract.
+__device__ __forceinline__ double residual_at(const ResidualSrc& s, uint64_t i) {
+    return __dsub_rn(load_x(s, i), g_at(s, i));
+}
+
+constexpr int RES_ITEMS = 4;
+__global__ void __launch_bounds__(THREADS) k_codes_residual(ResidualSrc s, uint64_t n, DevCtl* ctl,
+                                                           uint32_t* __restrict__ codes) {
+    const uint64_t i0 = (blockIdx.x * (uint64_t)THREADS + threadIdx.x) * RES_ITEMS;
+    if (i0 >= n) return;
+    const double bin = ctl->bin[1], tau = ctl->tau_c[1];
+    const double lim = k_limit(1, 1);
+    double Kp = i0 ? round(residual_at(s, i0 - 1) / bin) : 0.0;
+#pragma unroll
+    for (int k = 0; k < RES_ITEMS; ++k) {
+        const uint64_t i = i0 + k;
+        if (i >= n) break;
+        const double K = lattice_k(residual_at(s, i), bin, tau, lim, ctl, 1);
+        codes[i] = (uint32_t)zz_enc((int64_t)K - (int64_t)Kp);
+        Kp = K;
+    }
+}
+
+__global__ void __launch_bounds__(THREADS) k_lossless_residual(ResidualSrc s, uint64_t n,
+                                                              uint64_t* __restrict__ codes) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i >= n) return;
+    const double r = residual_at(s, i);
+    const double p = i ? residual_at(s, i - 1) : 0.0;
+    codes[i] = (uint64_t)__double_as_longlong(r) ^ (uint64_t)__double_as_longlong(p);
+}
+
+__global__ void __launch_bounds__(THREADS) k_materialize_residual(ResidualSrc s, uint64_t n,
+                                                                 double* __restrict__ out) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i < n) out[i] = residual_at(s, i);
+}
+
+__global__ void __launch_bounds__(THREADS) k_recompose(ResidualSrc s, uint64_t n, double* __restrict__ io) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i < n) io[i] = __dadd_rn(g_at(s, i), io[i]);  // approx[i] + x2[i], pipeline.hpp:208
+}
+
+// ---- exact serial replicas (one thread) -------------------------------------
+struct SerialPred {
+    NdShape sh;
+    int pred;
+    uint64_t idx[8];
+    __device__ void init(const NdShape& s, int p) {
+        sh = s;
+        pred = p;
+        for (int d = 0; d < 8; ++d) idx[d] = 0;
+    }
+    __device__ double predict(const double* recon, uint64_t lin) const {  // codec.hpp:94-102
+        if (pred == 0) return 0.0;
+        if (pred == 1) return lin == 0 ? 0.0 : recon[lin - 1];
+        double p = 0.0;
+        for (unsigned mask = 1; mask < (1u << sh.D); ++mask) {
+            uint64_t off = 0;
+            bool ok = true;
+            for (int d = 0; d < sh.D; ++d)
+                if ((mask >> d) & 1u) {
+                    if (idx[d] == 0) { ok = false; break; }
+                    off += sh.strides[d];
+                }
+            if (!ok) continue;
+            const double term = recon[lin - off];
+            p = (__popc(mask) & 1) ? __dadd_rn(p, term) : __dsub_rn(p, term);
+        }
+        return p;
+    }
+    __device__ void advance() {  // codec.hpp:104-109
+        for (int d = sh.D - 1; d >= 0; --d) {
+            if (++idx[d] < sh.dims[d]) return;
+            idx[d] = 0;
+        }
+    }
+};
+
+__global__ void k_serial_encode(const double* __restrict__ v, uint64_t n, int pred, NdShape sh,
+                                double tau, uint64_t* __restrict__ codes, double* __restrict__ recon,
+                                uint64_t* __restrict__ esc_idx, double* __restrict__ esc_val,
+                                DevCtl* ctl, int comp) {
+    if (threadIdx.x | blockIdx.x) return;
+    SerialPred ps;
+    ps.init(sh, pred);
+    const double bin = __dmul_rn(2.0, tau);
+    uint64_t ne = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const double p = ps.predict(recon, i);
+        if (tau == 0.0) {
+            codes[i] = (uint64_t)__double_as_longlong(v[i]) ^ (uint64_t)__double_as_longlong(p);
+            recon[i] = v[i];
+        } else {
+            const double qd = round(__ddiv_rn(__dsub_rn(v[i], p), bin));
+            bool escape = !(fabs(qd) <= kQLimit);
+            double r = 0.0;
+            if (!escape) {
+                r = __dadd_rn(p, __dmul_rn(qd, bin));
+                escape = !(fabs(__dsub_rn(v[i], r)) <= tau);
+            }
+            if (escape) {
+                esc_idx[ne] = i;
+                esc_val[ne] = v[i];
+                ++ne;
+                codes[i] = 0;
+                recon[i] = v[i];
+            } else {
+                codes[i] = zz_enc((int64_t)qd);
+                recon[i] = r;
+            }
+        }
+        ps.advance();
+    }
+    ctl->n_esc[comp] = ne;
+}
+
+__global__ void k_serial_decode(const uint64_t* __restrict__ codes, uint64_t n, int pred, NdShape sh,
+                                double tau, const uint64_t* __restrict__ esc_idx,
+                                const double* __restrict__ esc_val, uint64_t n_esc,
+                                double* __restrict__ recon) {
+    if (threadIdx.x | blockIdx.x) return;
+    SerialPred ps;
+    ps.init(sh, pred);
+    const double bin = __dmul_rn(2.0, tau);
+    uint64_t next = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const double p = ps.predict(recon, i);
+        const uint64_t z = codes[i];
+        if (tau == 0.0) {
+            recon[i] = __longlong_as_double((long long)(z ^ (uint64_t)__double_as_longlong(p)));
+        } else if (next < n_esc && esc_idx[next] == i) {
+            recon[i] = esc_val[next++];
+        } else {
+            recon[i] = __dadd_rn(p, __dmul_rn((double)zz_dec(z), bin));
+        }
+        ps.advance();
+    }
+}
+
+// ---- decode: lattice reconstruction ----------------------------------------
+// 1-D inclusive scan of zz_dec(codes) in three passes (tile sums, one-CTA
+// scan of tile sums, tile scan + epilogue).
+constexpr int SC_ITEMS = 8;
+constexpr uint64_t SC_TILE = THREADS * SC_ITEMS;
+
+__global__ void __launch_bounds__(THREADS) k_tile_sums(const uint64_t* __restrict__ codes, uint64_t n,
+                                                      int64_t* __restrict__ sums) {
+    using BR = cub::BlockReduce<int64_t, THREADS>;
+    __shared__ typename BR::TempStorage tmp;
+    const uint64_t b = blockIdx.x * SC_TILE + (uint64_t)threadIdx.x * SC_ITEMS;
+    int64_t s = 0;
+    for (int k = 0; k < SC_ITEMS; ++k)
+        if (b + k < n) s += zz_dec(codes[b + k]);
+    const int64_t t = BR(tmp).Sum(s);
+    if (threadIdx.x == 0) sums[blockIdx.x] = t;
+}
+
+__global__ void k_scan_sums(int64_t* __restrict__ sums, uint64_t T) {
+    using BS = cub::BlockScan<int64_t, 1024>;
+    __shared__ typename BS::TempStorage tmp;
+    const uint64_t per = (T + 1023) / 1024;
+    const uint64_t t0 = threadIdx.x * per, t1 = min(T, t0 + per);
+    int64_t local = 0;
+    for (uint64_t t = t0; t < t1; ++t) local += sums[t];
+    int64_t excl;
+    BS(tmp).ExclusiveSum(local, excl);
+    for (uint64_t t = t0; t < t1; ++t) {
+        const int64_t c = sums[t];
+        sums[t] = excl;
+        excl += c;
+    }
+}
+
+__device__ __forceinline__ void note_k(DevCtl* ctl, int64_t K) {
+    const unsigned long long a = (unsigned long long)(K < 0 ? -K : K);
+    if (a > ctl->max_abs_k[0]) atomicMax(&ctl->max_abs_k[0], a);
+}
+
+__global__ void __launch_bounds__(THREADS) k_tile_recon_1d(const uint64_t* __restrict__ codes, uint64_t n,
+                                                          const int64_t* __restrict__ carry, double bin,
+                                                          double* __restrict__ out, DevCtl* ctl) {
+    using BS = cub::BlockScan<int64_t, THREADS>;
+    __shared__ typename BS::TempStorage tmp;
+    const uint64_t b = blockIdx.x * SC_TILE + (uint64_t)threadIdx.x * SC_ITEMS;
+    int64_t q[SC_ITEMS];
+    int64_t s = 0;
+#pragma unroll
+    for (int k = 0; k < SC_ITEMS; ++k) {
+        q[k] = b + k < n ? zz_dec(codes[b + k]) : 0;
+        s += q[k];
+    }
+    int64_t excl;
+    BS(tmp).ExclusiveSum(s, excl);
+    int64_t K = excl + carry[blockIdx.x];
+    int64_t kmax = 0;
+#pragma unroll
+    for (int k = 0; k < SC_ITEMS; ++k) {
+        if (b + k >= n) break;
+        K += q[k];
+        out[b + k] = __dmul_rn((double)K, bin);
+        const int64_t a = K < 0 ? -K : K;
+        kmax = a > kmax ? a : kmax;
+    }
+    note_k(ctl, kmax);
+}
+
+__global__ void __launch_bounds__(THREADS) k_recon_none(const uint64_t* __restrict__ codes, uint64_t n,
+                                                       double bin, double* __restrict__ out) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i < n) out[i] = __dmul_rn((double)zz_dec(codes[i]), bin);
+}
+
+__global__ void __launch_bounds__(THREADS) k_zz_to_k(const uint64_t* __restrict__ codes, uint64_t n,
+                                                    int64_t* __restrict__ K) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i < n) K[i] = zz_dec(codes[i]);
+}
+
+// Inclusive prefix sum along axis d of an N-D int64 array, one thread per
+// line (lines along the last axis are handled the same way; adequate for the
+// grid component, which is ~n/8 of the residual component).
+__global__ void __launch_bounds__(THREADS) k_axis_scan(int64_t* __restrict__ K, NdShape sh, int d,
+                                                      uint64_t n_lines) {
+    const uint64_t line = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (line >= n_lines) return;
+    const uint64_t stride = sh.strides[d], len = sh.dims[d];
+    // line -> base offset: decompose over all axes except d
+    const uint64_t inner = stride;             // product of dims after d
+    const uint64_t outer_i = line / inner, inner_i = line % inner;
+    const uint64_t base = outer_i * (len * stride) + inner_i;
+    int64_t acc = 0;
+    for (uint64_t k = 0; k < len; ++k) {
+        acc += K[base + k * stride];
+        K[base + k * stride] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(THREADS) k_k_to_recon(const int64_t* __restrict__ K, uint64_t n, double bin,
+                                                       double* __restrict__ out, DevCtl* ctl) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    int64_t a = 0;
+    if (i < n) {
+        out[i] = __dmul_rn((double)K[i], bin);
+        a = K[i] < 0 ? -K[i] : K[i];
+    }
+    using BR = cub::BlockReduce<int64_t, THREADS>;
+    __shared__ typename BR::TempStorage tmp;
+    const int64_t m = BR(tmp).Reduce(a, cub::Max());
+    if (threadIdx.x == 0) note_k(ctl, m);
+}
+
+// lossless 1-D: recon bits = XOR prefix of codes (codec.hpp:429-430 with
+// pred = previous exact value).
+__global__ void __launch_bounds__(THREADS) k_tile_xor(const uint64_t* __restrict__ codes, uint64_t n,
+                                                     uint64_t* __restrict__ sums) {
+    using BR = cub::BlockReduce<uint64_t, THREADS>;
+    __shared__ typename BR::TempStorage tmp;
+    const uint64_t b = blockIdx.x * SC_TILE + (uint64_t)threadIdx.x * SC_ITEMS;
+    uint64_t s = 0;
+    for (int k = 0; k < SC_ITEMS; ++k)
+        if (b + k < n) s ^= codes[b + k];
+    struct X { __device__ uint64_t operator()(uint64_t a, uint64_t b) const { return a ^ b; } };
+    const uint64_t t = BR(tmp).Reduce(s, X());
+    if (threadIdx.x == 0) sums[blockIdx.x] = t;
+}
+
+__global__ void k_scan_xor(uint64_t* __restrict__ sums, uint64_t T) {
+    using BS = cub::BlockScan<uint64_t, 1024>;
+    __shared__ typename BS::TempStorage tmp;
+    struct X { __device__ uint64_t operator()(uint64_t a, uint64_t b) const { return a ^ b; } };
+    const uint64_t per = (T + 1023) / 1024;
+    const uint64_t t0 = threadIdx.x * per, t1 = min(T, t0 + per);
+    uint64_t local = 0;
+    for (uint64_t t = t0; t < t1; ++t) local ^= sums[t];
+    uint64_t excl;
+    BS(tmp).ExclusiveScan(local, excl, 0ull, X());
+    for (uint64_t t = t0; t < t1; ++t) {
+        const uint64_t c = sums[t];
+        sums[t] = excl;
+        excl ^= c;
+    }
+}
+
+__global__ void __launch_bounds__(THREADS) k_tile_recon_xor(const uint64_t* __restrict__ codes, uint64_t n,
+                                                           const uint64_t* __restrict__ carry,
+                                                           double* __restrict__ out) {
+    using BS = cub::BlockScan<uint64_t, THREADS>;
+    __shared__ typename BS::TempStorage tmp;
+    struct X { __device__ uint64_t operator()(uint64_t a, uint64_t b) const { return a ^ b; } };
+    const uint64_t b = blockIdx.x * SC_TILE + (uint64_t)threadIdx.x * SC_ITEMS;
+    uint64_t z[SC_ITEMS];
+    uint64_t s = 0;
+#pragma unroll
+    for (int k = 0; k < SC_ITEMS; ++k) {
+        z[k] = b + k < n ? codes[b + k] : 0;
+        s ^= z[k];
+    }
+    uint64_t excl;
+    BS(tmp).ExclusiveScan(s, excl, 0ull, X());
+    uint64_t acc = excl ^ carry[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < SC_ITEMS; ++k) {
+        if (b + k >= n) break;
+        acc ^= z[k];
+        out[b + k] = __longlong_as_double((long long)acc);
+    }
+}
+
+__global__ void __launch_bounds__(THREADS) k_recon_lossless_none(const uint64_t* __restrict__ codes,
+                                                                uint64_t n, double* __restrict__ out) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i < n) out[i] = __longlong_as_double((long long)codes[i]);
+}
+
+inline unsigned blocks(uint64_t n, uint64_t per = THREADS) { return (unsigned)cdiv(n, per); }
+
+}  // namespace
+
+void codes_lossy_values(const double* v, uint64_t n, int pred, const NdShape& sh, DevCtl* ctl, int comp,
+                        uint32_t* codes, int32_t* kbuf, cudaStream_t st) {
+    if (!n) return;
+    if (pred == 2 && sh.D > 1) {
+        k_lattice_nd<<<blocks(n), THREADS, 0, st>>>(v, n, sh.D, ctl, comp, kbuf);
+        UMCG_LAUNCHED();
+        k_stencil_nd<<<blocks(n), THREADS, 0, st>>>(kbuf, n, sh, codes);
+        UMCG_LAUNCHED();
+    } else {
+        // lorenzo_nd over a single axis is lorenzo_1d
+        k_codes_1d<<<blocks(n), THREADS, 0, st>>>(v, n, pred == 0 ? 0 : 1, ctl, comp, codes);
+        UMCG_LAUNCHED();
+    }
+}
+
+void codes_lossless_values(const double* v, uint64_t n, int pred, const NdShape& sh, uint64_t* codes,
+                           cudaStream_t st) {
+    if (!n) return;
+    k_lossless<<<blocks(n), THREADS, 0, st>>>(v, n, pred, sh, codes);
+    UMCG_LAUNCHED();
+}
+
+void codes_lossy_residual(const ResidualSrc& src, uint64_t n, DevCtl* ctl, uint32_t* codes, cudaStream_t st) {
+    if (!n) return;
+    k_codes_residual<<<blocks(n, (uint64_t)THREADS * RES_ITEMS), THREADS, 0, st>>>(src, n, ctl, codes);
+    UMCG_LAUNCHED();
+}
+
+void codes_lossless_residual(const ResidualSrc& src, uint64_t n, uint64_t* codes, cudaStream_t st) {
+    if (!n) return;
+    k_lossless_residual<<<blocks(n), THREADS, 0, st>>>(src, n, codes);
+    UMCG_LAUNCHED();
+}
+
+void materialize_residual(const ResidualSrc& src, uint64_t n, double* out, cudaStream_t st) {
+    if (!n) return;
+    k_materialize_residual<<<blocks(n), THREADS, 0, st>>>(src, n, out);
+    UMCG_LAUNCHED();
+}
+
+void recompose(const ResidualSrc& src, uint64_t n, double* inout, cudaStream_t st) {
+    if (!n) return;
+    k_recompose<<<blocks(n), THREADS, 0, st>>>(src, n, inout);
+    UMCG_LAUNCHED();
+}
+
+void serial_encode(const double* v, uint64_t n, int pred, const NdShape& sh, double tau, uint64_t* codes,
+                   double* recon_scratch, uint64_t* esc_idx, double* esc_val, DevCtl* ctl, int comp,
+                   cudaStream_t st) {
+    k_serial_encode<<<1, 32, 0, st>>>(v, n, pred, sh, tau, codes, recon_scratch, esc_idx, esc_val, ctl, comp);
+    UMCG_LAUNCHED();
+}
+
+void serial_decode(const uint64_t* codes, uint64_t n, int pred, const NdShape& sh, double tau,
+                   const uint64_t* esc_idx, const double* esc_val, uint64_t n_esc, double* out,
+                   cudaStream_t st) {
+    k_serial_decode<<<1, 32, 0, st>>>(codes, n, pred, sh, tau, esc_idx, esc_val, n_esc, out);
+    UMCG_LAUNCHED();
+}
+
+void recon_lossy(const uint64_t* codes, uint64_t n, int pred, const NdShape& sh, double bin, int64_t* kbuf,
+                 double* out, DevCtl* ctl, cudaStream_t st) {
+    if (!n) return;
+    if (pred == 0) {
+        k_recon_none<<<blocks(n), THREADS, 0, st>>>(codes, n, bin, out);
+        UMCG_LAUNCHED();
+        return;
+    }
+    if (pred == 1 || sh.D <= 1) {
+        const uint64_t T = cdiv(n, SC_TILE);
+        k_tile_sums<<<(unsigned)T, THREADS, 0, st>>>(codes, n, kbuf);
+        UMCG_LAUNCHED();
+        k_scan_sums<<<1, 1024, 0, st>>>(kbuf, T);
+        UMCG_LAUNCHED();
+        k_tile_recon_1d<<<(unsigned)T, THREADS, 0, st>>>(codes, n, kbuf, bin, out, ctl);
+        UMCG_LAUNCHED();
+        return;
+    }
+    k_zz_to_k<<<blocks(n), THREADS, 0, st>>>(codes, n, kbuf);
+    UMCG_LAUNCHED();
+    for (int d = sh.D - 1; d >= 0; --d) {
+        const uint64_t lines = n / sh.dims[d];
+        k_axis_scan<<<blocks(lines), THREADS, 0, st>>>(kbuf, sh, d, lines);
+        UMCG_LAUNCHED();
+    }
+    k_k_to_recon<<<blocks(n), THREADS, 0, st>>>(kbuf, n, bin, out, ctl);
+    UMCG_LAUNCHED();
+}
+
+void recon_lossless(const uint64_t* codes, uint64_t n, int pred, double* out, uint64_t* scratch,
+                    cudaStream_t st) {
+    if (!n) return;
+    if (pred == 0) {
+        k_recon_lossless_none<<<blocks(n), THREADS, 0, st>>>(codes, n, out);
+        UMCG_LAUNCHED();
+        return;
+    }
+    // pred == 1 only (N-D lossless goes through serial_decode)
+    const uint64_t T = cdiv(n, SC_TILE);
+    uint64_t* sums = scratch;  // [cdiv(n, SC_TILE)]
+    k_tile_xor<<<(unsigned)T, THREADS, 0, st>>>(codes, n, sums);
+    UMCG_LAUNCHED();
+    k_scan_xor<<<1, 1024, 0, st>>>(sums, T);
+    UMCG_LAUNCHED();
+    k_tile_recon_xor<<<(unsigned)T, THREADS, 0, st>>>(codes, n, sums, out);
+    UMCG_LAUNCHED();
+}
+
+}  // namespace umcg

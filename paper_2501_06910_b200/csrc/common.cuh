@@ -1,0 +1,331 @@
+// Shared host/device helpers for the umcg sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/umcg.h"
+
+namespace umcg {
+
+// ---------------------------------------------------------------------------
+// Host-side error plumbing: internal code throws Error; the C ABI catches it
+// and returns the status (include/umcg.h).
+// ---------------------------------------------------------------------------
+struct Error : std::runtime_error {
+    umcg_status status;
+    Error(umcg_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+[[noreturn]] inline void fail(umcg_status s, const std::string& m) { throw Error(s, m); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(UMCG_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define UMCG_CUDA(x) ::umcg::cuda_check((x), #x)
+
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+#define UMCG_LAUNCHED()                                  \
+    do {                                                 \
+        ::umcg::count_launch();                          \
+        ::umcg::cuda_check(cudaGetLastError(), "launch"); \
+    } while (0)
+
+inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// Error codes raised on the device land in DevCtl::err (first writer wins).
+enum DevErr : int {
+    DE_NONE = 0,
+    DE_CORRUPT_END = 1,       // unexpected end of data
+    DE_CORRUPT_VARINT = 2,    // varint exceeds 64 bits
+    DE_CORRUPT_TOKEN = 3,     // unknown token in lossless stream
+    DE_CORRUPT_TRAILING = 4,  // trailing bytes in quantized stream
+    DE_CORRUPT_ESCAPE = 5,    // bad escape index sequence
+};
+
+// ---------------------------------------------------------------------------
+// varint / zig-zag (reference common.hpp:60-66, 99-107, 129-135)
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint32_t vlen64(uint64_t v) {
+    // bytes of ByteWriter::varint(v): 1 + floor(log128(v))
+    uint32_t bits = v ? 64u - (uint32_t)
+#ifdef __CUDA_ARCH__
+                                  __clzll((long long)v)
+#else
+                                  __builtin_clzll(v)
+#endif
+                      : 1u;
+    return (bits + 6u) / 7u;
+}
+
+__host__ __device__ __forceinline__ uint64_t zz_enc(int64_t v) {
+    return ((uint64_t)v << 1) ^ (uint64_t)(v >> 63);
+}
+__host__ __device__ __forceinline__ int64_t zz_dec(uint64_t v) {
+    return (int64_t)(v >> 1) ^ -(int64_t)(v & 1);
+}
+
+// ---------------------------------------------------------------------------
+// Zero-RLE stream structure (reference lossless.hpp:24-51).
+//
+// The byte stream is the concatenation of varint(code_i). A 0x00 byte occurs
+// exactly when code_i == 0 (every byte of a multi-byte varint is nonzero), so
+// the RLE token structure is decided at code granularity: maximal runs of
+// >= 8 zero codes become Z tokens, everything between becomes literal
+// tokens. RleSum summarizes a contiguous chunk of codes so that chunks
+// compose associatively (used for block- and grid-level scans).
+// ---------------------------------------------------------------------------
+constexpr uint64_t kMinZeroRun = 8;     // lossless.hpp:13 (detail::kMinZeroRun)
+constexpr uint32_t kNoOrigin = 0xffffffffu;
+
+__host__ __device__ __forceinline__ uint64_t lit_size(uint64_t b) { return 1 + vlen64(b) + b; }
+__host__ __device__ __forceinline__ uint64_t z_size(uint64_t r) { return 1 + vlen64(r); }
+
+struct RleSum {
+    uint64_t lz;      // leading zero codes (== chunk length when allzero)
+    uint64_t tz;      // trailing zero codes (0 when allzero)
+    uint64_t fb;      // bytes of the first core segment
+    uint64_t lb;      // bytes of the last core segment (valid when has_int)
+    uint64_t mid;     // output bytes of complete pieces between first and last segment
+    uint32_t origin;  // chunk id where the last segment started
+    uint32_t flags;   // bit0 allzero, bit1 has_int
+    __host__ __device__ bool allzero() const { return flags & 1u; }
+    __host__ __device__ bool has_int() const { return flags & 2u; }
+};
+
+__host__ __device__ __forceinline__ RleSum rle_identity() {
+    RleSum s;
+    s.lz = s.tz = s.fb = s.lb = s.mid = 0;
+    s.origin = kNoOrigin;
+    s.flags = 1u;
+    return s;
+}
+
+__host__ __device__ __forceinline__ RleSum rle_leaf(uint64_t code_bytes, bool zero, uint32_t origin) {
+    RleSum s;
+    s.tz = s.lb = s.mid = 0;
+    if (zero) {
+        s.lz = 1; s.fb = 0; s.origin = kNoOrigin; s.flags = 1u;
+    } else {
+        s.lz = 0; s.fb = code_bytes; s.origin = origin; s.flags = 0u;
+    }
+    return s;
+}
+
+// Summary of A followed by B.
+__host__ __device__ __forceinline__ RleSum rle_compose(const RleSum& A, const RleSum& B) {
+    if (A.allzero()) {
+        RleSum r = B;
+        r.lz += A.lz;
+        return r;
+    }
+    if (B.allzero()) {
+        RleSum r = A;
+        r.tz += B.lz;
+        return r;
+    }
+    RleSum r;
+    r.lz = A.lz;
+    r.tz = B.tz;
+    const uint64_t J = A.tz + B.lz;
+    const bool ah = A.has_int(), bh = B.has_int();
+    if (J >= kMinZeroRun) {
+        r.fb = A.fb;
+        r.lb = bh ? B.lb : B.fb;
+        r.mid = (ah ? A.mid + lit_size(A.lb) : 0) + z_size(J) + (bh ? lit_size(B.fb) + B.mid : 0);
+        r.origin = B.origin;
+        r.flags = 2u;
+    } else {
+        if (!ah && !bh) {
+            r.fb = A.fb + J + B.fb; r.lb = 0; r.mid = 0; r.flags = 0u; r.origin = A.origin;
+        } else if (ah && !bh) {
+            r.fb = A.fb; r.mid = A.mid; r.lb = A.lb + J + B.fb; r.flags = 2u; r.origin = A.origin;
+        } else if (!ah && bh) {
+            r.fb = A.fb + J + B.fb; r.mid = B.mid; r.lb = B.lb; r.flags = 2u; r.origin = B.origin;
+        } else {
+            r.fb = A.fb; r.mid = A.mid + lit_size(A.lb + J + B.fb) + B.mid; r.lb = B.lb;
+            r.flags = 2u; r.origin = B.origin;
+        }
+    }
+    return r;
+}
+
+// Sequential encoder state between chunks: C = output bytes of closed pieces
+// (== header position of the open literal), Lb = bytes in the open literal,
+// Zp = pending (unclassified) zero codes, origin = chunk id of the open literal.
+struct RleState {
+    uint64_t C, Lb, Zp;
+    uint32_t origin;
+    uint32_t has;
+};
+
+__host__ __device__ __forceinline__ RleState rle_state0() {
+    RleState s;
+    s.C = s.Lb = s.Zp = 0;
+    s.origin = kNoOrigin;
+    s.has = 0;
+    return s;
+}
+
+// Advance a state over a summarized chunk. Reports the close of the literal
+// that was open on entry (only if one was open and it closes in the chunk).
+__host__ __device__ __forceinline__ RleState rle_apply(RleState st, const RleSum& S, bool* closed,
+                                                       uint64_t* closed_total) {
+    *closed = false;
+    if (S.allzero()) {
+        st.Zp += S.lz;
+        return st;
+    }
+    const bool entry_open = st.has != 0;
+    const uint64_t J = st.Zp + S.lz;
+    if (J >= kMinZeroRun) {
+        if (entry_open) {
+            *closed = true;
+            *closed_total = st.Lb;
+            st.C += lit_size(st.Lb);
+        }
+        st.C += z_size(J);
+        st.Lb = S.fb;
+        st.origin = S.origin;
+    } else {
+        if (!entry_open) st.origin = S.origin;
+        st.Lb = (entry_open ? st.Lb : 0) + J + S.fb;
+        if (entry_open && S.has_int()) {
+            *closed = true;          // entry literal closes at the first interior run
+            *closed_total = st.Lb;
+        }
+    }
+    st.has = 1;
+    if (S.has_int()) {
+        st.C += lit_size(st.Lb) + S.mid;
+        st.Lb = S.lb;
+        st.origin = S.origin;
+    }
+    st.Zp = S.tz;
+    return st;
+}
+
+// Final close: total stream bytes given the state after the last code.
+__host__ __device__ __forceinline__ uint64_t rle_finish(const RleState& st, bool* closes,
+                                                        uint64_t* total_lit) {
+    *closes = false;
+    if (st.Zp >= kMinZeroRun) {
+        uint64_t c = st.C;
+        if (st.has) { c += lit_size(st.Lb); *closes = true; *total_lit = st.Lb; }
+        return c + z_size(st.Zp);
+    }
+    const uint64_t lb = st.Lb + st.Zp;
+    if (st.has || st.Zp > 0) {
+        *closes = true;
+        *total_lit = lb;
+        return st.C + lit_size(lb);
+    }
+    return st.C;
+}
+
+// ---------------------------------------------------------------------------
+// Per-call device control block: scalars produced and consumed by kernels so
+// that a compress call needs a single host synchronization at the end.
+// ---------------------------------------------------------------------------
+struct DevCtl {
+    // value range / validation (pipeline.hpp:31-41, mesh.hpp:58-64)
+    unsigned long long min_key, max_key;  // order-preserving integer keys of min/max
+    int nonfinite;
+    int err;                              // DevErr, first writer wins
+    // budget (pipeline.hpp:43-57, 94)
+    double tau_abs, tau1, tau2;           // unshaved split
+    double tau_c[2];                      // shaved per component
+    double bin[2];                        // 2 * tau_c
+    int lossless;                         // tau_abs == 0
+    // per-component fast-path verdicts
+    int need_serial[2];                   // escape / regime violation: redo exactly
+    unsigned long long max_abs_k[2];      // |K| maxima (decode regime check)
+    // stream lengths and archive layout
+    uint64_t stream_len[2];
+    uint64_t n_esc[2];
+    uint64_t payload_len[2];
+    uint64_t stream_off[2];               // byte offset of each stream in the output buffer
+    uint64_t archive_len;
+    uint64_t count;                       // generic counter (code ends etc.)
+    uint64_t aux[8];
+};
+
+__device__ __forceinline__ void set_err(DevCtl* c, int e) { atomicCAS(&c->err, 0, e); }
+
+// Order-preserving map double -> u64 (for atomicMin/Max over doubles).
+__host__ __device__ __forceinline__ unsigned long long dkey(double v) {
+    unsigned long long u;
+#ifdef __CUDA_ARCH__
+    u = (unsigned long long)__double_as_longlong(v);
+#else
+    std::memcpy(&u, &v, 8);
+#endif
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__host__ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
+    unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    double v;
+#ifdef __CUDA_ARCH__
+    v = __longlong_as_double((long long)u);
+#else
+    std::memcpy(&v, &u, 8);
+#endif
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// Growable device scratch buffers (per plan / per thread).
+// ---------------------------------------------------------------------------
+class DevBuf {
+public:
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void* reserve(size_t bytes) {
+        if (bytes > cap_) {
+            release();
+            size_t c = bytes < 256 ? 256 : bytes;
+            UMCG_CUDA(cudaMalloc(&p_, c));
+            cap_ = c;
+        }
+        return p_;
+    }
+    template <class T> T* as(size_t n) { return static_cast<T*>(reserve(n * sizeof(T))); }
+    void release() {
+        if (p_) cudaFree(p_);
+        p_ = nullptr;
+        cap_ = 0;
+    }
+    void* get() const { return p_; }
+    size_t capacity() const { return cap_; }
+
+private:
+    void* p_ = nullptr;
+    size_t cap_ = 0;
+};
+
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    ~PinnedBuf() { if (p) cudaFreeHost(p); }
+    void* reserve(size_t bytes) {
+        if (bytes > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            UMCG_CUDA(cudaMallocHost(&p, bytes < 64 ? 64 : bytes));
+            cap = bytes;
+        }
+        return p;
+    }
+};
+
+}  // namespace umcg

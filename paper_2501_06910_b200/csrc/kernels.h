@@ -1,0 +1,124 @@
+// Host-side launchers for the umcg kernels (one declaration per kernel family).
+#pragma once
+
+#include "common.cuh"
+
+namespace umcg {
+
+// ---- stream.cu: zero-RLE varint stream encode / decode --------------------
+constexpr int ENC_THREADS = 256;
+constexpr int ENC_ITEMS = 8;  // <= 9 so a thread opens at most one literal
+constexpr uint64_t ENC_TILE = ENC_THREADS * ENC_ITEMS;
+
+struct StreamEncScratch {
+    RleSum* sums = nullptr;      // [T]
+    RleState* states = nullptr;  // [T+1]
+    uint64_t* P = nullptr;       // [T+1] output start per tile
+    uint64_t* lit_total = nullptr;  // [T]
+};
+size_t stream_enc_scratch_bytes(uint64_t n);
+StreamEncScratch stream_enc_carve(void* base, uint64_t n);
+
+// Encode codes[0..n) (u32 or u64 varint values) as the zero-RLE token stream.
+// Writes ctl->stream_len[comp]; output at dst + ctl->stream_off[comp] when
+// dst_off_from_ctl, else at dst.
+void stream_encode_u32(const uint32_t* codes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl,
+                       int comp, uint8_t* dst, bool dst_off_from_ctl, cudaStream_t st);
+void stream_encode_u64(const uint64_t* codes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl,
+                       int comp, uint8_t* dst, bool dst_off_from_ctl, cudaStream_t st);
+// Phase split used by the pipeline (summaries/scan first, layout, then write).
+void stream_plan_u32(const uint32_t* codes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl,
+                     int comp, cudaStream_t st);
+void stream_plan_u64(const uint64_t* codes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl,
+                     int comp, cudaStream_t st);
+void stream_write_u32(const uint32_t* codes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl,
+                      int comp, uint8_t* dst, bool dst_off_from_ctl, cudaStream_t st);
+void stream_write_u64(const uint64_t* codes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl,
+                      int comp, uint8_t* dst, bool dst_off_from_ctl, cudaStream_t st);
+
+// Decode: zero-RLE token stream -> varint codes (u64 values) [n].
+struct StreamDecScratch {
+    DevBuf tokens;   // token table
+    DevBuf unpacked; // expanded byte stream
+    DevBuf counts;   // per-tile code-end counts
+};
+// Returns on host after a synchronization: fills codes[0..n). Throws corrupt_payload.
+void stream_decode(const uint8_t* d_stream, uint64_t len, uint64_t n, uint64_t* d_codes,
+                   StreamDecScratch& s, DevCtl* ctl, cudaStream_t st);
+
+// Raw byte RLE (umcg_rle_compress): bytes -> codes u64 view is not needed;
+// treated as 1-byte "codes" where zero bytes are zero codes.
+void rle_bytes_encode(const uint8_t* d_in, uint64_t n, const StreamEncScratch& s, DevCtl* ctl,
+                      uint8_t* dst, cudaStream_t st);
+
+// ---- codes.cu: quantization codes (lattice fast path) + exact serial path --
+struct NdShape {
+    int D;
+    uint64_t dims[8];
+    uint64_t strides[8];
+};
+NdShape make_shape(int D, const uint64_t* dims);
+
+// lossy codes of a values array. pred 0 none, 1 lorenzo_1d, 2 lorenzo_nd.
+// Reads bin/tau from ctl->bin[comp]/tau_c[comp]. Flags ctl->need_serial[comp]
+// when the lattice formulation may differ from the serial reference chain.
+void codes_lossy_values(const double* v, uint64_t n, int pred, const NdShape& sh, DevCtl* ctl,
+                        int comp, uint32_t* codes, int32_t* kbuf, cudaStream_t st);
+// lossless (tau == 0) XOR codes (codec.hpp:276-294); always exact.
+void codes_lossless_values(const double* v, uint64_t n, int pred, const NdShape& sh,
+                           uint64_t* codes, cudaStream_t st);
+
+// Residual component (pipeline.hpp:140-146): r_i = x_i - g(x1)_i, lorenzo_1d.
+struct ResidualSrc {
+    const void* x;        // fp64 or fp32 field
+    int x_f32;
+    const uint32_t* node; // slot per vertex (nearest)
+    const double* x1;     // grid component (exact cluster means)
+    int g_kind;           // 0 nearest, 1 multilinear
+    const double* coords; // [n*D] (multilinear)
+    const double* axes;   // concatenated axes (multilinear)
+    const uint64_t* axis_off;  // [D] offsets into axes
+    uint64_t shape[3];
+    int D;
+};
+void codes_lossy_residual(const ResidualSrc& src, uint64_t n, DevCtl* ctl, uint32_t* codes,
+                          cudaStream_t st);
+void codes_lossless_residual(const ResidualSrc& src, uint64_t n, uint64_t* codes, cudaStream_t st);
+void materialize_residual(const ResidualSrc& src, uint64_t n, double* out, cudaStream_t st);
+
+// Exact serial replica of the reference predictor loop (codec.hpp:306-326):
+// codes (u64) + escape records; n_esc -> ctl->n_esc[comp]. One GPU thread.
+void serial_encode(const double* v, uint64_t n, int pred, const NdShape& sh, double tau,
+                   uint64_t* codes, double* recon_scratch, uint64_t* esc_idx, double* esc_val,
+                   DevCtl* ctl, int comp, cudaStream_t st);
+// Exact serial replica of decode (codec.hpp:422-437).
+void serial_decode(const uint64_t* codes, uint64_t n, int pred, const NdShape& sh, double tau,
+                   const uint64_t* esc_idx, const double* esc_val, uint64_t n_esc, double* out,
+                   cudaStream_t st);
+
+// Lattice reconstruction (decode fast path). recon = fl(K * bin), K the
+// (N-D) prefix sum of zigzag-decoded codes. Writes max|K| key into
+// ctl->max_abs_k[0]. out may be a grid array; for the residual component
+// the recompose epilogue adds g(x1')_i.
+void recon_lossy(const uint64_t* codes, uint64_t n, int pred, const NdShape& sh, double bin,
+                 int64_t* kbuf, double* out, DevCtl* ctl, cudaStream_t st);
+void recon_lossless(const uint64_t* codes, uint64_t n, int pred, double* out, uint64_t* scratch,
+                    cudaStream_t st);
+constexpr uint64_t RECON_TILE = 2048;  // scratch for recon_lossless / recon_lossy: cdiv(n, RECON_TILE)+1
+// out[i] = g(x1')_i + recon2[i] (pipeline.hpp:206-208), in place on out.
+void recompose(const ResidualSrc& src, uint64_t n, double* inout, cudaStream_t st);
+
+// ---- interp.cu: range, budget, cluster mean, fill --------------------------
+void minmax(const void* x, int x_f32, uint64_t n, DevCtl* ctl, cudaStream_t st);
+struct BudgetArgs {
+    double tau, rho, coeff_abs_sum;
+    int bound_kind;
+    uint64_t n;
+};
+void budget(const BudgetArgs& a, DevCtl* ctl, cudaStream_t st);
+void cluster_mean(const void* x, int x_f32, const uint32_t* perm, const uint32_t* seg_off,
+                  uint64_t n_slots, double* x1, cudaStream_t st);
+void fill_nearest_visited(const uint32_t* seg_off, uint64_t n_slots, uint64_t row, double* x1,
+                          cudaStream_t st);
+
+}  // namespace umcg

@@ -1,0 +1,381 @@
+// Plan construction: device-resident mapping, stable slot sort, digest, and
+// the GPU grid_coarsen (grid_builder.hpp:286-421).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "plan.h"
+
+namespace umcg {
+
+namespace {
+
+constexpr int THREADS = 256;
+inline unsigned blocks(uint64_t n) { return (unsigned)cdiv(n, THREADS); }
+
+struct Fnv {
+    uint64_t h = 0xcbf29ce484222325ull;
+    void byte(uint8_t b) { h ^= b; h *= 0x100000001b3ull; }
+    void le(uint64_t v, int k) { for (int i = 0; i < k; ++i) byte((uint8_t)(v >> (8 * i))); }
+};
+
+__global__ void k_iota(uint32_t* __restrict__ v, uint64_t n) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i < n) v[i] = (uint32_t)i;
+}
+
+__global__ void k_count(const uint32_t* __restrict__ node, uint64_t n, uint32_t* __restrict__ cnt) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i < n) atomicAdd(&cnt[node[i]], 1u);
+}
+
+__global__ void k_count_visited(const uint32_t* __restrict__ seg, uint64_t n_slots,
+                                unsigned long long* __restrict__ out) {
+    const uint64_t j = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    const int v = (j < n_slots && seg[j + 1] > seg[j]) ? 1 : 0;
+    const int w = __syncthreads_count(v);
+    if (threadIdx.x == 0 && w) atomicAdd(out, (unsigned long long)w);
+}
+
+// map_vertex (grid_builder.hpp:286-305): nearest node per axis, ties to the
+// lower index, outside points clamp; per-axis plane index.
+__global__ void k_map_axes(const double* __restrict__ coords, uint64_t n, int D,
+                           const double* __restrict__ axes, const uint64_t* __restrict__ off,
+                           const uint64_t* __restrict__ sizes, uint32_t* __restrict__ idx) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i >= n) return;
+    for (int d = 0; d < D; ++d) {
+        const double* a = axes + off[d];
+        const uint64_t m = sizes[d];
+        const double x = coords[i * D + d];
+        uint64_t lo = 0, hi = m;  // std::lower_bound
+        while (lo < hi) {
+            const uint64_t mid = lo + (hi - lo) / 2;
+            if (a[mid] < x) lo = mid + 1; else hi = mid;
+        }
+        uint64_t k;
+        if (lo == 0) k = 0;
+        else if (lo == m) k = m - 1;
+        else k = (__dsub_rn(x, a[lo - 1]) <= __dsub_rn(a[lo], x)) ? lo - 1 : lo;
+        idx[(uint64_t)d * n + i] = (uint32_t)k;
+    }
+}
+
+__global__ void k_plane_flags(const uint32_t* __restrict__ idx, uint64_t n, int D,
+                              const uint64_t* __restrict__ foff, uint8_t* __restrict__ flags) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i >= n) return;
+    for (int d = 0; d < D; ++d) flags[foff[d] + idx[(uint64_t)d * n + i]] = 1;
+}
+
+// remap_after_coarsen (grid_builder.hpp:313-354)
+__global__ void k_remap(const uint32_t* __restrict__ idx, uint64_t n, int D,
+                        const int64_t* __restrict__ o2n, const uint64_t* __restrict__ foff,
+                        const uint64_t* __restrict__ new_size, uint64_t* __restrict__ lin) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i >= n) return;
+    uint64_t l = 0;
+    for (int d = 0; d < D; ++d) l = l * new_size[d] + (uint64_t)o2n[foff[d] + idx[(uint64_t)d * n + i]];
+    lin[i] = l;
+}
+
+// seed mode: position of each assignment in the sorted visited list.
+__global__ void k_rank(const uint64_t* __restrict__ lin, uint64_t n, const uint64_t* __restrict__ vis,
+                       uint64_t nv, uint32_t* __restrict__ out) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t x = lin[i];
+    uint64_t lo = 0, hi = nv;
+    while (lo < hi) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (vis[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    out[i] = (uint32_t)lo;
+}
+
+__global__ void k_u64_to_u32(const uint64_t* __restrict__ a, uint64_t n, uint32_t* __restrict__ b) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i < n) b[i] = (uint32_t)a[i];
+}
+
+}  // namespace
+
+uint64_t mapping_digest_host(int mode, uint64_t n, const uint64_t* assign, uint64_t nv, const uint64_t* vis) {
+    Fnv f;
+    f.byte('U'); f.byte('M'); f.byte('C'); f.byte('P');
+    f.le(1, 2);
+    f.byte((uint8_t)mode);
+    f.le(n, 8);
+    for (uint64_t i = 0; i < n; ++i) f.le(assign[i], 8);
+    if (mode == 1) {
+        f.le(nv, 8);
+        for (uint64_t i = 0; i < nv; ++i) f.le(vis[i], 8);
+    }
+    return f.h;
+}
+
+uint64_t mapping_digest_host32(int mode, uint64_t n, const uint32_t* assign, uint64_t nv, const uint64_t* vis) {
+    Fnv f;
+    f.byte('U'); f.byte('M'); f.byte('C'); f.byte('P');
+    f.le(1, 2);
+    f.byte((uint8_t)mode);
+    f.le(n, 8);
+    for (uint64_t i = 0; i < n; ++i) f.le(assign[i], 8);
+    if (mode == 1) {
+        f.le(nv, 8);
+        for (uint64_t i = 0; i < nv; ++i) f.le(vis[i], 8);
+    }
+    return f.h;
+}
+
+void plan_build_segments(umcg_plan* p, cudaStream_t st) {
+    const uint64_t n = p->n, ns = p->n_slots;
+    uint32_t* node = p->d_node.as<uint32_t>(n ? n : 1);
+    uint32_t* perm = p->d_perm.as<uint32_t>(n ? n : 1);
+    uint32_t* seg = p->d_seg.as<uint32_t>(ns + 1);
+    DevBuf tmp_keys, tmp_vals, cnt, scratch;
+    uint32_t* keys_out = tmp_keys.as<uint32_t>(n ? n : 1);
+    uint32_t* iota = tmp_vals.as<uint32_t>(n ? n : 1);
+    uint32_t* c = cnt.as<uint32_t>(ns + 1);
+    UMCG_CUDA(cudaMemsetAsync(c, 0, (ns + 1) * 4, st));
+    if (n) {
+        k_iota<<<blocks(n), THREADS, 0, st>>>(iota, n);
+        UMCG_LAUNCHED();
+        k_count<<<blocks(n), THREADS, 0, st>>>(node, n, c);
+        UMCG_LAUNCHED();
+        int end_bit = 1;
+        while (end_bit < 32 && (1ull << end_bit) < ns) ++end_bit;
+        size_t tb = 0;
+        UMCG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, node, keys_out, iota, perm, (int)n, 0, end_bit, st));
+        void* t = scratch.reserve(tb);
+        UMCG_CUDA(cub::DeviceRadixSort::SortPairs(t, tb, node, keys_out, iota, perm, (int)n, 0, end_bit, st));
+    }
+    size_t tb = 0;
+    UMCG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, c, seg, (int)(ns + 1), st));
+    void* t = scratch.reserve(std::max<size_t>(tb, scratch.capacity()));
+    UMCG_CUDA(cub::DeviceScan::ExclusiveSum(t, tb, c, seg, (int)(ns + 1), st));
+    // visited count (dense info)
+    DevBuf vc;
+    auto* v = vc.as<unsigned long long>(1);
+    UMCG_CUDA(cudaMemsetAsync(v, 0, 8, st));
+    k_count_visited<<<blocks(ns), THREADS, 0, st>>>(seg, ns, v);
+    UMCG_LAUNCHED();
+    unsigned long long hv = 0;
+    UMCG_CUDA(cudaMemcpyAsync(&hv, v, 8, cudaMemcpyDeviceToHost, st));
+    UMCG_CUDA(cudaStreamSynchronize(st));
+    if (p->mode == 0) {
+        p->n_visited = hv;
+        p->visited_fraction = p->node_count ? (double)hv / (double)p->node_count : 0.0;
+    }
+}
+
+static void upload_grid(umcg_plan* p, const umcg_grid_desc* g) {
+    if (!g || !g->axis_sizes || !g->axes) fail(UMCG_INVALID_ARGUMENT, "grid descriptor is NULL");
+    if (g->dim != 2 && g->dim != 3) fail(UMCG_MALFORMED_FILE, "grid dimension must be 2 or 3");
+    p->dim = g->dim;
+    p->axes.clear();
+    p->axis_off.assign(g->dim, 0);
+    p->node_count = 1;
+    for (int d = 0; d < g->dim; ++d) {
+        const uint64_t m = g->axis_sizes[d];
+        if (m == 0) fail(UMCG_MALFORMED_FILE, "empty grid axis");
+        p->axis_off[d] = p->axes.size();
+        p->shape[d] = m;
+        p->node_count *= m;
+        // validate_grid (grid.hpp:34-47)
+        const double* a = g->axes + p->axis_off[d];
+        for (uint64_t i = 0; i < m; ++i) {
+            if (!std::isfinite(a[i])) fail(UMCG_NON_FINITE_VALUE, "non-finite axis coordinate");
+            if (i > 0 && !(a[i] > a[i - 1])) fail(UMCG_MALFORMED_FILE, "grid axis not strictly increasing");
+        }
+        p->axes.insert(p->axes.end(), a, a + m);
+    }
+    for (int d = g->dim; d < 3; ++d) p->shape[d] = 1;
+    double* da = p->d_axes.as<double>(p->axes.size());
+    UMCG_CUDA(cudaMemcpy(da, p->axes.data(), p->axes.size() * 8, cudaMemcpyHostToDevice));
+    uint64_t* doff = p->d_axis_off.as<uint64_t>(3);
+    UMCG_CUDA(cudaMemcpy(doff, p->axis_off.data(), p->dim * 8, cudaMemcpyHostToDevice));
+}
+
+umcg_plan* plan_create_host(const umcg_grid_desc* g, const umcg_mapping_desc* m, int mesh_dim,
+                            const double* coords) {
+    if (!m) fail(UMCG_INVALID_ARGUMENT, "mapping descriptor is NULL");
+    auto* p = new umcg_plan;
+    try {
+        UMCG_CUDA(cudaGetDevice(&p->device));
+        upload_grid(p, g);
+        p->mode = m->mode ? 1 : 0;
+        p->n = m->n_vertices;
+        if (p->n >= (1ull << 32)) fail(UMCG_INVALID_ARGUMENT, "more than 2^32-1 vertices per plan");
+        if (p->mode == 1) {
+            p->n_slots = m->n_visited;
+            p->n_visited = m->n_visited;
+            // validate_mapping (grid.hpp:94-110)
+            for (uint64_t i = 0; i < m->n_visited; ++i) {
+                if (m->visited_nodes[i] >= p->node_count) fail(UMCG_INDEX_OUT_OF_RANGE, "visited node out of grid range");
+                if (i > 0 && !(m->visited_nodes[i] > m->visited_nodes[i - 1]))
+                    fail(UMCG_MALFORMED_FILE, "visited node list not strictly increasing");
+            }
+            p->visited_fraction = p->node_count ? (double)m->n_visited / (double)p->node_count : 0.0;
+            uint64_t* dv = p->d_visited.as<uint64_t>(m->n_visited ? m->n_visited : 1);
+            if (m->n_visited)
+                UMCG_CUDA(cudaMemcpy(dv, m->visited_nodes, m->n_visited * 8, cudaMemcpyHostToDevice));
+        } else {
+            p->n_slots = p->node_count;
+        }
+        if (p->n_slots >= (1ull << 32)) fail(UMCG_INVALID_ARGUMENT, "grid component longer than 2^32-1");
+        std::vector<uint32_t> a32(p->n);
+        for (uint64_t i = 0; i < p->n; ++i) {
+            const uint64_t a = m->assignments[i];
+            if (a >= p->n_slots)
+                fail(UMCG_INDEX_OUT_OF_RANGE, p->mode ? "seed assignment out of visited list range"
+                                                     : "dense assignment out of grid range");
+            a32[i] = (uint32_t)a;
+        }
+        uint32_t* dn = p->d_node.as<uint32_t>(p->n ? p->n : 1);
+        if (p->n) UMCG_CUDA(cudaMemcpy(dn, a32.data(), p->n * 4, cudaMemcpyHostToDevice));
+        if (coords && p->n) {
+            if (mesh_dim != p->dim) fail(UMCG_MALFORMED_FILE, "mesh dimension does not match grid");
+            double* dc = p->d_coords.as<double>(p->n * p->dim);
+            UMCG_CUDA(cudaMemcpy(dc, coords, p->n * p->dim * 8, cudaMemcpyHostToDevice));
+            p->has_coords = true;
+        }
+        plan_build_segments(p, 0);
+        p->digest = mapping_digest_host(p->mode, p->n, m->assignments, m->n_visited, m->visited_nodes);
+    } catch (...) {
+        delete p;
+        throw;
+    }
+    return p;
+}
+
+// GPU grid_coarsen (grid_builder.hpp:365-421).
+umcg_plan* plan_build_gpu(const umcg_grid_desc* g0, uint64_t n, const double* d_coords, double thr,
+                          int keep_coords) {
+    if (!g0 || !d_coords) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
+    if (!(thr > 0.0) || thr > 1.0) fail(UMCG_ERROR, "seed mode threshold must be in (0, 1]");
+    if (n >= (1ull << 32)) fail(UMCG_INVALID_ARGUMENT, "more than 2^32-1 vertices per plan");
+    const int D = g0->dim;
+    if (D != 2 && D != 3) fail(UMCG_MALFORMED_FILE, "grid dimension must be 2 or 3");
+    cudaStream_t st = 0;
+    std::vector<uint64_t> sizes(D), off(D);
+    uint64_t tot = 0;
+    for (int d = 0; d < D; ++d) { sizes[d] = g0->axis_sizes[d]; off[d] = tot; tot += sizes[d]; }
+    DevBuf axes, doff, dsz, idx, flags, o2n, nsz, lin, lin_sorted, uniq, nuniq, scratch;
+    double* da = axes.as<double>(tot);
+    UMCG_CUDA(cudaMemcpy(da, g0->axes, tot * 8, cudaMemcpyHostToDevice));
+    uint64_t* dof = doff.as<uint64_t>(D);
+    UMCG_CUDA(cudaMemcpy(dof, off.data(), D * 8, cudaMemcpyHostToDevice));
+    uint64_t* dsize = dsz.as<uint64_t>(D);
+    UMCG_CUDA(cudaMemcpy(dsize, sizes.data(), D * 8, cudaMemcpyHostToDevice));
+    uint32_t* didx = idx.as<uint32_t>(D * (n ? n : 1));
+    uint8_t* dfl = flags.as<uint8_t>(tot);
+    UMCG_CUDA(cudaMemset(dfl, 0, tot));
+    if (n) {
+        k_map_axes<<<blocks(n), THREADS, 0, st>>>(d_coords, n, D, da, dof, dsize, didx);
+        UMCG_LAUNCHED();
+        k_plane_flags<<<blocks(n), THREADS, 0, st>>>(didx, n, D, dof, dfl);
+        UMCG_LAUNCHED();
+    }
+    std::vector<uint8_t> hfl(tot);
+    UMCG_CUDA(cudaMemcpy(hfl.data(), dfl, tot, cudaMemcpyDeviceToHost));
+    // coarse axes + old->new plane maps
+    std::vector<int64_t> ho2n(tot, -1);
+    std::vector<uint64_t> nsize(D, 0);
+    std::vector<double> caxes;
+    std::vector<uint64_t> csizes(D);
+    for (int d = 0; d < D; ++d) {
+        int64_t next = 0;
+        for (uint64_t k = 0; k < sizes[d]; ++k)
+            if (hfl[off[d] + k]) {
+                ho2n[off[d] + k] = next++;
+                caxes.push_back(g0->axes[off[d] + k]);
+            }
+        nsize[d] = (uint64_t)next;
+        csizes[d] = (uint64_t)next;
+    }
+    int64_t* do2n = o2n.as<int64_t>(tot);
+    UMCG_CUDA(cudaMemcpy(do2n, ho2n.data(), tot * 8, cudaMemcpyHostToDevice));
+    uint64_t* dnsz = nsz.as<uint64_t>(D);
+    UMCG_CUDA(cudaMemcpy(dnsz, nsize.data(), D * 8, cudaMemcpyHostToDevice));
+    uint64_t* dlin = lin.as<uint64_t>(n ? n : 1);
+    if (n) {
+        k_remap<<<blocks(n), THREADS, 0, st>>>(didx, n, D, do2n, dof, dnsz, dlin);
+        UMCG_LAUNCHED();
+    }
+    // visited = sort + unique of assignments
+    uint64_t* dsorted = lin_sorted.as<uint64_t>(n ? n : 1);
+    uint64_t* duniq = uniq.as<uint64_t>(n ? n : 1);
+    auto* dnu = nuniq.as<unsigned long long>(1);
+    uint64_t nv = 0;
+    if (n) {
+        size_t tb = 0;
+        UMCG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, dlin, dsorted, (int)n, 0, 64, st));
+        void* t = scratch.reserve(tb);
+        UMCG_CUDA(cub::DeviceRadixSort::SortKeys(t, tb, dlin, dsorted, (int)n, 0, 64, st));
+        size_t tb2 = 0;
+        UMCG_CUDA(cub::DeviceSelect::Unique(nullptr, tb2, dsorted, duniq, dnu, (int)n, st));
+        t = scratch.reserve(std::max(tb, tb2));
+        UMCG_CUDA(cub::DeviceSelect::Unique(t, tb2, dsorted, duniq, dnu, (int)n, st));
+        unsigned long long h = 0;
+        UMCG_CUDA(cudaMemcpy(&h, dnu, 8, cudaMemcpyDeviceToHost));
+        nv = h;
+    }
+    uint64_t survivors = 1;
+    for (int d = 0; d < D; ++d) survivors *= csizes[d];
+    const double frac = (double)nv / (double)survivors;
+
+    auto* p = new umcg_plan;
+    try {
+        UMCG_CUDA(cudaGetDevice(&p->device));
+        std::vector<uint64_t> csz(csizes);
+        umcg_grid_desc cg{D, csz.data(), caxes.data()};
+        upload_grid(p, &cg);
+        p->n = n;
+        p->n_visited = nv;
+        p->visited_fraction = frac;
+        p->mode = frac < thr ? 1 : 0;
+        uint32_t* dn = p->d_node.as<uint32_t>(n ? n : 1);
+        std::vector<uint64_t> hvis;
+        if (p->mode == 1) {
+            p->n_slots = nv;
+            uint64_t* dv = p->d_visited.as<uint64_t>(nv ? nv : 1);
+            if (nv) UMCG_CUDA(cudaMemcpy(dv, duniq, nv * 8, cudaMemcpyDeviceToDevice));
+            if (n) {
+                k_rank<<<blocks(n), THREADS, 0, st>>>(dlin, n, dv, nv, dn);
+                UMCG_LAUNCHED();
+            }
+            hvis.resize(nv);
+            if (nv) UMCG_CUDA(cudaMemcpy(hvis.data(), dv, nv * 8, cudaMemcpyDeviceToHost));
+        } else {
+            p->n_slots = p->node_count;
+            if (p->n_slots >= (1ull << 32)) fail(UMCG_INVALID_ARGUMENT, "grid component longer than 2^32-1");
+            if (n) {
+                k_u64_to_u32<<<blocks(n), THREADS, 0, st>>>(dlin, n, dn);
+                UMCG_LAUNCHED();
+            }
+        }
+        if (keep_coords && n) {
+            double* dc = p->d_coords.as<double>(n * D);
+            UMCG_CUDA(cudaMemcpy(dc, d_coords, n * D * 8, cudaMemcpyDeviceToDevice));
+            p->has_coords = true;
+        }
+        plan_build_segments(p, st);
+        std::vector<uint32_t> h32(n);
+        if (n) UMCG_CUDA(cudaMemcpy(h32.data(), dn, n * 4, cudaMemcpyDeviceToHost));
+        p->digest = mapping_digest_host32(p->mode, n, h32.data(), nv, hvis.data());
+        if (p->mode == 0) {
+            p->n_visited = nv;
+            p->visited_fraction = frac;
+        }
+    } catch (...) {
+        delete p;
+        throw;
+    }
+    return p;
+}
+
+}  // namespace umcg

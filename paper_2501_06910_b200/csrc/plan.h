@@ -1,0 +1,64 @@
+// The immutable per-mesh device plan + per-call workspace.
+#pragma once
+
+#include <mutex>
+
+#include "kernels.h"
+
+struct umcg_plan {
+    int device = 0;
+    int dim = 2;
+    int mode = 0;                 // 0 dense, 1 seed
+    uint64_t n = 0;               // vertices
+    uint64_t n_slots = 0;         // grid-component length
+    uint64_t node_count = 0;      // coarse grid nodes
+    uint64_t n_visited = 0;
+    uint64_t shape[3] = {1, 1, 1};
+    double visited_fraction = 0.0;
+    uint64_t digest = 0;
+    std::vector<double> axes;        // concatenated coarse axes (host copy)
+    std::vector<uint64_t> axis_off;  // [dim]
+    // device-resident static inputs
+    umcg::DevBuf d_node;     // u32 [n]   slot of each vertex (dense node / seed position)
+    umcg::DevBuf d_perm;     // u32 [n]   vertices stably sorted by slot
+    umcg::DevBuf d_seg;      // u32 [n_slots+1] segment offsets into perm
+    umcg::DevBuf d_visited;  // u64 [n_visited] visited linear node ids (seed mode)
+    umcg::DevBuf d_axes;     // f64 concatenated axes
+    umcg::DevBuf d_axis_off; // u64 [dim]
+    umcg::DevBuf d_coords;   // f64 [n*dim] (multilinear g), optional
+    bool has_coords = false;
+    // workspace (serialized by mu)
+    std::mutex mu;
+    umcg::DevBuf ctl, x1, codes1, codes2, kbuf, enc1, enc2, hdr, scratch_a, scratch_b, scratch_c,
+        scratch_d, dx1, dcodes;
+    umcg::StreamDecScratch dec;
+    umcg::PinnedBuf hctl, hstage;
+};
+
+namespace umcg {
+
+// Host-side FNV-1a-64 of serialize_mapping bytes (serialize.hpp:255-267, 300-303).
+uint64_t mapping_digest_host(int mode, uint64_t n, const uint64_t* assign, uint64_t n_visited,
+                             const uint64_t* visited);
+// Same digest with u32 assignments (widened to u64 LE bytes as the reference writes them).
+uint64_t mapping_digest_host32(int mode, uint64_t n, const uint32_t* assign, uint64_t n_visited,
+                               const uint64_t* visited);
+
+// Build perm / seg_off from d_node on the plan (stable radix sort by slot).
+void plan_build_segments(umcg_plan* p, cudaStream_t st);
+
+// Component payload decode (codec.hpp:364-441) of a payload in device memory
+// into d_out [n]; header already parsed. Throws the reference's error kinds.
+struct CompHeader {
+    int codec, pred, backend, D;
+    double tau;
+    uint64_t n, dims[8];
+    uint64_t n_esc;
+    uint64_t esc_off;     // byte offset of the escape records in the payload
+    uint64_t stream_off;  // byte offset of the RLE stream in the payload
+    uint64_t stream_len;
+};
+void decode_component(umcg_plan* ws, const CompHeader& h, const uint8_t* d_payload, double* d_out,
+                      cudaStream_t st);
+
+}  // namespace umcg

@@ -1,0 +1,283 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracles.
+
+Bar (BASELINE.json north_star): archives / payloads byte-identical to the
+reference, except codes whose value sits in the quantizer's rounding window
+(|frac((v - p_ref)/bin) - 0.5| < WINDOW, p_ref the reference's serial
+prediction); decoded values within 1e-12 x max(range, max|x|) of the
+reference's decode; the error bound on 100% of vertices.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2501_06910_b200 as umcg
+from helpers import (GOLDEN, load_cases, load_seed7, lorenzo_pred, parse_archive, parse_payload,
+                     window_distance)
+
+pytestmark = pytest.mark.gpu
+
+WINDOW = 1e-6          # rounding-window half width, in bins
+REL_TOL = 1e-12        # decode tolerance relative to max(range, max|x|)
+
+
+def plan_for(s, coords=True):
+    return umcg.Plan.from_mapping(s.dim, s.axes, s.mode, s.assignments, s.visited,
+                                  coords=s.coords if coords else None)
+
+
+def budget_of(p):
+    return umcg.Budget(tau=p.get("tau", 1e-3), split_rho=p.get("rho", 0.5),
+                       bound_kind=p.get("bound_kind", 1), g_kind=p.get("g_kind", 0),
+                       fill=p.get("fill", 0))
+
+
+def dev(x):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(x, np.float64)).cuda()
+
+
+def check_component(gp, rp, values, pred_ref, oracle, label):
+    """Byte-exact payload, or code-level diff confined to the rounding window."""
+    if gp == rp:
+        return 0
+    g = parse_payload(gp, oracle.rle_decompress)
+    r = parse_payload(rp, oracle.rle_decompress)
+    for k in ("codec", "pred", "backend", "tau", "n", "dims"):
+        assert g[k] == r[k], (label, k)
+    assert len(g["esc"]) == len(r["esc"]) and np.array_equal(g["esc"], r["esc"]), label
+    assert len(g["codes"]) == len(r["codes"]) == g["n"], label
+    bad = np.flatnonzero(g["codes"] != r["codes"])
+    assert bad.size > 0, f"{label}: payloads differ but codes agree (stream encoder bug)"
+    wd = window_distance(values[bad], pred_ref[bad], r["tau"])
+    assert np.all(wd < WINDOW), (label, bad[:10], wd[:10])
+    return bad.size
+
+
+def check_archive(gpu_ar, ref_ar, s, x, p, oracle, label):
+    if gpu_ar == ref_ar:
+        return
+    ga, ra = parse_archive(gpu_ar), parse_archive(ref_ar)
+    for k in ("flags", "name", "digest", "tau", "rho"):
+        assert ga[k] == ra[k], (label, k)
+    # component 1: grid, exact cluster means vs reference Lorenzo prediction
+    x1 = oracle.interpolate_to_grid(s, x, fill=p.get("fill", 0))
+    rec1 = oracle.decode(ra["p1"])
+    if s.mode == 1:
+        pred1 = np.concatenate([[0.0], rec1[:-1]])
+    else:
+        pred1 = lorenzo_pred(rec1, list(s.shape))
+    check_component(ga["p1"], ra["p1"], x1, pred1, oracle, label + "/grid")
+    # component 2: residuals vs the previous reconstructed residual
+    x2 = oracle.residuals(s, x, fill=p.get("fill", 0), g_kind=p.get("g_kind", 0))
+    rec2 = oracle.decode(ra["p2"])
+    pred2 = np.concatenate([[0.0], rec2[:-1]])
+    check_component(ga["p2"], ra["p2"], x2, pred2, oracle, label + "/resid")
+
+
+def check_decode(out, ref_out, x, tau_abs, label):
+    scale = max(float(np.ptp(x)) if x.size else 0.0, float(np.abs(x).max()) if x.size else 0.0, 1e-300)
+    if tau_abs == 0.0:
+        assert np.array_equal(out.view(np.uint64), ref_out.view(np.uint64)), label
+        return
+    assert np.max(np.abs(out - ref_out)) <= REL_TOL * scale, (label, np.max(np.abs(out - ref_out)))
+    assert np.max(np.abs(out - x)) <= tau_abs, (label, np.max(np.abs(out - x)), tau_abs)
+
+
+# ---------------------------------------------------------------------------
+
+
+def test_golden_archive_bit_exact(cuda):
+    s, x, ar = load_seed7()
+    plan = plan_for(s)
+    got = plan.compress(dev(x), umcg.Budget(tau=1e-3, split_rho=0.5, bound_kind=1), name="white-noise")
+    assert got == ar
+    out = plan.decompress(ar).cpu().numpy()
+    assert np.max(np.abs(out - x)) <= 1e-3 * np.ptp(x)
+
+
+def test_plan_digest_matches_reference(cuda, ref):
+    s, x, ar = load_seed7()
+    assert plan_for(s).digest == ref.mapping_digest(s) == parse_archive(ar)["digest"]
+
+
+@pytest.mark.parametrize("case_idx", range(7))
+def test_fixture_cases(cuda, case_idx, ref, oracle):
+    params, cases = load_cases()
+    k, s, x, archives = cases[case_idx]
+    plan = plan_for(s)
+    dx = dev(x)
+    for p, ref_ar in zip(params, archives):
+        label = f"case{k} {p}"
+        b = budget_of(p)
+        if ref_ar.startswith(b"ERR:"):
+            with pytest.raises(umcg.UmcgError) as ei:
+                plan.compress(dx, b, name=f"case{k}")
+            assert ei.value.kind == "seed_mode_unsupported"
+            continue
+        got = plan.compress(dx, b, name=f"case{k}")
+        check_archive(got, ref_ar, s, x, p, oracle, label)
+        tau_abs = p.get("tau", 1e-3) * (np.ptp(x) if p.get("bound_kind", 1) == 1 else 1.0)
+        # GPU decode of the reference archive and of our own archive
+        ref_dec = ref.decompress(s, ref_ar)
+        out_ref_ar = plan.decompress(ref_ar).cpu().numpy()
+        check_decode(out_ref_ar, ref_dec, x, tau_abs, label + " gpu(ref archive)")
+        out_own = plan.decompress(got).cpu().numpy()
+        check_decode(out_own, ref.decompress(s, got), x, tau_abs, label + " gpu(own archive)")
+
+
+def test_codec_known_answers(cuda, ref):
+    z = np.load(os.path.join(GOLDEN, "codec.npz"))
+    assert umcg.encode(dev(z["worked_in"]), predictor=0, tau=0.05) == z["worked_payload"].tobytes()
+    assert umcg.decode(z["worked_payload"].tobytes()).cpu().numpy()[0] == 0.4
+    # escapes: exact serial path
+    assert umcg.encode(dev(z["esc_in"]), predictor=1, tau=1e-12) == z["esc_payload"].tobytes()
+    out = umcg.decode(z["esc_payload"].tobytes()).cpu().numpy()
+    assert np.all(np.abs(out - z["esc_in"]) <= 1e-12)
+    for pred in (0, 1):
+        pl = z[f"lossless_payload{pred}"].tobytes()
+        assert umcg.encode(dev(z["lossless_in"]), predictor=pred, tau=0.0) == pl
+        back = umcg.decode(pl).cpu().numpy()
+        assert np.array_equal(back.view(np.uint64), z["lossless_in"].view(np.uint64))
+    for t in (0.0, 1e-6, 0.5):
+        pl = z[f"zeros_payload_{t}"].tobytes()
+        assert umcg.encode(dev(np.zeros(10000)), predictor=1, tau=t) == pl
+        assert np.array_equal(umcg.decode(pl).cpu().numpy(), np.zeros(10000))
+    nd = z["nd_in"]
+    assert umcg.encode(dev(nd), predictor=2, dims=[17, 9, 5], tau=0.0) == z["nd0_payload"].tobytes()
+    back = umcg.decode(z["nd0_payload"].tobytes()).cpu().numpy()
+    assert np.array_equal(back.view(np.uint64), nd.view(np.uint64))
+    got = umcg.encode(dev(nd), predictor=2, dims=[17, 9, 5], tau=1e-3)
+    assert got == z["nd_payload"].tobytes()
+
+
+def test_codec_random_walk_and_smooth(cuda, ref, oracle):
+    z = np.load(os.path.join(GOLDEN, "codec.npz"))
+    w = z["walk_in"]
+    got = umcg.encode(dev(w), predictor=1, tau=1e-3)
+    rp = z["walk_payload"].tobytes()
+    rec = oracle.decode(rp)
+    check_component(got, rp, w, np.concatenate([[0.0], rec[:-1]]), oracle, "walk")
+    out = umcg.decode(got).cpu().numpy()
+    assert np.max(np.abs(out - w)) <= 1e-3
+    for t in (1e-6, 1e-5, 1e-4, 1e-3, 1e-2):
+        pl = z[f"smooth_payload_{t}"].tobytes()
+        sm = z["smooth_in"]
+        got = umcg.encode(dev(sm), predictor=1, tau=t)
+        rec = oracle.decode(pl)
+        check_component(got, pl, sm, np.concatenate([[0.0], rec[:-1]]), oracle, f"smooth{t}")
+        back = umcg.decode(pl).cpu().numpy()
+        assert np.max(np.abs(back - rec)) <= REL_TOL * 10.0
+        assert np.max(np.abs(back - sm)) <= t
+
+
+def test_codec_bound_random_shapes(cuda, ref, oracle):
+    """test_codec.cpp:74-104 'hard error bound across shapes and tolerances'."""
+    rng = np.random.default_rng(100)
+    for trial in range(40):
+        nd = 1 + int(rng.integers(0, 3))
+        dims = [1 + int(rng.integers(0, 400 if d == 0 else 20)) for d in range(nd)]
+        n = int(np.prod(dims))
+        v = rng.uniform(-50, 50, n)
+        if trial % 3 == 0:
+            v = np.cumsum(v * 0.01)
+        tau = 10.0 ** (-1 - int(rng.integers(0, 6))) * np.ptp(v) if n > 1 else 1e-3
+        if tau == 0:
+            tau = 1e-3
+        pred = 1 if nd == 1 else 2
+        got = umcg.encode(dev(v), predictor=pred, dims=dims, tau=tau)
+        rp = ref.encode(v, predictor=pred, dims=dims, tau=tau)
+        rec = oracle.decode(rp)
+        p_ref = np.concatenate([[0.0], rec[:-1]]) if nd == 1 else lorenzo_pred(rec, dims)
+        check_component(got, rp, v, p_ref, oracle, f"shape{dims}")
+        out = umcg.decode(got).cpu().numpy()
+        assert np.all(np.abs(out - v) <= tau)
+        out_r = umcg.decode(rp).cpu().numpy()
+        assert np.all(np.abs(out_r - v) <= tau)
+
+
+def test_gpu_grid_coarsen_matches_reference(cuda, ref):
+    import torch
+    rng = np.random.default_rng(5)
+    for dim, m, gsz in [(2, 90, 30), (3, 20, 9), (2, 60, 200)]:
+        h = 1.0 / (m - 1)
+        idx = np.stack(np.meshgrid(*([np.arange(m)] * dim), indexing="ij"), -1).reshape(-1, dim)
+        coords = idx * h + rng.uniform(-0.3, 0.3, idx.shape) * h * ((idx > 0) & (idx < m - 1))
+        coords = coords[rng.permutation(len(coords))]
+        if gsz == 200:  # sparse occupancy -> seed mode
+            coords = coords[: len(coords) // 7]
+        axes = [np.linspace(0, 1, gsz) for _ in range(dim)]
+        s, frac = ref.grid_coarsen(dim, coords, axes)
+        plan = umcg.Plan.build(axes, torch.from_numpy(coords).cuda())
+        mode, gaxes, assign, visited = plan.export()
+        assert mode == s.mode
+        for a, b in zip(gaxes, s.axes):
+            assert np.array_equal(a, b)
+        assert np.array_equal(assign, s.assignments)
+        if mode == 1:
+            assert np.array_equal(visited, s.visited)
+        assert plan.digest == ref.mapping_digest(s)
+        assert plan.info.visited_fraction == frac
+
+
+def test_errors_follow_reference_taxonomy(cuda, ref):
+    params, cases = load_cases()
+    k, s, x, archives = cases[0]
+    plan = plan_for(s)
+    dx = dev(x)
+    ar = archives[1]
+    # wrong mapping -> mapping_mismatch (pipeline.hpp:188-189)
+    k2, s2, x2, _ = cases[1]
+    with pytest.raises(umcg.UmcgError) as e:
+        plan_for(s2).decompress(ar)
+    assert e.value.kind == "mapping_mismatch"
+    # truncation -> malformed_file (deserialize_archive)
+    for cut in (len(ar) - 1, len(ar) // 2, 10, 3):
+        with pytest.raises(umcg.UmcgError) as e:
+            plan.decompress(ar[:cut])
+        assert e.value.kind == "malformed_file"
+    # non-finite input
+    bad = x.copy()
+    bad[5] = np.nan
+    with pytest.raises(umcg.UmcgError) as e:
+        plan.compress(dev(bad))
+    assert e.value.kind == "non_finite_value"
+    # budget
+    for b in (umcg.Budget(split_rho=1.0), umcg.Budget(split_rho=0.0), umcg.Budget(tau=-1.0)):
+        with pytest.raises(umcg.UmcgError) as e:
+            plan.compress(dx, b)
+        assert e.value.kind == "budget_inadmissible"
+    # non-finite beats budget (validate_field runs first)
+    with pytest.raises(umcg.UmcgError) as e:
+        plan.compress(dev(bad), umcg.Budget(split_rho=2.0))
+    assert e.value.kind == "non_finite_value"
+    with pytest.raises(umcg.UmcgError) as e:
+        plan.compress(dx, umcg.Budget(codec_id=17))
+    assert e.value.kind == "unknown_codec"
+    # corrupt payload bytes inside the residual stream -> corrupt_payload
+    a = parse_archive(ar)
+    p2_off = ar.index(a["p2"])
+    broken = bytearray(ar)
+    broken[p2_off + 37 + 8] = 0x07  # first RLE token tag -> unknown token
+    with pytest.raises(umcg.UmcgError) as e:
+        plan.decompress(bytes(broken))
+    assert e.value.kind == "corrupt_payload"
+    # truncated component payloads -> corrupt_payload (test_codec.cpp:147-157)
+    z = np.load(os.path.join(GOLDEN, "codec.npz"))
+    pl = z["walk_payload"].tobytes()
+    for cut in (len(pl) - 1, len(pl) // 2, 10):
+        with pytest.raises(umcg.UmcgError) as e:
+            umcg.decode(pl[:cut], n_capacity=len(z["walk_in"]))
+        assert e.value.kind == "corrupt_payload"
+
+
+def test_determinism_and_host_path(cuda):
+    params, cases = load_cases()
+    k, s, x, archives = cases[5]
+    plan = plan_for(s)
+    a1 = plan.compress(dev(x), umcg.Budget(tau=1e-4))
+    a2 = plan.compress(dev(x), umcg.Budget(tau=1e-4))
+    a3 = plan.compress_host(x, umcg.Budget(tau=1e-4))
+    assert a1 == a2 == a3
+    y = plan.decompress_host(a1)
+    assert np.array_equal(y, plan.decompress(a1).cpu().numpy())
