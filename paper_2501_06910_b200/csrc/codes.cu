@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_sums(const uint64_t* __restric
     if (threadIdx.x == 0) sums[blockIdx.x] = t;
 }
 
-__global__ void k_scan_sums(int64_t* __restrict__ sums, uint64_t T) {
+__global__ void __launch_bounds__(1024) k_scan_sums(int64_t* __restrict__ sums, uint64_t T) {
     using BS = cub::BlockScan<int64_t, 1024>;
     __shared__ typename BS::TempStorage tmp;
     const uint64_t per = (T + 1023) / 1024;
@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_xor(const uint64_t* __restrict
     if (threadIdx.x == 0) sums[blockIdx.x] = t;
 }
 
-__global__ void k_scan_xor(uint64_t* __restrict__ sums, uint64_t T) {
+__global__ void __launch_bounds__(1024) k_scan_xor(uint64_t* __restrict__ sums, uint64_t T) {
     using BS = cub::BlockScan<uint64_t, 1024>;
     __shared__ typename BS::TempStorage tmp;
     struct X { __device__ uint64_t operator()(uint64_t a, uint64_t b) const { return a ^ b; } };

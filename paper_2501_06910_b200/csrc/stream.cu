@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(VD_THREADS) k_varint_count(const uint8_t* __re
 }
 
 // Exclusive scan of tile counts in one CTA; total -> ctl->count.
-__global__ void k_scan_counts(uint64_t* __restrict__ counts, uint64_t T, DevCtl* ctl) {
+__global__ void __launch_bounds__(1024) k_scan_counts(uint64_t* __restrict__ counts, uint64_t T, DevCtl* ctl) {
     using BS = cub::BlockScan<uint64_t, 1024>;
     __shared__ typename BS::TempStorage tmp;
     const uint64_t per = (T + 1023) / 1024;

@@ -258,7 +258,7 @@ def test_errors_follow_reference_taxonomy(cuda, ref):
     a = parse_archive(ar)
     p2_off = ar.index(a["p2"])
     broken = bytearray(ar)
-    broken[p2_off + 37 + 8] = 0x07  # first RLE token tag -> unknown token
+    broken[p2_off + 37] = 0x07  # first RLE token tag -> unknown token
     with pytest.raises(umcg.UmcgError) as e:
         plan.decompress(bytes(broken))
     assert e.value.kind == "corrupt_payload"
