@@ -6,6 +6,7 @@
 #include <memory>
 #include <string>
 
+#include "decode.h"
 #include "plan.h"
 
 namespace umcg {
@@ -413,35 +414,85 @@ void finish_comp_header(const uint8_t* b, uint64_t avail, uint64_t payload_len, 
 
 }  // namespace
 
-// codec.hpp:364-441 on device memory. h.n_esc/esc_off already read.
-void decode_component(umcg_plan* p, const CompHeader& h, const uint8_t* d_payload, double* d_out, cudaStream_t st) {
-    const uint64_t payload_len = h.stream_off + h.stream_len;  // set by caller as full payload length
-    (void)payload_len;
+// Common prelude of decode (codec.hpp:364-421): codec / escape validation.
+static void decode_prelude(umcg_plan* p, const CompHeader& h, const uint8_t* d_payload, uint64_t** eidx,
+                           double** evals, cudaStream_t st) {
     if (h.codec == 1 || h.codec >= 128)
         fail(UMCG_UNKNOWN_CODEC, "codec " + std::to_string(h.codec) + " is a host plugin (out of the device path)");
     if (h.codec != 0) fail(UMCG_CORRUPT_PAYLOAD, "unknown codec id in payload");
     if (h.D > 8) fail(UMCG_CORRUPT_PAYLOAD, "codec supports at most 8 dimensions");
     if (h.n_esc > h.n) fail(UMCG_CORRUPT_PAYLOAD, "escape count exceeds element count");
     auto* ctl = p->ctl.as<DevCtl>(1);
-    init_ctl(ctl, st);
-    uint64_t* eidx = nullptr;
-    double* evals = nullptr;
+    *eidx = nullptr;
+    *evals = nullptr;
     if (h.n_esc) {
+        init_ctl(ctl, st);
         if (h.stream_off < h.esc_off + 16 * h.n_esc) fail(UMCG_CORRUPT_PAYLOAD, "unexpected end of data");
-        eidx = p->scratch_a.as<uint64_t>(h.n_esc);
-        evals = p->scratch_b.as<double>(h.n_esc);
-        k_read_escapes<<<blocks(h.n_esc), THREADS, 0, st>>>(d_payload + h.esc_off, h.n_esc, h.n, eidx, evals, ctl);
+        *eidx = p->scratch_a.as<uint64_t>(h.n_esc);
+        *evals = p->scratch_b.as<double>(h.n_esc);
+        k_read_escapes<<<blocks(h.n_esc), THREADS, 0, st>>>(d_payload + h.esc_off, h.n_esc, h.n, *eidx, *evals, ctl);
         UMCG_LAUNCHED();
         const DevCtl hc = read_ctl(p, ctl, st);
         if (hc.err == DE_CORRUPT_ESCAPE) fail(UMCG_CORRUPT_PAYLOAD, "bad escape index sequence");
     }
     if (h.backend != 0)
         fail(UMCG_UNKNOWN_CODEC, "lossless backend " + std::to_string(h.backend) + " not registered");
+}
+
+// Validation after a fused decode: exact code count, no dangling varint.
+static DevCtl check_fused(umcg_plan* p, DevCtl* ctl, const uint8_t* U, uint64_t ulen, uint64_t n, cudaStream_t st) {
+    auto* h = static_cast<DevCtl*>(p->hctl.reserve(sizeof(DevCtl) + 16));
+    uint8_t* last = reinterpret_cast<uint8_t*>(h + 1);
+    *last = 0;
+    UMCG_CUDA(cudaMemcpyAsync(h, ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
+    if (ulen) UMCG_CUDA(cudaMemcpyAsync(last, U + ulen - 1, 1, cudaMemcpyDeviceToHost, st));
+    UMCG_CUDA(cudaStreamSynchronize(st));
+    if (h->err == DE_CORRUPT_VARINT) fail(UMCG_CORRUPT_PAYLOAD, "varint exceeds 64 bits");
+    const uint64_t ends = ulen ? h->count : 0;
+    if (ends < n) fail(UMCG_CORRUPT_PAYLOAD, "unexpected end of data");
+    if (ends > n || (ulen && (*last & 0x80))) fail(UMCG_CORRUPT_PAYLOAD, "trailing bytes in quantized stream");
+    return *h;
+}
+
+static double k_lim(int pred, int D) { return pred == 1 || D <= 1 ? 1073741824.0 : std::ldexp(1.0, 31 - D); }
+
+// codec.hpp:364-441 on device memory, general path: values [n] fp64.
+void decode_component(umcg_plan* p, const CompHeader& h, const uint8_t* d_payload, double* d_out, cudaStream_t st) {
+    uint64_t* eidx;
+    double* evals;
+    decode_prelude(p, h, d_payload, &eidx, &evals, st);
+    auto* ctl = p->ctl.as<DevCtl>(1);
+    const NdShape sh = make_shape(h.D, h.dims);
+    const int pred = (h.pred == 2 && h.D == 1) ? 1 : h.pred;  // 1-axis Lorenzo == lorenzo_1d
+    const double bin = 2.0 * h.tau;
+    const bool lattice = h.tau != 0.0 && !h.n_esc && std::isfinite(bin) && pred != 0;
+    if (lattice) {
+        init_ctl(ctl, st);
+        uint64_t ulen = 0;
+        const uint8_t* U = stream_unpack(d_payload + h.stream_off, h.stream_len, p->dec, ctl, st, &ulen);
+        init_ctl(ctl, st);
+        void* status = p->scratch_c.reserve(dec_status_bytes(ulen));
+        if (pred == 1) {
+            dec_fused(DEC_VALUES, U, ulen, h.n, status, ctl, nullptr, nullptr, 0.0, bin, d_out, nullptr, st);
+            const DevCtl hc = check_fused(p, ctl, U, ulen, h.n, st);
+            if ((double)hc.max_abs_k[1] < k_lim(1, 1)) return;
+        } else {
+            int64_t* P = p->kbuf.as<int64_t>(2 * (h.n ? h.n : 1));
+            int32_t* K32 = p->dx1.as<int32_t>(h.n ? h.n : 1);
+            dec_fused(DEC_P64, U, ulen, h.n, status, ctl, nullptr, nullptr, 0.0, bin, nullptr, P, st);
+            check_fused(p, ctl, U, ulen, h.n, st);
+            nd_from_prefix(P, h.n, sh, P + h.n, K32, ctl, st);
+            const DevCtl hc = read_ctl(p, ctl, st);
+            if ((double)hc.max_abs_k[0] < k_lim(2, h.D)) {
+                k32_to_f64(K32, h.n, bin, d_out, st);
+                return;
+            }
+        }
+        // far from the lattice regime: replay the reference chain exactly
+    }
     uint64_t* codes = p->dcodes.as<uint64_t>(h.n ? h.n : 1);
     init_ctl(ctl, st);
     stream_decode(d_payload + h.stream_off, h.stream_len, h.n, codes, p->dec, ctl, st);
-    const NdShape sh = make_shape(h.D, h.dims);
-    const int pred = (h.pred == 2 && h.D == 1) ? 1 : h.pred;  // 1-axis Lorenzo == lorenzo_1d
     if (h.tau == 0.0) {
         if (h.n_esc != 0) fail(UMCG_CORRUPT_PAYLOAD, "lossless payload with escapes");
         if (pred == 2) {
@@ -452,20 +503,41 @@ void decode_component(umcg_plan* p, const CompHeader& h, const uint8_t* d_payloa
         }
         return;
     }
-    const double bin = 2.0 * h.tau;
-    if (h.n_esc || !std::isfinite(bin)) {
-        serial_decode(codes, h.n, h.pred, sh, h.tau, eidx, evals, h.n_esc, d_out, st);
+    if (pred == 0 && !h.n_esc && std::isfinite(bin)) {
+        int64_t* kb = p->kbuf.as<int64_t>(1);
+        recon_lossy(codes, h.n, 0, sh, bin, kb, d_out, ctl, st);
         return;
     }
-    int64_t* kb = p->kbuf.as<int64_t>(std::max<uint64_t>(h.n, cdiv(h.n, RECON_TILE) + 1));
-    init_ctl(ctl, st);
-    recon_lossy(codes, h.n, pred, sh, bin, kb, d_out, ctl, st);
-    if (pred != 0) {
+    serial_decode(codes, h.n, h.pred, sh, h.tau, eidx, evals, h.n_esc, d_out, st);
+}
+
+// Grid component in the pipeline: prefer the int32 lattice form (K1). Returns
+// true with K1 filled, or false with x1f (fp64 values) filled.
+static bool decode_grid(umcg_plan* p, const CompHeader& h, const uint8_t* d_payload, int32_t* K1, double* x1f,
+                        cudaStream_t st) {
+    const int pred = (h.pred == 2 && h.D == 1) ? 1 : h.pred;
+    const double bin = 2.0 * h.tau;
+    const bool lattice = h.codec == 0 && h.backend == 0 && h.D <= 8 && h.tau != 0.0 && !h.n_esc &&
+                         std::isfinite(bin) && pred != 0;
+    if (lattice) {
+        uint64_t* eidx;
+        double* evals;
+        decode_prelude(p, h, d_payload, &eidx, &evals, st);
+        auto* ctl = p->ctl.as<DevCtl>(1);
+        init_ctl(ctl, st);
+        uint64_t ulen = 0;
+        const uint8_t* U = stream_unpack(d_payload + h.stream_off, h.stream_len, p->dec, ctl, st, &ulen);
+        init_ctl(ctl, st);
+        void* status = p->scratch_c.reserve(dec_status_bytes(ulen));
+        int64_t* P = p->kbuf.as<int64_t>(2 * (h.n ? h.n : 1));
+        dec_fused(DEC_P64, U, ulen, h.n, status, ctl, nullptr, nullptr, 0.0, bin, nullptr, P, st);
+        check_fused(p, ctl, U, ulen, h.n, st);
+        nd_from_prefix(P, h.n, make_shape(h.D, h.dims), P + h.n, K1, ctl, st);
         const DevCtl hc = read_ctl(p, ctl, st);
-        const double lim = pred == 1 ? 1073741824.0 : std::ldexp(1.0, 31 - h.D);
-        if (!((double)hc.max_abs_k[0] < lim))  // far from the lattice regime: replay the chain exactly
-            serial_decode(codes, h.n, h.pred, sh, h.tau, nullptr, nullptr, 0, d_out, st);
+        if ((double)hc.max_abs_k[0] < k_lim(pred, h.D)) return true;
     }
+    decode_component(p, h, d_payload, x1f, st);
+    return false;
 }
 
 namespace {
@@ -543,9 +615,32 @@ void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_
     prep(h1, hb + p1, head - p1, l1);
     prep(h2, tail + 8, tl - 8, l2);
     double* x1 = p->x1.as<double>(p->n_slots ? p->n_slots : 1);
-    decode_component(p, h1, d_ar + p1, x1, st);
-    decode_component(p, h2, d_ar + p2, d_out, st);
+    int32_t* K1 = p->codes1.as<int32_t>(p->n_slots ? p->n_slots : 1);
     const int g_kind = (flags & 2u) ? 1 : 0;
+    const bool k1_lattice = decode_grid(p, h1, d_ar + p1, K1, x1, st);
+    const double bin1 = 2.0 * h1.tau;
+    // Fast path: nearest g over the lattice grid, residual decoded and
+    // recomposed in one pass (decode.cu, DEC_RECOMPOSE).
+    const int pred2 = (h2.pred == 2 && h2.D == 1) ? 1 : h2.pred;
+    const double bin2 = 2.0 * h2.tau;
+    if (k1_lattice && g_kind == 0 && h2.codec == 0 && h2.backend == 0 && h2.D == 1 && pred2 == 1 &&
+        h2.tau != 0.0 && !h2.n_esc && std::isfinite(bin2)) {
+        uint64_t* eidx;
+        double* evals;
+        decode_prelude(p, h2, d_ar + p2, &eidx, &evals, st);
+        auto* ctl = p->ctl.as<DevCtl>(1);
+        init_ctl(ctl, st);
+        uint64_t ulen = 0;
+        const uint8_t* U = stream_unpack(d_ar + p2 + h2.stream_off, h2.stream_len, p->dec, ctl, st, &ulen);
+        init_ctl(ctl, st);
+        void* status = p->scratch_c.reserve(dec_status_bytes(ulen));
+        dec_fused(DEC_RECOMPOSE, U, ulen, p->n, status, ctl, p->d_node.as<uint32_t>(1), K1, bin1, bin2, d_out,
+                  nullptr, st);
+        const DevCtl hc = check_fused(p, ctl, U, ulen, p->n, st);
+        if ((double)hc.max_abs_k[1] < k_lim(1, 1)) return;
+    }
+    if (k1_lattice) k32_to_f64(K1, p->n_slots, bin1, x1, st);
+    decode_component(p, h2, d_ar + p2, d_out, st);
     if (g_kind == 1 && seed) fail(UMCG_SEED_MODE_UNSUPPORTED, "multilinear back-interpolation needs a dense grid component");
     if (g_kind == 1 && !p->has_coords) fail(UMCG_INVALID_ARGUMENT, "multilinear g needs a plan with vertex coordinates");
     ResidualSrc rs{};

@@ -1,0 +1,278 @@
+// Fused single-pass decode of a 1-D varint code stream on sm_100a:
+//   unpacked varint bytes -> code boundaries (MSB-clear bytes) -> element
+//   index and lattice index K = inclusive prefix of zigzag codes, both by one
+//   decoupled look-back scan over 4 KiB byte tiles -> epilogue.
+// Epilogues:
+//   P64        K as int64 (grid component, further N-D scans follow)
+//   VALUES     fl(K * bin)                       (codec.hpp:434 on the lattice)
+//   RECOMPOSE  fl(fl(K1[node_i] * bin1) + fl(K * bin2))  (pipeline.hpp:206-208,
+//              nearest g, grid component as int32 lattice indices: the decoded
+//              grid value x1'[j] is exactly fl(K1[j] * bin1), so the gather
+//              touches a 4-byte array that stays resident in L2)
+#include <cub/block/block_scan.cuh>
+
+#include "decode.h"
+#include <cub/block/block_reduce.cuh>
+
+namespace umcg {
+
+namespace {
+
+
+struct CS {
+    uint64_t cnt;
+    int64_t sum;
+};
+struct CSAdd {
+    __device__ __forceinline__ CS operator()(const CS& a, const CS& b) const {
+        return CS{a.cnt + b.cnt, a.sum + b.sum};
+    }
+};
+
+__device__ __forceinline__ uint64_t varint_back(const uint8_t* sb, int e) {
+    int s = e;
+    while (s > 0 && (sb[s - 1] & 0x80) && e - (s - 1) < 10) --s;
+    uint64_t v = 0;
+    int shift = 0;
+    for (int j = s; j <= e; ++j, shift += 7) v |= (uint64_t)(sb[j] & 0x7f) << shift;
+    return v;
+}
+
+// ---- three-phase (reduce, scan, apply) decode: every phase is fully
+// parallel, no inter-CTA waiting. Tiles of 8 KiB of varint bytes.
+constexpr int RT = 256;
+constexpr int RB = 32;
+constexpr uint64_t RTILE = (uint64_t)RT * RB;
+constexpr int RHALO = 16;
+
+// Stage tile bytes [base-16, base+RTILE) into smem with aligned 16-byte loads
+// (a 16-byte granule holding a valid byte lies inside the allocation).
+__device__ __forceinline__ void stage_tile(const uint8_t* __restrict__ U, uint64_t ulen, int64_t base,
+                                           uint8_t* sb) {
+    const uintptr_t u0 = (uintptr_t)U;
+    const int64_t lo = base - RHALO, hi = base + (int64_t)RTILE;  // byte range wanted
+    const uintptr_t a0 = (u0 + (lo < 0 ? 0 : lo)) & ~(uintptr_t)15;
+    const uintptr_t end = u0 + (uint64_t)(hi < (int64_t)ulen ? hi : (int64_t)ulen);
+    const uintptr_t a1 = (end + 15) & ~(uintptr_t)15;
+    const int64_t nvec = (int64_t)((a1 - a0) / 16);
+    // smem index of byte at address a: (a - u0) - lo
+    for (int64_t k = threadIdx.x; k < nvec; k += RT) {
+        const uintptr_t a = a0 + 16 * k;
+        const uint4 w = __ldg(reinterpret_cast<const uint4*>(a));
+        const uint8_t* wb = reinterpret_cast<const uint8_t*>(&w);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int64_t off = (int64_t)(a + j - u0);  // stream offset
+            if (off >= lo && off < hi && off >= 0 && off < (int64_t)ulen) sb[off - lo] = wb[j];
+        }
+    }
+    // padding: before the stream start -> 0x00 (a code end), past the end -> 0x80
+    for (int k = threadIdx.x; k < RHALO + (int)RTILE; k += RT) {
+        const int64_t off = lo + k;
+        if (off < 0) sb[k] = 0x00;
+        else if (off >= (int64_t)ulen) sb[k] = 0x80;
+    }
+}
+
+__device__ __forceinline__ CS thread_counts(const uint8_t* sb, int my, bool* bad, int64_t base, uint64_t ulen) {
+    uint32_t c = 0;
+    int64_t s = 0;
+#pragma unroll 4
+    for (int k = 0; k < RB; ++k) {
+        const uint8_t b = sb[my + k];
+        if (!(b & 0x80)) {
+            s += zz_dec(varint_back(sb, my + k));
+            ++c;
+        } else if (my + k >= 9 && base + (my + k - RHALO) < (int64_t)ulen) {
+            bool all = true;
+#pragma unroll
+            for (int j = 1; j <= 9; ++j) all &= (sb[my + k - j] & 0x80) != 0;
+            *bad |= all;
+        }
+    }
+    return CS{c, s};
+}
+
+__global__ void __launch_bounds__(RT) k_dec_agg(const uint8_t* __restrict__ U, uint64_t ulen,
+                                               CS* __restrict__ aggs, DevCtl* ctl) {
+    using BR = cub::BlockReduce<CS, RT>;
+    __shared__ typename BR::TempStorage tmp;
+    __shared__ __align__(16) uint8_t sb[RHALO + RTILE + 16];
+    const int64_t base = (int64_t)blockIdx.x * (int64_t)RTILE;
+    stage_tile(U, ulen, base, sb);
+    __syncthreads();
+    bool bad = false;
+    const CS mine = thread_counts(sb, RHALO + threadIdx.x * RB, &bad, base, ulen);
+    if (bad) set_err(ctl, DE_CORRUPT_VARINT);
+    const CS t = BR(tmp).Reduce(mine, CSAdd());
+    if (threadIdx.x == 0) aggs[blockIdx.x] = t;
+}
+
+// Exclusive scan of tile aggregates in one CTA; total count -> ctl->count.
+__global__ void __launch_bounds__(1024) k_scan_cs(CS* __restrict__ aggs, uint64_t T, DevCtl* ctl) {
+    using BS = cub::BlockScan<CS, 1024>;
+    __shared__ typename BS::TempStorage tmp;
+    const uint64_t per = (T + 1023) / 1024;
+    const uint64_t t0 = threadIdx.x * per, t1 = min(T, t0 + per);
+    CS local{0, 0};
+    for (uint64_t t = t0; t < t1; ++t) local = CSAdd()(local, aggs[t]);
+    CS excl, tot;
+    BS(tmp).ExclusiveScan(local, excl, CS{0, 0}, CSAdd(), tot);
+    for (uint64_t t = t0; t < t1; ++t) {
+        const CS c = aggs[t];
+        aggs[t] = excl;
+        excl = CSAdd()(excl, c);
+    }
+    if (threadIdx.x == 0) ctl->count = tot.cnt;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(RT) k_dec_out(const uint8_t* __restrict__ U, uint64_t ulen, uint64_t n,
+                                               const CS* __restrict__ pre, DevCtl* ctl,
+                                               const uint32_t* __restrict__ node, const int32_t* __restrict__ K1,
+                                               double bin1, double bin, double* __restrict__ out,
+                                               int64_t* __restrict__ P64) {
+    using BS = cub::BlockScan<CS, RT>;
+    __shared__ typename BS::TempStorage tmp;
+    __shared__ __align__(16) uint8_t sb[RHALO + RTILE + 16];
+    __shared__ int32_t kb[MODE == DEC_P64 ? 1 : RTILE];
+    const int64_t base = (int64_t)blockIdx.x * (int64_t)RTILE;
+    stage_tile(U, ulen, base, sb);
+    __syncthreads();
+    const int my = RHALO + threadIdx.x * RB;
+    bool bad = false;
+    const CS mine = thread_counts(sb, my, &bad, base, ulen);
+    CS excl, tot;
+    BS(tmp).ExclusiveScan(mine, excl, CS{0, 0}, CSAdd(), tot);
+    const CS tp = pre[blockIdx.x];
+    const uint64_t e0 = tp.cnt;           // first element of the tile
+    uint32_t li = (uint32_t)excl.cnt;     // local element index
+    int64_t K = tp.sum + excl.sum;
+    uint64_t kmax = 0;
+    for (int k = 0; k < RB; ++k) {
+        if (sb[my + k] & 0x80) continue;
+        K += zz_dec(varint_back(sb, my + k));
+        const uint64_t a = (uint64_t)(K < 0 ? -K : K);
+        kmax = a > kmax ? a : kmax;
+        if (MODE == DEC_P64) {
+            const uint64_t i = e0 + li;
+            if (i < n) P64[i] = K;
+        } else {
+            kb[li] = (int32_t)K;  // |K| < 2^30 on the fast path (checked via kmax)
+        }
+        ++li;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const uint64_t b2 = __shfl_xor_sync(0xffffffffu, kmax, o);
+        kmax = b2 > kmax ? b2 : kmax;
+    }
+    if ((threadIdx.x & 31) == 0 && kmax > ctl->max_abs_k[1]) atomicMax(&ctl->max_abs_k[1], (unsigned long long)kmax);
+    if (MODE == DEC_P64) return;
+    __syncthreads();
+    const uint32_t cnt = (uint32_t)tot.cnt;
+    for (uint32_t e = threadIdx.x; e < cnt; e += RT) {
+        const uint64_t i = e0 + e;
+        if (i >= n) break;
+        const double r = __dmul_rn((double)kb[e], bin);
+        if (MODE == DEC_VALUES) {
+            out[i] = r;
+        } else {
+            const double g = __dmul_rn((double)__ldg(&K1[__ldg(&node[i])]), bin1);
+            out[i] = __dadd_rn(g, r);
+        }
+    }
+}
+
+// Row differencing of a plain prefix P into per-row prefixes (scan along the
+// fastest axis), i.e. the first axis of the N-D inclusive prefix sum.
+__global__ void k_rows(const int64_t* __restrict__ P, uint64_t n, uint64_t R, int64_t* __restrict__ K) {
+    const uint64_t i = blockIdx.x * 256ull + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t r0 = i - i % R;
+    K[i] = P[i] - (r0 ? P[r0 - 1] : 0);
+}
+
+// Inclusive scan along axis d (d < D-1): threads own consecutive positions
+// of the fastest axis (coalesced), loop over the scanned axis.
+__global__ void k_axis_cols(int64_t* __restrict__ K, uint64_t n, uint64_t len, uint64_t stride) {
+    const uint64_t line = blockIdx.x * 256ull + threadIdx.x;
+    const uint64_t n_lines = n / len;
+    if (line >= n_lines) return;
+    const uint64_t outer = line / stride, inner = line % stride;
+    const uint64_t b = outer * len * stride + inner;
+    int64_t acc = 0;
+    for (uint64_t k = 0; k < len; ++k) {
+        acc += K[b + k * stride];
+        K[b + k * stride] = acc;
+    }
+}
+
+__global__ void k_k32(const int64_t* __restrict__ K, uint64_t n, int32_t* __restrict__ K32, DevCtl* ctl) {
+    const uint64_t i = blockIdx.x * 256ull + threadIdx.x;
+    uint64_t a = 0;
+    if (i < n) {
+        const int64_t v = K[i];
+        K32[i] = (int32_t)v;
+        a = (uint64_t)(v < 0 ? -v : v);
+    }
+    for (int o = 16; o; o >>= 1) {
+        const uint64_t b = __shfl_xor_sync(0xffffffffu, a, o);
+        a = b > a ? b : a;
+    }
+    if ((threadIdx.x & 31) == 0 && a > ctl->max_abs_k[0]) atomicMax(&ctl->max_abs_k[0], (unsigned long long)a);
+}
+
+__global__ void k_k32_to_f64(const int32_t* __restrict__ K, uint64_t n, double bin, double* __restrict__ x) {
+    const uint64_t i = blockIdx.x * 256ull + threadIdx.x;
+    if (i < n) x[i] = __dmul_rn((double)K[i], bin);
+}
+
+}  // namespace
+
+size_t dec_status_bytes(uint64_t ulen) { return (cdiv(ulen, RTILE) + 1) * sizeof(CS); }
+
+void dec_fused(int mode, const uint8_t* U, uint64_t ulen, uint64_t n, void* status, DevCtl* ctl,
+               const uint32_t* node, const int32_t* K1, double bin1, double bin, double* out, int64_t* P64,
+               cudaStream_t st) {
+    const uint64_t T = cdiv(ulen, RTILE);
+    if (!T) return;
+    auto* aggs = static_cast<CS*>(status);
+    k_dec_agg<<<(unsigned)T, RT, 0, st>>>(U, ulen, aggs, ctl);
+    UMCG_LAUNCHED();
+    k_scan_cs<<<1, 1024, 0, st>>>(aggs, T, ctl);
+    UMCG_LAUNCHED();
+    if (mode == DEC_P64)
+        k_dec_out<DEC_P64><<<(unsigned)T, RT, 0, st>>>(U, ulen, n, aggs, ctl, node, K1, bin1, bin, out, P64);
+    else if (mode == DEC_VALUES)
+        k_dec_out<DEC_VALUES><<<(unsigned)T, RT, 0, st>>>(U, ulen, n, aggs, ctl, node, K1, bin1, bin, out, P64);
+    else
+        k_dec_out<DEC_RECOMPOSE><<<(unsigned)T, RT, 0, st>>>(U, ulen, n, aggs, ctl, node, K1, bin1, bin, out, P64);
+    UMCG_LAUNCHED();
+}
+
+void nd_from_prefix(const int64_t* P, uint64_t n, const NdShape& sh, int64_t* Kw, int32_t* K32, DevCtl* ctl,
+                    cudaStream_t st) {
+    const unsigned g = (unsigned)cdiv(n, 256);
+    if (!n) return;
+    const int64_t* src = P;
+    if (sh.D > 1) {
+        k_rows<<<g, 256, 0, st>>>(P, n, sh.dims[sh.D - 1], Kw);
+        UMCG_LAUNCHED();
+        for (int d = sh.D - 2; d >= 0; --d) {
+            const uint64_t lines = n / sh.dims[d];
+            k_axis_cols<<<(unsigned)cdiv(lines, 256), 256, 0, st>>>(Kw, n, sh.dims[d], sh.strides[d]);
+            UMCG_LAUNCHED();
+        }
+        src = Kw;
+    }
+    k_k32<<<g, 256, 0, st>>>(src, n, K32, ctl);
+    UMCG_LAUNCHED();
+}
+
+void k32_to_f64(const int32_t* K, uint64_t n, double bin, double* x, cudaStream_t st) {
+    if (!n) return;
+    k_k32_to_f64<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(K, n, bin, x);
+    UMCG_LAUNCHED();
+}
+
+}  // namespace umcg

@@ -1,0 +1,32 @@
+// Fused stream decode (decode.cu) + N-D lattice reconstruction helpers.
+#pragma once
+
+#include "kernels.h"
+
+namespace umcg {
+
+enum DecMode : int { DEC_P64 = 0, DEC_VALUES = 1, DEC_RECOMPOSE = 2 };
+
+size_t dec_status_bytes(uint64_t ulen);
+// One pass over the unpacked varint bytes U[0..ulen): see decode.cu. Writes
+// ctl->count (number of complete varints), ctl->max_abs_k[1] and flags
+// DE_CORRUPT_VARINT. ctl->aux[6] is used as the tile ticket.
+void dec_fused(int mode, const uint8_t* U, uint64_t ulen, uint64_t n, void* status, DevCtl* ctl,
+               const uint32_t* node, const int32_t* K1, double bin1, double bin, double* out, int64_t* P64,
+               cudaStream_t st);
+// N-D inclusive prefix from the plain 1-D prefix P of row-major codes:
+// row differencing (fastest axis) + scans along the other axes -> int32 K,
+// max|K| -> ctl->max_abs_k[0]. Kw is int64 scratch [n] (unused when D == 1).
+void nd_from_prefix(const int64_t* P, uint64_t n, const NdShape& sh, int64_t* Kw, int32_t* K32, DevCtl* ctl,
+                    cudaStream_t st);
+void k32_to_f64(const int32_t* K, uint64_t n, double bin, double* x, cudaStream_t st);
+
+// RLE token stream -> unpacked varint bytes (in place for a single literal
+// token). Synchronizes; throws corrupt_payload on malformed token streams.
+const uint8_t* stream_unpack(const uint8_t* d_stream, uint64_t len, StreamDecScratch& s, DevCtl* ctl,
+                             cudaStream_t st, uint64_t* ulen);
+// varint bytes -> codes[n] (u64); validates counts (corrupt_payload).
+void varint_codes(const uint8_t* U, uint64_t ulen, uint64_t n, uint64_t* d_codes, StreamDecScratch& s,
+                  DevCtl* ctl, cudaStream_t st);
+
+}  // namespace umcg

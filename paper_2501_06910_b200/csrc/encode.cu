@@ -1,0 +1,508 @@
+// Zero-RLE varint stream encoder on sm_100a.
+//
+// Byte format: the reference's ByteWriter::varint stream of the codes
+// (common.hpp:60-66) passed through rle_compress (lossless.hpp:24-51):
+// maximal zero runs of >= 8 bytes become {0x00, varint(len)}, everything in
+// between becomes {0x01, varint(len), bytes}. A 0x00 byte occurs iff a code
+// is 0, so the token structure is decided on codes (RleSum, common.cuh).
+//
+// Kernels (every phase fully parallel; no inter-CTA waiting):
+//   tiles/chunks/cscan/states: reduce-then-scan of per-2048-code RleSum tile
+//            summaries -> each tile's entry state; the tile that sees a
+//            literal close records that literal's total byte length.
+//   write:   per tile, output range [P_t, P_t+1) from the entry states.
+//            Fast path (no zero run >= 8 strictly inside the tile): one u32
+//            block scan of byte lengths places every varint; the head
+//            (pending zeros, Z token, literal header) is written by thread 0.
+//            General path: exact per-thread walk of the state machine.
+//            Bytes are staged in shared memory and leave in 4-byte stores.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include "kernels.h"
+
+namespace umcg {
+
+namespace {
+
+struct RleComposeOp {
+    __device__ __forceinline__ RleSum operator()(const RleSum& a, const RleSum& b) const {
+        return rle_compose(a, b);
+    }
+};
+
+template <class T>
+__device__ __forceinline__ void write_varint(uint8_t* out, uint64_t pos, uint64_t base, uint64_t cap, T v) {
+    uint64_t u = (uint64_t)v;
+    uint64_t p = pos - base;
+    while (u >= 0x80) {
+        if (p < cap) out[p] = (uint8_t)u | 0x80;
+        ++p;
+        u >>= 7;
+    }
+    if (p < cap) out[p] = (uint8_t)u;
+}
+
+template <class T>
+__device__ __forceinline__ int load_items(const T* codes, uint64_t n, uint64_t first, T (&v)[ENC_ITEMS]) {
+    int cnt = 0;
+    if (first + ENC_ITEMS <= n && sizeof(T) == 4 && (first % 4) == 0) {
+        const uint4* p = reinterpret_cast<const uint4*>(codes + first);
+        const uint4 a = __ldg(p), b = __ldg(p + 1);
+        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int k = 0; k < ENC_ITEMS; ++k) v[k] = (T)w[k];
+        return ENC_ITEMS;
+    }
+#pragma unroll
+    for (int k = 0; k < ENC_ITEMS; ++k) {
+        const uint64_t i = first + k;
+        if (i < n) { v[k] = codes[i]; cnt = k + 1; } else { v[k] = 0; }
+    }
+    return cnt;
+}
+
+template <class T>
+__device__ __forceinline__ RleSum thread_summary(const T (&v)[ENC_ITEMS], int cnt, uint32_t origin) {
+    // <= 8 codes cannot hold a zero run >= 8 strictly between two nonzeros,
+    // so a thread summary never has interior runs.
+    static_assert(ENC_ITEMS <= 9, "fast thread summary assumes <= 9 items");
+    uint32_t zm = 0;
+#pragma unroll
+    for (int k = 0; k < ENC_ITEMS; ++k) zm |= (k < cnt && v[k] == 0) ? (1u << k) : 0u;
+    const uint32_t valid = cnt >= 32 ? ~0u : ((1u << cnt) - 1u);
+    const uint32_t nz = ~zm & valid;
+    RleSum s;
+    s.tz = s.lb = s.mid = 0;
+    if (nz == 0) {
+        s.lz = (uint64_t)cnt; s.fb = 0; s.origin = kNoOrigin; s.flags = 1u;
+        return s;
+    }
+    const int lo = __ffs(nz) - 1, hi = 31 - __clz(nz);
+    uint64_t fb = 0;
+#pragma unroll
+    for (int k = 0; k < ENC_ITEMS; ++k)
+        if (k >= lo && k <= hi) fb += v[k] == 0 ? 1u : vlen64((uint64_t)v[k]);
+    s.lz = (uint64_t)lo;
+    s.tz = (uint64_t)(cnt - 1 - hi);
+    s.fb = fb;
+    s.origin = origin;
+    s.flags = 0u;
+    return s;
+}
+
+// Phase 1: tile summaries (independent tiles).
+template <class T>
+__global__ void __launch_bounds__(ENC_THREADS) k_rle_tiles(const T* __restrict__ codes, uint64_t n,
+                                                           RleSum* __restrict__ sums) {
+    using BR = cub::BlockReduce<RleSum, ENC_THREADS>;
+    __shared__ typename BR::TempStorage tmp;
+    const uint64_t tile = blockIdx.x;
+    const uint64_t first = tile * ENC_TILE + (uint64_t)threadIdx.x * ENC_ITEMS;
+    T v[ENC_ITEMS];
+    const int cnt = load_items(codes, n, first, v);
+    const RleSum s = thread_summary(v, cnt, (uint32_t)tile);
+    const RleSum tot = BR(tmp).Reduce(s, RleComposeOp());
+    if (threadIdx.x == 0) sums[tile] = tot;
+}
+
+constexpr int CH = 256;  // tiles per chunk
+
+// Phase 2: chunk aggregates of CH tile summaries.
+__global__ void __launch_bounds__(CH) k_rle_chunks(const RleSum* __restrict__ sums, uint64_t T,
+                                                   RleSum* __restrict__ csum) {
+    using BR = cub::BlockReduce<RleSum, CH>;
+    __shared__ typename BR::TempStorage tmp;
+    const uint64_t t = blockIdx.x * (uint64_t)CH + threadIdx.x;
+    const RleSum s = t < T ? sums[t] : rle_identity();
+    const RleSum tot = BR(tmp).Reduce(s, RleComposeOp());
+    if (threadIdx.x == 0) csum[blockIdx.x] = tot;
+}
+
+// Phase 3: exclusive scan of chunk aggregates (one CTA).
+__global__ void __launch_bounds__(256) k_rle_cscan(RleSum* __restrict__ csum, uint64_t C) {
+    using BS = cub::BlockScan<RleSum, 256>;
+    __shared__ typename BS::TempStorage tmp;
+    const uint64_t per = (C + 255) / 256;
+    const uint64_t c0 = threadIdx.x * per, c1 = min(C, c0 + per);
+    RleSum local = rle_identity();
+    for (uint64_t c = c0; c < c1; ++c) local = rle_compose(local, csum[c]);
+    RleSum excl;
+    BS(tmp).ExclusiveScan(local, excl, rle_identity(), RleComposeOp());
+    for (uint64_t c = c0; c < c1; ++c) {
+        const RleSum v = csum[c];
+        csum[c] = excl;
+        excl = rle_compose(excl, v);
+    }
+}
+
+// Phase 4: per-tile entry states, literal totals (keyed by the tile the
+// literal opened in), final length, and the list of tiles that need the
+// general writer.
+__global__ void __launch_bounds__(CH) k_rle_states(const RleSum* __restrict__ sums, uint64_t T,
+                                                   const RleSum* __restrict__ csum, RleState* __restrict__ states,
+                                                   uint64_t* __restrict__ lit_total, uint32_t* __restrict__ glist,
+                                                   DevCtl* ctl, int comp) {
+    using BS = cub::BlockScan<RleSum, CH>;
+    __shared__ typename BS::TempStorage tmp;
+    const uint64_t t = blockIdx.x * (uint64_t)CH + threadIdx.x;
+    const RleSum S = t < T ? sums[t] : rle_identity();
+    RleSum excl;
+    BS(tmp).ExclusiveScan(S, excl, rle_identity(), RleComposeOp());
+    if (t >= T) return;
+    bool cl;
+    uint64_t tt;
+    const RleState st = rle_apply(rle_state0(), rle_compose(csum[blockIdx.x], excl), &cl, &tt);
+    states[t] = st;
+    const RleState nx = rle_apply(st, S, &cl, &tt);
+    if (cl) lit_total[st.origin] = tt;
+    const bool last = t == T - 1;
+    if (S.has_int() || (S.allzero() && last))
+        glist[atomicAdd(reinterpret_cast<unsigned int*>(&ctl->aux[4 + comp]), 1u)] = (uint32_t)t;
+    if (last) {
+        states[T] = nx;
+        bool closes;
+        uint64_t tl = 0;
+        const uint64_t len = rle_finish(nx, &closes, &tl);
+        if (closes && nx.has) lit_total[nx.origin] = tl;
+        ctl->stream_len[comp] = len;
+    }
+}
+
+constexpr uint32_t kEntry = ENC_THREADS;  // slot of the literal open on tile entry
+constexpr uint64_t kUnknown = ~0ull;
+
+// Per-thread exact walk of the RLE state machine over its codes (general path).
+// WRITE=false: record literal closes; WRITE=true: emit bytes.
+template <bool WRITE, class T>
+__device__ __forceinline__ void walk(RleState st, const T (&v)[ENC_ITEMS], int cnt, bool finalize,
+                                     uint64_t* closeTot, uint8_t* out, uint64_t base, uint64_t cap) {
+    const uint32_t me = threadIdx.x;
+    auto data_pos = [&](const RleState& s) { return s.C + 1 + vlen64(closeTot[s.origin]) + s.Lb; };
+    auto open_lit = [&](RleState& s) {
+        s.origin = me;
+        s.Lb = 0;
+        s.has = 1;
+        if (WRITE) {
+            const uint64_t p = s.C - base;
+            if (p < cap) out[p] = 0x01;
+            write_varint(out, s.C + 1, base, cap, closeTot[me]);
+        }
+    };
+    auto put_zeros = [&](RleState& s, uint64_t J) {
+        if (WRITE) {
+            const uint64_t p0 = data_pos(s) - base;
+            for (uint64_t k = 0; k < J; ++k)
+                if (p0 + k < cap) out[p0 + k] = 0;
+        }
+        s.Lb += J;
+    };
+    auto put_z = [&](RleState& s, uint64_t J) {
+        if (WRITE) {
+            const uint64_t p = s.C - base;
+            if (p < cap) out[p] = 0x00;
+            write_varint(out, s.C + 1, base, cap, J);
+        }
+        s.C += z_size(J);
+    };
+    auto close_lit = [&](RleState& s) {
+        if (!WRITE) closeTot[s.origin] = s.Lb;
+        s.C += lit_size(s.Lb);
+        s.has = 0;
+    };
+#pragma unroll
+    for (int k = 0; k < ENC_ITEMS; ++k) {
+        if (k >= cnt) break;
+        const T c = v[k];
+        if (c == 0) { st.Zp += 1; continue; }
+        const uint64_t J = st.Zp;
+        if (J >= kMinZeroRun) {
+            if (st.has) close_lit(st);
+            put_z(st, J);
+            open_lit(st);
+        } else {
+            if (!st.has) open_lit(st);
+            put_zeros(st, J);
+        }
+        st.Zp = 0;
+        if (WRITE) write_varint(out, data_pos(st), base, cap, c);
+        st.Lb += vlen64((uint64_t)c);
+    }
+    if (finalize) {
+        const uint64_t J = st.Zp;
+        if (J >= kMinZeroRun) {
+            if (st.has) close_lit(st);
+            put_z(st, J);
+        } else if (J > 0 || st.has) {
+            if (!st.has) open_lit(st);
+            put_zeros(st, J);
+            close_lit(st);
+        }
+    }
+}
+
+__device__ __forceinline__ uint64_t state_pos(const RleState& s, const uint64_t* lit_total) {
+    return s.has ? s.C + 1 + vlen64(lit_total[s.origin]) + s.Lb : s.C;
+}
+
+// Staged bytes -> global, 4-byte stores after a byte-wise head.
+__device__ __forceinline__ void copy_out(const uint8_t* out, uint64_t len, uint8_t* d) {
+    const uint32_t head = (uint32_t)((4 - ((uintptr_t)d & 3)) & 3);
+    const uint64_t h = head < len ? head : len;
+    if (threadIdx.x < h) d[threadIdx.x] = out[threadIdx.x];
+    const uint64_t words = (len - h) / 4;
+    uint32_t* dw = reinterpret_cast<uint32_t*>(d + h);
+    for (uint64_t w = threadIdx.x; w < words; w += ENC_THREADS) {
+        const uint8_t* s = out + h + 4 * w;
+        dw[w] = (uint32_t)s[0] | ((uint32_t)s[1] << 8) | ((uint32_t)s[2] << 16) | ((uint32_t)s[3] << 24);
+    }
+    const uint64_t t0 = h + 4 * words;
+    if (t0 + threadIdx.x < len) d[t0 + threadIdx.x] = out[t0 + threadIdx.x];
+}
+
+template <class T>
+__global__ void __launch_bounds__(ENC_THREADS) k_rle_write_fast(const T* __restrict__ codes, uint64_t n,
+                                                           const RleState* __restrict__ states,
+                                                           const RleSum* __restrict__ sums,
+                                                           const uint64_t* __restrict__ lit_total,
+                                                           const DevCtl* __restrict__ ctl, int comp,
+                                                           uint8_t* __restrict__ dst, int off_from_ctl) {
+    constexpr uint64_t CAP = ENC_TILE * (sizeof(T) == 8 ? 10 : 5) + 64;
+    using BS = cub::BlockScan<RleSum, ENC_THREADS>;
+    using BS32 = cub::BlockScan<uint32_t, ENC_THREADS>;
+    __shared__ union {
+        typename BS::TempStorage rle;
+        typename BS32::TempStorage u32;
+    } tmp;
+    __shared__ uint64_t closeTot[ENC_THREADS + 1];
+    __shared__ __align__(16) uint8_t out[CAP];
+
+    const uint64_t tile = blockIdx.x;
+    {
+        const RleSum S0 = sums[tile];
+        if (S0.has_int() || S0.allzero()) return;  // general writer (or nothing to write)
+    }
+    const uint64_t T_ = (n + ENC_TILE - 1) / ENC_TILE;
+    const bool last = tile == T_ - 1;
+    const RleState entry = states[tile];
+    const RleSum S = sums[tile];
+    const uint64_t P0 = state_pos(entry, lit_total);
+    const uint64_t P1 = last ? ctl->stream_len[comp] : state_pos(states[tile + 1], lit_total);
+    const uint64_t len = P1 - P0;
+    if (len == 0) return;  // all-zero tile: its zeros stay pending
+    uint8_t* d = dst + (off_from_ctl ? ctl->stream_off[comp] : 0) + P0;
+
+    const uint64_t first = tile * ENC_TILE + (uint64_t)threadIdx.x * ENC_ITEMS;
+    T v[ENC_ITEMS];
+    const int cnt = load_items(codes, n, first, v);
+
+    {
+        // ---- fast path: the core is one literal segment ----
+        const uint64_t tile_cnt = min((uint64_t)ENC_TILE, n - tile * ENC_TILE);
+        const uint64_t core_lo = S.lz, core_hi = tile_cnt - S.tz;  // [lo, hi)
+        uint32_t w = 0;
+        const uint64_t r0 = (uint64_t)threadIdx.x * ENC_ITEMS;
+#pragma unroll
+        for (int k = 0; k < ENC_ITEMS; ++k) {
+            const uint64_t r = r0 + k;
+            if (k < cnt && r >= core_lo && r < core_hi) w += v[k] == 0 ? 1u : vlen64((uint64_t)v[k]);
+        }
+        uint32_t off, core_total;
+        BS32(tmp.u32).ExclusiveSum(w, off, core_total);
+        // head: pending zeros from before + this tile's leading zeros
+        const uint64_t J0 = entry.Zp + S.lz;
+        uint64_t data_base, zero_pos = 0, zpos = 0, lpos = 0, totn = 0;
+        bool ztok = false, hdr = false;
+        if (J0 >= kMinZeroRun) {
+            zpos = entry.C + (entry.has ? lit_size(entry.Lb) : 0);
+            ztok = true;
+            lpos = zpos + z_size(J0);
+            hdr = true;
+            totn = lit_total[tile];
+            data_base = lpos + 1 + vlen64(totn);
+        } else if (entry.has) {
+            zero_pos = entry.C + 1 + vlen64(lit_total[entry.origin]) + entry.Lb;
+            data_base = zero_pos + J0;
+        } else {
+            lpos = entry.C;
+            hdr = true;
+            totn = lit_total[tile];
+            zero_pos = lpos + 1 + vlen64(totn);
+            data_base = zero_pos + J0;
+        }
+        if (threadIdx.x == 0) {
+            if (ztok) {
+                out[zpos - P0] = 0x00;
+                write_varint(out, zpos + 1, P0, CAP, J0);
+            }
+            if (hdr) {
+                out[lpos - P0] = 0x01;
+                write_varint(out, lpos + 1, P0, CAP, totn);
+            }
+            if (!ztok)
+                for (uint64_t k = 0; k < J0; ++k) out[zero_pos - P0 + k] = 0;
+            if (last) {  // rle_finish: trailing zeros close the stream
+                const uint64_t core_end = data_base + core_total;
+                if (S.tz >= kMinZeroRun) {
+                    out[core_end - P0] = 0x00;
+                    write_varint(out, core_end + 1, P0, CAP, S.tz);
+                } else {
+                    for (uint64_t k = 0; k < S.tz; ++k) out[core_end - P0 + k] = 0;
+                }
+            }
+        }
+        uint64_t pos = data_base + off;
+#pragma unroll
+        for (int k = 0; k < ENC_ITEMS; ++k) {
+            const uint64_t r = r0 + k;
+            if (k < cnt && r >= core_lo && r < core_hi) {
+                if (v[k] == 0) {
+                    out[pos - P0] = 0;
+                    pos += 1;
+                } else {
+                    write_varint(out, pos, P0, CAP, v[k]);
+                    pos += vlen64((uint64_t)v[k]);
+                }
+            }
+        }
+        __syncthreads();
+        copy_out(out, len, d);
+        return;
+    }
+
+}
+
+template <class T>
+__global__ void __launch_bounds__(ENC_THREADS) k_rle_write_general(const T* __restrict__ codes, uint64_t n,
+                                                           const RleState* __restrict__ states,
+                                                           const RleSum* __restrict__ sums,
+                                                           const uint64_t* __restrict__ lit_total,
+                                                           const DevCtl* __restrict__ ctl, int comp, const uint32_t* __restrict__ glist,
+                                                           uint8_t* __restrict__ dst, int off_from_ctl) {
+    constexpr uint64_t CAP = ENC_TILE * (sizeof(T) == 8 ? 10 : 5) + 64;
+    using BS = cub::BlockScan<RleSum, ENC_THREADS>;
+    using BS32 = cub::BlockScan<uint32_t, ENC_THREADS>;
+    __shared__ union {
+        typename BS::TempStorage rle;
+        typename BS32::TempStorage u32;
+    } tmp;
+    __shared__ uint64_t closeTot[ENC_THREADS + 1];
+    __shared__ __align__(16) uint8_t out[CAP];
+
+    if (blockIdx.x >= (uint32_t)ctl->aux[4 + comp]) return;
+    const uint64_t tile = glist[blockIdx.x];
+    const uint64_t T_ = (n + ENC_TILE - 1) / ENC_TILE;
+    const bool last = tile == T_ - 1;
+    const RleState entry = states[tile];
+    const RleSum S = sums[tile];
+    const uint64_t P0 = state_pos(entry, lit_total);
+    const uint64_t P1 = last ? ctl->stream_len[comp] : state_pos(states[tile + 1], lit_total);
+    const uint64_t len = P1 - P0;
+    if (len == 0) return;  // all-zero tile: its zeros stay pending
+    uint8_t* d = dst + (off_from_ctl ? ctl->stream_off[comp] : 0) + P0;
+
+    const uint64_t first = tile * ENC_TILE + (uint64_t)threadIdx.x * ENC_ITEMS;
+    T v[ENC_ITEMS];
+    const int cnt = load_items(codes, n, first, v);
+
+    // ---- general path: exact walk of the state machine ----
+    const RleSum s = thread_summary(v, cnt, threadIdx.x);
+    RleSum excl;
+    BS(tmp.rle).ExclusiveScan(s, excl, rle_identity(), RleComposeOp());
+    RleState e = entry;
+    e.origin = entry.has ? kEntry : kNoOrigin;
+    bool cl;
+    uint64_t tt;
+    const RleState st = rle_apply(e, excl, &cl, &tt);
+    const bool finalize = cnt > 0 && first + cnt == n;
+    for (uint32_t k = threadIdx.x; k <= ENC_THREADS; k += ENC_THREADS) closeTot[k] = kUnknown;
+    __syncthreads();
+    walk<false>(st, v, cnt, finalize, closeTot, nullptr, 0, 0);
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k <= ENC_THREADS; k += ENC_THREADS) {
+        if (closeTot[k] == kUnknown) {
+            if (k == kEntry) closeTot[k] = entry.has ? lit_total[entry.origin] : 0;
+            else closeTot[k] = lit_total[tile];
+        }
+    }
+    __syncthreads();
+    walk<true>(st, v, cnt, finalize, closeTot, out, P0, CAP);
+    __syncthreads();
+    copy_out(out, len, d);
+}
+
+}  // namespace
+
+size_t stream_enc_scratch_bytes(uint64_t n) {
+    const uint64_t T = cdiv(n, ENC_TILE) + 1;
+    return T * (2 * sizeof(RleSum) + sizeof(RleState) + sizeof(uint64_t) + sizeof(uint32_t)) + 4096;
+}
+
+StreamEncScratch stream_enc_carve(void* base, uint64_t n) {
+    const uint64_t T = cdiv(n, ENC_TILE) + 1;
+    StreamEncScratch s;
+    char* p = static_cast<char*>(base);
+    s.csum = reinterpret_cast<RleSum*>(p);
+    p += T * sizeof(RleSum);
+    s.sums = reinterpret_cast<RleSum*>(p);
+    p += T * sizeof(RleSum);
+    s.states = reinterpret_cast<RleState*>(p);
+    p += T * sizeof(RleState);
+    s.lit_total = reinterpret_cast<uint64_t*>(p);
+    p += T * sizeof(uint64_t);
+    s.glist = reinterpret_cast<uint32_t*>(p);
+    return s;
+}
+
+template <class T>
+static void plan_impl(const T* codes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp, cudaStream_t st) {
+    const uint64_t T_ = cdiv(n, ENC_TILE);
+    if (!T_) {
+        UMCG_CUDA(cudaMemsetAsync(&ctl->stream_len[comp], 0, 8, st));
+        return;
+    }
+    const uint64_t C = cdiv(T_, CH);
+    UMCG_CUDA(cudaMemsetAsync(&ctl->aux[4 + comp], 0, 8, st));
+    k_rle_tiles<T><<<(unsigned)T_, ENC_THREADS, 0, st>>>(codes, n, s.sums);
+    UMCG_LAUNCHED();
+    k_rle_chunks<<<(unsigned)C, CH, 0, st>>>(s.sums, T_, s.csum);
+    UMCG_LAUNCHED();
+    k_rle_cscan<<<1, 256, 0, st>>>(s.csum, C);
+    UMCG_LAUNCHED();
+    k_rle_states<<<(unsigned)C, CH, 0, st>>>(s.sums, T_, s.csum, s.states, s.lit_total, s.glist, ctl, comp);
+    UMCG_LAUNCHED();
+}
+
+template <class T>
+static void write_impl(const T* codes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp, uint8_t* dst,
+                       bool off_ctl, cudaStream_t st) {
+    const uint64_t T_ = cdiv(n, ENC_TILE);
+    if (!T_) return;
+    k_rle_write_fast<T><<<(unsigned)T_, ENC_THREADS, 0, st>>>(codes, n, s.states, s.sums, s.lit_total, ctl, comp,
+                                                              dst, off_ctl ? 1 : 0);
+    UMCG_LAUNCHED();
+    k_rle_write_general<T><<<(unsigned)T_, ENC_THREADS, 0, st>>>(codes, n, s.states, s.sums, s.lit_total, ctl,
+                                                                 comp, s.glist, dst, off_ctl ? 1 : 0);
+    UMCG_LAUNCHED();
+}
+
+void stream_plan_u32(const uint32_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
+                     cudaStream_t st) { plan_impl(c, n, s, ctl, comp, st); }
+void stream_plan_u64(const uint64_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
+                     cudaStream_t st) { plan_impl(c, n, s, ctl, comp, st); }
+void stream_write_u32(const uint32_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
+                      uint8_t* dst, bool o, cudaStream_t st) { write_impl(c, n, s, ctl, comp, dst, o, st); }
+void stream_write_u64(const uint64_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
+                      uint8_t* dst, bool o, cudaStream_t st) { write_impl(c, n, s, ctl, comp, dst, o, st); }
+void stream_encode_u32(const uint32_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
+                       uint8_t* dst, bool o, cudaStream_t st) {
+    plan_impl(c, n, s, ctl, comp, st);
+    write_impl(c, n, s, ctl, comp, dst, o, st);
+}
+void stream_encode_u64(const uint64_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
+                       uint8_t* dst, bool o, cudaStream_t st) {
+    plan_impl(c, n, s, ctl, comp, st);
+    write_impl(c, n, s, ctl, comp, dst, o, st);
+}
+
+}  // namespace umcg

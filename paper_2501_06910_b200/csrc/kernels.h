@@ -11,10 +11,11 @@ constexpr int ENC_ITEMS = 8;  // <= 9 so a thread opens at most one literal
 constexpr uint64_t ENC_TILE = ENC_THREADS * ENC_ITEMS;
 
 struct StreamEncScratch {
-    RleSum* sums = nullptr;      // [T]
-    RleState* states = nullptr;  // [T+1]
-    uint64_t* P = nullptr;       // [T+1] output start per tile
-    uint64_t* lit_total = nullptr;  // [T]
+    RleSum* csum = nullptr;         // [T/256] chunk aggregates -> exclusive prefixes
+    RleSum* sums = nullptr;         // [T]   tile summaries
+    RleState* states = nullptr;     // [T+1] entry state per tile (+ final)
+    uint64_t* lit_total = nullptr;  // [T]   literal byte totals, keyed by opening tile
+    uint32_t* glist = nullptr;      // [T]   tiles for the general writer (count in ctl->aux[4+comp])
 };
 size_t stream_enc_scratch_bytes(uint64_t n);
 StreamEncScratch stream_enc_carve(void* base, uint64_t n);

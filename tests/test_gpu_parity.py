@@ -281,3 +281,33 @@ def test_determinism_and_host_path(cuda):
     assert a1 == a2 == a3
     y = plan.decompress_host(a1)
     assert np.array_equal(y, plan.decompress(a1).cpu().numpy())
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_rle_stream_patterns_bit_exact(cuda, ref, seed):
+    """Zero-run structure at every scale (runs of 0..40 zero codes, all-zero
+    tiles, runs crossing the 2048-code tiles, long literals) through the
+    predictor=none path, whose codes are exact, so payloads must match the
+    reference byte for byte (lossless.hpp:24-51 token structure)."""
+    rng = np.random.default_rng(1000 + seed)
+    n = [5000, 70000, 300000, 2048 * 3, 2048 * 5 + 7, 1][seed % 6] if seed < 6 else 10000
+    q = np.zeros(n, np.int64)
+    i = 0
+    while i < n:
+        if rng.random() < 0.5:
+            run = int(rng.choice([1, 3, 7, 8, 9, 15, 40, 2048, 5000]))
+            i += run  # zeros
+        else:
+            lit = int(rng.integers(1, 60))
+            q[i:i + lit] = rng.integers(-300, 300, size=min(lit, n - i))
+            i += lit
+    if seed == 4:
+        q[:] = 0
+        q[-1] = 5  # one long run then a literal
+    tau = 0.5
+    v = q.astype(np.float64) * (2 * tau)
+    got = umcg.encode(dev(v), predictor=0, tau=tau)
+    want = ref.encode(v, predictor=0, tau=tau)
+    assert got == want
+    back = umcg.decode(want).cpu().numpy()
+    assert np.array_equal(back, ref.decode(want, n))
