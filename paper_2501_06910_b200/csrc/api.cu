@@ -186,12 +186,23 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     const uint64_t n = p->n, n1 = p->n_slots;
     auto* ctl = p->ctl.as<DevCtl>(1);
     init_ctl(ctl, st);
-    minmax(d_x, x_f32, n, ctl, st);
-    budget(BudgetArgs{prm.tau, prm.split_rho, prm.coeff_abs_sum, prm.bound_kind, n}, ctl, st);
-
-    // f: cluster means (interp.hpp:46-93)
+    // nearest g: partitioned layout (partition.cu); multilinear: gathers
+    const bool part = prm.g_kind == 0 && p->n_buckets > 0;
     double* x1 = p->x1.as<double>(n1 ? n1 : 1);
-    cluster_mean(d_x, x_f32, p->d_perm.as<uint32_t>(1), p->d_seg.as<uint32_t>(1), n1, x1, st);
+    int32_t* Kp = nullptr;
+    if (part) {
+        double* xp = p->scratch_c.as<double>(n ? n : 1);
+        Kp = p->kbuf.as<int32_t>(std::max<uint64_t>(n, n1) + 1);
+        partition_values(d_x, x_f32, p, xp, ctl, st);  // + range / finiteness
+        budget(BudgetArgs{prm.tau, prm.split_rho, prm.coeff_abs_sum, prm.bound_kind, n}, ctl, st);
+        // f: cluster means (interp.hpp:46-93) + residual lattice indices
+        bucket_means_residuals(p, xp, ctl, x1, Kp, st);
+    } else {
+        minmax(d_x, x_f32, n, ctl, st);
+        budget(BudgetArgs{prm.tau, prm.split_rho, prm.coeff_abs_sum, prm.bound_kind, n}, ctl, st);
+        // f: cluster means (interp.hpp:46-93)
+        cluster_mean(d_x, x_f32, p->d_perm.as<uint32_t>(1), p->d_seg.as<uint32_t>(1), n1, x1, st);
+    }
     if (prm.fill == 1 && p->mode == 0) fill_nearest_visited(p->d_seg.as<uint32_t>(1), n1, p->shape[p->dim - 1], x1, st);
 
     // component specs (grid_codec_spec, pipeline.hpp:96-110)
@@ -234,7 +245,7 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     } else if (m.lossless[0]) {
         codes_lossless_values(x1, n1, pred1, sh1, static_cast<uint64_t*>(codes[0]), st);
     } else {
-        int32_t* kb = p->kbuf.as<int32_t>(n1 ? n1 : 1);
+        int32_t* kb = p->scratch_d.as<int32_t>(n1 ? n1 : 1);
         codes_lossy_values(x1, n1, pred1, sh1, ctl, 0, static_cast<uint32_t*>(codes[0]), kb, st);
     }
     // residual component
@@ -250,16 +261,24 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
                       esc_idx[1], ev, ctl, 1, st);
     } else if (m.lossless[1]) {
         codes_lossless_residual(rs, n, static_cast<uint64_t*>(codes[1]), st);
-    } else {
-        codes_lossy_residual(rs, n, ctl, static_cast<uint32_t*>(codes[1]), st);
     }
-
-    // stream structure, layout, headers, bytes
     StreamEncScratch es[2];
     for (int c = 0; c < 2; ++c) {
         DevBuf& eb = c == 0 ? p->enc1 : p->enc2;
         es[c] = stream_enc_carve(eb.reserve(stream_enc_scratch_bytes(ncode[c])), ncode[c]);
-        if (wide[c]) stream_plan_u64(static_cast<uint64_t*>(codes[c]), ncode[c], es[c], ctl, c, st);
+    }
+    const bool fused_resid = part && !m.serial[1] && !m.lossless[1];
+    if (fused_resid) {
+        // q = K2_i - K2_{i-1} back in vertex order + RLE tile summaries (partition.cu)
+        resid_codes_tiles(p, Kp, static_cast<uint32_t*>(codes[1]), es[1], st);
+    } else if (!m.serial[1] && !m.lossless[1]) {
+        codes_lossy_residual(rs, n, ctl, static_cast<uint32_t*>(codes[1]), st);
+    }
+
+    // stream structure, layout, headers, bytes
+    for (int c = 0; c < 2; ++c) {
+        if (c == 1 && fused_resid) stream_plan_from_sums(ncode[c], es[c], ctl, c, st);
+        else if (wide[c]) stream_plan_u64(static_cast<uint64_t*>(codes[c]), ncode[c], es[c], ctl, c, st);
         else stream_plan_u32(static_cast<uint32_t*>(codes[c]), ncode[c], es[c], ctl, c, st);
     }
     HdrArgs h{};

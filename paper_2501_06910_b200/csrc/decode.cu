@@ -45,28 +45,39 @@ constexpr int RB = 32;
 constexpr uint64_t RTILE = (uint64_t)RT * RB;
 constexpr int RHALO = 16;
 
-// Stage tile bytes [base-16, base+RTILE) into smem with aligned 16-byte loads
-// (a 16-byte granule holding a valid byte lies inside the allocation).
+// Stage tile bytes [base-16, base+RTILE) into 16-byte aligned shared memory:
+// aligned 16-byte global loads (a 16-byte granule holding a valid byte lies
+// inside the allocation) realigned with funnel shifts, then padding bytes:
+// before the stream -> 0x00 (acts as a code end), past the end -> 0x80.
 __device__ __forceinline__ void stage_tile(const uint8_t* __restrict__ U, uint64_t ulen, int64_t base,
                                            uint8_t* sb) {
-    const uintptr_t u0 = (uintptr_t)U;
-    const int64_t lo = base - RHALO, hi = base + (int64_t)RTILE;  // byte range wanted
-    const uintptr_t a0 = (u0 + (lo < 0 ? 0 : lo)) & ~(uintptr_t)15;
-    const uintptr_t end = u0 + (uint64_t)(hi < (int64_t)ulen ? hi : (int64_t)ulen);
-    const uintptr_t a1 = (end + 15) & ~(uintptr_t)15;
-    const int64_t nvec = (int64_t)((a1 - a0) / 16);
-    // smem index of byte at address a: (a - u0) - lo
-    for (int64_t k = threadIdx.x; k < nvec; k += RT) {
-        const uintptr_t a = a0 + 16 * k;
-        const uint4 w = __ldg(reinterpret_cast<const uint4*>(a));
-        const uint8_t* wb = reinterpret_cast<const uint8_t*>(&w);
+    const int64_t lo = base - RHALO;
+    const intptr_t A = (intptr_t)U + lo;  // address of smem byte 0 (may precede U)
+    const intptr_t a0 = A & ~(intptr_t)15;
+    const int sh = (int)(A - a0);
+    const intptr_t g_lo = (intptr_t)U & ~(intptr_t)15;
+    const intptr_t g_hi = ((intptr_t)U + (intptr_t)ulen + 15) & ~(intptr_t)15;
+    constexpr int NCH = (RHALO + (int)RTILE) / 16;
+    uint4* dst = reinterpret_cast<uint4*>(sb);
+    for (int j = threadIdx.x; j < NCH; j += RT) {
+        const intptr_t c0 = a0 + 16 * (intptr_t)j, c1 = c0 + 16;
+        uint4 x = make_uint4(0, 0, 0, 0), y = make_uint4(0, 0, 0, 0);
+        if (c0 >= g_lo && c0 < g_hi) x = __ldg(reinterpret_cast<const uint4*>(c0));
+        if (sh && c1 >= g_lo && c1 < g_hi) y = __ldg(reinterpret_cast<const uint4*>(c1));
+        const uint32_t w[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+        const int ws = sh >> 2, bs = 8 * (sh & 3);
+        uint32_t o[4];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int64_t off = (int64_t)(a + j - u0);  // stream offset
-            if (off >= lo && off < hi && off >= 0 && off < (int64_t)ulen) sb[off - lo] = wb[j];
+        for (int m = 0; m < 4; ++m) {
+            uint32_t l = w[m], h = w[m + 1];
+#pragma unroll
+            for (int q = 1; q < 4; ++q)
+                if (ws == q) { l = w[m + q]; h = w[m + q + 1]; }
+            o[m] = __funnelshift_r(l, h, bs);
         }
+        dst[j] = make_uint4(o[0], o[1], o[2], o[3]);
     }
-    // padding: before the stream start -> 0x00 (a code end), past the end -> 0x80
+    __syncthreads();
     for (int k = threadIdx.x; k < RHALO + (int)RTILE; k += RT) {
         const int64_t off = lo + k;
         if (off < 0) sb[k] = 0x00;
@@ -74,22 +85,60 @@ __device__ __forceinline__ void stage_tile(const uint8_t* __restrict__ U, uint64
     }
 }
 
+// Sequential varint walk over a thread's 32 bytes held in registers, seeded
+// with the partial varint that straddles in from the 16 halo bytes. emit(v)
+// is called for every code that ends inside the thread's bytes.
+template <class F>
+__device__ __forceinline__ void thread_walk(const uint8_t* sb, int my, int64_t gbase, uint64_t ulen, bool* bad,
+                                            F&& emit) {
+    const uint4* p = reinterpret_cast<const uint4*>(sb + my - 16);
+    const uint4 h = p[0], a = p[1], b = p[2];
+    const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    // continuation bytes immediately before my first byte
+    int hlen = 0;
+    bool run = true;
+#pragma unroll
+    for (int j = 15; j >= 6; --j) {
+        const uint32_t hb = (hw[j >> 2] >> (8 * (j & 3))) & 0xffu;
+        run = run && (hb & 0x80u);
+        hlen += run ? 1 : 0;
+    }
+    uint64_t acc = 0;
+    int shift = 0;
+#pragma unroll
+    for (int j = 6; j < 16; ++j) {
+        const uint32_t hb = (hw[j >> 2] >> (8 * (j & 3))) & 0xffu;
+        if (j >= 16 - hlen) {
+            acc |= (uint64_t)(hb & 0x7fu) << shift;
+            shift += 7;
+        }
+    }
+    int crun = hlen;
+#pragma unroll
+    for (int k = 0; k < RB; ++k) {
+        const uint32_t byte = (w[k >> 2] >> (8 * (k & 3))) & 0xffu;
+        if (shift < 64) acc |= (uint64_t)(byte & 0x7fu) << shift;
+        shift += 7;
+        if (!(byte & 0x80u)) {
+            emit(acc);
+            acc = 0;
+            shift = 0;
+            crun = 0;
+        } else {
+            ++crun;
+            if (crun >= 10 && gbase + k < (int64_t)ulen) *bad = true;
+        }
+    }
+}
+
 __device__ __forceinline__ CS thread_counts(const uint8_t* sb, int my, bool* bad, int64_t base, uint64_t ulen) {
     uint32_t c = 0;
     int64_t s = 0;
-#pragma unroll 4
-    for (int k = 0; k < RB; ++k) {
-        const uint8_t b = sb[my + k];
-        if (!(b & 0x80)) {
-            s += zz_dec(varint_back(sb, my + k));
-            ++c;
-        } else if (my + k >= 9 && base + (my + k - RHALO) < (int64_t)ulen) {
-            bool all = true;
-#pragma unroll
-            for (int j = 1; j <= 9; ++j) all &= (sb[my + k - j] & 0x80) != 0;
-            *bad |= all;
-        }
-    }
+    thread_walk(sb, my, base + (my - RHALO), ulen, bad, [&](uint64_t v) {
+        ++c;
+        s += zz_dec(v);
+    });
     return CS{c, s};
 }
 
@@ -149,9 +198,9 @@ __global__ void __launch_bounds__(RT) k_dec_out(const uint8_t* __restrict__ U, u
     uint32_t li = (uint32_t)excl.cnt;     // local element index
     int64_t K = tp.sum + excl.sum;
     uint64_t kmax = 0;
-    for (int k = 0; k < RB; ++k) {
-        if (sb[my + k] & 0x80) continue;
-        K += zz_dec(varint_back(sb, my + k));
+    bool bad2 = false;
+    thread_walk(sb, my, base + (my - RHALO), ulen, &bad2, [&](uint64_t v) {
+        K += zz_dec(v);
         const uint64_t a = (uint64_t)(K < 0 ? -K : K);
         kmax = a > kmax ? a : kmax;
         if (MODE == DEC_P64) {
@@ -161,7 +210,7 @@ __global__ void __launch_bounds__(RT) k_dec_out(const uint8_t* __restrict__ U, u
             kb[li] = (int32_t)K;  // |K| < 2^30 on the fast path (checked via kmax)
         }
         ++li;
-    }
+    });
     for (int o = 16; o; o >>= 1) {
         const uint64_t b2 = __shfl_xor_sync(0xffffffffu, kmax, o);
         kmax = b2 > kmax ? b2 : kmax;
@@ -170,15 +219,28 @@ __global__ void __launch_bounds__(RT) k_dec_out(const uint8_t* __restrict__ U, u
     if (MODE == DEC_P64) return;
     __syncthreads();
     const uint32_t cnt = (uint32_t)tot.cnt;
-    for (uint32_t e = threadIdx.x; e < cnt; e += RT) {
-        const uint64_t i = e0 + e;
-        if (i >= n) break;
-        const double r = __dmul_rn((double)kb[e], bin);
-        if (MODE == DEC_VALUES) {
-            out[i] = r;
-        } else {
-            const double g = __dmul_rn((double)__ldg(&K1[__ldg(&node[i])]), bin1);
-            out[i] = __dadd_rn(g, r);
+    constexpr int UN = 8;  // independent gathers in flight per thread
+    for (uint32_t e0 = 0; e0 < cnt; e0 += RT * UN) {
+        uint32_t nd[UN];
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+            const uint32_t e = e0 + u * RT + threadIdx.x;
+            nd[u] = (MODE == DEC_RECOMPOSE && e < cnt && tp.cnt + e < n) ? __ldcs(&node[tp.cnt + e]) : 0u;
+        }
+        int32_t g1[UN];
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+            const uint32_t e = e0 + u * RT + threadIdx.x;
+            g1[u] = (MODE == DEC_RECOMPOSE && e < cnt && tp.cnt + e < n) ? __ldg(&K1[nd[u]]) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+            const uint32_t e = e0 + u * RT + threadIdx.x;
+            const uint64_t i = tp.cnt + e;
+            if (e >= cnt || i >= n) continue;
+            const double r = __dmul_rn((double)kb[e], bin);
+            if (MODE == DEC_VALUES) __stcs(&out[i], r);
+            else __stcs(&out[i], __dadd_rn(__dmul_rn((double)g1[u], bin1), r));
         }
     }
 }

@@ -32,6 +32,9 @@ void stream_plan_u32(const uint32_t* codes, uint64_t n, const StreamEncScratch& 
                      int comp, cudaStream_t st);
 void stream_plan_u64(const uint64_t* codes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl,
                      int comp, cudaStream_t st);
+// Phases 2-4 only, when the tile summaries (s.sums) were produced by a fused
+// code kernel (partition.cu).
+void stream_plan_from_sums(uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp, cudaStream_t st);
 void stream_write_u32(const uint32_t* codes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl,
                       int comp, uint8_t* dst, bool dst_off_from_ctl, cudaStream_t st);
 void stream_write_u64(const uint64_t* codes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl,

@@ -1,0 +1,265 @@
+// Partitioned compress path (nearest g): cluster means and residual lattice
+// indices with coalesced HBM traffic only.
+//
+// The reference computes x1[j] = (sum of x_i over the vertices mapped to j,
+// in ascending i) / count_j with a random scatter in vertex order
+// (interp.hpp:58-64), then x2_i = x_i - x1[m_i] with a random gather
+// (interp.hpp:145-147, 167-168). Vertex order carries no locality (the mesh
+// is permuted), so on the GPU both would be random 8-byte accesses into
+// 1 GB / 134 MB arrays. Instead, with the plan's static bucketing
+// (plan.cu: contiguous slot ranges of <= 4096 vertices, vertices of a bucket
+// in ascending vertex order):
+//   k_partition   x -> xp (bucket order) + value range / finiteness
+//                 (pipeline.hpp:31-41, mesh.hpp:58-64), one streaming pass;
+//   k_bucket      per bucket, xp staged in shared memory: ordered segment
+//                 sums (bit-exact: same additions in the same order as the
+//                 reference), x1 written once, residual lattice index
+//                 K2 = round((x - x1[m]) / bin2) per vertex (bucket order);
+//   k_resid_codes back to vertex order through dst: q_i = K2_i - K2_{i-1},
+//                 zigzag codes + the RLE tile summary in the same pass.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include "encode_dev.cuh"
+#include "plan.h"
+
+namespace umcg {
+
+namespace {
+
+constexpr int PT = 256;
+constexpr int PI = 4;  // vertices per thread in the partition pass
+
+// Forward permutation into layout E: xE[p] = x[srcE[p]] (gather inside one
+// epoch's window) + value range / finiteness over the same values.
+constexpr int GI = 8;  // items per thread (strided by PT for coalescing)
+template <class T>
+__global__ void __launch_bounds__(PT) k_gather_fwd(const T* __restrict__ x, uint64_t n,
+                                                  const uint32_t* __restrict__ srcE, double* __restrict__ xE,
+                                                  DevCtl* ctl) {
+    using BR = cub::BlockReduce<unsigned long long, PT>;
+    __shared__ typename BR::TempStorage t1, t2;
+    unsigned long long lo = ~0ull, hi = 0ull;
+    int bad = 0;
+    const uint64_t base = (uint64_t)blockIdx.x * PT * GI + threadIdx.x;
+    uint32_t s[GI];
+#pragma unroll
+    for (int k = 0; k < GI; ++k) {
+        const uint64_t p = base + (uint64_t)k * PT;
+        s[k] = p < n ? __ldcs(srcE + p) : 0u;
+    }
+    double v[GI];
+#pragma unroll
+    for (int k = 0; k < GI; ++k) {
+        const uint64_t p = base + (uint64_t)k * PT;
+        v[k] = p < n ? (double)__ldg(x + s[k]) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < GI; ++k) {
+        const uint64_t p = base + (uint64_t)k * PT;
+        if (p >= n) break;
+        if (!isfinite(v[k])) { bad = 1; continue; }
+        const unsigned long long key = dkey(v[k]);
+        lo = key < lo ? key : lo;
+        hi = key > hi ? key : hi;
+        xE[p] = v[k];
+    }
+    const unsigned long long blo = BR(t1).Reduce(lo, cub::Min());
+    const unsigned long long bhi = BR(t2).Reduce(hi, cub::Max());
+    if (threadIdx.x == 0) {
+        if (blo != ~0ull) atomicMin(&ctl->min_key, blo);
+        if (bhi != 0ull) atomicMax(&ctl->max_key, bhi);
+    }
+    if (bad) ctl->nonfinite = 1;
+}
+
+constexpr int BT = 256;
+
+__device__ __forceinline__ void flag_serial1(DevCtl* ctl) {
+    if (ctl->need_serial[1] == 0) atomicExch(&ctl->need_serial[1], 1);
+}
+
+// lattice index with the escape / regime checks of codec.hpp:305-314
+// (same as codes.cu lattice_k, 1-D limit 2^30).
+__device__ __forceinline__ int32_t resid_k(double r, double bin, double tau, DevCtl* ctl) {
+    const double K = round(__ddiv_rn(r, bin));
+    bool bad = !(fabs(K) < 1073741824.0);
+    if (!bad) bad = !(fabs(__dsub_rn(r, __dmul_rn(K, bin))) <= tau);
+    if (bad) flag_serial1(ctl);
+    return bad ? 0 : (int32_t)K;
+}
+
+// Bucket b's elements, in bucket order l = 0..m-1, live in layout E as one
+// chunk per epoch; pre[e] = first l of epoch e's chunk, cbase[e] = its
+// layout-E position.
+__device__ __forceinline__ uint32_t chunk_pos(const uint32_t* pre, const uint32_t* cbase, uint32_t E, uint32_t l) {
+    uint32_t lo = 0, hi = E;  // last e with pre[e] <= l
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (pre[mid] <= l) lo = mid; else hi = mid;
+    }
+    return cbase[lo] + (l - pre[lo]);
+}
+
+__global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, const uint32_t* __restrict__ bk,
+                                              uint64_t B, uint32_t E, const uint32_t* __restrict__ ech,
+                                              const uint16_t* __restrict__ lnode,
+                                              const uint16_t* __restrict__ lperm, const uint32_t* __restrict__ seg,
+                                              DevCtl* ctl, double* __restrict__ x1, int32_t* __restrict__ KE) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* xs = reinterpret_cast<double*>(smem);                      // [kBucketCap]
+    double* x1s = xs + kBucketCap;                                     // [kBucketNodes]
+    uint32_t* pre = reinterpret_cast<uint32_t*>(x1s + kBucketNodes);   // [E+1]
+    uint32_t* cbase = pre + (E + 1);                                   // [E]
+    uint16_t* lp = reinterpret_cast<uint16_t*>(cbase + E);             // [kBucketCap]
+    using BS = cub::BlockScan<uint32_t, BT>;
+    __shared__ typename BS::TempStorage tmp;
+    const uint32_t* bstart = bk;
+    const uint32_t* bnode = bk + B + 1;
+    const uint64_t b = blockIdx.x;
+    const uint32_t s0 = bstart[b], s1 = bstart[b + 1], m = s1 - s0;
+    const uint32_t j0 = bnode[b], j1 = bnode[b + 1];
+    const double bin = ctl->bin[1], tau = ctl->tau_c[1];
+    // chunk table of this bucket
+    uint32_t carry = 0;
+    for (uint32_t e0 = 0; e0 < E; e0 += BT) {
+        const uint32_t e = e0 + threadIdx.x;
+        uint32_t c = 0, o = 0;
+        if (e < E) {
+            o = ech[(uint64_t)e * (B + 1) + b];
+            c = ech[(uint64_t)e * (B + 1) + b + 1] - o;
+        }
+        uint32_t ex, tot;
+        BS(tmp).ExclusiveSum(c, ex, tot);
+        if (e < E) {
+            pre[e] = carry + ex;
+            cbase[e] = (uint32_t)((uint64_t)e * kEpoch + o);
+        }
+        carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) pre[E] = carry;
+    __syncthreads();
+    if (m > kBucketCap) {
+        // one heavy slot: ordered sum straight from global memory
+        if (threadIdx.x == 0) {
+            double s = 0.0;
+            for (uint32_t l = 0; l < m; ++l) s = __dadd_rn(s, xE[chunk_pos(pre, cbase, E, l)]);
+            x1s[0] = __ddiv_rn(s, (double)m);
+            x1[j0] = x1s[0];
+        }
+        __syncthreads();
+        const double mean = x1s[0];
+        for (uint32_t l = threadIdx.x; l < m; l += BT) {
+            const uint32_t q = chunk_pos(pre, cbase, E, l);
+            KE[q] = resid_k(__dsub_rn(xE[q], mean), bin, tau, ctl);
+        }
+        return;
+    }
+    for (uint32_t l = threadIdx.x; l < m; l += BT) {
+        xs[l] = xE[chunk_pos(pre, cbase, E, l)];
+        lp[l] = lperm[s0 + l];
+    }
+    __syncthreads();
+    // interpolate_to_grid (interp.hpp:58-64): 0.0 + x_a + x_b + ... in ascending vertex order
+    for (uint32_t j = threadIdx.x; j < j1 - j0; j += BT) {
+        const uint32_t k0 = seg[j0 + j] - s0, k1 = seg[j0 + j + 1] - s0;
+        double s = 0.0;
+        for (uint32_t k = k0; k < k1; ++k) s = __dadd_rn(s, xs[lp[k]]);
+        const double v = k1 > k0 ? __ddiv_rn(s, (double)(k1 - k0)) : 0.0;
+        x1s[j] = v;
+        x1[j0 + j] = v;
+    }
+    __syncthreads();
+    // compute_residuals (interp.hpp:161-170) + lattice index (codec.hpp:307-314)
+    for (uint32_t l = threadIdx.x; l < m; l += BT)
+        KE[chunk_pos(pre, cbase, E, l)] = resid_k(__dsub_rn(xs[l], x1s[lnode[s0 + l]]), bin, tau, ctl);
+}
+
+// Vertex order: q_i = K_i - K_{i-1} through dstE (gather inside an epoch
+// window), zigzag codes, RLE tile summary.
+__global__ void __launch_bounds__(ENC_THREADS) k_resid_codes(const uint32_t* __restrict__ dst,
+                                                            const int32_t* __restrict__ Kp, uint64_t n,
+                                                            uint32_t* __restrict__ codes, RleSum* __restrict__ sums) {
+    using BR = cub::BlockReduce<RleSum, ENC_THREADS>;
+    __shared__ typename BR::TempStorage tmp;
+    const uint64_t tile = blockIdx.x;
+    const uint64_t first = tile * ENC_TILE + (uint64_t)threadIdx.x * ENC_ITEMS;
+    uint32_t v[ENC_ITEMS];
+    int cnt = 0;
+    if (first < n) {
+        int64_t prev = first ? (int64_t)Kp[dst[first - 1]] : 0;
+        uint32_t d[ENC_ITEMS];
+        if (first + ENC_ITEMS <= n) {
+            const uint4 a = __ldg(reinterpret_cast<const uint4*>(dst + first));
+            const uint4 c = __ldg(reinterpret_cast<const uint4*>(dst + first) + 1);
+            d[0] = a.x; d[1] = a.y; d[2] = a.z; d[3] = a.w; d[4] = c.x; d[5] = c.y; d[6] = c.z; d[7] = c.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < ENC_ITEMS; ++k) d[k] = first + k < n ? dst[first + k] : 0;
+        }
+        int32_t K[ENC_ITEMS];
+#pragma unroll
+        for (int k = 0; k < ENC_ITEMS; ++k) K[k] = first + k < n ? __ldg(&Kp[d[k]]) : 0;
+#pragma unroll
+        for (int k = 0; k < ENC_ITEMS; ++k) {
+            if (first + k < n) {
+                v[k] = (uint32_t)zz_enc((int64_t)K[k] - prev);
+                prev = K[k];
+                cnt = k + 1;
+            } else {
+                v[k] = 0;
+            }
+        }
+        if (cnt == ENC_ITEMS) {
+            uint4* o = reinterpret_cast<uint4*>(codes + first);
+            o[0] = make_uint4(v[0], v[1], v[2], v[3]);
+            o[1] = make_uint4(v[4], v[5], v[6], v[7]);
+        } else {
+            for (int k = 0; k < cnt; ++k) codes[first + k] = v[k];
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < ENC_ITEMS; ++k) v[k] = 0;
+    }
+    const RleSum s = thread_summary(v, cnt, (uint32_t)tile);
+    const RleSum tot = BR(tmp).Reduce(s, RleComposeOp());
+    if (threadIdx.x == 0) sums[tile] = tot;
+}
+
+}  // namespace
+
+void partition_values(const void* x, int x_f32, umcg_plan* p, double* xE, DevCtl* ctl, cudaStream_t st) {
+    const uint64_t n = p->n;
+    if (!n) return;
+    const unsigned g = (unsigned)cdiv(n, (uint64_t)PT * GI);
+    const uint32_t* srcE = p->d_srcE.as<uint32_t>(1);
+    if (x_f32) k_gather_fwd<float><<<g, PT, 0, st>>>(static_cast<const float*>(x), n, srcE, xE, ctl);
+    else k_gather_fwd<double><<<g, PT, 0, st>>>(static_cast<const double*>(x), n, srcE, xE, ctl);
+    UMCG_LAUNCHED();
+}
+
+void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double* x1, int32_t* KE, cudaStream_t st) {
+    if (!p->n_buckets) return;
+    const uint32_t E = (uint32_t)p->n_epochs;
+    const size_t smem = kBucketCap * 8 + kBucketNodes * 8 + (2 * (size_t)E + 1) * 4 + kBucketCap * 2 + 16;
+    static bool configured = false;
+    if (!configured) {
+        UMCG_CUDA(cudaFuncSetAttribute(k_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        configured = true;
+    }
+    k_bucket<<<(unsigned)p->n_buckets, BT, smem, st>>>(xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E,
+                                                        p->d_ech.as<uint32_t>(1), p->d_lnode.as<uint16_t>(1),
+                                                        p->d_lperm.as<uint16_t>(1), p->d_seg.as<uint32_t>(1), ctl, x1,
+                                                        KE);
+    UMCG_LAUNCHED();
+}
+
+void resid_codes_tiles(umcg_plan* p, const int32_t* KE, uint32_t* codes, const StreamEncScratch& s, cudaStream_t st) {
+    const uint64_t T = cdiv(p->n, ENC_TILE);
+    if (!T) return;
+    k_resid_codes<<<(unsigned)T, ENC_THREADS, 0, st>>>(p->d_dstE.as<uint32_t>(1), KE, p->n, codes, s.sums);
+    UMCG_LAUNCHED();
+}
+
+}  // namespace umcg

@@ -101,6 +101,64 @@ __global__ void k_u64_to_u32(const uint64_t* __restrict__ a, uint64_t n, uint32_
     if (i < n) b[i] = (uint32_t)a[i];
 }
 
+// ---- bucketed layout -------------------------------------------------------
+__global__ void k_slot_bucket(const uint32_t* __restrict__ bnode, uint64_t B, uint32_t* __restrict__ sb) {
+    const uint64_t b = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (b >= B) return;
+    for (uint32_t j = bnode[b]; j < bnode[b + 1]; ++j) sb[j] = (uint32_t)b;
+}
+
+__global__ void k_bucket_keys(const uint32_t* __restrict__ node, uint64_t n, const uint32_t* __restrict__ sb,
+                              uint32_t* __restrict__ keys) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i < n) keys[i] = sb[node[i]];
+}
+
+__global__ void k_dst_lnode(const uint32_t* __restrict__ L, const uint32_t* __restrict__ kb, uint64_t n,
+                            const uint32_t* __restrict__ node, const uint32_t* __restrict__ bnode,
+                            uint32_t* __restrict__ dst, uint16_t* __restrict__ lnode) {
+    const uint64_t k = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (k >= n) return;
+    const uint32_t v = L[k];
+    dst[v] = (uint32_t)k;
+    lnode[k] = (uint16_t)(node[v] - bnode[kb[k]]);
+}
+
+__global__ void k_epoch_keys(const uint32_t* __restrict__ node, uint64_t n, const uint32_t* __restrict__ sb,
+                             uint64_t B, uint32_t* __restrict__ keys, uint32_t* __restrict__ cnt) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = (uint32_t)((i / kEpoch) * B + sb[node[i]]);
+    keys[i] = k;
+    atomicAdd(&cnt[k], 1u);
+}
+
+__global__ void k_dstE(const uint32_t* __restrict__ L, uint64_t n, uint32_t* __restrict__ dstE) {
+    const uint64_t p = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (p < n) dstE[L[p]] = (uint32_t)p;
+}
+
+// per-epoch exclusive scan of bucket counts (one thread per epoch; E*B small)
+__global__ void k_epoch_offsets(const uint32_t* __restrict__ cnt, uint64_t E, uint64_t B, uint32_t* __restrict__ ech) {
+    const uint64_t e = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (e >= E) return;
+    uint32_t acc = 0;
+    for (uint64_t b = 0; b < B; ++b) {
+        ech[e * (B + 1) + b] = acc;
+        acc += cnt[e * B + b];
+    }
+    ech[e * (B + 1) + B] = acc;
+}
+
+__global__ void k_lperm(const uint32_t* __restrict__ perm, uint64_t n, const uint32_t* __restrict__ dst,
+                        const uint32_t* __restrict__ node, const uint32_t* __restrict__ sb,
+                        const uint32_t* __restrict__ bstart, uint16_t* __restrict__ lperm) {
+    const uint64_t k = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (k >= n) return;
+    const uint32_t v = perm[k];
+    lperm[k] = (uint16_t)(dst[v] - bstart[sb[node[v]]]);
+}
+
 }  // namespace
 
 uint64_t mapping_digest_host(int mode, uint64_t n, const uint64_t* assign, uint64_t nv, const uint64_t* vis) {
@@ -170,6 +228,91 @@ void plan_build_segments(umcg_plan* p, cudaStream_t st) {
         p->n_visited = hv;
         p->visited_fraction = p->node_count ? (double)hv / (double)p->node_count : 0.0;
     }
+    plan_build_buckets(p, st);
+}
+
+// Bucketed layout for the partitioned compress path: greedy contiguous slot
+// ranges with <= kBucketCap vertices and <= kBucketNodes slots (a heavier
+// slot forms its own bucket). dst = stable (by vertex) sort of vertices by
+// bucket, so each bucket holds its vertices in ascending vertex order; lperm
+// maps the node-sorted order (perm) into that bucket-local order.
+void plan_build_buckets(umcg_plan* p, cudaStream_t st) {
+    const uint64_t n = p->n, ns = p->n_slots;
+    std::vector<uint32_t> seg(ns + 1);
+    UMCG_CUDA(cudaMemcpyAsync(seg.data(), p->d_seg.get(), (ns + 1) * 4, cudaMemcpyDeviceToHost, st));
+    UMCG_CUDA(cudaStreamSynchronize(st));
+    std::vector<uint32_t> bnode;
+    uint64_t j = 0;
+    while (j < ns) {
+        const uint64_t j0 = j;
+        bnode.push_back((uint32_t)j0);
+        if (seg[j0 + 1] - seg[j0] > kBucketCap) { j = j0 + 1; continue; }
+        ++j;
+        while (j < ns && j - j0 < kBucketNodes && seg[j + 1] - seg[j0] <= kBucketCap) ++j;
+    }
+    const uint64_t B = bnode.size();
+    bnode.push_back((uint32_t)ns);
+    std::vector<uint32_t> tab(2 * (B + 1));
+    for (uint64_t b = 0; b <= B; ++b) {
+        tab[b] = seg[bnode[b]];
+        tab[B + 1 + b] = bnode[b];
+    }
+    p->n_buckets = B;
+    uint32_t* dbk = p->d_bk.as<uint32_t>(tab.size());
+    UMCG_CUDA(cudaMemcpyAsync(dbk, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice, st));
+    const uint32_t* bstart = dbk;
+    const uint32_t* dbn = dbk + B + 1;
+    DevBuf dstbuf;
+    uint32_t* dst = dstbuf.as<uint32_t>(n ? n : 1);  // bucket-order position (temporary)
+    uint16_t* lnode = p->d_lnode.as<uint16_t>(n ? n : 1);
+    uint16_t* lperm = p->d_lperm.as<uint16_t>(n ? n : 1);
+    if (!n || !B) { UMCG_CUDA(cudaStreamSynchronize(st)); return; }
+    DevBuf sbuf, keys, keys_s, iota, L, scratch;
+    uint32_t* sb = sbuf.as<uint32_t>(ns);
+    k_slot_bucket<<<blocks(B), THREADS, 0, st>>>(dbn, B, sb);
+    UMCG_LAUNCHED();
+    uint32_t* kk = keys.as<uint32_t>(n);
+    uint32_t* ks = keys_s.as<uint32_t>(n);
+    uint32_t* io = iota.as<uint32_t>(n);
+    uint32_t* Lv = L.as<uint32_t>(n);
+    k_bucket_keys<<<blocks(n), THREADS, 0, st>>>(p->d_node.as<uint32_t>(1), n, sb, kk);
+    UMCG_LAUNCHED();
+    k_iota<<<blocks(n), THREADS, 0, st>>>(io, n);
+    UMCG_LAUNCHED();
+    int end_bit = 1;
+    while (end_bit < 32 && (1ull << end_bit) < B) ++end_bit;
+    size_t tb = 0;
+    UMCG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kk, ks, io, Lv, (int)n, 0, end_bit, st));
+    void* t = scratch.reserve(tb);
+    UMCG_CUDA(cub::DeviceRadixSort::SortPairs(t, tb, kk, ks, io, Lv, (int)n, 0, end_bit, st));
+    k_dst_lnode<<<blocks(n), THREADS, 0, st>>>(Lv, ks, n, p->d_node.as<uint32_t>(1), dbn, dst, lnode);
+    UMCG_LAUNCHED();
+    k_lperm<<<blocks(n), THREADS, 0, st>>>(p->d_perm.as<uint32_t>(1), n, dst, p->d_node.as<uint32_t>(1), sb,
+                                           bstart, lperm);
+    UMCG_LAUNCHED();
+    // layout E: stable sort by (epoch, bucket)
+    const uint64_t E = cdiv(n, kEpoch);
+    if (E > kMaxEpochs) fail(UMCG_INVALID_ARGUMENT, "too many vertices for layout E");
+    p->n_epochs = E;
+    DevBuf ecnt;
+    uint32_t* ec = ecnt.as<uint32_t>(E * B + 1);
+    UMCG_CUDA(cudaMemsetAsync(ec, 0, (E * B + 1) * 4, st));
+    k_epoch_keys<<<blocks(n), THREADS, 0, st>>>(p->d_node.as<uint32_t>(1), n, sb, B, kk, ec);
+    UMCG_LAUNCHED();
+    k_iota<<<blocks(n), THREADS, 0, st>>>(io, n);
+    UMCG_LAUNCHED();
+    uint32_t* srcE = p->d_srcE.as<uint32_t>(n);
+    end_bit = 1;
+    while (end_bit < 32 && (1ull << end_bit) < E * B) ++end_bit;
+    tb = 0;
+    UMCG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kk, ks, io, srcE, (int)n, 0, end_bit, st));
+    t = scratch.reserve(std::max(tb, scratch.capacity()));
+    UMCG_CUDA(cub::DeviceRadixSort::SortPairs(t, tb, kk, ks, io, srcE, (int)n, 0, end_bit, st));
+    k_dstE<<<blocks(n), THREADS, 0, st>>>(srcE, n, p->d_dstE.as<uint32_t>(n));
+    UMCG_LAUNCHED();
+    k_epoch_offsets<<<blocks(E), THREADS, 0, st>>>(ec, E, B, p->d_ech.as<uint32_t>(E * (B + 1)));
+    UMCG_LAUNCHED();
+    UMCG_CUDA(cudaStreamSynchronize(st));
 }
 
 static void upload_grid(umcg_plan* p, const umcg_grid_desc* g) {

@@ -27,6 +27,21 @@ struct umcg_plan {
     umcg::DevBuf d_axis_off; // u64 [dim]
     umcg::DevBuf d_coords;   // f64 [n*dim] (multilinear g), optional
     bool has_coords = false;
+    // bucketed layout for the partitioned compress path (partition.cu):
+    // buckets are contiguous slot ranges holding <= kBucketCap vertices
+    // (a heavier slot gets a bucket of its own).
+    // Physical layout "E": epochs of kEpoch consecutive vertices; inside an
+    // epoch, vertices grouped by bucket (ascending vertex within a group).
+    // Both directions of the permutation are then gathers inside one
+    // epoch's window (L2 resident).
+    uint64_t n_buckets = 0;
+    uint64_t n_epochs = 0;
+    umcg::DevBuf d_srcE;     // u32 [n]    vertex at layout-E position p
+    umcg::DevBuf d_dstE;     // u32 [n]    layout-E position of vertex i
+    umcg::DevBuf d_ech;      // u32 [E*(B+1)] offset of bucket b inside epoch e's block
+    umcg::DevBuf d_lnode;    // u16 [n]    bucket-local slot of bucket-order element
+    umcg::DevBuf d_lperm;    // u16 [n]    bucket-local element of node-sorted position
+    umcg::DevBuf d_bk;       // u32 [2*(B+1)] bucket start (vertex) and first slot
     // workspace (serialized by mu)
     std::mutex mu;
     umcg::DevBuf ctl, x1, codes1, codes2, kbuf, enc1, enc2, hdr, scratch_a, scratch_b, scratch_c,
@@ -44,8 +59,14 @@ uint64_t mapping_digest_host(int mode, uint64_t n, const uint64_t* assign, uint6
 uint64_t mapping_digest_host32(int mode, uint64_t n, const uint32_t* assign, uint64_t n_visited,
                                const uint64_t* visited);
 
-// Build perm / seg_off from d_node on the plan (stable radix sort by slot).
+// Build perm / seg_off from d_node on the plan (stable radix sort by slot),
+// then the bucketed layout (plan_build_buckets).
 void plan_build_segments(umcg_plan* p, cudaStream_t st);
+constexpr uint32_t kBucketCap = 4096;   // vertices per bucket (smem staging)
+constexpr uint64_t kEpoch = 1ull << 21;  // vertices per epoch of layout E
+constexpr uint32_t kMaxEpochs = 2048;    // k_bucket stages per-epoch chunk prefixes
+constexpr uint32_t kBucketNodes = 1016; // slots per bucket (48 KB static smem in k_bucket)
+void plan_build_buckets(umcg_plan* p, cudaStream_t st);
 
 // Component payload decode (codec.hpp:364-441) of a payload in device memory
 // into d_out [n]; header already parsed. Throws the reference's error kinds.
@@ -61,4 +82,13 @@ struct CompHeader {
 void decode_component(umcg_plan* ws, const CompHeader& h, const uint8_t* d_payload, double* d_out,
                       cudaStream_t st);
 
+}  // namespace umcg
+
+namespace umcg {
+// partition.cu: the partitioned (bucketed) compress path for nearest g.
+void partition_values(const void* x, int x_f32, umcg_plan* p, double* xp, DevCtl* ctl, cudaStream_t st);
+void bucket_means_residuals(umcg_plan* p, const double* xp, DevCtl* ctl, double* x1, int32_t* Kp,
+                            cudaStream_t st);
+void resid_codes_tiles(umcg_plan* p, const int32_t* Kp, uint32_t* codes, const StreamEncScratch& s,
+                       cudaStream_t st);
 }  // namespace umcg
