@@ -112,6 +112,25 @@ __global__ void __launch_bounds__(THREADS) k_stencil_nd(const int32_t* __restric
     codes[i] = (uint32_t)zz_enc((int64_t)K[i] - pred);
 }
 
+// Integer Lorenzo stencil for D = 2 / 3 with the grid laid out by axis:
+// blockIdx.x spans the fastest axis, blockIdx.y / z the others (no 64-bit
+// division per element). Missing neighbours (index -1) contribute 0, which
+// is exactly the reference's skipped masks (codec.hpp:70-75).
+__global__ void __launch_bounds__(THREADS) k_stencil_3d(const int32_t* __restrict__ K, uint64_t d0, uint64_t d1,
+                                                       uint64_t d2, uint32_t* __restrict__ codes) {
+    const uint64_t k = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (k >= d2) return;
+    const uint64_t j = blockIdx.y, i = blockIdx.z;
+    const uint64_t s1 = d2, s0 = d1 * d2;
+    const uint64_t c = i * s0 + j * s1 + k;
+    auto at = [&](bool ok, uint64_t off) -> int64_t { return ok ? (int64_t)K[c - off] : 0; };
+    const bool ai = i > 0, aj = j > 0, ak = k > 0;
+    const int64_t pred = at(ak, 1) + at(aj, s1) + at(ai, s0) - at(aj && ak, s1 + 1) - at(ai && ak, s0 + 1) -
+                         at(ai && aj, s0 + s1) + at(ai && aj && ak, s0 + s1 + 1);
+    codes[c] = (uint32_t)zz_enc((int64_t)K[c] - pred);
+    (void)d0;
+}
+
 // ---- lossless XOR codes (codec.hpp:276-294) --------------------------------
 __device__ __forceinline__ double lorenzo_fp(const double* __restrict__ v, uint64_t i, const NdShape& sh) {
     uint64_t idx[8];
@@ -514,7 +533,14 @@ void codes_lossy_values(const double* v, uint64_t n, int pred, const NdShape& sh
     if (pred == 2 && sh.D > 1) {
         k_lattice_nd<<<blocks(n), THREADS, 0, st>>>(v, n, sh.D, ctl, comp, kbuf);
         UMCG_LAUNCHED();
-        k_stencil_nd<<<blocks(n), THREADS, 0, st>>>(kbuf, n, sh, codes);
+        if ((sh.D == 2 || sh.D == 3) && sh.dims[0] < 65536 && (sh.D == 2 || sh.dims[1] < 65536)) {
+            const uint64_t d0 = sh.D == 3 ? sh.dims[0] : 1, d1 = sh.D == 3 ? sh.dims[1] : sh.dims[0];
+            const uint64_t d2 = sh.dims[sh.D - 1];
+            dim3 g((unsigned)cdiv(d2, THREADS), (unsigned)d1, (unsigned)d0);
+            k_stencil_3d<<<g, THREADS, 0, st>>>(kbuf, d0, d1, d2, codes);
+        } else {
+            k_stencil_nd<<<blocks(n), THREADS, 0, st>>>(kbuf, n, sh, codes);
+        }
         UMCG_LAUNCHED();
     } else {
         // lorenzo_nd over a single axis is lorenzo_1d

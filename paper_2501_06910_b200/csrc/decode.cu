@@ -58,12 +58,13 @@ __device__ __forceinline__ void stage_tile(const uint8_t* __restrict__ U, uint64
     const intptr_t g_lo = (intptr_t)U & ~(intptr_t)15;
     const intptr_t g_hi = ((intptr_t)U + (intptr_t)ulen + 15) & ~(intptr_t)15;
     constexpr int NCH = (RHALO + (int)RTILE) / 16;
+    const uint64_t pol = l2_evict_first();
     uint4* dst = reinterpret_cast<uint4*>(sb);
     for (int j = threadIdx.x; j < NCH; j += RT) {
         const intptr_t c0 = a0 + 16 * (intptr_t)j, c1 = c0 + 16;
         uint4 x = make_uint4(0, 0, 0, 0), y = make_uint4(0, 0, 0, 0);
-        if (c0 >= g_lo && c0 < g_hi) x = __ldg(reinterpret_cast<const uint4*>(c0));
-        if (sh && c1 >= g_lo && c1 < g_hi) y = __ldg(reinterpret_cast<const uint4*>(c1));
+        if (c0 >= g_lo && c0 < g_hi) x = ld_v4_hint(reinterpret_cast<const void*>(c0), pol);
+        if (sh && c1 >= g_lo && c1 < g_hi) y = ld_v4_hint(reinterpret_cast<const void*>(c1), pol);
         const uint32_t w[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
         const int ws = sh >> 2, bs = 8 * (sh & 3);
         uint32_t o[4];
@@ -78,10 +79,12 @@ __device__ __forceinline__ void stage_tile(const uint8_t* __restrict__ U, uint64
         dst[j] = make_uint4(o[0], o[1], o[2], o[3]);
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < RHALO + (int)RTILE; k += RT) {
-        const int64_t off = lo + k;
-        if (off < 0) sb[k] = 0x00;
-        else if (off >= (int64_t)ulen) sb[k] = 0x80;
+    if (lo < 0 || base + (int64_t)RTILE > (int64_t)ulen) {  // first / last tile only
+        for (int k = threadIdx.x; k < RHALO + (int)RTILE; k += RT) {
+            const int64_t off = lo + k;
+            if (off < 0) sb[k] = 0x00;
+            else if (off >= (int64_t)ulen) sb[k] = 0x80;
+        }
     }
 }
 
@@ -220,18 +223,19 @@ __global__ void __launch_bounds__(RT) k_dec_out(const uint8_t* __restrict__ U, u
     __syncthreads();
     const uint32_t cnt = (uint32_t)tot.cnt;
     constexpr int UN = 8;  // independent gathers in flight per thread
+    const uint64_t pf = l2_evict_first(), pl = l2_evict_last();
     for (uint32_t e0 = 0; e0 < cnt; e0 += RT * UN) {
         uint32_t nd[UN];
 #pragma unroll
         for (int u = 0; u < UN; ++u) {
             const uint32_t e = e0 + u * RT + threadIdx.x;
-            nd[u] = (MODE == DEC_RECOMPOSE && e < cnt && tp.cnt + e < n) ? __ldcs(&node[tp.cnt + e]) : 0u;
+            nd[u] = (MODE == DEC_RECOMPOSE && e < cnt && tp.cnt + e < n) ? ld_u32_hint(&node[tp.cnt + e], pf) : 0u;
         }
         int32_t g1[UN];
 #pragma unroll
         for (int u = 0; u < UN; ++u) {
             const uint32_t e = e0 + u * RT + threadIdx.x;
-            g1[u] = (MODE == DEC_RECOMPOSE && e < cnt && tp.cnt + e < n) ? __ldg(&K1[nd[u]]) : 0;
+            g1[u] = (MODE == DEC_RECOMPOSE && e < cnt && tp.cnt + e < n) ? ld_s32_hint(&K1[nd[u]], pl) : 0;
         }
 #pragma unroll
         for (int u = 0; u < UN; ++u) {
@@ -239,8 +243,8 @@ __global__ void __launch_bounds__(RT) k_dec_out(const uint8_t* __restrict__ U, u
             const uint64_t i = tp.cnt + e;
             if (e >= cnt || i >= n) continue;
             const double r = __dmul_rn((double)kb[e], bin);
-            if (MODE == DEC_VALUES) __stcs(&out[i], r);
-            else __stcs(&out[i], __dadd_rn(__dmul_rn((double)g1[u], bin1), r));
+            if (MODE == DEC_VALUES) st_f64_hint(&out[i], r, pf);
+            else st_f64_hint(&out[i], __dadd_rn(__dmul_rn((double)g1[u], bin1), r), pf);
         }
     }
 }

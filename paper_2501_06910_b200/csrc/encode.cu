@@ -194,116 +194,128 @@ __device__ __forceinline__ void copy_out(const uint8_t* out, uint64_t len, uint8
     if (t0 + threadIdx.x < len) d[t0 + threadIdx.x] = out[t0 + threadIdx.x];
 }
 
+// Byte writer into the staging buffer (no bounds checks: the tile's output
+// fits CAP by construction). Returns the varint length.
+template <class T>
+__device__ __forceinline__ uint32_t put_varint(uint8_t* o, T v) {
+    uint64_t u = (uint64_t)v;
+    uint32_t k = 0;
+    while (u >= 0x80) {
+        o[k++] = (uint8_t)u | 0x80;
+        u >>= 7;
+    }
+    o[k++] = (uint8_t)u;
+    return k;
+}
+
+// Staged bytes out[ao, ao+len) -> d[0, len) where ao = d & 15: 16-byte
+// stores for the aligned middle, bytes at the two ends.
+__device__ __forceinline__ void copy_out16(const uint8_t* out, uint32_t ao, uint32_t len, uint8_t* d) {
+    uint8_t* g = d - ao;  // 16-byte aligned
+    const uint32_t end = ao + len;
+    const uint32_t w0 = (ao + 15) / 16, w1 = end / 16;  // full words [w0, w1)
+    if (w0 >= w1) {
+        for (uint32_t k = ao + threadIdx.x; k < end; k += ENC_THREADS) g[k] = out[k];
+        return;
+    }
+    for (uint32_t k = ao + threadIdx.x; k < 16 * w0; k += ENC_THREADS) g[k] = out[k];
+    for (uint32_t k = 16 * w1 + threadIdx.x; k < end; k += ENC_THREADS) g[k] = out[k];
+    const uint4* s4 = reinterpret_cast<const uint4*>(out);
+    uint4* g4 = reinterpret_cast<uint4*>(g);
+    for (uint32_t w = w0 + threadIdx.x; w < w1; w += ENC_THREADS) g4[w] = s4[w];
+}
+
 template <class T>
 __global__ void __launch_bounds__(ENC_THREADS) k_rle_write_fast(const T* __restrict__ codes, uint64_t n,
-                                                           const RleState* __restrict__ states,
-                                                           const RleSum* __restrict__ sums,
-                                                           const uint64_t* __restrict__ lit_total,
-                                                           const DevCtl* __restrict__ ctl, int comp,
-                                                           uint8_t* __restrict__ dst, int off_from_ctl) {
-    constexpr uint64_t CAP = ENC_TILE * (sizeof(T) == 8 ? 10 : 5) + 64;
-    using BS = cub::BlockScan<RleSum, ENC_THREADS>;
+                                                               const RleState* __restrict__ states,
+                                                               const RleSum* __restrict__ sums,
+                                                               const uint64_t* __restrict__ lit_total,
+                                                               const DevCtl* __restrict__ ctl, int comp,
+                                                               uint8_t* __restrict__ dst, int off_from_ctl) {
+    constexpr uint32_t CAP = ENC_TILE * (sizeof(T) == 8 ? 10 : 5) + 96;
     using BS32 = cub::BlockScan<uint32_t, ENC_THREADS>;
-    __shared__ union {
-        typename BS::TempStorage rle;
-        typename BS32::TempStorage u32;
-    } tmp;
-    __shared__ uint64_t closeTot[ENC_THREADS + 1];
+    __shared__ typename BS32::TempStorage tmp;
     __shared__ __align__(16) uint8_t out[CAP];
 
     const uint64_t tile = blockIdx.x;
-    {
-        const RleSum S0 = sums[tile];
-        if (S0.has_int() || S0.allzero()) return;  // general writer (or nothing to write)
-    }
+    const RleSum S = sums[tile];
+    if (S.has_int() || S.allzero()) return;  // general writer (or nothing to write)
     const uint64_t T_ = (n + ENC_TILE - 1) / ENC_TILE;
     const bool last = tile == T_ - 1;
     const RleState entry = states[tile];
-    const RleSum S = sums[tile];
     const uint64_t P0 = state_pos(entry, lit_total);
     const uint64_t P1 = last ? ctl->stream_len[comp] : state_pos(states[tile + 1], lit_total);
-    const uint64_t len = P1 - P0;
-    if (len == 0) return;  // all-zero tile: its zeros stay pending
+    const uint32_t len = (uint32_t)(P1 - P0);
     uint8_t* d = dst + (off_from_ctl ? ctl->stream_off[comp] : 0) + P0;
+    const uint32_t ao = (uint32_t)((uintptr_t)d & 15);
+    uint8_t* o = out + ao - 0;  // o[pos - P0] is the staged byte of stream position pos
 
     const uint64_t first = tile * ENC_TILE + (uint64_t)threadIdx.x * ENC_ITEMS;
     T v[ENC_ITEMS];
     const int cnt = load_items(codes, n, first, v);
 
-    {
-        // ---- fast path: the core is one literal segment ----
-        const uint64_t tile_cnt = min((uint64_t)ENC_TILE, n - tile * ENC_TILE);
-        const uint64_t core_lo = S.lz, core_hi = tile_cnt - S.tz;  // [lo, hi)
-        uint32_t w = 0;
-        const uint64_t r0 = (uint64_t)threadIdx.x * ENC_ITEMS;
+    // the core [lz, tile_cnt - tz) is one literal segment
+    const uint32_t tile_cnt = (uint32_t)min((uint64_t)ENC_TILE, n - tile * ENC_TILE);
+    const uint32_t core_lo = (uint32_t)S.lz, core_hi = tile_cnt - (uint32_t)S.tz;
+    const uint32_t r0 = threadIdx.x * ENC_ITEMS;
+    uint32_t w = 0;
 #pragma unroll
-        for (int k = 0; k < ENC_ITEMS; ++k) {
-            const uint64_t r = r0 + k;
-            if (k < cnt && r >= core_lo && r < core_hi) w += v[k] == 0 ? 1u : vlen64((uint64_t)v[k]);
-        }
-        uint32_t off, core_total;
-        BS32(tmp.u32).ExclusiveSum(w, off, core_total);
-        // head: pending zeros from before + this tile's leading zeros
-        const uint64_t J0 = entry.Zp + S.lz;
-        uint64_t data_base, zero_pos = 0, zpos = 0, lpos = 0, totn = 0;
-        bool ztok = false, hdr = false;
-        if (J0 >= kMinZeroRun) {
-            zpos = entry.C + (entry.has ? lit_size(entry.Lb) : 0);
-            ztok = true;
-            lpos = zpos + z_size(J0);
-            hdr = true;
-            totn = lit_total[tile];
-            data_base = lpos + 1 + vlen64(totn);
-        } else if (entry.has) {
-            zero_pos = entry.C + 1 + vlen64(lit_total[entry.origin]) + entry.Lb;
-            data_base = zero_pos + J0;
-        } else {
-            lpos = entry.C;
-            hdr = true;
-            totn = lit_total[tile];
-            zero_pos = lpos + 1 + vlen64(totn);
-            data_base = zero_pos + J0;
-        }
-        if (threadIdx.x == 0) {
-            if (ztok) {
-                out[zpos - P0] = 0x00;
-                write_varint(out, zpos + 1, P0, CAP, J0);
-            }
-            if (hdr) {
-                out[lpos - P0] = 0x01;
-                write_varint(out, lpos + 1, P0, CAP, totn);
-            }
-            if (!ztok)
-                for (uint64_t k = 0; k < J0; ++k) out[zero_pos - P0 + k] = 0;
-            if (last) {  // rle_finish: trailing zeros close the stream
-                const uint64_t core_end = data_base + core_total;
-                if (S.tz >= kMinZeroRun) {
-                    out[core_end - P0] = 0x00;
-                    write_varint(out, core_end + 1, P0, CAP, S.tz);
-                } else {
-                    for (uint64_t k = 0; k < S.tz; ++k) out[core_end - P0 + k] = 0;
-                }
-            }
-        }
-        uint64_t pos = data_base + off;
-#pragma unroll
-        for (int k = 0; k < ENC_ITEMS; ++k) {
-            const uint64_t r = r0 + k;
-            if (k < cnt && r >= core_lo && r < core_hi) {
-                if (v[k] == 0) {
-                    out[pos - P0] = 0;
-                    pos += 1;
-                } else {
-                    write_varint(out, pos, P0, CAP, v[k]);
-                    pos += vlen64((uint64_t)v[k]);
-                }
-            }
-        }
-        __syncthreads();
-        copy_out(out, len, d);
-        return;
+    for (int k = 0; k < ENC_ITEMS; ++k) {
+        const uint32_t r = r0 + k;
+        if (k < cnt && r >= core_lo && r < core_hi) w += v[k] == 0 ? 1u : vlen64((uint64_t)v[k]);
     }
-
+    uint32_t off, core_total;
+    BS32(tmp).ExclusiveSum(w, off, core_total);
+    // head: pending zeros from before + this tile's leading zeros
+    const uint64_t J0 = entry.Zp + S.lz;
+    uint64_t data_base, zero_pos = 0, zpos = 0, lpos = 0, totn = 0;
+    bool ztok = false, hdr = false;
+    if (J0 >= kMinZeroRun) {
+        zpos = entry.C + (entry.has ? lit_size(entry.Lb) : 0);
+        ztok = true;
+        lpos = zpos + z_size(J0);
+        hdr = true;
+        totn = lit_total[tile];
+        data_base = lpos + 1 + vlen64(totn);
+    } else if (entry.has) {
+        zero_pos = entry.C + 1 + vlen64(lit_total[entry.origin]) + entry.Lb;
+        data_base = zero_pos + J0;
+    } else {
+        lpos = entry.C;
+        hdr = true;
+        totn = lit_total[tile];
+        zero_pos = lpos + 1 + vlen64(totn);
+        data_base = zero_pos + J0;
+    }
+    if (threadIdx.x == 0) {
+        if (ztok) {
+            o[zpos - P0] = 0x00;
+            put_varint(o + (zpos + 1 - P0), J0);
+        }
+        if (hdr) {
+            o[lpos - P0] = 0x01;
+            put_varint(o + (lpos + 1 - P0), totn);
+        }
+        if (!ztok)
+            for (uint32_t k = 0; k < (uint32_t)J0; ++k) o[zero_pos - P0 + k] = 0;
+        if (last) {  // rle_finish: trailing zeros close the stream
+            const uint32_t ce = (uint32_t)(data_base - P0) + core_total;
+            if (S.tz >= kMinZeroRun) {
+                o[ce] = 0x00;
+                put_varint(o + ce + 1, S.tz);
+            } else {
+                for (uint32_t k = 0; k < (uint32_t)S.tz; ++k) o[ce + k] = 0;
+            }
+        }
+    }
+    uint32_t pos = (uint32_t)(data_base - P0) + off;
+#pragma unroll
+    for (int k = 0; k < ENC_ITEMS; ++k) {
+        const uint32_t r = r0 + k;
+        if (k < cnt && r >= core_lo && r < core_hi) pos += put_varint(o + pos, v[k]);
+    }
+    __syncthreads();
+    copy_out16(out, ao, len, d);
 }
 
 template <class T>

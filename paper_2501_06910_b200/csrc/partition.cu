@@ -90,17 +90,8 @@ __device__ __forceinline__ int32_t resid_k(double r, double bin, double tau, Dev
 }
 
 // Bucket b's elements, in bucket order l = 0..m-1, live in layout E as one
-// chunk per epoch; pre[e] = first l of epoch e's chunk, cbase[e] = its
-// layout-E position.
-__device__ __forceinline__ uint32_t chunk_pos(const uint32_t* pre, const uint32_t* cbase, uint32_t E, uint32_t l) {
-    uint32_t lo = 0, hi = E;  // last e with pre[e] <= l
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (pre[mid] <= l) lo = mid; else hi = mid;
-    }
-    return cbase[lo] + (l - pre[lo]);
-}
-
+// chunk per epoch: pre[e] = first l of epoch e's chunk, cbase[e] = its
+// layout-E position. Each warp moves whole chunks (coalesced).
 __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, const uint32_t* __restrict__ bk,
                                               uint64_t B, uint32_t E, const uint32_t* __restrict__ ech,
                                               const uint16_t* __restrict__ lnode,
@@ -111,7 +102,6 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
     double* x1s = xs + kBucketCap;                                     // [kBucketNodes]
     uint32_t* pre = reinterpret_cast<uint32_t*>(x1s + kBucketNodes);   // [E+1]
     uint32_t* cbase = pre + (E + 1);                                   // [E]
-    uint16_t* lp = reinterpret_cast<uint16_t*>(cbase + E);             // [kBucketCap]
     using BS = cub::BlockScan<uint32_t, BT>;
     __shared__ typename BS::TempStorage tmp;
     const uint32_t* bstart = bk;
@@ -120,14 +110,14 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
     const uint32_t s0 = bstart[b], s1 = bstart[b + 1], m = s1 - s0;
     const uint32_t j0 = bnode[b], j1 = bnode[b + 1];
     const double bin = ctl->bin[1], tau = ctl->tau_c[1];
-    // chunk table of this bucket
+    // chunk table of this bucket: one chunk per epoch
     uint32_t carry = 0;
     for (uint32_t e0 = 0; e0 < E; e0 += BT) {
         const uint32_t e = e0 + threadIdx.x;
         uint32_t c = 0, o = 0;
         if (e < E) {
-            o = ech[(uint64_t)e * (B + 1) + b];
-            c = ech[(uint64_t)e * (B + 1) + b + 1] - o;
+            o = __ldg(&ech[(uint64_t)e * (B + 1) + b]);
+            c = __ldg(&ech[(uint64_t)e * (B + 1) + b + 1]) - o;
         }
         uint32_t ex, tot;
         BS(tmp).ExclusiveSum(c, ex, tot);
@@ -140,40 +130,48 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
     }
     if (threadIdx.x == 0) pre[E] = carry;
     __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int NW = BT / 32;
     if (m > kBucketCap) {
         // one heavy slot: ordered sum straight from global memory
         if (threadIdx.x == 0) {
             double s = 0.0;
-            for (uint32_t l = 0; l < m; ++l) s = __dadd_rn(s, xE[chunk_pos(pre, cbase, E, l)]);
+            for (uint32_t e = 0; e < E; ++e)
+                for (uint32_t l = pre[e]; l < pre[e + 1]; ++l) s = __dadd_rn(s, xE[cbase[e] + (l - pre[e])]);
             x1s[0] = __ddiv_rn(s, (double)m);
             x1[j0] = x1s[0];
         }
         __syncthreads();
         const double mean = x1s[0];
-        for (uint32_t l = threadIdx.x; l < m; l += BT) {
-            const uint32_t q = chunk_pos(pre, cbase, E, l);
-            KE[q] = resid_k(__dsub_rn(xE[q], mean), bin, tau, ctl);
-        }
+        for (uint32_t e = warp; e < E; e += NW)
+            for (uint32_t l = pre[e] + lane; l < pre[e + 1]; l += 32) {
+                const uint32_t q = cbase[e] + (l - pre[e]);
+                KE[q] = resid_k(__dsub_rn(xE[q], mean), bin, tau, ctl);
+            }
         return;
     }
-    for (uint32_t l = threadIdx.x; l < m; l += BT) {
-        xs[l] = xE[chunk_pos(pre, cbase, E, l)];
-        lp[l] = lperm[s0 + l];
+    // stage the bucket (chunk per epoch, one warp per chunk: coalesced)
+    for (uint32_t e = warp; e < E; e += NW) {
+        const uint32_t l0 = pre[e], l1 = pre[e + 1], cb = cbase[e];
+        for (uint32_t l = l0 + lane; l < l1; l += 32) xs[l] = __ldcs(&xE[cb + (l - l0)]);
     }
     __syncthreads();
     // interpolate_to_grid (interp.hpp:58-64): 0.0 + x_a + x_b + ... in ascending vertex order
     for (uint32_t j = threadIdx.x; j < j1 - j0; j += BT) {
         const uint32_t k0 = seg[j0 + j] - s0, k1 = seg[j0 + j + 1] - s0;
         double s = 0.0;
-        for (uint32_t k = k0; k < k1; ++k) s = __dadd_rn(s, xs[lp[k]]);
+        for (uint32_t k = k0; k < k1; ++k) s = __dadd_rn(s, xs[__ldg(&lperm[s0 + k])]);
         const double v = k1 > k0 ? __ddiv_rn(s, (double)(k1 - k0)) : 0.0;
         x1s[j] = v;
         x1[j0 + j] = v;
     }
     __syncthreads();
     // compute_residuals (interp.hpp:161-170) + lattice index (codec.hpp:307-314)
-    for (uint32_t l = threadIdx.x; l < m; l += BT)
-        KE[chunk_pos(pre, cbase, E, l)] = resid_k(__dsub_rn(xs[l], x1s[lnode[s0 + l]]), bin, tau, ctl);
+    for (uint32_t e = warp; e < E; e += NW) {
+        const uint32_t l0 = pre[e], l1 = pre[e + 1], cb = cbase[e];
+        for (uint32_t l = l0 + lane; l < l1; l += 32)
+            KE[cb + (l - l0)] = resid_k(__dsub_rn(xs[l], x1s[__ldg(&lnode[s0 + l])]), bin, tau, ctl);
+    }
 }
 
 // Vertex order: q_i = K_i - K_{i-1} through dstE (gather inside an epoch
@@ -242,7 +240,7 @@ void partition_values(const void* x, int x_f32, umcg_plan* p, double* xE, DevCtl
 void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double* x1, int32_t* KE, cudaStream_t st) {
     if (!p->n_buckets) return;
     const uint32_t E = (uint32_t)p->n_epochs;
-    const size_t smem = kBucketCap * 8 + kBucketNodes * 8 + (2 * (size_t)E + 1) * 4 + kBucketCap * 2 + 16;
+    const size_t smem = kBucketCap * 8 + kBucketNodes * 8 + (2 * (size_t)E + 1) * 4 + 16;
     static bool configured = false;
     if (!configured) {
         UMCG_CUDA(cudaFuncSetAttribute(k_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
