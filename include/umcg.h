@@ -192,8 +192,11 @@ umcg_status umcg_rle_decompress(const uint8_t* d_in, uint64_t n, uint8_t* d_out,
 umcg_status umcg_gen_config(int config, uint64_t lattice, uint64_t seed, double* d_coords,
                             void* d_values, uint64_t* n_out, void* stream);
 
-/* Instrumentation: number of kernels this library launched since load. */
+/* Instrumentation: number of kernels this library launched since load, and
+ * how many times a component took the exact one-thread replica of the
+ * reference recurrence (escapes, non-lattice regimes; 0 on normal data). */
 uint64_t umcg_kernel_launches(void);
+uint64_t umcg_serial_fallbacks(void);
 const char* umcg_last_error(void);
 const char* umcg_version(void);
 

@@ -38,7 +38,7 @@ EXPORTED = [
     "umcg_plan_export", "umcg_compress_bound", "umcg_compress", "umcg_compress_batch",
     "umcg_decompress", "umcg_compress_host", "umcg_decompress_host", "umcg_encode_bound",
     "umcg_encode", "umcg_decode", "umcg_rle_compress", "umcg_rle_decompress", "umcg_gen_config",
-    "umcg_kernel_launches", "umcg_last_error", "umcg_version",
+    "umcg_kernel_launches", "umcg_serial_fallbacks", "umcg_last_error", "umcg_version",
 ]
 
 
@@ -93,6 +93,7 @@ def lib():
     L.umcg_last_error.restype = C.c_char_p
     L.umcg_version.restype = C.c_char_p
     L.umcg_kernel_launches.restype = C.c_uint64
+    L.umcg_serial_fallbacks.restype = C.c_uint64
     L.umcg_encode_bound.restype = C.c_uint64
     L.umcg_encode_bound.argtypes = [C.c_uint64, C.c_int]
     L.umcg_plan_create.argtypes = [C.POINTER(GridDesc), C.POINTER(MappingDesc), C.c_int, f64p,
@@ -124,6 +125,11 @@ def _check(rc: int):
 
 def kernel_launches() -> int:
     return int(lib().umcg_kernel_launches())
+
+
+def serial_fallbacks() -> int:
+    """Times a component used the one-thread exact replica of the reference loop."""
+    return int(lib().umcg_serial_fallbacks())
 
 
 def _ptr(a, t):

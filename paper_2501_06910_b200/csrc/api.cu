@@ -12,6 +12,7 @@
 namespace umcg {
 
 std::atomic<uint64_t> g_launches{0};
+std::atomic<uint64_t> g_serial_fallbacks{0};
 static thread_local std::string g_last_error;
 
 umcg_plan* plan_create_host(const umcg_grid_desc*, const umcg_mapping_desc*, int, const double*);
@@ -494,15 +495,15 @@ void decode_component(umcg_plan* p, const CompHeader& h, const uint8_t* d_payloa
         if (pred == 1) {
             dec_fused(DEC_VALUES, U, ulen, h.n, status, ctl, nullptr, nullptr, 0.0, bin, d_out, nullptr, st);
             const DevCtl hc = check_fused(p, ctl, U, ulen, h.n, st);
-            if ((double)hc.max_abs_k[1] < k_lim(1, 1)) return;
+            if (!hc.aux[7] && (double)hc.max_abs_k[1] < k_lim(1, 1)) return;
         } else {
             int64_t* P = p->kbuf.as<int64_t>(2 * (h.n ? h.n : 1));
             int32_t* K32 = p->dx1.as<int32_t>(h.n ? h.n : 1);
             dec_fused(DEC_P64, U, ulen, h.n, status, ctl, nullptr, nullptr, 0.0, bin, nullptr, P, st);
-            check_fused(p, ctl, U, ulen, h.n, st);
+            const bool wide = check_fused(p, ctl, U, ulen, h.n, st).aux[7] != 0;
             nd_from_prefix(P, h.n, sh, P + h.n, K32, ctl, st);
             const DevCtl hc = read_ctl(p, ctl, st);
-            if ((double)hc.max_abs_k[0] < k_lim(2, h.D)) {
+            if (!wide && (double)hc.max_abs_k[0] < k_lim(2, h.D)) {
                 k32_to_f64(K32, h.n, bin, d_out, st);
                 return;
             }
@@ -533,7 +534,7 @@ void decode_component(umcg_plan* p, const CompHeader& h, const uint8_t* d_payloa
 // Grid component in the pipeline: prefer the int32 lattice form (K1). Returns
 // true with K1 filled, or false with x1f (fp64 values) filled.
 static bool decode_grid(umcg_plan* p, const CompHeader& h, const uint8_t* d_payload, int32_t* K1, double* x1f,
-                        cudaStream_t st) {
+                        uint64_t* kmax, cudaStream_t st) {
     const int pred = (h.pred == 2 && h.D == 1) ? 1 : h.pred;
     const double bin = 2.0 * h.tau;
     const bool lattice = h.codec == 0 && h.backend == 0 && h.D <= 8 && h.tau != 0.0 && !h.n_esc &&
@@ -550,10 +551,11 @@ static bool decode_grid(umcg_plan* p, const CompHeader& h, const uint8_t* d_payl
         void* status = p->scratch_c.reserve(dec_status_bytes(ulen));
         int64_t* P = p->kbuf.as<int64_t>(2 * (h.n ? h.n : 1));
         dec_fused(DEC_P64, U, ulen, h.n, status, ctl, nullptr, nullptr, 0.0, bin, nullptr, P, st);
-        check_fused(p, ctl, U, ulen, h.n, st);
+        const bool wide = check_fused(p, ctl, U, ulen, h.n, st).aux[7] != 0;
         nd_from_prefix(P, h.n, make_shape(h.D, h.dims), P + h.n, K1, ctl, st);
         const DevCtl hc = read_ctl(p, ctl, st);
-        if ((double)hc.max_abs_k[0] < k_lim(pred, h.D)) return true;
+        *kmax = hc.max_abs_k[0];
+        if (!wide && (double)hc.max_abs_k[0] < k_lim(pred, h.D)) return true;
     }
     decode_component(p, h, d_payload, x1f, st);
     return false;
@@ -636,7 +638,8 @@ void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_
     double* x1 = p->x1.as<double>(p->n_slots ? p->n_slots : 1);
     int32_t* K1 = p->codes1.as<int32_t>(p->n_slots ? p->n_slots : 1);
     const int g_kind = (flags & 2u) ? 1 : 0;
-    const bool k1_lattice = decode_grid(p, h1, d_ar + p1, K1, x1, st);
+    uint64_t k1max = ~0ull;
+    const bool k1_lattice = decode_grid(p, h1, d_ar + p1, K1, x1, &k1max, st);
     const double bin1 = 2.0 * h1.tau;
     // Fast path: nearest g over the lattice grid, residual decoded and
     // recomposed in one pass (decode.cu, DEC_RECOMPOSE).
@@ -653,10 +656,18 @@ void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_
         const uint8_t* U = stream_unpack(d_ar + p2 + h2.stream_off, h2.stream_len, p->dec, ctl, st, &ulen);
         init_ctl(ctl, st);
         void* status = p->scratch_c.reserve(dec_status_bytes(ulen));
-        dec_fused(DEC_RECOMPOSE, U, ulen, p->n, status, ctl, p->d_node.as<uint32_t>(1), K1, bin1, bin2, d_out,
-                  nullptr, st);
+        // |K1| < 2^15: gather from an int16 copy (half the L2 footprint)
+        const bool k16 = k1max < 32768;
+        const int32_t* ktab = K1;
+        if (k16) {
+            int16_t* K16 = p->dx1.as<int16_t>(p->n_slots ? p->n_slots : 1);
+            k32_to_k16(K1, p->n_slots, K16, st);
+            ktab = reinterpret_cast<const int32_t*>(K16);
+        }
+        dec_fused(k16 ? DEC_RECOMPOSE16 : DEC_RECOMPOSE, U, ulen, p->n, status, ctl, p->d_node.as<uint32_t>(1),
+                  ktab, bin1, bin2, d_out, nullptr, st);
         const DevCtl hc = check_fused(p, ctl, U, ulen, p->n, st);
-        if ((double)hc.max_abs_k[1] < k_lim(1, 1)) return;
+        if (!hc.aux[7] && (double)hc.max_abs_k[1] < k_lim(1, 1)) return;
     }
     if (k1_lattice) k32_to_f64(K1, p->n_slots, bin1, x1, st);
     decode_component(p, h2, d_ar + p2, d_out, st);
@@ -785,6 +796,7 @@ extern "C" {
 const char* umcg_last_error(void) { return g_last_error.c_str(); }
 const char* umcg_version(void) { return "umcg 0.1 (sm_100a)"; }
 uint64_t umcg_kernel_launches(void) { return g_launches.load(); }
+uint64_t umcg_serial_fallbacks(void) { return g_serial_fallbacks.load(); }
 
 umcg_status umcg_plan_create(const umcg_grid_desc* grid, const umcg_mapping_desc* mapping, int mesh_dim,
                              const double* coords, umcg_plan** out) {

@@ -583,6 +583,7 @@ void recompose(const ResidualSrc& src, uint64_t n, double* inout, cudaStream_t s
 void serial_encode(const double* v, uint64_t n, int pred, const NdShape& sh, double tau, uint64_t* codes,
                    double* recon_scratch, uint64_t* esc_idx, double* esc_val, DevCtl* ctl, int comp,
                    cudaStream_t st) {
+    g_serial_fallbacks.fetch_add(1);
     k_serial_encode<<<1, 32, 0, st>>>(v, n, pred, sh, tau, codes, recon_scratch, esc_idx, esc_val, ctl, comp);
     UMCG_LAUNCHED();
 }
@@ -590,6 +591,7 @@ void serial_encode(const double* v, uint64_t n, int pred, const NdShape& sh, dou
 void serial_decode(const uint64_t* codes, uint64_t n, int pred, const NdShape& sh, double tau,
                    const uint64_t* esc_idx, const double* esc_val, uint64_t n_esc, double* out,
                    cudaStream_t st) {
+    g_serial_fallbacks.fetch_add(1);
     k_serial_decode<<<1, 32, 0, st>>>(codes, n, pred, sh, tau, esc_idx, esc_val, n_esc, out);
     UMCG_LAUNCHED();
 }

@@ -32,6 +32,8 @@ inline void cuda_check(cudaError_t e, const char* what) {
 #define UMCG_CUDA(x) ::umcg::cuda_check((x), #x)
 
 extern std::atomic<uint64_t> g_launches;
+// exact-serial fallbacks taken (encode / decode): should stay 0 on normal data
+extern std::atomic<uint64_t> g_serial_fallbacks;
 inline void count_launch(uint64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 #define UMCG_LAUNCHED()                                  \
     do {                                                 \

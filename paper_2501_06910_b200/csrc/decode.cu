@@ -90,10 +90,13 @@ __device__ __forceinline__ void stage_tile(const uint8_t* __restrict__ U, uint64
 
 // Sequential varint walk over a thread's 32 bytes held in registers, seeded
 // with the partial varint that straddles in from the 16 halo bytes. emit(v)
-// is called for every code that ends inside the thread's bytes.
+// is called for every code that ends inside the thread's bytes. Lossy PQ
+// codes are zigzag(int32) < 2^32 (codec.hpp:305, 322), so values are
+// accumulated in 32 bits; a longer varint sets *wide and the caller falls
+// back to the general decoder.
 template <class F>
 __device__ __forceinline__ void thread_walk(const uint8_t* sb, int my, int64_t gbase, uint64_t ulen, bool* bad,
-                                            F&& emit) {
+                                            bool* wide, F&& emit) {
     const uint4* p = reinterpret_cast<const uint4*>(sb + my - 16);
     const uint4 h = p[0], a = p[1], b = p[2];
     const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
@@ -107,21 +110,23 @@ __device__ __forceinline__ void thread_walk(const uint8_t* sb, int my, int64_t g
         run = run && (hb & 0x80u);
         hlen += run ? 1 : 0;
     }
-    uint64_t acc = 0;
+    uint32_t acc = 0;
     int shift = 0;
 #pragma unroll
-    for (int j = 6; j < 16; ++j) {
+    for (int j = 11; j < 16; ++j) {
         const uint32_t hb = (hw[j >> 2] >> (8 * (j & 3))) & 0xffu;
         if (j >= 16 - hlen) {
-            acc |= (uint64_t)(hb & 0x7fu) << shift;
+            acc |= (hb & 0x7fu) << shift;
             shift += 7;
         }
     }
     int crun = hlen;
+    bool wd = hlen > 4 && gbase < (int64_t)ulen;
 #pragma unroll
     for (int k = 0; k < RB; ++k) {
         const uint32_t byte = (w[k >> 2] >> (8 * (k & 3))) & 0xffu;
-        if (shift < 64) acc |= (uint64_t)(byte & 0x7fu) << shift;
+        acc |= (byte & 0x7fu) << (shift & 31);
+        wd |= (shift == 28) && (byte > 0x0fu) && (gbase + k < (int64_t)ulen);
         shift += 7;
         if (!(byte & 0x80u)) {
             emit(acc);
@@ -130,17 +135,24 @@ __device__ __forceinline__ void thread_walk(const uint8_t* sb, int my, int64_t g
             crun = 0;
         } else {
             ++crun;
-            if (crun >= 10 && gbase + k < (int64_t)ulen) *bad = true;
+            if (crun >= 5 && gbase + k < (int64_t)ulen) {  // padding past the end is 0x80
+                wd = true;
+                if (crun >= 10) *bad = true;
+            }
         }
     }
+    *wide |= wd;
 }
 
-__device__ __forceinline__ CS thread_counts(const uint8_t* sb, int my, bool* bad, int64_t base, uint64_t ulen) {
+__device__ __forceinline__ int64_t zz_dec32(uint32_t v) { return (int64_t)(v >> 1) ^ -(int64_t)(v & 1u); }
+
+__device__ __forceinline__ CS thread_counts(const uint8_t* sb, int my, bool* bad, bool* wide, int64_t base,
+                                            uint64_t ulen) {
     uint32_t c = 0;
     int64_t s = 0;
-    thread_walk(sb, my, base + (my - RHALO), ulen, bad, [&](uint64_t v) {
+    thread_walk(sb, my, base + (my - RHALO), ulen, bad, wide, [&](uint32_t v) {
         ++c;
-        s += zz_dec(v);
+        s += zz_dec32(v);
     });
     return CS{c, s};
 }
@@ -153,9 +165,10 @@ __global__ void __launch_bounds__(RT) k_dec_agg(const uint8_t* __restrict__ U, u
     const int64_t base = (int64_t)blockIdx.x * (int64_t)RTILE;
     stage_tile(U, ulen, base, sb);
     __syncthreads();
-    bool bad = false;
-    const CS mine = thread_counts(sb, RHALO + threadIdx.x * RB, &bad, base, ulen);
+    bool bad = false, wide = false;
+    const CS mine = thread_counts(sb, RHALO + threadIdx.x * RB, &bad, &wide, base, ulen);
     if (bad) set_err(ctl, DE_CORRUPT_VARINT);
+    if (wide) ctl->aux[7] = 1;
     const CS t = BR(tmp).Reduce(mine, CSAdd());
     if (threadIdx.x == 0) aggs[blockIdx.x] = t;
 }
@@ -178,10 +191,10 @@ __global__ void __launch_bounds__(1024) k_scan_cs(CS* __restrict__ aggs, uint64_
     if (threadIdx.x == 0) ctl->count = tot.cnt;
 }
 
-template <int MODE>
+template <int MODE, class KT>
 __global__ void __launch_bounds__(RT) k_dec_out(const uint8_t* __restrict__ U, uint64_t ulen, uint64_t n,
                                                const CS* __restrict__ pre, DevCtl* ctl,
-                                               const uint32_t* __restrict__ node, const int32_t* __restrict__ K1,
+                                               const uint32_t* __restrict__ node, const KT* __restrict__ K1,
                                                double bin1, double bin, double* __restrict__ out,
                                                int64_t* __restrict__ P64) {
     using BS = cub::BlockScan<CS, RT>;
@@ -192,8 +205,8 @@ __global__ void __launch_bounds__(RT) k_dec_out(const uint8_t* __restrict__ U, u
     stage_tile(U, ulen, base, sb);
     __syncthreads();
     const int my = RHALO + threadIdx.x * RB;
-    bool bad = false;
-    const CS mine = thread_counts(sb, my, &bad, base, ulen);
+    bool bad = false, wide = false;
+    const CS mine = thread_counts(sb, my, &bad, &wide, base, ulen);
     CS excl, tot;
     BS(tmp).ExclusiveScan(mine, excl, CS{0, 0}, CSAdd(), tot);
     const CS tp = pre[blockIdx.x];
@@ -201,9 +214,9 @@ __global__ void __launch_bounds__(RT) k_dec_out(const uint8_t* __restrict__ U, u
     uint32_t li = (uint32_t)excl.cnt;     // local element index
     int64_t K = tp.sum + excl.sum;
     uint64_t kmax = 0;
-    bool bad2 = false;
-    thread_walk(sb, my, base + (my - RHALO), ulen, &bad2, [&](uint64_t v) {
-        K += zz_dec(v);
+    bool bad2 = false, wide2 = false;
+    thread_walk(sb, my, base + (my - RHALO), ulen, &bad2, &wide2, [&](uint32_t v) {
+        K += zz_dec32(v);
         const uint64_t a = (uint64_t)(K < 0 ? -K : K);
         kmax = a > kmax ? a : kmax;
         if (MODE == DEC_P64) {
@@ -235,7 +248,11 @@ __global__ void __launch_bounds__(RT) k_dec_out(const uint8_t* __restrict__ U, u
 #pragma unroll
         for (int u = 0; u < UN; ++u) {
             const uint32_t e = e0 + u * RT + threadIdx.x;
-            g1[u] = (MODE == DEC_RECOMPOSE && e < cnt && tp.cnt + e < n) ? ld_s32_hint(&K1[nd[u]], pl) : 0;
+            if (MODE == DEC_RECOMPOSE && e < cnt && tp.cnt + e < n)
+                g1[u] = sizeof(KT) == 4 ? ld_s32_hint(reinterpret_cast<const int32_t*>(K1) + nd[u], pl)
+                                        : (int32_t)__ldg(K1 + nd[u]);
+            else
+                g1[u] = 0;
         }
 #pragma unroll
         for (int u = 0; u < UN; ++u) {
@@ -288,6 +305,11 @@ __global__ void k_k32(const int64_t* __restrict__ K, uint64_t n, int32_t* __rest
     if ((threadIdx.x & 31) == 0 && a > ctl->max_abs_k[0]) atomicMax(&ctl->max_abs_k[0], (unsigned long long)a);
 }
 
+__global__ void k_k32_to_k16(const int32_t* __restrict__ K, uint64_t n, int16_t* __restrict__ K16) {
+    const uint64_t i = blockIdx.x * 256ull + threadIdx.x;
+    if (i < n) K16[i] = (int16_t)K[i];
+}
+
 __global__ void k_k32_to_f64(const int32_t* __restrict__ K, uint64_t n, double bin, double* __restrict__ x) {
     const uint64_t i = blockIdx.x * 256ull + threadIdx.x;
     if (i < n) x[i] = __dmul_rn((double)K[i], bin);
@@ -308,11 +330,15 @@ void dec_fused(int mode, const uint8_t* U, uint64_t ulen, uint64_t n, void* stat
     k_scan_cs<<<1, 1024, 0, st>>>(aggs, T, ctl);
     UMCG_LAUNCHED();
     if (mode == DEC_P64)
-        k_dec_out<DEC_P64><<<(unsigned)T, RT, 0, st>>>(U, ulen, n, aggs, ctl, node, K1, bin1, bin, out, P64);
+        k_dec_out<DEC_P64, int32_t><<<(unsigned)T, RT, 0, st>>>(U, ulen, n, aggs, ctl, node, K1, bin1, bin, out, P64);
     else if (mode == DEC_VALUES)
-        k_dec_out<DEC_VALUES><<<(unsigned)T, RT, 0, st>>>(U, ulen, n, aggs, ctl, node, K1, bin1, bin, out, P64);
+        k_dec_out<DEC_VALUES, int32_t><<<(unsigned)T, RT, 0, st>>>(U, ulen, n, aggs, ctl, node, K1, bin1, bin, out, P64);
+    else if (mode == DEC_RECOMPOSE16)
+        k_dec_out<DEC_RECOMPOSE, int16_t><<<(unsigned)T, RT, 0, st>>>(U, ulen, n, aggs, ctl, node,
+                                                                     reinterpret_cast<const int16_t*>(K1), bin1, bin,
+                                                                     out, P64);
     else
-        k_dec_out<DEC_RECOMPOSE><<<(unsigned)T, RT, 0, st>>>(U, ulen, n, aggs, ctl, node, K1, bin1, bin, out, P64);
+        k_dec_out<DEC_RECOMPOSE, int32_t><<<(unsigned)T, RT, 0, st>>>(U, ulen, n, aggs, ctl, node, K1, bin1, bin, out, P64);
     UMCG_LAUNCHED();
 }
 
@@ -332,6 +358,12 @@ void nd_from_prefix(const int64_t* P, uint64_t n, const NdShape& sh, int64_t* Kw
         src = Kw;
     }
     k_k32<<<g, 256, 0, st>>>(src, n, K32, ctl);
+    UMCG_LAUNCHED();
+}
+
+void k32_to_k16(const int32_t* K, uint64_t n, int16_t* K16, cudaStream_t st) {
+    if (!n) return;
+    k_k32_to_k16<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(K, n, K16);
     UMCG_LAUNCHED();
 }
 

@@ -5,12 +5,14 @@
 
 namespace umcg {
 
-enum DecMode : int { DEC_P64 = 0, DEC_VALUES = 1, DEC_RECOMPOSE = 2 };
+enum DecMode : int { DEC_P64 = 0, DEC_VALUES = 1, DEC_RECOMPOSE = 2, DEC_RECOMPOSE16 = 3 };
 
 size_t dec_status_bytes(uint64_t ulen);
 // One pass over the unpacked varint bytes U[0..ulen): see decode.cu. Writes
-// ctl->count (number of complete varints), ctl->max_abs_k[1] and flags
-// DE_CORRUPT_VARINT. ctl->aux[6] is used as the tile ticket.
+// ctl->count (number of complete varints), ctl->max_abs_k[1], flags
+// DE_CORRUPT_VARINT, and ctl->aux[7] = 1 when a varint longer than a lossy
+// PQ code (> 5 bytes / >= 2^32) was seen (caller must use the general path).
+// With DEC_RECOMPOSE16, K1 points to an int16 table.
 void dec_fused(int mode, const uint8_t* U, uint64_t ulen, uint64_t n, void* status, DevCtl* ctl,
                const uint32_t* node, const int32_t* K1, double bin1, double bin, double* out, int64_t* P64,
                cudaStream_t st);
@@ -19,6 +21,7 @@ void dec_fused(int mode, const uint8_t* U, uint64_t ulen, uint64_t n, void* stat
 // max|K| -> ctl->max_abs_k[0]. Kw is int64 scratch [n] (unused when D == 1).
 void nd_from_prefix(const int64_t* P, uint64_t n, const NdShape& sh, int64_t* Kw, int32_t* K32, DevCtl* ctl,
                     cudaStream_t st);
+void k32_to_k16(const int32_t* K, uint64_t n, int16_t* K16, cudaStream_t st);
 void k32_to_f64(const int32_t* K, uint64_t n, double bin, double* x, cudaStream_t st);
 
 // RLE token stream -> unpacked varint bytes (in place for a single literal

@@ -115,6 +115,7 @@ def test_fixture_cases(cuda, case_idx, ref, oracle):
                 plan.compress(dx, b, name=f"case{k}")
             assert ei.value.kind == "seed_mode_unsupported"
             continue
+        fb0 = umcg.serial_fallbacks()
         got = plan.compress(dx, b, name=f"case{k}")
         check_archive(got, ref_ar, s, x, p, oracle, label)
         tau_abs = p.get("tau", 1e-3) * (np.ptp(x) if p.get("bound_kind", 1) == 1 else 1.0)
@@ -124,6 +125,9 @@ def test_fixture_cases(cuda, case_idx, ref, oracle):
         check_decode(out_ref_ar, ref_dec, x, tau_abs, label + " gpu(ref archive)")
         out_own = plan.decompress(got).cpu().numpy()
         check_decode(out_own, ref.decompress(s, got), x, tau_abs, label + " gpu(own archive)")
+        if p.get("tau", 1e-3) > 0:
+            # lossy data in the lattice regime never takes the one-thread exact path
+            assert umcg.serial_fallbacks() == fb0, label
 
 
 def test_codec_known_answers(cuda, ref):
