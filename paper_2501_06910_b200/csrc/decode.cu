@@ -290,6 +290,89 @@ __global__ void k_axis_cols(int64_t* __restrict__ K, uint64_t n, uint64_t len, u
     }
 }
 
+// Fused N-D prefix for D = 2 / 3 from the plain row-major prefix P:
+//   out[..., j, k] = sum_{j' <= j} (P[..., j', k] - P[row(..., j') - 1])
+// i.e. the row scan (fastest axis) by differencing P, then the scan along
+// the middle axis. Threads own (outer, k) lines, 8 loads in flight.
+// For D == 2 the result is final (int32 + max|K|); for D == 3 an int64
+// intermediate follows, finished by k_nd_outer.
+template <bool FINAL>
+__global__ void __launch_bounds__(256) k_nd_mid(const int64_t* __restrict__ P, uint64_t d_out, uint64_t d_mid,
+                                               uint64_t d_fast, int64_t* __restrict__ Kw, int32_t* __restrict__ K32,
+                                               DevCtl* ctl) {
+    const uint64_t line = blockIdx.x * 256ull + threadIdx.x;  // over d_out * d_fast
+    uint64_t amax = 0;
+    if (line < d_out * d_fast) {
+        const uint64_t o = line / d_fast, k = line % d_fast;
+        const uint64_t base = o * d_mid * d_fast;
+        int64_t acc = 0;
+        for (uint64_t j0 = 0; j0 < d_mid; j0 += 8) {
+            int64_t v[8], rb[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint64_t j = j0 + u;
+                if (j < d_mid) {
+                    const uint64_t r = base + j * d_fast;
+                    v[u] = __ldcs(&P[r + k]);
+                    rb[u] = r ? __ldg(&P[r - 1]) : 0;
+                } else {
+                    v[u] = 0;
+                    rb[u] = 0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint64_t j = j0 + u;
+                if (j >= d_mid) break;
+                acc += v[u] - rb[u];
+                const uint64_t idx = base + j * d_fast + k;
+                if (FINAL) {
+                    K32[idx] = (int32_t)acc;
+                    const uint64_t a = (uint64_t)(acc < 0 ? -acc : acc);
+                    amax = a > amax ? a : amax;
+                } else {
+                    Kw[idx] = acc;
+                }
+            }
+        }
+    }
+    if (FINAL) {
+        for (int o = 16; o; o >>= 1) {
+            const uint64_t b = __shfl_xor_sync(0xffffffffu, amax, o);
+            amax = b > amax ? b : amax;
+        }
+        if ((threadIdx.x & 31) == 0 && amax > ctl->max_abs_k[0]) atomicMax(&ctl->max_abs_k[0], (unsigned long long)amax);
+    }
+}
+
+// Last scan for D == 3 along the outer axis (stride d1*d2), int32 out + max|K|.
+__global__ void __launch_bounds__(256) k_nd_outer(const int64_t* __restrict__ Kw, uint64_t d0, uint64_t plane,
+                                                 int32_t* __restrict__ K32, DevCtl* ctl) {
+    const uint64_t c = blockIdx.x * 256ull + threadIdx.x;
+    uint64_t amax = 0;
+    if (c < plane) {
+        int64_t acc = 0;
+        for (uint64_t i0 = 0; i0 < d0; i0 += 8) {
+            int64_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = i0 + u < d0 ? __ldcs(&Kw[(i0 + u) * plane + c]) : 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (i0 + u >= d0) break;
+                acc += v[u];
+                K32[(i0 + u) * plane + c] = (int32_t)acc;
+                const uint64_t a = (uint64_t)(acc < 0 ? -acc : acc);
+                amax = a > amax ? a : amax;
+            }
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        const uint64_t b = __shfl_xor_sync(0xffffffffu, amax, o);
+        amax = b > amax ? b : amax;
+    }
+    if ((threadIdx.x & 31) == 0 && amax > ctl->max_abs_k[0]) atomicMax(&ctl->max_abs_k[0], (unsigned long long)amax);
+}
+
 __global__ void k_k32(const int64_t* __restrict__ K, uint64_t n, int32_t* __restrict__ K32, DevCtl* ctl) {
     const uint64_t i = blockIdx.x * 256ull + threadIdx.x;
     uint64_t a = 0;
@@ -347,6 +430,20 @@ void nd_from_prefix(const int64_t* P, uint64_t n, const NdShape& sh, int64_t* Kw
     const unsigned g = (unsigned)cdiv(n, 256);
     if (!n) return;
     const int64_t* src = P;
+    if (sh.D == 2 || sh.D == 3) {
+        const uint64_t d2 = sh.dims[sh.D - 1], d1 = sh.dims[sh.D - 2], d0 = sh.D == 3 ? sh.dims[0] : 1;
+        const unsigned g1 = (unsigned)cdiv(d0 * d2, 256);
+        if (sh.D == 2) {
+            k_nd_mid<true><<<g1, 256, 0, st>>>(P, d0, d1, d2, nullptr, K32, ctl);
+            UMCG_LAUNCHED();
+        } else {
+            k_nd_mid<false><<<g1, 256, 0, st>>>(P, d0, d1, d2, Kw, nullptr, ctl);
+            UMCG_LAUNCHED();
+            k_nd_outer<<<(unsigned)cdiv(d1 * d2, 256), 256, 0, st>>>(Kw, d0, d1 * d2, K32, ctl);
+            UMCG_LAUNCHED();
+        }
+        return;
+    }
     if (sh.D > 1) {
         k_rows<<<g, 256, 0, st>>>(P, n, sh.dims[sh.D - 1], Kw);
         UMCG_LAUNCHED();

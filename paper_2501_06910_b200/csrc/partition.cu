@@ -92,85 +92,109 @@ __device__ __forceinline__ int32_t resid_k(double r, double bin, double tau, Dev
 // Bucket b's elements, in bucket order l = 0..m-1, live in layout E as one
 // chunk per epoch: pre[e] = first l of epoch e's chunk, cbase[e] = its
 // layout-E position. Each warp moves whole chunks (coalesced).
+constexpr int PER = kBucketCap / BT;  // elements per thread in a bucket
+
 __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, const uint32_t* __restrict__ bk,
-                                              uint64_t B, uint32_t E, const uint32_t* __restrict__ ech,
+                                              uint64_t B, uint32_t E, const uint2* __restrict__ bct,
                                               const uint16_t* __restrict__ lnode,
                                               const uint16_t* __restrict__ lperm, const uint32_t* __restrict__ seg,
                                               DevCtl* ctl, double* __restrict__ x1, int32_t* __restrict__ KE) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* xs = reinterpret_cast<double*>(smem);                      // [kBucketCap]
     double* x1s = xs + kBucketCap;                                     // [kBucketNodes]
-    uint32_t* pre = reinterpret_cast<uint32_t*>(x1s + kBucketNodes);   // [E+1]
-    uint32_t* cbase = pre + (E + 1);                                   // [E]
-    using BS = cub::BlockScan<uint32_t, BT>;
-    __shared__ typename BS::TempStorage tmp;
+    uint32_t* sg = reinterpret_cast<uint32_t*>(x1s + kBucketNodes);    // [kBucketNodes + 1]
+    uint2* ch = reinterpret_cast<uint2*>(sg + kBucketNodes + 2);       // [E+1]
+    uint16_t* lp = reinterpret_cast<uint16_t*>(ch + (E + 1));          // [kBucketCap]
+    uint16_t* ln = lp + kBucketCap;                                    // [kBucketCap]
     const uint32_t* bstart = bk;
     const uint32_t* bnode = bk + B + 1;
     const uint64_t b = blockIdx.x;
     const uint32_t s0 = bstart[b], s1 = bstart[b + 1], m = s1 - s0;
-    const uint32_t j0 = bnode[b], j1 = bnode[b + 1];
+    const uint32_t j0 = bnode[b], j1 = bnode[b + 1], nj = j1 - j0;
     const double bin = ctl->bin[1], tau = ctl->tau_c[1];
-    // chunk table of this bucket: one chunk per epoch
-    uint32_t carry = 0;
-    for (uint32_t e0 = 0; e0 < E; e0 += BT) {
-        const uint32_t e = e0 + threadIdx.x;
-        uint32_t c = 0, o = 0;
-        if (e < E) {
-            o = __ldg(&ech[(uint64_t)e * (B + 1) + b]);
-            c = __ldg(&ech[(uint64_t)e * (B + 1) + b + 1]) - o;
-        }
-        uint32_t ex, tot;
-        BS(tmp).ExclusiveSum(c, ex, tot);
-        if (e < E) {
-            pre[e] = carry + ex;
-            cbase[e] = (uint32_t)((uint64_t)e * kEpoch + o);
-        }
-        carry += tot;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) pre[E] = carry;
-    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int NW = BT / 32;
-    if (m > kBucketCap) {
+    // chunk table (one chunk per epoch, bucket-major) + segment offsets
+    for (uint32_t e = threadIdx.x; e <= E; e += BT) ch[e] = __ldg(&bct[b * (uint64_t)(E + 1) + e]);
+    const bool heavy = m > kBucketCap;
+    if (!heavy)
+        for (uint32_t j = threadIdx.x; j <= nj; j += BT) sg[j] = __ldg(&seg[j0 + j]) - s0;
+    __syncthreads();
+    if (heavy) {
         // one heavy slot: ordered sum straight from global memory
         if (threadIdx.x == 0) {
             double s = 0.0;
             for (uint32_t e = 0; e < E; ++e)
-                for (uint32_t l = pre[e]; l < pre[e + 1]; ++l) s = __dadd_rn(s, xE[cbase[e] + (l - pre[e])]);
+                for (uint32_t l = ch[e].x; l < ch[e + 1].x; ++l) s = __dadd_rn(s, xE[ch[e].y + (l - ch[e].x)]);
             x1s[0] = __ddiv_rn(s, (double)m);
             x1[j0] = x1s[0];
         }
         __syncthreads();
         const double mean = x1s[0];
         for (uint32_t e = warp; e < E; e += NW)
-            for (uint32_t l = pre[e] + lane; l < pre[e + 1]; l += 32) {
-                const uint32_t q = cbase[e] + (l - pre[e]);
+            for (uint32_t l = ch[e].x + lane; l < ch[e + 1].x; l += 32) {
+                const uint32_t q = ch[e].y + (l - ch[e].x);
                 KE[q] = resid_k(__dsub_rn(xE[q], mean), bin, tau, ctl);
             }
         return;
     }
-    // stage the bucket (chunk per epoch, one warp per chunk: coalesced)
-    for (uint32_t e = warp; e < E; e += NW) {
-        const uint32_t l0 = pre[e], l1 = pre[e + 1], cb = cbase[e];
-        for (uint32_t l = l0 + lane; l < l1; l += 32) xs[l] = __ldcs(&xE[cb + (l - l0)]);
+    // each thread owns bucket elements l = t + k*BT; all loads issued up front
+    uint32_t e_first = 0;
+    {
+        uint32_t lo = 0, hi = E;  // last chunk with first index <= threadIdx.x
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (ch[mid].x <= threadIdx.x) lo = mid; else hi = mid;
+        }
+        e_first = lo;
+    }
+    {
+        double xv[PER];
+        uint32_t e = e_first;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const uint32_t l = threadIdx.x + k * BT;
+            if (l < m) {
+                while (l >= ch[e + 1].x) ++e;
+                xv[k] = __ldcs(&xE[ch[e].y + (l - ch[e].x)]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const uint32_t l = threadIdx.x + k * BT;
+            if (l < m) {
+                lp[l] = __ldg(&lperm[s0 + l]);
+                ln[l] = __ldg(&lnode[s0 + l]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const uint32_t l = threadIdx.x + k * BT;
+            if (l < m) xs[l] = xv[k];
+        }
     }
     __syncthreads();
     // interpolate_to_grid (interp.hpp:58-64): 0.0 + x_a + x_b + ... in ascending vertex order
-    for (uint32_t j = threadIdx.x; j < j1 - j0; j += BT) {
-        const uint32_t k0 = seg[j0 + j] - s0, k1 = seg[j0 + j + 1] - s0;
+    for (uint32_t j = threadIdx.x; j < nj; j += BT) {
+        const uint32_t k0 = sg[j], k1 = sg[j + 1];
         double s = 0.0;
-        for (uint32_t k = k0; k < k1; ++k) s = __dadd_rn(s, xs[__ldg(&lperm[s0 + k])]);
+        for (uint32_t k = k0; k < k1; ++k) s = __dadd_rn(s, xs[lp[k]]);
         const double v = k1 > k0 ? __ddiv_rn(s, (double)(k1 - k0)) : 0.0;
         x1s[j] = v;
         x1[j0 + j] = v;
     }
     __syncthreads();
     // compute_residuals (interp.hpp:161-170) + lattice index (codec.hpp:307-314)
-    for (uint32_t e = warp; e < E; e += NW) {
-        const uint32_t l0 = pre[e], l1 = pre[e + 1], cb = cbase[e];
-        for (uint32_t l = l0 + lane; l < l1; l += 32)
-            KE[cb + (l - l0)] = resid_k(__dsub_rn(xs[l], x1s[__ldg(&lnode[s0 + l])]), bin, tau, ctl);
+    {
+        uint32_t e = e_first;
+#pragma unroll 4
+        for (int k = 0; k < PER; ++k) {
+            const uint32_t l = threadIdx.x + k * BT;
+            if (l < m) {
+                while (l >= ch[e + 1].x) ++e;
+                KE[ch[e].y + (l - ch[e].x)] = resid_k(__dsub_rn(xs[l], x1s[ln[l]]), bin, tau, ctl);
+            }
+        }
     }
 }
 
@@ -240,14 +264,14 @@ void partition_values(const void* x, int x_f32, umcg_plan* p, double* xE, DevCtl
 void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double* x1, int32_t* KE, cudaStream_t st) {
     if (!p->n_buckets) return;
     const uint32_t E = (uint32_t)p->n_epochs;
-    const size_t smem = kBucketCap * 8 + kBucketNodes * 8 + (2 * (size_t)E + 1) * 4 + 16;
+    const size_t smem = kBucketCap * 8 + kBucketNodes * 8 + (kBucketNodes + 2) * 4 + ((size_t)E + 1) * 8 + kBucketCap * 4 + 16;
     static bool configured = false;
     if (!configured) {
         UMCG_CUDA(cudaFuncSetAttribute(k_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         configured = true;
     }
     k_bucket<<<(unsigned)p->n_buckets, BT, smem, st>>>(xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E,
-                                                        p->d_ech.as<uint32_t>(1), p->d_lnode.as<uint16_t>(1),
+                                                        p->d_bct.as<uint2>(1), p->d_lnode.as<uint16_t>(1),
                                                         p->d_lperm.as<uint16_t>(1), p->d_seg.as<uint32_t>(1), ctl, x1,
                                                         KE);
     UMCG_LAUNCHED();

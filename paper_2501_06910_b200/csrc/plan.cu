@@ -150,6 +150,21 @@ __global__ void k_epoch_offsets(const uint32_t* __restrict__ cnt, uint64_t E, ui
     ech[e * (B + 1) + B] = acc;
 }
 
+// bucket-major chunk table: for bucket b, epoch e: x = first bucket-local
+// index of the epoch-e chunk (x of e = E is the bucket size), y = its layout-E
+// position. One thread per bucket (E is small).
+__global__ void k_bucket_chunks(const uint32_t* __restrict__ ech, uint64_t E, uint64_t B, uint2* __restrict__ bct) {
+    const uint64_t b = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (b >= B) return;
+    uint32_t acc = 0;
+    for (uint64_t e = 0; e < E; ++e) {
+        const uint32_t o = ech[e * (B + 1) + b];
+        bct[b * (E + 1) + e] = make_uint2(acc, (uint32_t)(e * kEpoch + o));
+        acc += ech[e * (B + 1) + b + 1] - o;
+    }
+    bct[b * (E + 1) + E] = make_uint2(acc, 0u);
+}
+
 __global__ void k_lperm(const uint32_t* __restrict__ perm, uint64_t n, const uint32_t* __restrict__ dst,
                         const uint32_t* __restrict__ node, const uint32_t* __restrict__ sb,
                         const uint32_t* __restrict__ bstart, uint16_t* __restrict__ lperm) {
@@ -311,6 +326,8 @@ void plan_build_buckets(umcg_plan* p, cudaStream_t st) {
     k_dstE<<<blocks(n), THREADS, 0, st>>>(srcE, n, p->d_dstE.as<uint32_t>(n));
     UMCG_LAUNCHED();
     k_epoch_offsets<<<blocks(E), THREADS, 0, st>>>(ec, E, B, p->d_ech.as<uint32_t>(E * (B + 1)));
+    UMCG_LAUNCHED();
+    k_bucket_chunks<<<blocks(B), THREADS, 0, st>>>(p->d_ech.as<uint32_t>(1), E, B, p->d_bct.as<uint2>(B * (E + 1)));
     UMCG_LAUNCHED();
     UMCG_CUDA(cudaStreamSynchronize(st));
 }

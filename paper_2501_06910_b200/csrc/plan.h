@@ -39,6 +39,7 @@ struct umcg_plan {
     umcg::DevBuf d_srcE;     // u32 [n]    vertex at layout-E position p
     umcg::DevBuf d_dstE;     // u32 [n]    layout-E position of vertex i
     umcg::DevBuf d_ech;      // u32 [E*(B+1)] offset of bucket b inside epoch e's block
+    umcg::DevBuf d_bct;      // uint2 [B*(E+1)] per bucket: (first bucket-local index, layout-E base) per epoch
     umcg::DevBuf d_lnode;    // u16 [n]    bucket-local slot of bucket-order element
     umcg::DevBuf d_lperm;    // u16 [n]    bucket-local element of node-sorted position
     umcg::DevBuf d_bk;       // u32 [2*(B+1)] bucket start (vertex) and first slot
@@ -62,10 +63,10 @@ uint64_t mapping_digest_host32(int mode, uint64_t n, const uint32_t* assign, uin
 // Build perm / seg_off from d_node on the plan (stable radix sort by slot),
 // then the bucketed layout (plan_build_buckets).
 void plan_build_segments(umcg_plan* p, cudaStream_t st);
-constexpr uint32_t kBucketCap = 2048;   // vertices per bucket (smem staging)
+constexpr uint32_t kBucketCap = 4096;   // vertices per bucket (smem staging)
 constexpr uint64_t kEpoch = 1ull << 21;  // vertices per epoch of layout E
 constexpr uint32_t kMaxEpochs = 2048;    // k_bucket stages per-epoch chunk prefixes
-constexpr uint32_t kBucketNodes = 512;  // slots per bucket
+constexpr uint32_t kBucketNodes = 1016; // slots per bucket
 void plan_build_buckets(umcg_plan* p, cudaStream_t st);
 
 // Component payload decode (codec.hpp:364-441) of a payload in device memory
