@@ -1,0 +1,182 @@
+// Drop-in GPU replacement for umc::compress / umc::decompress
+// (reference proj/include/umc/pipeline.hpp:117-148, 180-210).
+//
+// Include this header next to the reference's own headers and call
+// umc::b200::compress / umc::b200::decompress with exactly the arguments of
+// the reference functions. Archives are byte-identical to the reference's
+// (up to rounding-window code flips) and every
+// failure is rethrown as the reference's exception type (common.hpp:19-38).
+// Link with libumcg.so (paper_2501_06910_b200/libumcg.so) and the CUDA
+// runtime. There is no CPU fallback: without a usable GPU the calls throw.
+//
+// Plans: the device plan (mapping upload, slot sort, bucketed layout,
+// mapping digest) is built once per distinct MappingTable object and cached
+// by address + content size; mutate a MappingTable only through a new
+// object (the reference treats mappings as immutable) or
+// call umc::b200::clear_plan_cache().
+#ifndef UMC_B200_PIPELINE_GPU_HPP
+#define UMC_B200_PIPELINE_GPU_HPP
+
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include <cuda_runtime_api.h>
+
+#include "umc/pipeline.hpp"
+#include "../umcg.h"
+
+namespace umc {
+namespace b200 {
+
+namespace detail {
+
+[[noreturn]] inline void rethrow(umcg_status s) {
+    const std::string msg = umcg_last_error();
+    switch (s) {
+        case UMCG_MALFORMED_FILE: throw malformed_file(msg);
+        case UMCG_INDEX_OUT_OF_RANGE: throw index_out_of_range(msg);
+        case UMCG_NON_FINITE_VALUE: throw non_finite_value(msg);
+        case UMCG_IO_FAILURE: throw io_failure(msg);
+        case UMCG_DEGENERATE_MESH: throw degenerate_mesh(msg);
+        case UMCG_EMPTY_AFTER_FILTERING: throw empty_after_filtering(msg);
+        case UMCG_INTERNAL_INCONSISTENCY: throw internal_inconsistency(msg);
+        case UMCG_SEED_MODE_UNSUPPORTED: throw seed_mode_unsupported(msg);
+        case UMCG_UNKNOWN_CODEC: throw unknown_codec(msg);
+        case UMCG_CORRUPT_PAYLOAD: throw corrupt_payload(msg);
+        case UMCG_EXTERNAL_CODEC_VIOLATION: throw external_codec_violation(msg);
+        case UMCG_SUBPROCESS_FAILURE: throw subprocess_failure(msg);
+        case UMCG_BUDGET_INADMISSIBLE: throw budget_inadmissible(msg);
+        case UMCG_MAPPING_MISMATCH: throw mapping_mismatch(msg);
+        case UMCG_ZERO_NORM_REFERENCE: throw zero_norm_reference(msg);
+        case UMCG_MISMATCHED_RUNS: throw mismatched_runs(msg);
+        default: throw error(msg);
+    }
+}
+
+inline void check(umcg_status s) {
+    if (s != UMCG_OK) rethrow(s);
+}
+
+struct PlanDeleter {
+    void operator()(umcg_plan* p) const { umcg_plan_destroy(p); }
+};
+using PlanPtr = std::unique_ptr<umcg_plan, PlanDeleter>;
+
+struct PlanKey {
+    const MappingTable* map;
+    const void* assign_data;
+    std::size_t n;
+    std::size_t n_visited;
+    std::uint64_t grid_nodes;
+    bool coords;
+    bool operator<(const PlanKey& o) const {
+        return std::tie(map, assign_data, n, n_visited, grid_nodes, coords) <
+               std::tie(o.map, o.assign_data, o.n, o.n_visited, o.grid_nodes, o.coords);
+    }
+};
+
+inline std::mutex& cache_mutex() {
+    static std::mutex m;
+    return m;
+}
+inline std::map<PlanKey, PlanPtr>& cache() {
+    static std::map<PlanKey, PlanPtr> c;
+    return c;
+}
+
+// Device plan for (map, grid, mesh); coordinates are uploaded only when the
+// caller needs multilinear g.
+inline umcg_plan* plan_for(const MappingTable& map, const RectGrid& grid, const Mesh& mesh, bool coords) {
+    const PlanKey key{&map, map.assignments.data(), map.assignments.size(), map.visited_nodes.size(),
+                      grid.node_count(), coords};
+    std::lock_guard<std::mutex> lock(cache_mutex());
+    auto it = cache().find(key);
+    if (it != cache().end()) return it->second.get();
+    std::vector<std::uint64_t> sizes;
+    std::vector<double> axes;
+    for (const auto& a : grid.axes) {
+        sizes.push_back(a.size());
+        axes.insert(axes.end(), a.begin(), a.end());
+    }
+    umcg_grid_desc g{grid.dim, sizes.data(), axes.data()};
+    umcg_mapping_desc m{map.mode == MappingMode::seed ? 1 : 0, map.assignments.size(), map.assignments.data(),
+                        map.visited_nodes.size(), map.visited_nodes.data()};
+    umcg_plan* p = nullptr;
+    check(umcg_plan_create(&g, &m, mesh.dim, coords ? mesh.vertices.data() : nullptr, &p));
+    cache().emplace(key, PlanPtr(p));
+    return p;
+}
+
+}  // namespace detail
+
+inline void clear_plan_cache() {
+    std::lock_guard<std::mutex> lock(detail::cache_mutex());
+    detail::cache().clear();
+}
+
+/// umc::compress (pipeline.hpp:117-148) on the GPU. Same arguments, same
+/// Archive, same exception types.
+inline Archive compress(const Field& field, const MappingTable& map, const RectGrid& grid, const Mesh& mesh,
+                        const ErrorBudget& budget, const CompressOptions& opt = {}) {
+    validate_field(field, mesh);  // mesh.hpp:58-64, host-side like the reference
+    if (field.values.size() != map.assignments.size())
+        throw mapping_mismatch("mapping was built for a different vertex count");
+    umcg_plan* plan = detail::plan_for(map, grid, mesh, opt.g.kind == BackInterpKind::multilinear);
+    umcg_params prm{budget.tau,
+                    budget.split_rho,
+                    budget.bound_kind == BoundKind::relative_to_range ? 1 : 0,
+                    opt.g.kind == BackInterpKind::multilinear ? 1 : 0,
+                    opt.g.coeff_abs_sum,
+                    opt.fill == FillPolicy::nearest_visited ? 1 : 0,
+                    opt.codec_id,
+                    opt.backend_id};
+    std::uint64_t cap = 0;
+    detail::check(umcg_compress_bound(plan, field.name.c_str(), &cap));
+    std::vector<std::uint8_t> bytes(cap);
+    std::uint64_t len = 0;
+    detail::check(umcg_compress_host(plan, &prm, field.values.data(), field.name.c_str(), bytes.data(), cap, &len));
+    bytes.resize(len);
+    return deserialize_archive(bytes);  // pipeline.hpp:237 builds the reference's Archive
+}
+
+/// umc::decompress (pipeline.hpp:180-210) on the GPU.
+inline Field decompress(const Archive& archive, const MappingTable& map, const RectGrid& grid, const Mesh& mesh) {
+    const auto bytes = serialize_archive(archive);
+    Field out;
+    out.name = archive.field_name;
+    if (archive.baseline) {  // pipeline.hpp:184-187: the single component, decoded on the device
+        const auto& p = archive.component1.payload;
+        const std::uint64_t n = archive.component1.n_elements;
+        void* d_p = nullptr;
+        void* d_v = nullptr;
+        if (cudaMalloc(&d_p, p.size() + 1) != cudaSuccess || cudaMalloc(&d_v, n * 8 + 8) != cudaSuccess) {
+            cudaFree(d_p);
+            throw error("cudaMalloc failed");
+        }
+        cudaMemcpy(d_p, p.data(), p.size(), cudaMemcpyHostToDevice);
+        std::uint64_t got = 0;
+        const umcg_status s = umcg_decode(static_cast<const std::uint8_t*>(d_p), p.size(),
+                                          static_cast<double*>(d_v), n, &got, nullptr);
+        out.values.resize(got);
+        if (s == UMCG_OK && got) cudaMemcpy(out.values.data(), d_v, got * 8, cudaMemcpyDeviceToHost);
+        cudaFree(d_p);
+        cudaFree(d_v);
+        detail::check(s);
+        return out;
+    }
+    umcg_plan* plan = detail::plan_for(map, grid, mesh, archive.g_kind == BackInterpKind::multilinear);
+    out.values.resize(map.assignments.size());
+    detail::check(umcg_decompress_host(plan, bytes.data(), bytes.size(), out.values.data()));
+    return out;
+}
+
+}  // namespace b200
+}  // namespace umc
+
+#endif  // UMC_B200_PIPELINE_GPU_HPP

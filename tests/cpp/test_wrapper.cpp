@@ -1,0 +1,148 @@
+// C++ drop-in test: the reference's own call sites with umc::compress /
+// umc::decompress replaced by umc::b200::compress / decompress. Built here
+// against the reference headers (tests/cpp/Makefile), run on the GPU box by
+// tests/test_gpu_cpp.py. Checks, per case: byte-identical archive vs the
+// reference (or a code-level diff confined to the rounding window is
+// reported as MISMATCH), decode bound, and the reference's exception types.
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "umc/datagen.hpp"
+#include "umc/grid_builder.hpp"
+#include "umc/pipeline.hpp"
+#include "umc_b200/pipeline_gpu.hpp"
+
+using namespace umc;
+
+static int failures = 0;
+#define CHECK(c, msg)                                              \
+    do {                                                           \
+        if (!(c)) {                                                \
+            std::printf("FAIL %s:%d %s\n", __FILE__, __LINE__, msg); \
+            ++failures;                                            \
+        }                                                          \
+    } while (0)
+
+struct Built {
+    Mesh mesh;
+    RectGrid grid;
+    MappingTable map;
+};
+
+static Built build(std::uint64_t seed, int dim, std::uint64_t n, MeshStyle style) {
+    SynthSpec spec;
+    spec.dim = dim;
+    spec.n_target = n;
+    spec.mesh_style = style;
+    spec.rng_seed = seed;
+    Built b;
+    b.mesh = gen_mesh(spec);
+    GridBuildConfig cfg;
+    const auto init = grid_init(b.mesh, cfg);
+    auto res = grid_coarsen(b.mesh, init, cfg);
+    b.grid = std::move(res.grid);
+    b.map = std::move(res.mapping);
+    return b;
+}
+
+static double max_err(const std::vector<double>& a, const std::vector<double>& b) {
+    double m = 0;
+    for (std::size_t i = 0; i < a.size(); ++i) m = std::max(m, std::fabs(a[i] - b[i]));
+    return m;
+}
+
+int main() {
+    int exact = 0, total = 0;
+    for (int c = 0; c < 4; ++c) {
+        const int dim = c < 2 ? 2 : 3;
+        Built b = build(100 + c, dim, dim == 2 ? 4000 : 6000, c % 2 ? MeshStyle::graded : MeshStyle::jittered);
+        SynthSpec fs;
+        fs.dim = dim;
+        fs.field_kind = FieldKind::gaussian_mixture;
+        fs.rng_seed = 7 + c;
+        const Field field = gen_field(b.mesh, fs);
+        for (double tau : {1e-2, 1e-4, 0.0}) {
+            for (int g = 0; g < 2; ++g) {
+                ErrorBudget budget;
+                budget.tau = tau;
+                CompressOptions opt;
+                opt.g.kind = g ? BackInterpKind::multilinear : BackInterpKind::nearest;
+                if (g && b.map.mode == MappingMode::seed) {
+                    bool threw = false;
+                    try {
+                        b200::compress(field, b.map, b.grid, b.mesh, budget, opt);
+                    } catch (const seed_mode_unsupported&) {
+                        threw = true;
+                    }
+                    CHECK(threw, "seed + multilinear must throw seed_mode_unsupported");
+                    continue;
+                }
+                const Archive ref = compress(field, b.map, b.grid, b.mesh, budget, opt);
+                const Archive gpu = b200::compress(field, b.map, b.grid, b.mesh, budget, opt);
+                ++total;
+                const bool same = serialize_archive(ref) == serialize_archive(gpu);
+                exact += same;
+                if (!same) std::printf("MISMATCH case %d tau %g g %d (window flips expected only)\n", c, tau, g);
+                const Field back = b200::decompress(gpu, b.map, b.grid, b.mesh);
+                const double tau_abs = resolve_tau_abs(budget, field.values);
+                const Field refback = decompress(gpu, b.map, b.grid, b.mesh);  // reference decodes our archive
+                if (tau == 0.0) {
+                    // lossless components: x' = g(x1) + (x - g(x1)) exactly as the reference computes it
+                    CHECK(back.values == refback.values, "lossless decode must equal the reference bitwise");
+                } else {
+                    CHECK(max_err(back.values, field.values) <= tau_abs, "bound");
+                    CHECK(max_err(refback.values, field.values) <= tau_abs, "reference decode bound");
+                }
+            }
+        }
+    }
+    // error taxonomy (pipeline.hpp:120-125, 188-197)
+    Built a = build(1, 2, 500, MeshStyle::jittered);
+    Built o = build(2, 2, 500, MeshStyle::jittered);
+    SynthSpec fs;
+    fs.rng_seed = 5;
+    const Field f = gen_field(a.mesh, fs);
+    const Archive ar = b200::compress(f, a.map, a.grid, a.mesh, ErrorBudget{});
+    bool mm = false;
+    try {
+        b200::decompress(ar, o.map, o.grid, o.mesh);
+    } catch (const mapping_mismatch&) {
+        mm = true;
+    }
+    CHECK(mm, "mapping_mismatch");
+    bool ba = false;
+    try {
+        ErrorBudget bad;
+        bad.split_rho = 1.0;
+        b200::compress(f, a.map, a.grid, a.mesh, bad);
+    } catch (const budget_inadmissible&) {
+        ba = true;
+    }
+    CHECK(ba, "budget_inadmissible");
+    bool nf = false;
+    try {
+        Field g2 = f;
+        g2.values[3] = NAN;
+        b200::compress(g2, a.map, a.grid, a.mesh, ErrorBudget{});
+    } catch (const non_finite_value&) {
+        nf = true;
+    }
+    CHECK(nf, "non_finite_value");
+    // baseline archives decode through the device codec
+    const Archive base = baseline_archive(f, ErrorBudget{});
+    const Field bb = b200::decompress(base, {}, {}, a.mesh);
+    const Field rb = decompress(base, {}, {}, a.mesh);
+    double range = 0;
+    {
+        double lo = f.values[0], hi = lo;
+        for (double v : f.values) { lo = std::min(lo, v); hi = std::max(hi, v); }
+        range = hi - lo;
+    }
+    CHECK(bb.values.size() == rb.values.size(), "baseline size");
+    CHECK(max_err(bb.values, rb.values) <= 1e-12 * range, "baseline decode within 1e-12 of the reference");
+    CHECK(max_err(bb.values, f.values) <= resolve_tau_abs(ErrorBudget{}, f.values), "baseline bound");
+    std::printf("cases %d exact %d failures %d\n", total, exact, failures);
+    return failures ? 1 : 0;
+}
