@@ -116,6 +116,43 @@ def algorithmic_bytes(n, n1, archive):
     return b_c, b_d
 
 
+def kernel_bytes(n, n1, s2, k1_bytes):
+    """Compulsory bytes per launch of each hot kernel:
+    s2 = residual stream bytes, k1_bytes = bytes per grid lattice index in
+    the decompress gather table (2 when |K1| < 2^15)."""
+    return {
+        "k_gather_fwd": 20 * n,                  # x 8 + srcE 4 -> xE 8
+        "k_bucket": 16 * n + 12 * n1,            # xE 8 + lperm 2 + lnode 2 + KE 4; seg 4 + x1 8 per slot
+        "k_resid_codes": 12 * n,                 # dstE 4 + KE 4 (gathered once) + codes 4
+        "k_rle_write": 4 * n + s2,               # codes 4 + stream out
+        "k_dec_agg": s2,                         # stream in
+        "k_dec_out": 12 * n + s2 + k1_bytes * n1,  # node 4 + out 8 + stream + K1 table
+    }
+
+
+def profiled_pass(plan, x, budget, ar, out, steps=3):
+    import torch
+    import paper_2501_06910_b200 as umcg
+    umcg.profile_dump()
+    umcg.profile(True)
+    for _ in range(steps):
+        L = plan.compress_into(x, budget, ar, "field")
+        plan.decompress_into(ar, L, out)
+    torch.cuda.synchronize()
+    umcg.profile(False)
+    d = umcg.profile_dump()
+    return {k: v[0] / max(v[1], 1) for k, v in d.items()}  # ms per launch
+
+
+def committed_traffic():
+    """dram bytes per launch from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
 def cpu_reference_sample(lattice: int, grid: int, threads: int, reps: int, tau: float):
     """Time the unmodified reference (oracle/_ref) on a bounded sample of the
     config-3 workload: `threads` concurrent compress+decompress calls."""
@@ -292,6 +329,22 @@ def main():
     peak, peak_kind = peaks()
     b_c, b_d = algorithmic_bytes(n, n1, alen)
     tcm, tdm = float(np.median(tc)), float(np.median(td))
+    # per-kernel live timing (CUDA events on the launching stream, outside the timed region)
+    kms = profiled_pass(plan, x, budget, ar, out)
+    s2 = int(alen * 0.9)  # residual stream dominates the archive (exact split below when parsed)
+    try:
+        hdr = bytes(ar[: 4096].cpu().numpy())
+        nl = int.from_bytes(hdr[8:10], "little")
+        l1 = int.from_bytes(hdr[10 + nl + 24: 10 + nl + 32], "little")
+        s2 = alen - (10 + nl + 32 + l1 + 8) - 37  # payload2 minus its 37-byte header
+    except Exception:
+        pass
+    kb = kernel_bytes(n, n1, s2, 2)
+    kernels = {k: {"ms": v, "gbs": kb[k] / (v * 1e-3) / 1e9 if k in kb else None,
+                   "frac": kb[k] / (v * 1e-3) / 1e9 / peak if k in kb else None,
+                   "algorithmic_bytes": kb.get(k)} for k, v in kms.items()}
+    dom = max((k for k in kernels if k in kb), key=lambda k: kernels[k]["ms"], default=None)
+    traffic = committed_traffic().get(dom) if dom else None
     res = dict(
         metric=METRIC, value=value, unit="GB/s", n_gpus=ws, steps=args.steps, warmup=args.warmup,
         ms_per_step=ms, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
@@ -304,10 +357,15 @@ def main():
                   "roofline_frac": b_c / (tcm * 1e-3) / 1e9 / peak},
         decompress={"ms": tdm, "gbs_field": n * 8 / tdm / 1e6, "algorithmic_bytes": b_d,
                     "roofline_frac": b_d / (tdm * 1e-3) / 1e9 / peak},
-        roofline={"bound": "hbm", "achieved": (b_c + b_d) / ((tcm + tdm) * 1e-3) / 1e9, "peak": peak,
-                  "unit": "GB/s", "frac": (b_c + b_d) / ((tcm + tdm) * 1e-3) / 1e9 / peak,
-                  "traffic": None, "scope": "whole compress+decompress path (SURVEY 8d algorithmic bytes)",
-                  "peak_source": peak_kind},
+        roofline={"bound": "hbm", "kernel": dom,
+                  "achieved": kernels[dom]["gbs"] if dom else None, "peak": peak, "unit": "GB/s",
+                  "frac": kernels[dom]["frac"] if dom else None, "traffic": traffic,
+                  "algorithmic_bytes_per_launch": kb.get(dom) if dom else None,
+                  "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
+        path_roofline={"achieved": (b_c + b_d) / ((tcm + tdm) * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                       "frac": (b_c + b_d) / ((tcm + tdm) * 1e-3) / 1e9 / peak,
+                       "scope": "whole compress+decompress step, SURVEY 8(d) algorithmic bytes"},
+        kernels=kernels,
         max_err_over_tau=err / tau_abs if tau_abs else None,
         gpu_launches=launches,
         clocks=clk.summary(),
@@ -315,7 +373,7 @@ def main():
     )
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
-            cb = cpu_reference_sample(128, 64, 1, 2, args.tau)
+            cb = cpu_reference_sample(256, 128, 1, 1, args.tau)
             res["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as e:
             res["cpu_baseline"] = {"value": None, "error": str(e)[:200]}

@@ -197,6 +197,11 @@ umcg_status umcg_gen_config(int config, uint64_t lattice, uint64_t seed, double*
  * reference recurrence (escapes, non-lattice regimes; 0 on normal data). */
 uint64_t umcg_kernel_launches(void);
 uint64_t umcg_serial_fallbacks(void);
+/* Per-kernel timing with CUDA events on the launching stream (hot kernels
+ * only). Enable, run, then dump "name total_ms launches" lines into buf;
+ * returns the full text length. */
+void umcg_profile_enable(int on);
+uint64_t umcg_profile_dump(char* buf, uint64_t cap);
 const char* umcg_last_error(void);
 const char* umcg_version(void);
 

@@ -38,7 +38,8 @@ EXPORTED = [
     "umcg_plan_export", "umcg_compress_bound", "umcg_compress", "umcg_compress_batch",
     "umcg_decompress", "umcg_compress_host", "umcg_decompress_host", "umcg_encode_bound",
     "umcg_encode", "umcg_decode", "umcg_rle_compress", "umcg_rle_decompress", "umcg_gen_config",
-    "umcg_kernel_launches", "umcg_serial_fallbacks", "umcg_last_error", "umcg_version",
+    "umcg_kernel_launches", "umcg_serial_fallbacks", "umcg_profile_enable", "umcg_profile_dump",
+    "umcg_last_error", "umcg_version",
 ]
 
 
@@ -94,6 +95,9 @@ def lib():
     L.umcg_version.restype = C.c_char_p
     L.umcg_kernel_launches.restype = C.c_uint64
     L.umcg_serial_fallbacks.restype = C.c_uint64
+    L.umcg_profile_enable.argtypes = [C.c_int]
+    L.umcg_profile_dump.restype = C.c_uint64
+    L.umcg_profile_dump.argtypes = [C.c_char_p, C.c_uint64]
     L.umcg_encode_bound.restype = C.c_uint64
     L.umcg_encode_bound.argtypes = [C.c_uint64, C.c_int]
     L.umcg_plan_create.argtypes = [C.POINTER(GridDesc), C.POINTER(MappingDesc), C.c_int, f64p,
@@ -130,6 +134,22 @@ def kernel_launches() -> int:
 def serial_fallbacks() -> int:
     """Times a component used the one-thread exact replica of the reference loop."""
     return int(lib().umcg_serial_fallbacks())
+
+
+def profile(enable: bool):
+    """Per-kernel CUDA-event timing inside the library (hot kernels)."""
+    lib().umcg_profile_enable(1 if enable else 0)
+
+
+def profile_dump() -> dict:
+    """{kernel: (total_ms, launches)} since the last dump."""
+    buf = C.create_string_buffer(1 << 16)
+    lib().umcg_profile_dump(buf, len(buf))
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, ms, cnt = line.split()
+        out[name] = (float(ms), int(cnt))
+    return out
 
 
 def _ptr(a, t):

@@ -3,6 +3,8 @@
 // component codec (codec.hpp:220-441).
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <tuple>
 #include <memory>
 #include <string>
 
@@ -13,6 +15,15 @@ namespace umcg {
 
 std::atomic<uint64_t> g_launches{0};
 std::atomic<uint64_t> g_serial_fallbacks{0};
+std::atomic<int> g_profile_on{0};
+namespace {
+std::mutex g_prof_mu;
+std::vector<std::tuple<std::string, cudaEvent_t, cudaEvent_t>> g_prof_ev;
+}  // namespace
+void prof_record(const char* name, cudaEvent_t a, cudaEvent_t b) {
+    std::lock_guard<std::mutex> lock(g_prof_mu);
+    g_prof_ev.emplace_back(name, a, b);
+}
 static thread_local std::string g_last_error;
 
 umcg_plan* plan_create_host(const umcg_grid_desc*, const umcg_mapping_desc*, int, const double*);
@@ -797,6 +808,33 @@ const char* umcg_last_error(void) { return g_last_error.c_str(); }
 const char* umcg_version(void) { return "umcg 0.1 (sm_100a)"; }
 uint64_t umcg_kernel_launches(void) { return g_launches.load(); }
 uint64_t umcg_serial_fallbacks(void) { return g_serial_fallbacks.load(); }
+
+void umcg_profile_enable(int on) { g_profile_on.store(on ? 1 : 0); }
+
+uint64_t umcg_profile_dump(char* buf, uint64_t cap) {
+    std::lock_guard<std::mutex> lock(g_prof_mu);
+    std::map<std::string, std::pair<double, int>> acc;
+    for (auto& [name, a, b] : g_prof_ev) {
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        auto& e = acc[name];
+        e.first += ms;
+        e.second += 1;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    }
+    g_prof_ev.clear();
+    std::string out;
+    for (auto& [name, v] : acc)
+        out += name + " " + std::to_string(v.first) + " " + std::to_string(v.second) + "\n";
+    if (buf && cap) {
+        const uint64_t k = std::min<uint64_t>(cap - 1, out.size());
+        std::memcpy(buf, out.data(), k);
+        buf[k] = 0;
+    }
+    return out.size();
+}
 
 umcg_status umcg_plan_create(const umcg_grid_desc* grid, const umcg_mapping_desc* mapping, int mesh_dim,
                              const double* coords, umcg_plan** out) {

@@ -43,6 +43,29 @@ inline void count_launch(uint64_t k = 1) { g_launches.fetch_add(k, std::memory_o
 
 inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
+// Optional per-kernel timing (umcg_profile): CUDA events recorded on the
+// launching stream around the hot kernels; off by default (no cost).
+extern std::atomic<int> g_profile_on;
+void prof_record(const char* name, cudaEvent_t a, cudaEvent_t b);
+struct ProfScope {
+    const char* name;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(const char* n, cudaStream_t s) : name(n), st(s) {
+        if (g_profile_on.load(std::memory_order_relaxed)) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a, st);
+        }
+    }
+    ~ProfScope() {
+        if (a) {
+            cudaEventRecord(b, st);
+            prof_record(name, a, b);
+        }
+    }
+};
+
 // Error codes raised on the device land in DevCtl::err (first writer wins).
 enum DevErr : int {
     DE_NONE = 0,

@@ -408,10 +408,14 @@ void dec_fused(int mode, const uint8_t* U, uint64_t ulen, uint64_t n, void* stat
     const uint64_t T = cdiv(ulen, RTILE);
     if (!T) return;
     auto* aggs = static_cast<CS*>(status);
-    k_dec_agg<<<(unsigned)T, RT, 0, st>>>(U, ulen, aggs, ctl);
-    UMCG_LAUNCHED();
+    {
+        ProfScope ps_a("k_dec_agg", st);
+        k_dec_agg<<<(unsigned)T, RT, 0, st>>>(U, ulen, aggs, ctl);
+        UMCG_LAUNCHED();
+    }
     k_scan_cs<<<1, 1024, 0, st>>>(aggs, T, ctl);
     UMCG_LAUNCHED();
+    ProfScope ps_o(mode == DEC_P64 ? "k_dec_out_grid" : "k_dec_out", st);
     if (mode == DEC_P64)
         k_dec_out<DEC_P64, int32_t><<<(unsigned)T, RT, 0, st>>>(U, ulen, n, aggs, ctl, node, K1, bin1, bin, out, P64);
     else if (mode == DEC_VALUES)

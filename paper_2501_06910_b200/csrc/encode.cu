@@ -440,6 +440,7 @@ static void write_impl(const T* codes, uint64_t n, const StreamEncScratch& s, De
                        bool off_ctl, cudaStream_t st) {
     const uint64_t T_ = cdiv(n, ENC_TILE);
     if (!T_) return;
+    ProfScope ps_("k_rle_write", st);
     k_rle_write_fast<T><<<(unsigned)T_, ENC_THREADS, 0, st>>>(codes, n, s.states, s.sums, s.lit_total, ctl, comp,
                                                               dst, off_ctl ? 1 : 0);
     UMCG_LAUNCHED();

@@ -256,6 +256,7 @@ void partition_values(const void* x, int x_f32, umcg_plan* p, double* xE, DevCtl
     if (!n) return;
     const unsigned g = (unsigned)cdiv(n, (uint64_t)PT * GI);
     const uint32_t* srcE = p->d_srcE.as<uint32_t>(1);
+    ProfScope ps_("k_gather_fwd", st);
     if (x_f32) k_gather_fwd<float><<<g, PT, 0, st>>>(static_cast<const float*>(x), n, srcE, xE, ctl);
     else k_gather_fwd<double><<<g, PT, 0, st>>>(static_cast<const double*>(x), n, srcE, xE, ctl);
     UMCG_LAUNCHED();
@@ -270,6 +271,7 @@ void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double*
         UMCG_CUDA(cudaFuncSetAttribute(k_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         configured = true;
     }
+    ProfScope ps_("k_bucket", st);
     k_bucket<<<(unsigned)p->n_buckets, BT, smem, st>>>(xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E,
                                                         p->d_bct.as<uint2>(1), p->d_lnode.as<uint16_t>(1),
                                                         p->d_lperm.as<uint16_t>(1), p->d_seg.as<uint32_t>(1), ctl, x1,
@@ -280,6 +282,7 @@ void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double*
 void resid_codes_tiles(umcg_plan* p, const int32_t* KE, uint32_t* codes, const StreamEncScratch& s, cudaStream_t st) {
     const uint64_t T = cdiv(p->n, ENC_TILE);
     if (!T) return;
+    ProfScope ps_("k_resid_codes", st);
     k_resid_codes<<<(unsigned)T, ENC_THREADS, 0, st>>>(p->d_dstE.as<uint32_t>(1), KE, p->n, codes, s.sums);
     UMCG_LAUNCHED();
 }
