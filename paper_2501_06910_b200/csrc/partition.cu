@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
                                               uint64_t B, uint32_t E, const uint2* __restrict__ bct,
                                               const uint16_t* __restrict__ lnode,
                                               const uint16_t* __restrict__ lperm, const uint32_t* __restrict__ seg,
-                                              DevCtl* ctl, double* __restrict__ x1, int32_t* __restrict__ KE) {
+                                              DevCtl* ctl, double* __restrict__ x1, int32_t* __restrict__ KE,
+                                              int heavy_only) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* xs = reinterpret_cast<double*>(smem);                      // [kBucketCap]
     double* x1s = xs + kBucketCap;                                     // [kBucketNodes]
@@ -117,6 +118,7 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
     // chunk table (one chunk per epoch, bucket-major) + segment offsets
     for (uint32_t e = threadIdx.x; e <= E; e += BT) ch[e] = __ldg(&bct[b * (uint64_t)(E + 1) + e]);
     const bool heavy = m > kBucketCap;
+    if (heavy_only && !heavy) return;
     if (!heavy)
         for (uint32_t j = threadIdx.x; j <= nj; j += BT) sg[j] = __ldg(&seg[j0 + j]) - s0;
     __syncthreads();
@@ -198,6 +200,143 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
     }
 }
 
+constexpr int BTP = 512;  // threads per persistent bucket CTA
+
+// ---- software-pipelined persistent variant ---------------------------------
+// Persistent CTAs walk the regular (<= kBucketCap) buckets round-robin with
+// two shared-memory stages: while bucket k is summed and quantized, the
+// cp.async copies of bucket k+1 (xE chunks, lperm, lnode, segment offsets)
+// are in flight, and the chunk table of bucket k+2 is prefetched to
+// registers. Same arithmetic, same order as k_bucket.
+__device__ __forceinline__ void cp_async(void* smem_dst, const void* gmem_src, int bytes) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+    if (bytes == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem_src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+struct PipeStage {
+    double* xs;     // [kBucketCap]
+    uint16_t* lp;   // [kBucketCap + 2]
+    uint16_t* ln;   // [kBucketCap + 2]
+    uint32_t* sg;   // [kBucketNodes + 2]
+    uint2* ch;      // [E + 1]
+};
+
+__device__ __forceinline__ uint32_t chunk_of(const uint2* ch, uint32_t E, uint32_t l) {
+    uint32_t lo = 0, hi = E;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (ch[mid].x <= l) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ void issue_bucket(const PipeStage& S, const double* __restrict__ xE,
+                                             const uint16_t* __restrict__ lperm, const uint16_t* __restrict__ lnode,
+                                             const uint32_t* __restrict__ seg, uint32_t s0, uint32_t m, uint32_t j0,
+                                             uint32_t nj, uint32_t E) {
+    (void)m;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (uint32_t e = warp; e < E; e += BTP / 32) {  // one warp per epoch chunk
+        const uint2 c0 = S.ch[e], c1 = S.ch[e + 1];
+        for (uint32_t l = c0.x + lane; l < c1.x; l += 32) cp_async(&S.xs[l], &xE[c0.y + (l - c0.x)], 8);
+    }
+    const uint32_t a0 = s0 & ~1u, words = (s0 + m - a0 + 1) >> 1;
+    for (uint32_t w = threadIdx.x; w < words; w += BTP) {
+        cp_async(reinterpret_cast<uint32_t*>(S.lp) + w, reinterpret_cast<const uint32_t*>(lperm + a0) + w, 4);
+        cp_async(reinterpret_cast<uint32_t*>(S.ln) + w, reinterpret_cast<const uint32_t*>(lnode + a0) + w, 4);
+    }
+    for (uint32_t j = threadIdx.x; j <= nj; j += BTP) cp_async(&S.sg[j], &seg[j0 + j], 4);
+}
+
+__global__ void __launch_bounds__(BTP) k_bucket_pipe(const double* __restrict__ xE, const uint32_t* __restrict__ bk,
+                                                   uint64_t B, uint32_t E, const uint2* __restrict__ bct,
+                                                   const uint32_t* __restrict__ regular, uint32_t n_regular,
+                                                   const uint16_t* __restrict__ lnode,
+                                                   const uint16_t* __restrict__ lperm,
+                                                   const uint32_t* __restrict__ seg, DevCtl* ctl,
+                                                   double* __restrict__ x1, int32_t* __restrict__ KE) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    PipeStage S[2];
+    unsigned char* p = smem;
+    double* x1s = reinterpret_cast<double*>(p);
+    p += kBucketNodes * 8;
+    for (int st = 0; st < 2; ++st) {
+        S[st].xs = reinterpret_cast<double*>(p);
+        p += kBucketCap * 8;
+        S[st].sg = reinterpret_cast<uint32_t*>(p);
+        p += (kBucketNodes + 2) * 4;
+        S[st].ch = reinterpret_cast<uint2*>(p);
+        p += (E + 1) * 8;
+        S[st].lp = reinterpret_cast<uint16_t*>(p);
+        p += (kBucketCap + 4) * 2;
+        S[st].ln = reinterpret_cast<uint16_t*>(p);
+        p += (kBucketCap + 4) * 2;
+        p = reinterpret_cast<unsigned char*>(((uintptr_t)p + 15) & ~(uintptr_t)15);
+    }
+    const uint32_t* bstart = bk;
+    const uint32_t* bnode = bk + B + 1;
+    const double bin = ctl->bin[1], tau = ctl->tau_c[1];
+    const uint32_t G = gridDim.x;
+    uint32_t k = blockIdx.x;
+    if (k >= n_regular) return;
+    // prologue: chunk table of the first bucket, copies of the first bucket,
+    // chunk table of the second bucket into registers
+    uint32_t b = regular[k];
+    if (threadIdx.x <= E) S[0].ch[threadIdx.x] = __ldg(&bct[b * (uint64_t)(E + 1) + threadIdx.x]);
+    __syncthreads();
+    issue_bucket(S[0], xE, lperm, lnode, seg, bstart[b], bstart[b + 1] - bstart[b], bnode[b], bnode[b + 1] - bnode[b], E);
+    cp_commit();
+    uint2 chreg = make_uint2(0, 0);
+    if (k + G < n_regular && threadIdx.x <= E) chreg = __ldg(&bct[regular[k + G] * (uint64_t)(E + 1) + threadIdx.x]);
+    for (uint32_t it = 0; k < n_regular; ++it, k += G) {
+        const int st = it & 1;
+        b = regular[k];
+        const bool has_next = k + G < n_regular;
+        if (has_next && threadIdx.x <= E) S[st ^ 1].ch[threadIdx.x] = chreg;
+        __syncthreads();
+        if (has_next) {
+            const uint32_t bn = regular[k + G];
+            issue_bucket(S[st ^ 1], xE, lperm, lnode, seg, bstart[bn], bstart[bn + 1] - bstart[bn], bnode[bn],
+                         bnode[bn + 1] - bnode[bn], E);
+            if (k + 2 * G < n_regular && threadIdx.x <= E)
+                chreg = __ldg(&bct[regular[k + 2 * G] * (uint64_t)(E + 1) + threadIdx.x]);
+        }
+        cp_commit();
+        cp_wait<1>();
+        __syncthreads();
+        const PipeStage& C = S[st];
+        const uint32_t s0 = bstart[b], m = bstart[b + 1] - s0, j0 = bnode[b], nj = bnode[b + 1] - j0;
+        const uint32_t off = s0 & 1u;
+        // interpolate_to_grid (interp.hpp:58-64): 0.0 + x_a + x_b + ... in ascending vertex order
+        for (uint32_t j = threadIdx.x; j < nj; j += BTP) {
+            const uint32_t k0 = C.sg[j] - s0, k1 = C.sg[j + 1] - s0;
+            double s = 0.0;
+            for (uint32_t q = k0; q < k1; ++q) s = __dadd_rn(s, C.xs[C.lp[q + off]]);
+            const double v = k1 > k0 ? __ddiv_rn(s, (double)(k1 - k0)) : 0.0;
+            x1s[j] = v;
+            x1[j0 + j] = v;
+        }
+        __syncthreads();
+        // compute_residuals (interp.hpp:161-170) + lattice index (codec.hpp:307-314)
+        {
+            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+            for (uint32_t e = warp; e < E; e += BTP / 32) {
+                const uint2 c0 = C.ch[e], c1 = C.ch[e + 1];
+                for (uint32_t l = c0.x + lane; l < c1.x; l += 32)
+                    KE[c0.y + (l - c0.x)] = resid_k(__dsub_rn(C.xs[l], x1s[C.ln[l + off]]), bin, tau, ctl);
+            }
+        }
+        __syncthreads();
+    }
+    cp_wait<0>();
+}
+
 // Vertex order: q_i = K_i - K_{i-1} through dstE (gather inside an epoch
 // window), zigzag codes, RLE tile summary.
 __global__ void __launch_bounds__(ENC_THREADS) k_resid_codes(const uint32_t* __restrict__ dst,
@@ -264,19 +403,39 @@ void partition_values(const void* x, int x_f32, umcg_plan* p, double* xE, DevCtl
 
 void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double* x1, int32_t* KE, cudaStream_t st) {
     if (!p->n_buckets) return;
+    ProfScope ps_("k_bucket", st);
     const uint32_t E = (uint32_t)p->n_epochs;
-    const size_t smem = kBucketCap * 8 + kBucketNodes * 8 + (kBucketNodes + 2) * 4 + ((size_t)E + 1) * 8 + kBucketCap * 4 + 16;
     static bool configured = false;
     if (!configured) {
         UMCG_CUDA(cudaFuncSetAttribute(k_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        UMCG_CUDA(cudaFuncSetAttribute(k_bucket_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         configured = true;
     }
-    ProfScope ps_("k_bucket", st);
-    k_bucket<<<(unsigned)p->n_buckets, BT, smem, st>>>(xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E,
-                                                        p->d_bct.as<uint2>(1), p->d_lnode.as<uint16_t>(1),
-                                                        p->d_lperm.as<uint16_t>(1), p->d_seg.as<uint32_t>(1), ctl, x1,
-                                                        KE);
-    UMCG_LAUNCHED();
+    const bool pipe = E + 1 <= BTP && p->n_regular > 0;
+    if (pipe) {
+        size_t smem = kBucketNodes * 8;
+        for (int st2 = 0; st2 < 2; ++st2)
+            smem = ((smem + kBucketCap * 8 + (kBucketNodes + 2) * 4 + ((size_t)E + 1) * 8 + (kBucketCap + 4) * 4) + 15) & ~(size_t)15;
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const unsigned g = (unsigned)std::min<uint64_t>(p->n_regular, (uint64_t)sms * 2);
+        k_bucket_pipe<<<g, BTP, smem, st>>>(xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E, p->d_bct.as<uint2>(1),
+                                           p->d_regular.as<uint32_t>(1), (uint32_t)p->n_regular,
+                                           p->d_lnode.as<uint16_t>(1), p->d_lperm.as<uint16_t>(1),
+                                           p->d_seg.as<uint32_t>(1), ctl, x1, KE);
+        UMCG_LAUNCHED();
+    }
+    if (!pipe || p->n_regular < p->n_buckets) {
+        // all buckets (no pipeline possible) or the heavy single-slot buckets
+        const size_t smem = kBucketCap * 8 + kBucketNodes * 8 + (kBucketNodes + 2) * 4 + ((size_t)E + 1) * 8 +
+                            kBucketCap * 4 + 16;
+        k_bucket<<<(unsigned)p->n_buckets, BT, smem, st>>>(xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E,
+                                                            p->d_bct.as<uint2>(1), p->d_lnode.as<uint16_t>(1),
+                                                            p->d_lperm.as<uint16_t>(1), p->d_seg.as<uint32_t>(1), ctl,
+                                                            x1, KE, pipe ? 1 : 0);
+        UMCG_LAUNCHED();
+    }
 }
 
 void resid_codes_tiles(umcg_plan* p, const int32_t* KE, uint32_t* codes, const StreamEncScratch& s, cudaStream_t st) {

@@ -273,6 +273,15 @@ void plan_build_buckets(umcg_plan* p, cudaStream_t st) {
         tab[B + 1 + b] = bnode[b];
     }
     p->n_buckets = B;
+    {
+        std::vector<uint32_t> reg;
+        for (uint64_t b = 0; b < B; ++b)
+            if (tab[b + 1] - tab[b] <= kBucketCap) reg.push_back((uint32_t)b);
+        p->n_regular = reg.size();
+        uint32_t* dr = p->d_regular.as<uint32_t>(reg.size() + 1);
+        if (!reg.empty()) UMCG_CUDA(cudaMemcpyAsync(dr, reg.data(), reg.size() * 4, cudaMemcpyHostToDevice, st));
+        UMCG_CUDA(cudaStreamSynchronize(st));
+    }
     uint32_t* dbk = p->d_bk.as<uint32_t>(tab.size());
     UMCG_CUDA(cudaMemcpyAsync(dbk, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice, st));
     const uint32_t* bstart = dbk;

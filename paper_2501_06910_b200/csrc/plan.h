@@ -40,6 +40,8 @@ struct umcg_plan {
     umcg::DevBuf d_dstE;     // u32 [n]    layout-E position of vertex i
     umcg::DevBuf d_ech;      // u32 [E*(B+1)] offset of bucket b inside epoch e's block
     umcg::DevBuf d_bct;      // uint2 [B*(E+1)] per bucket: (first bucket-local index, layout-E base) per epoch
+    umcg::DevBuf d_regular;  // u32 [n_regular] buckets with <= kBucketCap vertices (pipelined kernel)
+    uint64_t n_regular = 0;
     umcg::DevBuf d_lnode;    // u16 [n]    bucket-local slot of bucket-order element
     umcg::DevBuf d_lperm;    // u16 [n]    bucket-local element of node-sorted position
     umcg::DevBuf d_bk;       // u32 [2*(B+1)] bucket start (vertex) and first slot
