@@ -45,6 +45,7 @@ struct StreamDecScratch {
     DevBuf tokens;   // token table
     DevBuf unpacked; // expanded byte stream
     DevBuf counts;   // per-tile code-end counts
+    DevBuf parse;    // parallel token parse: exit table, chunk entries
 };
 // Returns on host after a synchronization: fills codes[0..n). Throws corrupt_payload.
 void stream_decode(const uint8_t* d_stream, uint64_t len, uint64_t n, uint64_t* d_codes,

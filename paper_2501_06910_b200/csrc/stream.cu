@@ -22,12 +22,14 @@ struct Token {
 };
 
 // Serial walk over token headers (rle_decompress, lossless.hpp:53-70).
+// Stops after max_tok tokens; aux[1] = 1 when the stream is not finished
+// (the caller then switches to the parallel parse below).
 __global__ void k_token_walk(const uint8_t* __restrict__ s, uint64_t len, Token* __restrict__ tok,
-                             uint64_t tok_cap, DevCtl* ctl) {
+                             uint64_t tok_cap, uint64_t max_tok, DevCtl* ctl) {
     if (threadIdx.x | blockIdx.x) return;
     uint64_t pos = 0, u = 0, k = 0;
     int err = 0;
-    while (pos < len) {
+    while (pos < len && k < max_tok) {
         const uint8_t tag = s[pos++];
         uint64_t v = 0;
         bool done = false;
@@ -55,6 +57,284 @@ __global__ void k_token_walk(const uint8_t* __restrict__ s, uint64_t len, Token*
     if (err) set_err(ctl, err);
     ctl->count = k;
     ctl->aux[0] = u;  // unpacked length
+    ctl->aux[1] = !err && pos < len;
+}
+
+// ---------------------------------------------------------------------------
+// Parallel token parse for streams with many tokens.
+//
+// The token chain is a functional graph on stream offsets: next(p) = p + 1 +
+// |varint| (+ literal length). Every offset is a potential token start.
+//  1. k_tok_jump: per chunk of PJ_C offsets, the "exit" of EVERY offset (the
+//     first chain offset at or past the chunk end) by pointer jumping in
+//     shared memory, plus the chunk's set of distinct live exits (<= PJ_K;
+//     garbage chains inside literal data converge to a handful of exits).
+//  2. k_tok_groups: per group of PJ_G chunks, one lane per possible entry
+//     (the distinct exits of the chunk before the group) follows its chain
+//     through the group's exit tables; records each chunk's entry per lane
+//     and the group's exit per lane.
+//  3. k_tok_resolve: one warp chains the groups from offset 0 -- a shared
+//     memory match per group -- and picks each group's true lane (groups with
+//     too many possible entries are chained chunk by chunk instead).
+//  4. k_tok_walk_chunks: every chunk re-walks its own tokens from its
+//     resolved entry, verifying the chain (must land exactly on the next
+//     chunk's entry, no malformed header) and counting, then emitting, the
+//     token table.
+// Any disagreement sends the caller to the serial walk, which reports the
+// reference's exact error.
+// ---------------------------------------------------------------------------
+constexpr int PJ_THREADS = 1024;
+constexpr uint64_t PJ_C = 8192;  // offsets per chunk
+constexpr int PJ_HALO = 16;      // tag + 10-byte varint past the chunk end
+constexpr int PJ_K = 32;         // distinct exits kept per chunk (one warp)
+constexpr int PJ_HS = 128;       // hash slots for the distinct-exit set
+constexpr uint64_t PJ_G = 64;    // chunks per group
+constexpr uint64_t PJ_DEAD = ~0ull;
+constexpr uint32_t PJ_MANY = 0xFFFFFFFFu;
+constexpr uint8_t PJ_SLOW = 0xFF;
+constexpr size_t PJ_SMEM = PJ_C * 8 + PJ_C + PJ_HALO;
+
+// One token header at p (< len), the checks of k_token_walk: next token
+// start, or PJ_DEAD when the header is malformed or the literal overruns.
+template <class At>
+__device__ __forceinline__ uint64_t tok_next(At at, uint64_t len, uint64_t p, uint64_t& v, uint32_t& tag) {
+    tag = at(p++);
+    v = 0;
+    if (tag > 1) return PJ_DEAD;
+    for (int shift = 0; shift < 64; shift += 7) {
+        if (p >= len) return PJ_DEAD;
+        const uint32_t b = at(p++);
+        v |= (uint64_t)(b & 0x7f) << shift;
+        if (!(b & 0x80)) {
+            if (tag == 0) return p;
+            return len - p < v ? PJ_DEAD : p + v;
+        }
+    }
+    return PJ_DEAD;
+}
+
+__global__ void __launch_bounds__(PJ_THREADS) k_tok_jump(const uint8_t* __restrict__ s, uint64_t len,
+                                                         uint32_t* __restrict__ ex, uint32_t* __restrict__ dcount,
+                                                         uint64_t* __restrict__ dvals) {
+    extern __shared__ __align__(16) uint8_t pj_smem[];
+    __shared__ unsigned long long hs[PJ_HS];
+    __shared__ int hcount, hpos;
+    uint64_t* nx = reinterpret_cast<uint64_t*>(pj_smem);
+    uint8_t* sb = pj_smem + PJ_C * 8;
+    const uint64_t P = blockIdx.x * PJ_C;
+    const uint64_t E = min(len, P + PJ_C);
+    const int n = (int)(E - P);
+    for (int i = threadIdx.x; i < (int)PJ_C + PJ_HALO; i += PJ_THREADS) sb[i] = P + i < len ? s[P + i] : 0;
+    for (int i = threadIdx.x; i < PJ_HS; i += PJ_THREADS) hs[i] = PJ_DEAD;
+    if (threadIdx.x == 0) hcount = hpos = 0;
+    __syncthreads();
+    auto at = [&](uint64_t q) -> uint32_t { return sb[q - P]; };
+    for (int i = threadIdx.x; i < n; i += PJ_THREADS) {
+        uint64_t v;
+        uint32_t tag;
+        nx[i] = tok_next(at, len, P + i, v, tag);
+    }
+    __syncthreads();
+    // Pointer jumping. Updates are in place: a reader sees either the old or
+    // the new successor, both on the same chain, so the fixed point is exact.
+    for (;;) {
+        int moved = 0;
+        for (int i = threadIdx.x; i < n; i += PJ_THREADS) {
+            const uint64_t v = nx[i];
+            if (v < E) {
+                const uint64_t w = nx[v - P];
+                nx[i] = w;
+                moved |= w < E;
+            }
+        }
+        if (!__syncthreads_or(moved)) break;
+    }
+    // exit table + distinct live exits (warp-deduplicated hash insert)
+    const int lane = threadIdx.x & 31;
+    for (int base = 0; base < n; base += PJ_THREADS) {
+        const int i = base + threadIdx.x;
+        const uint64_t v = i < n ? nx[i] : PJ_DEAD;
+        if (i < n) ex[P + i] = v == PJ_DEAD ? 0xFFFFFFFFu : (uint32_t)(v - P);
+        const unsigned m = __match_any_sync(0xffffffffu, v);
+        if (v != PJ_DEAD && __ffs(m) - 1 == lane && *(volatile int*)&hcount <= PJ_K) {
+            unsigned h = (unsigned)((v * 0x9E3779B97F4A7C15ull) >> 57);
+            int k = 0;
+            for (; k < PJ_HS; ++k, h = (h + 1) & (PJ_HS - 1)) {
+                const unsigned long long old = atomicCAS(&hs[h], PJ_DEAD, v);
+                if (old == PJ_DEAD) { atomicAdd(&hcount, 1); break; }
+                if (old == v) break;
+            }
+            if (k == PJ_HS) atomicAdd(&hcount, PJ_K + 1);
+        }
+    }
+    __syncthreads();
+    const int hc = hcount;
+    if (threadIdx.x < PJ_HS && hc <= PJ_K) {
+        const uint64_t v = hs[threadIdx.x];
+        if (v != PJ_DEAD) dvals[blockIdx.x * PJ_K + atomicAdd(&hpos, 1)] = v;
+    }
+    if (threadIdx.x == 0) dcount[blockIdx.x] = hc <= PJ_K ? (uint32_t)hc : PJ_MANY;
+}
+
+// One warp per group of PJ_G chunks; lane = one possible group entry.
+__global__ void __launch_bounds__(32) k_tok_groups(const uint32_t* __restrict__ ex,
+                                                   const uint32_t* __restrict__ dcount,
+                                                   const uint64_t* __restrict__ dvals, uint64_t nc, uint64_t len,
+                                                   uint64_t* __restrict__ gent, uint64_t* __restrict__ gin,
+                                                   uint64_t* __restrict__ gout, uint32_t* __restrict__ gn) {
+    const uint64_t g = blockIdx.x;
+    const int lane = threadIdx.x;
+    const uint64_t c0 = g * PJ_G, c1 = min(nc, c0 + PJ_G);
+    uint32_t ne = 1;
+    uint64_t s = lane == 0 ? 0 : PJ_DEAD;
+    if (g) {
+        ne = dcount[c0 - 1];
+        if (ne == PJ_MANY) {
+            if (lane == 0) gn[g] = PJ_MANY;
+            return;
+        }
+        s = lane < (int)ne ? dvals[(c0 - 1) * PJ_K + lane] : PJ_DEAD;
+    }
+    gin[g * 32 + lane] = s;
+    for (uint64_t c = c0; c < c1; ++c) {
+        gent[c * 32 + lane] = s;
+        const uint64_t P = c * PJ_C, E = min(len, P + PJ_C);
+        if (s < E) {
+            const uint32_t r = ex[s];
+            s = r == 0xFFFFFFFFu ? PJ_DEAD : P + r;
+        }
+    }
+    gout[g * 32 + lane] = s;
+    if (lane == 0) gn[g] = ne;
+}
+
+// Chain the groups from offset 0: glane[g] = true lane of group g (PJ_SLOW:
+// entries chained chunk by chunk into eslow -- too many possible entries, or
+// an entry that a long literal carried past the chunk before the group). entry_end = chain end.
+// aux[1] = 1 when the chain breaks.
+__global__ void __launch_bounds__(1024) k_tok_resolve(const uint32_t* __restrict__ ex,
+                                                      const uint64_t* __restrict__ gin,
+                                                      const uint64_t* __restrict__ gout,
+                                                      const uint32_t* __restrict__ gn, uint64_t nc, uint64_t len,
+                                                      uint8_t* __restrict__ glane, uint64_t* __restrict__ eslow,
+                                                      uint64_t* __restrict__ entry_end, DevCtl* ctl) {
+    __shared__ uint64_t si[1024], so[1024];
+    __shared__ uint32_t sn[32];
+    const uint64_t ng = (nc + PJ_G - 1) / PJ_G;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t s = 0;  // warp 0's chain position
+    bool bad = false;
+    for (uint64_t gb = 0; gb < ng; gb += 32) {
+        const uint64_t g = gb + warp;
+        __syncthreads();
+        if (g < ng) {
+            si[threadIdx.x] = gin[g * 32 + lane];
+            so[threadIdx.x] = gout[g * 32 + lane];
+            if (lane == 0) sn[warp] = gn[g];
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const int m = (int)min((uint64_t)32, ng - gb);
+            for (int k = 0; k < m; ++k) {
+                const uint64_t gg = gb + k;
+                uint8_t gl = PJ_SLOW;
+                if (sn[k] != PJ_MANY) {
+                    const unsigned hit = __ballot_sync(0xffffffffu, lane < (int)sn[k] && si[k * 32 + lane] == s);
+                    if (hit) {
+                        gl = (uint8_t)(__ffs(hit) - 1);
+                        s = so[k * 32 + gl];
+                    }
+                    // no hit: the entry came from a literal that jumped over
+                    // the chunk before the group -- chain this group slowly
+                }
+                if (gl == PJ_SLOW && !bad) {  // chunk-by-chunk through this group
+                    const uint64_t c0 = gg * PJ_G, c1 = min(nc, c0 + PJ_G);
+                    for (uint64_t c = c0; c < c1; ++c) {
+                        if (lane == 0) eslow[c] = s;
+                        const uint64_t P = c * PJ_C, E = min(len, P + PJ_C);
+                        if (s < E) {
+                            const uint32_t r = ex[s];
+                            if (r == 0xFFFFFFFFu) { bad = true; break; }
+                            s = P + r;
+                        }
+                    }
+                }
+                if (lane == 0) glane[gg] = gl;
+                if (bad) break;
+            }
+        }
+        if (__syncthreads_or(bad)) break;
+    }
+    if (threadIdx.x == 0) {
+        *entry_end = s;
+        if (bad || s != len) ctl->aux[1] = 1;
+    }
+}
+
+__device__ __forceinline__ uint64_t chunk_entry(uint64_t c, uint64_t nc, const uint8_t* glane,
+                                                const uint64_t* gent, const uint64_t* eslow,
+                                                const uint64_t* entry_end) {
+    if (c >= nc) return *entry_end;
+    const uint8_t l = glane[c / PJ_G];
+    return l == PJ_SLOW ? eslow[c] : gent[c * 32 + l];
+}
+
+// One thread per chunk: walk the chunk's tokens from its entry. EMIT = false
+// verifies and counts (tokens, unpacked bytes); EMIT = true writes the token
+// table at the scanned offsets.
+template <bool EMIT>
+__global__ void __launch_bounds__(128) k_tok_walk_chunks(const uint8_t* __restrict__ s, uint64_t len, uint64_t nc,
+                                                         const uint8_t* __restrict__ glane,
+                                                         const uint64_t* __restrict__ gent,
+                                                         const uint64_t* __restrict__ eslow,
+                                                         const uint64_t* __restrict__ entry_end,
+                                                         uint64_t* __restrict__ cnt, uint64_t* __restrict__ ub,
+                                                         Token* __restrict__ tok, DevCtl* ctl) {
+    const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    const uint64_t E = min(len, (c + 1) * PJ_C);
+    uint64_t p = chunk_entry(c, nc, glane, gent, eslow, entry_end), k = 0, u = 0;
+    if (EMIT) { k = cnt[c]; u = ub[c]; }
+    auto at = [&](uint64_t q) -> uint32_t { return s[q]; };
+    while (p < E) {
+        uint64_t v;
+        uint32_t tag;
+        const uint64_t q = tok_next(at, len, p, v, tag);
+        if (q == PJ_DEAD) { ctl->aux[1] = 1; return; }
+        if (EMIT) {
+            tok[k] = tag ? Token{q - v, u, v | (1ull << 63)} : Token{0, u, v};
+        }
+        ++k;
+        u += v;
+        p = q;
+    }
+    if (!EMIT) {
+        if (p != chunk_entry(c + 1, nc, glane, gent, eslow, entry_end)) ctl->aux[1] = 1;
+        cnt[c] = k;
+        ub[c] = u;
+    }
+}
+
+// Exclusive scan of two u64 arrays in one CTA; totals -> tot[0], tot[1].
+__global__ void __launch_bounds__(1024) k_scan_pair(uint64_t* __restrict__ a, uint64_t* __restrict__ b,
+                                                    uint64_t T, uint64_t* __restrict__ tot) {
+    using BS = cub::BlockScan<ulonglong2, 1024>;
+    __shared__ typename BS::TempStorage tmp;
+    const uint64_t per = (T + 1023) / 1024;
+    const uint64_t t0 = threadIdx.x * per, t1 = min(T, t0 + per);
+    ulonglong2 local = make_ulonglong2(0, 0);
+    for (uint64_t t = t0; t < t1; ++t) { local.x += a[t]; local.y += b[t]; }
+    ulonglong2 excl, total;
+    auto add = [](const ulonglong2& x, const ulonglong2& y) { return make_ulonglong2(x.x + y.x, x.y + y.y); };
+    BS(tmp).ExclusiveScan(local, excl, make_ulonglong2(0, 0), add, total);
+    for (uint64_t t = t0; t < t1; ++t) {
+        const uint64_t ca = a[t], cb = b[t];
+        a[t] = excl.x;
+        b[t] = excl.y;
+        excl.x += ca;
+        excl.y += cb;
+    }
+    if (threadIdx.x == 0) { tot[0] = total.x; tot[1] = total.y; }
 }
 
 constexpr int EXP_THREADS = 256;
@@ -166,24 +446,102 @@ __global__ void __launch_bounds__(VD_THREADS) k_varint_decode(const uint8_t* __r
 
 }  // namespace
 
+// Parallel parse; returns false when the chain is broken (corrupt stream).
+static bool parallel_tokens(const uint8_t* d_stream, uint64_t len, Token* tok, StreamDecScratch& sc, DevCtl* ctl,
+                            cudaStream_t st, uint64_t* ntok, uint64_t* ulen) {
+    static bool attr = false;
+    if (!attr) {
+        UMCG_CUDA(cudaFuncSetAttribute(k_tok_jump, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PJ_SMEM));
+        attr = true;
+    }
+    const uint64_t nc = cdiv(len, PJ_C), ng = cdiv(nc, PJ_G);
+    // scratch: ex u32[len] | dcount u32[nc] | dvals u64[nc*K] | gent u64[nc*32] | gin, gout u64[ng*32] |
+    //          gn u32[ng] | eslow, cnt, ub u64[nc] | tot u64[2] | entry_end | glane u8[ng]
+    const uint64_t ex_b = (len * 4 + 7) & ~7ull, dc_b = (nc * 4 + 7) & ~7ull, gn_b = (ng * 4 + 7) & ~7ull;
+    const uint64_t bytes = ex_b + dc_b + nc * PJ_K * 8 + nc * 32 * 8 + ng * 32 * 16 + gn_b + nc * 24 + 24 + ng + 8;
+    uint8_t* q = sc.parse.as<uint8_t>(bytes);
+    uint32_t* ex = reinterpret_cast<uint32_t*>(q); q += ex_b;
+    uint32_t* dcount = reinterpret_cast<uint32_t*>(q); q += dc_b;
+    uint64_t* dvals = reinterpret_cast<uint64_t*>(q); q += nc * PJ_K * 8;
+    uint64_t* gent = reinterpret_cast<uint64_t*>(q); q += nc * 32 * 8;
+    uint64_t* gin = reinterpret_cast<uint64_t*>(q); q += ng * 32 * 8;
+    uint64_t* gout = reinterpret_cast<uint64_t*>(q); q += ng * 32 * 8;
+    uint32_t* gn = reinterpret_cast<uint32_t*>(q); q += gn_b;
+    uint64_t* eslow = reinterpret_cast<uint64_t*>(q); q += nc * 8;
+    uint64_t* cnt = reinterpret_cast<uint64_t*>(q); q += nc * 8;
+    uint64_t* ub = reinterpret_cast<uint64_t*>(q); q += nc * 8;
+    uint64_t* tot = reinterpret_cast<uint64_t*>(q); q += 16;
+    uint64_t* entry_end = reinterpret_cast<uint64_t*>(q); q += 8;
+    uint8_t* glane = q;
+    UMCG_CUDA(cudaMemsetAsync(&ctl->aux[1], 0, 8, st));
+    {
+        ProfScope ps("k_tok_jump", st);
+        k_tok_jump<<<(unsigned)nc, PJ_THREADS, PJ_SMEM, st>>>(d_stream, len, ex, dcount, dvals);
+        UMCG_LAUNCHED();
+    }
+    {
+        ProfScope ps("k_tok_resolve", st);
+        k_tok_groups<<<(unsigned)ng, 32, 0, st>>>(ex, dcount, dvals, nc, len, gent, gin, gout, gn);
+        UMCG_LAUNCHED();
+        k_tok_resolve<<<1, 1024, 0, st>>>(ex, gin, gout, gn, nc, len, glane, eslow, entry_end, ctl);
+        UMCG_LAUNCHED();
+    }
+    const unsigned g = (unsigned)cdiv(nc, 128);
+    {
+        ProfScope ps("k_tok_count", st);
+        k_tok_walk_chunks<false><<<g, 128, 0, st>>>(d_stream, len, nc, glane, gent, eslow, entry_end, cnt, ub,
+                                                    tok, ctl);
+        UMCG_LAUNCHED();
+    }
+    k_scan_pair<<<1, 1024, 0, st>>>(cnt, ub, nc, tot);
+    UMCG_LAUNCHED();
+    {
+        ProfScope ps("k_tok_emit", st);
+        k_tok_walk_chunks<true><<<g, 128, 0, st>>>(d_stream, len, nc, glane, gent, eslow, entry_end, cnt, ub,
+                                                   tok, ctl);
+        UMCG_LAUNCHED();
+    }
+    struct { uint64_t bad, t[2]; } h;
+    UMCG_CUDA(cudaMemcpyAsync(&h.bad, &ctl->aux[1], 8, cudaMemcpyDeviceToHost, st));
+    UMCG_CUDA(cudaMemcpyAsync(h.t, tot, 16, cudaMemcpyDeviceToHost, st));
+    UMCG_CUDA(cudaStreamSynchronize(st));
+    *ntok = h.t[0];
+    *ulen = h.t[1];
+    return !h.bad;
+}
+
 const uint8_t* stream_unpack(const uint8_t* d_stream, uint64_t len, StreamDecScratch& sc, DevCtl* ctl,
                              cudaStream_t st, uint64_t* ulen_out) {
     const uint64_t tok_cap = len / 2 + 1;
     Token* tok = sc.tokens.as<Token>(tok_cap);
-    k_token_walk<<<1, 32, 0, st>>>(d_stream, len, tok, tok_cap, ctl);
+    // Short serial probe: a lossy stream is usually a handful of tokens.
+    constexpr uint64_t kProbe = 64;
+    const bool par_ok = len >= 2 * PJ_C && len < 0xFFFFFFF0ull;
+    k_token_walk<<<1, 32, 0, st>>>(d_stream, len, tok, tok_cap, par_ok ? kProbe : ~0ull, ctl);
     UMCG_LAUNCHED();
     struct { DevCtl c; Token t; } h;
     UMCG_CUDA(cudaMemcpyAsync(&h.c, ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
     UMCG_CUDA(cudaMemcpyAsync(&h.t, tok, sizeof(Token), cudaMemcpyDeviceToHost, st));
     UMCG_CUDA(cudaStreamSynchronize(st));
+    uint64_t ntok = h.c.count, ulen = h.c.aux[0];
+    if (!h.c.err && h.c.aux[1]) {
+        if (!parallel_tokens(d_stream, len, tok, sc, ctl, st, &ntok, &ulen)) {
+            // broken chain: the serial walk reports the reference's error
+            k_token_walk<<<1, 32, 0, st>>>(d_stream, len, tok, tok_cap, ~0ull, ctl);
+            UMCG_LAUNCHED();
+            UMCG_CUDA(cudaMemcpyAsync(&h.c, ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
+            UMCG_CUDA(cudaStreamSynchronize(st));
+            if (!h.c.err) fail(UMCG_INTERNAL_INCONSISTENCY, "parallel token parse disagrees with the serial walk");
+        }
+    }
     if (h.c.err) fail(UMCG_CORRUPT_PAYLOAD, h.c.err == DE_CORRUPT_TOKEN ? "unknown token in lossless stream"
                                             : h.c.err == DE_CORRUPT_VARINT ? "varint exceeds 64 bits"
                                                                            : "unexpected end of data");
-    const uint64_t ntok = h.c.count, ulen = h.c.aux[0];
     *ulen_out = ulen;
     if (ntok == 1 && (h.t.len >> 63)) return d_stream + h.t.src;  // single literal: decode in place
     if (!ulen) return d_stream;
     uint8_t* ub = sc.unpacked.as<uint8_t>(ulen);
+    ProfScope ps("k_expand", st);
     k_expand<<<(unsigned)cdiv(ulen, EXP_TILE), EXP_THREADS, 0, st>>>(d_stream, tok, ntok, ulen, ub);
     UMCG_LAUNCHED();
     return ub;

@@ -12,6 +12,7 @@ import numpy as np
 import pytest
 
 import paper_2501_06910_b200 as umcg
+from oracle.bindings import Setup
 from helpers import (GOLDEN, load_cases, load_seed7, lorenzo_pred, parse_archive, parse_payload,
                      window_distance)
 
@@ -315,3 +316,120 @@ def test_rle_stream_patterns_bit_exact(cuda, ref, seed):
     assert got == want
     back = umcg.decode(want).cpu().numpy()
     assert np.array_equal(back, ref.decode(want, n))
+
+
+def _token_dense_codes(rng, n, long_lits=False):
+    """Codes whose zero-RLE stream is dense with tokens (short literals between
+    8..12-zero runs), optionally interleaved with literals spanning many
+    8 KiB parse chunks."""
+    q = np.zeros(n, np.int64)
+    i = 0
+    while i < n:
+        if long_lits and rng.random() < 0.002:
+            lit = int(rng.integers(20000, 120000))
+            q[i:i + lit] = rng.integers(-3, 4, size=min(lit, n - i)) | 1
+            i += lit
+        else:
+            lit = int(rng.integers(1, 4))
+            q[i:i + lit] = rng.choice([-2, -1, 1, 2, 70, -9000], size=min(lit, n - i))
+            i += lit + int(rng.integers(8, 13))
+    return q
+
+
+@pytest.mark.parametrize("variant", ["dense", "long_literals", "all_dense_small"])
+def test_many_token_streams_parallel_parse(cuda, ref, variant):
+    """Streams with 10^5-10^6 tokens go through the parallel token parse
+    (stream.cu k_tok_jump/resolve/walk); payloads and decodes must match the
+    reference byte for byte (lossless.hpp:53-70)."""
+    rng = np.random.default_rng({"dense": 1, "long_literals": 2, "all_dense_small": 3}[variant])
+    n = 1_500_000 if variant != "all_dense_small" else 40_000
+    q = _token_dense_codes(rng, n, long_lits=variant == "long_literals")
+    tau = 0.5
+    v = q.astype(np.float64) * (2 * tau)
+    got = umcg.encode(dev(v), predictor=0, tau=tau)
+    want = ref.encode(v, predictor=0, tau=tau)
+    assert got == want
+    back = umcg.decode(want).cpu().numpy()
+    assert np.array_equal(back, v)
+
+
+def test_many_token_streams_corruption_matches_reference(cuda, ref):
+    """Byte flips anywhere in a token-dense stream: the GPU decoder fails with
+    corrupt_payload exactly when the reference fails, else decodes the same
+    values (the parallel parse falls back to the serial walk on a broken
+    chain)."""
+    rng = np.random.default_rng(9)
+    n = 400_000
+    q = _token_dense_codes(rng, n)
+    v = q.astype(np.float64)
+    pl = ref.encode(v, predictor=0, tau=0.5)
+    hdr = 21 + 8 + 8  # 1-D header + escape count (codec.hpp:231-250)
+    for trial in range(24):
+        b = bytearray(pl)
+        pos = int(rng.integers(hdr, len(b)))
+        b[pos] = int(rng.choice([0x00, 0x01, 0x05, 0x80, 0xFF, int(rng.integers(0, 256))]))
+        b = bytes(b)
+        try:
+            r = ref.decode(b, n)
+            r_err = None
+        except Exception as e:  # noqa: BLE001
+            r, r_err = None, e
+        try:
+            g = umcg.decode(b, n_capacity=n).cpu().numpy()
+            g_err = None
+        except umcg.UmcgError as e:
+            g, g_err = None, e
+        if r_err is not None:
+            assert g_err is not None and g_err.kind == "corrupt_payload", (trial, pos, r_err)
+        else:
+            assert g_err is None, (trial, pos, g_err)
+            assert np.array_equal(g, r), (trial, pos)
+
+
+@pytest.mark.parametrize("tau", [1e-2, 1e-4])
+def test_config3_at_scale_matches_reference(cuda, ref, oracle, tau):
+    """BASELINE config 3 (jittered 3-D lattice, Feistel-permuted vertex order)
+    at lattice 128 (2.1M vertices, grid 64): the GPU archive against the
+    reference's on the same mapping (byte-exact up to rounding-window codes),
+    both decoders, and the bound on every vertex. tau=1e-2 gives a stream with
+    ~10^5 tokens (parallel token parse)."""
+    import torch
+    xyz, x = umcg.gen_config(3, 128, 20250113, device="cuda")
+    axes = [np.linspace(0.0, 1.0, 64) for _ in range(3)]
+    plan = umcg.Plan.build(axes, xyz)
+    mode, gaxes, assign, visited = plan.export()
+    s = Setup(dim=3, axes=gaxes, mode=mode, assignments=assign, visited=visited)
+    xh = x.cpu().numpy()
+    b = umcg.Budget(tau=tau, split_rho=0.5, bound_kind=1)
+    got = plan.compress(x, b, name="c3")
+    want = ref.compress(s, xh, name="c3", tau=tau)
+    check_archive(got, want, s, xh, dict(tau=tau), oracle, f"config3 tau={tau}")
+    tau_abs = tau * np.ptp(xh)
+    out = plan.decompress(got).cpu().numpy()
+    check_decode(out, ref.decompress(s, got), xh, tau_abs, "own archive")
+    out_r = plan.decompress(want).cpu().numpy()
+    check_decode(out_r, ref.decompress(s, want), xh, tau_abs, "ref archive")
+    del torch
+
+
+@pytest.mark.parametrize("tau", [1e-1, 1e-2, 1e-4, 1e-7])
+def test_config3_full_size_properties(cuda, tau):
+    """Config 3 at the bench size (512^3 vertices, grid 256): size-independent
+    properties -- the bound on 100% of vertices, determinism, host path ==
+    device path -- across the tau range (1e-1: dense token streams)."""
+    import torch
+    xyz, x = umcg.gen_config(3, 512, 20250113, device="cuda")
+    axes = [np.linspace(0.0, 1.0, 256) for _ in range(3)]
+    plan = umcg.Plan.build(axes, xyz)
+    del xyz
+    b = umcg.Budget(tau=tau, split_rho=0.5, bound_kind=1)
+    a1 = plan.compress(x, b)
+    a2 = plan.compress(x, b)
+    assert a1 == a2
+    fb0 = umcg.serial_fallbacks()
+    out = plan.decompress(a1)
+    assert umcg.serial_fallbacks() == fb0
+    rng = float((x.max() - x.min()).item())
+    err = (out - x).abs().max().item()
+    assert err <= tau * rng, (err, tau * rng)
+    torch.cuda.synchronize()
