@@ -103,95 +103,8 @@ __global__ void __launch_bounds__(CH) k_rle_states(const RleSum* __restrict__ su
     }
 }
 
-constexpr uint32_t kEntry = ENC_THREADS;  // slot of the literal open on tile entry
-constexpr uint64_t kUnknown = ~0ull;
-
-// Per-thread exact walk of the RLE state machine over its codes (general path).
-// WRITE=false: record literal closes; WRITE=true: emit bytes.
-template <bool WRITE, class T>
-__device__ __forceinline__ void walk(RleState st, const T (&v)[ENC_ITEMS], int cnt, bool finalize,
-                                     uint64_t* closeTot, uint8_t* out, uint64_t base, uint64_t cap) {
-    const uint32_t me = threadIdx.x;
-    auto data_pos = [&](const RleState& s) { return s.C + 1 + vlen64(closeTot[s.origin]) + s.Lb; };
-    auto open_lit = [&](RleState& s) {
-        s.origin = me;
-        s.Lb = 0;
-        s.has = 1;
-        if (WRITE) {
-            const uint64_t p = s.C - base;
-            if (p < cap) out[p] = 0x01;
-            write_varint(out, s.C + 1, base, cap, closeTot[me]);
-        }
-    };
-    auto put_zeros = [&](RleState& s, uint64_t J) {
-        if (WRITE) {
-            const uint64_t p0 = data_pos(s) - base;
-            for (uint64_t k = 0; k < J; ++k)
-                if (p0 + k < cap) out[p0 + k] = 0;
-        }
-        s.Lb += J;
-    };
-    auto put_z = [&](RleState& s, uint64_t J) {
-        if (WRITE) {
-            const uint64_t p = s.C - base;
-            if (p < cap) out[p] = 0x00;
-            write_varint(out, s.C + 1, base, cap, J);
-        }
-        s.C += z_size(J);
-    };
-    auto close_lit = [&](RleState& s) {
-        if (!WRITE) closeTot[s.origin] = s.Lb;
-        s.C += lit_size(s.Lb);
-        s.has = 0;
-    };
-#pragma unroll
-    for (int k = 0; k < ENC_ITEMS; ++k) {
-        if (k >= cnt) break;
-        const T c = v[k];
-        if (c == 0) { st.Zp += 1; continue; }
-        const uint64_t J = st.Zp;
-        if (J >= kMinZeroRun) {
-            if (st.has) close_lit(st);
-            put_z(st, J);
-            open_lit(st);
-        } else {
-            if (!st.has) open_lit(st);
-            put_zeros(st, J);
-        }
-        st.Zp = 0;
-        if (WRITE) write_varint(out, data_pos(st), base, cap, c);
-        st.Lb += vlen64((uint64_t)c);
-    }
-    if (finalize) {
-        const uint64_t J = st.Zp;
-        if (J >= kMinZeroRun) {
-            if (st.has) close_lit(st);
-            put_z(st, J);
-        } else if (J > 0 || st.has) {
-            if (!st.has) open_lit(st);
-            put_zeros(st, J);
-            close_lit(st);
-        }
-    }
-}
-
 __device__ __forceinline__ uint64_t state_pos(const RleState& s, const uint64_t* lit_total) {
     return s.has ? s.C + 1 + vlen64(lit_total[s.origin]) + s.Lb : s.C;
-}
-
-// Staged bytes -> global, 4-byte stores after a byte-wise head.
-__device__ __forceinline__ void copy_out(const uint8_t* out, uint64_t len, uint8_t* d) {
-    const uint32_t head = (uint32_t)((4 - ((uintptr_t)d & 3)) & 3);
-    const uint64_t h = head < len ? head : len;
-    if (threadIdx.x < h) d[threadIdx.x] = out[threadIdx.x];
-    const uint64_t words = (len - h) / 4;
-    uint32_t* dw = reinterpret_cast<uint32_t*>(d + h);
-    for (uint64_t w = threadIdx.x; w < words; w += ENC_THREADS) {
-        const uint8_t* s = out + h + 4 * w;
-        dw[w] = (uint32_t)s[0] | ((uint32_t)s[1] << 8) | ((uint32_t)s[2] << 16) | ((uint32_t)s[3] << 24);
-    }
-    const uint64_t t0 = h + 4 * words;
-    if (t0 + threadIdx.x < len) d[t0 + threadIdx.x] = out[t0 + threadIdx.x];
 }
 
 // Byte writer into the staging buffer (no bounds checks: the tile's output
@@ -318,6 +231,16 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_write_fast(const T* __restr
     copy_out16(out, ao, len, d);
 }
 
+// General writer: tiles with a zero run >= 8 strictly inside, and the last
+// tile. Units = the tile's nonzero codes; unit j carries the zero run before
+// it (J_j, the first one including the zeros pending on entry). A long run
+// (J_j >= 8) emits a Z token and opens a literal at j; so does the first unit
+// when no literal is open on entry. Four u32 block scans place everything:
+//   1. last nonzero before each thread       -> J_j, long/open flags
+//   2. prefix of literal data bytes d_j      -> literal totals T_j =
+//   3. suffix "next long unit"                  D(next long unit) - D(j)
+//   4. prefix of unit bytes U_j              -> output positions
+// (literals still open at the tile end take T from lit_total[tile]).
 template <class T>
 __global__ void __launch_bounds__(ENC_THREADS) k_rle_write_general(const T* __restrict__ codes, uint64_t n,
                                                            const RleState* __restrict__ states,
@@ -325,56 +248,147 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_write_general(const T* __re
                                                            const uint64_t* __restrict__ lit_total,
                                                            const DevCtl* __restrict__ ctl, int comp, const uint32_t* __restrict__ glist,
                                                            uint8_t* __restrict__ dst, int off_from_ctl) {
-    constexpr uint64_t CAP = ENC_TILE * (sizeof(T) == 8 ? 10 : 5) + 64;
-    using BS = cub::BlockScan<RleSum, ENC_THREADS>;
-    using BS32 = cub::BlockScan<uint32_t, ENC_THREADS>;
+    constexpr uint32_t CAP = ENC_TILE * (sizeof(T) == 8 ? 10 : 5) + 96;
+    constexpr int NONE = 0x7fffffff;
+    using BSi = cub::BlockScan<int, ENC_THREADS>;
+    using BSu = cub::BlockScan<uint32_t, ENC_THREADS>;
     __shared__ union {
-        typename BS::TempStorage rle;
-        typename BS32::TempStorage u32;
+        typename BSi::TempStorage i;
+        typename BSu::TempStorage u;
     } tmp;
-    __shared__ uint64_t closeTot[ENC_THREADS + 1];
+    __shared__ uint32_t dpre[ENC_TILE + 1];  // exclusive prefix of d at each item
+    __shared__ int sfx[ENC_THREADS];
     __shared__ __align__(16) uint8_t out[CAP];
 
     if (blockIdx.x >= (uint32_t)ctl->aux[4 + comp]) return;
     const uint64_t tile = glist[blockIdx.x];
     const uint64_t T_ = (n + ENC_TILE - 1) / ENC_TILE;
     const bool last = tile == T_ - 1;
-    const RleState entry = states[tile];
-    const RleSum S = sums[tile];
-    const uint64_t P0 = state_pos(entry, lit_total);
+    const RleState E = states[tile];
+    const uint64_t P0 = state_pos(E, lit_total);
     const uint64_t P1 = last ? ctl->stream_len[comp] : state_pos(states[tile + 1], lit_total);
-    const uint64_t len = P1 - P0;
+    const uint32_t len = (uint32_t)(P1 - P0);
     if (len == 0) return;  // all-zero tile: its zeros stay pending
     uint8_t* d = dst + (off_from_ctl ? ctl->stream_off[comp] : 0) + P0;
+    const uint32_t ao = (uint32_t)((uintptr_t)d & 15);
+    uint8_t* o = out + ao;
 
-    const uint64_t first = tile * ENC_TILE + (uint64_t)threadIdx.x * ENC_ITEMS;
+    const uint32_t tile_cnt = (uint32_t)min((uint64_t)ENC_TILE, n - tile * ENC_TILE);
+    const int r0 = threadIdx.x * ENC_ITEMS;
     T v[ENC_ITEMS];
-    const int cnt = load_items(codes, n, first, v);
+    const int cnt = load_items(codes, n, tile * ENC_TILE + (uint64_t)r0, v);
+    uint32_t nzm = 0;
+#pragma unroll
+    for (int k = 0; k < ENC_ITEMS; ++k) nzm |= (k < cnt && v[k] != 0) ? (1u << k) : 0u;
 
-    // ---- general path: exact walk of the state machine ----
-    const RleSum s = thread_summary(v, cnt, threadIdx.x);
-    RleSum excl;
-    BS(tmp.rle).ExclusiveScan(s, excl, rle_identity(), RleComposeOp());
-    RleState e = entry;
-    e.origin = entry.has ? kEntry : kNoOrigin;
-    bool cl;
-    uint64_t tt;
-    const RleState st = rle_apply(e, excl, &cl, &tt);
-    const bool finalize = cnt > 0 && first + cnt == n;
-    for (uint32_t k = threadIdx.x; k <= ENC_THREADS; k += ENC_THREADS) closeTot[k] = kUnknown;
+    // 1. last nonzero item before this thread (-1: none in the tile)
+    int prev_t;
+    BSi(tmp.i).ExclusiveScan(nzm ? r0 + 31 - __clz(nzm) : -1, prev_t, -1, cub::Max());
     __syncthreads();
-    walk<false>(st, v, cnt, finalize, closeTot, nullptr, 0, 0);
+    // J_j per unit (int64: the entry's pending zeros can be many tiles long)
+    auto run_before = [&](int r, int prev) -> uint64_t {
+        return prev >= 0 ? (uint64_t)(r - prev - 1) : (uint64_t)r + E.Zp;
+    };
+    uint32_t lngm = 0, opnm = 0, dsum = 0;
+    {
+        int prev = prev_t;
+#pragma unroll
+        for (int k = 0; k < ENC_ITEMS; ++k) {
+            if (!(nzm >> k & 1)) continue;
+            const uint64_t J = run_before(r0 + k, prev);
+            const bool lng = J >= kMinZeroRun;
+            lngm |= (uint32_t)lng << k;
+            opnm |= (uint32_t)(lng || (prev < 0 && !E.has)) << k;
+            dsum += (lng ? 0u : (uint32_t)J) + vlen64((uint64_t)v[k]);
+            prev = r0 + k;
+        }
+    }
+    // 2. prefix of literal data bytes
+    uint32_t dex, dtot;
+    BSu(tmp.u).ExclusiveSum(dsum, dex, dtot);
+    {
+        int prev = prev_t;
+        uint32_t acc = dex;
+#pragma unroll
+        for (int k = 0; k < ENC_ITEMS; ++k) {
+            dpre[r0 + k] = acc;
+            if (!(nzm >> k & 1)) continue;
+            const uint64_t J = run_before(r0 + k, prev);
+            acc += (lngm >> k & 1 ? 0u : (uint32_t)J) + vlen64((uint64_t)v[k]);
+            prev = r0 + k;
+        }
+        if (threadIdx.x == ENC_THREADS - 1) dpre[ENC_TILE] = acc;
+    }
+    // 3. next long unit after this thread (suffix min via a reversed scan)
+    sfx[threadIdx.x] = lngm ? r0 + __ffs(lngm) - 1 : NONE;
     __syncthreads();
-    for (uint32_t k = threadIdx.x; k <= ENC_THREADS; k += ENC_THREADS) {
-        if (closeTot[k] == kUnknown) {
-            if (k == kEntry) closeTot[k] = entry.has ? lit_total[entry.origin] : 0;
-            else closeTot[k] = lit_total[tile];
+    int nl_rev;
+    BSi(tmp.i).ExclusiveScan(sfx[ENC_THREADS - 1 - threadIdx.x], nl_rev, NONE, cub::Min());
+    __syncthreads();
+    sfx[ENC_THREADS - 1 - threadIdx.x] = nl_rev;
+    __syncthreads();
+    const int next_long_after = sfx[threadIdx.x];
+    const uint64_t tail_total = lit_total[tile];
+    auto lit_T = [&](int k) -> uint64_t {
+        const uint32_t later = lngm & ~((2u << k) - 1u);
+        const int kl = later ? r0 + __ffs(later) - 1 : next_long_after;
+        return kl != NONE ? (uint64_t)(dpre[kl] - dpre[r0 + k]) : tail_total;
+    };
+    // 4. unit bytes -> positions
+    uint32_t usum = 0;
+    {
+        int prev = prev_t;
+#pragma unroll
+        for (int k = 0; k < ENC_ITEMS; ++k) {
+            if (!(nzm >> k & 1)) continue;
+            const uint64_t J = run_before(r0 + k, prev);
+            const bool lng = lngm >> k & 1;
+            usum += (lng ? 1u + vlen64(J) : (uint32_t)J) + vlen64((uint64_t)v[k]);
+            if (opnm >> k & 1) usum += 1u + vlen64(lit_T(k));
+            prev = r0 + k;
+        }
+    }
+    uint32_t pos, utot;
+    BSu(tmp.u).ExclusiveSum(usum, pos, utot);
+    {
+        int prev = prev_t;
+#pragma unroll
+        for (int k = 0; k < ENC_ITEMS; ++k) {
+            if (!(nzm >> k & 1)) continue;
+            const uint64_t J = run_before(r0 + k, prev);
+            const bool lng = lngm >> k & 1;
+            if (lng) {
+                o[pos] = 0x00;
+                pos += 1 + put_varint(o + pos + 1, J);
+            }
+            if (opnm >> k & 1) {
+                o[pos] = 0x01;
+                pos += 1 + put_varint(o + pos + 1, lit_T(k));
+            }
+            if (!lng)
+                for (uint32_t z = 0; z < (uint32_t)J; ++z) o[pos++] = 0;
+            pos += put_varint(o + pos, v[k]);
+            prev = r0 + k;
+        }
+    }
+    if (last && threadIdx.x == ENC_THREADS - 1) {  // rle_finish: trailing zeros
+        const int lastnz = nzm ? r0 + 31 - __clz(nzm) : prev_t;
+        const uint64_t t = lastnz >= 0 ? (uint64_t)(tile_cnt - 1 - lastnz) : E.Zp + tile_cnt;
+        const bool open = lastnz >= 0 || E.has;
+        uint32_t q = utot;
+        if (t >= kMinZeroRun) {
+            o[q] = 0x00;
+            put_varint(o + q + 1, t);
+        } else {
+            if (!open) {
+                o[q] = 0x01;
+                q += 1 + put_varint(o + q + 1, t);
+            }
+            for (uint32_t z = 0; z < (uint32_t)t; ++z) o[q++] = 0;
         }
     }
     __syncthreads();
-    walk<true>(st, v, cnt, finalize, closeTot, out, P0, CAP);
-    __syncthreads();
-    copy_out(out, len, d);
+    copy_out16(out, ao, len, d);
 }
 
 }  // namespace
