@@ -90,9 +90,10 @@ constexpr int PJ_K = 32;         // distinct exits kept per chunk (one warp)
 constexpr int PJ_HS = 128;       // hash slots for the distinct-exit set
 constexpr uint64_t PJ_G = 64;    // chunks per group
 constexpr uint64_t PJ_DEAD = ~0ull;
+constexpr uint32_t PJ_DEAD32 = 0xFFFFFFFFu;
 constexpr uint32_t PJ_MANY = 0xFFFFFFFFu;
 constexpr uint8_t PJ_SLOW = 0xFF;
-constexpr size_t PJ_SMEM = PJ_C * 8 + PJ_C + PJ_HALO;
+constexpr size_t PJ_SMEM = PJ_C * 4 + PJ_C + PJ_HALO;
 
 // One token header at p (< len), the checks of k_token_walk: next token
 // start, or PJ_DEAD when the header is malformed or the literal overruns.
@@ -119,42 +120,58 @@ __global__ void __launch_bounds__(PJ_THREADS) k_tok_jump(const uint8_t* __restri
     extern __shared__ __align__(16) uint8_t pj_smem[];
     __shared__ unsigned long long hs[PJ_HS];
     __shared__ int hcount, hpos;
-    uint64_t* nx = reinterpret_cast<uint64_t*>(pj_smem);
-    uint8_t* sb = pj_smem + PJ_C * 8;
+    // nx[i]: successor of offset P + i, relative to P (>= n: an exit; PJ_DEAD32: malformed)
+    uint32_t* nx = reinterpret_cast<uint32_t*>(pj_smem);
+    uint8_t* sb = pj_smem + PJ_C * 4;
     const uint64_t P = blockIdx.x * PJ_C;
     const uint64_t E = min(len, P + PJ_C);
-    const int n = (int)(E - P);
-    for (int i = threadIdx.x; i < (int)PJ_C + PJ_HALO; i += PJ_THREADS) sb[i] = P + i < len ? s[P + i] : 0;
+    const uint32_t n = (uint32_t)(E - P);
+    {
+        // bytes [P, P + C + HALO): 16-byte loads where aligned
+        const uint8_t* src = s + P;
+        const uint64_t avail = len - P;
+        const uint32_t want = (uint32_t)min((uint64_t)(PJ_C + PJ_HALO), avail);
+        if (((uintptr_t)src & 15) == 0) {
+            for (uint32_t w = threadIdx.x; w < want / 16; w += PJ_THREADS)
+                reinterpret_cast<uint4*>(sb)[w] = __ldg(reinterpret_cast<const uint4*>(src) + w);
+            for (uint32_t i = (want & ~15u) + threadIdx.x; i < PJ_C + PJ_HALO; i += PJ_THREADS)
+                sb[i] = i < want ? src[i] : 0;
+        } else {
+            for (uint32_t i = threadIdx.x; i < PJ_C + PJ_HALO; i += PJ_THREADS) sb[i] = i < want ? src[i] : 0;
+        }
+    }
     for (int i = threadIdx.x; i < PJ_HS; i += PJ_THREADS) hs[i] = PJ_DEAD;
     if (threadIdx.x == 0) hcount = hpos = 0;
     __syncthreads();
     auto at = [&](uint64_t q) -> uint32_t { return sb[q - P]; };
-    for (int i = threadIdx.x; i < n; i += PJ_THREADS) {
+    for (uint32_t i = threadIdx.x; i < n; i += PJ_THREADS) {
         uint64_t v;
         uint32_t tag;
-        nx[i] = tok_next(at, len, P + i, v, tag);
+        const uint64_t q = tok_next(at, len, P + i, v, tag);
+        nx[i] = q == PJ_DEAD ? PJ_DEAD32 : (uint32_t)(q - P);
     }
     __syncthreads();
     // Pointer jumping. Updates are in place: a reader sees either the old or
     // the new successor, both on the same chain, so the fixed point is exact.
     for (;;) {
         int moved = 0;
-        for (int i = threadIdx.x; i < n; i += PJ_THREADS) {
-            const uint64_t v = nx[i];
-            if (v < E) {
-                const uint64_t w = nx[v - P];
+        for (uint32_t i = threadIdx.x; i < n; i += PJ_THREADS) {
+            const uint32_t v = nx[i];
+            if (v < n) {
+                const uint32_t w = nx[v];
                 nx[i] = w;
-                moved |= w < E;
+                moved |= w < n;
             }
         }
         if (!__syncthreads_or(moved)) break;
     }
     // exit table + distinct live exits (warp-deduplicated hash insert)
     const int lane = threadIdx.x & 31;
-    for (int base = 0; base < n; base += PJ_THREADS) {
-        const int i = base + threadIdx.x;
-        const uint64_t v = i < n ? nx[i] : PJ_DEAD;
-        if (i < n) ex[P + i] = v == PJ_DEAD ? 0xFFFFFFFFu : (uint32_t)(v - P);
+    for (uint32_t base = 0; base < n; base += PJ_THREADS) {
+        const uint32_t i = base + threadIdx.x;
+        const uint32_t r = i < n ? nx[i] : PJ_DEAD32;
+        if (i < n) ex[P + i] = r;
+        const uint64_t v = r == PJ_DEAD32 ? PJ_DEAD : P + r;
         const unsigned m = __match_any_sync(0xffffffffu, v);
         if (v != PJ_DEAD && __ffs(m) - 1 == lane && *(volatile int*)&hcount <= PJ_K) {
             unsigned h = (unsigned)((v * 0x9E3779B97F4A7C15ull) >> 57);
@@ -338,29 +355,78 @@ __global__ void __launch_bounds__(1024) k_scan_pair(uint64_t* __restrict__ a, ui
 }
 
 constexpr int EXP_THREADS = 256;
-constexpr uint64_t EXP_TILE = 8192;
+constexpr uint64_t EXP_TILE = EXP_THREADS * 16;  // 16 output bytes per thread
+constexpr int EXP_TOK = 1024;                   // tokens staged per tile
 
-// Expand tokens into the unpacked byte stream: each CTA fills one 8 KiB tile
-// of the output, locating its first token by binary search.
+// Expand tokens into the unpacked byte stream. Each CTA fills one 4 KiB
+// tile: the tokens overlapping it are staged in shared memory, then every
+// thread assembles 16 bytes (binary search for its first token) and writes
+// one 16-byte store. Tiles overlapping more than EXP_TOK tokens (zero-length
+// tokens) take the token-by-token loop.
 __global__ void __launch_bounds__(EXP_THREADS) k_expand(const uint8_t* __restrict__ s,
                                                         const Token* __restrict__ tok, uint64_t ntok,
                                                         uint64_t ulen, uint8_t* __restrict__ u) {
+    __shared__ uint64_t t_uoff[EXP_TOK], t_src[EXP_TOK], t_len[EXP_TOK];
+    __shared__ uint64_t range[2];
     const uint64_t o0 = blockIdx.x * EXP_TILE;
     const uint64_t o1 = min(ulen, o0 + EXP_TILE);
-    // last token with uoff <= o0
-    uint64_t lo = 0, hi = ntok;
-    while (hi - lo > 1) {
-        const uint64_t mid = (lo + hi) / 2;
-        if (tok[mid].uoff <= o0) lo = mid; else hi = mid;
+    if (threadIdx.x < 2) {
+        // last token with uoff <= target (tokens are sorted by uoff)
+        const uint64_t target = threadIdx.x ? o1 - 1 : o0;
+        uint64_t lo = 0, hi = ntok;
+        while (hi - lo > 1) {
+            const uint64_t mid = (lo + hi) / 2;
+            if (tok[mid].uoff <= target) lo = mid; else hi = mid;
+        }
+        range[threadIdx.x] = lo;
     }
-    for (uint64_t k = lo; k < ntok; ++k) {
-        const Token t = tok[k];
-        const uint64_t tl = t.len & ~(1ull << 63);
-        if (t.uoff >= o1) break;
-        const uint64_t a = max(o0, t.uoff), b = min(o1, t.uoff + tl);
-        const bool lit = t.len >> 63;
-        for (uint64_t o = a + threadIdx.x; o < b; o += EXP_THREADS)
-            u[o] = lit ? s[t.src + (o - t.uoff)] : 0;
+    __syncthreads();
+    const uint64_t k0 = range[0], nt = range[1] - range[0] + 1;
+    if (nt > (uint64_t)EXP_TOK) {
+        for (uint64_t k = k0; k < ntok; ++k) {
+            const Token t = tok[k];
+            const uint64_t tl = t.len & ~(1ull << 63);
+            if (t.uoff >= o1) break;
+            const uint64_t a = max(o0, t.uoff), b = min(o1, t.uoff + tl);
+            const bool lit = t.len >> 63;
+            for (uint64_t o = a + threadIdx.x; o < b; o += EXP_THREADS) u[o] = lit ? s[t.src + (o - t.uoff)] : 0;
+        }
+        return;
+    }
+    for (uint32_t k = threadIdx.x; k < (uint32_t)nt; k += EXP_THREADS) {
+        const Token t = tok[k0 + k];
+        t_uoff[k] = t.uoff;
+        t_src[k] = t.src;
+        t_len[k] = t.len;
+    }
+    __syncthreads();
+    const uint64_t o = o0 + threadIdx.x * 16ull;
+    if (o >= o1) return;
+    uint32_t lo = 0, hi = (uint32_t)nt;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) / 2;
+        if (t_uoff[mid] <= o) lo = mid; else hi = mid;
+    }
+    uint32_t w[4] = {0, 0, 0, 0};
+    const int m = (int)min((uint64_t)16, o1 - o);
+    uint32_t k = lo;
+    uint64_t tu = t_uoff[k], tl = t_len[k] & ~(1ull << 63), ts = t_src[k];
+    bool lit = t_len[k] >> 63;
+    for (int j = 0; j < m; ++j) {
+        const uint64_t q = o + j;
+        while (q >= tu + tl) {  // next token (zero-length ones are skipped)
+            ++k;
+            tu = t_uoff[k];
+            tl = t_len[k] & ~(1ull << 63);
+            ts = t_src[k];
+            lit = t_len[k] >> 63;
+        }
+        if (lit) w[j >> 2] |= (uint32_t)s[ts + (q - tu)] << (8 * (j & 3));
+    }
+    if (m == 16) {
+        *reinterpret_cast<uint4*>(u + o) = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {
+        for (int j = 0; j < m; ++j) u[o + j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
     }
 }
 
