@@ -671,7 +671,7 @@ void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_
         const bool k16 = k1max < 32768;
         const int32_t* ktab = K1;
         if (k16) {
-            int16_t* K16 = p->dx1.as<int16_t>(p->n_slots ? p->n_slots : 1);
+            int16_t* K16 = p->dx1.as<int16_t>(p->n_slots + 2);  // word gathers may read one entry past the end
             k32_to_k16(K1, p->n_slots, K16, st);
             ktab = reinterpret_cast<const int32_t*>(K16);
         }

@@ -276,9 +276,32 @@ __device__ __forceinline__ uint32_t ld_u32_hint(const uint32_t* a, uint64_t pol)
     asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
     return v;
 }
+// cp.async (LDGSTS) helpers: global -> shared copies that complete
+// asynchronously; _hint takes an L2 cache policy (createpolicy).
+__device__ __forceinline__ void cp_async(void* smem_dst, const void* gmem_src, int bytes) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+    if (bytes == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem_src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async4_hint(void* smem_dst, const void* gmem_src, uint64_t pol) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(d), "l"(gmem_src), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 __device__ __forceinline__ int32_t ld_s32_hint(const int32_t* a, uint64_t pol) {
     int32_t v;
     asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int32_t ld_s16_hint(const int16_t* a, uint64_t pol) {
+    int16_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.s16 %0, [%1], %2;" : "=h"(v) : "l"(a), "l"(pol));
     return v;
 }
 __device__ __forceinline__ uint4 ld_v4_hint(const void* a, uint64_t pol) {

@@ -208,17 +208,6 @@ constexpr int BTP = 512;  // threads per persistent bucket CTA
 // cp.async copies of bucket k+1 (xE chunks, lperm, lnode, segment offsets)
 // are in flight, and the chunk table of bucket k+2 is prefetched to
 // registers. Same arithmetic, same order as k_bucket.
-__device__ __forceinline__ void cp_async(void* smem_dst, const void* gmem_src, int bytes) {
-    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
-    if (bytes == 8)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem_src) : "memory");
-    else
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gmem_src) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
 struct PipeStage {
     double* xs;     // [kBucketCap]
     uint16_t* lp;   // [kBucketCap + 2]
