@@ -512,7 +512,7 @@ void decode_component(umcg_plan* p, const CompHeader& h, const uint8_t* d_payloa
             int32_t* K32 = p->dx1.as<int32_t>(h.n ? h.n : 1);
             dec_fused(DEC_P64, U, ulen, h.n, status, ctl, nullptr, nullptr, 0.0, bin, nullptr, P, st);
             const bool wide = check_fused(p, ctl, U, ulen, h.n, st).aux[7] != 0;
-            nd_from_prefix(P, h.n, sh, P + h.n, K32, ctl, st);
+            nd_from_prefix(P, h.n, sh, P + h.n, K32, nullptr, ctl, st);
             const DevCtl hc = read_ctl(p, ctl, st);
             if (!wide && (double)hc.max_abs_k[0] < k_lim(2, h.D)) {
                 k32_to_f64(K32, h.n, bin, d_out, st);
@@ -544,8 +544,9 @@ void decode_component(umcg_plan* p, const CompHeader& h, const uint8_t* d_payloa
 
 // Grid component in the pipeline: prefer the int32 lattice form (K1). Returns
 // true with K1 filled, or false with x1f (fp64 values) filled.
-static bool decode_grid(umcg_plan* p, const CompHeader& h, const uint8_t* d_payload, int32_t* K1, double* x1f,
-                        uint64_t* kmax, cudaStream_t st) {
+// K16 (optional) receives (int16)K1, exact when *kmax < 2^15.
+static bool decode_grid(umcg_plan* p, const CompHeader& h, const uint8_t* d_payload, int32_t* K1, int16_t* K16,
+                        double* x1f, uint64_t* kmax, cudaStream_t st) {
     const int pred = (h.pred == 2 && h.D == 1) ? 1 : h.pred;
     const double bin = 2.0 * h.tau;
     const bool lattice = h.codec == 0 && h.backend == 0 && h.D <= 8 && h.tau != 0.0 && !h.n_esc &&
@@ -563,7 +564,7 @@ static bool decode_grid(umcg_plan* p, const CompHeader& h, const uint8_t* d_payl
         int64_t* P = p->kbuf.as<int64_t>(2 * (h.n ? h.n : 1));
         dec_fused(DEC_P64, U, ulen, h.n, status, ctl, nullptr, nullptr, 0.0, bin, nullptr, P, st);
         const bool wide = check_fused(p, ctl, U, ulen, h.n, st).aux[7] != 0;
-        nd_from_prefix(P, h.n, make_shape(h.D, h.dims), P + h.n, K1, ctl, st);
+        nd_from_prefix(P, h.n, make_shape(h.D, h.dims), P + h.n, K1, K16, ctl, st);
         const DevCtl hc = read_ctl(p, ctl, st);
         *kmax = hc.max_abs_k[0];
         if (!wide && (double)hc.max_abs_k[0] < k_lim(pred, h.D)) return true;
@@ -650,7 +651,8 @@ void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_
     int32_t* K1 = p->codes1.as<int32_t>(p->n_slots ? p->n_slots : 1);
     const int g_kind = (flags & 2u) ? 1 : 0;
     uint64_t k1max = ~0ull;
-    const bool k1_lattice = decode_grid(p, h1, d_ar + p1, K1, x1, &k1max, st);
+    int16_t* K16 = p->dx1.as<int16_t>(p->n_slots + 2);  // word gathers may read one entry past the end
+    const bool k1_lattice = decode_grid(p, h1, d_ar + p1, K1, K16, x1, &k1max, st);
     const double bin1 = 2.0 * h1.tau;
     // Fast path: nearest g over the lattice grid, residual decoded and
     // recomposed in one pass (decode.cu, DEC_RECOMPOSE).
@@ -670,11 +672,7 @@ void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_
         // |K1| < 2^15: gather from an int16 copy (half the L2 footprint)
         const bool k16 = k1max < 32768;
         const int32_t* ktab = K1;
-        if (k16) {
-            int16_t* K16 = p->dx1.as<int16_t>(p->n_slots + 2);  // word gathers may read one entry past the end
-            k32_to_k16(K1, p->n_slots, K16, st);
-            ktab = reinterpret_cast<const int32_t*>(K16);
-        }
+        if (k16) ktab = reinterpret_cast<const int32_t*>(K16);  // written by decode_grid
         dec_fused(k16 ? DEC_RECOMPOSE16 : DEC_RECOMPOSE, U, ulen, p->n, status, ctl, p->d_node.as<uint32_t>(1),
                   ktab, bin1, bin2, d_out, nullptr, st);
         const DevCtl hc = check_fused(p, ctl, U, ulen, p->n, st);

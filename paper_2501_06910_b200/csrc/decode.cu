@@ -174,19 +174,32 @@ __global__ void __launch_bounds__(RT) k_dec_agg(const uint8_t* __restrict__ U, u
 }
 
 // Exclusive scan of tile aggregates in one CTA; total count -> ctl->count.
+// Each thread owns a contiguous run of tiles, read 8 at a time so the loads
+// overlap (the scan is latency-bound).
 __global__ void __launch_bounds__(1024) k_scan_cs(CS* __restrict__ aggs, uint64_t T, DevCtl* ctl) {
     using BS = cub::BlockScan<CS, 1024>;
     __shared__ typename BS::TempStorage tmp;
     const uint64_t per = (T + 1023) / 1024;
-    const uint64_t t0 = threadIdx.x * per, t1 = min(T, t0 + per);
+    const uint64_t t0 = min(T, threadIdx.x * per), t1 = min(T, t0 + per);
     CS local{0, 0};
-    for (uint64_t t = t0; t < t1; ++t) local = CSAdd()(local, aggs[t]);
+    for (uint64_t t = t0; t < t1; t += 8) {
+        CS v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = t + k < t1 ? aggs[t + k] : CS{0, 0};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) local = CSAdd()(local, v[k]);
+    }
     CS excl, tot;
     BS(tmp).ExclusiveScan(local, excl, CS{0, 0}, CSAdd(), tot);
-    for (uint64_t t = t0; t < t1; ++t) {
-        const CS c = aggs[t];
-        aggs[t] = excl;
-        excl = CSAdd()(excl, c);
+    for (uint64_t t = t0; t < t1; t += 8) {
+        CS v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = t + k < t1 ? aggs[t + k] : CS{0, 0};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (t + k < t1) aggs[t + k] = excl;
+            excl = CSAdd()(excl, v[k]);
+        }
     }
     if (threadIdx.x == 0) ctl->count = tot.cnt;
 }
@@ -299,7 +312,7 @@ __global__ void k_axis_cols(int64_t* __restrict__ K, uint64_t n, uint64_t len, u
 template <bool FINAL>
 __global__ void __launch_bounds__(256) k_nd_mid(const int64_t* __restrict__ P, uint64_t d_out, uint64_t d_mid,
                                                uint64_t d_fast, int64_t* __restrict__ Kw, int32_t* __restrict__ K32,
-                                               DevCtl* ctl) {
+                                               int16_t* __restrict__ K16, DevCtl* ctl) {
     const uint64_t line = blockIdx.x * 256ull + threadIdx.x;  // over d_out * d_fast
     uint64_t amax = 0;
     if (line < d_out * d_fast) {
@@ -328,6 +341,7 @@ __global__ void __launch_bounds__(256) k_nd_mid(const int64_t* __restrict__ P, u
                 const uint64_t idx = base + j * d_fast + k;
                 if (FINAL) {
                     K32[idx] = (int32_t)acc;
+                    if (K16) K16[idx] = (int16_t)acc;
                     const uint64_t a = (uint64_t)(acc < 0 ? -acc : acc);
                     amax = a > amax ? a : amax;
                 } else {
@@ -347,7 +361,7 @@ __global__ void __launch_bounds__(256) k_nd_mid(const int64_t* __restrict__ P, u
 
 // Last scan for D == 3 along the outer axis (stride d1*d2), int32 out + max|K|.
 __global__ void __launch_bounds__(256) k_nd_outer(const int64_t* __restrict__ Kw, uint64_t d0, uint64_t plane,
-                                                 int32_t* __restrict__ K32, DevCtl* ctl) {
+                                                 int32_t* __restrict__ K32, int16_t* __restrict__ K16, DevCtl* ctl) {
     const uint64_t c = blockIdx.x * 256ull + threadIdx.x;
     uint64_t amax = 0;
     if (c < plane) {
@@ -361,6 +375,7 @@ __global__ void __launch_bounds__(256) k_nd_outer(const int64_t* __restrict__ Kw
                 if (i0 + u >= d0) break;
                 acc += v[u];
                 K32[(i0 + u) * plane + c] = (int32_t)acc;
+                if (K16) K16[(i0 + u) * plane + c] = (int16_t)acc;
                 const uint64_t a = (uint64_t)(acc < 0 ? -acc : acc);
                 amax = a > amax ? a : amax;
             }
@@ -373,12 +388,14 @@ __global__ void __launch_bounds__(256) k_nd_outer(const int64_t* __restrict__ Kw
     if ((threadIdx.x & 31) == 0 && amax > ctl->max_abs_k[0]) atomicMax(&ctl->max_abs_k[0], (unsigned long long)amax);
 }
 
-__global__ void k_k32(const int64_t* __restrict__ K, uint64_t n, int32_t* __restrict__ K32, DevCtl* ctl) {
+__global__ void k_k32(const int64_t* __restrict__ K, uint64_t n, int32_t* __restrict__ K32,
+                      int16_t* __restrict__ K16, DevCtl* ctl) {
     const uint64_t i = blockIdx.x * 256ull + threadIdx.x;
     uint64_t a = 0;
     if (i < n) {
         const int64_t v = K[i];
         K32[i] = (int32_t)v;
+        if (K16) K16[i] = (int16_t)v;
         a = (uint64_t)(v < 0 ? -v : v);
     }
     for (int o = 16; o; o >>= 1) {
@@ -429,8 +446,8 @@ void dec_fused(int mode, const uint8_t* U, uint64_t ulen, uint64_t n, void* stat
     UMCG_LAUNCHED();
 }
 
-void nd_from_prefix(const int64_t* P, uint64_t n, const NdShape& sh, int64_t* Kw, int32_t* K32, DevCtl* ctl,
-                    cudaStream_t st) {
+void nd_from_prefix(const int64_t* P, uint64_t n, const NdShape& sh, int64_t* Kw, int32_t* K32, int16_t* K16,
+                    DevCtl* ctl, cudaStream_t st) {
     const unsigned g = (unsigned)cdiv(n, 256);
     if (!n) return;
     const int64_t* src = P;
@@ -438,12 +455,12 @@ void nd_from_prefix(const int64_t* P, uint64_t n, const NdShape& sh, int64_t* Kw
         const uint64_t d2 = sh.dims[sh.D - 1], d1 = sh.dims[sh.D - 2], d0 = sh.D == 3 ? sh.dims[0] : 1;
         const unsigned g1 = (unsigned)cdiv(d0 * d2, 256);
         if (sh.D == 2) {
-            k_nd_mid<true><<<g1, 256, 0, st>>>(P, d0, d1, d2, nullptr, K32, ctl);
+            k_nd_mid<true><<<g1, 256, 0, st>>>(P, d0, d1, d2, nullptr, K32, K16, ctl);
             UMCG_LAUNCHED();
         } else {
-            k_nd_mid<false><<<g1, 256, 0, st>>>(P, d0, d1, d2, Kw, nullptr, ctl);
+            k_nd_mid<false><<<g1, 256, 0, st>>>(P, d0, d1, d2, Kw, nullptr, nullptr, ctl);
             UMCG_LAUNCHED();
-            k_nd_outer<<<(unsigned)cdiv(d1 * d2, 256), 256, 0, st>>>(Kw, d0, d1 * d2, K32, ctl);
+            k_nd_outer<<<(unsigned)cdiv(d1 * d2, 256), 256, 0, st>>>(Kw, d0, d1 * d2, K32, K16, ctl);
             UMCG_LAUNCHED();
         }
         return;
@@ -458,7 +475,7 @@ void nd_from_prefix(const int64_t* P, uint64_t n, const NdShape& sh, int64_t* Kw
         }
         src = Kw;
     }
-    k_k32<<<g, 256, 0, st>>>(src, n, K32, ctl);
+    k_k32<<<g, 256, 0, st>>>(src, n, K32, K16, ctl);
     UMCG_LAUNCHED();
 }
 

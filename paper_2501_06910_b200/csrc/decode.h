@@ -19,7 +19,8 @@ void dec_fused(int mode, const uint8_t* U, uint64_t ulen, uint64_t n, void* stat
 // N-D inclusive prefix from the plain 1-D prefix P of row-major codes:
 // row differencing (fastest axis) + scans along the other axes -> int32 K,
 // max|K| -> ctl->max_abs_k[0]. Kw is int64 scratch [n] (unused when D == 1).
-void nd_from_prefix(const int64_t* P, uint64_t n, const NdShape& sh, int64_t* Kw, int32_t* K32, DevCtl* ctl,
+void nd_from_prefix(const int64_t* P, uint64_t n, const NdShape& sh, int64_t* Kw, int32_t* K32, int16_t* K16,
+                    DevCtl* ctl,
                     cudaStream_t st);
 void k32_to_k16(const int32_t* K, uint64_t n, int16_t* K16, cudaStream_t st);
 void k32_to_f64(const int32_t* K, uint64_t n, double bin, double* x, cudaStream_t st);
