@@ -732,6 +732,7 @@ void encode_impl(const double* d_v, uint64_t n, int pred, int D, const uint64_t*
         DevCtl hset{};
         hset.tau_c[0] = tau;
         hset.bin[0] = 2.0 * tau;
+        hset.inv_bin[0] = 1.0 / hset.bin[0];
         hset.min_key = ~0ull;
         UMCG_CUDA(cudaMemcpyAsync(ctl, &hset, sizeof(DevCtl), cudaMemcpyHostToDevice, st));
         const bool wide = lossless || serial;

@@ -53,7 +53,7 @@ __device__ __forceinline__ void flag_serial(DevCtl* ctl, int comp) {
 // Lattice index of v with the escape / regime checks of codec.hpp:305-314.
 __device__ __forceinline__ double lattice_k(double v, double bin, double tau, double lim,
                                             DevCtl* ctl, int comp) {
-    const double K = round(v / bin);
+    const double K = round_div(v, bin, ctl->inv_bin[comp]);
     bool bad = !(fabs(K) < lim);
     if (!bad) bad = !(fabs(v - K * bin) <= tau);
     if (bad) flag_serial(ctl, comp);
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(THREADS) k_codes_1d(const double* __restrict__
     const double lim = k_limit(pred, 1);
     const double K = lattice_k(v[i], bin, tau, lim, ctl, comp);
     double Kp = 0.0;
-    if (pred == 1 && i > 0) Kp = round(v[i - 1] / bin);
+    if (pred == 1 && i > 0) Kp = round_div(v[i - 1], bin, ctl->inv_bin[comp]);
     const int64_t q = (int64_t)K - (int64_t)Kp;
     codes[i] = (uint32_t)zz_enc(q);
 }
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(THREADS) k_codes_residual(ResidualSrc s, uint6
     if (i0 >= n) return;
     const double bin = ctl->bin[1], tau = ctl->tau_c[1];
     const double lim = k_limit(1, 1);
-    double Kp = i0 ? round(residual_at(s, i0 - 1) / bin) : 0.0;
+    double Kp = i0 ? round_div(residual_at(s, i0 - 1), bin, ctl->inv_bin[1]) : 0.0;
 #pragma unroll
     for (int k = 0; k < RES_ITEMS; ++k) {
         const uint64_t i = i0 + k;

@@ -328,6 +328,7 @@ struct DevCtl {
     double tau_abs, tau1, tau2;           // unshaved split
     double tau_c[2];                      // shaved per component
     double bin[2];                        // 2 * tau_c
+    double inv_bin[2];                    // fl(1 / bin) for round_div
     int lossless;                         // tau_abs == 0
     // per-component fast-path verdicts
     int need_serial[2];                   // escape / regime violation: redo exactly
@@ -343,6 +344,18 @@ struct DevCtl {
 };
 
 __device__ __forceinline__ void set_err(DevCtl* c, int e) { atomicCAS(&c->err, 0, e); }
+
+// round(fl(r / bin)) (the reference's std::round(r / bin), codec.hpp:307)
+// without the IEEE divide on the common path: q = fl(r * inv), inv =
+// fl(1 / bin), lies within 3 ulp of fl(r / bin), so unless q is within
+// 8 ulp of a half-integer both round (half away from zero) to the same
+// integer. The ambiguous band and non-finite q take the exact divide.
+__device__ __forceinline__ double round_div(double r, double bin, double inv) {
+    const double q = __dmul_rn(r, inv);
+    const double f = fabs(__dsub_rn(q, trunc(q)));
+    if (!(fabs(__dsub_rn(f, 0.5)) > __dmul_rn(fabs(q), 0x1p-49))) return round(__ddiv_rn(r, bin));
+    return round(q);
+}
 
 // Order-preserving map double -> u64 (for atomicMin/Max over doubles).
 __host__ __device__ __forceinline__ unsigned long long dkey(double v) {

@@ -52,6 +52,8 @@ __global__ void k_budget(BudgetArgs a, DevCtl* ctl) {
     ctl->tau_c[1] = __dmul_rn(t2, shave);
     ctl->bin[0] = __dmul_rn(2.0, ctl->tau_c[0]);
     ctl->bin[1] = __dmul_rn(2.0, ctl->tau_c[1]);
+    ctl->inv_bin[0] = __ddiv_rn(1.0, ctl->bin[0]);
+    ctl->inv_bin[1] = __ddiv_rn(1.0, ctl->bin[1]);
     ctl->lossless = (ctl->tau_c[0] == 0.0 ? 1 : 0) | (ctl->tau_c[1] == 0.0 ? 2 : 0);
 }
 

@@ -81,8 +81,8 @@ __device__ __forceinline__ void flag_serial1(DevCtl* ctl) {
 
 // lattice index with the escape / regime checks of codec.hpp:305-314
 // (same as codes.cu lattice_k, 1-D limit 2^30).
-__device__ __forceinline__ int32_t resid_k(double r, double bin, double tau, DevCtl* ctl) {
-    const double K = round(__ddiv_rn(r, bin));
+__device__ __forceinline__ int32_t resid_k(double r, double bin, double inv, double tau, DevCtl* ctl) {
+    const double K = round_div(r, bin, inv);
     bool bad = !(fabs(K) < 1073741824.0);
     if (!bad) bad = !(fabs(__dsub_rn(r, __dmul_rn(K, bin))) <= tau);
     if (bad) flag_serial1(ctl);
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
     const uint64_t b = blockIdx.x;
     const uint32_t s0 = bstart[b], s1 = bstart[b + 1], m = s1 - s0;
     const uint32_t j0 = bnode[b], j1 = bnode[b + 1], nj = j1 - j0;
-    const double bin = ctl->bin[1], tau = ctl->tau_c[1];
+    const double bin = ctl->bin[1], inv = ctl->inv_bin[1], tau = ctl->tau_c[1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int NW = BT / 32;
     // chunk table (one chunk per epoch, bucket-major) + segment offsets
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
         for (uint32_t e = warp; e < E; e += NW)
             for (uint32_t l = ch[e].x + lane; l < ch[e + 1].x; l += 32) {
                 const uint32_t q = ch[e].y + (l - ch[e].x);
-                KE[q] = resid_k(__dsub_rn(xE[q], mean), bin, tau, ctl);
+                KE[q] = resid_k(__dsub_rn(xE[q], mean), bin, inv, tau, ctl);
             }
         return;
     }
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
             const uint32_t l = threadIdx.x + k * BT;
             if (l < m) {
                 while (l >= ch[e + 1].x) ++e;
-                KE[ch[e].y + (l - ch[e].x)] = resid_k(__dsub_rn(xs[l], x1s[ln[l]]), bin, tau, ctl);
+                KE[ch[e].y + (l - ch[e].x)] = resid_k(__dsub_rn(xs[l], x1s[ln[l]]), bin, inv, tau, ctl);
             }
         }
     }
@@ -270,37 +270,57 @@ __global__ void __launch_bounds__(BTP) k_bucket_pipe(const double* __restrict__ 
     }
     const uint32_t* bstart = bk;
     const uint32_t* bnode = bk + B + 1;
-    const double bin = ctl->bin[1], tau = ctl->tau_c[1];
+    const double bin = ctl->bin[1], inv = ctl->inv_bin[1], tau = ctl->tau_c[1];
     const uint32_t G = gridDim.x;
     uint32_t k = blockIdx.x;
     if (k >= n_regular) return;
-    // prologue: chunk table of the first bucket, copies of the first bucket,
-    // chunk table of the second bucket into registers
-    uint32_t b = regular[k];
+    // Per-bucket scalars travel through registers ahead of use so no
+    // dependent global-load chain (regular -> bstart/bnode) sits on the
+    // critical path: info of bucket k+G and the id of bucket k+2G are loaded
+    // one iteration early.
+    struct Info { uint32_t s0, m, j0, nj; };
+    auto load_info = [&](uint32_t bb) {
+        const uint32_t a0 = __ldg(&bstart[bb]), a1 = __ldg(&bstart[bb + 1]);
+        const uint32_t c0 = __ldg(&bnode[bb]), c1 = __ldg(&bnode[bb + 1]);
+        return Info{a0, a1 - a0, c0, c1 - c0};
+    };
+    // prologue: chunk table + copies of the first bucket; chunk table, info
+    // of the second; id of the third
+    uint32_t b = __ldg(&regular[k]);
+    Info cur = load_info(b);
     if (threadIdx.x <= E) S[0].ch[threadIdx.x] = __ldg(&bct[b * (uint64_t)(E + 1) + threadIdx.x]);
     __syncthreads();
-    issue_bucket(S[0], xE, lperm, lnode, seg, bstart[b], bstart[b + 1] - bstart[b], bnode[b], bnode[b + 1] - bnode[b], E);
+    issue_bucket(S[0], xE, lperm, lnode, seg, cur.s0, cur.m, cur.j0, cur.nj, E);
     cp_commit();
     uint2 chreg = make_uint2(0, 0);
-    if (k + G < n_regular && threadIdx.x <= E) chreg = __ldg(&bct[regular[k + G] * (uint64_t)(E + 1) + threadIdx.x]);
+    Info nxt{0, 0, 0, 0};
+    uint32_t b2 = 0;
+    if (k + G < n_regular) {
+        const uint32_t bn = __ldg(&regular[k + G]);
+        nxt = load_info(bn);
+        if (threadIdx.x <= E) chreg = __ldg(&bct[bn * (uint64_t)(E + 1) + threadIdx.x]);
+        if (k + 2 * G < n_regular) b2 = __ldg(&regular[k + 2 * G]);
+    }
     for (uint32_t it = 0; k < n_regular; ++it, k += G) {
         const int st = it & 1;
-        b = regular[k];
         const bool has_next = k + G < n_regular;
         if (has_next && threadIdx.x <= E) S[st ^ 1].ch[threadIdx.x] = chreg;
         __syncthreads();
+        Info nn{0, 0, 0, 0};
+        uint32_t b3 = 0;
         if (has_next) {
-            const uint32_t bn = regular[k + G];
-            issue_bucket(S[st ^ 1], xE, lperm, lnode, seg, bstart[bn], bstart[bn + 1] - bstart[bn], bnode[bn],
-                         bnode[bn + 1] - bnode[bn], E);
-            if (k + 2 * G < n_regular && threadIdx.x <= E)
-                chreg = __ldg(&bct[regular[k + 2 * G] * (uint64_t)(E + 1) + threadIdx.x]);
+            issue_bucket(S[st ^ 1], xE, lperm, lnode, seg, nxt.s0, nxt.m, nxt.j0, nxt.nj, E);
+            if (k + 2 * G < n_regular) {
+                nn = load_info(b2);
+                if (threadIdx.x <= E) chreg = __ldg(&bct[b2 * (uint64_t)(E + 1) + threadIdx.x]);
+                if (k + 3 * G < n_regular) b3 = __ldg(&regular[k + 3 * G]);
+            }
         }
         cp_commit();
         cp_wait<1>();
         __syncthreads();
         const PipeStage& C = S[st];
-        const uint32_t s0 = bstart[b], m = bstart[b + 1] - s0, j0 = bnode[b], nj = bnode[b + 1] - j0;
+        const uint32_t s0 = cur.s0, j0 = cur.j0, nj = cur.nj;
         const uint32_t off = s0 & 1u;
         // interpolate_to_grid (interp.hpp:58-64): 0.0 + x_a + x_b + ... in ascending vertex order
         for (uint32_t j = threadIdx.x; j < nj; j += BTP) {
@@ -318,9 +338,12 @@ __global__ void __launch_bounds__(BTP) k_bucket_pipe(const double* __restrict__ 
             for (uint32_t e = warp; e < E; e += BTP / 32) {
                 const uint2 c0 = C.ch[e], c1 = C.ch[e + 1];
                 for (uint32_t l = c0.x + lane; l < c1.x; l += 32)
-                    KE[c0.y + (l - c0.x)] = resid_k(__dsub_rn(C.xs[l], x1s[C.ln[l + off]]), bin, tau, ctl);
+                    KE[c0.y + (l - c0.x)] = resid_k(__dsub_rn(C.xs[l], x1s[C.ln[l + off]]), bin, inv, tau, ctl);
             }
         }
+        cur = nxt;
+        nxt = nn;
+        b2 = b3;
         __syncthreads();
     }
     cp_wait<0>();

@@ -1,7 +1,9 @@
-"""Per-CUDA-source-line stall samples of one kernel (.ncu-rep source page)."""
+"""Per-CUDA-source-line stall samples (or another source-page column, e.g.
+"Instructions Executed") of one kernel: ncu_hot.py rep kernel [top] [column]."""
 import csv, subprocess, sys
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
+col = sys.argv[4] if len(sys.argv) > 4 else "Warp Stall Sampling (All Samples)"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kern}", "--print-source", "sass,cuda"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
@@ -10,7 +12,7 @@ agg, cur = {}, None
 for r in rows:
     if r and r[0] == "Line No":
         hdr = r
-        si = hdr.index("Warp Stall Sampling (All Samples)")
+        si = hdr.index(col)
         continue
     if not hdr or len(r) <= si:
         continue
