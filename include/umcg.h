@@ -178,7 +178,10 @@ umcg_status umcg_encode(const double* d_values, uint64_t n, int predictor, int n
 umcg_status umcg_decode(const uint8_t* d_payload, uint64_t len, double* d_out, uint64_t n_capacity,
                         uint64_t* n_out, void* stream);
 
-/* Zero-RLE byte stage alone (lossless.hpp:24-70), device to device. */
+/* Zero-RLE byte stage alone (lossless.hpp:24-70, rle_compress /
+ * rle_decompress), device to device. umcg_rle_bound(n) bounds the output of
+ * umcg_rle_compress; errors follow rle_decompress (corrupt_payload). */
+uint64_t umcg_rle_bound(uint64_t n);
 umcg_status umcg_rle_compress(const uint8_t* d_in, uint64_t n, uint8_t* d_out, uint64_t capacity,
                               uint64_t* out_len, void* stream);
 umcg_status umcg_rle_decompress(const uint8_t* d_in, uint64_t n, uint8_t* d_out,

@@ -37,7 +37,8 @@ EXPORTED = [
     "umcg_plan_create", "umcg_plan_build", "umcg_plan_destroy", "umcg_plan_get_info",
     "umcg_plan_export", "umcg_compress_bound", "umcg_compress", "umcg_compress_batch",
     "umcg_decompress", "umcg_compress_host", "umcg_decompress_host", "umcg_encode_bound",
-    "umcg_encode", "umcg_decode", "umcg_rle_compress", "umcg_rle_decompress", "umcg_gen_config",
+    "umcg_encode", "umcg_decode", "umcg_rle_bound", "umcg_rle_compress", "umcg_rle_decompress",
+    "umcg_gen_config",
     "umcg_kernel_launches", "umcg_serial_fallbacks", "umcg_profile_enable", "umcg_profile_dump",
     "umcg_last_error", "umcg_version",
 ]
@@ -100,6 +101,10 @@ def lib():
     L.umcg_profile_dump.argtypes = [C.c_char_p, C.c_uint64]
     L.umcg_encode_bound.restype = C.c_uint64
     L.umcg_encode_bound.argtypes = [C.c_uint64, C.c_int]
+    L.umcg_rle_bound.restype = C.c_uint64
+    L.umcg_rle_bound.argtypes = [C.c_uint64]
+    L.umcg_rle_compress.argtypes = [vp, C.c_uint64, vp, C.c_uint64, u64p, vp]
+    L.umcg_rle_decompress.argtypes = [vp, C.c_uint64, vp, C.c_uint64, u64p, vp]
     L.umcg_plan_create.argtypes = [C.POINTER(GridDesc), C.POINTER(MappingDesc), C.c_int, f64p,
                                    C.POINTER(vp)]
     L.umcg_plan_build.argtypes = [C.POINTER(GridDesc), C.c_uint64, vp, C.c_double, C.c_int,
@@ -328,6 +333,32 @@ def decode(payload: bytes, n_capacity: int | None = None, device="cuda"):
     _check(lib().umcg_decode(C.c_void_p(a.data_ptr()), len(payload), C.c_void_p(out.data_ptr()),
                              n_capacity, C.byref(n), _stream_ptr()))
     return out[: n.value]
+
+
+def rle_compress(data: bytes, device="cuda") -> bytes:
+    """umc::rle_compress (lossless.hpp:24-51) of a byte string, on the device."""
+    import torch
+    n = len(data)
+    a = torch.from_numpy(np.frombuffer(data, np.uint8).copy()).to(device) if n else \
+        torch.zeros(1, dtype=torch.uint8, device=device)
+    cap = int(lib().umcg_rle_bound(n))
+    out = torch.empty(max(cap, 1), dtype=torch.uint8, device=device)
+    ln = C.c_uint64()
+    _check(lib().umcg_rle_compress(C.c_void_p(a.data_ptr()), n, C.c_void_p(out.data_ptr()), cap,
+                                   C.byref(ln), _stream_ptr()))
+    return bytes(out[: ln.value].cpu().numpy())
+
+
+def rle_decompress(stream: bytes, capacity: int, device="cuda") -> bytes:
+    """umc::rle_decompress (lossless.hpp:53-70) of a token stream, on the device."""
+    import torch
+    a = torch.from_numpy(np.frombuffer(stream, np.uint8).copy()).to(device) if stream else \
+        torch.zeros(1, dtype=torch.uint8, device=device)
+    out = torch.empty(max(capacity, 1), dtype=torch.uint8, device=device)
+    ln = C.c_uint64()
+    _check(lib().umcg_rle_decompress(C.c_void_p(a.data_ptr()), len(stream), C.c_void_p(out.data_ptr()),
+                                     capacity, C.byref(ln), _stream_ptr()))
+    return bytes(out[: ln.value].cpu().numpy())
 
 
 def gen_config(config: int, lattice: int, seed: int, coords: bool = True, values: bool = True,

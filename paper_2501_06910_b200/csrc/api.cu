@@ -63,7 +63,7 @@ struct HdrArgs {
     int pred[2], D[2];
     uint64_t dims[2][3];
     uint64_t n[2];
-    int lossless_codes[2];  // unused by layout, kept for debugging
+    int codec;              // 0 builtin PQ, 1 verbatim (both components)
 };
 
 __device__ __forceinline__ void put_le(uint8_t* d, uint64_t off, uint64_t v, int k) {
@@ -71,9 +71,9 @@ __device__ __forceinline__ void put_le(uint8_t* d, uint64_t off, uint64_t v, int
 }
 __device__ __forceinline__ uint64_t comp_hdr_bytes(int D) { return 4 + 8 + 8 + 1 + 8ull * D + 8; }
 
-__device__ uint64_t write_comp_header(uint8_t* a, uint64_t o, int pred, double tau, uint64_t n, int D,
+__device__ uint64_t write_comp_header(uint8_t* a, uint64_t o, int codec, int pred, double tau, uint64_t n, int D,
                                       const uint64_t* dims, uint64_t n_esc) {
-    a[o] = 0;              // codec_id (builtin PQ)
+    a[o] = (uint8_t)codec;  // codec_id: 0 builtin PQ, 1 verbatim
     a[o + 1] = (uint8_t)pred;
     a[o + 2] = 0;          // backend_id
     a[o + 3] = 0;
@@ -106,7 +106,7 @@ __global__ void k_layout_archive(HdrArgs h, DevCtl* ctl, uint8_t* a) {
         ctl->payload_len[c] = pl;
         put_le(a, o, pl, 8);
         o += 8;
-        const uint64_t e = write_comp_header(a, o, h.pred[c], ctl->tau_c[c], h.n[c], h.D[c], h.dims[c],
+        const uint64_t e = write_comp_header(a, o, h.codec, h.pred[c], ctl->tau_c[c], h.n[c], h.D[c], h.dims[c],
                                              ctl->n_esc[c]);
         ctl->aux[2 + c] = e;  // escape records offset
         ctl->stream_off[c] = e + 16 * ctl->n_esc[c];
@@ -116,9 +116,9 @@ __global__ void k_layout_archive(HdrArgs h, DevCtl* ctl, uint8_t* a) {
 }
 
 // Bare component payload (umcg_encode).
-__global__ void k_layout_component(int pred, int D, NdShape sh, uint64_t n, DevCtl* ctl, uint8_t* a) {
+__global__ void k_layout_component(int codec, int pred, int D, NdShape sh, uint64_t n, DevCtl* ctl, uint8_t* a) {
     if (threadIdx.x | blockIdx.x) return;
-    const uint64_t e = write_comp_header(a, 0, pred, ctl->tau_c[0], n, D, sh.dims, ctl->n_esc[0]);
+    const uint64_t e = write_comp_header(a, 0, codec, pred, ctl->tau_c[0], n, D, sh.dims, ctl->n_esc[0]);
     ctl->aux[2] = e;
     ctl->stream_off[0] = e + 16 * ctl->n_esc[0];
     ctl->payload_len[0] = ctl->stream_off[0] + ctl->stream_len[0];
@@ -190,7 +190,60 @@ void host_budget(double tau_abs, double rho, double coeff, double* tc) {
 struct CompressMode {
     bool lossless[2];
     bool serial[2];
+    bool verbatim;  // codec 1: both components are RLE'd raw fp64 bytes (codec.hpp:240-248)
 };
+
+HdrArgs archive_hdr(umcg_plan* p, const umcg_params& prm, const std::string& name, int codec, int pred1, int D1,
+                    const uint64_t* dims1, cudaStream_t st) {
+    HdrArgs h{};
+    uint16_t flags = 0;
+    if (p->mode == 1) flags |= 1u;
+    if (prm.g_kind == 1) flags |= 2u;
+    if (prm.bound_kind == 1) flags |= 4u;
+    h.flags = flags;
+    h.name_len = (uint16_t)name.size();
+    uint8_t* dname = p->hdr.as<uint8_t>(name.size() + 1);
+    if (!name.empty()) {
+        auto* hs = static_cast<uint8_t*>(p->hstage.reserve(name.size()));
+        std::memcpy(hs, name.data(), name.size());
+        UMCG_CUDA(cudaMemcpyAsync(dname, hs, name.size(), cudaMemcpyHostToDevice, st));
+    }
+    h.name = dname;
+    h.digest = p->digest;
+    h.tau = prm.tau;
+    h.rho = prm.split_rho;
+    h.codec = codec;
+    h.pred[0] = pred1; h.pred[1] = 1;
+    h.D[0] = D1; h.D[1] = 1;
+    for (int d = 0; d < 3; ++d) { h.dims[0][d] = dims1[d]; h.dims[1][d] = d == 0 ? p->n : 1; }
+    h.n[0] = p->n_slots; h.n[1] = p->n;
+    return h;
+}
+
+// Verbatim codec (id 1) for both components: the raw little-endian fp64
+// bytes of x1 and of the residuals through the zero-RLE stage
+// (codec.hpp:240-248, lossless.hpp:96-99); no escapes.
+DevCtl verbatim_pass(umcg_plan* p, const umcg_params& prm, const std::string& name, uint8_t* d_ar,
+                     const ResidualSrc& rs, const double* x1, int pred1, int D1, const uint64_t* dims1,
+                     cudaStream_t st) {
+    const uint64_t n = p->n, n1 = p->n_slots;
+    auto* ctl = p->ctl.as<DevCtl>(1);
+    double* x2 = p->scratch_c.as<double>(n ? n : 1);
+    materialize_residual(rs, n, x2, st);
+    const uint8_t* bytes[2] = {reinterpret_cast<const uint8_t*>(x1), reinterpret_cast<const uint8_t*>(x2)};
+    const uint64_t nb[2] = {8 * n1, 8 * n};
+    StreamEncScratch es[2];
+    for (int c = 0; c < 2; ++c) {
+        DevBuf& eb = c == 0 ? p->enc1 : p->enc2;
+        es[c] = stream_enc_carve(eb.reserve(stream_enc_scratch_bytes(nb[c])), nb[c]);
+        stream_plan_u8(bytes[c], nb[c], es[c], ctl, c, st);
+    }
+    const HdrArgs h = archive_hdr(p, prm, name, 1, pred1, D1, dims1, st);
+    k_layout_archive<<<1, 32, 0, st>>>(h, ctl, d_ar);
+    UMCG_LAUNCHED();
+    for (int c = 0; c < 2; ++c) stream_write_u8(bytes[c], nb[c], es[c], ctl, c, d_ar, true, st);
+    return read_ctl(p, ctl, st);
+}
 
 // One pass of the compress pipeline. Returns the device control block.
 DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int x_f32, const std::string& name,
@@ -199,7 +252,7 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     auto* ctl = p->ctl.as<DevCtl>(1);
     init_ctl(ctl, st);
     // nearest g: partitioned layout (partition.cu); multilinear: gathers
-    const bool part = prm.g_kind == 0 && p->n_buckets > 0;
+    const bool part = prm.g_kind == 0 && p->n_buckets > 0 && !m.verbatim;
     double* x1 = p->x1.as<double>(n1 ? n1 : 1);
     int32_t* Kp = nullptr;
     if (part) {
@@ -235,6 +288,8 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     rs.axis_off = p->d_axis_off.as<uint64_t>(1);
     rs.D = p->dim;
     for (int d = 0; d < 3; ++d) rs.shape[d] = p->shape[d];
+
+    if (m.verbatim) return verbatim_pass(p, prm, name, d_ar, rs, x1, pred1, D1, dims1, st);
 
     // codes
     void* codes[2] = {nullptr, nullptr};
@@ -293,27 +348,7 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
         else if (wide[c]) stream_plan_u64(static_cast<uint64_t*>(codes[c]), ncode[c], es[c], ctl, c, st);
         else stream_plan_u32(static_cast<uint32_t*>(codes[c]), ncode[c], es[c], ctl, c, st);
     }
-    HdrArgs h{};
-    uint16_t flags = 0;
-    if (p->mode == 1) flags |= 1u;
-    if (prm.g_kind == 1) flags |= 2u;
-    if (prm.bound_kind == 1) flags |= 4u;
-    h.flags = flags;
-    h.name_len = (uint16_t)name.size();
-    uint8_t* dname = p->hdr.as<uint8_t>(name.size() + 1);
-    if (!name.empty()) {
-        auto* hs = static_cast<uint8_t*>(p->hstage.reserve(name.size()));
-        std::memcpy(hs, name.data(), name.size());
-        UMCG_CUDA(cudaMemcpyAsync(dname, hs, name.size(), cudaMemcpyHostToDevice, st));
-    }
-    h.name = dname;
-    h.digest = p->digest;
-    h.tau = prm.tau;
-    h.rho = prm.split_rho;
-    h.pred[0] = pred1; h.pred[1] = 1;
-    h.D[0] = D1; h.D[1] = 1;
-    for (int d = 0; d < 3; ++d) { h.dims[0][d] = dims1[d]; h.dims[1][d] = d == 0 ? n : 1; }
-    h.n[0] = n1; h.n[1] = n;
+    const HdrArgs h = archive_hdr(p, prm, name, 0, pred1, D1, dims1, st);
     k_layout_archive<<<1, 32, 0, st>>>(h, ctl, d_ar);
     UMCG_LAUNCHED();
     for (int c = 0; c < 2; ++c) {
@@ -350,7 +385,8 @@ void compress_impl(umcg_plan* p, const umcg_params* prm_in, const void* d_x, int
     else if (!(prm.coeff_abs_sum > 0.0)) { perr = UMCG_BUDGET_INADMISSIBLE; pmsg = "coefficient sum must be positive"; }
     else if (prm.g_kind == 1 && p->mode == 1) { perr = UMCG_SEED_MODE_UNSUPPORTED; pmsg = "multilinear back-interpolation needs a dense grid component"; }
     else if (prm.g_kind == 1 && !p->has_coords) { perr = UMCG_INVALID_ARGUMENT; pmsg = "multilinear g needs a plan with vertex coordinates"; }
-    else if (prm.codec_id != 0) { perr = UMCG_UNKNOWN_CODEC; pmsg = "only the builtin PQ codec (id 0) runs on the device path"; }
+    else if (prm.codec_id >= 128) { perr = UMCG_UNKNOWN_CODEC; pmsg = "external codec " + std::to_string(prm.codec_id) + " is a host subprocess plugin (out of the device path)"; }
+    else if (prm.codec_id > 1) { perr = UMCG_UNKNOWN_CODEC; pmsg = "unknown codec id " + std::to_string(prm.codec_id); }
     else if (prm.backend_id != 0) { perr = UMCG_UNKNOWN_CODEC; pmsg = "lossless backend " + std::to_string(prm.backend_id) + " not registered"; }
     else if (name.size() > 0xffff) { perr = UMCG_MALFORMED_FILE; pmsg = "field name too long"; }
     if (perr != UMCG_OK) {
@@ -375,9 +411,14 @@ void compress_impl(umcg_plan* p, const umcg_params* prm_in, const void* d_x, int
     } else {
         m.lossless[0] = m.lossless[1] = prm.tau == 0.0;
     }
+    m.verbatim = prm.codec_id == 1;
     for (int iter = 0; iter < 3; ++iter) {
         const DevCtl hc = compress_pass(p, prm, d_x, x_f32, name, d_ar, m, st);
         if (hc.nonfinite) fail(UMCG_NON_FINITE_VALUE, "non-finite field value");
+        if (m.verbatim) {
+            *out_len = hc.archive_len;
+            return;
+        }
         bool redo = false;
         for (int c = 0; c < 2; ++c) {
             const bool ll = (hc.lossless >> c) & 1;
@@ -489,6 +530,18 @@ static double k_lim(int pred, int D) { return pred == 1 || D <= 1 ? 1073741824.0
 
 // codec.hpp:364-441 on device memory, general path: values [n] fp64.
 void decode_component(umcg_plan* p, const CompHeader& h, const uint8_t* d_payload, double* d_out, cudaStream_t st) {
+    if (h.codec == 1) {  // verbatim (codec.hpp:387-397)
+        if (h.n_esc != 0) fail(UMCG_CORRUPT_PAYLOAD, "verbatim payload with escapes");
+        if (h.backend != 0)
+            fail(UMCG_UNKNOWN_CODEC, "lossless backend " + std::to_string(h.backend) + " not registered");
+        auto* ctl = p->ctl.as<DevCtl>(1);
+        init_ctl(ctl, st);
+        uint64_t ulen = 0;
+        const uint8_t* U = stream_unpack(d_payload + h.stream_off, h.stream_len, p->dec, ctl, st, &ulen);
+        if (ulen != 8 * h.n) fail(UMCG_CORRUPT_PAYLOAD, "verbatim stream length mismatch");
+        if (ulen) UMCG_CUDA(cudaMemcpyAsync(d_out, U, ulen, cudaMemcpyDeviceToDevice, st));
+        return;
+    }
     uint64_t* eidx;
     double* evals;
     decode_prelude(p, h, d_payload, &eidx, &evals, st);
@@ -718,12 +771,28 @@ void encode_impl(const double* d_v, uint64_t n, int pred, int D, const uint64_t*
     minmax(d_v, 0, n, ctl, st);
     DevCtl hc = read_ctl(p, ctl, st);
     if (hc.nonfinite) fail(UMCG_NON_FINITE_VALUE, "non-finite input to encode");
-    if (codec == 1 || codec >= 128) fail(UMCG_UNKNOWN_CODEC, "codec " + std::to_string(codec) + " is a host plugin (out of the device path)");
-    if (codec != 0) fail(UMCG_UNKNOWN_CODEC, "unknown codec id " + std::to_string(codec));
+    if (codec >= 128) fail(UMCG_UNKNOWN_CODEC, "external codec " + std::to_string(codec) + " is a host subprocess plugin (out of the device path)");
+    if (codec > 1) fail(UMCG_UNKNOWN_CODEC, "unknown codec id " + std::to_string(codec));
     if (backend != 0) fail(UMCG_UNKNOWN_CODEC, "lossless backend " + std::to_string(backend) + " not registered");
     const uint64_t need = payload_bound(n, D);
     if (!d_out || cap < need) fail(UMCG_INVALID_ARGUMENT, "payload capacity " + std::to_string(cap) + " < bound " + std::to_string(need));
     const NdShape sh = make_shape(D, dims);
+    if (codec == 1) {  // verbatim: header, no escapes, RLE of the raw fp64 bytes (codec.hpp:240-248)
+        init_ctl(ctl, st);
+        DevCtl hset{};
+        hset.tau_c[0] = tau;
+        hset.min_key = ~0ull;
+        UMCG_CUDA(cudaMemcpyAsync(ctl, &hset, sizeof(DevCtl), cudaMemcpyHostToDevice, st));
+        const uint64_t nb = 8 * n;
+        StreamEncScratch es = stream_enc_carve(p->enc1.reserve(stream_enc_scratch_bytes(nb)), nb);
+        const auto* bytes = reinterpret_cast<const uint8_t*>(d_v);
+        stream_plan_u8(bytes, nb, es, ctl, 0, st);
+        k_layout_component<<<1, 32, 0, st>>>(1, pred, D, sh, n, ctl, d_out);
+        UMCG_LAUNCHED();
+        stream_write_u8(bytes, nb, es, ctl, 0, d_out, true, st);
+        *out_len = read_ctl(p, ctl, st).archive_len;
+        return;
+    }
     const int epred = (pred == 2 && D == 1) ? 1 : pred;
     const bool lossless = tau == 0.0;
     bool serial = false;
@@ -756,7 +825,7 @@ void encode_impl(const double* d_v, uint64_t n, int pred, int D, const uint64_t*
         StreamEncScratch es = stream_enc_carve(p->enc1.reserve(stream_enc_scratch_bytes(n)), n);
         if (wide) stream_plan_u64(static_cast<uint64_t*>(codes), n, es, ctl, 0, st);
         else stream_plan_u32(static_cast<uint32_t*>(codes), n, es, ctl, 0, st);
-        k_layout_component<<<1, 32, 0, st>>>(pred, D, sh, n, ctl, d_out);
+        k_layout_component<<<1, 32, 0, st>>>(0, pred, D, sh, n, ctl, d_out);
         UMCG_LAUNCHED();
         if (serial) {
             hc = read_ctl(p, ctl, st);
@@ -970,11 +1039,43 @@ umcg_status umcg_decode(const uint8_t* d_payload, uint64_t len, double* d_out, u
     return guarded([&] { decode_impl(d_payload, len, d_out, n_cap, n_out, static_cast<cudaStream_t>(stream)); });
 }
 
-umcg_status umcg_rle_compress(const uint8_t*, uint64_t, uint8_t*, uint64_t, uint64_t*, void*) {
-    return guarded([&] { fail(UMCG_ERROR, "umcg_rle_compress: not built in this round"); });
+uint64_t umcg_rle_bound(uint64_t n) { return n + 16 + 2 * (n / 8 + 2) * 11; }
+
+umcg_status umcg_rle_compress(const uint8_t* d_in, uint64_t n, uint8_t* d_out, uint64_t cap, uint64_t* out_len,
+                              void* stream) {
+    return guarded([&] {
+        if (!out_len || (n && !d_in)) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
+        const auto st = static_cast<cudaStream_t>(stream);
+        umcg_plan* p = codec_ws();
+        auto* ctl = p->ctl.as<DevCtl>(1);
+        init_ctl(ctl, st);
+        StreamEncScratch es = stream_enc_carve(p->enc1.reserve(stream_enc_scratch_bytes(n)), n);
+        stream_plan_u8(d_in, n, es, ctl, 0, st);
+        const uint64_t len = read_ctl(p, ctl, st).stream_len[0];
+        if (len > cap || (len && !d_out))
+            fail(UMCG_INVALID_ARGUMENT, "output capacity " + std::to_string(cap) + " < " + std::to_string(len));
+        stream_write_u8(d_in, n, es, ctl, 0, d_out, false, st);
+        UMCG_CUDA(cudaStreamSynchronize(st));
+        *out_len = len;
+    });
 }
-umcg_status umcg_rle_decompress(const uint8_t*, uint64_t, uint8_t*, uint64_t, uint64_t*, void*) {
-    return guarded([&] { fail(UMCG_ERROR, "umcg_rle_decompress: not built in this round"); });
+
+umcg_status umcg_rle_decompress(const uint8_t* d_in, uint64_t len, uint8_t* d_out, uint64_t cap,
+                                uint64_t* out_len, void* stream) {
+    return guarded([&] {
+        if (!out_len || (len && !d_in)) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
+        const auto st = static_cast<cudaStream_t>(stream);
+        umcg_plan* p = codec_ws();
+        auto* ctl = p->ctl.as<DevCtl>(1);
+        init_ctl(ctl, st);
+        uint64_t ulen = 0;
+        const uint8_t* U = stream_unpack(d_in, len, p->dec, ctl, st, &ulen);
+        if (ulen > cap || (ulen && !d_out))
+            fail(UMCG_INVALID_ARGUMENT, "output capacity " + std::to_string(cap) + " < " + std::to_string(ulen));
+        if (ulen) UMCG_CUDA(cudaMemcpyAsync(d_out, U, ulen, cudaMemcpyDeviceToDevice, st));
+        UMCG_CUDA(cudaStreamSynchronize(st));
+        *out_len = ulen;
+    });
 }
 
 }  // extern "C"

@@ -110,6 +110,9 @@ __device__ __forceinline__ uint64_t state_pos(const RleState& s, const uint64_t*
 // Byte writer into the staging buffer (no bounds checks: the tile's output
 // fits CAP by construction). Returns the varint length.
 template <class T>
+__device__ __forceinline__ uint32_t put_code(uint8_t* o, T v);
+
+template <class T>
 __device__ __forceinline__ uint32_t put_varint(uint8_t* o, T v) {
     uint64_t u = (uint64_t)v;
     uint32_t k = 0;
@@ -119,6 +122,16 @@ __device__ __forceinline__ uint32_t put_varint(uint8_t* o, T v) {
     }
     o[k++] = (uint8_t)u;
     return k;
+}
+
+// One code's stream bytes (see clen).
+template <class T>
+__device__ __forceinline__ uint32_t put_code(uint8_t* o, T v) {
+    if (sizeof(T) == 1) {
+        o[0] = (uint8_t)v;
+        return 1u;
+    }
+    return put_varint(o, v);
 }
 
 // Staged bytes out[ao, ao+len) -> d[0, len) where ao = d & 15: 16-byte
@@ -175,7 +188,7 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_write_fast(const T* __restr
 #pragma unroll
     for (int k = 0; k < ENC_ITEMS; ++k) {
         const uint32_t r = r0 + k;
-        if (k < cnt && r >= core_lo && r < core_hi) w += v[k] == 0 ? 1u : vlen64((uint64_t)v[k]);
+        if (k < cnt && r >= core_lo && r < core_hi) w += clen(v[k]);
     }
     uint32_t off, core_total;
     BS32(tmp).ExclusiveSum(w, off, core_total);
@@ -225,7 +238,7 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_write_fast(const T* __restr
 #pragma unroll
     for (int k = 0; k < ENC_ITEMS; ++k) {
         const uint32_t r = r0 + k;
-        if (k < cnt && r >= core_lo && r < core_hi) pos += put_varint(o + pos, v[k]);
+        if (k < cnt && r >= core_lo && r < core_hi) pos += put_code(o + pos, v[k]);
     }
     __syncthreads();
     copy_out16(out, ao, len, d);
@@ -299,7 +312,7 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_write_general(const T* __re
             const bool lng = J >= kMinZeroRun;
             lngm |= (uint32_t)lng << k;
             opnm |= (uint32_t)(lng || (prev < 0 && !E.has)) << k;
-            dsum += (lng ? 0u : (uint32_t)J) + vlen64((uint64_t)v[k]);
+            dsum += (lng ? 0u : (uint32_t)J) + clen(v[k]);
             prev = r0 + k;
         }
     }
@@ -314,7 +327,7 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_write_general(const T* __re
             dpre[r0 + k] = acc;
             if (!(nzm >> k & 1)) continue;
             const uint64_t J = run_before(r0 + k, prev);
-            acc += (lngm >> k & 1 ? 0u : (uint32_t)J) + vlen64((uint64_t)v[k]);
+            acc += (lngm >> k & 1 ? 0u : (uint32_t)J) + clen(v[k]);
             prev = r0 + k;
         }
         if (threadIdx.x == ENC_THREADS - 1) dpre[ENC_TILE] = acc;
@@ -343,7 +356,7 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_write_general(const T* __re
             if (!(nzm >> k & 1)) continue;
             const uint64_t J = run_before(r0 + k, prev);
             const bool lng = lngm >> k & 1;
-            usum += (lng ? 1u + vlen64(J) : (uint32_t)J) + vlen64((uint64_t)v[k]);
+            usum += (lng ? 1u + vlen64(J) : (uint32_t)J) + clen(v[k]);
             if (opnm >> k & 1) usum += 1u + vlen64(lit_T(k));
             prev = r0 + k;
         }
@@ -367,7 +380,7 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_write_general(const T* __re
             }
             if (!lng)
                 for (uint32_t z = 0; z < (uint32_t)J; ++z) o[pos++] = 0;
-            pos += put_varint(o + pos, v[k]);
+            pos += put_code(o + pos, v[k]);
             prev = r0 + k;
         }
     }
@@ -471,6 +484,10 @@ void stream_write_u32(const uint32_t* c, uint64_t n, const StreamEncScratch& s, 
                       uint8_t* dst, bool o, cudaStream_t st) { write_impl(c, n, s, ctl, comp, dst, o, st); }
 void stream_write_u64(const uint64_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
                       uint8_t* dst, bool o, cudaStream_t st) { write_impl(c, n, s, ctl, comp, dst, o, st); }
+void stream_plan_u8(const uint8_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
+                    cudaStream_t st) { plan_impl(c, n, s, ctl, comp, st); }
+void stream_write_u8(const uint8_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
+                     uint8_t* dst, bool o, cudaStream_t st) { write_impl(c, n, s, ctl, comp, dst, o, st); }
 void stream_encode_u32(const uint32_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
                        uint8_t* dst, bool o, cudaStream_t st) {
     plan_impl(c, n, s, ctl, comp, st);

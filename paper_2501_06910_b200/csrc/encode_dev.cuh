@@ -11,6 +11,15 @@ struct RleComposeOp {
     }
 };
 
+// Bytes one code occupies in the stream before RLE: varint(code) for the
+// quantizer's codes (common.hpp:60-66); one raw byte for uint8_t "codes"
+// (the verbatim codec and umcg_rle_compress feed raw bytes, lossless.hpp:24).
+template <class T>
+__device__ __forceinline__ uint32_t clen(T v) {
+    if (sizeof(T) == 1) return 1u;
+    return v == 0 ? 1u : vlen64((uint64_t)v);
+}
+
 template <class T>
 __device__ __forceinline__ void write_varint(uint8_t* out, uint64_t pos, uint64_t base, uint64_t cap, T v) {
     uint64_t u = (uint64_t)v;
@@ -62,7 +71,7 @@ __device__ __forceinline__ RleSum thread_summary(const T (&v)[ENC_ITEMS], int cn
     uint64_t fb = 0;
 #pragma unroll
     for (int k = 0; k < ENC_ITEMS; ++k)
-        if (k >= lo && k <= hi) fb += v[k] == 0 ? 1u : vlen64((uint64_t)v[k]);
+        if (k >= lo && k <= hi) fb += clen(v[k]);
     s.lz = (uint64_t)lo;
     s.tz = (uint64_t)(cnt - 1 - hi);
     s.fb = fb;

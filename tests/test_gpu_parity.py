@@ -433,3 +433,67 @@ def test_config3_full_size_properties(cuda, tau):
     err = (out - x).abs().max().item()
     assert err <= tau * rng, (err, tau * rng)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_rle_raw_bytes_match_reference(cuda, ref, seed):
+    """umcg_rle_compress / umcg_rle_decompress against rle_compress /
+    rle_decompress (lossless.hpp:24-70): empty input, all zeros, bytes >= 0x80,
+    zero runs of every length around the 8-byte threshold, sizes across the
+    2048-byte tiles (test_lossless.cpp:188-220 cases)."""
+    rng = np.random.default_rng(300 + seed)
+    cases = [b"", bytes(1000), bytes([0x80] * 9), bytes(7) + b"\xff" + bytes(8)]
+    for _ in range(6):
+        n = int(rng.choice([1, 17, 2047, 2048, 2049, 30000, 300000]))
+        parts, tot = [], 0
+        while tot < n:
+            if rng.random() < 0.4:
+                k = int(rng.choice([1, 6, 7, 8, 9, 15, 100, 5000]))
+                parts.append(bytes(k))
+            else:
+                k = int(rng.integers(1, 40))
+                parts.append(rng.integers(0, 256, k, dtype=np.uint8).tobytes())
+            tot += k
+        cases.append(b"".join(parts)[:n])
+    for data in cases:
+        want = ref.rle_compress(data)
+        assert umcg.rle_compress(data) == want, len(data)
+        assert umcg.rle_decompress(want, len(data)) == data
+    with pytest.raises(umcg.UmcgError) as e:
+        umcg.rle_decompress(b"\x02\x05", 16)
+    assert e.value.kind == "corrupt_payload"
+
+
+def test_verbatim_codec_matches_reference(cuda, ref):
+    """Codec id 1 (codec.hpp:240-248, 387-397): payload byte-identical to
+    the reference, decode bitwise, and the verbatim error checks."""
+    rng = np.random.default_rng(44)
+    arrays = [np.zeros(5000), rng.normal(size=20000), np.array([1.0, -0.0, 5e307, 1e-300]),
+              np.repeat(rng.normal(size=300), 40)]
+    for v in arrays:
+        for pred, dims in ((1, None), (0, None)):
+            got = umcg.encode(dev(v), predictor=pred, dims=dims, tau=1e-3, codec_id=1)
+            want = ref.encode(v, predictor=pred, dims=dims, tau=1e-3, codec_id=1)
+            assert got == want
+            back = umcg.decode(got).cpu().numpy()
+            assert np.array_equal(back.view(np.uint64), v.view(np.uint64))
+    pl = bytearray(ref.encode(arrays[1], predictor=1, tau=1e-3, codec_id=1))
+    with pytest.raises(umcg.UmcgError) as e:
+        umcg.decode(bytes(pl[:-3]), n_capacity=len(arrays[1]))
+    assert e.value.kind == "corrupt_payload"
+
+
+def test_pipeline_verbatim_codec_matches_reference(cuda, ref, oracle):
+    """compress(..., codec_id=1): both components verbatim (pipeline.hpp:
+    96-110, 140-146). Cluster means and residuals are exact, so the archive
+    is byte-identical and the decode bitwise equal to the reference's."""
+    params, cases = load_cases()
+    for k, s, x, archives in cases[:4]:
+        plan = plan_for(s)
+        for fill in (0, 1) if s.mode == 0 else (0,):
+            b = umcg.Budget(tau=1e-3, codec_id=1, fill=fill)
+            got = plan.compress(dev(x), b, name="v")
+            want = ref.compress(s, x, name="v", tau=1e-3, codec_id=1, fill=fill)
+            assert got == want, (k, fill)
+            out = plan.decompress(got).cpu().numpy()
+            assert np.array_equal(out.view(np.uint64), ref.decompress(s, want).view(np.uint64))
