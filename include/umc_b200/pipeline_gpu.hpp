@@ -145,6 +145,54 @@ inline Archive compress(const Field& field, const MappingTable& map, const RectG
     return deserialize_archive(bytes);  // pipeline.hpp:237 builds the reference's Archive
 }
 
+/// umc::compress_baseline (pipeline.hpp:152-162) on the GPU: one 1-D
+/// component at tau_abs (umcg_encode, codec 0 or 1).
+inline EncodedComponent compress_baseline(const Field& field, double tau_abs,
+                                          std::uint8_t codec_id = kCodecBuiltinPQ, std::uint8_t backend_id = 0) {
+    const std::uint64_t n = field.values.size();
+    void* d_v = nullptr;
+    void* d_p = nullptr;
+    const std::uint64_t cap = umcg_encode_bound(n, 1);
+    if (cudaMalloc(&d_v, n * 8 + 8) != cudaSuccess || cudaMalloc(&d_p, cap) != cudaSuccess) {
+        cudaFree(d_v);
+        throw error("cudaMalloc failed");
+    }
+    if (n) cudaMemcpy(d_v, field.values.data(), n * 8, cudaMemcpyHostToDevice);
+    const std::uint64_t dims[1] = {n};
+    std::uint64_t len = 0;
+    const umcg_status s = umcg_encode(static_cast<const double*>(d_v), n, 1, 1, dims, tau_abs, codec_id, backend_id,
+                                      static_cast<std::uint8_t*>(d_p), cap, &len, nullptr);
+    EncodedComponent comp;
+    if (s == UMCG_OK) {
+        comp.payload.resize(len);
+        cudaMemcpy(comp.payload.data(), d_p, len, cudaMemcpyDeviceToHost);
+    }
+    cudaFree(d_v);
+    cudaFree(d_p);
+    detail::check(s);
+    comp.spec.codec_id = codec_id;
+    comp.spec.backend_id = backend_id;
+    comp.spec.predictor = Predictor::lorenzo_1d;
+    comp.spec.dims = {n};
+    comp.spec.tau_abs = tau_abs;
+    comp.n_elements = n;
+    comp.original_bytes = n * 8;
+    return comp;
+}
+
+/// umc::baseline_archive (pipeline.hpp:164-176) on the GPU.
+inline Archive baseline_archive(const Field& field, const ErrorBudget& budget,
+                                std::uint8_t codec_id = kCodecBuiltinPQ, std::uint8_t backend_id = 0) {
+    Archive ar;
+    ar.baseline = true;
+    ar.bound_kind = budget.bound_kind;
+    ar.field_name = field.name;
+    ar.tau = budget.tau;
+    ar.rho = budget.split_rho;
+    ar.component1 = b200::compress_baseline(field, resolve_tau_abs(budget, field.values), codec_id, backend_id);
+    return ar;
+}
+
 /// umc::decompress (pipeline.hpp:180-210) on the GPU.
 inline Field decompress(const Archive& archive, const MappingTable& map, const RectGrid& grid, const Mesh& mesh) {
     const auto bytes = serialize_archive(archive);

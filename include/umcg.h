@@ -178,6 +178,16 @@ umcg_status umcg_encode(const double* d_values, uint64_t n, int predictor, int n
 umcg_status umcg_decode(const uint8_t* d_payload, uint64_t len, double* d_out, uint64_t n_capacity,
                         uint64_t* n_out, void* stream);
 
+/* Serialization baseline (pipeline.hpp:152-176, baseline_archive): the
+ * field in file order as ONE lorenzo_1d component at the full budget,
+ * tau_abs = resolve_tau_abs(budget, values); archive flag 8, digest 0, empty
+ * residual component. Decoded by umcg_decode on component 1 (the drop-in
+ * wrapper's decompress does this, pipeline.hpp:184-187). */
+uint64_t umcg_baseline_bound(uint64_t n, uint64_t name_len);
+umcg_status umcg_compress_baseline(const umcg_params* params, const double* d_values, uint64_t n,
+                                   const char* name, uint8_t* d_archive, uint64_t capacity,
+                                   uint64_t* out_len, void* stream);
+
 /* Zero-RLE byte stage alone (lossless.hpp:24-70, rle_compress /
  * rle_decompress), device to device. umcg_rle_bound(n) bounds the output of
  * umcg_rle_compress; errors follow rle_decompress (corrupt_payload). */

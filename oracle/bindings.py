@@ -208,6 +208,14 @@ class Ref:
                                            C.byref(p), C.byref(n)))
         return _bytes_out(self, p, n)
 
+    def baseline_archive(self, x, name="x", tau=1e-3, rho=0.5, bound_kind=1, codec_id=0) -> bytes:
+        x = np.ascontiguousarray(x, np.float64)
+        p, n = u8p(), C.c_uint64()
+        self._check(self.lib.umcref_baseline_archive(_ptr(x, f64p), len(x), name.encode(), C.c_double(tau),
+                                                     C.c_double(rho), bound_kind, codec_id, C.byref(p),
+                                                     C.byref(n)))
+        return _bytes_out(self, p, n)
+
     def decode(self, payload: bytes, n_cap: int) -> np.ndarray:
         buf = np.frombuffer(payload, np.uint8)
         out = np.empty(max(n_cap, 1), np.float64)

@@ -212,6 +212,24 @@ int umcref_encode(const double* v, std::uint64_t n, int predictor, int ndims,
     });
 }
 
+// umc::baseline_archive (pipeline.hpp:164-176), serialized.
+int umcref_baseline_archive(const double* values, std::uint64_t n, const char* name, double tau, double rho,
+                            int bound_kind, int codec_id, std::uint8_t** out, std::uint64_t* out_len) {
+    return guarded([&] {
+        umc::Field f;
+        f.name = name ? name : "";
+        f.values.assign(values, values + n);
+        umc::ErrorBudget b;
+        b.tau = tau;
+        b.split_rho = rho;
+        b.bound_kind = bound_kind ? umc::BoundKind::relative_to_range : umc::BoundKind::absolute;
+        const auto ar = umc::baseline_archive(f, b, static_cast<std::uint8_t>(codec_id));
+        const auto bytes = umc::serialize_archive(ar);
+        *out = dup_bytes(bytes);
+        *out_len = bytes.size();
+    });
+}
+
 int umcref_decode(const std::uint8_t* p, std::uint64_t len, double* out, std::uint64_t n_cap,
                   std::uint64_t* n_out) {
     return guarded([&] {

@@ -37,7 +37,7 @@ EXPORTED = [
     "umcg_plan_create", "umcg_plan_build", "umcg_plan_destroy", "umcg_plan_get_info",
     "umcg_plan_export", "umcg_compress_bound", "umcg_compress", "umcg_compress_batch",
     "umcg_decompress", "umcg_compress_host", "umcg_decompress_host", "umcg_encode_bound",
-    "umcg_encode", "umcg_decode", "umcg_rle_bound", "umcg_rle_compress", "umcg_rle_decompress",
+    "umcg_encode", "umcg_decode", "umcg_baseline_bound", "umcg_compress_baseline", "umcg_rle_bound", "umcg_rle_compress", "umcg_rle_decompress",
     "umcg_gen_config",
     "umcg_kernel_launches", "umcg_serial_fallbacks", "umcg_profile_enable", "umcg_profile_dump",
     "umcg_last_error", "umcg_version",
@@ -101,6 +101,9 @@ def lib():
     L.umcg_profile_dump.argtypes = [C.c_char_p, C.c_uint64]
     L.umcg_encode_bound.restype = C.c_uint64
     L.umcg_encode_bound.argtypes = [C.c_uint64, C.c_int]
+    L.umcg_baseline_bound.restype = C.c_uint64
+    L.umcg_baseline_bound.argtypes = [C.c_uint64, C.c_uint64]
+    L.umcg_compress_baseline.argtypes = [C.POINTER(Params), vp, C.c_uint64, C.c_char_p, vp, C.c_uint64, u64p, vp]
     L.umcg_rle_bound.restype = C.c_uint64
     L.umcg_rle_bound.argtypes = [C.c_uint64]
     L.umcg_rle_compress.argtypes = [vp, C.c_uint64, vp, C.c_uint64, u64p, vp]
@@ -333,6 +336,20 @@ def decode(payload: bytes, n_capacity: int | None = None, device="cuda"):
     _check(lib().umcg_decode(C.c_void_p(a.data_ptr()), len(payload), C.c_void_p(out.data_ptr()),
                              n_capacity, C.byref(n), _stream_ptr()))
     return out[: n.value]
+
+
+def compress_baseline(d_values, budget: "Budget", name: str = "") -> bytes:
+    """umc::baseline_archive (pipeline.hpp:164-176) serialized: one lorenzo_1d
+    component of the field at the full budget."""
+    import torch
+    n = d_values.numel()
+    nb = name.encode()
+    cap = int(lib().umcg_baseline_bound(n, len(nb)))
+    buf = torch.empty(cap, dtype=torch.uint8, device=d_values.device)
+    ln = C.c_uint64()
+    _check(lib().umcg_compress_baseline(C.byref(budget.c()), C.c_void_p(d_values.data_ptr()), n, nb,
+                                        C.c_void_p(buf.data_ptr()), cap, C.byref(ln), _stream_ptr()))
+    return bytes(buf[: ln.value].cpu().numpy())
 
 
 def rle_compress(data: bytes, device="cuda") -> bytes:

@@ -1039,6 +1039,57 @@ umcg_status umcg_decode(const uint8_t* d_payload, uint64_t len, double* d_out, u
     return guarded([&] { decode_impl(d_payload, len, d_out, n_cap, n_out, static_cast<cudaStream_t>(stream)); });
 }
 
+uint64_t umcg_baseline_bound(uint64_t n, uint64_t name_len) { return 10 + name_len + 24 + 16 + payload_bound(n, 1); }
+
+umcg_status umcg_compress_baseline(const umcg_params* prm, const double* d_values, uint64_t n, const char* name_c,
+                                   uint8_t* d_ar, uint64_t cap, uint64_t* len, void* stream) {
+    return guarded([&] {
+        if (!prm || !len || (n && !d_values)) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
+        const auto st = static_cast<cudaStream_t>(stream);
+        const std::string name = name_c ? name_c : "";
+        // resolve_tau_abs (pipeline.hpp:37-41), then compress_baseline's encode
+        if (!(prm->tau >= 0.0)) fail(UMCG_BUDGET_INADMISSIBLE, "tau must be >= 0");
+        double tau_abs = prm->tau;
+        umcg_plan* p = codec_ws();
+        if (prm->bound_kind == 1) {
+            auto* ctl = p->ctl.as<DevCtl>(1);
+            init_ctl(ctl, st);
+            minmax(d_values, 0, n, ctl, st);
+            const DevCtl hc = read_ctl(p, ctl, st);
+            const double range = n ? dkey_inv(hc.max_key) - dkey_inv(hc.min_key) : 0.0;
+            tau_abs = prm->tau * range;
+        }
+        const uint64_t h1 = 10 + name.size() + 24 + 8;
+        if (!d_ar || cap < umcg_baseline_bound(n, name.size()))
+            fail(UMCG_INVALID_ARGUMENT, "archive capacity below umcg_baseline_bound");
+        const uint64_t dims[1] = {n};
+        uint64_t l1 = 0;
+        encode_impl(d_values, n, 1, 1, dims, tau_abs, prm->codec_id, prm->backend_id, d_ar + h1, cap - h1 - 8, &l1,
+                    st);
+        if (name.size() > 0xffff) fail(UMCG_MALFORMED_FILE, "field name too long");
+        // serialize_archive (pipeline.hpp:214-235): baseline flag 8, no digest, empty component 2
+        std::vector<uint8_t> hb(h1), tail(8, 0);
+        auto put = [&](uint64_t o, uint64_t v, int k) { for (int i = 0; i < k; ++i) hb[o + i] = (uint8_t)(v >> (8 * i)); };
+        hb[0] = 'U'; hb[1] = 'M'; hb[2] = 'C'; hb[3] = 'Z';
+        put(4, 1, 2);
+        put(6, 8u | (prm->bound_kind == 1 ? 4u : 0u), 2);
+        put(8, name.size(), 2);
+        std::memcpy(hb.data() + 10, name.data(), name.size());
+        uint64_t o = 10 + name.size();
+        uint64_t tb, rb;
+        std::memcpy(&tb, &prm->tau, 8);
+        std::memcpy(&rb, &prm->split_rho, 8);
+        put(o, 0, 8);
+        put(o + 8, tb, 8);
+        put(o + 16, rb, 8);
+        put(o + 24, l1, 8);
+        UMCG_CUDA(cudaMemcpyAsync(d_ar, hb.data(), h1, cudaMemcpyHostToDevice, st));
+        UMCG_CUDA(cudaMemcpyAsync(d_ar + h1 + l1, tail.data(), 8, cudaMemcpyHostToDevice, st));
+        UMCG_CUDA(cudaStreamSynchronize(st));
+        *len = h1 + l1 + 8;
+    });
+}
+
 uint64_t umcg_rle_bound(uint64_t n) { return n + 16 + 2 * (n / 8 + 2) * 11; }
 
 umcg_status umcg_rle_compress(const uint8_t* d_in, uint64_t n, uint8_t* d_out, uint64_t cap, uint64_t* out_len,

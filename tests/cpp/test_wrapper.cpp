@@ -143,6 +143,25 @@ int main() {
     CHECK(bb.values.size() == rb.values.size(), "baseline size");
     CHECK(max_err(bb.values, rb.values) <= 1e-12 * range, "baseline decode within 1e-12 of the reference");
     CHECK(max_err(bb.values, f.values) <= resolve_tau_abs(ErrorBudget{}, f.values), "baseline bound");
+    // baseline_archive through the drop-in (pipeline.hpp:164-176); codec 0 may
+    // differ from the reference only by rounding-window flips, so compare the
+    // decodes; verbatim (codec 1) is exact bytes
+    const Archive gbase = b200::baseline_archive(f, ErrorBudget{});
+    const Field gb = b200::decompress(gbase, {}, {}, a.mesh);
+    CHECK(max_err(gb.values, f.values) <= resolve_tau_abs(ErrorBudget{}, f.values), "drop-in baseline bound");
+    CHECK(serialize_archive(b200::baseline_archive(f, ErrorBudget{}, kCodecVerbatim)) ==
+              serialize_archive(baseline_archive(f, ErrorBudget{}, kCodecVerbatim)),
+          "verbatim baseline archive byte-identical");
+    // verbatim pipeline archive (codec 1 on both components)
+    {
+        CompressOptions vo;
+        vo.codec_id = kCodecVerbatim;
+        const Archive rv = compress(f, a.map, a.grid, a.mesh, ErrorBudget{}, vo);
+        const Archive gv = b200::compress(f, a.map, a.grid, a.mesh, ErrorBudget{}, vo);
+        CHECK(serialize_archive(rv) == serialize_archive(gv), "verbatim archive byte-identical");
+        CHECK(b200::decompress(gv, a.map, a.grid, a.mesh).values == decompress(rv, a.map, a.grid, a.mesh).values,
+              "verbatim decode bitwise");
+    }
     std::printf("cases %d exact %d failures %d\n", total, exact, failures);
     return failures ? 1 : 0;
 }

@@ -497,3 +497,28 @@ def test_pipeline_verbatim_codec_matches_reference(cuda, ref, oracle):
             assert got == want, (k, fill)
             out = plan.decompress(got).cpu().numpy()
             assert np.array_equal(out.view(np.uint64), ref.decompress(s, want).view(np.uint64))
+
+
+def test_baseline_archive_matches_reference(cuda, ref, oracle):
+    """umcg_compress_baseline == serialize_archive(baseline_archive(...))
+    (pipeline.hpp:152-176, 214-235): one lorenzo_1d component at the full
+    budget, flag 8, no digest; its decode meets the bound."""
+    params, cases = load_cases()
+    rng = np.random.default_rng(8)
+    fields = [cases[0][2], cases[3][2], np.cumsum(rng.normal(size=50000)), np.zeros(1000)]
+    for x in fields:
+        for tau, bk, codec in ((1e-3, 1, 0), (1e-4, 1, 0), (0.01, 0, 0), (1e-3, 1, 1), (0.0, 1, 0)):
+            b = umcg.Budget(tau=tau, bound_kind=bk, codec_id=codec)
+            got = umcg.compress_baseline(dev(x), b, name="base")
+            want = ref.baseline_archive(x, name="base", tau=tau, bound_kind=bk, codec_id=codec)
+            if got != want:
+                ga, ra = parse_archive(got), parse_archive(want)
+                pred = np.concatenate([[0.0], ref.decode(ra["p1"], len(x))[:-1]])
+                check_component(ga["p1"], ra["p1"], x, pred, oracle, f"baseline tau={tau}")
+            p1 = parse_archive(want)["p1"]
+            out = umcg.decode(p1).cpu().numpy()
+            tau_abs = tau * (np.ptp(x) if bk else 1.0)
+            check_decode(out, ref.decode(p1, len(x)), x, tau_abs, f"baseline decode tau={tau}")
+    with pytest.raises(umcg.UmcgError) as e:
+        umcg.compress_baseline(dev(fields[0]), umcg.Budget(tau=-1.0))
+    assert e.value.kind == "budget_inadmissible"
