@@ -216,6 +216,25 @@ struct PipeStage {
     uint2* ch;      // [E + 1]
 };
 
+__host__ __device__ __forceinline__ uint32_t pipe_stage_bytes(uint32_t E) {
+    const uint32_t b = kBucketCap * 8 + (kBucketNodes + 2) * 4 + (E + 1) * 8 + 2 * (kBucketCap + 4) * 2;
+    return (b + 15) & ~15u;
+}
+
+__device__ __forceinline__ PipeStage make_stage(unsigned char* p, uint32_t E) {
+    PipeStage S;
+    S.xs = reinterpret_cast<double*>(p);
+    p += kBucketCap * 8;
+    S.sg = reinterpret_cast<uint32_t*>(p);
+    p += (kBucketNodes + 2) * 4;
+    S.ch = reinterpret_cast<uint2*>(p);
+    p += (E + 1) * 8;
+    S.lp = reinterpret_cast<uint16_t*>(p);
+    p += (kBucketCap + 4) * 2;
+    S.ln = reinterpret_cast<uint16_t*>(p);
+    return S;
+}
+
 __device__ __forceinline__ uint32_t chunk_of(const uint2* ch, uint32_t E, uint32_t l) {
     uint32_t lo = 0, hi = E;
     while (hi - lo > 1) {
@@ -251,23 +270,12 @@ __global__ void __launch_bounds__(BTP) k_bucket_pipe(const double* __restrict__ 
                                                    const uint32_t* __restrict__ seg, DevCtl* ctl,
                                                    double* __restrict__ x1, int32_t* __restrict__ KE) {
     extern __shared__ __align__(16) unsigned char smem[];
-    PipeStage S[2];
-    unsigned char* p = smem;
-    double* x1s = reinterpret_cast<double*>(p);
-    p += kBucketNodes * 8;
-    for (int st = 0; st < 2; ++st) {
-        S[st].xs = reinterpret_cast<double*>(p);
-        p += kBucketCap * 8;
-        S[st].sg = reinterpret_cast<uint32_t*>(p);
-        p += (kBucketNodes + 2) * 4;
-        S[st].ch = reinterpret_cast<uint2*>(p);
-        p += (E + 1) * 8;
-        S[st].lp = reinterpret_cast<uint16_t*>(p);
-        p += (kBucketCap + 4) * 2;
-        S[st].ln = reinterpret_cast<uint16_t*>(p);
-        p += (kBucketCap + 4) * 2;
-        p = reinterpret_cast<unsigned char*>(((uintptr_t)p + 15) & ~(uintptr_t)15);
-    }
+    // Stage pointers are recomputed from the extern shared array (never kept
+    // in a runtime-indexed array) so every access compiles to LDS/STS rather
+    // than generic loads.
+    double* x1s = reinterpret_cast<double*>(smem);
+    const uint32_t stage_bytes = pipe_stage_bytes(E);
+    auto stage = [&](int st) { return make_stage(smem + kBucketNodes * 8 + st * stage_bytes, E); };
     const uint32_t* bstart = bk;
     const uint32_t* bnode = bk + B + 1;
     const double bin = ctl->bin[1], inv = ctl->inv_bin[1], tau = ctl->tau_c[1];
@@ -288,9 +296,9 @@ __global__ void __launch_bounds__(BTP) k_bucket_pipe(const double* __restrict__ 
     // of the second; id of the third
     uint32_t b = __ldg(&regular[k]);
     Info cur = load_info(b);
-    if (threadIdx.x <= E) S[0].ch[threadIdx.x] = __ldg(&bct[b * (uint64_t)(E + 1) + threadIdx.x]);
+    if (threadIdx.x <= E) stage(0).ch[threadIdx.x] = __ldg(&bct[b * (uint64_t)(E + 1) + threadIdx.x]);
     __syncthreads();
-    issue_bucket(S[0], xE, lperm, lnode, seg, cur.s0, cur.m, cur.j0, cur.nj, E);
+    issue_bucket(stage(0), xE, lperm, lnode, seg, cur.s0, cur.m, cur.j0, cur.nj, E);
     cp_commit();
     uint2 chreg = make_uint2(0, 0);
     Info nxt{0, 0, 0, 0};
@@ -304,12 +312,12 @@ __global__ void __launch_bounds__(BTP) k_bucket_pipe(const double* __restrict__ 
     for (uint32_t it = 0; k < n_regular; ++it, k += G) {
         const int st = it & 1;
         const bool has_next = k + G < n_regular;
-        if (has_next && threadIdx.x <= E) S[st ^ 1].ch[threadIdx.x] = chreg;
+        if (has_next && threadIdx.x <= E) stage(st ^ 1).ch[threadIdx.x] = chreg;
         __syncthreads();
         Info nn{0, 0, 0, 0};
         uint32_t b3 = 0;
         if (has_next) {
-            issue_bucket(S[st ^ 1], xE, lperm, lnode, seg, nxt.s0, nxt.m, nxt.j0, nxt.nj, E);
+            issue_bucket(stage(st ^ 1), xE, lperm, lnode, seg, nxt.s0, nxt.m, nxt.j0, nxt.nj, E);
             if (k + 2 * G < n_regular) {
                 nn = load_info(b2);
                 if (threadIdx.x <= E) chreg = __ldg(&bct[b2 * (uint64_t)(E + 1) + threadIdx.x]);
@@ -319,7 +327,7 @@ __global__ void __launch_bounds__(BTP) k_bucket_pipe(const double* __restrict__ 
         cp_commit();
         cp_wait<1>();
         __syncthreads();
-        const PipeStage& C = S[st];
+        const PipeStage C = stage(st);
         const uint32_t s0 = cur.s0, j0 = cur.j0, nj = cur.nj;
         const uint32_t off = s0 & 1u;
         // interpolate_to_grid (interp.hpp:58-64): 0.0 + x_a + x_b + ... in ascending vertex order
@@ -425,9 +433,7 @@ void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double*
     }
     const bool pipe = E + 1 <= BTP && p->n_regular > 0;
     if (pipe) {
-        size_t smem = kBucketNodes * 8;
-        for (int st2 = 0; st2 < 2; ++st2)
-            smem = ((smem + kBucketCap * 8 + (kBucketNodes + 2) * 4 + ((size_t)E + 1) * 8 + (kBucketCap + 4) * 4) + 15) & ~(size_t)15;
+        const size_t smem = kBucketNodes * 8 + 2 * (size_t)pipe_stage_bytes(E);
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
