@@ -53,9 +53,9 @@ __device__ __forceinline__ void flag_serial(DevCtl* ctl, int comp) {
 // Lattice index of v with the escape / regime checks of codec.hpp:305-314.
 __device__ __forceinline__ double lattice_k(double v, double bin, double tau, double lim,
                                             DevCtl* ctl, int comp) {
-    const double K = round_div(v, bin, ctl->inv_bin[comp]);
-    bool bad = !(fabs(K) < lim);
-    if (!bad) bad = !(fabs(v - K * bin) <= tau);
+    double err;
+    const double K = lattice_round(v, bin, ctl->inv_bin[comp], tau, &err);
+    const bool bad = !(fabs(K) < lim) || !(err <= tau);
     if (bad) flag_serial(ctl, comp);
     return K;
 }

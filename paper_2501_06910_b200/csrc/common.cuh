@@ -345,6 +345,23 @@ struct DevCtl {
 
 __device__ __forceinline__ void set_err(DevCtl* c, int e) { atomicCAS(&c->err, 0, e); }
 
+// Lattice index + bound check in one step (codec.hpp:305-314 on the
+// lattice): K = round(fl(r / bin)) and err = |r - K*bin|, bin = 2*tau.
+// K comes from q = fl(r * inv); it can differ from the reference's only when
+// fl(r / bin) lies within a few ulp of a half-integer, and then err sits
+// within ~5 ulp(r) of bin/2 = tau. That band (widened to 2^-45 |r|) takes the
+// IEEE divide, so K and err are exactly the reference's everywhere.
+__device__ __forceinline__ double lattice_round(double r, double bin, double inv, double tau, double* err) {
+    double K = round(__dmul_rn(r, inv));
+    double e = fabs(__dsub_rn(r, __dmul_rn(K, bin)));
+    if (fabs(__dsub_rn(e, tau)) <= __dmul_rn(fabs(r), 0x1p-45)) {
+        K = round(__ddiv_rn(r, bin));
+        e = fabs(__dsub_rn(r, __dmul_rn(K, bin)));
+    }
+    *err = e;
+    return K;
+}
+
 // round(fl(r / bin)) (the reference's std::round(r / bin), codec.hpp:307)
 // without the IEEE divide on the common path: q = fl(r * inv), inv =
 // fl(1 / bin), lies within 3 ulp of fl(r / bin), so unless q is within

@@ -82,9 +82,9 @@ __device__ __forceinline__ void flag_serial1(DevCtl* ctl) {
 // lattice index with the escape / regime checks of codec.hpp:305-314
 // (same as codes.cu lattice_k, 1-D limit 2^30).
 __device__ __forceinline__ int32_t resid_k(double r, double bin, double inv, double tau, DevCtl* ctl) {
-    const double K = round_div(r, bin, inv);
-    bool bad = !(fabs(K) < 1073741824.0);
-    if (!bad) bad = !(fabs(__dsub_rn(r, __dmul_rn(K, bin))) <= tau);
+    double err;
+    const double K = lattice_round(r, bin, inv, tau, &err);
+    const bool bad = !(fabs(K) < 1073741824.0) || !(err <= tau);
     if (bad) flag_serial1(ctl);
     return bad ? 0 : (int32_t)K;
 }

@@ -522,3 +522,27 @@ def test_baseline_archive_matches_reference(cuda, ref, oracle):
     with pytest.raises(umcg.UmcgError) as e:
         umcg.compress_baseline(dev(fields[0]), umcg.Budget(tau=-1.0))
     assert e.value.kind == "budget_inadmissible"
+
+
+def test_lattice_rounding_at_half_integers(cuda, ref):
+    """Values on and 1-4 ulp around the quantizer's rounding boundaries
+    (v / bin = k + 1/2): the GPU lattice index (multiply by fl(1/bin), exact
+    divide inside the ambiguity band) must equal std::round(v / bin) of the
+    reference exactly -- predictor none makes every code the lattice index
+    itself, so the payloads must be byte-identical."""
+    rng = np.random.default_rng(77)
+    for tau in (0.05, 1e-3, 0.37e-7, 3.3):
+        bin_ = 2 * tau
+        k = rng.integers(-2**20, 2**20, 4000).astype(np.float64)
+        base = (k + 0.5) * bin_
+        vals = [base]
+        for s in (1, 2, 3, 4):
+            up, dn = base.copy(), base.copy()
+            for _ in range(s):
+                up = np.nextafter(up, np.inf)
+                dn = np.nextafter(dn, -np.inf)
+            vals += [up, dn]
+        v = np.concatenate(vals)
+        got = umcg.encode(dev(v), predictor=0, tau=tau)
+        want = ref.encode(v, predictor=0, tau=tau)
+        assert got == want, tau
