@@ -144,16 +144,71 @@ __device__ __forceinline__ void thread_walk(const uint8_t* sb, int my, int64_t g
     *wide |= wd;
 }
 
+// 7-bit payloads of 4 varint bytes, concatenated (byte 0 lowest): 28 bits.
+__device__ __forceinline__ uint32_t payload28(uint32_t x) {
+    uint32_t y = x & 0x7f7f7f7fu;
+    y = (y & 0x007f007fu) | ((y & 0x7f007f00u) >> 1);
+    return (y & 0x00003fffu) | ((y & 0x3fff0000u) >> 2);
+}
+// Bit k set when byte k of x ends a varint (MSB clear).
+__device__ __forceinline__ uint32_t ends4(uint32_t x) {
+    return ((((~x) & 0x80808080u) >> 7) * 0x10204080u) >> 28;
+}
+
+// SWAR fast path of thread_walk for the common case: every code that ends
+// in this thread's bytes is <= 4 bytes long (values < 2^28) and no run of 4
+// continuation bytes touches them. Code ends come from a bit mask, values
+// from a 64-bit window of concatenated 7-bit payloads, so the cost is per
+// code rather than per byte. Returns false -- having emitted nothing -- when
+// the general walk must run instead (long codes, end padding, corruption).
+template <class F>
+__device__ __forceinline__ bool thread_walk_fast(const uint8_t* sb, int my, F&& emit) {
+    const uint4* p = reinterpret_cast<const uint4*>(sb + my - 16);
+    const uint32_t h3 = p[0].w;  // the 4 bytes before mine
+    uint32_t w[RB / 4];
+#pragma unroll
+    for (int q = 0; q < RB / 16; ++q) {
+        const uint4 a = p[1 + q];
+        w[4 * q] = a.x;
+        w[4 * q + 1] = a.y;
+        w[4 * q + 2] = a.z;
+        w[4 * q + 3] = a.w;
+    }
+    uint64_t E = ends4(h3);  // bit i: byte i - 4 ends a code
+#pragma unroll
+    for (int q = 0; q < RB / 4; ++q) E |= (uint64_t)ends4(w[q]) << (4 + 4 * q);
+    const uint64_t C = ~E & ((1ull << (4 + RB)) - 1);  // continuation bytes
+    if (C & (C >> 1) & (C >> 2) & (C >> 3)) return false;
+    // partial code entering from the halo: its trailing 0..3 continuation bytes
+    const int hl = (C >> 3 & 1) ? ((C >> 2 & 1) ? ((C >> 1 & 1) ? 3 : 2) : 1) : 0;
+    uint32_t acc = hl ? payload28(h3) >> (7 * (4 - hl)) : 0u;
+    uint32_t shift = 7 * hl;
+    // uniform byte loop without the long-code bookkeeping (ruled out above)
+#pragma unroll
+    for (int k = 0; k < RB; ++k) {
+        const uint32_t byte = __byte_perm(w[k >> 2], 0, k & 3);
+        acc |= (byte & 0x7fu) << shift;
+        shift += 7;
+        if (!(byte & 0x80u)) {
+            emit(acc);
+            acc = 0;
+            shift = 0;
+        }
+    }
+    return true;
+}
+
 __device__ __forceinline__ int64_t zz_dec32(uint32_t v) { return (int64_t)(v >> 1) ^ -(int64_t)(v & 1u); }
 
 __device__ __forceinline__ CS thread_counts(const uint8_t* sb, int my, bool* bad, bool* wide, int64_t base,
                                             uint64_t ulen) {
     uint32_t c = 0;
     int64_t s = 0;
-    thread_walk(sb, my, base + (my - RHALO), ulen, bad, wide, [&](uint32_t v) {
+    auto f = [&](uint32_t v) {
         ++c;
         s += zz_dec32(v);
-    });
+    };
+    if (!thread_walk_fast(sb, my, f)) thread_walk(sb, my, base + (my - RHALO), ulen, bad, wide, f);
     return CS{c, s};
 }
 
@@ -228,7 +283,7 @@ __global__ void __launch_bounds__(RT) k_dec_out(const uint8_t* __restrict__ U, u
     int64_t K = tp.sum + excl.sum;
     uint64_t kmax = 0;
     bool bad2 = false, wide2 = false;
-    thread_walk(sb, my, base + (my - RHALO), ulen, &bad2, &wide2, [&](uint32_t v) {
+    auto f = [&](uint32_t v) {
         K += zz_dec32(v);
         const uint64_t a = (uint64_t)(K < 0 ? -K : K);
         kmax = a > kmax ? a : kmax;
@@ -239,7 +294,8 @@ __global__ void __launch_bounds__(RT) k_dec_out(const uint8_t* __restrict__ U, u
             kb[li] = (int32_t)K;  // |K| < 2^30 on the fast path (checked via kmax)
         }
         ++li;
-    });
+    };
+    if (!thread_walk_fast(sb, my, f)) thread_walk(sb, my, base + (my - RHALO), ulen, &bad2, &wide2, f);
     for (int o = 16; o; o >>= 1) {
         const uint64_t b2 = __shfl_xor_sync(0xffffffffu, kmax, o);
         kmax = b2 > kmax ? b2 : kmax;
