@@ -557,13 +557,13 @@ void decode_component(umcg_plan* p, const CompHeader& h, const uint8_t* d_payloa
         init_ctl(ctl, st);
         void* status = p->scratch_c.reserve(dec_status_bytes(ulen));
         if (pred == 1) {
-            dec_fused(DEC_VALUES, U, ulen, h.n, status, ctl, nullptr, nullptr, 0.0, bin, d_out, nullptr, st);
+            dec_fused(DEC_VALUES, host_src(U, ulen), dec_tiles(ulen), h.n, status, ctl, nullptr, nullptr, 0.0, bin, d_out, nullptr, st);
             const DevCtl hc = check_fused(p, ctl, U, ulen, h.n, st);
             if (!hc.aux[7] && (double)hc.max_abs_k[1] < k_lim(1, 1)) return;
         } else {
             int64_t* P = p->kbuf.as<int64_t>(2 * (h.n ? h.n : 1));
             int32_t* K32 = p->dx1.as<int32_t>(h.n ? h.n : 1);
-            dec_fused(DEC_P64, U, ulen, h.n, status, ctl, nullptr, nullptr, 0.0, bin, nullptr, P, st);
+            dec_fused(DEC_P64, host_src(U, ulen), dec_tiles(ulen), h.n, status, ctl, nullptr, nullptr, 0.0, bin, nullptr, P, st);
             const bool wide = check_fused(p, ctl, U, ulen, h.n, st).aux[7] != 0;
             nd_from_prefix(P, h.n, sh, P + h.n, K32, nullptr, ctl, st);
             const DevCtl hc = read_ctl(p, ctl, st);
@@ -615,9 +615,10 @@ static bool decode_grid(umcg_plan* p, const CompHeader& h, const uint8_t* d_payl
         init_ctl(ctl, st);
         void* status = p->scratch_c.reserve(dec_status_bytes(ulen));
         int64_t* P = p->kbuf.as<int64_t>(2 * (h.n ? h.n : 1));
-        dec_fused(DEC_P64, U, ulen, h.n, status, ctl, nullptr, nullptr, 0.0, bin, nullptr, P, st);
+        dec_fused(DEC_P64, host_src(U, ulen), dec_tiles(ulen), h.n, status, ctl, nullptr, nullptr, 0.0, bin, nullptr, P, st);
         const bool wide = check_fused(p, ctl, U, ulen, h.n, st).aux[7] != 0;
-        nd_from_prefix(P, h.n, make_shape(h.D, h.dims), P + h.n, K1, K16, ctl, st);
+        const uint64_t flat[1] = {h.n};
+        nd_from_prefix(P, h.n, pred == 2 ? make_shape(h.D, h.dims) : make_shape(1, flat), P + h.n, K1, K16, ctl, st);
         const DevCtl hc = read_ctl(p, ctl, st);
         *kmax = hc.max_abs_k[0];
         if (!wide && (double)hc.max_abs_k[0] < k_lim(pred, h.D)) return true;
@@ -627,6 +628,79 @@ static bool decode_grid(umcg_plan* p, const CompHeader& h, const uint8_t* d_payl
 }
 
 namespace {
+
+// Verdict of the speculative decompress: every check the step-by-step path
+// makes on the host (codec.hpp:375-439 on the lattice): one literal token per
+// stream, no malformed varint, exact code counts, no dangling varint, no wide
+// code, lattice regimes. 0 = accept.
+__global__ void k_fast_verdict(const DevCtl* c, DecSrc s1, DecSrc s2, uint64_t n1, uint64_t n2, double lim1,
+                               double lim2, unsigned long long* verdict) {
+    if (threadIdx.x | blockIdx.x) return;
+    unsigned long long v = 0;
+    const DecSrc s[2] = {s1, s2};
+    const uint64_t n[2] = {n1, n2};
+    for (int k = 0; k < 2; ++k) {
+        const DevCtl& d = c[2 * k + 1];
+        const uint8_t* U;
+        uint64_t ulen;
+        resolve_src(s[k], U, ulen);
+        const int sh = 8 * k;
+        if (!ulen) v |= 1ull << sh;
+        else if (U[ulen - 1] & 0x80) v |= 2ull << sh;
+        if (d.err) v |= 4ull << sh;
+        if (d.count != n[k]) v |= 8ull << sh;
+        if (d.aux[7]) v |= 16ull << sh;
+    }
+    if (!((double)c[1].max_abs_k[0] < lim1)) v |= 1ull << 16;
+    if (!((double)c[3].max_abs_k[1] < lim2)) v |= 1ull << 17;
+    *verdict = v;
+}
+
+// Speculative nearest-g decompress (the common case): both token probes, the
+// grid decode + N-D prefix and the fused residual decode + recomposition are
+// queued back to back and checked by one verdict kernel -- one host
+// synchronization instead of one per step. Returns false (output undefined)
+// whenever the step-by-step path must run; that path also reports the
+// reference's error for malformed payloads.
+static bool fast_decompress(umcg_plan* p, const uint8_t* d_ar, uint64_t p1, const CompHeader& h1, uint64_t p2,
+                            const CompHeader& h2, double* d_out, cudaStream_t st) {
+    const int pred1 = (h1.pred == 2 && h1.D == 1) ? 1 : h1.pred;
+    const int pred2 = (h2.pred == 2 && h2.D == 1) ? 1 : h2.pred;
+    const double bin1 = 2.0 * h1.tau, bin2 = 2.0 * h2.tau;
+    auto lattice = [](const CompHeader& h, double bin) {
+        return h.codec == 0 && h.backend == 0 && h.D <= 8 && h.tau != 0.0 && !h.n_esc && std::isfinite(bin) &&
+               h.n > 0;
+    };
+    if (!lattice(h1, bin1) || !lattice(h2, bin2) || pred1 == 0 || pred2 != 1 || h2.D != 1) return false;
+    const uint64_t n1 = h1.n, n = h2.n;
+    auto* c = p->ctl.as<DevCtl>(5);  // token ctl / decode ctl per component + verdict
+    UMCG_CUDA(cudaMemsetAsync(c, 0, 5 * sizeof(DevCtl), st));
+    const uint8_t* s1b = d_ar + p1 + h1.stream_off;
+    const uint8_t* s2b = d_ar + p2 + h2.stream_off;
+    const Token* t1 = stream_probe(s1b, h1.stream_len, p->dec, &c[0], st);
+    const Token* t2 = stream_probe(s2b, h2.stream_len, p->dec2, &c[2], st);
+    const DecSrc src1{nullptr, 0, s1b, t1, &c[0]};
+    const DecSrc src2{nullptr, 0, s2b, t2, &c[2]};
+    void* st1 = p->scratch_c.reserve(dec_status_bytes(h1.stream_len));
+    void* st2 = p->scratch_d.reserve(dec_status_bytes(h2.stream_len));
+    int64_t* P = p->kbuf.as<int64_t>(2 * n1);
+    int32_t* K1 = p->codes1.as<int32_t>(n1);
+    dec_fused(DEC_P64, src1, dec_tiles(h1.stream_len), n1, st1, &c[1], nullptr, nullptr, 0.0, bin1, nullptr, P, st);
+    const uint64_t flat[1] = {n1};
+    int16_t* K16 = p->dx1.as<int16_t>(n1 + 2);
+    nd_from_prefix(P, n1, pred1 == 2 ? make_shape(h1.D, h1.dims) : make_shape(1, flat), P + n1, K1, K16, &c[1],
+                   st);
+    dec_fused(DEC_RECOMPOSE, src2, dec_tiles(h2.stream_len), n, st2, &c[3], p->d_node.as<uint32_t>(1), K1, bin1,
+              bin2, d_out, nullptr, st, &c[1], K16);
+    auto* verdict = reinterpret_cast<unsigned long long*>(&c[4].aux[0]);
+    k_fast_verdict<<<1, 1, 0, st>>>(c, src1, src2, n1, n, k_lim(pred1, pred1 == 2 ? h1.D : 1), k_lim(1, 1),
+                                    verdict);
+    UMCG_LAUNCHED();
+    auto* hv = static_cast<unsigned long long*>(p->hctl.reserve(sizeof(DevCtl)));
+    UMCG_CUDA(cudaMemcpyAsync(hv, verdict, 8, cudaMemcpyDeviceToHost, st));
+    UMCG_CUDA(cudaStreamSynchronize(st));
+    return *hv == 0;
+}
 
 void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_out, cudaStream_t st) {
     if (!p || (!d_ar && len)) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
@@ -700,6 +774,8 @@ void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_
     if (h2.n != p->n) fail(UMCG_MAPPING_MISMATCH, "vertex count does not match archive component");
     prep(h1, hb + p1, head - p1, l1);
     prep(h2, tail + 8, tl - 8, l2);
+    const int g_kind0 = (flags & 2u) ? 1 : 0;
+    if (g_kind0 == 0 && fast_decompress(p, d_ar, p1, h1, p2, h2, d_out, st)) return;
     double* x1 = p->x1.as<double>(p->n_slots ? p->n_slots : 1);
     int32_t* K1 = p->codes1.as<int32_t>(p->n_slots ? p->n_slots : 1);
     const int g_kind = (flags & 2u) ? 1 : 0;
@@ -726,7 +802,7 @@ void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_
         const bool k16 = k1max < 32768;
         const int32_t* ktab = K1;
         if (k16) ktab = reinterpret_cast<const int32_t*>(K16);  // written by decode_grid
-        dec_fused(k16 ? DEC_RECOMPOSE16 : DEC_RECOMPOSE, U, ulen, p->n, status, ctl, p->d_node.as<uint32_t>(1),
+        dec_fused(k16 ? DEC_RECOMPOSE16 : DEC_RECOMPOSE, host_src(U, ulen), dec_tiles(ulen), p->n, status, ctl, p->d_node.as<uint32_t>(1),
                   ktab, bin1, bin2, d_out, nullptr, st);
         const DevCtl hc = check_fused(p, ctl, U, ulen, p->n, st);
         if (!hc.aux[7] && (double)hc.max_abs_k[1] < k_lim(1, 1)) return;

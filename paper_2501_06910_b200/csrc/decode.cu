@@ -212,8 +212,11 @@ __device__ __forceinline__ CS thread_counts(const uint8_t* sb, int my, bool* bad
     return CS{c, s};
 }
 
-__global__ void __launch_bounds__(RT) k_dec_agg(const uint8_t* __restrict__ U, uint64_t ulen,
-                                               CS* __restrict__ aggs, DevCtl* ctl) {
+__global__ void __launch_bounds__(RT) k_dec_agg(const DecSrc src, CS* __restrict__ aggs, DevCtl* ctl) {
+    const uint8_t* U;
+    uint64_t ulen;
+    resolve_src(src, U, ulen);
+    if ((uint64_t)blockIdx.x * RTILE >= ulen) return;
     using BR = cub::BlockReduce<CS, RT>;
     __shared__ typename BR::TempStorage tmp;
     __shared__ __align__(16) uint8_t sb[RHALO + RTILE + 16];
@@ -231,9 +234,13 @@ __global__ void __launch_bounds__(RT) k_dec_agg(const uint8_t* __restrict__ U, u
 // Exclusive scan of tile aggregates in one CTA; total count -> ctl->count.
 // Each thread owns a contiguous run of tiles, read 8 at a time so the loads
 // overlap (the scan is latency-bound).
-__global__ void __launch_bounds__(1024) k_scan_cs(CS* __restrict__ aggs, uint64_t T, DevCtl* ctl) {
+__global__ void __launch_bounds__(1024) k_scan_cs(const DecSrc src, CS* __restrict__ aggs, DevCtl* ctl) {
     using BS = cub::BlockScan<CS, 1024>;
     __shared__ typename BS::TempStorage tmp;
+    const uint8_t* U;
+    uint64_t ulen;
+    resolve_src(src, U, ulen);
+    const uint64_t T = (ulen + RTILE - 1) / RTILE;
     const uint64_t per = (T + 1023) / 1024;
     const uint64_t t0 = min(T, threadIdx.x * per), t1 = min(T, t0 + per);
     CS local{0, 0};
@@ -260,15 +267,23 @@ __global__ void __launch_bounds__(1024) k_scan_cs(CS* __restrict__ aggs, uint64_
 }
 
 template <int MODE, class KT>
-__global__ void __launch_bounds__(RT) k_dec_out(const uint8_t* __restrict__ U, uint64_t ulen, uint64_t n,
+__global__ void __launch_bounds__(RT) k_dec_out(const DecSrc src, uint64_t n,
                                                const CS* __restrict__ pre, DevCtl* ctl,
                                                const uint32_t* __restrict__ node, const KT* __restrict__ K1,
                                                double bin1, double bin, double* __restrict__ out,
-                                               int64_t* __restrict__ P64) {
+                                               int64_t* __restrict__ P64, const DevCtl* __restrict__ kctl,
+                                               const int16_t* __restrict__ K16) {
     using BS = cub::BlockScan<CS, RT>;
     __shared__ typename BS::TempStorage tmp;
     __shared__ __align__(16) uint8_t sb[RHALO + RTILE + 16];
     __shared__ int32_t kb[MODE == DEC_P64 ? 1 : RTILE];
+    // int32 tables: switch to the int16 copy when the grid's max|K1| (known
+    // on the device only) allows -- half the L2 footprint of the gather
+    const bool use16 = sizeof(KT) == 4 && K16 && kctl && kctl->max_abs_k[0] < 32768;
+    const uint8_t* U;
+    uint64_t ulen;
+    resolve_src(src, U, ulen);
+    if ((uint64_t)blockIdx.x * RTILE >= ulen) return;
     const int64_t base = (int64_t)blockIdx.x * (int64_t)RTILE;
     stage_tile(U, ulen, base, sb);
     __syncthreads();
@@ -318,8 +333,9 @@ __global__ void __launch_bounds__(RT) k_dec_out(const uint8_t* __restrict__ U, u
         for (int u = 0; u < UN; ++u) {
             const uint32_t e = e0 + u * RT + threadIdx.x;
             if (MODE == DEC_RECOMPOSE && e < cnt && tp.cnt + e < n)
-                g1[u] = sizeof(KT) == 4 ? ld_s32_hint(reinterpret_cast<const int32_t*>(K1) + nd[u], pl)
-                                        : (int32_t)__ldg(K1 + nd[u]);
+                g1[u] = sizeof(KT) == 2 || use16
+                            ? (int32_t)__ldg((sizeof(KT) == 2 ? reinterpret_cast<const int16_t*>(K1) : K16) + nd[u])
+                            : ld_s32_hint(reinterpret_cast<const int32_t*>(K1) + nd[u], pl);
             else
                 g1[u] = 0;
         }
@@ -474,31 +490,34 @@ __global__ void k_k32_to_f64(const int32_t* __restrict__ K, uint64_t n, double b
 }  // namespace
 
 size_t dec_status_bytes(uint64_t ulen) { return (cdiv(ulen, RTILE) + 1) * sizeof(CS); }
+uint64_t dec_tiles(uint64_t ulen_bound) { return cdiv(ulen_bound, RTILE); }
 
-void dec_fused(int mode, const uint8_t* U, uint64_t ulen, uint64_t n, void* status, DevCtl* ctl,
+void dec_fused(int mode, const DecSrc& src, uint64_t T, uint64_t n, void* status, DevCtl* ctl,
                const uint32_t* node, const int32_t* K1, double bin1, double bin, double* out, int64_t* P64,
-               cudaStream_t st) {
-    const uint64_t T = cdiv(ulen, RTILE);
-    if (!T) return;
+               cudaStream_t st, const DevCtl* kctl, const int16_t* K16) {
     auto* aggs = static_cast<CS*>(status);
-    {
+    if (T) {
         ProfScope ps_a("k_dec_agg", st);
-        k_dec_agg<<<(unsigned)T, RT, 0, st>>>(U, ulen, aggs, ctl);
+        k_dec_agg<<<(unsigned)T, RT, 0, st>>>(src, aggs, ctl);
         UMCG_LAUNCHED();
     }
-    k_scan_cs<<<1, 1024, 0, st>>>(aggs, T, ctl);
+    k_scan_cs<<<1, 1024, 0, st>>>(src, aggs, ctl);
     UMCG_LAUNCHED();
+    if (!T) return;
     ProfScope ps_o(mode == DEC_P64 ? "k_dec_out_grid" : "k_dec_out", st);
     if (mode == DEC_P64)
-        k_dec_out<DEC_P64, int32_t><<<(unsigned)T, RT, 0, st>>>(U, ulen, n, aggs, ctl, node, K1, bin1, bin, out, P64);
+        k_dec_out<DEC_P64, int32_t><<<(unsigned)T, RT, 0, st>>>(src, n, aggs, ctl, node, K1, bin1, bin, out, P64,
+                                                               nullptr, nullptr);
     else if (mode == DEC_VALUES)
-        k_dec_out<DEC_VALUES, int32_t><<<(unsigned)T, RT, 0, st>>>(U, ulen, n, aggs, ctl, node, K1, bin1, bin, out, P64);
+        k_dec_out<DEC_VALUES, int32_t><<<(unsigned)T, RT, 0, st>>>(src, n, aggs, ctl, node, K1, bin1, bin, out, P64,
+                                                                  nullptr, nullptr);
     else if (mode == DEC_RECOMPOSE16)
-        k_dec_out<DEC_RECOMPOSE, int16_t><<<(unsigned)T, RT, 0, st>>>(U, ulen, n, aggs, ctl, node,
+        k_dec_out<DEC_RECOMPOSE, int16_t><<<(unsigned)T, RT, 0, st>>>(src, n, aggs, ctl, node,
                                                                      reinterpret_cast<const int16_t*>(K1), bin1, bin,
-                                                                     out, P64);
+                                                                     out, P64, nullptr, nullptr);
     else
-        k_dec_out<DEC_RECOMPOSE, int32_t><<<(unsigned)T, RT, 0, st>>>(U, ulen, n, aggs, ctl, node, K1, bin1, bin, out, P64);
+        k_dec_out<DEC_RECOMPOSE, int32_t><<<(unsigned)T, RT, 0, st>>>(src, n, aggs, ctl, node, K1, bin1, bin, out, P64,
+                                                                     kctl, K16);
     UMCG_LAUNCHED();
 }
 

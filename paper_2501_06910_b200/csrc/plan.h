@@ -49,7 +49,7 @@ struct umcg_plan {
     std::mutex mu;
     umcg::DevBuf ctl, x1, codes1, codes2, kbuf, enc1, enc2, hdr, scratch_a, scratch_b, scratch_c,
         scratch_d, dx1, dcodes;
-    umcg::StreamDecScratch dec;
+    umcg::StreamDecScratch dec, dec2;
     umcg::PinnedBuf hctl, hstage;
 };
 

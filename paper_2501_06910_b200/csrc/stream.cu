@@ -15,12 +15,6 @@ namespace umcg {
 // ===========================================================================
 namespace {
 
-struct Token {
-    uint64_t src;   // literal data offset in the stream (unused for zero runs)
-    uint64_t uoff;  // offset in the unpacked byte stream
-    uint64_t len;   // unpacked bytes; bit 63 set for literal tokens
-};
-
 // Serial walk over token headers (rle_decompress, lossless.hpp:53-70).
 // Stops after max_tok tokens; aux[1] = 1 when the stream is not finished
 // (the caller then switches to the parallel parse below).
@@ -574,6 +568,15 @@ static bool parallel_tokens(const uint8_t* d_stream, uint64_t len, Token* tok, S
     *ntok = h.t[0];
     *ulen = h.t[1];
     return !h.bad;
+}
+
+const Token* stream_probe(const uint8_t* d_stream, uint64_t len, StreamDecScratch& sc, DevCtl* tctl,
+                          cudaStream_t st) {
+    const uint64_t tok_cap = len / 2 + 1;
+    Token* tok = sc.tokens.as<Token>(tok_cap);
+    k_token_walk<<<1, 32, 0, st>>>(d_stream, len, tok, tok_cap, 64, tctl);
+    UMCG_LAUNCHED();
+    return tok;
 }
 
 const uint8_t* stream_unpack(const uint8_t* d_stream, uint64_t len, StreamDecScratch& sc, DevCtl* ctl,
