@@ -629,6 +629,40 @@ static bool decode_grid(umcg_plan* p, const CompHeader& h, const uint8_t* d_payl
 
 namespace {
 
+constexpr uint64_t kHeadShort = 512;              // container + component-1 header, short names
+constexpr uint64_t kTailBytes = 8 + 29 + 64 + 8;   // component-2 length + header
+
+// Container header + component 1 header -> out[0, kHeadShort); component 2's
+// length + header -> out[kHeadShort, +kTailBytes) with its byte count at
+// out[kHeadShort + kTailBytes] (0 when it could not be located).
+__global__ void k_gather_headers(const uint8_t* __restrict__ a, uint64_t len, uint8_t* __restrict__ out) {
+    const uint64_t head = len < kHeadShort ? len : kHeadShort;
+    for (uint64_t i = threadIdx.x; i < kHeadShort; i += blockDim.x) out[i] = i < head ? a[i] : 0;
+    __shared__ uint64_t o2s;
+    if (threadIdx.x == 0) {
+        o2s = 0;
+        if (len >= 10) {
+            const uint64_t nl = (uint64_t)a[8] | ((uint64_t)a[9] << 8);
+            const uint64_t lp = 10 + nl + 24;
+            if (lp + 8 <= len) {
+                uint64_t l1 = 0;
+                for (int k = 0; k < 8; ++k) l1 |= (uint64_t)a[lp + k] << (8 * k);
+                const uint64_t o2 = lp + 8 + l1;
+                if (l1 <= len && o2 <= len && o2 >= lp + 8) o2s = o2;
+            }
+        }
+    }
+    __syncthreads();
+    const uint64_t o2 = o2s;
+    const uint64_t tl = o2 && len > o2 ? (len - o2 < kTailBytes ? len - o2 : kTailBytes) : 0;
+    for (uint64_t i = threadIdx.x; i < kTailBytes; i += blockDim.x) out[kHeadShort + i] = i < tl ? a[o2 + i] : 0;
+    if (threadIdx.x == 0)
+        for (int k = 0; k < 8; ++k) {
+            out[kHeadShort + kTailBytes + k] = (uint8_t)(tl >> (8 * k));
+            out[kHeadShort + kTailBytes + 8 + k] = (uint8_t)(o2 >> (8 * k));
+        }
+}
+
 // Verdict of the speculative decompress: every check the step-by-step path
 // makes on the host (codec.hpp:375-439 on the lattice): one literal token per
 // stream, no malformed varint, exact code counts, no dangling varint, no wide
@@ -706,11 +740,35 @@ void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_
     if (!p || (!d_ar && len)) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
     std::lock_guard<std::mutex> lock(p->mu);
     UMCG_CUDA(cudaSetDevice(p->device));
-    // deserialize_archive (pipeline.hpp:237-267): all truncation -> malformed_file
-    const uint64_t head = std::min<uint64_t>(len, 10 + 65535 + 24 + 8 + 29 + 64);
-    auto* hb = static_cast<uint8_t*>(p->hstage.reserve(std::max<uint64_t>(head, 128) + 128));
-    if (head) UMCG_CUDA(cudaMemcpyAsync(hb, d_ar, head, cudaMemcpyDeviceToHost, st));
-    UMCG_CUDA(cudaStreamSynchronize(st));
+    // deserialize_archive (pipeline.hpp:237-267): all truncation -> malformed_file.
+    // One device gather brings the container header, component 1's header and
+    // component 2's header to the host in one copy (names up to kShortName
+    // bytes); longer names take two dependent copies.
+    uint64_t head = std::min<uint64_t>(len, kHeadShort);
+    auto* hb = static_cast<uint8_t*>(p->hstage.reserve(10 + 65535 + 24 + 8 + 29 + 64 + 512));
+    uint8_t tail[kTailBytes];
+    uint64_t tl_gathered = 0, o2_gathered = 0;
+    {
+        auto* dbuf = p->hdr.as<uint8_t>(kHeadShort + kTailBytes + 16);
+        k_gather_headers<<<1, 128, 0, st>>>(d_ar, len, dbuf);
+        UMCG_LAUNCHED();
+        UMCG_CUDA(cudaMemcpyAsync(hb, dbuf, kHeadShort + kTailBytes + 16, cudaMemcpyDeviceToHost, st));
+        UMCG_CUDA(cudaStreamSynchronize(st));
+        uint64_t tlen = 0;
+        std::memcpy(&tlen, hb + kHeadShort + kTailBytes, 8);
+        std::memcpy(&o2_gathered, hb + kHeadShort + kTailBytes + 8, 8);
+        if (tlen) {
+            std::memcpy(tail, hb + kHeadShort, kTailBytes);
+            tl_gathered = tlen;
+        }
+        const uint64_t nl = len >= 10 ? (uint64_t)hb[8] | ((uint64_t)hb[9] << 8) : 0;
+        if (len >= 10 && 10 + nl + 24 + 8 + 29 + 64 > kHeadShort && len > kHeadShort) {
+            head = std::min<uint64_t>(len, 10 + 65535 + 24 + 8 + 29 + 64);
+            UMCG_CUDA(cudaMemcpyAsync(hb, d_ar, head, cudaMemcpyDeviceToHost, st));
+            UMCG_CUDA(cudaStreamSynchronize(st));
+            tl_gathered = 0;
+        }
+    }
     if (len < 4) fail(UMCG_MALFORMED_FILE, "file too short for archive header");
     if (std::memcmp(hb, "UMCZ", 4) != 0) fail(UMCG_MALFORMED_FILE, "bad magic for archive");
     HostReader r{hb, head};
@@ -735,10 +793,11 @@ void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_
     // component 2 header
     const uint64_t o2 = p1 + l1;
     if (len - o2 < 8) fail(UMCG_MALFORMED_FILE, "truncated archive: unexpected end of data");
-    uint8_t tail[8 + 29 + 64 + 8];
-    const uint64_t tl = std::min<uint64_t>(sizeof tail, len - o2);
-    UMCG_CUDA(cudaMemcpyAsync(tail, d_ar + o2, tl, cudaMemcpyDeviceToHost, st));
-    UMCG_CUDA(cudaStreamSynchronize(st));
+    const uint64_t tl = std::min<uint64_t>(kTailBytes, len - o2);
+    if (tl_gathered != tl || o2_gathered != o2) {
+        UMCG_CUDA(cudaMemcpyAsync(tail, d_ar + o2, tl, cudaMemcpyDeviceToHost, st));
+        UMCG_CUDA(cudaStreamSynchronize(st));
+    }
     HostReader r2{tail, tl};
     const uint64_t l2 = r2.le(8);
     const uint64_t p2 = o2 + 8;
