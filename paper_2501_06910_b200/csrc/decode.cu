@@ -232,38 +232,38 @@ __global__ void __launch_bounds__(RT) k_dec_agg(const DecSrc src, CS* __restrict
 }
 
 // Exclusive scan of tile aggregates in one CTA; total count -> ctl->count.
-// Each thread owns a contiguous run of tiles, read 8 at a time so the loads
-// overlap (the scan is latency-bound).
+// Segments of 1024 x 4 consecutive aggregates: coalesced loads, one block
+// scan per segment, running carry (the scan is latency-bound: few segments).
 __global__ void __launch_bounds__(1024) k_scan_cs(const DecSrc src, CS* __restrict__ aggs, DevCtl* ctl) {
+    constexpr int IT = 4;
     using BS = cub::BlockScan<CS, 1024>;
     __shared__ typename BS::TempStorage tmp;
     const uint8_t* U;
     uint64_t ulen;
     resolve_src(src, U, ulen);
     const uint64_t T = (ulen + RTILE - 1) / RTILE;
-    const uint64_t per = (T + 1023) / 1024;
-    const uint64_t t0 = min(T, threadIdx.x * per), t1 = min(T, t0 + per);
-    CS local{0, 0};
-    for (uint64_t t = t0; t < t1; t += 8) {
-        CS v[8];
+    CS carry{0, 0};
+    for (uint64_t s0 = 0; s0 < T; s0 += 1024 * IT) {
+        const uint64_t t0 = s0 + (uint64_t)threadIdx.x * IT;
+        CS v[IT];
+        CS local{0, 0};
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = t + k < t1 ? aggs[t + k] : CS{0, 0};
+        for (int k = 0; k < IT; ++k) {
+            v[k] = t0 + k < T ? aggs[t0 + k] : CS{0, 0};
+            local = CSAdd()(local, v[k]);
+        }
+        CS excl, tot;
+        BS(tmp).ExclusiveScan(local, excl, CS{0, 0}, CSAdd(), tot);
+        excl = CSAdd()(excl, carry);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) local = CSAdd()(local, v[k]);
-    }
-    CS excl, tot;
-    BS(tmp).ExclusiveScan(local, excl, CS{0, 0}, CSAdd(), tot);
-    for (uint64_t t = t0; t < t1; t += 8) {
-        CS v[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = t + k < t1 ? aggs[t + k] : CS{0, 0};
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            if (t + k < t1) aggs[t + k] = excl;
+        for (int k = 0; k < IT; ++k) {
+            if (t0 + k < T) aggs[t0 + k] = excl;
             excl = CSAdd()(excl, v[k]);
         }
+        carry = CSAdd()(carry, tot);
+        __syncthreads();
     }
-    if (threadIdx.x == 0) ctl->count = tot.cnt;
+    if (threadIdx.x == 0) ctl->count = carry.cnt;
 }
 
 template <int MODE, class KT>
