@@ -198,10 +198,12 @@ umcg_status umcg_rle_decompress(const uint8_t* d_in, uint64_t n, uint8_t* d_out,
                                 uint64_t capacity, uint64_t* out_len, void* stream);
 
 /* Synthetic BASELINE inputs generated on the device (SplitMix64-seeded,
- * counter-based). config: 1 (2D 1024^2 jittered
- * lattice), 3 (3D jittered lattice), 4 (2D lattice, 5 fp32 variables).
- * lattice = points per axis. d_coords [n*dim] fp64; d_values [n_fields*n]
- * (fp64, or fp32 for config 4). Returns n via *n_out when pointers are NULL. */
+ * counter-based). config: 1 (2D jittered lattice),
+ * 2 (2D graded annulus), 3 (3D jittered lattice), 4 (2D lattice, 5 fp32
+ * variables), 5 (3D clustered cylinder shell). lattice = points per axis for
+ * configs 1, 3, 4 and the vertex count for configs 2, 5. d_coords [n*dim]
+ * fp64; d_values [n_fields*n] (fp64, or fp32 for config 4). Returns n via
+ * *n_out when pointers are NULL. */
 umcg_status umcg_gen_config(int config, uint64_t lattice, uint64_t seed, double* d_coords,
                             void* d_values, uint64_t* n_out, void* stream);
 

@@ -280,6 +280,27 @@ class Plan:
         n = self.compress_into(d_values, budget, buf, name)
         return bytes(buf[:n].cpu().numpy())
 
+    def compress_batch(self, d_values, budget: Budget = Budget(), names=None) -> list:
+        """umcg_compress_batch: V fields [V, n] (fp64 or fp32, BASELINE config
+        4) against this plan, one archive per field."""
+        import torch
+        V = int(d_values.shape[0])
+        dtype = 1 if d_values.dtype == torch.float32 else 0
+        names = names or [f"f{k}" for k in range(V)]
+        cap = sum(self.compress_bound(nm) for nm in names)
+        buf = torch.empty(cap, dtype=torch.uint8, device=d_values.device)
+        lens = np.zeros(V, np.uint64)
+        cn = (C.c_char_p * V)(*[nm.encode() for nm in names])
+        prm = budget.c()
+        _check(lib().umcg_compress_batch(self.h, C.byref(prm), C.c_void_p(d_values.data_ptr()), dtype, V, cn,
+                                         C.c_void_p(buf.data_ptr()), cap, _ptr(lens, u64p), _stream_ptr()))
+        host = bytes(buf[: int(lens.sum())].cpu().numpy())
+        out, o = [], 0
+        for ln in lens:
+            out.append(host[o: o + int(ln)])
+            o += int(ln)
+        return out
+
     def decompress(self, archive: bytes, device="cuda"):
         import torch
         a = torch.from_numpy(np.frombuffer(archive, np.uint8).copy()).to(device)
@@ -385,7 +406,7 @@ def gen_config(config: int, lattice: int, seed: int, coords: bool = True, values
     n = C.c_uint64()
     _check(lib().umcg_gen_config(config, lattice, seed, None, None, C.byref(n), None))
     n = n.value
-    dim = 3 if config == 3 else 2
+    dim = 3 if config in (3, 5) else 2
     xyz = torch.empty((n, dim), dtype=torch.float64, device=device) if coords else None
     if config == 4:
         vals = torch.empty((5, n), dtype=torch.float32, device=device) if values else None

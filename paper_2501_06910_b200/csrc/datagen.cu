@@ -147,6 +147,64 @@ __global__ void k_gen4(uint64_t m, uint64_t seed, Feistel perm, double* __restri
     f[4 * n + v] = (float)uni;
 }
 
+__device__ __forceinline__ double gauss(uint64_t seed, uint64_t stream, uint64_t i) {
+    const double u1 = u01(hash3(seed, stream, i)), u2 = u01(hash3(seed, stream + 1, i));
+    return sqrt(-2.0 * log(u1 > 0 ? u1 : 1e-300)) * cos(2.0 * M_PI * u2);
+}
+
+__device__ __forceinline__ double fourier3(const double* p) {
+    double s = 0.0;
+    for (int q = 0; q < 64; ++q) {
+        const double arg = 2.0 * M_PI * (c_modes.k[q][0] * p[0] + c_modes.k[q][1] * p[1] + c_modes.k[q][2] * p[2]) +
+                           c_modes.phase[q];
+        s += c_modes.amp[q] * cos(arg);
+    }
+    return s;
+}
+
+// Config 2: graded 2D annulus around (0.5, 0.5), r in [0.3, 0.45]: 90 % of
+// the vertices from the radial density exp(-((r - 0.4) / 0.02)^2) (a normal
+// with sigma 0.02/sqrt(2), truncated to the annulus), 10 % uniform over the
+// annulus area; theta ~ U[0, 2pi). Field tanh((r - 0.4) / 0.005) +
+// 0.05 cos(12 theta) + N(0, 1e-4). Vertices are i.i.d., so their order is
+// already random.
+__global__ void k_gen2(uint64_t n, uint64_t seed, double* __restrict__ xy, double* __restrict__ f) {
+    const uint64_t v = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (v >= n) return;
+    double r;
+    if (u01(hash3(seed, 1, v)) < 0.1) {
+        const double a = u01(hash3(seed, 2, v));
+        r = sqrt(0.09 + a * (0.2025 - 0.09));
+    } else {
+        r = 0.4;
+        for (uint64_t t = 0; t < 64; ++t) {
+            r = 0.4 + gauss(seed, 3 + 2 * t, v) * (0.02 / M_SQRT2);
+            if (r >= 0.3 && r <= 0.45) break;
+            r = 0.4;
+        }
+    }
+    const double th = 2.0 * M_PI * u01(hash3(seed, 200, v));
+    const double x = 0.5 + r * cos(th), y = 0.5 + r * sin(th);
+    if (xy) { xy[2 * v] = x; xy[2 * v + 1] = y; }
+    if (f) f[v] = tanh((r - 0.4) / 0.005) + 0.05 * cos(12.0 * th) + 1e-4 * gauss(seed, 201, v);
+}
+
+// Config 5: clustered 3D shell around the axis (0.5, 0.5, z): r = 0.2 +
+// N(0, 0.01), theta ~ U[0, 2pi), z ~ U[0, 1]; field = the config-3 Fourier
+// field x exp(-((r - 0.2) / 0.01)^2 / 2).
+__global__ void k_gen5(uint64_t n, uint64_t seed, double* __restrict__ xyz, double* __restrict__ f) {
+    const uint64_t v = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (v >= n) return;
+    const double r = 0.2 + 0.01 * gauss(seed, 1, v);
+    const double th = 2.0 * M_PI * u01(hash3(seed, 3, v));
+    const double p[3] = {0.5 + r * cos(th), 0.5 + r * sin(th), u01(hash3(seed, 4, v))};
+    if (xyz) { xyz[3 * v] = p[0]; xyz[3 * v + 1] = p[1]; xyz[3 * v + 2] = p[2]; }
+    if (f) {
+        const double d = (r - 0.2) / 0.01;
+        f[v] = fourier3(p) * exp(-0.5 * d * d);
+    }
+}
+
 void upload_modes(uint64_t seed) {
     Modes3 md;
     uint64_t s = seed ^ 0xa0761d6478bd642full;
@@ -176,13 +234,16 @@ void gen_config(int config, uint64_t m, uint64_t seed, double* d_coords, void* d
     uint64_t n;
     if (config == 3) n = m * m * m;
     else if (config == 1 || config == 4) n = m * m;
-    else fail(UMCG_INVALID_ARGUMENT, "config must be 1, 3 or 4");
+    else if (config == 2 || config == 5) n = m;  // vertex count
+    else fail(UMCG_INVALID_ARGUMENT, "config must be 1..5");
     if (n_out) *n_out = n;
     if (!d_coords && !d_values) return;
     upload_modes(seed);
     const Feistel perm = make_feistel(n, seed);
     const unsigned g = (unsigned)cdiv(n, THREADS);
-    if (config == 3) k_gen3<<<g, THREADS, 0, st>>>(m, seed, perm, d_coords, static_cast<double*>(d_values));
+    if (config == 2) k_gen2<<<g, THREADS, 0, st>>>(n, seed, d_coords, static_cast<double*>(d_values));
+    else if (config == 5) k_gen5<<<g, THREADS, 0, st>>>(n, seed, d_coords, static_cast<double*>(d_values));
+    else if (config == 3) k_gen3<<<g, THREADS, 0, st>>>(m, seed, perm, d_coords, static_cast<double*>(d_values));
     else if (config == 1) k_gen1<<<g, THREADS, 0, st>>>(m, seed, perm, d_coords, static_cast<double*>(d_values));
     else k_gen4<<<g, THREADS, 0, st>>>(m, seed, perm, d_coords, static_cast<float*>(d_values));
     UMCG_LAUNCHED();

@@ -546,3 +546,102 @@ def test_lattice_rounding_at_half_integers(cuda, ref):
         got = umcg.encode(dev(v), predictor=0, tau=tau)
         want = ref.encode(v, predictor=0, tau=tau)
         assert got == want, tau
+
+
+def _bbox_plan(xyz, g):
+    """Uniform axes over the vertex bbox (SURVEY 8(d) grid recipe), GPU
+    grid_coarsen, and the equivalent oracle Setup."""
+    lo = xyz.min(0).values.cpu().numpy()
+    hi = xyz.max(0).values.cpu().numpy()
+    axes = [np.linspace(lo[d], hi[d], g) for d in range(xyz.shape[1])]
+    plan = umcg.Plan.build(axes, xyz)
+    mode, gaxes, assign, visited = plan.export()
+    s = Setup(dim=xyz.shape[1], axes=gaxes, mode=mode, assignments=assign, visited=visited)
+    return plan, s
+
+
+def _parity_case(plan, s, x_dev, xh, p, ref, oracle, label):
+    b = budget_of(p)
+    got = plan.compress(x_dev, b, name="c")
+    want = ref.compress(s, xh, name="c", tau=p["tau"], rho=p.get("rho", 0.5))
+    check_archive(got, want, s, xh, p, oracle, label)
+    tau_abs = p["tau"] * np.ptp(xh)
+    check_decode(plan.decompress(got).cpu().numpy(), ref.decompress(s, got), xh, tau_abs, label + " own")
+    check_decode(plan.decompress(want).cpu().numpy(), ref.decompress(s, want), xh, tau_abs, label + " ref")
+
+
+@pytest.mark.parametrize("g", [256, 1024])
+def test_config2_graded_annulus_matches_reference(cuda, ref, oracle, g):
+    """BASELINE config 2 (graded annulus, large clusters) at 2^20 vertices:
+    archives against the reference at tau 1e-2 / 1e-4 / 1e-6."""
+    xy, x = umcg.gen_config(2, 1 << 20, 20250102, device="cuda")
+    plan, s = _bbox_plan(xy, g)
+    xh = x.cpu().numpy()
+    for tau in (1e-2, 1e-4, 1e-6):
+        _parity_case(plan, s, x, xh, dict(tau=tau), ref, oracle, f"config2 g={g} tau={tau} mode={s.mode}")
+
+
+@pytest.mark.parametrize("g", [64, 128])
+def test_config5_shell_matches_reference(cuda, ref, oracle, g):
+    """BASELINE config 5 (clustered cylinder shell; seed mode when the
+    visited fraction drops under 0.35) at 2^21 vertices: the error split and
+    tau sweep of the config (rho 0.1 / 0.9, tau 1e-2 / 1e-5)."""
+    xyz, x = umcg.gen_config(5, 1 << 21, 20250105, device="cuda")
+    plan, s = _bbox_plan(xyz, g)
+    xh = x.cpu().numpy()
+    for tau, rho in ((1e-2, 0.1), (1e-5, 0.9), (1e-3, 0.5)):
+        _parity_case(plan, s, x, xh, dict(tau=tau, rho=rho), ref, oracle,
+                     f"config5 g={g} tau={tau} rho={rho} mode={s.mode}")
+
+
+def test_config5_modes_cover_dense_and_seed(cuda):
+    """The shell switches the grid builder to seed mode as the grid refines
+    (128^3 dense, 256^3 seed at 200M vertices)."""
+    xyz, _ = umcg.gen_config(5, 1 << 21, 20250105, device="cuda", values=False)
+    modes = {g: _bbox_plan(xyz, g)[0].info.mode for g in (32, 160)}
+    assert modes[32] == 0 and modes[160] == 1, modes
+
+
+@pytest.mark.parametrize("tau", [1e-3, 1e-5])
+def test_config4_fp32_batch_matches_reference(cuda, ref, oracle, tau):
+    """BASELINE config 4: five fp32 variables in one umcg_compress_batch call
+    against five reference compress calls on the widened values
+    (SURVEY 8(a) row 16)."""
+    m = 1024
+    xy, vals = umcg.gen_config(4, m, 20250104, device="cuda")
+    plan, s = _bbox_plan(xy, 512)
+    archives = plan.compress_batch(vals, umcg.Budget(tau=tau), names=[f"v{k}" for k in range(5)])
+    assert len(archives) == 5
+    for k in range(5):
+        xh = vals[k].double().cpu().numpy()
+        want = ref.compress(s, xh, name=f"v{k}", tau=tau)
+        check_archive(archives[k], want, s, xh, dict(tau=tau), oracle, f"config4 var{k} tau={tau}")
+        out = plan.decompress(archives[k]).cpu().numpy()
+        check_decode(out, ref.decompress(s, archives[k]), xh, tau * np.ptp(xh), f"config4 var{k}")
+
+
+@pytest.mark.parametrize("g", [128, 256])
+def test_config5_full_size_properties(cuda, g):
+    """Config 5 at its full 200M vertices (seed mode at 256^3): bound on every
+    vertex, determinism, no serial fallback, across the tau range."""
+    import torch
+    xyz, x = umcg.gen_config(5, 200_000_000, 20250105, device="cuda")
+    lo = xyz.min(0).values.cpu().numpy()
+    hi = xyz.max(0).values.cpu().numpy()
+    plan = umcg.Plan.build([np.linspace(lo[d], hi[d], g) for d in range(3)], xyz)
+    del xyz
+    # SURVEY 8(d): visited fraction 0.376 at 128^3 (dense), 0.317 at 256^3 (seed)
+    print(f"g={g} mode={plan.info.mode} visited={plan.info.visited_fraction:.3f}")
+    assert plan.info.mode == (1 if g == 256 else 0)
+    torch.cuda.empty_cache()
+    rng = float((x.max() - x.min()).item())
+    for tau in (1e-2, 1e-6):
+        b = umcg.Budget(tau=tau)
+        a1 = plan.compress(x, b)
+        assert plan.compress(x, b) == a1
+        fb0 = umcg.serial_fallbacks()
+        out = plan.decompress(a1)
+        assert umcg.serial_fallbacks() == fb0
+        err = (out - x).abs().max().item()
+        assert err <= tau * rng, (g, tau, err, tau * rng)
+        del out
