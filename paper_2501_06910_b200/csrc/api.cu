@@ -580,7 +580,8 @@ void decode_component(umcg_plan* p, const CompHeader& h, const uint8_t* d_payloa
     if (h.tau == 0.0) {
         if (h.n_esc != 0) fail(UMCG_CORRUPT_PAYLOAD, "lossless payload with escapes");
         if (pred == 2) {
-            serial_decode(codes, h.n, pred, sh, 0.0, nullptr, nullptr, 0, d_out, st);
+            if (!lossless_nd_wavefront(codes, h.n, sh, d_out, st))
+                serial_decode(codes, h.n, pred, sh, 0.0, nullptr, nullptr, 0, d_out, st);
         } else {
             uint64_t* sc = p->kbuf.as<uint64_t>(cdiv(h.n, RECON_TILE) + 1);
             recon_lossless(codes, h.n, pred, d_out, sc, st);

@@ -588,6 +588,51 @@ void serial_encode(const double* v, uint64_t n, int pred, const NdShape& sh, dou
     UMCG_LAUNCHED();
 }
 
+// N-D lossless decode (codec.hpp:429-430 with lorenzo_nd): recon_i =
+// bits^-1(code_i XOR bits(pred_i)) where pred_i is the floating-point Lorenzo
+// prediction from already reconstructed neighbours, so the dependency is
+// real. Every neighbour of (i, j[, k]) lies on an earlier hyperplane
+// i + j [+ k] = s, so the hyperplanes are decoded in order, each fully in
+// parallel with the reference's exact prediction (lorenzo_fp, same operation
+// order). D = 2, 3; other ranks use the serial replica.
+namespace {
+__global__ void __launch_bounds__(THREADS) k_lossless_plane(const uint64_t* __restrict__ codes, NdShape sh,
+                                                           uint64_t s, uint64_t i_lo, uint64_t cnt,
+                                                           double* __restrict__ recon) {
+    const uint64_t t = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (t >= cnt) return;
+    uint64_t lin;
+    if (sh.D == 2) {
+        const uint64_t i = i_lo + t, j = s - i;
+        lin = i * sh.dims[1] + j;
+    } else {
+        const uint64_t i = i_lo + t / sh.dims[1], j = t % sh.dims[1];
+        if (i + j > s) return;
+        const uint64_t k = s - i - j;
+        if (k >= sh.dims[2]) return;
+        lin = (i * sh.dims[1] + j) * sh.dims[2] + k;
+    }
+    const double p = lorenzo_fp(recon, lin, sh);
+    recon[lin] = __longlong_as_double((long long)(codes[lin] ^ (uint64_t)__double_as_longlong(p)));
+}
+}  // namespace
+
+bool lossless_nd_wavefront(const uint64_t* codes, uint64_t n, const NdShape& sh, double* out, cudaStream_t st) {
+    if (sh.D != 2 && sh.D != 3) return false;
+    if (!n) return true;
+    uint64_t smax = 0;
+    for (int d = 0; d < sh.D; ++d) smax += sh.dims[d] - 1;
+    const uint64_t d0 = sh.dims[0], rest = smax - (d0 - 1);  // max of the other coordinates' sum
+    for (uint64_t s = 0; s <= smax; ++s) {
+        const uint64_t i_lo = s > rest ? s - rest : 0, i_hi = std::min<uint64_t>(d0 - 1, s);
+        const uint64_t rows = i_hi - i_lo + 1;
+        const uint64_t cnt = sh.D == 2 ? rows : rows * sh.dims[1];
+        k_lossless_plane<<<(unsigned)cdiv(cnt, THREADS), THREADS, 0, st>>>(codes, sh, s, i_lo, cnt, out);
+        UMCG_LAUNCHED();
+    }
+    return true;
+}
+
 void serial_decode(const uint64_t* codes, uint64_t n, int pred, const NdShape& sh, double tau,
                    const uint64_t* esc_idx, const double* esc_val, uint64_t n_esc, double* out,
                    cudaStream_t st) {

@@ -102,6 +102,8 @@ void serial_encode(const double* v, uint64_t n, int pred, const NdShape& sh, dou
                    uint64_t* codes, double* recon_scratch, uint64_t* esc_idx, double* esc_val,
                    DevCtl* ctl, int comp, cudaStream_t st);
 // Exact serial replica of decode (codec.hpp:422-437).
+// N-D lossless decode by hyperplane wavefront (D = 2, 3); false otherwise.
+bool lossless_nd_wavefront(const uint64_t* codes, uint64_t n, const NdShape& sh, double* out, cudaStream_t st);
 void serial_decode(const uint64_t* codes, uint64_t n, int pred, const NdShape& sh, double tau,
                    const uint64_t* esc_idx, const double* esc_val, uint64_t n_esc, double* out,
                    cudaStream_t st);

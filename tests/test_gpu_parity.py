@@ -645,3 +645,21 @@ def test_config5_full_size_properties(cuda, g):
         err = (out - x).abs().max().item()
         assert err <= tau * rng, (g, tau, err, tau * rng)
         del out
+
+
+@pytest.mark.parametrize("dims", [[300, 200], [64, 48, 40], [1, 500, 3], [7, 1, 9]])
+def test_lossless_nd_wavefront_matches_reference(cuda, ref, dims):
+    """tau = 0 N-D decode (codec.hpp:276-294, 429-430): the hyperplane
+    wavefront reproduces the reference's floating-point Lorenzo chain bit
+    for bit, without the one-thread replica."""
+    rng = np.random.default_rng(sum(dims))
+    n = int(np.prod(dims))
+    v = np.cumsum(rng.normal(size=n)).reshape(dims)
+    v = (v + 1e-3 * rng.normal(size=dims)).ravel()
+    v[::7] = 0.0
+    pl = ref.encode(v, predictor=2, dims=dims, tau=0.0)
+    assert umcg.encode(dev(v), predictor=2, dims=dims, tau=0.0) == pl
+    fb0 = umcg.serial_fallbacks()
+    out = umcg.decode(pl).cpu().numpy()
+    assert np.array_equal(out.view(np.uint64), v.view(np.uint64))
+    assert umcg.serial_fallbacks() == fb0
