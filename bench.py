@@ -116,15 +116,23 @@ def algorithmic_bytes(n, n1, archive):
     return b_c, b_d
 
 
-def kernel_bytes(n, n1, s2, k1_bytes):
+def narrow_path(tau, rho=0.5):
+    """api.cu compress_pass: int16 lattice indices + u16 residual codes when
+    1 / (2 (1 - rho) tau) < 16000 under a relative bound."""
+    return tau > 0 and 1.0 / (2.0 * (1.0 - rho) * tau) < 16000.0
+
+
+def kernel_bytes(n, n1, s2, k1_bytes, narrow=False):
     """Compulsory bytes per launch of each hot kernel:
     s2 = residual stream bytes, k1_bytes = bytes per grid lattice index in
-    the decompress gather table (2 when |K1| < 2^15)."""
+    the decompress gather table (2 when |K1| < 2^15), narrow = int16 KE and
+    u16 codes."""
+    kb, cb = (2, 2) if narrow else (4, 4)
     return {
         "k_gather_fwd": 20 * n,                  # x 8 + srcE 4 -> xE 8
-        "k_bucket": 16 * n + 12 * n1,            # xE 8 + lperm 2 + lnode 2 + KE 4; seg 4 + x1 8 per slot
-        "k_resid_codes": 12 * n,                 # dstE 4 + KE 4 (gathered once) + codes 4
-        "k_rle_write": 4 * n + s2,               # codes 4 + stream out
+        "k_bucket": (12 + kb) * n + 12 * n1,     # xE 8 + lperm 2 + lnode 2 + KE; seg 4 + x1 8 per slot
+        "k_resid_codes": (4 + kb + cb) * n,      # dstE 4 + KE (gathered once) + codes
+        "k_rle_write": cb * n + s2,              # codes + stream out
         "k_dec_agg": s2,                         # stream in
         "k_dec_out": 12 * n + s2 + k1_bytes * n1,  # node 4 + out 8 + stream + K1 table
     }
@@ -339,7 +347,7 @@ def main():
         s2 = alen - (10 + nl + 32 + l1 + 8) - 37  # payload2 minus its 37-byte header
     except Exception:
         pass
-    kb = kernel_bytes(n, n1, s2, 2)
+    kb = kernel_bytes(n, n1, s2, 2, narrow_path(args.tau))
     kernels = {k: {"ms": v, "gbs": kb[k] / (v * 1e-3) / 1e9 if k in kb else None,
                    "frac": kb[k] / (v * 1e-3) / 1e9 / peak if k in kb else None,
                    "algorithmic_bytes": kb.get(k)} for k, v in kms.items()}

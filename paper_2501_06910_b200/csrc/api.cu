@@ -253,6 +253,12 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     init_ctl(ctl, st);
     // nearest g: partitioned layout (partition.cu); multilinear: gathers
     const bool part = prm.g_kind == 0 && p->n_buckets > 0 && !m.verbatim;
+    // Narrow residual path (int16 lattice indices, u16 codes): a residual is
+    // x_i minus the mean of its cluster, so |r| <= range and, for a relative
+    // bound, |K2| <= range / bin2 ~ 1 / (2 (1 - rho) tau): <= 16383 keeps every
+    // code zigzag(K_i - K_{i-1}) < 2^16.
+    const bool narrow = part && !m.serial[1] && !m.lossless[1] && prm.bound_kind == 1 && prm.tau > 0.0 &&
+                        1.0 / (2.0 * (1.0 - prm.split_rho) * prm.tau) < 16000.0;
     double* x1 = p->x1.as<double>(n1 ? n1 : 1);
     int32_t* Kp = nullptr;
     if (part) {
@@ -261,7 +267,7 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
         partition_values(d_x, x_f32, p, xp, ctl, st);  // + range / finiteness
         budget(BudgetArgs{prm.tau, prm.split_rho, prm.coeff_abs_sum, prm.bound_kind, n}, ctl, st);
         // f: cluster means (interp.hpp:46-93) + residual lattice indices
-        bucket_means_residuals(p, xp, ctl, x1, Kp, st);
+        bucket_means_residuals(p, xp, ctl, x1, Kp, narrow, st);
     } else {
         minmax(d_x, x_f32, n, ctl, st);
         budget(BudgetArgs{prm.tau, prm.split_rho, prm.coeff_abs_sum, prm.bound_kind, n}, ctl, st);
@@ -298,7 +304,7 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     for (int c = 0; c < 2; ++c) {
         DevBuf& cb = c == 0 ? p->codes1 : p->codes2;
         wide[c] = m.lossless[c] || m.serial[c];
-        codes[c] = cb.reserve((ncode[c] ? ncode[c] : 1) * (wide[c] ? 8 : 4));
+        codes[c] = cb.reserve((ncode[c] ? ncode[c] : 1) * (wide[c] ? 8 : (c == 1 && narrow) ? 2 : 4));
     }
     uint64_t* esc_idx[2] = {nullptr, nullptr};
     double* esc_val[2] = {nullptr, nullptr};
@@ -337,7 +343,7 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     const bool fused_resid = part && !m.serial[1] && !m.lossless[1];
     if (fused_resid) {
         // q = K2_i - K2_{i-1} back in vertex order + RLE tile summaries (partition.cu)
-        resid_codes_tiles(p, Kp, static_cast<uint32_t*>(codes[1]), es[1], st);
+        resid_codes_tiles(p, Kp, codes[1], narrow, es[1], st);
     } else if (!m.serial[1] && !m.lossless[1]) {
         codes_lossy_residual(rs, n, ctl, static_cast<uint32_t*>(codes[1]), st);
     }
@@ -361,6 +367,7 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
             }
         }
         if (wide[c]) stream_write_u64(static_cast<uint64_t*>(codes[c]), ncode[c], es[c], ctl, c, d_ar, true, st);
+        else if (c == 1 && narrow) stream_write_u16(static_cast<uint16_t*>(codes[c]), ncode[c], es[c], ctl, c, d_ar, true, st);
         else stream_write_u32(static_cast<uint32_t*>(codes[c]), ncode[c], es[c], ctl, c, d_ar, true, st);
     }
     return read_ctl(p, ctl, st);

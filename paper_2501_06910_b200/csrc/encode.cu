@@ -484,6 +484,8 @@ void stream_write_u32(const uint32_t* c, uint64_t n, const StreamEncScratch& s, 
                       uint8_t* dst, bool o, cudaStream_t st) { write_impl(c, n, s, ctl, comp, dst, o, st); }
 void stream_write_u64(const uint64_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
                       uint8_t* dst, bool o, cudaStream_t st) { write_impl(c, n, s, ctl, comp, dst, o, st); }
+void stream_write_u16(const uint16_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
+                      uint8_t* dst, bool o, cudaStream_t st) { write_impl(c, n, s, ctl, comp, dst, o, st); }
 void stream_plan_u8(const uint8_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
                     cudaStream_t st) { plan_impl(c, n, s, ctl, comp, st); }
 void stream_write_u8(const uint8_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,

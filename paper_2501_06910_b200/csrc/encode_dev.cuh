@@ -35,6 +35,13 @@ __device__ __forceinline__ void write_varint(uint8_t* out, uint64_t pos, uint64_
 template <class T>
 __device__ __forceinline__ int load_items(const T* codes, uint64_t n, uint64_t first, T (&v)[ENC_ITEMS]) {
     int cnt = 0;
+    if (first + ENC_ITEMS <= n && sizeof(T) == 2 && (first % 8) == 0) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(codes + first));
+        const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+        for (int k = 0; k < ENC_ITEMS; ++k) v[k] = (T)(w[k >> 1] >> (16 * (k & 1)));
+        return ENC_ITEMS;
+    }
     if (first + ENC_ITEMS <= n && sizeof(T) == 4 && (first % 4) == 0) {
         const uint4* p = reinterpret_cast<const uint4*>(codes + first);
         const uint4 a = __ldg(p), b = __ldg(p + 1);

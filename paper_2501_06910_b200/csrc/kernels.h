@@ -35,6 +35,9 @@ void stream_plan_u64(const uint64_t* codes, uint64_t n, const StreamEncScratch& 
 // Phases 2-4 only, when the tile summaries (s.sums) were produced by a fused
 // code kernel (partition.cu).
 void stream_plan_from_sums(uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp, cudaStream_t st);
+// u16 codes (narrow residual path)
+void stream_write_u16(const uint16_t* codes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
+                      uint8_t* dst, bool dst_off_from_ctl, cudaStream_t st);
 // Raw bytes as codes (lossless_compress of a byte buffer, lossless.hpp:24-51).
 void stream_plan_u8(const uint8_t* bytes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
                     cudaStream_t st);

@@ -17,6 +17,8 @@
 //                 K2 = round((x - x1[m]) / bin2) per vertex (bucket order);
 //   k_resid_codes back to vertex order through dst: q_i = K2_i - K2_{i-1},
 //                 zigzag codes + the RLE tile summary in the same pass.
+#include <type_traits>
+
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
@@ -94,11 +96,12 @@ __device__ __forceinline__ int32_t resid_k(double r, double bin, double inv, dou
 // layout-E position. Each warp moves whole chunks (coalesced).
 constexpr int PER = kBucketCap / BT;  // elements per thread in a bucket
 
+template <class KT>
 __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, const uint32_t* __restrict__ bk,
                                               uint64_t B, uint32_t E, const uint2* __restrict__ bct,
                                               const uint16_t* __restrict__ lnode,
                                               const uint16_t* __restrict__ lperm, const uint32_t* __restrict__ seg,
-                                              DevCtl* ctl, double* __restrict__ x1, int32_t* __restrict__ KE,
+                                              DevCtl* ctl, double* __restrict__ x1, KT* __restrict__ KE,
                                               int heavy_only) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* xs = reinterpret_cast<double*>(smem);                      // [kBucketCap]
@@ -136,7 +139,7 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
         for (uint32_t e = warp; e < E; e += NW)
             for (uint32_t l = ch[e].x + lane; l < ch[e + 1].x; l += 32) {
                 const uint32_t q = ch[e].y + (l - ch[e].x);
-                KE[q] = resid_k(__dsub_rn(xE[q], mean), bin, inv, tau, ctl);
+                KE[q] = (KT)resid_k(__dsub_rn(xE[q], mean), bin, inv, tau, ctl);
             }
         return;
     }
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
             const uint32_t l = threadIdx.x + k * BT;
             if (l < m) {
                 while (l >= ch[e + 1].x) ++e;
-                KE[ch[e].y + (l - ch[e].x)] = resid_k(__dsub_rn(xs[l], x1s[ln[l]]), bin, inv, tau, ctl);
+                KE[ch[e].y + (l - ch[e].x)] = (KT)resid_k(__dsub_rn(xs[l], x1s[ln[l]]), bin, inv, tau, ctl);
             }
         }
     }
@@ -262,13 +265,14 @@ __device__ __forceinline__ void issue_bucket(const PipeStage& S, const double* _
     for (uint32_t j = threadIdx.x; j <= nj; j += BTP) cp_async(&S.sg[j], &seg[j0 + j], 4);
 }
 
+template <class KT>
 __global__ void __launch_bounds__(BTP) k_bucket_pipe(const double* __restrict__ xE, const uint32_t* __restrict__ bk,
                                                    uint64_t B, uint32_t E, const uint2* __restrict__ bct,
                                                    const uint32_t* __restrict__ regular, uint32_t n_regular,
                                                    const uint16_t* __restrict__ lnode,
                                                    const uint16_t* __restrict__ lperm,
                                                    const uint32_t* __restrict__ seg, DevCtl* ctl,
-                                                   double* __restrict__ x1, int32_t* __restrict__ KE) {
+                                                   double* __restrict__ x1, KT* __restrict__ KE) {
     extern __shared__ __align__(16) unsigned char smem[];
     // Stage pointers are recomputed from the extern shared array (never kept
     // in a runtime-indexed array) so every access compiles to LDS/STS rather
@@ -346,7 +350,7 @@ __global__ void __launch_bounds__(BTP) k_bucket_pipe(const double* __restrict__ 
             for (uint32_t e = warp; e < E; e += BTP / 32) {
                 const uint2 c0 = C.ch[e], c1 = C.ch[e + 1];
                 for (uint32_t l = c0.x + lane; l < c1.x; l += 32)
-                    KE[c0.y + (l - c0.x)] = resid_k(__dsub_rn(C.xs[l], x1s[C.ln[l + off]]), bin, inv, tau, ctl);
+                    KE[c0.y + (l - c0.x)] = (KT)resid_k(__dsub_rn(C.xs[l], x1s[C.ln[l + off]]), bin, inv, tau, ctl);
             }
         }
         cur = nxt;
@@ -359,14 +363,15 @@ __global__ void __launch_bounds__(BTP) k_bucket_pipe(const double* __restrict__ 
 
 // Vertex order: q_i = K_i - K_{i-1} through dstE (gather inside an epoch
 // window), zigzag codes, RLE tile summary.
+template <class KT, class CT>
 __global__ void __launch_bounds__(ENC_THREADS) k_resid_codes(const uint32_t* __restrict__ dst,
-                                                            const int32_t* __restrict__ Kp, uint64_t n,
-                                                            uint32_t* __restrict__ codes, RleSum* __restrict__ sums) {
+                                                            const KT* __restrict__ Kp, uint64_t n,
+                                                            CT* __restrict__ codes, RleSum* __restrict__ sums) {
     using BR = cub::BlockReduce<RleSum, ENC_THREADS>;
     __shared__ typename BR::TempStorage tmp;
     const uint64_t tile = blockIdx.x;
     const uint64_t first = tile * ENC_TILE + (uint64_t)threadIdx.x * ENC_ITEMS;
-    uint32_t v[ENC_ITEMS];
+    CT v[ENC_ITEMS];
     int cnt = 0;
     if (first < n) {
         int64_t prev = first ? (int64_t)Kp[dst[first - 1]] : 0;
@@ -381,11 +386,11 @@ __global__ void __launch_bounds__(ENC_THREADS) k_resid_codes(const uint32_t* __r
         }
         int32_t K[ENC_ITEMS];
 #pragma unroll
-        for (int k = 0; k < ENC_ITEMS; ++k) K[k] = first + k < n ? __ldg(&Kp[d[k]]) : 0;
+        for (int k = 0; k < ENC_ITEMS; ++k) K[k] = first + k < n ? (int32_t)__ldg(&Kp[d[k]]) : 0;
 #pragma unroll
         for (int k = 0; k < ENC_ITEMS; ++k) {
             if (first + k < n) {
-                v[k] = (uint32_t)zz_enc((int64_t)K[k] - prev);
+                v[k] = (CT)zz_enc((int64_t)K[k] - prev);
                 prev = K[k];
                 cnt = k + 1;
             } else {
@@ -393,9 +398,15 @@ __global__ void __launch_bounds__(ENC_THREADS) k_resid_codes(const uint32_t* __r
             }
         }
         if (cnt == ENC_ITEMS) {
-            uint4* o = reinterpret_cast<uint4*>(codes + first);
-            o[0] = make_uint4(v[0], v[1], v[2], v[3]);
-            o[1] = make_uint4(v[4], v[5], v[6], v[7]);
+            if (sizeof(CT) == 4) {
+                uint4* o = reinterpret_cast<uint4*>(codes + first);
+                o[0] = make_uint4(v[0], v[1], v[2], v[3]);
+                o[1] = make_uint4(v[4], v[5], v[6], v[7]);
+            } else {
+                *reinterpret_cast<uint4*>(codes + first) =
+                    make_uint4((uint32_t)v[0] | ((uint32_t)v[1] << 16), (uint32_t)v[2] | ((uint32_t)v[3] << 16),
+                               (uint32_t)v[4] | ((uint32_t)v[5] << 16), (uint32_t)v[6] | ((uint32_t)v[7] << 16));
+            }
         } else {
             for (int k = 0; k < cnt; ++k) codes[first + k] = v[k];
         }
@@ -421,14 +432,17 @@ void partition_values(const void* x, int x_f32, umcg_plan* p, double* xE, DevCtl
     UMCG_LAUNCHED();
 }
 
-void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double* x1, int32_t* KE, cudaStream_t st) {
+void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double* x1, void* KE, bool narrow,
+                            cudaStream_t st) {
     if (!p->n_buckets) return;
     ProfScope ps_("k_bucket", st);
     const uint32_t E = (uint32_t)p->n_epochs;
     static bool configured = false;
     if (!configured) {
-        UMCG_CUDA(cudaFuncSetAttribute(k_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        UMCG_CUDA(cudaFuncSetAttribute(k_bucket_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        UMCG_CUDA(cudaFuncSetAttribute(k_bucket<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        UMCG_CUDA(cudaFuncSetAttribute(k_bucket<int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        UMCG_CUDA(cudaFuncSetAttribute(k_bucket_pipe<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        UMCG_CUDA(cudaFuncSetAttribute(k_bucket_pipe<int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         configured = true;
     }
     const bool pipe = E + 1 <= BTP && p->n_regular > 0;
@@ -438,29 +452,44 @@ void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double*
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const unsigned g = (unsigned)std::min<uint64_t>(p->n_regular, (uint64_t)sms * 2);
-        k_bucket_pipe<<<g, BTP, smem, st>>>(xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E, p->d_bct.as<uint2>(1),
-                                           p->d_regular.as<uint32_t>(1), (uint32_t)p->n_regular,
-                                           p->d_lnode.as<uint16_t>(1), p->d_lperm.as<uint16_t>(1),
-                                           p->d_seg.as<uint32_t>(1), ctl, x1, KE);
+        auto launch = [&](auto* ke) {
+            using KT = std::remove_pointer_t<decltype(ke)>;
+            k_bucket_pipe<KT><<<g, BTP, smem, st>>>(xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E,
+                                                   p->d_bct.as<uint2>(1), p->d_regular.as<uint32_t>(1),
+                                                   (uint32_t)p->n_regular, p->d_lnode.as<uint16_t>(1),
+                                                   p->d_lperm.as<uint16_t>(1), p->d_seg.as<uint32_t>(1), ctl, x1, ke);
+        };
+        if (narrow) launch(static_cast<int16_t*>(KE));
+        else launch(static_cast<int32_t*>(KE));
         UMCG_LAUNCHED();
     }
     if (!pipe || p->n_regular < p->n_buckets) {
         // all buckets (no pipeline possible) or the heavy single-slot buckets
         const size_t smem = kBucketCap * 8 + kBucketNodes * 8 + (kBucketNodes + 2) * 4 + ((size_t)E + 1) * 8 +
                             kBucketCap * 4 + 16;
-        k_bucket<<<(unsigned)p->n_buckets, BT, smem, st>>>(xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E,
-                                                            p->d_bct.as<uint2>(1), p->d_lnode.as<uint16_t>(1),
-                                                            p->d_lperm.as<uint16_t>(1), p->d_seg.as<uint32_t>(1), ctl,
-                                                            x1, KE, pipe ? 1 : 0);
+        auto launch = [&](auto* ke) {
+            using KT = std::remove_pointer_t<decltype(ke)>;
+            k_bucket<KT><<<(unsigned)p->n_buckets, BT, smem, st>>>(xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E,
+                                                                   p->d_bct.as<uint2>(1), p->d_lnode.as<uint16_t>(1),
+                                                                   p->d_lperm.as<uint16_t>(1),
+                                                                   p->d_seg.as<uint32_t>(1), ctl, x1, ke, pipe ? 1 : 0);
+        };
+        if (narrow) launch(static_cast<int16_t*>(KE));
+        else launch(static_cast<int32_t*>(KE));
         UMCG_LAUNCHED();
     }
 }
-
-void resid_codes_tiles(umcg_plan* p, const int32_t* KE, uint32_t* codes, const StreamEncScratch& s, cudaStream_t st) {
+void resid_codes_tiles(umcg_plan* p, const void* KE, void* codes, bool narrow, const StreamEncScratch& s,
+                       cudaStream_t st) {
     const uint64_t T = cdiv(p->n, ENC_TILE);
     if (!T) return;
     ProfScope ps_("k_resid_codes", st);
-    k_resid_codes<<<(unsigned)T, ENC_THREADS, 0, st>>>(p->d_dstE.as<uint32_t>(1), KE, p->n, codes, s.sums);
+    if (narrow)
+        k_resid_codes<int16_t, uint16_t><<<(unsigned)T, ENC_THREADS, 0, st>>>(
+            p->d_dstE.as<uint32_t>(1), static_cast<const int16_t*>(KE), p->n, static_cast<uint16_t*>(codes), s.sums);
+    else
+        k_resid_codes<int32_t, uint32_t><<<(unsigned)T, ENC_THREADS, 0, st>>>(
+            p->d_dstE.as<uint32_t>(1), static_cast<const int32_t*>(KE), p->n, static_cast<uint32_t*>(codes), s.sums);
     UMCG_LAUNCHED();
 }
 

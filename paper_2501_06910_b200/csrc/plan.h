@@ -90,8 +90,10 @@ void decode_component(umcg_plan* ws, const CompHeader& h, const uint8_t* d_paylo
 namespace umcg {
 // partition.cu: the partitioned (bucketed) compress path for nearest g.
 void partition_values(const void* x, int x_f32, umcg_plan* p, double* xp, DevCtl* ctl, cudaStream_t st);
-void bucket_means_residuals(umcg_plan* p, const double* xp, DevCtl* ctl, double* x1, int32_t* Kp,
+// narrow: KE int16 and residual codes u16 (the caller guarantees
+// |K2| <= 16383 from the budget: |x - x1| <= range, see api.cu).
+void bucket_means_residuals(umcg_plan* p, const double* xp, DevCtl* ctl, double* x1, void* Kp, bool narrow,
                             cudaStream_t st);
-void resid_codes_tiles(umcg_plan* p, const int32_t* Kp, uint32_t* codes, const StreamEncScratch& s,
+void resid_codes_tiles(umcg_plan* p, const void* Kp, void* codes, bool narrow, const StreamEncScratch& s,
                        cudaStream_t st);
 }  // namespace umcg
