@@ -259,6 +259,9 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     // code zigzag(K_i - K_{i-1}) < 2^16.
     const bool narrow = part && !m.serial[1] && !m.lossless[1] && prm.bound_kind == 1 && prm.tau > 0.0 &&
                         1.0 / (2.0 * (1.0 - prm.split_rho) * prm.tau) < 16000.0;
+    // dense N-D grid: the bucket kernels also write K1 = lattice(x1) (no fill
+    // pass may change x1 afterwards)
+    const bool fuse_k1 = part && p->mode == 0 && p->dim > 1 && !m.serial[0] && !m.lossless[0] && prm.fill == 0;
     double* x1 = p->x1.as<double>(n1 ? n1 : 1);
     int32_t* Kp = nullptr;
     if (part) {
@@ -267,7 +270,8 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
         partition_values(d_x, x_f32, p, xp, ctl, st);  // + range / finiteness
         budget(BudgetArgs{prm.tau, prm.split_rho, prm.coeff_abs_sum, prm.bound_kind, n}, ctl, st);
         // f: cluster means (interp.hpp:46-93) + residual lattice indices
-        bucket_means_residuals(p, xp, ctl, x1, Kp, narrow, st);
+        bucket_means_residuals(p, xp, ctl, x1, Kp, narrow, fuse_k1 ? p->scratch_d.as<int32_t>(n1 ? n1 : 1) : nullptr,
+                               p->dim, st);
     } else {
         minmax(d_x, x_f32, n, ctl, st);
         budget(BudgetArgs{prm.tau, prm.split_rho, prm.coeff_abs_sum, prm.bound_kind, n}, ctl, st);
@@ -319,7 +323,7 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
         codes_lossless_values(x1, n1, pred1, sh1, static_cast<uint64_t*>(codes[0]), st);
     } else {
         int32_t* kb = p->scratch_d.as<int32_t>(n1 ? n1 : 1);
-        codes_lossy_values(x1, n1, pred1, sh1, ctl, 0, static_cast<uint32_t*>(codes[0]), kb, st);
+        codes_lossy_values(x1, n1, pred1, sh1, ctl, 0, static_cast<uint32_t*>(codes[0]), kb, st, fuse_k1);
     }
     // residual component
     if (m.serial[1]) {

@@ -528,11 +528,13 @@ inline unsigned blocks(uint64_t n, uint64_t per = THREADS) { return (unsigned)cd
 }  // namespace
 
 void codes_lossy_values(const double* v, uint64_t n, int pred, const NdShape& sh, DevCtl* ctl, int comp,
-                        uint32_t* codes, int32_t* kbuf, cudaStream_t st) {
+                        uint32_t* codes, int32_t* kbuf, cudaStream_t st, bool k_ready) {
     if (!n) return;
     if (pred == 2 && sh.D > 1) {
-        k_lattice_nd<<<blocks(n), THREADS, 0, st>>>(v, n, sh.D, ctl, comp, kbuf);
-        UMCG_LAUNCHED();
+        if (!k_ready) {  // else kbuf holds the lattice indices already (fused into the bucket kernels)
+            k_lattice_nd<<<blocks(n), THREADS, 0, st>>>(v, n, sh.D, ctl, comp, kbuf);
+            UMCG_LAUNCHED();
+        }
         if ((sh.D == 2 || sh.D == 3) && sh.dims[0] < 65536 && (sh.D == 2 || sh.dims[1] < 65536)) {
             const uint64_t d0 = sh.D == 3 ? sh.dims[0] : 1, d1 = sh.D == 3 ? sh.dims[1] : sh.dims[0];
             const uint64_t d2 = sh.dims[sh.D - 1];

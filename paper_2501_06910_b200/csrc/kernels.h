@@ -75,8 +75,9 @@ NdShape make_shape(int D, const uint64_t* dims);
 // lossy codes of a values array. pred 0 none, 1 lorenzo_1d, 2 lorenzo_nd.
 // Reads bin/tau from ctl->bin[comp]/tau_c[comp]. Flags ctl->need_serial[comp]
 // when the lattice formulation may differ from the serial reference chain.
+// k_ready: kbuf already holds the N-D lattice indices (fused upstream).
 void codes_lossy_values(const double* v, uint64_t n, int pred, const NdShape& sh, DevCtl* ctl,
-                        int comp, uint32_t* codes, int32_t* kbuf, cudaStream_t st);
+                        int comp, uint32_t* codes, int32_t* kbuf, cudaStream_t st, bool k_ready = false);
 // lossless (tau == 0) XOR codes (codec.hpp:276-294); always exact.
 void codes_lossless_values(const double* v, uint64_t n, int pred, const NdShape& sh,
                            uint64_t* codes, cudaStream_t st);

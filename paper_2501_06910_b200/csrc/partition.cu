@@ -17,6 +17,7 @@
 //                 K2 = round((x - x1[m]) / bin2) per vertex (bucket order);
 //   k_resid_codes back to vertex order through dst: q_i = K2_i - K2_{i-1},
 //                 zigzag codes + the RLE tile summary in the same pass.
+#include <cmath>
 #include <type_traits>
 
 #include <cub/block/block_reduce.cuh>
@@ -91,6 +92,22 @@ __device__ __forceinline__ int32_t resid_k(double r, double bin, double inv, dou
     return bad ? 0 : (int32_t)K;
 }
 
+// Grid lattice index of a cluster mean, fused into the bucket kernels for the
+// dense N-D grid component (codes.cu lattice_k / k_lattice_nd, component 0).
+struct GridK {
+    int32_t* K1;  // nullptr: not fused
+    double lim;   // 2^(31-D)
+};
+__device__ __forceinline__ void grid_k(const GridK& g, uint64_t j, double v, DevCtl* ctl) {
+    if (!g.K1) return;
+    double err;
+    const double K = lattice_round(v, ctl->bin[0], ctl->inv_bin[0], ctl->tau_c[0], &err);
+    if (!(fabs(K) < g.lim) || !(err <= ctl->tau_c[0])) {
+        if (ctl->need_serial[0] == 0) atomicExch(&ctl->need_serial[0], 1);
+    }
+    g.K1[j] = (int32_t)K;
+}
+
 // Bucket b's elements, in bucket order l = 0..m-1, live in layout E as one
 // chunk per epoch: pre[e] = first l of epoch e's chunk, cbase[e] = its
 // layout-E position. Each warp moves whole chunks (coalesced).
@@ -102,7 +119,7 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
                                               const uint16_t* __restrict__ lnode,
                                               const uint16_t* __restrict__ lperm, const uint32_t* __restrict__ seg,
                                               DevCtl* ctl, double* __restrict__ x1, KT* __restrict__ KE,
-                                              int heavy_only) {
+                                              int heavy_only, GridK gk) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* xs = reinterpret_cast<double*>(smem);                      // [kBucketCap]
     double* x1s = xs + kBucketCap;                                     // [kBucketNodes]
@@ -133,6 +150,7 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
                 for (uint32_t l = ch[e].x; l < ch[e + 1].x; ++l) s = __dadd_rn(s, xE[ch[e].y + (l - ch[e].x)]);
             x1s[0] = __ddiv_rn(s, (double)m);
             x1[j0] = x1s[0];
+            grid_k(gk, j0, x1s[0], ctl);
         }
         __syncthreads();
         const double mean = x1s[0];
@@ -187,6 +205,7 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
         const double v = k1 > k0 ? __ddiv_rn(s, (double)(k1 - k0)) : 0.0;
         x1s[j] = v;
         x1[j0 + j] = v;
+        grid_k(gk, j0 + j, v, ctl);
     }
     __syncthreads();
     // compute_residuals (interp.hpp:161-170) + lattice index (codec.hpp:307-314)
@@ -272,7 +291,7 @@ __global__ void __launch_bounds__(BTP) k_bucket_pipe(const double* __restrict__ 
                                                    const uint16_t* __restrict__ lnode,
                                                    const uint16_t* __restrict__ lperm,
                                                    const uint32_t* __restrict__ seg, DevCtl* ctl,
-                                                   double* __restrict__ x1, KT* __restrict__ KE) {
+                                                   double* __restrict__ x1, KT* __restrict__ KE, GridK gk) {
     extern __shared__ __align__(16) unsigned char smem[];
     // Stage pointers are recomputed from the extern shared array (never kept
     // in a runtime-indexed array) so every access compiles to LDS/STS rather
@@ -342,6 +361,7 @@ __global__ void __launch_bounds__(BTP) k_bucket_pipe(const double* __restrict__ 
             const double v = k1 > k0 ? __ddiv_rn(s, (double)(k1 - k0)) : 0.0;
             x1s[j] = v;
             x1[j0 + j] = v;
+            grid_k(gk, j0 + j, v, ctl);
         }
         __syncthreads();
         // compute_residuals (interp.hpp:161-170) + lattice index (codec.hpp:307-314)
@@ -433,7 +453,8 @@ void partition_values(const void* x, int x_f32, umcg_plan* p, double* xE, DevCtl
 }
 
 void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double* x1, void* KE, bool narrow,
-                            cudaStream_t st) {
+                            int32_t* K1, int D1, cudaStream_t st) {
+    const GridK gk{K1, std::ldexp(1.0, 31 - (D1 < 1 ? 1 : D1))};
     if (!p->n_buckets) return;
     ProfScope ps_("k_bucket", st);
     const uint32_t E = (uint32_t)p->n_epochs;
@@ -457,7 +478,8 @@ void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double*
             k_bucket_pipe<KT><<<g, BTP, smem, st>>>(xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E,
                                                    p->d_bct.as<uint2>(1), p->d_regular.as<uint32_t>(1),
                                                    (uint32_t)p->n_regular, p->d_lnode.as<uint16_t>(1),
-                                                   p->d_lperm.as<uint16_t>(1), p->d_seg.as<uint32_t>(1), ctl, x1, ke);
+                                                   p->d_lperm.as<uint16_t>(1), p->d_seg.as<uint32_t>(1), ctl, x1, ke,
+                                                   gk);
         };
         if (narrow) launch(static_cast<int16_t*>(KE));
         else launch(static_cast<int32_t*>(KE));
@@ -472,7 +494,8 @@ void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double*
             k_bucket<KT><<<(unsigned)p->n_buckets, BT, smem, st>>>(xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E,
                                                                    p->d_bct.as<uint2>(1), p->d_lnode.as<uint16_t>(1),
                                                                    p->d_lperm.as<uint16_t>(1),
-                                                                   p->d_seg.as<uint32_t>(1), ctl, x1, ke, pipe ? 1 : 0);
+                                                                   p->d_seg.as<uint32_t>(1), ctl, x1, ke, pipe ? 1 : 0,
+                                                                   gk);
         };
         if (narrow) launch(static_cast<int16_t*>(KE));
         else launch(static_cast<int32_t*>(KE));

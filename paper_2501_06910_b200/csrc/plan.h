@@ -92,8 +92,10 @@ namespace umcg {
 void partition_values(const void* x, int x_f32, umcg_plan* p, double* xp, DevCtl* ctl, cudaStream_t st);
 // narrow: KE int16 and residual codes u16 (the caller guarantees
 // |K2| <= 16383 from the budget: |x - x1| <= range, see api.cu).
+// K1 (optional): the dense N-D grid component's lattice indices of x1,
+// fused (D1 = grid rank).
 void bucket_means_residuals(umcg_plan* p, const double* xp, DevCtl* ctl, double* x1, void* Kp, bool narrow,
-                            cudaStream_t st);
+                            int32_t* K1, int D1, cudaStream_t st);
 void resid_codes_tiles(umcg_plan* p, const void* Kp, void* codes, bool narrow, const StreamEncScratch& s,
                        cudaStream_t st);
 }  // namespace umcg
