@@ -98,6 +98,24 @@ def dist_env():
     return ws, rank, local
 
 
+def max_over_ranks(ms: float, device=None) -> float:
+    """Max of a per-rank time over all ranks (bench contract: device-timed,
+    max over ranks). Works with nccl (device tensor) and gloo (CPU)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return ms
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_value(ws: int, n: int, ms: float) -> float:
+    """Whole-job GB/s of field data: every replica processes its own n-vertex
+    fp64 field per step (weak scaling, no data-path collective)."""
+    return ws * n * 8 / (ms * 1e-3) / 1e9
+
+
 def setup_config3(lattice: int, grid: int, dev, keep_coords=False):
     import torch
     import paper_2501_06910_b200 as umcg
@@ -300,13 +318,8 @@ def main():
         torch.cuda.synchronize()
     barrier()
     launches = umcg.kernel_launches() - launches0
-    ms = e0.elapsed_time(e1) / args.steps
-    if ws > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = t.item()
-    value = ws * n * 8 / (ms * 1e-3) / 1e9
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, dev)
+    value = replica_value(ws, n, ms)
 
     # e2e through the host-buffer ABI with pinned buffers
     e2e = None
