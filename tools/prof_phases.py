@@ -11,13 +11,15 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2501_06910_b200 as umcg  # noqa: E402
 
 lattice = int(sys.argv[1]) if len(sys.argv) > 1 else 512
-taus = [float(t) for t in sys.argv[2:]] or [1e-4]
+args = sys.argv[2:]
+g_kind = 1 if "--multilinear" in args else 0
+taus = [float(t) for t in args if not t.startswith("--")] or [1e-4]
 xyz, x = umcg.gen_config(3, lattice, 20250113, device="cuda")
-plan = umcg.Plan.build([np.linspace(0.0, 1.0, lattice // 2) for _ in range(3)], xyz)
+plan = umcg.Plan.build([np.linspace(0.0, 1.0, lattice // 2) for _ in range(3)], xyz, keep_coords=bool(g_kind))
 del xyz
 out = torch.empty_like(x)
 for tau in taus:
-    b = umcg.Budget(tau=tau)
+    b = umcg.Budget(tau=tau, g_kind=g_kind)
     ar = torch.empty(int(plan.compress_bound("f")), dtype=torch.uint8, device="cuda")
     for _ in range(2):
         L = plan.compress_into(x, b, ar, "f")
@@ -34,6 +36,6 @@ for tau in taus:
     t2 = time.perf_counter()
     umcg.profile(False)
     d = umcg.profile_dump()
-    print(f"tau={tau:g} archive={L} B  compress wall {1e3*(t1-t0):.3f} ms  decompress wall {1e3*(t2-t1):.3f} ms")
+    print(f"g_kind={g_kind} tau={tau:g} archive={L} B  compress wall {1e3*(t1-t0):.3f} ms  decompress wall {1e3*(t2-t1):.3f} ms")
     for k, v in sorted(d.items(), key=lambda kv: -kv[1][0]):
         print(f"   {k:18s} {v[0]:8.3f} ms  x{v[1]}")
