@@ -265,7 +265,7 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     double* x1 = p->x1.as<double>(n1 ? n1 : 1);
     int32_t* Kp = nullptr;
     if (part) {
-        double* xp = p->scratch_c.as<double>(n ? n : 1);
+        double* xp = p->scratch_c.as<double>(n + 4);  // + padding: 16-byte bulk copies may overrun
         Kp = p->kbuf.as<int32_t>(std::max<uint64_t>(n, n1) + 1);
         partition_values(d_x, x_f32, p, xp, ctl, st);  // + range / finiteness
         budget(BudgetArgs{prm.tau, prm.split_rho, prm.coeff_abs_sum, prm.bound_kind, n}, ctl, st);

@@ -18,6 +18,7 @@
 //   k_resid_codes back to vertex order through dst: q_i = K2_i - K2_{i-1},
 //                 zigzag codes + the RLE tile summary in the same pass.
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 
 #include <cub/block/block_reduce.cuh>
@@ -381,6 +382,209 @@ __global__ void __launch_bounds__(BTP) k_bucket_pipe(const double* __restrict__ 
     cp_wait<0>();
 }
 
+// ---- TMA variant ------------------------------------------------------------
+// Same schedule as k_bucket_pipe, but every bucket arrives through bulk
+// asynchronous copies (cp.async.bulk, completion on an mbarrier): one copy
+// per epoch chunk of xE, one each for the slot map, lnode and the segment
+// offsets, issued by one warp. Chunk e is staged at slot base
+// c0.x + 2e + phase_e (parity of the layout-E position, plan.cu k_lslot) so
+// every copy is a 16-byte aligned superset of the chunk; the sums read xs
+// through the plan's slot map instead of lperm.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+struct TmaStage {
+    double* xs;     // [kBucketCap + 2E + 4] slots
+    uint16_t* ls;   // [kBucketCap + 16]   slot map (node-sorted), phase s0 & 7
+    uint16_t* ln;   // [kBucketCap + 16]   lnode (bucket order),    phase s0 & 7
+    uint2* ch;      // [E + 1]
+};
+
+// (segment offsets go straight to registers: two CTAs fit per SM)
+__host__ __device__ __forceinline__ uint32_t tma_stage_bytes(uint32_t E) {
+    const uint32_t b = (kBucketCap + 2 * E + 4) * 8 + 2 * (kBucketCap + 16) * 2 + (E + 1) * 8;
+    return (b + 127) & ~127u;
+}
+
+__device__ __forceinline__ TmaStage make_tma_stage(unsigned char* p, uint32_t E) {
+    TmaStage S;
+    S.xs = reinterpret_cast<double*>(p);
+    p += (kBucketCap + 2 * E + 4) * 8;
+    S.ls = reinterpret_cast<uint16_t*>(p);
+    p += (kBucketCap + 16) * 2;
+    S.ln = reinterpret_cast<uint16_t*>(p);
+    p += (kBucketCap + 16) * 2;
+    S.ch = reinterpret_cast<uint2*>(p);
+    return S;
+}
+
+// Warp 0 issues the bulk copies of one bucket into S (its chunk table S.ch
+// must already be in shared memory and visible to warp 0).
+__device__ __forceinline__ void tma_issue(const TmaStage& S, uint64_t* bar, const double* __restrict__ xE,
+                                          const uint16_t* __restrict__ lslot, const uint16_t* __restrict__ lnode,
+                                          uint32_t s0, uint32_t m, uint32_t E) {
+    const int lane = threadIdx.x & 31;
+    // bytes of this lane's chunks
+    uint32_t bytes = 0;
+    for (uint32_t e = lane; e < E; e += 32) {
+        const uint2 c0 = S.ch[e], c1 = S.ch[e + 1];
+        const uint32_t cnt = c1.x - c0.x;
+        if (!cnt) continue;
+        const uint32_t glo = c0.y & ~1u, ghi = (c0.y + cnt + 1) & ~1u;
+        bytes += 8 * (ghi - glo);
+    }
+    for (int o = 16; o; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+    const uint32_t a0 = s0 & ~7u, a1 = (s0 + m + 7) & ~7u;  // u16 arrays
+    const uint32_t small = (a1 - a0) * 2 * 2;
+    // prior generic-proxy reads of this stage (ordered by __syncthreads) before
+    // the async-proxy writes
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (lane == 0) {
+        mbar_expect_tx(bar, bytes + small);
+        if (a1 > a0) {
+            bulk_g2s(S.ls, lslot + a0, (a1 - a0) * 2, bar);
+            bulk_g2s(S.ln, lnode + a0, (a1 - a0) * 2, bar);
+        }
+    }
+    __syncwarp();
+    for (uint32_t e = lane; e < E; e += 32) {
+        const uint2 c0 = S.ch[e], c1 = S.ch[e + 1];
+        const uint32_t cnt = c1.x - c0.x;
+        if (!cnt) continue;
+        const uint32_t glo = c0.y & ~1u, ghi = (c0.y + cnt + 1) & ~1u;
+        const uint32_t sbase = c0.x + 2 * e + ((c0.y - c0.x - 2 * e) & 1u);
+        bulk_g2s(S.xs + (sbase - (c0.y & 1u)), xE + glo, 8 * (ghi - glo), bar);
+    }
+}
+
+static_assert(kBucketNodes <= 2 * BTP, "k_bucket_tma keeps <= 2 slots per thread in registers");
+
+template <class KT>
+__global__ void __launch_bounds__(BTP) k_bucket_tma(const double* __restrict__ xE, const uint32_t* __restrict__ bk,
+                                                  uint64_t B, uint32_t E, const uint2* __restrict__ bct,
+                                                  const uint32_t* __restrict__ regular, uint32_t n_regular,
+                                                  const uint16_t* __restrict__ lnode,
+                                                  const uint16_t* __restrict__ lslot,
+                                                  const uint32_t* __restrict__ seg, DevCtl* ctl,
+                                                  double* __restrict__ x1, KT* __restrict__ KE, GridK gk) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[2];
+    double* x1s = reinterpret_cast<double*>(smem);
+    const uint32_t stage_bytes = tma_stage_bytes(E);
+    auto stage = [&](int st) { return make_tma_stage(smem + kBucketNodes * 8 + st * stage_bytes, E); };
+    const uint32_t* bstart = bk;
+    const uint32_t* bnode = bk + B + 1;
+    const double bin = ctl->bin[1], inv = ctl->inv_bin[1], tau = ctl->tau_c[1];
+    const uint32_t G = gridDim.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t k = blockIdx.x;
+    if (k >= n_regular) return;
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    struct Info { uint32_t s0, m, j0, nj; };
+    auto load_info = [&](uint32_t bb) {
+        const uint32_t a0 = __ldg(&bstart[bb]), a1 = __ldg(&bstart[bb + 1]);
+        const uint32_t c0 = __ldg(&bnode[bb]), c1 = __ldg(&bnode[bb + 1]);
+        return Info{a0, a1 - a0, c0, c1 - c0};
+    };
+    uint32_t b = __ldg(&regular[k]);
+    Info cur = load_info(b);
+    if (threadIdx.x <= E) stage(0).ch[threadIdx.x] = __ldg(&bct[b * (uint64_t)(E + 1) + threadIdx.x]);
+    __syncthreads();
+    if (warp == 0) tma_issue(stage(0), &bars[0], xE, lslot, lnode, cur.s0, cur.m, E);
+    uint2 chreg = make_uint2(0, 0);
+    Info nxt{0, 0, 0, 0};
+    uint32_t b2 = 0;
+    if (k + G < n_regular) {
+        const uint32_t bn = __ldg(&regular[k + G]);
+        nxt = load_info(bn);
+        if (threadIdx.x <= E) chreg = __ldg(&bct[bn * (uint64_t)(E + 1) + threadIdx.x]);
+        if (k + 2 * G < n_regular) b2 = __ldg(&regular[k + 2 * G]);
+    }
+    for (uint32_t it = 0; k < n_regular; ++it, k += G) {
+        const int st = it & 1;
+        const bool has_next = k + G < n_regular;
+        if (has_next && threadIdx.x <= E) stage(st ^ 1).ch[threadIdx.x] = chreg;
+        __syncthreads();
+        Info nn{0, 0, 0, 0};
+        uint32_t b3 = 0;
+        if (has_next) {
+            if (warp == 0)
+                tma_issue(stage(st ^ 1), &bars[st ^ 1], xE, lslot, lnode, nxt.s0, nxt.m, E);
+            if (k + 2 * G < n_regular) {
+                nn = load_info(b2);
+                if (threadIdx.x <= E) chreg = __ldg(&bct[b2 * (uint64_t)(E + 1) + threadIdx.x]);
+                if (k + 3 * G < n_regular) b3 = __ldg(&regular[k + 3 * G]);
+            }
+        }
+        const uint32_t s0 = cur.s0, j0 = cur.j0, nj = cur.nj;
+        // segment offsets of this thread's slots (kBucketNodes <= 2 * BTP), in flight during the wait
+        uint32_t sgr[2][2] = {{0, 0}, {0, 0}};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t j = threadIdx.x + h * BTP;
+            if (j < nj) {
+                sgr[h][0] = __ldg(&seg[j0 + j]);
+                sgr[h][1] = __ldg(&seg[j0 + j + 1]);
+            }
+        }
+        mbar_wait(&bars[st], (it >> 1) & 1u);
+        const TmaStage C = stage(st);
+        const uint32_t lo8 = s0 & 7u;
+        // interpolate_to_grid (interp.hpp:58-64): 0.0 + x_a + x_b + ... in ascending vertex order
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t j = threadIdx.x + h * BTP;
+            if (j >= nj) break;
+            const uint32_t k0 = sgr[h][0] - s0, k1 = sgr[h][1] - s0;
+            double sum = 0.0;
+            for (uint32_t q = k0; q < k1; ++q) sum = __dadd_rn(sum, C.xs[C.ls[q + lo8]]);
+            const double v = k1 > k0 ? __ddiv_rn(sum, (double)(k1 - k0)) : 0.0;
+            x1s[j] = v;
+            x1[j0 + j] = v;
+            grid_k(gk, j0 + j, v, ctl);
+        }
+        __syncthreads();
+        // compute_residuals (interp.hpp:161-170) + lattice index (codec.hpp:307-314)
+        for (uint32_t e = warp; e < E; e += BTP / 32) {
+            const uint2 c0 = C.ch[e], c1 = C.ch[e + 1];
+            const uint32_t sbase = c0.x + 2 * e + ((c0.y - c0.x - 2 * e) & 1u);
+            for (uint32_t l = c0.x + lane; l < c1.x; l += 32)
+                KE[c0.y + (l - c0.x)] =
+                    (KT)resid_k(__dsub_rn(C.xs[sbase + (l - c0.x)], x1s[C.ln[l + lo8]]), bin, inv, tau, ctl);
+        }
+        cur = nxt;
+        nxt = nn;
+        b2 = b3;
+        __syncthreads();
+    }
+}
+
 // Vertex order: q_i = K_i - K_{i-1} through dstE (gather inside an epoch
 // window), zigzag codes, RLE tile summary.
 template <class KT, class CT>
@@ -467,7 +671,31 @@ void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double*
         configured = true;
     }
     const bool pipe = E + 1 <= BTP && p->n_regular > 0;
-    if (pipe) {
+    const size_t tma_smem = kBucketNodes * 8 + 2 * (size_t)tma_stage_bytes(E);
+    static bool tma_configured = false;
+    if (!tma_configured) {
+        UMCG_CUDA(cudaFuncSetAttribute(k_bucket_tma<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        UMCG_CUDA(cudaFuncSetAttribute(k_bucket_tma<int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        tma_configured = true;
+    }
+    const bool tma = pipe && tma_smem <= 112 * 1024 && !std::getenv("UMCG_NO_TMA");
+    if (tma) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const unsigned g = (unsigned)std::min<uint64_t>(p->n_regular, (uint64_t)sms * 2);
+        auto launch = [&](auto* ke) {
+            using KT = std::remove_pointer_t<decltype(ke)>;
+            k_bucket_tma<KT><<<g, BTP, tma_smem, st>>>(xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E,
+                                                      p->d_bct.as<uint2>(1), p->d_regular.as<uint32_t>(1),
+                                                      (uint32_t)p->n_regular, p->d_lnode.as<uint16_t>(1),
+                                                      p->d_lslot.as<uint16_t>(1), p->d_seg.as<uint32_t>(1), ctl, x1,
+                                                      ke, gk);
+        };
+        if (narrow) launch(static_cast<int16_t*>(KE));
+        else launch(static_cast<int32_t*>(KE));
+        UMCG_LAUNCHED();
+    } else if (pipe) {
         const size_t smem = kBucketNodes * 8 + 2 * (size_t)pipe_stage_bytes(E);
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);

@@ -174,6 +174,28 @@ __global__ void k_lperm(const uint32_t* __restrict__ perm, uint64_t n, const uin
     lperm[k] = (uint16_t)(dst[v] - bstart[sb[node[v]]]);
 }
 
+// Shared-memory slot of each node-sorted element for the TMA bucket kernel
+// (partition.cu k_bucket_tma): chunk e of a bucket is staged at slot base
+// c0.x + 2e + phase_e, phase_e chosen so the slot and the layout-E position
+// have the same parity (16-byte aligned bulk copies of 8-byte values).
+__global__ void k_lslot(const uint32_t* __restrict__ perm, uint64_t n, const uint32_t* __restrict__ node,
+                        const uint32_t* __restrict__ sb, const uint16_t* __restrict__ lperm,
+                        const uint2* __restrict__ bct, uint64_t E, uint16_t* __restrict__ lslot) {
+    const uint64_t q = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (q >= n) return;
+    const uint32_t b = sb[node[perm[q]]];
+    const uint32_t l = lperm[q];
+    const uint2* c = bct + b * (E + 1);
+    uint32_t lo = 0, hi = (uint32_t)E;  // last chunk with first index <= l
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (c[mid].x <= l) lo = mid; else hi = mid;
+    }
+    const uint32_t e = lo;
+    const uint32_t phase = (c[e].y - c[e].x - 2 * e) & 1u;
+    lslot[q] = (uint16_t)(l + 2 * e + phase);
+}
+
 }  // namespace
 
 uint64_t mapping_digest_host(int mode, uint64_t n, const uint64_t* assign, uint64_t nv, const uint64_t* vis) {
@@ -208,7 +230,7 @@ void plan_build_segments(umcg_plan* p, cudaStream_t st) {
     const uint64_t n = p->n, ns = p->n_slots;
     uint32_t* node = p->d_node.as<uint32_t>(n ? n : 1);
     uint32_t* perm = p->d_perm.as<uint32_t>(n ? n : 1);
-    uint32_t* seg = p->d_seg.as<uint32_t>(ns + 1);
+    uint32_t* seg = p->d_seg.as<uint32_t>(ns + 8);  // + padding for 16-byte bulk copies
     DevBuf tmp_keys, tmp_vals, cnt, scratch;
     uint32_t* keys_out = tmp_keys.as<uint32_t>(n ? n : 1);
     uint32_t* iota = tmp_vals.as<uint32_t>(n ? n : 1);
@@ -288,8 +310,8 @@ void plan_build_buckets(umcg_plan* p, cudaStream_t st) {
     const uint32_t* dbn = dbk + B + 1;
     DevBuf dstbuf;
     uint32_t* dst = dstbuf.as<uint32_t>(n ? n : 1);  // bucket-order position (temporary)
-    uint16_t* lnode = p->d_lnode.as<uint16_t>(n ? n : 1);
-    uint16_t* lperm = p->d_lperm.as<uint16_t>(n ? n : 1);
+    uint16_t* lnode = p->d_lnode.as<uint16_t>(n + 16);  // + padding: 16-byte bulk copies may overrun
+    uint16_t* lperm = p->d_lperm.as<uint16_t>(n + 16);
     if (!n || !B) { UMCG_CUDA(cudaStreamSynchronize(st)); return; }
     DevBuf sbuf, keys, keys_s, iota, L, scratch;
     uint32_t* sb = sbuf.as<uint32_t>(ns);
@@ -337,6 +359,9 @@ void plan_build_buckets(umcg_plan* p, cudaStream_t st) {
     k_epoch_offsets<<<blocks(E), THREADS, 0, st>>>(ec, E, B, p->d_ech.as<uint32_t>(E * (B + 1)));
     UMCG_LAUNCHED();
     k_bucket_chunks<<<blocks(B), THREADS, 0, st>>>(p->d_ech.as<uint32_t>(1), E, B, p->d_bct.as<uint2>(B * (E + 1)));
+    UMCG_LAUNCHED();
+    k_lslot<<<blocks(n), THREADS, 0, st>>>(p->d_perm.as<uint32_t>(1), n, p->d_node.as<uint32_t>(1), sb, lperm,
+                                           p->d_bct.as<uint2>(1), E, p->d_lslot.as<uint16_t>(n + 16));
     UMCG_LAUNCHED();
     UMCG_CUDA(cudaStreamSynchronize(st));
 }

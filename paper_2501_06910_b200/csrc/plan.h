@@ -44,6 +44,7 @@ struct umcg_plan {
     uint64_t n_regular = 0;
     umcg::DevBuf d_lnode;    // u16 [n]    bucket-local slot of bucket-order element
     umcg::DevBuf d_lperm;    // u16 [n]    bucket-local element of node-sorted position
+    umcg::DevBuf d_lslot;    // u16 [n]    shared-memory slot of node-sorted position (TMA staging)
     umcg::DevBuf d_bk;       // u32 [2*(B+1)] bucket start (vertex) and first slot
     // workspace (serialized by mu)
     std::mutex mu;
