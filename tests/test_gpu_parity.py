@@ -663,3 +663,21 @@ def test_lossless_nd_wavefront_matches_reference(cuda, ref, dims):
     out = umcg.decode(pl).cpu().numpy()
     assert np.array_equal(out.view(np.uint64), v.view(np.uint64))
     assert umcg.serial_fallbacks() == fb0
+
+
+@pytest.mark.parametrize("g", [6, 12])
+def test_heavy_slots_match_reference(cuda, ref, oracle, g):
+    """Grids so coarse that single slots hold > 4096 vertices (the bucket
+    kernels' one-slot heavy path, partition.cu k_bucket heavy_only) next to
+    regular buckets: config-1 lattice at 2^20 vertices."""
+    xy, x = umcg.gen_config(1, 1024, 20250101, device="cuda")
+    c = xy.cpu().numpy()
+    axes = [np.linspace(0.0, 1.0, g) for _ in range(2)]
+    idx = [np.clip(np.rint(c[:, d] * (g - 1)), 0, g - 1).astype(np.uint64) for d in range(2)]
+    s = Setup(dim=2, axes=axes, mode=0, assignments=idx[0] * np.uint64(g) + idx[1], coords=c)
+    plan = plan_for(s)
+    counts = np.bincount(s.assignments.astype(np.int64))
+    assert counts.max() > 4096
+    xh = x.cpu().numpy()
+    for tau in (1e-2, 1e-5):
+        _parity_case(plan, s, x, xh, dict(tau=tau), ref, oracle, f"heavy g={g} tau={tau}")
