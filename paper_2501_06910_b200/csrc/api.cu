@@ -252,7 +252,10 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     auto* ctl = p->ctl.as<DevCtl>(1);
     init_ctl(ctl, st);
     // nearest g: partitioned layout (partition.cu); multilinear: gathers
-    const bool part = prm.g_kind == 0 && p->n_buckets > 0 && !m.verbatim;
+    // multilinear g on the partitioned layout: means as for nearest, then the
+    // residuals bucket by bucket (partition.cu k_ml_bucket)
+    const bool ml_part = prm.g_kind == 1 && p->n_buckets > 0 && p->has_coords && p->mode == 0 && !m.verbatim;
+    const bool part = (prm.g_kind == 0 && p->n_buckets > 0 && !m.verbatim) || ml_part;
     // Narrow residual path (int16 lattice indices, u16 codes): a residual is
     // x_i minus the mean of its cluster, so |r| <= range and, for a relative
     // bound, |K2| <= range / bin2 ~ 1 / (2 (1 - rho) tau): <= 16383 keeps every
@@ -270,8 +273,8 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
         partition_values(d_x, x_f32, p, xp, ctl, st);  // + range / finiteness
         budget(BudgetArgs{prm.tau, prm.split_rho, prm.coeff_abs_sum, prm.bound_kind, n}, ctl, st);
         // f: cluster means (interp.hpp:46-93) + residual lattice indices
-        bucket_means_residuals(p, xp, ctl, x1, Kp, narrow, fuse_k1 ? p->scratch_d.as<int32_t>(n1 ? n1 : 1) : nullptr,
-                               p->dim, st);
+        bucket_means_residuals(p, xp, ctl, x1, ml_part ? nullptr : Kp, narrow,
+                               fuse_k1 ? p->scratch_d.as<int32_t>(n1 ? n1 : 1) : nullptr, p->dim, st);
     } else {
         minmax(d_x, x_f32, n, ctl, st);
         budget(BudgetArgs{prm.tau, prm.split_rho, prm.coeff_abs_sum, prm.bound_kind, n}, ctl, st);
@@ -279,6 +282,8 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
         cluster_mean(d_x, x_f32, p->d_perm.as<uint32_t>(1), p->d_seg.as<uint32_t>(1), n1, x1, st);
     }
     if (prm.fill == 1 && p->mode == 0) fill_nearest_visited(p->d_seg.as<uint32_t>(1), n1, p->shape[p->dim - 1], x1, st);
+    if (ml_part && !m.serial[1] && !m.lossless[1])
+        ml_residuals(p, p->scratch_c.as<double>(n + 4), x1, ctl, Kp, narrow, st);
 
     // component specs (grid_codec_spec, pipeline.hpp:96-110)
     const int pred1 = p->mode == 1 ? 1 : 2;
@@ -882,6 +887,11 @@ void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_
     decode_component(p, h2, d_ar + p2, d_out, st);
     if (g_kind == 1 && seed) fail(UMCG_SEED_MODE_UNSUPPORTED, "multilinear back-interpolation needs a dense grid component");
     if (g_kind == 1 && !p->has_coords) fail(UMCG_INVALID_ARGUMENT, "multilinear g needs a plan with vertex coordinates");
+    if (g_kind == 1 && p->n_buckets > 0) {
+        ml_recompose(p, x1, p->dcodes.as<double>(p->n), d_out, st);  // bucket-order g, gathered back
+        UMCG_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
     ResidualSrc rs{};
     rs.node = p->d_node.as<uint32_t>(1);
     rs.x1 = x1;

@@ -25,6 +25,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include "encode_dev.cuh"
+#include "multilinear.cuh"
 #include "plan.h"
 
 namespace umcg {
@@ -154,6 +155,7 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
             grid_k(gk, j0, x1s[0], ctl);
         }
         __syncthreads();
+        if (!KE) return;
         const double mean = x1s[0];
         for (uint32_t e = warp; e < E; e += NW)
             for (uint32_t l = ch[e].x + lane; l < ch[e + 1].x; l += 32) {
@@ -209,6 +211,7 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
         grid_k(gk, j0 + j, v, ctl);
     }
     __syncthreads();
+    if (!KE) return;
     // compute_residuals (interp.hpp:161-170) + lattice index (codec.hpp:307-314)
     {
         uint32_t e = e_first;
@@ -366,7 +369,7 @@ __global__ void __launch_bounds__(BTP) k_bucket_pipe(const double* __restrict__ 
         }
         __syncthreads();
         // compute_residuals (interp.hpp:161-170) + lattice index (codec.hpp:307-314)
-        {
+        if (KE) {
             const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
             for (uint32_t e = warp; e < E; e += BTP / 32) {
                 const uint2 c0 = C.ch[e], c1 = C.ch[e + 1];
@@ -571,7 +574,7 @@ __global__ void __launch_bounds__(BTP) k_bucket_tma(const double* __restrict__ x
         }
         __syncthreads();
         // compute_residuals (interp.hpp:161-170) + lattice index (codec.hpp:307-314)
-        for (uint32_t e = warp; e < E; e += BTP / 32) {
+        for (uint32_t e = warp; KE && e < E; e += BTP / 32) {
             const uint2 c0 = C.ch[e], c1 = C.ch[e + 1];
             const uint32_t sbase = c0.x + 2 * e + ((c0.y - c0.x - 2 * e) & 1u);
             for (uint32_t l = c0.x + lane; l < c1.x; l += 32)
@@ -583,6 +586,58 @@ __global__ void __launch_bounds__(BTP) k_bucket_tma(const double* __restrict__ x
         b2 = b3;
         __syncthreads();
     }
+}
+
+// ---- multilinear g in bucket order -------------------------------------------
+// A bucket is a contiguous range of grid slots, so the cells around its
+// vertices -- and the 2^D corner values multilinear_at reads -- stay within a
+// few grid rows: walking layout E bucket by bucket (one warp per epoch chunk)
+// keeps the corner gathers in L1/L2, where vertex order would scatter them
+// over the whole grid.
+__global__ void k_gather_coords(const double* __restrict__ coords, const uint32_t* __restrict__ srcE, uint64_t n,
+                                int D, double* __restrict__ cE) {
+    const uint64_t p = blockIdx.x * 256ull + threadIdx.x;
+    if (p >= n) return;
+    const uint64_t v = srcE[p];
+    for (int d = 0; d < D; ++d) cE[p * D + d] = coords[v * D + d];
+}
+
+struct MlGrid {
+    const double* axes;
+    const uint64_t* axis_off;
+    uint64_t shape[3];
+    int D;
+};
+
+// MODE 0: KE[p] = lattice(xE[p] - g(p)) (compute_residuals, interp.hpp:161-170)
+// MODE 1: gE[p] = g(p) (back_interpolate for the recomposition, pipeline.hpp:206-208)
+template <int MODE, class KT>
+__global__ void __launch_bounds__(256) k_ml_bucket(const double* __restrict__ xE, const double* __restrict__ cE,
+                                                 const uint2* __restrict__ bct, uint32_t E, MlGrid g,
+                                                 const double* __restrict__ x1, DevCtl* ctl, KT* __restrict__ KE,
+                                                 double* __restrict__ gE) {
+    const uint64_t b = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint2* ch = bct + b * (uint64_t)(E + 1);
+    double bin = 0, inv = 0, tau = 0;
+    if (MODE == 0) { bin = ctl->bin[1]; inv = ctl->inv_bin[1]; tau = ctl->tau_c[1]; }
+    for (uint32_t e = warp; e < E; e += 8) {
+        const uint2 c0 = __ldg(&ch[e]), c1 = __ldg(&ch[e + 1]);
+        for (uint32_t l = c0.x + lane; l < c1.x; l += 32) {
+            const uint64_t p = c0.y + (l - c0.x);
+            const double gv = multilinear_eval(g.axes, g.axis_off, g.shape, g.D, x1, cE + p * g.D);
+            if (MODE == 0) KE[p] = (KT)resid_k(__dsub_rn(__ldcs(&xE[p]), gv), bin, inv, tau, ctl);
+            else gE[p] = gv;
+        }
+    }
+}
+
+// x'_i = approx_i + x2'_i (pipeline.hpp:206-208) with approx gathered from
+// layout E (window-local gather through dstE).
+__global__ void k_add_gathered(const double* __restrict__ gE, const uint32_t* __restrict__ dstE, uint64_t n,
+                               double* __restrict__ io) {
+    const uint64_t i = blockIdx.x * 256ull + threadIdx.x;
+    if (i < n) io[i] = __dadd_rn(__ldg(&gE[dstE[i]]), io[i]);
 }
 
 // Vertex order: q_i = K_i - K_{i-1} through dstE (gather inside an epoch
@@ -741,6 +796,54 @@ void resid_codes_tiles(umcg_plan* p, const void* KE, void* codes, bool narrow, c
     else
         k_resid_codes<int32_t, uint32_t><<<(unsigned)T, ENC_THREADS, 0, st>>>(
             p->d_dstE.as<uint32_t>(1), static_cast<const int32_t*>(KE), p->n, static_cast<uint32_t*>(codes), s.sums);
+    UMCG_LAUNCHED();
+}
+
+static const double* coords_e(umcg_plan* p, cudaStream_t st) {
+    if (!p->has_coordsE) {
+        double* cE = p->d_coordsE.as<double>(p->n * p->dim);
+        k_gather_coords<<<(unsigned)cdiv(p->n, 256), 256, 0, st>>>(p->d_coords.as<double>(1), p->d_srcE.as<uint32_t>(1),
+                                                                   p->n, p->dim, cE);
+        UMCG_LAUNCHED();
+        p->has_coordsE = true;
+    }
+    return p->d_coordsE.as<double>(1);
+}
+
+static MlGrid ml_grid(umcg_plan* p) {
+    MlGrid g{};
+    g.axes = p->d_axes.as<double>(1);
+    g.axis_off = p->d_axis_off.as<uint64_t>(1);
+    for (int d = 0; d < 3; ++d) g.shape[d] = p->shape[d];
+    g.D = p->dim;
+    return g;
+}
+
+void ml_residuals(umcg_plan* p, const double* xE, const double* x1, DevCtl* ctl, void* KE, bool narrow,
+                  cudaStream_t st) {
+    if (!p->n_buckets) return;
+    ProfScope ps_("k_ml_resid", st);
+    const double* cE = coords_e(p, st);
+    const uint32_t E = (uint32_t)p->n_epochs;
+    if (narrow)
+        k_ml_bucket<0, int16_t><<<(unsigned)p->n_buckets, 256, 0, st>>>(
+            xE, cE, p->d_bct.as<uint2>(1), E, ml_grid(p), x1, ctl, static_cast<int16_t*>(KE), nullptr);
+    else
+        k_ml_bucket<0, int32_t><<<(unsigned)p->n_buckets, 256, 0, st>>>(
+            xE, cE, p->d_bct.as<uint2>(1), E, ml_grid(p), x1, ctl, static_cast<int32_t*>(KE), nullptr);
+    UMCG_LAUNCHED();
+}
+
+void ml_recompose(umcg_plan* p, const double* x1, double* gE, double* d_out, cudaStream_t st) {
+    if (!p->n) return;
+    ProfScope ps_("k_ml_recompose", st);
+    const double* cE = coords_e(p, st);
+    if (p->n_buckets) {
+        k_ml_bucket<1, int32_t><<<(unsigned)p->n_buckets, 256, 0, st>>>(
+            nullptr, cE, p->d_bct.as<uint2>(1), (uint32_t)p->n_epochs, ml_grid(p), x1, nullptr, nullptr, gE);
+        UMCG_LAUNCHED();
+    }
+    k_add_gathered<<<(unsigned)cdiv(p->n, 256), 256, 0, st>>>(gE, p->d_dstE.as<uint32_t>(1), p->n, d_out);
     UMCG_LAUNCHED();
 }
 

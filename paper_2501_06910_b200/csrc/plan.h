@@ -27,6 +27,8 @@ struct umcg_plan {
     umcg::DevBuf d_axis_off; // u64 [dim]
     umcg::DevBuf d_coords;   // f64 [n*dim] (multilinear g), optional
     bool has_coords = false;
+    umcg::DevBuf d_coordsE;  // f64 [n*dim] coordinates in layout-E order (built on first multilinear use)
+    bool has_coordsE = false;
     // bucketed layout for the partitioned compress path (partition.cu):
     // buckets are contiguous slot ranges holding <= kBucketCap vertices
     // (a heavier slot gets a bucket of its own).
@@ -99,4 +101,9 @@ void bucket_means_residuals(umcg_plan* p, const double* xp, DevCtl* ctl, double*
                             int32_t* K1, int D1, cudaStream_t st);
 void resid_codes_tiles(umcg_plan* p, const void* Kp, void* codes, bool narrow, const StreamEncScratch& s,
                        cudaStream_t st);
+// Multilinear g in bucket order (layout E): residual lattice indices KE
+// (compress) and the recomposition x' = g + x2' (decompress, gE [n] scratch).
+void ml_residuals(umcg_plan* p, const double* xE, const double* x1, DevCtl* ctl, void* KE, bool narrow,
+                  cudaStream_t st);
+void ml_recompose(umcg_plan* p, const double* x1, double* gE, double* d_out, cudaStream_t st);
 }  // namespace umcg
