@@ -301,6 +301,8 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     rs.coords = p->has_coords ? p->d_coords.as<double>(1) : nullptr;
     rs.axes = p->d_axes.as<double>(1);
     rs.axis_off = p->d_axis_off.as<uint64_t>(1);
+    rs.inv_cell = p->d_inv_cell.as<double>(1);
+    for (int d = 0; d < 3; ++d) rs.scale[d] = p->axis_scale[d];
     rs.D = p->dim;
     for (int d = 0; d < 3; ++d) rs.shape[d] = p->shape[d];
 
@@ -899,6 +901,8 @@ void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_
     rs.coords = p->has_coords ? p->d_coords.as<double>(1) : nullptr;
     rs.axes = p->d_axes.as<double>(1);
     rs.axis_off = p->d_axis_off.as<uint64_t>(1);
+    rs.inv_cell = p->d_inv_cell.as<double>(1);
+    for (int d = 0; d < 3; ++d) rs.scale[d] = p->axis_scale[d];
     rs.D = p->dim;
     for (int d = 0; d < 3; ++d) rs.shape[d] = p->shape[d];
     recompose(rs, p->n, d_out, st);

@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(THREADS) k_lossless(const double* __restrict__
 // detail::multilinear_at (interp.hpp:97-132), same operation order.
 // multilinear_at / axis_upper_bound: multilinear.cuh
 __device__ __forceinline__ double multilinear_at(const ResidualSrc& s, const double* __restrict__ p) {
-    return multilinear_eval(s.axes, s.axis_off, s.shape, s.D, s.x1, p);
+    return multilinear_eval(s.axes, s.axis_off, s.shape, s.D, s.x1, p, s.inv_cell, s.scale);
 }
 
 __device__ __forceinline__ double load_x(const ResidualSrc& s, uint64_t i) {

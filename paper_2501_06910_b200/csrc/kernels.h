@@ -92,6 +92,8 @@ struct ResidualSrc {
     const double* coords; // [n*D] (multilinear)
     const double* axes;   // concatenated axes (multilinear)
     const uint64_t* axis_off;  // [D] offsets into axes
+    const double* inv_cell;    // RN(1 / cell width), like axes (multilinear)
+    double scale[3];           // index-guess scale per axis (multilinear)
     uint64_t shape[3];
     int D;
 };

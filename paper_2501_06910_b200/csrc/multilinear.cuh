@@ -7,14 +7,15 @@
 
 namespace umcg {
 
-// std::upper_bound(axis, axis + n, p): guessed from the end points (exact
-// for uniform axes up to rounding), then corrected against the actual axis
-// values -- same result as the binary search, which remains the fallback
-// (outside the axis range, NaN, or a strongly graded axis).
-__device__ __forceinline__ uint64_t axis_upper_bound(const double* __restrict__ axis, uint64_t n, double p) {
+// std::upper_bound(axis, axis + n, p): guessed from the end points (any
+// guess is fine), then corrected against the actual axis values -- same
+// result as the binary search, which remains the fallback (outside the axis
+// range, NaN, or a strongly graded axis).
+__device__ __forceinline__ uint64_t axis_upper_bound(const double* __restrict__ axis, uint64_t n, double p,
+                                                    double scale) {
     const double a0 = axis[0], a1 = axis[n - 1];
     if (p >= a0 && p < a1) {
-        const double f = (p - a0) / (a1 - a0) * (double)(n - 1);
+        const double f = (p - a0) * scale;  // (n - 1) / (a1 - a0): only a guess
         uint64_t g = (uint64_t)f + 1;
         if (g > n - 1) g = n - 1;
         int steps = 0;
@@ -31,39 +32,75 @@ __device__ __forceinline__ uint64_t axis_upper_bound(const double* __restrict__ 
     return lo;
 }
 
-__device__ __forceinline__ double multilinear_eval(const double* __restrict__ axes, const uint64_t* __restrict__ axis_off,
-                                                  const uint64_t* shape, int D, const double* __restrict__ x1,
-                                                  const double* __restrict__ p) {
-    uint64_t lo_idx[3] = {0, 0, 0};
-    double t[3] = {0, 0, 0};
-    for (int d = 0; d < D; ++d) {
+// Corner weights are w = ((1.0 * a_0) * a_1) * a_2 with a_d = t_d or 1 - t_d
+// (interp.hpp:120-125, dimension 0 = lowest corner bit); 1.0 * a_0 == a_0, so
+// the partial products a_0 * a_1 are shared between corners without changing
+// any rounding. Corners whose weight is 0 are skipped exactly as in the
+// reference.
+//
+// The cell fraction (p - a_l) / (a_h - a_l) is the correctly rounded quotient
+// computed from inv = RN(1 / (a_h - a_l)) (precomputed per cell): q0 =
+// RN(num * inv), r = num - q0 * den exactly (fma), q = RN(q0 + r * inv) --
+// Markstein's theorem gives q = RN(num / den) for normal operands; others
+// take the IEEE divide.
+__device__ __forceinline__ double multilinear_eval(const double* __restrict__ axes,
+                                                  const uint64_t* __restrict__ axis_off, const uint64_t* shape,
+                                                  int D, const double* __restrict__ x1,
+                                                  const double* __restrict__ p, const double* __restrict__ inv_cell,
+                                                  const double* scale) {
+    double t[3] = {0, 0, 0}, om[3] = {1, 1, 1};
+    uint64_t base = 0, step[3] = {0, 0, 0};
+    uint64_t stride = 1;
+    for (int d = D - 1; d >= 0; --d) {
         const uint64_t n = shape[d];
-        const double* axis = axes + axis_off[d];
-        if (n == 1) { lo_idx[d] = 0; t[d] = 0.0; continue; }
-        uint64_t h = axis_upper_bound(axis, n, p[d]);
-        h = h < 1 ? 1 : h;
-        if (h > n - 1) h = n - 1;
-        const uint64_t l = h - 1;
-        const double w = __ddiv_rn(__dsub_rn(p[d], axis[l]), __dsub_rn(axis[h], axis[l]));
-        lo_idx[d] = l;
-        t[d] = (w < 0.0) ? 0.0 : ((1.0 < w) ? 1.0 : w);  // std::clamp
+        uint64_t l = 0;
+        double td = 0.0;
+        if (n > 1) {
+            const double* axis = axes + axis_off[d];
+            uint64_t h = axis_upper_bound(axis, n, p[d], scale[d]);
+            h = h < 1 ? 1 : h;
+            if (h > n - 1) h = n - 1;
+            l = h - 1;
+            const double num = __dsub_rn(p[d], axis[l]), den = __dsub_rn(axis[h], axis[l]);
+            const double y = inv_cell[axis_off[d] + l];
+            const double q0 = __dmul_rn(num, y);
+            double w = __fma_rn(__fma_rn(-q0, den, num), y, q0);
+            if (!(fabs(num) > 0x1p-900) || !(fabs(num) < 0x1p900)) w = __ddiv_rn(num, den);
+            td = (w < 0.0) ? 0.0 : ((1.0 < w) ? 1.0 : w);  // std::clamp
+            step[d] = stride;  // l + 1 <= n - 1 always here
+        }
+        t[d] = td;
+        om[d] = __dsub_rn(1.0, td);
+        base += l * stride;
+        stride *= n;
     }
     double acc = 0.0;
-    for (unsigned corner = 0; corner < (1u << D); ++corner) {
-        double w = 1.0;
-        uint64_t lin = 0;
-        for (int d = 0; d < D; ++d) {
-            const bool high = (corner >> d) & 1u;
-            w = __dmul_rn(w, high ? t[d] : __dsub_rn(1.0, t[d]));
-            const uint64_t n = shape[d];
-            uint64_t idx = lo_idx[d] + (high ? 1 : 0);
-            if (idx >= n) idx = n - 1;
-            lin = lin * n + idx;
+    if (D == 2) {
+#pragma unroll
+        for (unsigned corner = 0; corner < 4; ++corner) {
+            const bool h0 = corner & 1u, h1 = corner & 2u;
+            const double w = __dmul_rn(h0 ? t[0] : om[0], h1 ? t[1] : om[1]);
+            const uint64_t lin = base + (h0 ? step[0] : 0) + (h1 ? step[1] : 0);
+            if (w != 0.0) acc = __dadd_rn(acc, __dmul_rn(w, x1[lin]));
         }
-        if (w != 0.0) acc = __dadd_rn(acc, __dmul_rn(w, x1[lin]));
+        return acc;
+    }
+    double p01[4];
+#pragma unroll
+    for (unsigned c = 0; c < 4; ++c) p01[c] = __dmul_rn((c & 1u) ? t[0] : om[0], (c & 2u) ? t[1] : om[1]);
+    double v[8];
+#pragma unroll
+    for (unsigned corner = 0; corner < 8; ++corner) {
+        const uint64_t lin = base + ((corner & 1u) ? step[0] : 0) + ((corner & 2u) ? step[1] : 0) +
+                             ((corner & 4u) ? step[2] : 0);
+        v[corner] = x1[lin];
+    }
+#pragma unroll
+    for (unsigned corner = 0; corner < 8; ++corner) {
+        const double w = __dmul_rn(p01[corner & 3u], (corner & 4u) ? t[2] : om[2]);
+        if (w != 0.0) acc = __dadd_rn(acc, __dmul_rn(w, v[corner]));
     }
     return acc;
 }
-
 
 }  // namespace umcg

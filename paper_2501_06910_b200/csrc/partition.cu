@@ -599,12 +599,14 @@ __global__ void k_gather_coords(const double* __restrict__ coords, const uint32_
     const uint64_t p = blockIdx.x * 256ull + threadIdx.x;
     if (p >= n) return;
     const uint64_t v = srcE[p];
-    for (int d = 0; d < D; ++d) cE[p * D + d] = coords[v * D + d];
+    for (int d = 0; d < D; ++d) cE[d * n + p] = coords[v * D + d];  // structure of arrays: coalesced per axis
 }
 
 struct MlGrid {
     const double* axes;
     const uint64_t* axis_off;
+    const double* inv_cell;
+    double scale[3];
     uint64_t shape[3];
     int D;
 };
@@ -613,7 +615,7 @@ struct MlGrid {
 // MODE 1: gE[p] = g(p) (back_interpolate for the recomposition, pipeline.hpp:206-208)
 template <int MODE, class KT>
 __global__ void __launch_bounds__(256) k_ml_bucket(const double* __restrict__ xE, const double* __restrict__ cE,
-                                                 const uint2* __restrict__ bct, uint32_t E, MlGrid g,
+                                                 uint64_t n, const uint2* __restrict__ bct, uint32_t E, MlGrid g,
                                                  const double* __restrict__ x1, DevCtl* ctl, KT* __restrict__ KE,
                                                  double* __restrict__ gE) {
     const uint64_t b = blockIdx.x;
@@ -625,7 +627,9 @@ __global__ void __launch_bounds__(256) k_ml_bucket(const double* __restrict__ xE
         const uint2 c0 = __ldg(&ch[e]), c1 = __ldg(&ch[e + 1]);
         for (uint32_t l = c0.x + lane; l < c1.x; l += 32) {
             const uint64_t p = c0.y + (l - c0.x);
-            const double gv = multilinear_eval(g.axes, g.axis_off, g.shape, g.D, x1, cE + p * g.D);
+            double pc[3] = {0, 0, 0};
+            for (int d = 0; d < g.D; ++d) pc[d] = __ldcs(&cE[d * n + p]);
+            const double gv = multilinear_eval(g.axes, g.axis_off, g.shape, g.D, x1, pc, g.inv_cell, g.scale);
             if (MODE == 0) KE[p] = (KT)resid_k(__dsub_rn(__ldcs(&xE[p]), gv), bin, inv, tau, ctl);
             else gE[p] = gv;
         }
@@ -814,7 +818,11 @@ static MlGrid ml_grid(umcg_plan* p) {
     MlGrid g{};
     g.axes = p->d_axes.as<double>(1);
     g.axis_off = p->d_axis_off.as<uint64_t>(1);
-    for (int d = 0; d < 3; ++d) g.shape[d] = p->shape[d];
+    g.inv_cell = p->d_inv_cell.as<double>(1);
+    for (int d = 0; d < 3; ++d) {
+        g.shape[d] = p->shape[d];
+        g.scale[d] = p->axis_scale[d];
+    }
     g.D = p->dim;
     return g;
 }
@@ -827,10 +835,10 @@ void ml_residuals(umcg_plan* p, const double* xE, const double* x1, DevCtl* ctl,
     const uint32_t E = (uint32_t)p->n_epochs;
     if (narrow)
         k_ml_bucket<0, int16_t><<<(unsigned)p->n_buckets, 256, 0, st>>>(
-            xE, cE, p->d_bct.as<uint2>(1), E, ml_grid(p), x1, ctl, static_cast<int16_t*>(KE), nullptr);
+            xE, cE, p->n, p->d_bct.as<uint2>(1), E, ml_grid(p), x1, ctl, static_cast<int16_t*>(KE), nullptr);
     else
         k_ml_bucket<0, int32_t><<<(unsigned)p->n_buckets, 256, 0, st>>>(
-            xE, cE, p->d_bct.as<uint2>(1), E, ml_grid(p), x1, ctl, static_cast<int32_t*>(KE), nullptr);
+            xE, cE, p->n, p->d_bct.as<uint2>(1), E, ml_grid(p), x1, ctl, static_cast<int32_t*>(KE), nullptr);
     UMCG_LAUNCHED();
 }
 
@@ -840,7 +848,7 @@ void ml_recompose(umcg_plan* p, const double* x1, double* gE, double* d_out, cud
     const double* cE = coords_e(p, st);
     if (p->n_buckets) {
         k_ml_bucket<1, int32_t><<<(unsigned)p->n_buckets, 256, 0, st>>>(
-            nullptr, cE, p->d_bct.as<uint2>(1), (uint32_t)p->n_epochs, ml_grid(p), x1, nullptr, nullptr, gE);
+            nullptr, cE, p->n, p->d_bct.as<uint2>(1), (uint32_t)p->n_epochs, ml_grid(p), x1, nullptr, nullptr, gE);
         UMCG_LAUNCHED();
     }
     k_add_gathered<<<(unsigned)cdiv(p->n, 256), 256, 0, st>>>(gE, p->d_dstE.as<uint32_t>(1), p->n, d_out);

@@ -390,6 +390,17 @@ static void upload_grid(umcg_plan* p, const umcg_grid_desc* g) {
     for (int d = g->dim; d < 3; ++d) p->shape[d] = 1;
     double* da = p->d_axes.as<double>(p->axes.size());
     UMCG_CUDA(cudaMemcpy(da, p->axes.data(), p->axes.size() * 8, cudaMemcpyHostToDevice));
+    // multilinear helpers: RN(1 / (a[l+1] - a[l])) per cell (correctly rounded
+    // division by one fma correction, multilinear.cuh) and an index-guess scale
+    std::vector<double> inv(p->axes.size(), 0.0);
+    for (int d = 0; d < g->dim; ++d) {
+        const double* a = p->axes.data() + p->axis_off[d];
+        const uint64_t m = p->shape[d];
+        for (uint64_t l = 0; l + 1 < m; ++l) inv[p->axis_off[d] + l] = 1.0 / (a[l + 1] - a[l]);
+        p->axis_scale[d] = m > 1 ? (double)(m - 1) / (a[m - 1] - a[0]) : 0.0;
+    }
+    double* dinv = p->d_inv_cell.as<double>(inv.size());
+    UMCG_CUDA(cudaMemcpy(dinv, inv.data(), inv.size() * 8, cudaMemcpyHostToDevice));
     uint64_t* doff = p->d_axis_off.as<uint64_t>(3);
     UMCG_CUDA(cudaMemcpy(doff, p->axis_off.data(), p->dim * 8, cudaMemcpyHostToDevice));
 }

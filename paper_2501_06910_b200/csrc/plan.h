@@ -25,6 +25,8 @@ struct umcg_plan {
     umcg::DevBuf d_visited;  // u64 [n_visited] visited linear node ids (seed mode)
     umcg::DevBuf d_axes;     // f64 concatenated axes
     umcg::DevBuf d_axis_off; // u64 [dim]
+    umcg::DevBuf d_inv_cell; // f64, like d_axes: RN(1 / cell width) per axis cell
+    double axis_scale[3] = {0, 0, 0};  // (m - 1) / (a[m-1] - a[0]): index guess
     umcg::DevBuf d_coords;   // f64 [n*dim] (multilinear g), optional
     bool has_coords = false;
     umcg::DevBuf d_coordsE;  // f64 [n*dim] coordinates in layout-E order (built on first multilinear use)

@@ -490,11 +490,12 @@ def test_pipeline_verbatim_codec_matches_reference(cuda, ref, oracle):
     params, cases = load_cases()
     for k, s, x, archives in cases[:4]:
         plan = plan_for(s)
-        for fill in (0, 1) if s.mode == 0 else (0,):
-            b = umcg.Budget(tau=1e-3, codec_id=1, fill=fill)
+        for fill, g in ((0, 0), (1, 0), (0, 1), (1, 1)) if s.mode == 0 else ((0, 0),):
+            # verbatim residual bytes pin g itself bit for bit (multilinear included)
+            b = umcg.Budget(tau=1e-3, codec_id=1, fill=fill, g_kind=g)
             got = plan.compress(dev(x), b, name="v")
-            want = ref.compress(s, x, name="v", tau=1e-3, codec_id=1, fill=fill)
-            assert got == want, (k, fill)
+            want = ref.compress(s, x, name="v", tau=1e-3, codec_id=1, fill=fill, g_kind=g)
+            assert got == want, (k, fill, g)
             out = plan.decompress(got).cpu().numpy()
             assert np.array_equal(out.view(np.uint64), ref.decompress(s, want).view(np.uint64))
 
