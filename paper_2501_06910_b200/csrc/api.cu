@@ -319,6 +319,14 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     }
     uint64_t* esc_idx[2] = {nullptr, nullptr};
     double* esc_val[2] = {nullptr, nullptr};
+    // Common case: the grid component's chain (codes, stream plan, write) runs
+    // on a side stream beside the residual's; they share only the layout step.
+    const bool overlap = part && !m.serial[0] && !m.serial[1] && !m.lossless[0] && !m.lossless[1];
+    cudaStream_t sg = st;
+    if (overlap) {
+        sg = p->side.get();
+        p->side.link(st, sg, 0);
+    }
     // grid component
     if (m.serial[0]) {
         DevCtl hc = read_ctl(p, ctl, st);  // need the shaved tau on the host for the serial kernel
@@ -327,10 +335,10 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
         serial_encode(x1, n1, pred1, sh1, hc.tau_c[0], static_cast<uint64_t*>(codes[0]), esc_val[0] + n1,
                       esc_idx[0], esc_val[0], ctl, 0, st);
     } else if (m.lossless[0]) {
-        codes_lossless_values(x1, n1, pred1, sh1, static_cast<uint64_t*>(codes[0]), st);
+        codes_lossless_values(x1, n1, pred1, sh1, static_cast<uint64_t*>(codes[0]), sg);
     } else {
         int32_t* kb = p->scratch_d.as<int32_t>(n1 ? n1 : 1);
-        codes_lossy_values(x1, n1, pred1, sh1, ctl, 0, static_cast<uint32_t*>(codes[0]), kb, st, fuse_k1);
+        codes_lossy_values(x1, n1, pred1, sh1, ctl, 0, static_cast<uint32_t*>(codes[0]), kb, sg, fuse_k1);
     }
     // residual component
     if (m.serial[1]) {
@@ -361,13 +369,23 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
 
     // stream structure, layout, headers, bytes
     for (int c = 0; c < 2; ++c) {
-        if (c == 1 && fused_resid) stream_plan_from_sums(ncode[c], es[c], ctl, c, st);
-        else if (wide[c]) stream_plan_u64(static_cast<uint64_t*>(codes[c]), ncode[c], es[c], ctl, c, st);
-        else stream_plan_u32(static_cast<uint32_t*>(codes[c]), ncode[c], es[c], ctl, c, st);
+        cudaStream_t sc = c == 0 ? sg : st;
+        if (c == 1 && fused_resid) stream_plan_from_sums(ncode[c], es[c], ctl, c, sc);
+        else if (wide[c]) stream_plan_u64(static_cast<uint64_t*>(codes[c]), ncode[c], es[c], ctl, c, sc);
+        else stream_plan_u32(static_cast<uint32_t*>(codes[c]), ncode[c], es[c], ctl, c, sc);
     }
+    if (overlap) p->side.link(sg, st, 1);  // layout needs both stream lengths
     const HdrArgs h = archive_hdr(p, prm, name, 0, pred1, D1, dims1, st);
     k_layout_archive<<<1, 32, 0, st>>>(h, ctl, d_ar);
     UMCG_LAUNCHED();
+    if (overlap) {
+        p->side.link(st, sg, 2);
+        stream_write_u32(static_cast<uint32_t*>(codes[0]), ncode[0], es[0], ctl, 0, d_ar, true, sg);
+        if (narrow) stream_write_u16(static_cast<uint16_t*>(codes[1]), ncode[1], es[1], ctl, 1, d_ar, true, st);
+        else stream_write_u32(static_cast<uint32_t*>(codes[1]), ncode[1], es[1], ctl, 1, d_ar, true, st);
+        p->side.link(sg, st, 3);
+        return read_ctl(p, ctl, st);
+    }
     for (int c = 0; c < 2; ++c) {
         if (m.serial[c]) {
             // escapes count is on the device; launch for the worst case, kernel bounds itself

@@ -427,6 +427,29 @@ private:
     size_t cap_ = 0;
 };
 
+// A side stream + fork/join events, created on first use (non-blocking, so a
+// caller on the legacy default stream is not serialized against it).
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    ~SideStream() {
+        for (auto& e : ev) if (e) cudaEventDestroy(e);
+        if (s) cudaStreamDestroy(s);
+    }
+    cudaStream_t get() {
+        if (!s) {
+            UMCG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            for (auto& e : ev) UMCG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        return s;
+    }
+    // `to` waits for all work queued so far on `from` (event slot k)
+    void link(cudaStream_t from, cudaStream_t to, int k) {
+        UMCG_CUDA(cudaEventRecord(ev[k], from));
+        UMCG_CUDA(cudaStreamWaitEvent(to, ev[k], 0));
+    }
+};
+
 struct PinnedBuf {
     void* p = nullptr;
     size_t cap = 0;

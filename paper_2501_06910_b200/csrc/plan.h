@@ -55,6 +55,7 @@ struct umcg_plan {
     umcg::DevBuf ctl, x1, codes1, codes2, kbuf, enc1, enc2, hdr, scratch_a, scratch_b, scratch_c,
         scratch_d, dx1, dcodes;
     umcg::StreamDecScratch dec, dec2;
+    umcg::SideStream side;  // grid component's chain runs beside the residual's
     umcg::PinnedBuf hctl, hstage;
 };
 
