@@ -748,12 +748,17 @@ static bool fast_decompress(umcg_plan* p, const uint8_t* d_ar, uint64_t p1, cons
     UMCG_CUDA(cudaMemsetAsync(c, 0, 5 * sizeof(DevCtl), st));
     const uint8_t* s1b = d_ar + p1 + h1.stream_off;
     const uint8_t* s2b = d_ar + p2 + h2.stream_off;
+    // the residual stream's probe, tile aggregates and scan run on the side
+    // stream while the grid component decodes
+    cudaStream_t ss = p->side.get();
+    p->side.link(st, ss, 0);
     const Token* t1 = stream_probe(s1b, h1.stream_len, p->dec, &c[0], st);
-    const Token* t2 = stream_probe(s2b, h2.stream_len, p->dec2, &c[2], st);
+    const Token* t2 = stream_probe(s2b, h2.stream_len, p->dec2, &c[2], ss);
     const DecSrc src1{nullptr, 0, s1b, t1, &c[0]};
     const DecSrc src2{nullptr, 0, s2b, t2, &c[2]};
     void* st1 = p->scratch_c.reserve(dec_status_bytes(h1.stream_len));
     void* st2 = p->scratch_d.reserve(dec_status_bytes(h2.stream_len));
+    dec_prepare(src2, dec_tiles(h2.stream_len), st2, &c[3], ss);
     int64_t* P = p->kbuf.as<int64_t>(2 * n1);
     int32_t* K1 = p->codes1.as<int32_t>(n1);
     dec_fused(DEC_P64, src1, dec_tiles(h1.stream_len), n1, st1, &c[1], nullptr, nullptr, 0.0, bin1, nullptr, P, st);
@@ -761,8 +766,9 @@ static bool fast_decompress(umcg_plan* p, const uint8_t* d_ar, uint64_t p1, cons
     int16_t* K16 = p->dx1.as<int16_t>(n1 + 2);
     nd_from_prefix(P, n1, pred1 == 2 ? make_shape(h1.D, h1.dims) : make_shape(1, flat), P + n1, K1, K16, &c[1],
                    st);
+    p->side.link(ss, st, 1);
     dec_fused(DEC_RECOMPOSE, src2, dec_tiles(h2.stream_len), n, st2, &c[3], p->d_node.as<uint32_t>(1), K1, bin1,
-              bin2, d_out, nullptr, st, &c[1], K16);
+              bin2, d_out, nullptr, st, &c[1], K16, true);
     auto* verdict = reinterpret_cast<unsigned long long*>(&c[4].aux[0]);
     k_fast_verdict<<<1, 1, 0, st>>>(c, src1, src2, n1, n, k_lim(pred1, pred1 == 2 ? h1.D : 1), k_lim(1, 1),
                                     verdict);

@@ -492,9 +492,7 @@ __global__ void k_k32_to_f64(const int32_t* __restrict__ K, uint64_t n, double b
 size_t dec_status_bytes(uint64_t ulen) { return (cdiv(ulen, RTILE) + 1) * sizeof(CS); }
 uint64_t dec_tiles(uint64_t ulen_bound) { return cdiv(ulen_bound, RTILE); }
 
-void dec_fused(int mode, const DecSrc& src, uint64_t T, uint64_t n, void* status, DevCtl* ctl,
-               const uint32_t* node, const int32_t* K1, double bin1, double bin, double* out, int64_t* P64,
-               cudaStream_t st, const DevCtl* kctl, const int16_t* K16) {
+void dec_prepare(const DecSrc& src, uint64_t T, void* status, DevCtl* ctl, cudaStream_t st) {
     auto* aggs = static_cast<CS*>(status);
     if (T) {
         ProfScope ps_a("k_dec_agg", st);
@@ -503,6 +501,13 @@ void dec_fused(int mode, const DecSrc& src, uint64_t T, uint64_t n, void* status
     }
     k_scan_cs<<<1, 1024, 0, st>>>(src, aggs, ctl);
     UMCG_LAUNCHED();
+}
+
+void dec_fused(int mode, const DecSrc& src, uint64_t T, uint64_t n, void* status, DevCtl* ctl,
+               const uint32_t* node, const int32_t* K1, double bin1, double bin, double* out, int64_t* P64,
+               cudaStream_t st, const DevCtl* kctl, const int16_t* K16, bool prepared) {
+    auto* aggs = static_cast<CS*>(status);
+    if (!prepared) dec_prepare(src, T, status, ctl, st);
     if (!T) return;
     ProfScope ps_o(mode == DEC_P64 ? "k_dec_out_grid" : "k_dec_out", st);
     if (mode == DEC_P64)

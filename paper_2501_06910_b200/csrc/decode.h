@@ -51,9 +51,12 @@ size_t dec_status_bytes(uint64_t ulen);
 uint64_t dec_tiles(uint64_t ulen_bound);
 // DEC_RECOMPOSE with kctl/K16: gathers from K16 (int16 copy of K1) when
 // kctl->max_abs_k[0] < 2^15 on the device.
+// prepared: dec_prepare (tile aggregates + their scan) already ran for this
+// source/status/ctl, possibly on another stream ordered before st.
 void dec_fused(int mode, const DecSrc& src, uint64_t t_tiles, uint64_t n, void* status, DevCtl* ctl,
                const uint32_t* node, const int32_t* K1, double bin1, double bin, double* out, int64_t* P64,
-               cudaStream_t st, const DevCtl* kctl = nullptr, const int16_t* K16 = nullptr);
+               cudaStream_t st, const DevCtl* kctl = nullptr, const int16_t* K16 = nullptr, bool prepared = false);
+void dec_prepare(const DecSrc& src, uint64_t t_tiles, void* status, DevCtl* ctl, cudaStream_t st);
 // N-D inclusive prefix from the plain 1-D prefix P of row-major codes:
 // row differencing (fastest axis) + scans along the other axes -> int32 K,
 // max|K| -> ctl->max_abs_k[0]. Kw is int64 scratch [n] (unused when D == 1).
