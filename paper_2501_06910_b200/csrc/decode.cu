@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(RT) k_dec_out(const DecSrc src, uint64_t n,
     if (MODE == DEC_P64) return;
     __syncthreads();
     const uint32_t cnt = (uint32_t)tot.cnt;
-    constexpr int UN = 8;  // independent gathers in flight per thread
+    constexpr int UN = 12;  // independent gathers in flight per thread
     const uint64_t pf = l2_evict_first(), pl = l2_evict_last();
     for (uint32_t e0 = 0; e0 < cnt; e0 += RT * UN) {
         uint32_t nd[UN];
