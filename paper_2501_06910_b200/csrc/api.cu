@@ -152,11 +152,6 @@ __global__ void k_read_escapes(const uint8_t* __restrict__ p, uint64_t ne, uint6
     val[e] = __longlong_as_double((long long)v);
 }
 
-__global__ void k_widen(const float* __restrict__ x, uint64_t n, double* __restrict__ y) {
-    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
-    if (i < n) y[i] = (double)x[i];
-}
-
 inline unsigned blocks(uint64_t n) { return (unsigned)cdiv(n, THREADS); }
 
 uint64_t stream_bound(uint64_t n) { return 10 * n + 3 * (n / 8 + 2) * 11 + 16; }

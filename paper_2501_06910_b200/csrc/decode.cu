@@ -477,11 +477,6 @@ __global__ void k_k32(const int64_t* __restrict__ K, uint64_t n, int32_t* __rest
     if ((threadIdx.x & 31) == 0 && a > ctl->max_abs_k[0]) atomicMax(&ctl->max_abs_k[0], (unsigned long long)a);
 }
 
-__global__ void k_k32_to_k16(const int32_t* __restrict__ K, uint64_t n, int16_t* __restrict__ K16) {
-    const uint64_t i = blockIdx.x * 256ull + threadIdx.x;
-    if (i < n) K16[i] = (int16_t)K[i];
-}
-
 __global__ void k_k32_to_f64(const int32_t* __restrict__ K, uint64_t n, double bin, double* __restrict__ x) {
     const uint64_t i = blockIdx.x * 256ull + threadIdx.x;
     if (i < n) x[i] = __dmul_rn((double)K[i], bin);
@@ -556,12 +551,6 @@ void nd_from_prefix(const int64_t* P, uint64_t n, const NdShape& sh, int64_t* Kw
         src = Kw;
     }
     k_k32<<<g, 256, 0, st>>>(src, n, K32, K16, ctl);
-    UMCG_LAUNCHED();
-}
-
-void k32_to_k16(const int32_t* K, uint64_t n, int16_t* K16, cudaStream_t st) {
-    if (!n) return;
-    k_k32_to_k16<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(K, n, K16);
     UMCG_LAUNCHED();
 }
 

@@ -63,7 +63,6 @@ void dec_prepare(const DecSrc& src, uint64_t t_tiles, void* status, DevCtl* ctl,
 void nd_from_prefix(const int64_t* P, uint64_t n, const NdShape& sh, int64_t* Kw, int32_t* K32, int16_t* K16,
                     DevCtl* ctl,
                     cudaStream_t st);
-void k32_to_k16(const int32_t* K, uint64_t n, int16_t* K16, cudaStream_t st);
 void k32_to_f64(const int32_t* K, uint64_t n, double bin, double* x, cudaStream_t st);
 
 // Launch the serial token probe (<= 64 tokens) without synchronizing;
