@@ -178,6 +178,25 @@ umcg_status umcg_encode(const double* d_values, uint64_t n, int predictor, int n
 umcg_status umcg_decode(const uint8_t* d_payload, uint64_t len, double* d_out, uint64_t n_capacity,
                         uint64_t* n_out, void* stream);
 
+/* umc::grid_init (grid_builder.hpp:201-282) on the device: the initial
+ * rectilinear grid from the mesh's per-axis edge lengths -- cell edges
+ * (arity 3 tri, 4 quad, 8 hex; traverse_mesh) or, with no cells, each
+ * vertex's exact 1-nearest neighbour (knn_edge_stats) -- at the k-th
+ * nearest-rank percentile, raised by delta while an axis would exceed g_max
+ * nodes. d_coords [n_v*dim], d_cells [n_cells*arity] (u64 vertex ids).
+ * Writes axis_sizes[dim] and, when axes != NULL, the concatenated axes
+ * (axes_cap doubles). cfg NULL = the reference defaults (50, 4096, 5, 0.35).
+ * The result feeds umcg_plan_build (grid_coarsen). */
+typedef struct umcg_grid_config {
+    double percentile_k;
+    uint64_t g_max;
+    double delta;
+    double seed_mode_threshold;
+} umcg_grid_config;
+umcg_status umcg_grid_init(int dim, uint64_t n_vertices, const double* d_coords, int cell_arity,
+                           uint64_t n_cells, const uint64_t* d_cells, const umcg_grid_config* cfg,
+                           uint64_t* axis_sizes, double* axes, uint64_t axes_cap, void* stream);
+
 /* Serialization baseline (pipeline.hpp:152-176, baseline_archive): the
  * field in file order as ONE lorenzo_1d component at the full budget,
  * tau_abs = resolve_tau_abs(budget, values); archive flag 8, digest 0, empty

@@ -242,6 +242,25 @@ class Ref:
         return a.value, b.value
 
     # -- static inputs --------------------------------------------------------
+    def grid_init(self, coords, cells=None, arity=3, percentile_k=50.0, g_max=4096, delta=5.0, thr=0.35):
+        coords = np.ascontiguousarray(coords, np.float64)
+        n_v, dim = coords.shape
+        cl = np.ascontiguousarray(cells, np.uint64) if cells is not None else np.zeros(1, np.uint64)
+        n_c = len(cells) if cells is not None else 0
+        osz = np.zeros(dim, np.uint64)
+        oax = f64p()
+        self._check(self.lib.umcref_grid_init(dim, n_v, _ptr(coords, f64p), arity, n_c, _ptr(cl, u64p),
+                                              C.c_double(percentile_k), C.c_uint64(g_max), C.c_double(delta),
+                                              C.c_double(thr), _ptr(osz, u64p), C.byref(oax)))
+        tot = int(osz.sum())
+        cat = np.ctypeslib.as_array(oax, (max(tot, 1),))[:tot].copy()
+        self.lib.umcref_free(oax)
+        out, off = [], 0
+        for d in range(dim):
+            out.append(cat[off: off + int(osz[d])])
+            off += int(osz[d])
+        return out
+
     def grid_coarsen(self, dim, coords, axes, seed_threshold=0.35):
         coords = np.ascontiguousarray(coords, np.float64)
         n_v = coords.shape[0]

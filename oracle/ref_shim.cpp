@@ -338,6 +338,33 @@ int umcref_grid_coarsen(int dim, std::uint64_t n_v, const double* coords,
     });
 }
 
+// umc::grid_init (grid_builder.hpp:224) on an explicit mesh (cells optional:
+// n_cells == 0 takes the reference's 1-NN point-cloud path).
+int umcref_grid_init(int dim, std::uint64_t n_v, const double* coords, int arity, std::uint64_t n_cells,
+                     const std::uint64_t* cells, double pk, std::uint64_t g_max, double delta, double thr,
+                     std::uint64_t* out_sizes, double** out_axes) {
+    return guarded([&] {
+        umc::Mesh mesh;
+        mesh.dim = dim;
+        mesh.cell_arity = n_cells ? arity : 0;
+        mesh.vertices.assign(coords, coords + n_v * dim);
+        if (n_cells) mesh.cells.assign(cells, cells + n_cells * arity);
+        umc::GridBuildConfig cfg;
+        cfg.percentile_k = pk;
+        cfg.g_max = g_max;
+        cfg.delta = delta;
+        cfg.seed_mode_threshold = thr;
+        const auto grid = umc::grid_init(mesh, cfg);
+        std::vector<double> axes;
+        for (int d = 0; d < dim; ++d) {
+            out_sizes[d] = grid.axes[d].size();
+            axes.insert(axes.end(), grid.axes[d].begin(), grid.axes[d].end());
+        }
+        *out_axes = static_cast<double*>(std::malloc(axes.size() * 8 + 8));
+        std::memcpy(*out_axes, axes.data(), axes.size() * 8);
+    });
+}
+
 // grid_init (grid_builder.hpp:224) on a synthetic mesh from gen_mesh.
 // Synthetic mesh + field (datagen.hpp:116, 261); returns coords and values.
 int umcref_gen_case(int dim, std::uint64_t n_target, int mesh_style, int field_kind,

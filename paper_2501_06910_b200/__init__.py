@@ -37,7 +37,7 @@ EXPORTED = [
     "umcg_plan_create", "umcg_plan_build", "umcg_plan_destroy", "umcg_plan_get_info",
     "umcg_plan_export", "umcg_compress_bound", "umcg_compress", "umcg_compress_batch",
     "umcg_decompress", "umcg_compress_host", "umcg_decompress_host", "umcg_encode_bound",
-    "umcg_encode", "umcg_decode", "umcg_baseline_bound", "umcg_compress_baseline", "umcg_rle_bound", "umcg_rle_compress", "umcg_rle_decompress",
+    "umcg_encode", "umcg_decode", "umcg_grid_init", "umcg_baseline_bound", "umcg_compress_baseline", "umcg_rle_bound", "umcg_rle_compress", "umcg_rle_decompress",
     "umcg_gen_config",
     "umcg_kernel_launches", "umcg_serial_fallbacks", "umcg_profile_enable", "umcg_profile_dump",
     "umcg_last_error", "umcg_version",
@@ -101,6 +101,8 @@ def lib():
     L.umcg_profile_dump.argtypes = [C.c_char_p, C.c_uint64]
     L.umcg_encode_bound.restype = C.c_uint64
     L.umcg_encode_bound.argtypes = [C.c_uint64, C.c_int]
+    L.umcg_grid_init.argtypes = [C.c_int, C.c_uint64, vp, C.c_int, C.c_uint64, vp, C.POINTER(GridConfig), u64p,
+                                 f64p, C.c_uint64, vp]
     L.umcg_baseline_bound.restype = C.c_uint64
     L.umcg_baseline_bound.argtypes = [C.c_uint64, C.c_uint64]
     L.umcg_compress_baseline.argtypes = [C.POINTER(Params), vp, C.c_uint64, C.c_char_p, vp, C.c_uint64, u64p, vp]
@@ -357,6 +359,33 @@ def decode(payload: bytes, n_capacity: int | None = None, device="cuda"):
     _check(lib().umcg_decode(C.c_void_p(a.data_ptr()), len(payload), C.c_void_p(out.data_ptr()),
                              n_capacity, C.byref(n), _stream_ptr()))
     return out[: n.value]
+
+
+class GridConfig(C.Structure):
+    _fields_ = [("percentile_k", C.c_double), ("g_max", C.c_uint64), ("delta", C.c_double),
+                ("seed_mode_threshold", C.c_double)]
+
+
+def grid_init(d_coords, d_cells=None, arity=3, percentile_k=50.0, g_max=4096, delta=5.0, seed_threshold=0.35):
+    """umc::grid_init (grid_builder.hpp:201-282) on the device: the initial
+    grid axes from the mesh's edge-length statistics (cell edges, or the
+    1-NN point-cloud fallback when d_cells is None)."""
+    dim = int(d_coords.shape[1])
+    n_c = int(d_cells.shape[0]) if d_cells is not None else 0
+    cfg = GridConfig(percentile_k, g_max, delta, seed_threshold)
+    sizes = np.zeros(dim, np.uint64)
+    _check(lib().umcg_grid_init(dim, d_coords.shape[0], C.c_void_p(d_coords.data_ptr()), arity, n_c,
+                                C.c_void_p(d_cells.data_ptr()) if d_cells is not None else None, C.byref(cfg),
+                                _ptr(sizes, u64p), None, 0, _stream_ptr()))
+    cat = np.zeros(int(sizes.sum()), np.float64)
+    _check(lib().umcg_grid_init(dim, d_coords.shape[0], C.c_void_p(d_coords.data_ptr()), arity, n_c,
+                                C.c_void_p(d_cells.data_ptr()) if d_cells is not None else None, C.byref(cfg),
+                                _ptr(sizes, u64p), _ptr(cat, f64p), len(cat), _stream_ptr()))
+    out, off = [], 0
+    for d in range(dim):
+        out.append(cat[off: off + int(sizes[d])])
+        off += int(sizes[d])
+    return out
 
 
 def compress_baseline(d_values, budget: "Budget", name: str = "") -> bytes:

@@ -1219,6 +1219,30 @@ umcg_status umcg_decode(const uint8_t* d_payload, uint64_t len, double* d_out, u
     return guarded([&] { decode_impl(d_payload, len, d_out, n_cap, n_out, static_cast<cudaStream_t>(stream)); });
 }
 
+umcg_status umcg_grid_init(int dim, uint64_t n_v, const double* d_coords, int arity, uint64_t n_cells,
+                           const uint64_t* d_cells, const umcg_grid_config* cfg, uint64_t* axis_sizes, double* axes,
+                           uint64_t axes_cap, void* stream) {
+    return guarded([&] {
+        if (!d_coords || !axis_sizes || (n_cells && !d_cells)) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
+        const umcg_grid_config def{50.0, 4096, 5.0, 0.35};
+        const umcg_grid_config& c = cfg ? *cfg : def;
+        std::vector<std::vector<double>> ax;
+        grid_init_gpu(dim, n_v, d_coords, arity, n_cells, d_cells, c.percentile_k, c.g_max, c.delta,
+                      c.seed_mode_threshold, ax, static_cast<cudaStream_t>(stream));
+        uint64_t tot = 0;
+        for (int d = 0; d < dim; ++d) {
+            axis_sizes[d] = ax[d].size();
+            tot += ax[d].size();
+        }
+        if (axes) {
+            if (tot > axes_cap) fail(UMCG_INVALID_ARGUMENT, "axes capacity " + std::to_string(axes_cap) + " < " + std::to_string(tot));
+            uint64_t o = 0;
+            for (int d = 0; d < dim; ++d)
+                for (double v : ax[d]) axes[o++] = v;
+        }
+    });
+}
+
 uint64_t umcg_baseline_bound(uint64_t n, uint64_t name_len) { return 10 + name_len + 24 + 16 + payload_bound(n, 1); }
 
 umcg_status umcg_compress_baseline(const umcg_params* prm, const double* d_values, uint64_t n, const char* name_c,

@@ -1,6 +1,8 @@
 // Host-side launchers for the umcg kernels (one declaration per kernel family).
 #pragma once
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace umcg {
@@ -63,6 +65,11 @@ void stream_decode(const uint8_t* d_stream, uint64_t len, uint64_t n, uint64_t* 
 // treated as 1-byte "codes" where zero bytes are zero codes.
 void rle_bytes_encode(const uint8_t* d_in, uint64_t n, const StreamEncScratch& s, DevCtl* ctl,
                       uint8_t* dst, cudaStream_t st);
+
+// ---- gridinit.cu: umc::grid_init (grid_builder.hpp:201-282) ----------------
+void grid_init_gpu(int D, uint64_t n_v, const double* d_xyz, int arity, uint64_t n_cells, const uint64_t* d_cells,
+                   double percentile_k, uint64_t g_max, double delta, double seed_threshold,
+                   std::vector<std::vector<double>>& axes, cudaStream_t st);
 
 // ---- codes.cu: quantization codes (lattice fast path) + exact serial path --
 struct NdShape {

@@ -682,3 +682,61 @@ def test_heavy_slots_match_reference(cuda, ref, oracle, g):
     xh = x.cpu().numpy()
     for tau in (1e-2, 1e-5):
         _parity_case(plan, s, x, xh, dict(tau=tau), ref, oracle, f"heavy g={g} tau={tau}")
+
+
+def _lattice_mesh(rng, dims, jitter, kind):
+    """Jittered lattice with permuted vertex ids and cells: 'tri' (2 per
+    quad), 'quad', or 'hex'."""
+    idx = np.stack(np.meshgrid(*[np.arange(m) for m in dims], indexing="ij"), -1).reshape(-1, len(dims))
+    h = [1.0 / (m - 1) for m in dims]
+    xyz = idx * np.array(h) + (rng.uniform(-jitter, jitter, idx.shape) * np.array(h)) * \
+        ((idx > 0) & (idx < np.array(dims) - 1))
+    perm = rng.permutation(len(xyz))
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(len(perm))
+    lin = lambda *c: np.ravel_multi_index(c, dims)  # noqa: E731
+    if kind in ("tri", "quad"):
+        i, j = np.meshgrid(np.arange(dims[0] - 1), np.arange(dims[1] - 1), indexing="ij")
+        i, j = i.ravel(), j.ravel()
+        a, b, c, d = lin(i, j), lin(i + 1, j), lin(i + 1, j + 1), lin(i, j + 1)
+        cells = np.concatenate([np.stack([a, b, c], 1), np.stack([a, c, d], 1)]) if kind == "tri" else \
+            np.stack([a, b, c, d], 1)
+    else:
+        i, j, k = [x.ravel() for x in np.meshgrid(*[np.arange(m - 1) for m in dims], indexing="ij")]
+        corners = [lin(i + di, j + dj, k + dk) for dk in (0, 1) for (di, dj) in ((0, 0), (1, 0), (1, 1), (0, 1))]
+        cells = np.stack(corners, 1)
+    return xyz[perm], inv[cells].astype(np.uint64)
+
+
+@pytest.mark.parametrize("case", ["tri", "quad", "hex", "tri_gmax", "cloud2", "cloud3", "annulus", "tiny"])
+def test_grid_init_matches_reference(cuda, ref, case):
+    """umcg_grid_init against umc::grid_init (grid_builder.hpp:201-282):
+    cell-edge statistics for tri/quad/hex meshes, the 1-NN point-cloud
+    fallback, the g_max percentile loop and its uniform fallback, and a
+    collinear (degenerate-axis) cloud -- identical axes."""
+    import torch
+    rng = np.random.default_rng(hash(case) % 2**32)
+    cells, arity, kw = None, 3, {}
+    if case in ("tri", "quad", "tri_gmax"):
+        xyz, cells = _lattice_mesh(rng, [120, 90], 0.3, "tri" if case != "quad" else "quad")
+        arity = 4 if case == "quad" else 3
+        if case == "tri_gmax":
+            kw = dict(g_max=24, percentile_k=30.0, delta=7.5)
+    elif case == "hex":
+        xyz, cells = _lattice_mesh(rng, [30, 25, 20], 0.2, "hex")
+        arity = 8
+    elif case == "cloud2":
+        xyz = _lattice_mesh(rng, [300, 300], 0.3, "tri")[0]
+    elif case == "cloud3":
+        xyz = rng.uniform(0, 1, (60000, 3))
+    elif case == "annulus":
+        xy, _ = umcg.gen_config(2, 200000, 7, device="cuda", values=False)
+        xyz = xy.cpu().numpy()
+    else:
+        xyz = np.array([[0.0, 0.5], [1.0, 0.5], [0.25, 0.5], [0.7, 0.5]])
+    want = ref.grid_init(xyz, cells, arity, **kw)
+    d_cells = torch.from_numpy(cells.view(np.int64)).cuda() if cells is not None else None
+    got = umcg.grid_init(torch.from_numpy(xyz).cuda(), d_cells, arity, **kw)
+    assert len(got) == len(want)
+    for a, b in zip(got, want):
+        assert np.array_equal(a, b), (case, len(a), len(b))
