@@ -28,6 +28,7 @@
 
 #include <cuda_runtime_api.h>
 
+#include "umc/grid_builder.hpp"
 #include "umc/pipeline.hpp"
 #include "../umcg.h"
 
@@ -143,6 +144,87 @@ inline Archive compress(const Field& field, const MappingTable& map, const RectG
     detail::check(umcg_compress_host(plan, &prm, field.values.data(), field.name.c_str(), bytes.data(), cap, &len));
     bytes.resize(len);
     return deserialize_archive(bytes);  // pipeline.hpp:237 builds the reference's Archive
+}
+
+namespace detail {
+inline void validate_config_host(const GridBuildConfig& cfg) { validate_config(cfg); }  // grid_builder.hpp:25-33
+
+struct DeviceCoords {
+    void* p = nullptr;
+    ~DeviceCoords() { cudaFree(p); }
+};
+}  // namespace detail
+
+/// umc::grid_init (grid_builder.hpp:224-282) on the GPU: same RectGrid.
+inline RectGrid grid_init(const Mesh& mesh, const GridBuildConfig& cfg = {}) {
+    detail::validate_config_host(cfg);
+    const std::uint64_t n = mesh.vertex_count();
+    const std::uint64_t nc = mesh.cell_count();
+    detail::DeviceCoords dc, dl;
+    if (cudaMalloc(&dc.p, mesh.vertices.size() * 8 + 8) != cudaSuccess ||
+        cudaMalloc(&dl.p, mesh.cells.size() * 8 + 8) != cudaSuccess)
+        throw error("cudaMalloc failed");
+    cudaMemcpy(dc.p, mesh.vertices.data(), mesh.vertices.size() * 8, cudaMemcpyHostToDevice);
+    if (nc) cudaMemcpy(dl.p, mesh.cells.data(), mesh.cells.size() * 8, cudaMemcpyHostToDevice);
+    const umcg_grid_config c{cfg.percentile_k, cfg.g_max, cfg.delta, cfg.seed_mode_threshold};
+    std::uint64_t sizes[3] = {0, 0, 0};
+    const auto* cells = nc ? static_cast<const std::uint64_t*>(dl.p) : nullptr;
+    detail::check(umcg_grid_init(mesh.dim, n, static_cast<const double*>(dc.p), mesh.cell_arity, nc, cells, &c, sizes,
+                                 nullptr, 0, nullptr));
+    std::uint64_t tot = 0;
+    for (int d = 0; d < mesh.dim; ++d) tot += sizes[d];
+    std::vector<double> cat(tot);
+    detail::check(umcg_grid_init(mesh.dim, n, static_cast<const double*>(dc.p), mesh.cell_arity, nc, cells, &c, sizes,
+                                 cat.data(), tot, nullptr));
+    RectGrid grid;
+    grid.dim = mesh.dim;
+    grid.axes.resize(mesh.dim);
+    std::uint64_t o = 0;
+    for (int d = 0; d < mesh.dim; ++d) {
+        grid.axes[d].assign(cat.begin() + o, cat.begin() + o + sizes[d]);
+        o += sizes[d];
+    }
+    return grid;
+}
+
+/// umc::grid_coarsen (grid_builder.hpp:365-421) on the GPU: same mapping,
+/// coarsened grid and mode (umcg_plan_build + umcg_plan_export).
+inline CoarsenResult grid_coarsen(const Mesh& mesh, const RectGrid& grid, const GridBuildConfig& cfg) {
+    detail::validate_config_host(cfg);
+    const std::uint64_t n = mesh.vertex_count();
+    std::vector<std::uint64_t> sizes;
+    std::vector<double> axes;
+    for (const auto& a : grid.axes) {
+        sizes.push_back(a.size());
+        axes.insert(axes.end(), a.begin(), a.end());
+    }
+    umcg_grid_desc g{grid.dim, sizes.data(), axes.data()};
+    detail::DeviceCoords dc;
+    if (cudaMalloc(&dc.p, mesh.vertices.size() * 8 + 8) != cudaSuccess) throw error("cudaMalloc failed");
+    cudaMemcpy(dc.p, mesh.vertices.data(), mesh.vertices.size() * 8, cudaMemcpyHostToDevice);
+    umcg_plan* p = nullptr;
+    detail::check(umcg_plan_build(&g, n, static_cast<const double*>(dc.p), cfg.seed_mode_threshold, 0, &p));
+    detail::PlanPtr holder(p);
+    umcg_plan_info info{};
+    detail::check(umcg_plan_get_info(p, &info));
+    CoarsenResult res;
+    res.mapping.mode = info.mode ? MappingMode::seed : MappingMode::dense;
+    res.mapping.assignments.resize(n);
+    std::vector<std::uint64_t> visited(info.n_visited);
+    std::uint64_t tot = 0;
+    for (int d = 0; d < info.dim; ++d) tot += info.shape[d];
+    std::vector<double> cax(tot);
+    detail::check(umcg_plan_export(p, res.mapping.assignments.data(), visited.data(), cax.data()));
+    if (info.mode) res.mapping.visited_nodes = std::move(visited);
+    res.mapping.visited_fraction = info.visited_fraction;
+    res.grid.dim = info.dim;
+    res.grid.axes.resize(info.dim);
+    std::uint64_t o = 0;
+    for (int d = 0; d < info.dim; ++d) {
+        res.grid.axes[d].assign(cax.begin() + o, cax.begin() + o + info.shape[d]);
+        o += info.shape[d];
+    }
+    return res;
 }
 
 /// umc::compress_baseline (pipeline.hpp:152-162) on the GPU: one 1-D

@@ -162,6 +162,29 @@ int main() {
         CHECK(b200::decompress(gv, a.map, a.grid, a.mesh).values == decompress(rv, a.map, a.grid, a.mesh).values,
               "verbatim decode bitwise");
     }
+    // grid builder on the device (grid_builder.hpp:224-421): same axes, same
+    // mapping, same mode, for meshes with cells and for a bare point cloud
+    for (int c = 0; c < 4; ++c) {
+        const int dim = c < 2 ? 2 : 3;
+        SynthSpec spec;
+        spec.dim = dim;
+        spec.n_target = dim == 2 ? 5000 : 8000;
+        spec.mesh_style = c % 2 ? MeshStyle::graded : MeshStyle::jittered;
+        spec.rng_seed = 40 + c;
+        Mesh mesh = gen_mesh(spec);
+        if (c == 3) mesh.cells.clear();  // point cloud: 1-NN statistics
+        GridBuildConfig cfg;
+        const RectGrid gi = grid_init(mesh, cfg);
+        const RectGrid gg = b200::grid_init(mesh, cfg);
+        CHECK(gi.axes == gg.axes, "grid_init axes identical");
+        const auto rc = grid_coarsen(mesh, gi, cfg);
+        const auto gc = b200::grid_coarsen(mesh, gi, cfg);
+        CHECK(rc.grid.axes == gc.grid.axes, "grid_coarsen axes identical");
+        CHECK(rc.mapping.mode == gc.mapping.mode, "grid_coarsen mode");
+        CHECK(rc.mapping.assignments == gc.mapping.assignments, "grid_coarsen assignments identical");
+        CHECK(rc.mapping.visited_nodes == gc.mapping.visited_nodes, "grid_coarsen visited identical");
+        CHECK(mapping_digest(rc.mapping) == mapping_digest(gc.mapping), "mapping digest");
+    }
     std::printf("cases %d exact %d failures %d\n", total, exact, failures);
     return failures ? 1 : 0;
 }
