@@ -265,6 +265,9 @@ class Plan:
 
     # ---- device-pointer path (the measured one) ---------------------------
     def compress_into(self, d_values, budget: Budget, d_archive, name: str = "", stream=None) -> int:
+        import torch
+        if d_values.dtype != torch.float64:
+            raise TypeError("compress_into takes fp64 values; use compress_batch for fp32 fields")
         n = C.c_uint64()
         prm = budget.c()
         _check(lib().umcg_compress(self.h, C.byref(prm), C.c_void_p(d_values.data_ptr()),
@@ -282,20 +285,33 @@ class Plan:
         n = self.compress_into(d_values, budget, buf, name)
         return bytes(buf[:n].cpu().numpy())
 
-    def compress_batch(self, d_values, budget: Budget = Budget(), names=None) -> list:
-        """umcg_compress_batch: V fields [V, n] (fp64 or fp32, BASELINE config
-        4) against this plan, one archive per field."""
+    def compress_batch_into(self, d_values, budget: Budget, d_archive, names=None, stream=None):
+        """umcg_compress_batch into a device buffer: V fields [V, n] (fp64 or
+        fp32, BASELINE config 4); returns the V archive lengths (archives are
+        packed back to back)."""
         import torch
         V = int(d_values.shape[0])
+        if d_values.dtype not in (torch.float32, torch.float64):
+            raise TypeError("compress_batch takes fp32 or fp64 values")
         dtype = 1 if d_values.dtype == torch.float32 else 0
         names = names or [f"f{k}" for k in range(V)]
-        cap = sum(self.compress_bound(nm) for nm in names)
-        buf = torch.empty(cap, dtype=torch.uint8, device=d_values.device)
         lens = np.zeros(V, np.uint64)
         cn = (C.c_char_p * V)(*[nm.encode() for nm in names])
         prm = budget.c()
         _check(lib().umcg_compress_batch(self.h, C.byref(prm), C.c_void_p(d_values.data_ptr()), dtype, V, cn,
-                                         C.c_void_p(buf.data_ptr()), cap, _ptr(lens, u64p), _stream_ptr()))
+                                         C.c_void_p(d_archive.data_ptr()), d_archive.numel(), _ptr(lens, u64p),
+                                         _stream_ptr(stream)))
+        return lens
+
+    def compress_batch(self, d_values, budget: Budget = Budget(), names=None) -> list:
+        """umcg_compress_batch: V fields [V, n] (fp64 or fp32, BASELINE config
+        4) against this plan, one archive (bytes) per field."""
+        import torch
+        V = int(d_values.shape[0])
+        names = names or [f"f{k}" for k in range(V)]
+        cap = sum(self.compress_bound(nm) for nm in names)
+        buf = torch.empty(cap, dtype=torch.uint8, device=d_values.device)
+        lens = self.compress_batch_into(d_values, budget, buf, names)
         host = bytes(buf[: int(lens.sum())].cpu().numpy())
         out, o = [], 0
         for ln in lens:
