@@ -381,22 +381,54 @@ __global__ void k_axis_cols(int64_t* __restrict__ K, uint64_t n, uint64_t len, u
 // the middle axis. Threads own (outer, k) lines, 8 loads in flight.
 // For D == 2 the result is final (int32 + max|K|); for D == 3 an int64
 // intermediate follows, finished by k_nd_outer.
+// With few lines (2-D grids: one line per column) the middle axis is split
+// into blockIdx.y chunks of rows: chunk sums (k_nd_mid_sums), their exclusive
+// scan per line (k_nd_chunk_scan), then every chunk resumes from its offset.
+__global__ void __launch_bounds__(256) k_nd_mid_sums(const int64_t* __restrict__ P, uint64_t d_out, uint64_t d_mid,
+                                                    uint64_t d_fast, uint64_t rows, int64_t* __restrict__ csum) {
+    const uint64_t lines = d_out * d_fast;
+    const uint64_t line = blockIdx.x * 256ull + threadIdx.x;
+    if (line >= lines) return;
+    const uint64_t o = line / d_fast, k = line % d_fast;
+    const uint64_t base = o * d_mid * d_fast;
+    const uint64_t j0 = blockIdx.y * rows, j1 = min(d_mid, j0 + rows);
+    int64_t acc = 0;
+    for (uint64_t j = j0; j < j1; ++j) {
+        const uint64_t r = base + j * d_fast;
+        acc += __ldg(&P[r + k]) - (r ? __ldg(&P[r - 1]) : 0);
+    }
+    csum[blockIdx.y * lines + line] = acc;
+}
+
+__global__ void k_nd_chunk_scan(int64_t* __restrict__ csum, uint64_t lines, uint32_t nch) {
+    const uint64_t line = blockIdx.x * 256ull + threadIdx.x;
+    if (line >= lines) return;
+    int64_t acc = 0;
+    for (uint32_t c = 0; c < nch; ++c) {
+        const int64_t v = csum[c * lines + line];
+        csum[c * lines + line] = acc;
+        acc += v;
+    }
+}
+
 template <bool FINAL>
 __global__ void __launch_bounds__(256) k_nd_mid(const int64_t* __restrict__ P, uint64_t d_out, uint64_t d_mid,
                                                uint64_t d_fast, int64_t* __restrict__ Kw, int32_t* __restrict__ K32,
-                                               int16_t* __restrict__ K16, DevCtl* ctl) {
+                                               int16_t* __restrict__ K16, DevCtl* ctl,
+                                               const int64_t* __restrict__ coff, uint64_t rows) {
     const uint64_t line = blockIdx.x * 256ull + threadIdx.x;  // over d_out * d_fast
     uint64_t amax = 0;
     if (line < d_out * d_fast) {
         const uint64_t o = line / d_fast, k = line % d_fast;
         const uint64_t base = o * d_mid * d_fast;
-        int64_t acc = 0;
-        for (uint64_t j0 = 0; j0 < d_mid; j0 += 8) {
+        int64_t acc = coff ? coff[blockIdx.y * d_out * d_fast + line] : 0;
+        const uint64_t jb = blockIdx.y * rows, je = min(d_mid, jb + rows);
+        for (uint64_t j0 = jb; j0 < je; j0 += 8) {
             int64_t v[8], rb[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const uint64_t j = j0 + u;
-                if (j < d_mid) {
+                if (j < je) {
                     const uint64_t r = base + j * d_fast;
                     v[u] = __ldcs(&P[r + k]);
                     rb[u] = r ? __ldg(&P[r - 1]) : 0;
@@ -408,7 +440,7 @@ __global__ void __launch_bounds__(256) k_nd_mid(const int64_t* __restrict__ P, u
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const uint64_t j = j0 + u;
-                if (j >= d_mid) break;
+                if (j >= je) break;
                 acc += v[u] - rb[u];
                 const uint64_t idx = base + j * d_fast + k;
                 if (FINAL) {
@@ -528,12 +560,26 @@ void nd_from_prefix(const int64_t* P, uint64_t n, const NdShape& sh, int64_t* Kw
     const int64_t* src = P;
     if (sh.D == 2 || sh.D == 3) {
         const uint64_t d2 = sh.dims[sh.D - 1], d1 = sh.dims[sh.D - 2], d0 = sh.D == 3 ? sh.dims[0] : 1;
-        const unsigned g1 = (unsigned)cdiv(d0 * d2, 256);
+        const uint64_t lines = d0 * d2;
+        const unsigned g1 = (unsigned)cdiv(lines, 256);
+        // enough threads: split the middle axis into chunks when lines are few
+        uint32_t nch = 1;
+        while (nch < 64 && lines * nch < 65536 && d1 / (2 * nch) >= 16) nch *= 2;
+        const uint64_t rows = cdiv(d1, (uint64_t)nch);
+        int64_t* csum = nullptr;
+        if (nch > 1) {
+            // scratch: Kw is unused for D == 2; for D == 3 K32 is written only later
+            csum = sh.D == 2 ? Kw : reinterpret_cast<int64_t*>(K32);
+            k_nd_mid_sums<<<dim3(g1, nch), 256, 0, st>>>(P, d0, d1, d2, rows, csum);
+            UMCG_LAUNCHED();
+            k_nd_chunk_scan<<<g1, 256, 0, st>>>(csum, lines, nch);
+            UMCG_LAUNCHED();
+        }
         if (sh.D == 2) {
-            k_nd_mid<true><<<g1, 256, 0, st>>>(P, d0, d1, d2, nullptr, K32, K16, ctl);
+            k_nd_mid<true><<<dim3(g1, nch), 256, 0, st>>>(P, d0, d1, d2, nullptr, K32, K16, ctl, csum, rows);
             UMCG_LAUNCHED();
         } else {
-            k_nd_mid<false><<<g1, 256, 0, st>>>(P, d0, d1, d2, Kw, nullptr, nullptr, ctl);
+            k_nd_mid<false><<<dim3(g1, nch), 256, 0, st>>>(P, d0, d1, d2, Kw, nullptr, nullptr, ctl, csum, rows);
             UMCG_LAUNCHED();
             k_nd_outer<<<(unsigned)cdiv(d1 * d2, 256), 256, 0, st>>>(Kw, d0, d1 * d2, K32, K16, ctl);
             UMCG_LAUNCHED();
