@@ -872,7 +872,18 @@ void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_
     prep(h1, hb + p1, head - p1, l1);
     prep(h2, tail + 8, tl - 8, l2);
     const int g_kind0 = (flags & 2u) ? 1 : 0;
-    if (g_kind0 == 0 && fast_decompress(p, d_ar, p1, h1, p2, h2, d_out, st)) return;
+    // The speculative path needs single-literal streams; a plan whose last
+    // archive failed that (zero runs: multi-token streams) goes straight to
+    // the step-by-step path instead of wasting a full speculative decode.
+    if (g_kind0 == 0 && p->spec_misses < 2) {
+        if (fast_decompress(p, d_ar, p1, h1, p2, h2, d_out, st)) {
+            p->spec_misses = 0;
+            return;
+        }
+        ++p->spec_misses;
+    } else if (g_kind0 == 0 && ++p->spec_skips % 8 == 0) {
+        p->spec_misses = 0;  // retry the speculative path now and then
+    }
     double* x1 = p->x1.as<double>(p->n_slots ? p->n_slots : 1);
     int32_t* K1 = p->codes1.as<int32_t>(p->n_slots ? p->n_slots : 1);
     const int g_kind = (flags & 2u) ? 1 : 0;
