@@ -872,18 +872,24 @@ void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_
     prep(h1, hb + p1, head - p1, l1);
     prep(h2, tail + 8, tl - 8, l2);
     const int g_kind0 = (flags & 2u) ? 1 : 0;
-    // The speculative path needs single-literal streams; a plan whose last
-    // archive failed that (zero runs: multi-token streams) goes straight to
-    // the step-by-step path instead of wasting a full speculative decode.
-    if (g_kind0 == 0 && p->spec_misses < 2) {
-        if (fast_decompress(p, d_ar, p1, h1, p2, h2, d_out, st)) {
-            p->spec_misses = 0;
-            return;
+    // The speculative path needs single-literal streams. Both streams' first
+    // token header is in the bytes already on the host: one literal covering
+    // the whole stream is {0x01, varint(L), L bytes} with 1 + |varint| + L ==
+    // stream length; anything else (zero runs: many tokens) goes straight to
+    // the step-by-step path instead of wasting a speculative decode.
+    auto single_literal = [](const uint8_t* b, uint64_t avail, uint64_t slen) {
+        if (avail < 2 || b[0] != 0x01) return false;
+        uint64_t L = 0;
+        for (uint64_t k = 1; k < avail && k <= 10; ++k) {
+            L |= (uint64_t)(b[k] & 0x7f) << (7 * (k - 1));
+            if (!(b[k] & 0x80)) return 1 + k + L == slen;
         }
-        ++p->spec_misses;
-    } else if (g_kind0 == 0 && ++p->spec_skips % 8 == 0) {
-        p->spec_misses = 0;  // retry the speculative path now and then
-    }
+        return false;
+    };
+    const uint64_t s1 = p1 + h1.stream_off, s2t = 8 + h2.stream_off;  // in hb / tail
+    const bool one1 = s1 < head && single_literal(hb + s1, head - s1, h1.stream_len);
+    const bool one2 = s2t < tl && single_literal(tail + s2t, tl - s2t, h2.stream_len);
+    if (g_kind0 == 0 && one1 && one2 && fast_decompress(p, d_ar, p1, h1, p2, h2, d_out, st)) return;
     double* x1 = p->x1.as<double>(p->n_slots ? p->n_slots : 1);
     int32_t* K1 = p->codes1.as<int32_t>(p->n_slots ? p->n_slots : 1);
     const int g_kind = (flags & 2u) ? 1 : 0;

@@ -56,8 +56,6 @@ struct umcg_plan {
         scratch_d, dx1, dcodes;
     umcg::StreamDecScratch dec, dec2;
     umcg::SideStream side;  // grid component's chain runs beside the residual's
-    int spec_misses = 0;     // consecutive speculative-decompress misses (decompress_impl)
-    uint64_t spec_skips = 0;
     umcg::PinnedBuf hctl, hstage;
 };
 

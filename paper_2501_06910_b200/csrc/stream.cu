@@ -83,6 +83,8 @@ constexpr int PJ_HALO = 16;      // tag + 10-byte varint past the chunk end
 constexpr int PJ_K = 32;         // distinct exits kept per chunk (one warp)
 constexpr int PJ_HS = 128;       // hash slots for the distinct-exit set
 constexpr uint64_t PJ_G = 64;    // chunks per group
+constexpr int PJ_SB = 8;         // sub-chunks of 2^PJ_SB bytes for the token walks
+constexpr uint64_t PJ_NS = PJ_C >> PJ_SB;  // sub-chunks per chunk
 constexpr uint64_t PJ_DEAD = ~0ull;
 constexpr uint32_t PJ_DEAD32 = 0xFFFFFFFFu;
 constexpr uint32_t PJ_MANY = 0xFFFFFFFFu;
@@ -110,7 +112,7 @@ __device__ __forceinline__ uint64_t tok_next(At at, uint64_t len, uint64_t p, ui
 
 __global__ void __launch_bounds__(PJ_THREADS) k_tok_jump(const uint8_t* __restrict__ s, uint64_t len,
                                                          uint32_t* __restrict__ ex, uint32_t* __restrict__ dcount,
-                                                         uint64_t* __restrict__ dvals) {
+                                                         uint64_t* __restrict__ dvals, uint32_t* __restrict__ subex) {
     extern __shared__ __align__(16) uint8_t pj_smem[];
     __shared__ unsigned long long hs[PJ_HS];
     __shared__ int hcount, hpos;
@@ -147,6 +149,24 @@ __global__ void __launch_bounds__(PJ_THREADS) k_tok_jump(const uint8_t* __restri
     __syncthreads();
     // Pointer jumping. Updates are in place: a reader sees either the old or
     // the new successor, both on the same chain, so the fixed point is exact.
+    // First to the end of each offset's own 2^PJ_SB-byte sub-chunk (v < lim(i)
+    // implies v lies in i's sub-chunk, so nx[v] uses the same threshold): the
+    // sub-chunk exits the token walks start from; then, on those, to the end
+    // of the chunk (<= log2(PJ_NS) more rounds).
+    for (;;) {
+        int moved = 0;
+        for (uint32_t i = threadIdx.x; i < n; i += PJ_THREADS) {
+            const uint32_t lim = min(n, ((i >> PJ_SB) + 1) << PJ_SB);
+            const uint32_t v = nx[i];
+            if (v < lim) {
+                const uint32_t w = nx[v];
+                nx[i] = w;
+                moved |= w < lim;
+            }
+        }
+        if (!__syncthreads_or(moved)) break;
+    }
+    for (uint32_t i = threadIdx.x; i < n; i += PJ_THREADS) subex[P + i] = nx[i];
     for (;;) {
         int moved = 0;
         for (uint32_t i = threadIdx.x; i < n; i += PJ_THREADS) {
@@ -185,6 +205,34 @@ __global__ void __launch_bounds__(PJ_THREADS) k_tok_jump(const uint8_t* __restri
         if (v != PJ_DEAD) dvals[blockIdx.x * PJ_K + atomicAdd(&hpos, 1)] = v;
     }
     if (threadIdx.x == 0) dcount[blockIdx.x] = hc <= PJ_K ? (uint32_t)hc : PJ_MANY;
+}
+
+// Entry of every sub-chunk from its chunk's entry: 32 steps through the
+// sub-exit table per chunk (one thread per chunk); must land on the next
+// chunk's entry.
+__device__ __forceinline__ uint64_t chunk_entry(uint64_t c, uint64_t nc, const uint8_t* glane,
+                                                const uint64_t* gent, const uint64_t* eslow,
+                                                const uint64_t* entry_end);
+__global__ void __launch_bounds__(128) k_tok_sub_entries(uint64_t len, uint64_t nc, const uint8_t* __restrict__ glane,
+                                                         const uint64_t* __restrict__ gent,
+                                                         const uint64_t* __restrict__ eslow,
+                                                         const uint64_t* __restrict__ entry_end,
+                                                         const uint32_t* __restrict__ subex,
+                                                         uint64_t* __restrict__ sent, DevCtl* ctl) {
+    const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    const uint64_t P = c * PJ_C;
+    uint64_t e = chunk_entry(c, nc, glane, gent, eslow, entry_end);
+    for (uint64_t j = 0; j < PJ_NS; ++j) {
+        sent[c * PJ_NS + j] = e;
+        const uint64_t send = min(len, P + ((j + 1) << PJ_SB));
+        if (e < send) {
+            const uint32_t r = subex[e];
+            if (r == PJ_DEAD32) { ctl->aux[1] = 1; return; }
+            e = P + r;
+        }
+    }
+    if (e != chunk_entry(c + 1, nc, glane, gent, eslow, entry_end)) ctl->aux[1] = 1;
 }
 
 // One warp per group of PJ_G chunks; lane = one possible group entry.
@@ -290,62 +338,72 @@ __device__ __forceinline__ uint64_t chunk_entry(uint64_t c, uint64_t nc, const u
     return l == PJ_SLOW ? eslow[c] : gent[c * 32 + l];
 }
 
-// One thread per chunk: walk the chunk's tokens from its entry. EMIT = false
-// verifies and counts (tokens, unpacked bytes); EMIT = true writes the token
+// One thread per sub-chunk: walk its tokens from its entry. EMIT = false
+// verifies (must land exactly on the next sub-chunk's entry, no malformed
+// header) and counts (tokens, unpacked bytes); EMIT = true writes the token
 // table at the scanned offsets.
 template <bool EMIT>
-__global__ void __launch_bounds__(128) k_tok_walk_chunks(const uint8_t* __restrict__ s, uint64_t len, uint64_t nc,
-                                                         const uint8_t* __restrict__ glane,
-                                                         const uint64_t* __restrict__ gent,
-                                                         const uint64_t* __restrict__ eslow,
-                                                         const uint64_t* __restrict__ entry_end,
-                                                         uint64_t* __restrict__ cnt, uint64_t* __restrict__ ub,
-                                                         Token* __restrict__ tok, DevCtl* ctl) {
-    const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (c >= nc) return;
-    const uint64_t E = min(len, (c + 1) * PJ_C);
-    uint64_t p = chunk_entry(c, nc, glane, gent, eslow, entry_end), k = 0, u = 0;
-    if (EMIT) { k = cnt[c]; u = ub[c]; }
-    auto at = [&](uint64_t q) -> uint32_t { return s[q]; };
+__global__ void __launch_bounds__(128) k_tok_walk_subs(const uint8_t* __restrict__ s, uint64_t len, uint64_t ns,
+                                                       const uint64_t* __restrict__ sent,
+                                                       const uint64_t* __restrict__ entry_end,
+                                                       uint64_t* __restrict__ cnt, uint64_t* __restrict__ ub,
+                                                       Token* __restrict__ tok, DevCtl* ctl) {
+    const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (q >= ns) return;
+    const uint64_t E = min(len, (q + 1) << PJ_SB);
+    uint64_t p = sent[q], k = 0, u = 0;
+    if (EMIT) { k = cnt[q]; u = ub[q]; }
+    auto at = [&](uint64_t x) -> uint32_t { return s[x]; };
     while (p < E) {
         uint64_t v;
         uint32_t tag;
-        const uint64_t q = tok_next(at, len, p, v, tag);
-        if (q == PJ_DEAD) { ctl->aux[1] = 1; return; }
-        if (EMIT) {
-            tok[k] = tag ? Token{q - v, u, v | (1ull << 63)} : Token{0, u, v};
-        }
+        const uint64_t nq = tok_next(at, len, p, v, tag);
+        if (nq == PJ_DEAD) { ctl->aux[1] = 1; return; }
+        if (EMIT) tok[k] = tag ? Token{nq - v, u, v | (1ull << 63)} : Token{0, u, v};
         ++k;
         u += v;
-        p = q;
+        p = nq;
     }
     if (!EMIT) {
-        if (p != chunk_entry(c + 1, nc, glane, gent, eslow, entry_end)) ctl->aux[1] = 1;
-        cnt[c] = k;
-        ub[c] = u;
+        if (p != (q + 1 < ns ? sent[q + 1] : *entry_end)) ctl->aux[1] = 1;
+        cnt[q] = k;
+        ub[q] = u;
     }
 }
 
 // Exclusive scan of two u64 arrays in one CTA; totals -> tot[0], tot[1].
+// Segments of 1024 x 4 consecutive entries (coalesced), running carry.
 __global__ void __launch_bounds__(1024) k_scan_pair(uint64_t* __restrict__ a, uint64_t* __restrict__ b,
                                                     uint64_t T, uint64_t* __restrict__ tot) {
+    constexpr int IT = 4;
     using BS = cub::BlockScan<ulonglong2, 1024>;
     __shared__ typename BS::TempStorage tmp;
-    const uint64_t per = (T + 1023) / 1024;
-    const uint64_t t0 = threadIdx.x * per, t1 = min(T, t0 + per);
-    ulonglong2 local = make_ulonglong2(0, 0);
-    for (uint64_t t = t0; t < t1; ++t) { local.x += a[t]; local.y += b[t]; }
-    ulonglong2 excl, total;
     auto add = [](const ulonglong2& x, const ulonglong2& y) { return make_ulonglong2(x.x + y.x, x.y + y.y); };
-    BS(tmp).ExclusiveScan(local, excl, make_ulonglong2(0, 0), add, total);
-    for (uint64_t t = t0; t < t1; ++t) {
-        const uint64_t ca = a[t], cb = b[t];
-        a[t] = excl.x;
-        b[t] = excl.y;
-        excl.x += ca;
-        excl.y += cb;
+    ulonglong2 carry = make_ulonglong2(0, 0);
+    for (uint64_t s0 = 0; s0 < T; s0 += 1024 * IT) {
+        const uint64_t t0 = s0 + (uint64_t)threadIdx.x * IT;
+        ulonglong2 v[IT];
+        ulonglong2 local = make_ulonglong2(0, 0);
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            v[k] = t0 + k < T ? make_ulonglong2(a[t0 + k], b[t0 + k]) : make_ulonglong2(0, 0);
+            local = add(local, v[k]);
+        }
+        ulonglong2 excl, total;
+        BS(tmp).ExclusiveScan(local, excl, make_ulonglong2(0, 0), add, total);
+        excl = add(excl, carry);
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            if (t0 + k < T) {
+                a[t0 + k] = excl.x;
+                b[t0 + k] = excl.y;
+            }
+            excl = add(excl, v[k]);
+        }
+        carry = add(carry, total);
+        __syncthreads();
     }
-    if (threadIdx.x == 0) { tot[0] = total.x; tot[1] = total.y; }
+    if (threadIdx.x == 0) { tot[0] = carry.x; tot[1] = carry.y; }
 }
 
 constexpr int EXP_THREADS = 256;
@@ -514,13 +572,15 @@ static bool parallel_tokens(const uint8_t* d_stream, uint64_t len, Token* tok, S
         UMCG_CUDA(cudaFuncSetAttribute(k_tok_jump, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PJ_SMEM));
         attr = true;
     }
-    const uint64_t nc = cdiv(len, PJ_C), ng = cdiv(nc, PJ_G);
-    // scratch: ex u32[len] | dcount u32[nc] | dvals u64[nc*K] | gent u64[nc*32] | gin, gout u64[ng*32] |
-    //          gn u32[ng] | eslow, cnt, ub u64[nc] | tot u64[2] | entry_end | glane u8[ng]
+    const uint64_t nc = cdiv(len, PJ_C), ng = cdiv(nc, PJ_G), ns = nc * PJ_NS;
+    // scratch: ex, subex u32[len] | dcount u32[nc] | dvals u64[nc*K] | gent u64[nc*32] | gin, gout u64[ng*32] |
+    //          gn u32[ng] | eslow u64[nc] | sent, cnt, ub u64[ns] | tot u64[2] | entry_end | glane u8[ng]
     const uint64_t ex_b = (len * 4 + 7) & ~7ull, dc_b = (nc * 4 + 7) & ~7ull, gn_b = (ng * 4 + 7) & ~7ull;
-    const uint64_t bytes = ex_b + dc_b + nc * PJ_K * 8 + nc * 32 * 8 + ng * 32 * 16 + gn_b + nc * 24 + 24 + ng + 8;
+    const uint64_t bytes = 2 * ex_b + dc_b + nc * PJ_K * 8 + nc * 32 * 8 + ng * 32 * 16 + gn_b + nc * 8 +
+                           ns * 24 + 24 + ng + 8;
     uint8_t* q = sc.parse.as<uint8_t>(bytes);
     uint32_t* ex = reinterpret_cast<uint32_t*>(q); q += ex_b;
+    uint32_t* subex = reinterpret_cast<uint32_t*>(q); q += ex_b;
     uint32_t* dcount = reinterpret_cast<uint32_t*>(q); q += dc_b;
     uint64_t* dvals = reinterpret_cast<uint64_t*>(q); q += nc * PJ_K * 8;
     uint64_t* gent = reinterpret_cast<uint64_t*>(q); q += nc * 32 * 8;
@@ -528,15 +588,16 @@ static bool parallel_tokens(const uint8_t* d_stream, uint64_t len, Token* tok, S
     uint64_t* gout = reinterpret_cast<uint64_t*>(q); q += ng * 32 * 8;
     uint32_t* gn = reinterpret_cast<uint32_t*>(q); q += gn_b;
     uint64_t* eslow = reinterpret_cast<uint64_t*>(q); q += nc * 8;
-    uint64_t* cnt = reinterpret_cast<uint64_t*>(q); q += nc * 8;
-    uint64_t* ub = reinterpret_cast<uint64_t*>(q); q += nc * 8;
+    uint64_t* sent = reinterpret_cast<uint64_t*>(q); q += ns * 8;
+    uint64_t* cnt = reinterpret_cast<uint64_t*>(q); q += ns * 8;
+    uint64_t* ub = reinterpret_cast<uint64_t*>(q); q += ns * 8;
     uint64_t* tot = reinterpret_cast<uint64_t*>(q); q += 16;
     uint64_t* entry_end = reinterpret_cast<uint64_t*>(q); q += 8;
     uint8_t* glane = q;
     UMCG_CUDA(cudaMemsetAsync(&ctl->aux[1], 0, 8, st));
     {
         ProfScope ps("k_tok_jump", st);
-        k_tok_jump<<<(unsigned)nc, PJ_THREADS, PJ_SMEM, st>>>(d_stream, len, ex, dcount, dvals);
+        k_tok_jump<<<(unsigned)nc, PJ_THREADS, PJ_SMEM, st>>>(d_stream, len, ex, dcount, dvals, subex);
         UMCG_LAUNCHED();
     }
     {
@@ -545,20 +606,21 @@ static bool parallel_tokens(const uint8_t* d_stream, uint64_t len, Token* tok, S
         UMCG_LAUNCHED();
         k_tok_resolve<<<1, 1024, 0, st>>>(ex, gin, gout, gn, nc, len, glane, eslow, entry_end, ctl);
         UMCG_LAUNCHED();
-    }
-    const unsigned g = (unsigned)cdiv(nc, 128);
-    {
-        ProfScope ps("k_tok_count", st);
-        k_tok_walk_chunks<false><<<g, 128, 0, st>>>(d_stream, len, nc, glane, gent, eslow, entry_end, cnt, ub,
-                                                    tok, ctl);
+        k_tok_sub_entries<<<(unsigned)cdiv(nc, 128), 128, 0, st>>>(len, nc, glane, gent, eslow, entry_end, subex,
+                                                                     sent, ctl);
         UMCG_LAUNCHED();
     }
-    k_scan_pair<<<1, 1024, 0, st>>>(cnt, ub, nc, tot);
+    const unsigned g = (unsigned)cdiv(ns, 128);
+    {
+        ProfScope ps("k_tok_count", st);
+        k_tok_walk_subs<false><<<g, 128, 0, st>>>(d_stream, len, ns, sent, entry_end, cnt, ub, tok, ctl);
+        UMCG_LAUNCHED();
+    }
+    k_scan_pair<<<1, 1024, 0, st>>>(cnt, ub, ns, tot);
     UMCG_LAUNCHED();
     {
         ProfScope ps("k_tok_emit", st);
-        k_tok_walk_chunks<true><<<g, 128, 0, st>>>(d_stream, len, nc, glane, gent, eslow, entry_end, cnt, ub,
-                                                   tok, ctl);
+        k_tok_walk_subs<true><<<g, 128, 0, st>>>(d_stream, len, ns, sent, entry_end, cnt, ub, tok, ctl);
         UMCG_LAUNCHED();
     }
     struct { uint64_t bad, t[2]; } h;
