@@ -12,6 +12,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include "decode.h"
+#include "scan_tiles.cuh"
 #include <cub/block/block_reduce.cuh>
 
 namespace umcg {
@@ -212,11 +213,16 @@ __device__ __forceinline__ CS thread_counts(const uint8_t* sb, int my, bool* bad
     return CS{c, s};
 }
 
+// Tile aggregates (count, sum of zigzag values); tiles past the stream end
+// (T is a host-side bound when the stream is resolved on the device) add 0.
 __global__ void __launch_bounds__(RT) k_dec_agg(const DecSrc src, CS* __restrict__ aggs, DevCtl* ctl) {
     const uint8_t* U;
     uint64_t ulen;
     resolve_src(src, U, ulen);
-    if ((uint64_t)blockIdx.x * RTILE >= ulen) return;
+    if ((uint64_t)blockIdx.x * RTILE >= ulen) {
+        if (threadIdx.x == 0) aggs[blockIdx.x] = CS{0, 0};
+        return;
+    }
     using BR = cub::BlockReduce<CS, RT>;
     __shared__ typename BR::TempStorage tmp;
     __shared__ __align__(16) uint8_t sb[RHALO + RTILE + 16];
@@ -229,41 +235,6 @@ __global__ void __launch_bounds__(RT) k_dec_agg(const DecSrc src, CS* __restrict
     if (wide) ctl->aux[7] = 1;
     const CS t = BR(tmp).Reduce(mine, CSAdd());
     if (threadIdx.x == 0) aggs[blockIdx.x] = t;
-}
-
-// Exclusive scan of tile aggregates in one CTA; total count -> ctl->count.
-// Segments of 1024 x 4 consecutive aggregates: coalesced loads, one block
-// scan per segment, running carry (the scan is latency-bound: few segments).
-__global__ void __launch_bounds__(1024) k_scan_cs(const DecSrc src, CS* __restrict__ aggs, DevCtl* ctl) {
-    constexpr int IT = 4;
-    using BS = cub::BlockScan<CS, 1024>;
-    __shared__ typename BS::TempStorage tmp;
-    const uint8_t* U;
-    uint64_t ulen;
-    resolve_src(src, U, ulen);
-    const uint64_t T = (ulen + RTILE - 1) / RTILE;
-    CS carry{0, 0};
-    for (uint64_t s0 = 0; s0 < T; s0 += 1024 * IT) {
-        const uint64_t t0 = s0 + (uint64_t)threadIdx.x * IT;
-        CS v[IT];
-        CS local{0, 0};
-#pragma unroll
-        for (int k = 0; k < IT; ++k) {
-            v[k] = t0 + k < T ? aggs[t0 + k] : CS{0, 0};
-            local = CSAdd()(local, v[k]);
-        }
-        CS excl, tot;
-        BS(tmp).ExclusiveScan(local, excl, CS{0, 0}, CSAdd(), tot);
-        excl = CSAdd()(excl, carry);
-#pragma unroll
-        for (int k = 0; k < IT; ++k) {
-            if (t0 + k < T) aggs[t0 + k] = excl;
-            excl = CSAdd()(excl, v[k]);
-        }
-        carry = CSAdd()(carry, tot);
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) ctl->count = carry.cnt;
 }
 
 template <int MODE, class KT>
@@ -516,17 +487,29 @@ __global__ void k_k32_to_f64(const int32_t* __restrict__ K, uint64_t n, double b
 
 }  // namespace
 
-size_t dec_status_bytes(uint64_t ulen) { return (cdiv(ulen, RTILE) + 1) * sizeof(CS); }
+// status: exclusive tile prefixes CS[T + 1] | tile aggregates CS[T]
+size_t dec_status_bytes(uint64_t ulen) {
+    const uint64_t T = cdiv(ulen, RTILE);
+    return (2 * T + 1) * sizeof(CS);
+}
 uint64_t dec_tiles(uint64_t ulen_bound) { return cdiv(ulen_bound, RTILE); }
 
 void dec_prepare(const DecSrc& src, uint64_t T, void* status, DevCtl* ctl, cudaStream_t st) {
     auto* aggs = static_cast<CS*>(status);
-    if (T) {
+    if (!T) {
+        UMCG_CUDA(cudaMemsetAsync(&ctl->count, 0, sizeof(ctl->count), st));
+        return;
+    }
+    CS* raw = aggs + T + 1;
+    {
         ProfScope ps_a("k_dec_agg", st);
-        k_dec_agg<<<(unsigned)T, RT, 0, st>>>(src, aggs, ctl);
+        k_dec_agg<<<(unsigned)T, RT, 0, st>>>(src, raw, ctl);
         UMCG_LAUNCHED();
     }
-    k_scan_cs<<<1, 1024, 0, st>>>(src, aggs, ctl);
+    static_assert(sizeof(CS) == sizeof(ulonglong2), "CS scans as a pair of 64-bit sums");
+    k_scan_tiles<<<scan_tiles_grid(T), SCAN_TILES_THREADS, 0, st>>>(reinterpret_cast<const ulonglong2*>(raw),
+                                                                    reinterpret_cast<ulonglong2*>(aggs), T,
+                                                                    nullptr, &ctl->count);
     UMCG_LAUNCHED();
 }
 

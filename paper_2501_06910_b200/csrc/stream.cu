@@ -7,6 +7,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include "decode.h"
+#include "scan_tiles.cuh"
 
 namespace umcg {
 
@@ -52,6 +53,7 @@ __global__ void k_token_walk(const uint8_t* __restrict__ s, uint64_t len, Token*
     ctl->count = k;
     ctl->aux[0] = u;  // unpacked length
     ctl->aux[1] = !err && pos < len;
+    ctl->aux[2] = pos;  // bytes the probe covered (token density estimate)
 }
 
 // ---------------------------------------------------------------------------
@@ -89,7 +91,7 @@ constexpr uint64_t PJ_DEAD = ~0ull;
 constexpr uint32_t PJ_DEAD32 = 0xFFFFFFFFu;
 constexpr uint32_t PJ_MANY = 0xFFFFFFFFu;
 constexpr uint8_t PJ_SLOW = 0xFF;
-constexpr size_t PJ_SMEM = PJ_C * 4 + PJ_C + PJ_HALO;
+constexpr size_t PJ_SMEM = PJ_C * 4 + PJ_C + PJ_HALO + 16;
 
 // One token header at p (< len), the checks of k_token_walk: next token
 // start, or PJ_DEAD when the header is malformed or the literal overruns.
@@ -112,29 +114,27 @@ __device__ __forceinline__ uint64_t tok_next(At at, uint64_t len, uint64_t p, ui
 
 __global__ void __launch_bounds__(PJ_THREADS) k_tok_jump(const uint8_t* __restrict__ s, uint64_t len,
                                                          uint32_t* __restrict__ ex, uint32_t* __restrict__ dcount,
-                                                         uint64_t* __restrict__ dvals, uint32_t* __restrict__ subex) {
+                                                         uint64_t* __restrict__ dvals, uint32_t* __restrict__ subex,
+                                                         int sb_shift) {
     extern __shared__ __align__(16) uint8_t pj_smem[];
     __shared__ unsigned long long hs[PJ_HS];
     __shared__ int hcount, hpos;
     // nx[i]: successor of offset P + i, relative to P (>= n: an exit; PJ_DEAD32: malformed)
     uint32_t* nx = reinterpret_cast<uint32_t*>(pj_smem);
-    uint8_t* sb = pj_smem + PJ_C * 4;
     const uint64_t P = blockIdx.x * PJ_C;
     const uint64_t E = min(len, P + PJ_C);
     const uint32_t n = (uint32_t)(E - P);
+    // bytes [P, P + C + HALO) staged by aligned 16-byte loads from the 16-byte
+    // boundary at or below s + P (the stream sits at any offset of the
+    // archive); sb[k] = s[P + k]
+    const uint32_t sh = (uint32_t)((uintptr_t)(s + P) & 15);
+    uint8_t* sb = pj_smem + PJ_C * 4 + sh;
     {
-        // bytes [P, P + C + HALO): 16-byte loads where aligned
-        const uint8_t* src = s + P;
-        const uint64_t avail = len - P;
-        const uint32_t want = (uint32_t)min((uint64_t)(PJ_C + PJ_HALO), avail);
-        if (((uintptr_t)src & 15) == 0) {
-            for (uint32_t w = threadIdx.x; w < want / 16; w += PJ_THREADS)
-                reinterpret_cast<uint4*>(sb)[w] = __ldg(reinterpret_cast<const uint4*>(src) + w);
-            for (uint32_t i = (want & ~15u) + threadIdx.x; i < PJ_C + PJ_HALO; i += PJ_THREADS)
-                sb[i] = i < want ? src[i] : 0;
-        } else {
-            for (uint32_t i = threadIdx.x; i < PJ_C + PJ_HALO; i += PJ_THREADS) sb[i] = i < want ? src[i] : 0;
-        }
+        const uint4* src = reinterpret_cast<const uint4*>(s + P - sh);
+        const uint32_t want = (uint32_t)min((uint64_t)(PJ_C + PJ_HALO), len - P);
+        const uint32_t nw = (sh + want + 15) / 16;
+        for (uint32_t w = threadIdx.x; w < nw; w += PJ_THREADS)
+            reinterpret_cast<uint4*>(pj_smem + PJ_C * 4)[w] = __ldg(src + w);
     }
     for (int i = threadIdx.x; i < PJ_HS; i += PJ_THREADS) hs[i] = PJ_DEAD;
     if (threadIdx.x == 0) hcount = hpos = 0;
@@ -153,20 +153,22 @@ __global__ void __launch_bounds__(PJ_THREADS) k_tok_jump(const uint8_t* __restri
     // implies v lies in i's sub-chunk, so nx[v] uses the same threshold): the
     // sub-chunk exits the token walks start from; then, on those, to the end
     // of the chunk (<= log2(PJ_NS) more rounds).
-    for (;;) {
-        int moved = 0;
-        for (uint32_t i = threadIdx.x; i < n; i += PJ_THREADS) {
-            const uint32_t lim = min(n, ((i >> PJ_SB) + 1) << PJ_SB);
-            const uint32_t v = nx[i];
-            if (v < lim) {
-                const uint32_t w = nx[v];
-                nx[i] = w;
-                moved |= w < lim;
+    if (subex) {
+        for (;;) {
+            int moved = 0;
+            for (uint32_t i = threadIdx.x; i < n; i += PJ_THREADS) {
+                const uint32_t lim = min(n, ((i >> sb_shift) + 1) << sb_shift);
+                const uint32_t v = nx[i];
+                if (v < lim) {
+                    const uint32_t w = nx[v];
+                    nx[i] = w;
+                    moved |= w < lim;
+                }
             }
+            if (!__syncthreads_or(moved)) break;
         }
-        if (!__syncthreads_or(moved)) break;
+        for (uint32_t i = threadIdx.x; i < n; i += PJ_THREADS) subex[P + i] = nx[i];
     }
-    for (uint32_t i = threadIdx.x; i < n; i += PJ_THREADS) subex[P + i] = nx[i];
     for (;;) {
         int moved = 0;
         for (uint32_t i = threadIdx.x; i < n; i += PJ_THREADS) {
@@ -217,15 +219,20 @@ __global__ void __launch_bounds__(128) k_tok_sub_entries(uint64_t len, uint64_t 
                                                          const uint64_t* __restrict__ gent,
                                                          const uint64_t* __restrict__ eslow,
                                                          const uint64_t* __restrict__ entry_end,
-                                                         const uint32_t* __restrict__ subex,
+                                                         const uint32_t* __restrict__ subex, int sb_shift,
                                                          uint64_t* __restrict__ sent, DevCtl* ctl) {
     const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (c >= nc) return;
     const uint64_t P = c * PJ_C;
     uint64_t e = chunk_entry(c, nc, glane, gent, eslow, entry_end);
-    for (uint64_t j = 0; j < PJ_NS; ++j) {
-        sent[c * PJ_NS + j] = e;
-        const uint64_t send = min(len, P + ((j + 1) << PJ_SB));
+    if (!subex) {  // chunk-level walks
+        sent[c] = e;
+        return;
+    }
+    const uint64_t nsub = PJ_C >> sb_shift;
+    for (uint64_t j = 0; j < nsub; ++j) {
+        sent[c * nsub + j] = e;
+        const uint64_t send = min(len, P + ((j + 1) << sb_shift));
         if (e < send) {
             const uint32_t r = subex[e];
             if (r == PJ_DEAD32) { ctl->aux[1] = 1; return; }
@@ -342,68 +349,58 @@ __device__ __forceinline__ uint64_t chunk_entry(uint64_t c, uint64_t nc, const u
 // verifies (must land exactly on the next sub-chunk's entry, no malformed
 // header) and counts (tokens, unpacked bytes); EMIT = true writes the token
 // table at the scanned offsets.
+// Count pass (EMIT false): per sub-chunk token count and unpacked bytes
+// (cnt, ub) and their per-block sums (bsum); emit pass: block scan of (cnt,
+// ub) + the block's prefix (bpre, k_scan_tiles of bsum) = the sub-chunk's
+// first token index and unpacked offset.
 template <bool EMIT>
 __global__ void __launch_bounds__(128) k_tok_walk_subs(const uint8_t* __restrict__ s, uint64_t len, uint64_t ns,
-                                                       const uint64_t* __restrict__ sent,
+                                                       int shift, const uint64_t* __restrict__ sent,
                                                        const uint64_t* __restrict__ entry_end,
                                                        uint64_t* __restrict__ cnt, uint64_t* __restrict__ ub,
+                                                       ulonglong2* __restrict__ bsum,
+                                                       const ulonglong2* __restrict__ bpre,
                                                        Token* __restrict__ tok, DevCtl* ctl) {
+    using BS = cub::BlockScan<ulonglong2, 128>;
+    using BR = cub::BlockReduce<ulonglong2, 128>;
+    __shared__ union {
+        typename BS::TempStorage s;
+        typename BR::TempStorage r;
+    } tmp;
     const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (q >= ns) return;
-    const uint64_t E = min(len, (q + 1) << PJ_SB);
-    uint64_t p = sent[q], k = 0, u = 0;
-    if (EMIT) { k = cnt[q]; u = ub[q]; }
-    auto at = [&](uint64_t x) -> uint32_t { return s[x]; };
-    while (p < E) {
-        uint64_t v;
-        uint32_t tag;
-        const uint64_t nq = tok_next(at, len, p, v, tag);
-        if (nq == PJ_DEAD) { ctl->aux[1] = 1; return; }
-        if (EMIT) tok[k] = tag ? Token{nq - v, u, v | (1ull << 63)} : Token{0, u, v};
-        ++k;
-        u += v;
-        p = nq;
+    uint64_t k = 0, u = 0;
+    if (EMIT) {
+        const ulonglong2 mine = q < ns ? make_ulonglong2(cnt[q], ub[q]) : make_ulonglong2(0, 0);
+        ulonglong2 ex;
+        BS(tmp.s).ExclusiveScan(mine, ex, make_ulonglong2(0, 0), u2_add_op{});
+        const ulonglong2 b = bpre[blockIdx.x];
+        k = b.x + ex.x;
+        u = b.y + ex.y;
+    }
+    if (q < ns) {
+        const uint64_t E = min(len, (q + 1) << shift);
+        uint64_t p = sent[q];
+        auto at = [&](uint64_t x) -> uint32_t { return s[x]; };
+        while (p < E) {
+            uint64_t v;
+            uint32_t tag;
+            const uint64_t nq = tok_next(at, len, p, v, tag);
+            if (nq == PJ_DEAD) { ctl->aux[1] = 1; break; }
+            if (EMIT) tok[k] = tag ? Token{nq - v, u, v | (1ull << 63)} : Token{0, u, v};
+            ++k;
+            u += v;
+            p = nq;
+        }
+        if (!EMIT) {
+            if (p != (q + 1 < ns ? sent[q + 1] : *entry_end)) ctl->aux[1] = 1;
+            cnt[q] = k;
+            ub[q] = u;
+        }
     }
     if (!EMIT) {
-        if (p != (q + 1 < ns ? sent[q + 1] : *entry_end)) ctl->aux[1] = 1;
-        cnt[q] = k;
-        ub[q] = u;
+        const ulonglong2 t = BR(tmp.r).Reduce(make_ulonglong2(k, u), u2_add_op{});
+        if (threadIdx.x == 0) bsum[blockIdx.x] = t;
     }
-}
-
-// Exclusive scan of two u64 arrays in one CTA; totals -> tot[0], tot[1].
-// Segments of 1024 x 4 consecutive entries (coalesced), running carry.
-__global__ void __launch_bounds__(1024) k_scan_pair(uint64_t* __restrict__ a, uint64_t* __restrict__ b,
-                                                    uint64_t T, uint64_t* __restrict__ tot) {
-    constexpr int IT = 4;
-    using BS = cub::BlockScan<ulonglong2, 1024>;
-    __shared__ typename BS::TempStorage tmp;
-    auto add = [](const ulonglong2& x, const ulonglong2& y) { return make_ulonglong2(x.x + y.x, x.y + y.y); };
-    ulonglong2 carry = make_ulonglong2(0, 0);
-    for (uint64_t s0 = 0; s0 < T; s0 += 1024 * IT) {
-        const uint64_t t0 = s0 + (uint64_t)threadIdx.x * IT;
-        ulonglong2 v[IT];
-        ulonglong2 local = make_ulonglong2(0, 0);
-#pragma unroll
-        for (int k = 0; k < IT; ++k) {
-            v[k] = t0 + k < T ? make_ulonglong2(a[t0 + k], b[t0 + k]) : make_ulonglong2(0, 0);
-            local = add(local, v[k]);
-        }
-        ulonglong2 excl, total;
-        BS(tmp).ExclusiveScan(local, excl, make_ulonglong2(0, 0), add, total);
-        excl = add(excl, carry);
-#pragma unroll
-        for (int k = 0; k < IT; ++k) {
-            if (t0 + k < T) {
-                a[t0 + k] = excl.x;
-                b[t0 + k] = excl.y;
-            }
-            excl = add(excl, v[k]);
-        }
-        carry = add(carry, total);
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) { tot[0] = carry.x; tot[1] = carry.y; }
 }
 
 constexpr int EXP_THREADS = 256;
@@ -565,20 +562,30 @@ __global__ void __launch_bounds__(VD_THREADS) k_varint_decode(const uint8_t* __r
 }  // namespace
 
 // Parallel parse; returns false when the chain is broken (corrupt stream).
+// fine: token-dense stream (the probe saw > 1 token per KiB): token walks
+// per 256-byte sub-chunk (exits from the same pointer jumping); otherwise per
+// 8 KiB chunk, without the sub-exit table.
 static bool parallel_tokens(const uint8_t* d_stream, uint64_t len, Token* tok, StreamDecScratch& sc, DevCtl* ctl,
-                            cudaStream_t st, uint64_t* ntok, uint64_t* ulen) {
+                            cudaStream_t st, uint64_t* ntok, uint64_t* ulen, bool fine) {
     static bool attr = false;
     if (!attr) {
         UMCG_CUDA(cudaFuncSetAttribute(k_tok_jump, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PJ_SMEM));
         attr = true;
     }
-    const uint64_t nc = cdiv(len, PJ_C), ng = cdiv(nc, PJ_G), ns = nc * PJ_NS;
-    // scratch: ex, subex u32[len] | dcount u32[nc] | dvals u64[nc*K] | gent u64[nc*32] | gin, gout u64[ng*32] |
-    //          gn u32[ng] | eslow u64[nc] | sent, cnt, ub u64[ns] | tot u64[2] | entry_end | glane u8[ng]
+    const int shift = fine ? PJ_SB : 13;  // 2^13 == PJ_C
+    static_assert(PJ_C == (1ull << 13), "chunk-level walks use shift 13");
+    const uint64_t nc = cdiv(len, PJ_C), ng = cdiv(nc, PJ_G), ns = nc * (PJ_C >> shift);
+    // scratch: tot u64[2] | bsum, bpre u64[2][g] (16-byte aligned at the base) | ex, subex u32[len] |
+    //          dcount u32[nc] | dvals u64[nc*K] | gent u64[nc*32] | gin, gout u64[ng*32] | gn u32[ng] |
+    //          eslow u64[nc] | sent, cnt, ub u64[ns] | entry_end | glane u8[ng]
+    const uint64_t g = cdiv(ns, 128);
     const uint64_t ex_b = (len * 4 + 7) & ~7ull, dc_b = (nc * 4 + 7) & ~7ull, gn_b = (ng * 4 + 7) & ~7ull;
     const uint64_t bytes = 2 * ex_b + dc_b + nc * PJ_K * 8 + nc * 32 * 8 + ng * 32 * 16 + gn_b + nc * 8 +
-                           ns * 24 + 24 + ng + 8;
+                           ns * 24 + 24 + ng + 8 + g * 32;
     uint8_t* q = sc.parse.as<uint8_t>(bytes);
+    uint64_t* tot = reinterpret_cast<uint64_t*>(q); q += 16;
+    ulonglong2* bsum = reinterpret_cast<ulonglong2*>(q); q += g * 16;
+    ulonglong2* bpre = reinterpret_cast<ulonglong2*>(q); q += g * 16;
     uint32_t* ex = reinterpret_cast<uint32_t*>(q); q += ex_b;
     uint32_t* subex = reinterpret_cast<uint32_t*>(q); q += ex_b;
     uint32_t* dcount = reinterpret_cast<uint32_t*>(q); q += dc_b;
@@ -591,13 +598,13 @@ static bool parallel_tokens(const uint8_t* d_stream, uint64_t len, Token* tok, S
     uint64_t* sent = reinterpret_cast<uint64_t*>(q); q += ns * 8;
     uint64_t* cnt = reinterpret_cast<uint64_t*>(q); q += ns * 8;
     uint64_t* ub = reinterpret_cast<uint64_t*>(q); q += ns * 8;
-    uint64_t* tot = reinterpret_cast<uint64_t*>(q); q += 16;
     uint64_t* entry_end = reinterpret_cast<uint64_t*>(q); q += 8;
     uint8_t* glane = q;
     UMCG_CUDA(cudaMemsetAsync(&ctl->aux[1], 0, 8, st));
     {
         ProfScope ps("k_tok_jump", st);
-        k_tok_jump<<<(unsigned)nc, PJ_THREADS, PJ_SMEM, st>>>(d_stream, len, ex, dcount, dvals, subex);
+        k_tok_jump<<<(unsigned)nc, PJ_THREADS, PJ_SMEM, st>>>(d_stream, len, ex, dcount, dvals,
+                                                              fine ? subex : nullptr, shift);
         UMCG_LAUNCHED();
     }
     {
@@ -606,21 +613,23 @@ static bool parallel_tokens(const uint8_t* d_stream, uint64_t len, Token* tok, S
         UMCG_LAUNCHED();
         k_tok_resolve<<<1, 1024, 0, st>>>(ex, gin, gout, gn, nc, len, glane, eslow, entry_end, ctl);
         UMCG_LAUNCHED();
-        k_tok_sub_entries<<<(unsigned)cdiv(nc, 128), 128, 0, st>>>(len, nc, glane, gent, eslow, entry_end, subex,
-                                                                     sent, ctl);
+        k_tok_sub_entries<<<(unsigned)cdiv(nc, 128), 128, 0, st>>>(len, nc, glane, gent, eslow, entry_end,
+                                                                     fine ? subex : nullptr, shift, sent, ctl);
         UMCG_LAUNCHED();
     }
-    const unsigned g = (unsigned)cdiv(ns, 128);
     {
         ProfScope ps("k_tok_count", st);
-        k_tok_walk_subs<false><<<g, 128, 0, st>>>(d_stream, len, ns, sent, entry_end, cnt, ub, tok, ctl);
+        k_tok_walk_subs<false><<<(unsigned)g, 128, 0, st>>>(d_stream, len, ns, shift, sent, entry_end, cnt, ub, bsum, bpre,
+                                                  tok, ctl);
         UMCG_LAUNCHED();
     }
-    k_scan_pair<<<1, 1024, 0, st>>>(cnt, ub, ns, tot);
+    k_scan_tiles<<<scan_tiles_grid(g), SCAN_TILES_THREADS, 0, st>>>(bsum, bpre, g,
+                                                                    reinterpret_cast<ulonglong2*>(tot), nullptr);
     UMCG_LAUNCHED();
     {
         ProfScope ps("k_tok_emit", st);
-        k_tok_walk_subs<true><<<g, 128, 0, st>>>(d_stream, len, ns, sent, entry_end, cnt, ub, tok, ctl);
+        k_tok_walk_subs<true><<<(unsigned)g, 128, 0, st>>>(d_stream, len, ns, shift, sent, entry_end, cnt, ub, bsum, bpre,
+                                                 tok, ctl);
         UMCG_LAUNCHED();
     }
     struct { uint64_t bad, t[2]; } h;
@@ -656,7 +665,8 @@ const uint8_t* stream_unpack(const uint8_t* d_stream, uint64_t len, StreamDecScr
     UMCG_CUDA(cudaStreamSynchronize(st));
     uint64_t ntok = h.c.count, ulen = h.c.aux[0];
     if (!h.c.err && h.c.aux[1]) {
-        if (!parallel_tokens(d_stream, len, tok, sc, ctl, st, &ntok, &ulen)) {
+        const bool fine = h.c.aux[2] < 64 * 1024;  // the probe's 64 tokens spanned < 64 KiB
+        if (!parallel_tokens(d_stream, len, tok, sc, ctl, st, &ntok, &ulen, fine)) {
             // broken chain: the serial walk reports the reference's error
             k_token_walk<<<1, 32, 0, st>>>(d_stream, len, tok, tok_cap, ~0ull, ctl);
             UMCG_LAUNCHED();
