@@ -107,6 +107,15 @@ __device__ __forceinline__ uint64_t state_pos(const RleState& s, const uint64_t*
     return s.has ? s.C + 1 + vlen64(lit_total[s.origin]) + s.Lb : s.C;
 }
 
+// Stream position of every tile's first byte (pos[T] = stream length), so
+// the writers start from one load instead of a chain of dependent ones.
+__global__ void k_rle_pos(const RleState* __restrict__ states, const uint64_t* __restrict__ lit_total, uint64_t T,
+                          const DevCtl* __restrict__ ctl, int comp, uint64_t* __restrict__ pos) {
+    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (t < T) pos[t] = state_pos(states[t], lit_total);
+    else if (t == T) pos[t] = ctl->stream_len[comp];
+}
+
 // Byte writer into the staging buffer (no bounds checks: the tile's output
 // fits CAP by construction). Returns the varint length.
 template <class T>
@@ -131,6 +140,14 @@ __device__ __forceinline__ uint32_t put_code(uint8_t* o, T v) {
         o[0] = (uint8_t)v;
         return 1u;
     }
+    if (sizeof(T) == 2) {  // <= 3 bytes, no loop
+        const uint32_t x = (uint32_t)v;
+        const bool b2 = x >= 0x80, b3 = x >= 0x4000;
+        o[0] = (uint8_t)(x | (b2 ? 0x80u : 0u));
+        if (b2) o[1] = (uint8_t)((x >> 7) | (b3 ? 0x80u : 0u));
+        if (b3) o[2] = (uint8_t)(x >> 14);
+        return 1u + b2 + b3;
+    }
     return put_varint(o, v);
 }
 
@@ -152,10 +169,11 @@ __device__ __forceinline__ void copy_out16(const uint8_t* out, uint32_t ao, uint
 }
 
 template <class T>
-__global__ void __launch_bounds__(ENC_THREADS) k_rle_write_fast(const T* __restrict__ codes, uint64_t n,
+__global__ void __launch_bounds__(ENC_THREADS, 6) k_rle_write_fast(const T* __restrict__ codes, uint64_t n,
                                                                const RleState* __restrict__ states,
                                                                const RleSum* __restrict__ sums,
                                                                const uint64_t* __restrict__ lit_total,
+                                                               const uint64_t* __restrict__ tpos,
                                                                const DevCtl* __restrict__ ctl, int comp,
                                                                uint8_t* __restrict__ dst, int off_from_ctl) {
     constexpr uint32_t CAP = ENC_TILE * (sizeof(T) == 8 ? 10 : 5) + 96;
@@ -164,31 +182,37 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_write_fast(const T* __restr
     __shared__ __align__(16) uint8_t out[CAP];
 
     const uint64_t tile = blockIdx.x;
+    // every load up front (codes too: they do not depend on the tile's kind)
+    const uint64_t first = tile * ENC_TILE + (uint64_t)threadIdx.x * ENC_ITEMS;
+    T v[ENC_ITEMS];
+    const int cnt = load_items(codes, n, first, v);
     const RleSum S = sums[tile];
+    const RleState entry = states[tile];
+    const uint64_t P0 = tpos[tile], P1 = tpos[tile + 1];
     if (S.has_int() || S.allzero()) return;  // general writer (or nothing to write)
     const uint64_t T_ = (n + ENC_TILE - 1) / ENC_TILE;
     const bool last = tile == T_ - 1;
-    const RleState entry = states[tile];
-    const uint64_t P0 = state_pos(entry, lit_total);
-    const uint64_t P1 = last ? ctl->stream_len[comp] : state_pos(states[tile + 1], lit_total);
     const uint32_t len = (uint32_t)(P1 - P0);
     uint8_t* d = dst + (off_from_ctl ? ctl->stream_off[comp] : 0) + P0;
     const uint32_t ao = (uint32_t)((uintptr_t)d & 15);
     uint8_t* o = out + ao - 0;  // o[pos - P0] is the staged byte of stream position pos
 
-    const uint64_t first = tile * ENC_TILE + (uint64_t)threadIdx.x * ENC_ITEMS;
-    T v[ENC_ITEMS];
-    const int cnt = load_items(codes, n, first, v);
-
     // the core [lz, tile_cnt - tz) is one literal segment
     const uint32_t tile_cnt = (uint32_t)min((uint64_t)ENC_TILE, n - tile * ENC_TILE);
     const uint32_t core_lo = (uint32_t)S.lz, core_hi = tile_cnt - (uint32_t)S.tz;
     const uint32_t r0 = threadIdx.x * ENC_ITEMS;
+    // common case: all of the thread's items are in the core (no per-item checks)
+    const bool inner = cnt == ENC_ITEMS && r0 >= core_lo && r0 + ENC_ITEMS <= core_hi;
     uint32_t w = 0;
+    if (inner) {
 #pragma unroll
-    for (int k = 0; k < ENC_ITEMS; ++k) {
-        const uint32_t r = r0 + k;
-        if (k < cnt && r >= core_lo && r < core_hi) w += clen(v[k]);
+        for (int k = 0; k < ENC_ITEMS; ++k) w += clen(v[k]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < ENC_ITEMS; ++k) {
+            const uint32_t r = r0 + k;
+            if (k < cnt && r >= core_lo && r < core_hi) w += clen(v[k]);
+        }
     }
     uint32_t off, core_total;
     BS32(tmp).ExclusiveSum(w, off, core_total);
@@ -204,7 +228,7 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_write_fast(const T* __restr
         totn = lit_total[tile];
         data_base = lpos + 1 + vlen64(totn);
     } else if (entry.has) {
-        zero_pos = entry.C + 1 + vlen64(lit_total[entry.origin]) + entry.Lb;
+        zero_pos = P0;  // == state_pos(entry): the open literal's bytes so far
         data_base = zero_pos + J0;
     } else {
         lpos = entry.C;
@@ -235,10 +259,15 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_write_fast(const T* __restr
         }
     }
     uint32_t pos = (uint32_t)(data_base - P0) + off;
+    if (inner) {
 #pragma unroll
-    for (int k = 0; k < ENC_ITEMS; ++k) {
-        const uint32_t r = r0 + k;
-        if (k < cnt && r >= core_lo && r < core_hi) pos += put_code(o + pos, v[k]);
+        for (int k = 0; k < ENC_ITEMS; ++k) pos += put_code(o + pos, v[k]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < ENC_ITEMS; ++k) {
+            const uint32_t r = r0 + k;
+            if (k < cnt && r >= core_lo && r < core_hi) pos += put_code(o + pos, v[k]);
+        }
     }
     __syncthreads();
     copy_out16(out, ao, len, d);
@@ -255,11 +284,12 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_write_fast(const T* __restr
 //   4. prefix of unit bytes U_j              -> output positions
 // (literals still open at the tile end take T from lit_total[tile]).
 template <class T>
-__global__ void __launch_bounds__(ENC_THREADS) k_rle_write_general(const T* __restrict__ codes, uint64_t n,
+__global__ void __launch_bounds__(ENC_THREADS, 6) k_rle_write_general(const T* __restrict__ codes, uint64_t n,
                                                            const RleState* __restrict__ states,
                                                            const RleSum* __restrict__ sums,
                                                            const uint64_t* __restrict__ lit_total,
                                                            const DevCtl* __restrict__ ctl, int comp, const uint32_t* __restrict__ glist,
+                                                           const uint64_t* __restrict__ tpos,
                                                            uint8_t* __restrict__ dst, int off_from_ctl) {
     constexpr uint32_t CAP = ENC_TILE * (sizeof(T) == 8 ? 10 : 5) + 96;
     constexpr int NONE = 0x7fffffff;
@@ -278,8 +308,7 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_write_general(const T* __re
     const uint64_t T_ = (n + ENC_TILE - 1) / ENC_TILE;
     const bool last = tile == T_ - 1;
     const RleState E = states[tile];
-    const uint64_t P0 = state_pos(E, lit_total);
-    const uint64_t P1 = last ? ctl->stream_len[comp] : state_pos(states[tile + 1], lit_total);
+    const uint64_t P0 = tpos[tile], P1 = tpos[tile + 1];
     const uint32_t len = (uint32_t)(P1 - P0);
     if (len == 0) return;  // all-zero tile: its zeros stay pending
     uint8_t* d = dst + (off_from_ctl ? ctl->stream_off[comp] : 0) + P0;
@@ -290,6 +319,10 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_write_general(const T* __re
     const int r0 = threadIdx.x * ENC_ITEMS;
     T v[ENC_ITEMS];
     const int cnt = load_items(codes, n, tile * ENC_TILE + (uint64_t)r0, v);
+    // zero-filled staging: short zero runs inside literals are then skipped
+    // (the first __syncthreads below orders this before every byte write)
+    for (uint32_t w = threadIdx.x; w < CAP / 16; w += ENC_THREADS)
+        reinterpret_cast<uint4*>(out)[w] = make_uint4(0, 0, 0, 0);
     uint32_t nzm = 0;
 #pragma unroll
     for (int k = 0; k < ENC_ITEMS; ++k) nzm |= (k < cnt && v[k] != 0) ? (1u << k) : 0u;
@@ -378,8 +411,7 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_write_general(const T* __re
                 o[pos] = 0x01;
                 pos += 1 + put_varint(o + pos + 1, lit_T(k));
             }
-            if (!lng)
-                for (uint32_t z = 0; z < (uint32_t)J; ++z) o[pos++] = 0;
+            if (!lng) pos += (uint32_t)J;  // zero bytes (pre-filled)
             pos += put_code(o + pos, v[k]);
             prev = r0 + k;
         }
@@ -408,7 +440,7 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_write_general(const T* __re
 
 size_t stream_enc_scratch_bytes(uint64_t n) {
     const uint64_t T = cdiv(n, ENC_TILE) + 1;
-    return T * (2 * sizeof(RleSum) + sizeof(RleState) + sizeof(uint64_t) + sizeof(uint32_t)) + 4096;
+    return T * (2 * sizeof(RleSum) + sizeof(RleState) + 2 * sizeof(uint64_t) + sizeof(uint32_t)) + 4096;
 }
 
 StreamEncScratch stream_enc_carve(void* base, uint64_t n) {
@@ -422,6 +454,8 @@ StreamEncScratch stream_enc_carve(void* base, uint64_t n) {
     s.states = reinterpret_cast<RleState*>(p);
     p += T * sizeof(RleState);
     s.lit_total = reinterpret_cast<uint64_t*>(p);
+    p += T * sizeof(uint64_t);
+    s.pos = reinterpret_cast<uint64_t*>(p);
     p += T * sizeof(uint64_t);
     s.glist = reinterpret_cast<uint32_t*>(p);
     return s;
@@ -468,11 +502,13 @@ static void write_impl(const T* codes, uint64_t n, const StreamEncScratch& s, De
     const uint64_t T_ = cdiv(n, ENC_TILE);
     if (!T_) return;
     ProfScope ps_("k_rle_write", st);
-    k_rle_write_fast<T><<<(unsigned)T_, ENC_THREADS, 0, st>>>(codes, n, s.states, s.sums, s.lit_total, ctl, comp,
-                                                              dst, off_ctl ? 1 : 0);
+    k_rle_pos<<<(unsigned)cdiv(T_ + 1, 256), 256, 0, st>>>(s.states, s.lit_total, T_, ctl, comp, s.pos);
+    UMCG_LAUNCHED();
+    k_rle_write_fast<T><<<(unsigned)T_, ENC_THREADS, 0, st>>>(codes, n, s.states, s.sums, s.lit_total, s.pos, ctl,
+                                                              comp, dst, off_ctl ? 1 : 0);
     UMCG_LAUNCHED();
     k_rle_write_general<T><<<(unsigned)T_, ENC_THREADS, 0, st>>>(codes, n, s.states, s.sums, s.lit_total, ctl,
-                                                                 comp, s.glist, dst, off_ctl ? 1 : 0);
+                                                                 comp, s.glist, s.pos, dst, off_ctl ? 1 : 0);
     UMCG_LAUNCHED();
 }
 

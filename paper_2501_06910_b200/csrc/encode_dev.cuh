@@ -17,6 +17,7 @@ struct RleComposeOp {
 template <class T>
 __device__ __forceinline__ uint32_t clen(T v) {
     if (sizeof(T) == 1) return 1u;
+    if (sizeof(T) == 2) return 1u + (v >= 0x80) + (v >= 0x4000);
     return v == 0 ? 1u : vlen64((uint64_t)v);
 }
 

@@ -17,6 +17,7 @@ struct StreamEncScratch {
     RleSum* sums = nullptr;         // [T]   tile summaries
     RleState* states = nullptr;     // [T+1] entry state per tile (+ final)
     uint64_t* lit_total = nullptr;  // [T]   literal byte totals, keyed by opening tile
+    uint64_t* pos = nullptr;        // [T+1] stream position of each tile's first byte (writers)
     uint32_t* glist = nullptr;      // [T]   tiles for the general writer (count in ctl->aux[4+comp])
 };
 size_t stream_enc_scratch_bytes(uint64_t n);

@@ -114,8 +114,7 @@ __device__ __forceinline__ uint64_t tok_next(At at, uint64_t len, uint64_t p, ui
 
 __global__ void __launch_bounds__(PJ_THREADS) k_tok_jump(const uint8_t* __restrict__ s, uint64_t len,
                                                          uint32_t* __restrict__ ex, uint32_t* __restrict__ dcount,
-                                                         uint64_t* __restrict__ dvals, uint32_t* __restrict__ subex,
-                                                         int sb_shift) {
+                                                         uint64_t* __restrict__ dvals, uint32_t* __restrict__ subex) {
     extern __shared__ __align__(16) uint8_t pj_smem[];
     __shared__ unsigned long long hs[PJ_HS];
     __shared__ int hcount, hpos;
@@ -124,51 +123,69 @@ __global__ void __launch_bounds__(PJ_THREADS) k_tok_jump(const uint8_t* __restri
     const uint64_t P = blockIdx.x * PJ_C;
     const uint64_t E = min(len, P + PJ_C);
     const uint32_t n = (uint32_t)(E - P);
-    // bytes [P, P + C + HALO) staged by aligned 16-byte loads from the 16-byte
-    // boundary at or below s + P (the stream sits at any offset of the
-    // archive); sb[k] = s[P + k]
+    // Warp w owns sub-chunk w (2^PJ_SB offsets) up to the sub-chunk exits:
+    // staging, successors and the first jumping rounds are warp-local.
+    // Bytes come by aligned 16-byte loads from the 16-byte boundary at or
+    // below s + P (the stream sits at any offset of the archive): sb[k] =
+    // s[P + k] for the warp's [2^PJ_SB w, 2^PJ_SB (w + 1) + HALO).
+    static_assert(PJ_NS * 32 == PJ_THREADS, "one warp per sub-chunk");
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t sh = (uint32_t)((uintptr_t)(s + P) & 15);
-    uint8_t* sb = pj_smem + PJ_C * 4 + sh;
+    uint8_t* raw = pj_smem + PJ_C * 4;
+    uint8_t* sb = raw + sh;
+    const uint32_t s0 = (uint32_t)warp << PJ_SB, s1 = min(n, s0 + (1u << PJ_SB));
     {
         const uint4* src = reinterpret_cast<const uint4*>(s + P - sh);
         const uint32_t want = (uint32_t)min((uint64_t)(PJ_C + PJ_HALO), len - P);
         const uint32_t nw = (sh + want + 15) / 16;
-        for (uint32_t w = threadIdx.x; w < nw; w += PJ_THREADS)
-            reinterpret_cast<uint4*>(pj_smem + PJ_C * 4)[w] = __ldg(src + w);
+        const uint32_t w0 = (s0 + sh) / 16, w1 = min(nw, (s0 + (1u << PJ_SB) + PJ_HALO + sh + 15) / 16);
+        for (uint32_t w = w0 + lane; w < w1; w += 32) reinterpret_cast<uint4*>(raw)[w] = __ldg(src + w);
     }
     for (int i = threadIdx.x; i < PJ_HS; i += PJ_THREADS) hs[i] = PJ_DEAD;
     if (threadIdx.x == 0) hcount = hpos = 0;
-    __syncthreads();
+    __syncwarp();
     auto at = [&](uint64_t q) -> uint32_t { return sb[q - P]; };
-    for (uint32_t i = threadIdx.x; i < n; i += PJ_THREADS) {
-        uint64_t v;
-        uint32_t tag;
-        const uint64_t q = tok_next(at, len, P + i, v, tag);
-        nx[i] = q == PJ_DEAD ? PJ_DEAD32 : (uint32_t)(q - P);
+    const uint64_t rem = len - P;  // bytes from the chunk start to the stream end
+    for (uint32_t i = s0 + lane; i < s1; i += 32) {
+        // common case first: a 1-byte varint (32-bit offsets, rem >= i + 2)
+        const uint32_t tag = sb[i], b = sb[i + 1];
+        uint32_t r;
+        if (tag > 1) {
+            r = PJ_DEAD32;
+        } else if (b < 0x80 && i + 2 <= rem) {
+            const uint64_t e = (uint64_t)i + 2 + (tag ? b : 0);
+            r = e > rem ? PJ_DEAD32 : (uint32_t)e;
+        } else {
+            uint64_t v;
+            uint32_t tg;
+            const uint64_t q = tok_next(at, len, P + i, v, tg);
+            r = q == PJ_DEAD ? PJ_DEAD32 : (uint32_t)(q - P);
+        }
+        nx[i] = r;
     }
-    __syncthreads();
+    __syncwarp();
     // Pointer jumping. Updates are in place: a reader sees either the old or
     // the new successor, both on the same chain, so the fixed point is exact.
-    // First to the end of each offset's own 2^PJ_SB-byte sub-chunk (v < lim(i)
-    // implies v lies in i's sub-chunk, so nx[v] uses the same threshold): the
-    // sub-chunk exits the token walks start from; then, on those, to the end
-    // of the chunk (<= log2(PJ_NS) more rounds).
-    if (subex) {
-        for (;;) {
-            int moved = 0;
-            for (uint32_t i = threadIdx.x; i < n; i += PJ_THREADS) {
-                const uint32_t lim = min(n, ((i >> sb_shift) + 1) << sb_shift);
-                const uint32_t v = nx[i];
-                if (v < lim) {
-                    const uint32_t w = nx[v];
-                    nx[i] = w;
-                    moved |= w < lim;
-                }
+    // First, warp-local, to the end of each offset's own sub-chunk (v < s1
+    // implies v lies in the same sub-chunk): the sub-chunk exits the token
+    // walks start from; then, block-wide on those, to the end of the chunk
+    // (<= log2(PJ_NS) more rounds).
+    for (;;) {
+        int moved = 0;
+        for (uint32_t i = s0 + lane; i < s1; i += 32) {
+            const uint32_t v = nx[i];
+            if (v < s1) {
+                const uint32_t w = nx[v];
+                nx[i] = w;
+                moved |= w < s1;
             }
-            if (!__syncthreads_or(moved)) break;
         }
-        for (uint32_t i = threadIdx.x; i < n; i += PJ_THREADS) subex[P + i] = nx[i];
+        __syncwarp();
+        if (!__any_sync(0xffffffffu, moved)) break;
     }
+    if (subex)
+        for (uint32_t i = s0 + lane; i < s1; i += 32) subex[P + i] = nx[i];
+    __syncthreads();
     for (;;) {
         int moved = 0;
         for (uint32_t i = threadIdx.x; i < n; i += PJ_THREADS) {
@@ -182,7 +199,6 @@ __global__ void __launch_bounds__(PJ_THREADS) k_tok_jump(const uint8_t* __restri
         if (!__syncthreads_or(moved)) break;
     }
     // exit table + distinct live exits (warp-deduplicated hash insert)
-    const int lane = threadIdx.x & 31;
     for (uint32_t base = 0; base < n; base += PJ_THREADS) {
         const uint32_t i = base + threadIdx.x;
         const uint32_t r = i < n ? nx[i] : PJ_DEAD32;
@@ -604,7 +620,7 @@ static bool parallel_tokens(const uint8_t* d_stream, uint64_t len, Token* tok, S
     {
         ProfScope ps("k_tok_jump", st);
         k_tok_jump<<<(unsigned)nc, PJ_THREADS, PJ_SMEM, st>>>(d_stream, len, ex, dcount, dvals,
-                                                              fine ? subex : nullptr, shift);
+                                                              fine ? subex : nullptr);
         UMCG_LAUNCHED();
     }
     {
