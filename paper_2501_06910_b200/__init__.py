@@ -20,7 +20,8 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libumcg.so")
+# UMCG_LIB_PATH: an alternative build of the same library (tuning variants)
+LIB_PATH = os.environ.get("UMCG_LIB_PATH") or os.path.join(HERE, "libumcg.so")
 
 # umcg_status values == reference exception types (common.hpp:19-38)
 ERROR_NAMES = {

@@ -238,7 +238,13 @@ __global__ void __launch_bounds__(RT) k_dec_agg(const DecSrc src, CS* __restrict
 }
 
 template <int MODE, class KT>
-__global__ void __launch_bounds__(RT) k_dec_out(const DecSrc src, uint64_t n,
+#ifndef UMCG_DEC_MINB
+#define UMCG_DEC_MINB 5
+#endif
+#ifndef UMCG_DEC_UN
+#define UMCG_DEC_UN 12
+#endif
+__global__ void __launch_bounds__(RT, UMCG_DEC_MINB) k_dec_out(const DecSrc src, uint64_t n,
                                                const CS* __restrict__ pre, DevCtl* ctl,
                                                const uint32_t* __restrict__ node, const KT* __restrict__ K1,
                                                double bin1, double bin, double* __restrict__ out,
@@ -247,7 +253,10 @@ __global__ void __launch_bounds__(RT) k_dec_out(const DecSrc src, uint64_t n,
     using BS = cub::BlockScan<CS, RT>;
     __shared__ typename BS::TempStorage tmp;
     __shared__ __align__(16) uint8_t sb[RHALO + RTILE + 16];
-    __shared__ int32_t kb[MODE == DEC_P64 ? 1 : RTILE];
+    // lattice indices of the tile in element order, int16 (the decoded K of
+    // a lossy residual stream fits; a tile that does not takes the direct
+    // path below)
+    __shared__ int16_t kb[MODE == DEC_P64 ? 1 : RTILE];
     // int32 tables: switch to the int16 copy when the grid's max|K1| (known
     // on the device only) allows -- half the L2 footprint of the gather
     const bool use16 = sizeof(KT) == 4 && K16 && kctl && kctl->max_abs_k[0] < 32768;
@@ -269,6 +278,8 @@ __global__ void __launch_bounds__(RT) k_dec_out(const DecSrc src, uint64_t n,
     int64_t K = tp.sum + excl.sum;
     uint64_t kmax = 0;
     bool bad2 = false, wide2 = false;
+    const uint32_t li0 = li;
+    const int64_t K0 = K;
     auto f = [&](uint32_t v) {
         K += zz_dec32(v);
         const uint64_t a = (uint64_t)(K < 0 ? -K : K);
@@ -277,7 +288,7 @@ __global__ void __launch_bounds__(RT) k_dec_out(const DecSrc src, uint64_t n,
             const uint64_t i = e0 + li;
             if (i < n) P64[i] = K;
         } else {
-            kb[li] = (int32_t)K;  // |K| < 2^30 on the fast path (checked via kmax)
+            kb[li] = (int16_t)K;  // exact when kmax < 2^15 (else the direct path)
         }
         ++li;
     };
@@ -288,9 +299,35 @@ __global__ void __launch_bounds__(RT) k_dec_out(const DecSrc src, uint64_t n,
     }
     if ((threadIdx.x & 31) == 0 && kmax > ctl->max_abs_k[1]) atomicMax(&ctl->max_abs_k[1], (unsigned long long)kmax);
     if (MODE == DEC_P64) return;
-    __syncthreads();
+    const bool use16t = sizeof(KT) == 2 || use16;
+    auto recompose = [&](uint64_t i, int64_t k) {
+        const double r = __dmul_rn((double)k, bin);
+        if (MODE == DEC_VALUES) {
+            out[i] = r;
+        } else {
+            const uint32_t nd = node[i];
+            const int32_t g = use16t ? (int32_t)__ldg((sizeof(KT) == 2 ? reinterpret_cast<const int16_t*>(K1) : K16) + nd)
+                                     : reinterpret_cast<const int32_t*>(K1)[nd];
+            out[i] = __dadd_rn(__dmul_rn((double)g, bin1), r);
+        }
+    };
+    if (__syncthreads_or(kmax >= 32768)) {
+        // rare: some K of the tile does not fit int16 -- walk again and write
+        // the outputs in the walk's order
+        li = li0;
+        K = K0;
+        bool b3 = false, w3 = false;
+        auto g = [&](uint32_t v) {
+            K += zz_dec32(v);
+            const uint64_t i = e0 + li;
+            if (i < n) recompose(i, K);
+            ++li;
+        };
+        if (!thread_walk_fast(sb, my, g)) thread_walk(sb, my, base + (my - RHALO), ulen, &b3, &w3, g);
+        return;
+    }
     const uint32_t cnt = (uint32_t)tot.cnt;
-    constexpr int UN = 12;  // independent gathers in flight per thread
+    constexpr int UN = UMCG_DEC_UN;  // independent gathers in flight per thread
     const uint64_t pf = l2_evict_first(), pl = l2_evict_last();
     for (uint32_t e0 = 0; e0 < cnt; e0 += RT * UN) {
         uint32_t nd[UN];
