@@ -166,6 +166,12 @@ umcg_status umcg_compress_host(umcg_plan* plan, const umcg_params* params, const
                                uint64_t* archive_len);
 umcg_status umcg_decompress_host(umcg_plan* plan, const uint8_t* archive, uint64_t len,
                                  double* out);
+/* umcg_decompress_host that calls uploaded(ctx) (on the calling thread) once
+ * the archive bytes are on the device: a pipelining caller can then start the
+ * next field's host->device copy without queueing it ahead of this archive.
+ * Each host thread's calls use their own CUDA stream. */
+umcg_status umcg_decompress_host_notify(umcg_plan* plan, const uint8_t* archive, uint64_t len,
+                                        double* out, void (*uploaded)(void* ctx), void* ctx);
 
 /* Single component codec: umc::encode (codec.hpp:220-334) with codec 0 /
  * backend 0, and umc::decode (codec.hpp:364-441). predictor: 0 none,

@@ -37,12 +37,16 @@ ERROR_NAMES = {
 EXPORTED = [
     "umcg_plan_create", "umcg_plan_build", "umcg_plan_destroy", "umcg_plan_get_info",
     "umcg_plan_export", "umcg_compress_bound", "umcg_compress", "umcg_compress_batch",
-    "umcg_decompress", "umcg_compress_host", "umcg_decompress_host", "umcg_encode_bound",
+    "umcg_decompress", "umcg_compress_host", "umcg_decompress_host", "umcg_decompress_host_notify",
+    "umcg_encode_bound",
     "umcg_encode", "umcg_decode", "umcg_grid_init", "umcg_baseline_bound", "umcg_compress_baseline", "umcg_rle_bound", "umcg_rle_compress", "umcg_rle_decompress",
     "umcg_gen_config",
     "umcg_kernel_launches", "umcg_serial_fallbacks", "umcg_profile_enable", "umcg_profile_dump",
     "umcg_last_error", "umcg_version",
 ]
+
+
+_NOTIFY = C.CFUNCTYPE(None, C.c_void_p)
 
 
 class UmcgError(RuntimeError):
@@ -125,6 +129,7 @@ def lib():
     L.umcg_decompress.argtypes = [vp, vp, C.c_uint64, vp, vp]
     L.umcg_compress_host.argtypes = [vp, C.POINTER(Params), vp, C.c_char_p, vp, C.c_uint64, u64p]
     L.umcg_decompress_host.argtypes = [vp, vp, C.c_uint64, vp]
+    L.umcg_decompress_host_notify.argtypes = [vp, vp, C.c_uint64, vp, vp, vp]
     L.umcg_encode.argtypes = [vp, C.c_uint64, C.c_int, C.c_int, u64p, C.c_double, C.c_int, C.c_int,
                               vp, C.c_uint64, u64p, vp]
     L.umcg_decode.argtypes = [vp, C.c_uint64, vp, C.c_uint64, u64p, vp]
@@ -339,13 +344,113 @@ class Plan:
                                         C.byref(n)))
         return n.value if out is not None else buf[: n.value].tobytes()
 
-    def decompress_host(self, archive, out: np.ndarray | None = None) -> np.ndarray:
+    def decompress_host(self, archive, out: np.ndarray | None = None, uploaded=None) -> np.ndarray:
+        """uploaded: optional callable, run once the archive is on the device
+        (umcg_decompress_host_notify)."""
         a = np.frombuffer(archive, np.uint8) if isinstance(archive, (bytes, bytearray)) else archive
         length = len(archive) if isinstance(archive, (bytes, bytearray)) else int(a.size)
         y = out if out is not None else np.empty(self.n, np.float64)
-        _check(lib().umcg_decompress_host(self.h, C.c_void_p(a.ctypes.data), length,
-                                          C.c_void_p(y.ctypes.data)))
+        if uploaded is None:
+            _check(lib().umcg_decompress_host(self.h, C.c_void_p(a.ctypes.data), length,
+                                              C.c_void_p(y.ctypes.data)))
+        else:
+            cb = _NOTIFY(lambda _ctx: uploaded())
+            _check(lib().umcg_decompress_host_notify(self.h, C.c_void_p(a.ctypes.data), length,
+                                                     C.c_void_p(y.ctypes.data), C.cast(cb, C.c_void_p), None))
         return y
+
+
+class HostPipeline:
+    """Host-buffer round trips (compress_host -> host archive -> decompress_host)
+    of a sequence of fields, with field k+1's compress overlapping field k's
+    decompress.
+
+    The two directions run on two plans of the same mapping (independent
+    device scratch; archives are interchangeable: same mapping digest) from
+    two host threads; each host call runs on its own CUDA stream (api.cu
+    host_stream), so one field's host->device copy overlaps another's
+    device->host copy. Archives pass through host memory exactly as with
+    sequential calls (two slots, each reused once its decompress is done).
+    """
+
+    def __init__(self, plan_c: "Plan", plan_d: "Plan", archive_slots):
+        if plan_c.h == plan_d.h:
+            raise ValueError("HostPipeline needs two plans (one per direction)")
+        if len(archive_slots) < 2:
+            raise ValueError("HostPipeline needs two archive slots")
+        self.pc, self.pd, self.slots = plan_c, plan_d, archive_slots
+
+    def run(self, fields, budget: "Budget", outs, name: str = ""):
+        """Round-trip fields[k] -> outs[k] (host float64 arrays); returns the
+        archive length of each field."""
+        import queue
+        import threading
+
+        if not hasattr(self, "_jobs"):
+            # one long-lived compress thread: its per-thread device buffers and
+            # stream (api.cu) are reused across runs
+            self._jobs: "queue.Queue" = queue.Queue()
+
+            def worker():
+                while True:
+                    job = self._jobs.get()
+                    if job is None:
+                        return
+                    job()
+
+            self._worker = threading.Thread(target=worker, daemon=True)
+            self._worker.start()
+        nk = len(fields)
+        lens = [0] * nk
+        done: "queue.Queue" = queue.Queue()
+        free = threading.Semaphore(len(self.slots))
+        err = []
+
+        # field k+1's host->device copy is queued only after archive k reached
+        # the device (a copy engine serves queued copies in order)
+        uploaded = [threading.Event() for _ in range(nk)]
+
+        def produce():
+            try:
+                for k in range(nk):
+                    if k >= 1:
+                        uploaded[k - 1].wait()
+                    free.acquire()
+                    slot = self.slots[k % len(self.slots)]
+                    lens[k] = self.pc.compress_host(fields[k], budget, name, out=slot)
+                    done.put(k)
+            except BaseException as e:  # surfaced on the caller's thread
+                err.append(e)
+                done.put(None)
+
+        self._jobs.put(produce)
+        got = 0
+        try:
+            for _ in range(nk):
+                k = done.get()
+                if k is None:
+                    break
+                got += 1
+                slot = self.slots[k % len(self.slots)]
+                self.pd.decompress_host(slot[: lens[k]], out=outs[k], uploaded=uploaded[k].set)
+                free.release()
+        finally:
+            if got < nk and not err:  # a decompress failed: let the producer finish
+                for e in uploaded:
+                    e.set()
+                for _ in range(nk):
+                    free.release()
+                while got < nk and done.get() is not None:
+                    got += 1
+        if err:
+            raise err[0]
+        return lens
+
+    def close(self):
+        if hasattr(self, "_jobs"):
+            self._jobs.put(None)
+            self._worker.join()
+            del self._jobs
 
 
 def encode(d_values, predictor: int = 1, dims=None, tau: float = 1e-3, codec_id: int = 0,

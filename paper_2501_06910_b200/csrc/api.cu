@@ -1,3 +1,4 @@
+#include <cstdio>
 // C ABI (include/umcg.h): orchestration of the sm_100a kernels for
 // umc::compress / umc::decompress (pipeline.hpp:117-148, 180-210) and the
 // component codec (codec.hpp:220-441).
@@ -1106,6 +1107,7 @@ umcg_status umcg_plan_create(const umcg_grid_desc* grid, const umcg_mapping_desc
     return guarded([&] {
         if (!out) fail(UMCG_INVALID_ARGUMENT, "NULL out");
         *out = plan_create_host(grid, mapping, mesh_dim, coords);
+        UMCG_CUDA(cudaDeviceSynchronize());  // usable from any thread / stream afterwards
     });
 }
 
@@ -1114,6 +1116,7 @@ umcg_status umcg_plan_build(const umcg_grid_desc* init_grid, uint64_t n, const d
     return guarded([&] {
         if (!out) fail(UMCG_INVALID_ARGUMENT, "NULL out");
         *out = plan_build_gpu(init_grid, n, d_coords, thr, keep_coords);
+        UMCG_CUDA(cudaDeviceSynchronize());  // usable from any thread / stream afterwards
     });
 }
 
@@ -1188,10 +1191,73 @@ umcg_status umcg_decompress(umcg_plan* p, const uint8_t* d_archive, uint64_t len
     return guarded([&] { decompress_impl(p, d_archive, len, d_out, static_cast<cudaStream_t>(stream)); });
 }
 
+// The host-buffer calls run on a per-thread non-blocking stream: calls from
+// different host threads (on different plans) overlap, e.g. one field's
+// host->device copy with another's device->host copy.
+static cudaStream_t host_stream() {
+    thread_local struct S {
+        cudaStream_t s = nullptr;
+        ~S() { if (s) cudaStreamDestroy(s); }
+    } hs;
+    if (!hs.s) UMCG_CUDA(cudaStreamCreateWithFlags(&hs.s, cudaStreamNonBlocking));
+    return hs.s;
+}
+
+// Large host<->device copies go in 64 MiB pieces with at most two in flight
+// (the host waits on the older one before queueing the next). A copy engine
+// serves queued copies in order, so without the window a concurrent call's
+// small copy (an archive) would wait behind a whole 1 GB field.
+static void copy_pieces(void* dst, const void* src, uint64_t bytes, cudaMemcpyKind kind, cudaStream_t st) {
+    constexpr uint64_t kPiece = 64ull << 20;
+    thread_local struct Ev {
+        cudaEvent_t e[2] = {nullptr, nullptr};
+        ~Ev() {
+            for (auto x : e)
+                if (x) cudaEventDestroy(x);
+        }
+    } ev;
+    if (!ev.e[0])
+        for (auto& x : ev.e) UMCG_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    uint64_t i = 0;
+    for (uint64_t o = 0; o < bytes; o += kPiece, ++i) {
+        if (i >= 2) UMCG_CUDA(cudaEventSynchronize(ev.e[i & 1]));
+        UMCG_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + o, static_cast<const uint8_t*>(src) + o,
+                                  std::min(kPiece, bytes - o), kind, st));
+        UMCG_CUDA(cudaEventRecord(ev.e[i & 1], st));
+    }
+}
+
+// UMCG_HOST_TRACE=1: per-call phase times of the host-buffer calls on stderr
+// (copy in / device work / copy out, CUDA events on the call's stream).
+struct HostTrace {
+    bool on = std::getenv("UMCG_HOST_TRACE") != nullptr;
+    cudaEvent_t e[4] = {};
+    explicit HostTrace() {
+        if (on)
+            for (auto& x : e) cudaEventCreate(&x);
+    }
+    ~HostTrace() {
+        if (on)
+            for (auto& x : e) cudaEventDestroy(x);
+    }
+    void mark(int i, cudaStream_t st) {
+        if (on) cudaEventRecord(e[i], st);
+    }
+    void report(const char* what) {
+        if (!on) return;
+        float a = 0, b = 0, c = 0;
+        cudaEventElapsedTime(&a, e[0], e[1]);
+        cudaEventElapsedTime(&b, e[1], e[2]);
+        cudaEventElapsedTime(&c, e[2], e[3]);
+        std::fprintf(stderr, "[umcg trace] %s: copy-in %.2f ms, device %.2f ms, copy-out %.2f ms\n", what, a, b, c);
+    }
+};
+
 umcg_status umcg_compress_host(umcg_plan* p, const umcg_params* prm, const double* values, const char* name,
                                uint8_t* archive, uint64_t cap, uint64_t* len) {
     return guarded([&] {
         if (!p || !len) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
+        const cudaStream_t hst = host_stream();
         thread_local DevBuf dx, dar;
         const uint64_t n = p->n;
         uint64_t bound = 0;
@@ -1199,24 +1265,46 @@ umcg_status umcg_compress_host(umcg_plan* p, const umcg_params* prm, const doubl
         bound = archive_bound(n, p->n_slots, D1, name ? std::strlen(name) : 0);
         double* x = dx.as<double>(n ? n : 1);
         uint8_t* a = dar.as<uint8_t>(bound);
-        if (n) UMCG_CUDA(cudaMemcpyAsync(x, values, n * 8, cudaMemcpyHostToDevice, 0));
-        compress_impl(p, prm, x, 0, name, a, bound, len, 0);
+        HostTrace tr;
+        tr.mark(0, hst);
+        if (n) copy_pieces(x, values, n * 8, cudaMemcpyHostToDevice, hst);
+        tr.mark(1, hst);
+        compress_impl(p, prm, x, 0, name, a, bound, len, hst);
         if (*len > cap || !archive) fail(UMCG_INVALID_ARGUMENT, "archive buffer too small: need " + std::to_string(*len));
-        UMCG_CUDA(cudaMemcpyAsync(archive, a, *len, cudaMemcpyDeviceToHost, 0));
-        UMCG_CUDA(cudaStreamSynchronize(0));
+        tr.mark(2, hst);
+        copy_pieces(archive, a, *len, cudaMemcpyDeviceToHost, hst);
+        tr.mark(3, hst);
+        UMCG_CUDA(cudaStreamSynchronize(hst));
+        tr.report("compress_host");
     });
 }
 
 umcg_status umcg_decompress_host(umcg_plan* p, const uint8_t* archive, uint64_t len, double* out) {
+    return umcg_decompress_host_notify(p, archive, len, out, nullptr, nullptr);
+}
+
+umcg_status umcg_decompress_host_notify(umcg_plan* p, const uint8_t* archive, uint64_t len, double* out,
+                                        void (*uploaded)(void*), void* ctx) {
     return guarded([&] {
         if (!p) fail(UMCG_INVALID_ARGUMENT, "NULL plan");
+        const cudaStream_t hst = host_stream();
         thread_local DevBuf dar, dy;
         uint8_t* a = dar.as<uint8_t>(len ? len : 1);
         double* y = dy.as<double>(p->n ? p->n : 1);
-        if (len) UMCG_CUDA(cudaMemcpyAsync(a, archive, len, cudaMemcpyHostToDevice, 0));
-        decompress_impl(p, a, len, y, 0);
-        if (p->n) UMCG_CUDA(cudaMemcpyAsync(out, y, p->n * 8, cudaMemcpyDeviceToHost, 0));
-        UMCG_CUDA(cudaStreamSynchronize(0));
+        HostTrace tr;
+        tr.mark(0, hst);
+        if (len) copy_pieces(a, archive, len, cudaMemcpyHostToDevice, hst);
+        tr.mark(1, hst);
+        if (uploaded) {
+            UMCG_CUDA(cudaStreamSynchronize(hst));
+            uploaded(ctx);
+        }
+        decompress_impl(p, a, len, y, hst);
+        tr.mark(2, hst);
+        if (p->n) copy_pieces(out, y, p->n * 8, cudaMemcpyDeviceToHost, hst);
+        tr.mark(3, hst);
+        UMCG_CUDA(cudaStreamSynchronize(hst));
+        tr.report("decompress_host");
     });
 }
 

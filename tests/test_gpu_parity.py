@@ -412,6 +412,28 @@ def test_config3_at_scale_matches_reference(cuda, ref, oracle, tau):
     del torch
 
 
+def test_host_pipeline_matches_sequential_calls(cuda):
+    """HostPipeline (compress of field k+1 on one plan overlapping decompress of
+    field k on a second plan of the same mesh, two host threads, per-thread
+    streams) yields exactly the archives and fields of one-at-a-time calls."""
+    xyz, x = umcg.gen_config(3, 96, 7, device="cuda")
+    axes = [np.linspace(0.0, 1.0, 48) for _ in range(3)]
+    pc, pd = umcg.Plan.build(axes, xyz), umcg.Plan.build(axes, xyz)
+    rng = np.random.default_rng(3)
+    xs = [x.cpu().numpy() * (1.0 + 0.1 * k) + rng.normal(0, 1e-3, x.numel()) for k in range(5)]
+    b = umcg.Budget(tau=1e-3, split_rho=0.5, bound_kind=1)
+    cap = pc.compress_bound("f")
+    slots = [np.empty(cap, np.uint8) for _ in range(2)]
+    outs = [np.empty(x.numel()) for _ in range(5)]
+    lens = umcg.HostPipeline(pc, pd, slots).run(xs, b, outs, "f")
+    for k in range(5):
+        ar = pc.compress_host(xs[k], b, "f")
+        assert lens[k] == len(ar)
+        assert np.array_equal(outs[k], pd.decompress_host(ar)), k
+    with pytest.raises(ValueError):
+        umcg.HostPipeline(pc, pc, slots)
+
+
 @pytest.mark.parametrize("tau", [1e-1, 1e-2, 1e-4, 1e-7])
 def test_config3_full_size_properties(cuda, tau):
     """Config 3 at the bench size (512^3 vertices, grid 256): size-independent
