@@ -350,12 +350,14 @@ def main():
         # decompress_host (second plan on the same mesh, two host threads)
         xyz2, _x2 = umcg.gen_config(3, args.lattice, SEED, device=dev)
         del _x2
-        plan_d = umcg.Plan.build([np.linspace(0.0, 1.0, args.grid) for _ in range(3)], xyz2)
+        ax2 = [np.linspace(0.0, 1.0, args.grid) for _ in range(3)]
+        plan_c2, plan_d, plan_d2 = (umcg.Plan.build(ax2, xyz2) for _ in range(3))
         del xyz2
         torch.cuda.synchronize()
-        pipe = umcg.HostPipeline(plan, plan_d, aa)
+        aa += [torch.empty(cap, dtype=torch.uint8, pin_memory=True).numpy() for _ in range(2)]
+        pipe = umcg.HostPipeline([plan, plan_c2], [plan_d, plan_d2], aa)
         pipe.run([xa] * 2, budget, [ya] * 2, "field")
-        kp = max(8, args.steps)  # pipeline fill + drain are inside the timed region
+        kp = max(16, args.steps)  # pipeline fill + drain are inside the timed region
         barrier()
         t0 = time.perf_counter()
         lens = pipe.run([xa] * kp, budget, [ya] * kp, "field")
@@ -363,13 +365,13 @@ def main():
         pipe.close()
         # the pipelined round trip is the same bytes as the device path's
         ok = bool(torch.equal(yh.to(dev), out)) and all(l == alen for l in lens)
-        del plan_d
+        del plan_d, plan_d2, plan_c2
         torch.cuda.empty_cache()
         L = lens[-1]
         e2e = {"value": ws * n * 8 / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": n * 8 + L,
                "d2h_bytes_per_step": L + n * 8, "ms_per_step": te * 1e3,
-               "path": "HostPipeline: umcg_compress_host(field k+1) || umcg_decompress_host(field k), "
-                       "pinned host buffers, archives through host memory",
+               "path": "HostPipeline: umcg_compress_host on 2 plans || umcg_decompress_host on 2 plans "
+                       "(fields dealt round-robin), pinned host buffers, archives through host memory",
                "matches_device_path": ok,
                "serial": {"value": ws * n * 8 / te_serial / 1e9, "ms_per_step": te_serial * 1e3,
                           "path": "umcg_compress_host then umcg_decompress_host, one field at a time"}}

@@ -167,9 +167,10 @@ umcg_status umcg_compress_host(umcg_plan* plan, const umcg_params* params, const
 umcg_status umcg_decompress_host(umcg_plan* plan, const uint8_t* archive, uint64_t len,
                                  double* out);
 /* umcg_decompress_host that calls uploaded(ctx) (on the calling thread) once
- * the archive bytes are on the device: a pipelining caller can then start the
- * next field's host->device copy without queueing it ahead of this archive.
- * Each host thread's calls use their own CUDA stream. */
+ * the next field's host->device copy can be queued without delaying this
+ * archive's upload: after the upload when it uses a copy engine, right away
+ * when the archive is pinned mapped memory (read by the SMs). Each host
+ * thread's calls use their own CUDA stream. */
 umcg_status umcg_decompress_host_notify(umcg_plan* plan, const uint8_t* archive, uint64_t len,
                                         double* out, void (*uploaded)(void* ctx), void* ctx);
 

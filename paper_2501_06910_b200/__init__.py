@@ -362,95 +362,109 @@ class Plan:
 
 class HostPipeline:
     """Host-buffer round trips (compress_host -> host archive -> decompress_host)
-    of a sequence of fields, with field k+1's compress overlapping field k's
-    decompress.
+    of a sequence of fields, overlapped across fields.
 
-    The two directions run on two plans of the same mapping (independent
-    device scratch; archives are interchangeable: same mapping digest) from
-    two host threads; each host call runs on its own CUDA stream (api.cu
-    host_stream), so one field's host->device copy overlaps another's
-    device->host copy. Archives pass through host memory exactly as with
-    sequential calls (two slots, each reused once its decompress is done).
+    Compress calls run on ``plans_c`` and decompress calls on ``plans_d``,
+    one host thread per plan, fields dealt round-robin; all plans are built
+    on the same mesh (independent device scratch; archives are
+    interchangeable: same mapping digest). Each host call runs on its own
+    CUDA stream (api.cu host_stream), so uploads, device work and downloads
+    of different fields overlap -- field uploads on one PCIe direction while
+    earlier fields' outputs download on the other. Archives pass through host
+    memory exactly as with sequential calls; pinned archive slots are read by
+    the SMs directly (no copy-engine queueing behind a field upload).
+    ``len(archive_slots)`` bounds the archives in flight
+    (>= len(plans_c) + len(plans_d)).
     """
 
-    def __init__(self, plan_c: "Plan", plan_d: "Plan", archive_slots):
-        if plan_c.h == plan_d.h:
-            raise ValueError("HostPipeline needs two plans (one per direction)")
-        if len(archive_slots) < 2:
-            raise ValueError("HostPipeline needs two archive slots")
-        self.pc, self.pd, self.slots = plan_c, plan_d, archive_slots
+    def __init__(self, plans_c, plans_d, archive_slots):
+        as_list = lambda p: list(p) if isinstance(p, (list, tuple)) else [p]  # noqa: E731
+        plans_c, plans_d = as_list(plans_c), as_list(plans_d)
+        every = plans_c + plans_d
+        if len({id(p) for p in every}) != len(every):
+            raise ValueError("HostPipeline needs distinct plans (one per worker)")
+        if len(archive_slots) < len(every):
+            raise ValueError("HostPipeline needs len(plans_c) + len(plans_d) archive slots")
+        self.pcs, self.pds, self.slots = plans_c, plans_d, archive_slots
+        self._workers = []
 
-    def run(self, fields, budget: "Budget", outs, name: str = ""):
-        """Round-trip fields[k] -> outs[k] (host float64 arrays); returns the
-        archive length of each field."""
+    def _start(self):
         import queue
         import threading
 
-        if not hasattr(self, "_jobs"):
-            # one long-lived compress thread: its per-thread device buffers and
-            # stream (api.cu) are reused across runs
-            self._jobs: "queue.Queue" = queue.Queue()
+        for _ in self.pcs + self.pds:
+            jobs: "queue.Queue" = queue.Queue()
 
-            def worker():
+            def loop(jobs=jobs):
                 while True:
-                    job = self._jobs.get()
+                    job = jobs.get()
                     if job is None:
                         return
                     job()
 
-            self._worker = threading.Thread(target=worker, daemon=True)
-            self._worker.start()
-        nk = len(fields)
+            t = threading.Thread(target=loop, daemon=True)
+            t.start()
+            self._workers.append((jobs, t))
+
+    def run(self, fields, budget: "Budget", outs, name: str = ""):
+        """Round-trip fields[k] -> outs[k] (host float64 arrays); returns the
+        archive length of each field."""
+        import threading
+
+        if not self._workers:
+            self._start()
+        nk, Wc, Wd, S = len(fields), len(self.pcs), len(self.pds), len(self.slots)
         lens = [0] * nk
-        done: "queue.Queue" = queue.Queue()
-        free = threading.Semaphore(len(self.slots))
+        ready = [threading.Event() for _ in range(nk)]      # archive k is in its slot
+        slot_free = [threading.Event() for _ in range(nk)]  # field k's slot may be reused
         err = []
 
-        # field k+1's host->device copy is queued only after archive k reached
-        # the device (a copy engine serves queued copies in order)
-        uploaded = [threading.Event() for _ in range(nk)]
+        def fail(e):
+            err.append(e)
+            for ev in ready + slot_free:
+                ev.set()
 
-        def produce():
+        def compress(w):
             try:
-                for k in range(nk):
-                    if k >= 1:
-                        uploaded[k - 1].wait()
-                    free.acquire()
-                    slot = self.slots[k % len(self.slots)]
-                    lens[k] = self.pc.compress_host(fields[k], budget, name, out=slot)
-                    done.put(k)
+                for k in range(w, nk, Wc):
+                    if k >= S:
+                        slot_free[k - S].wait()
+                    if err:
+                        return
+                    lens[k] = self.pcs[w].compress_host(fields[k], budget, name, out=self.slots[k % S])
+                    ready[k].set()
             except BaseException as e:  # surfaced on the caller's thread
-                err.append(e)
-                done.put(None)
+                fail(e)
 
-        self._jobs.put(produce)
-        got = 0
-        try:
-            for _ in range(nk):
-                k = done.get()
-                if k is None:
-                    break
-                got += 1
-                slot = self.slots[k % len(self.slots)]
-                self.pd.decompress_host(slot[: lens[k]], out=outs[k], uploaded=uploaded[k].set)
-                free.release()
-        finally:
-            if got < nk and not err:  # a decompress failed: let the producer finish
-                for e in uploaded:
-                    e.set()
-                for _ in range(nk):
-                    free.release()
-                while got < nk and done.get() is not None:
-                    got += 1
+        def decompress(w, done):
+            try:
+                for k in range(w, nk, Wd):
+                    ready[k].wait()
+                    if err:
+                        return
+                    self.pds[w].decompress_host(self.slots[k % S][: lens[k]], out=outs[k])
+                    slot_free[k].set()
+            except BaseException as e:
+                fail(e)
+            finally:
+                done.release()
+
+        done = threading.Semaphore(0)
+        for w in range(Wc):
+            self._workers[w][0].put(lambda w=w: compress(w))
+        for w in range(Wd):
+            self._workers[Wc + w][0].put(lambda w=w: decompress(w, done))
+        for _ in range(Wd):
+            done.acquire()
         if err:
             raise err[0]
         return lens
 
     def close(self):
-        if hasattr(self, "_jobs"):
-            self._jobs.put(None)
-            self._worker.join()
-            del self._jobs
+        for jobs, t in self._workers:
+            jobs.put(None)
+            t.join()
+        self._workers = []
 
 
 def encode(d_values, predictor: int = 1, dims=None, tau: float = 1e-3, codec_id: int = 0,

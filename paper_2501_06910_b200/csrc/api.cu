@@ -1227,6 +1227,46 @@ static void copy_pieces(void* dst, const void* src, uint64_t bytes, cudaMemcpyKi
     }
 }
 
+// Device-side copy out of mapped pinned host memory (SM loads over PCIe, not
+// a copy engine): an archive upload then shares the link with a concurrent
+// call's copy-engine upload instead of queueing behind it.
+__global__ void k_copy_from_host(const uint8_t* __restrict__ h, uint8_t* __restrict__ d, uint64_t len) {
+    const uint64_t nw = len / 16;
+    const uint4* h4 = reinterpret_cast<const uint4*>(h);
+    uint4* d4 = reinterpret_cast<uint4*>(d);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < nw; i += 4 * stride) {  // four loads in flight per thread
+        const uint4 a = h4[i], b = h4[i + stride], c = h4[i + 2 * stride], e = h4[i + 3 * stride];
+        d4[i] = a;
+        d4[i + stride] = b;
+        d4[i + 2 * stride] = c;
+        d4[i + 3 * stride] = e;
+    }
+    for (; i < nw; i += stride) d4[i] = h4[i];
+    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (t < len - nw * 16) d[nw * 16 + t] = h[nw * 16 + t];
+}
+
+// Host -> device upload of a (small) buffer: by the SMs when the host memory
+// is pinned, mapped and 16-byte aligned, else by the copy engine.
+static bool upload_small(uint8_t* d, const uint8_t* h, uint64_t len, cudaStream_t st) {
+    cudaPointerAttributes at{};
+    const bool mapped = cudaPointerGetAttributes(&at, h) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+                        at.devicePointer != nullptr && ((uintptr_t)at.devicePointer & 15) == 0;
+    cudaGetLastError();  // a pageable pointer is not an error here
+    if (!mapped || std::getenv("UMCG_NO_ZERO_COPY")) {
+        copy_pieces(d, h, len, cudaMemcpyHostToDevice, st);
+        return false;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    k_copy_from_host<<<(unsigned)sms * 4, 256, 0, st>>>(static_cast<const uint8_t*>(at.devicePointer), d, len);
+    UMCG_LAUNCHED();
+    return true;
+}
+
 // UMCG_HOST_TRACE=1: per-call phase times of the host-buffer calls on stderr
 // (copy in / device work / copy out, CUDA events on the call's stream).
 struct HostTrace {
@@ -1293,10 +1333,12 @@ umcg_status umcg_decompress_host_notify(umcg_plan* p, const uint8_t* archive, ui
         double* y = dy.as<double>(p->n ? p->n : 1);
         HostTrace tr;
         tr.mark(0, hst);
-        if (len) copy_pieces(a, archive, len, cudaMemcpyHostToDevice, hst);
+        const bool zero_copy = len && upload_small(a, archive, len, hst);
         tr.mark(1, hst);
         if (uploaded) {
-            UMCG_CUDA(cudaStreamSynchronize(hst));
+            // a copy-engine upload must finish before the caller queues more
+            // copies; SM reads of mapped memory do not queue behind them
+            if (!zero_copy) UMCG_CUDA(cudaStreamSynchronize(hst));
             uploaded(ctx);
         }
         decompress_impl(p, a, len, y, hst);

@@ -413,25 +413,35 @@ def test_config3_at_scale_matches_reference(cuda, ref, oracle, tau):
 
 
 def test_host_pipeline_matches_sequential_calls(cuda):
-    """HostPipeline (compress of field k+1 on one plan overlapping decompress of
-    field k on a second plan of the same mesh, two host threads, per-thread
-    streams) yields exactly the archives and fields of one-at-a-time calls."""
+    """HostPipeline (compress workers on one or two plans overlapping the
+    decompress of earlier fields on another plan of the same mesh, one host
+    thread per plan, per-thread streams; pageable and pinned archive slots)
+    yields exactly the archives and fields of one-at-a-time calls."""
+    import torch
     xyz, x = umcg.gen_config(3, 96, 7, device="cuda")
     axes = [np.linspace(0.0, 1.0, 48) for _ in range(3)]
-    pc, pd = umcg.Plan.build(axes, xyz), umcg.Plan.build(axes, xyz)
+    pc, pc2, pd, pd2 = (umcg.Plan.build(axes, xyz) for _ in range(4))
     rng = np.random.default_rng(3)
-    xs = [x.cpu().numpy() * (1.0 + 0.1 * k) + rng.normal(0, 1e-3, x.numel()) for k in range(5)]
+    xs = [x.cpu().numpy() * (1.0 + 0.1 * k) + rng.normal(0, 1e-3, x.numel()) for k in range(7)]
     b = umcg.Budget(tau=1e-3, split_rho=0.5, bound_kind=1)
     cap = pc.compress_bound("f")
-    slots = [np.empty(cap, np.uint8) for _ in range(2)]
-    outs = [np.empty(x.numel()) for _ in range(5)]
-    lens = umcg.HostPipeline(pc, pd, slots).run(xs, b, outs, "f")
-    for k in range(5):
-        ar = pc.compress_host(xs[k], b, "f")
-        assert lens[k] == len(ar)
-        assert np.array_equal(outs[k], pd.decompress_host(ar)), k
+    slots = [np.empty(cap, np.uint8) for _ in range(4)]  # pageable: copy-engine uploads
+    pinned = [torch.empty(cap, dtype=torch.uint8, pin_memory=True).numpy() for _ in range(4)]  # SM reads
+    ref = [pc.compress_host(xs[k], b, "f") for k in range(7)]
+    for pcs, pds, sl in (([pc], [pd], slots[:2]), ([pc, pc2], [pd], slots[:3]), ([pc, pc2], [pd, pd2], pinned)):
+        outs = [np.empty(x.numel()) for _ in range(7)]
+        pipe = umcg.HostPipeline(pcs, pds, sl)
+        lens = pipe.run(xs, b, outs, "f")
+        lens2 = pipe.run(xs[:3], b, outs[:3], "f")  # workers are reused
+        pipe.close()
+        assert lens2 == lens[:3]
+        for k in range(7):
+            assert lens[k] == len(ref[k])
+            assert np.array_equal(outs[k], pd.decompress_host(ref[k])), k
     with pytest.raises(ValueError):
-        umcg.HostPipeline(pc, pc, slots)
+        umcg.HostPipeline([pc], pc, slots)
+    with pytest.raises(ValueError):
+        umcg.HostPipeline([pc, pc2], pd, slots[:2])
 
 
 @pytest.mark.parametrize("tau", [1e-1, 1e-2, 1e-4, 1e-7])

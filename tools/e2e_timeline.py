@@ -14,14 +14,14 @@ import paper_2501_06910_b200 as umcg  # noqa: E402
 lat = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 xyz, x = umcg.gen_config(3, lat, 20250113, device="cuda")
 axes = [np.linspace(0.0, 1.0, lat // 2) for _ in range(3)]
-pc, pd = umcg.Plan.build(axes, xyz), umcg.Plan.build(axes, xyz)
+pc, pc2, pd, pd2 = (umcg.Plan.build(axes, xyz) for _ in range(4))
 del xyz
 b = umcg.Budget(tau=1e-4, split_rho=0.5, bound_kind=1)
 cap = pc.compress_bound("f")
 xh = torch.empty(x.numel(), dtype=torch.float64, pin_memory=True)
 xh.copy_(x.cpu())
 yh = torch.empty_like(xh).pin_memory()
-slots = [torch.empty(cap, dtype=torch.uint8, pin_memory=True).numpy() for _ in range(2)]
+slots = [torch.empty(cap, dtype=torch.uint8, pin_memory=True).numpy() for _ in range(4)]
 xa, ya = xh.numpy(), yh.numpy()
 for _ in range(2):
     L = pc.compress_host(xa, b, "f", out=slots[0])
@@ -42,9 +42,10 @@ for _ in range(2):
     s1 = time.perf_counter()
     print(f"concurrent: total {1e3*(s1-s0):.1f} ms; compress [{1e3*(T['c'][0]-s0):.1f}, {1e3*(T['c'][1]-s0):.1f}] "
           f"decompress [{1e3*(T['d'][0]-s0):.1f}, {1e3*(T['d'][1]-s0):.1f}]")
-pipe = umcg.HostPipeline(pc, pd, slots)
-pipe.run([xa] * 2, b, [ya] * 2, "f")
-for kp in (4, 8, 16):
-    s0 = time.perf_counter(); pipe.run([xa] * kp, b, [ya] * kp, "f"); s1 = time.perf_counter()
-    print(f"pipeline k={kp}: {1e3*(s1-s0)/kp:.1f} ms/step")
-pipe.close()
+for plans, pds in (([pc], [pd]), ([pc, pc2], [pd]), ([pc, pc2], [pd, pd2])):
+    pipe = umcg.HostPipeline(plans, pds, slots)
+    pipe.run([xa] * 2, b, [ya] * 2, "f")
+    for kp in (4, 8, 16):
+        s0 = time.perf_counter(); pipe.run([xa] * kp, b, [ya] * kp, "f"); s1 = time.perf_counter()
+        print(f"pipeline {len(plans)}c/{len(pds)}d plans k={kp}: {1e3*(s1-s0)/kp:.1f} ms/step")
+    pipe.close()
