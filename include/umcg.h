@@ -126,6 +126,12 @@ umcg_status umcg_plan_build(const umcg_grid_desc* init_grid, uint64_t n_vertices
                             umcg_plan** out);
 
 umcg_status umcg_plan_destroy(umcg_plan* plan);
+/* A second handle on the same plan with its own workspace (scratch buffers,
+ * control block, streams): the static mapping arrays are shared, not copied.
+ * Calls on different handles run concurrently (calls on one handle are
+ * serialized). The origin's memory is released when it and every clone are
+ * destroyed, in any order. */
+umcg_status umcg_plan_clone(const umcg_plan* plan, umcg_plan** out);
 umcg_status umcg_plan_get_info(const umcg_plan* plan, umcg_plan_info* info);
 
 /* Copy the plan's mapping back to host arrays (tests / serialization):

@@ -35,7 +35,7 @@ ERROR_NAMES = {
 
 # public symbols of include/umcg.h (checked by tests/test_abi.py)
 EXPORTED = [
-    "umcg_plan_create", "umcg_plan_build", "umcg_plan_destroy", "umcg_plan_get_info",
+    "umcg_plan_create", "umcg_plan_build", "umcg_plan_destroy", "umcg_plan_clone", "umcg_plan_get_info",
     "umcg_plan_export", "umcg_compress_bound", "umcg_compress", "umcg_compress_batch",
     "umcg_decompress", "umcg_compress_host", "umcg_decompress_host", "umcg_decompress_host_notify",
     "umcg_encode_bound",
@@ -120,6 +120,7 @@ def lib():
     L.umcg_plan_build.argtypes = [C.POINTER(GridDesc), C.c_uint64, vp, C.c_double, C.c_int,
                                   C.POINTER(vp)]
     L.umcg_plan_destroy.argtypes = [vp]
+    L.umcg_plan_clone.argtypes = [vp, vp]
     L.umcg_plan_get_info.argtypes = [vp, C.POINTER(PlanInfo)]
     L.umcg_plan_export.argtypes = [vp, u64p, u64p, f64p]
     L.umcg_compress_bound.argtypes = [vp, C.c_char_p, u64p]
@@ -233,6 +234,14 @@ class Plan:
         _check(lib().umcg_plan_build(C.byref(g), d_coords.shape[0], C.c_void_p(d_coords.data_ptr()),
                                      seed_threshold, 1 if keep_coords else 0, C.byref(h)))
         return cls(h)
+
+    def clone(self) -> "Plan":
+        """umcg_plan_clone: another handle on this plan with its own workspace
+        (the mapping arrays are shared); calls on different handles run
+        concurrently."""
+        h = C.c_void_p()
+        _check(lib().umcg_plan_clone(self.h, C.byref(h)))
+        return Plan(h)
 
     def __del__(self):
         try:
@@ -365,9 +374,10 @@ class HostPipeline:
     of a sequence of fields, overlapped across fields.
 
     Compress calls run on ``plans_c`` and decompress calls on ``plans_d``,
-    one host thread per plan, fields dealt round-robin; all plans are built
-    on the same mesh (independent device scratch; archives are
-    interchangeable: same mapping digest). Each host call runs on its own
+    one host thread per plan, fields dealt round-robin; all plans are handles
+    on the same mesh -- ``Plan.clone()`` gives one with its own workspace and
+    shared mapping arrays (archives are interchangeable: same mapping
+    digest). Each host call runs on its own
     CUDA stream (api.cu host_stream), so uploads, device work and downloads
     of different fields overlap -- field uploads on one PCIe direction while
     earlier fields' outputs download on the other. Archives pass through host

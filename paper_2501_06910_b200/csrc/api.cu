@@ -1120,8 +1120,57 @@ umcg_status umcg_plan_build(const umcg_grid_desc* init_grid, uint64_t n, const d
     });
 }
 
+static void plan_release(umcg_plan* o) {
+    if (o && o->refs.fetch_sub(1) == 1) delete o;
+}
+
 umcg_status umcg_plan_destroy(umcg_plan* plan) {
-    return guarded([&] { delete plan; });
+    return guarded([&] {
+        if (!plan) return;
+        if (plan->origin) {
+            umcg_plan* o = plan->origin;
+            delete plan;
+            plan_release(o);
+        } else {
+            plan_release(plan);
+        }
+    });
+}
+
+umcg_status umcg_plan_clone(const umcg_plan* src, umcg_plan** out) {
+    return guarded([&] {
+        if (!src || !out) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
+        umcg_plan* o = src->origin ? src->origin : const_cast<umcg_plan*>(src);
+        auto c = std::make_unique<umcg_plan>();
+        c->device = o->device;
+        c->dim = o->dim;
+        c->mode = o->mode;
+        c->n = o->n;
+        c->n_slots = o->n_slots;
+        c->node_count = o->node_count;
+        c->n_visited = o->n_visited;
+        for (int d = 0; d < 3; ++d) {
+            c->shape[d] = o->shape[d];
+            c->axis_scale[d] = o->axis_scale[d];
+        }
+        c->visited_fraction = o->visited_fraction;
+        c->digest = o->digest;
+        c->axes = o->axes;
+        c->axis_off = o->axis_off;
+        c->has_coords = o->has_coords;
+        c->n_buckets = o->n_buckets;
+        c->n_epochs = o->n_epochs;
+        c->n_regular = o->n_regular;
+        for (auto m : {&umcg_plan::d_node, &umcg_plan::d_perm, &umcg_plan::d_seg, &umcg_plan::d_visited,
+                       &umcg_plan::d_axes, &umcg_plan::d_axis_off, &umcg_plan::d_inv_cell, &umcg_plan::d_coords,
+                       &umcg_plan::d_srcE, &umcg_plan::d_dstE, &umcg_plan::d_ech, &umcg_plan::d_bct,
+                       &umcg_plan::d_regular, &umcg_plan::d_lnode, &umcg_plan::d_lperm, &umcg_plan::d_lslot,
+                       &umcg_plan::d_bk})
+            ((*c).*m).alias((*o).*m);
+        o->refs.fetch_add(1);
+        c->origin = o;
+        *out = c.release();
+    });
 }
 
 umcg_status umcg_plan_get_info(const umcg_plan* p, umcg_plan_info* info) {

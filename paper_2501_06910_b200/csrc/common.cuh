@@ -415,9 +415,18 @@ public:
     }
     template <class T> T* as(size_t n) { return static_cast<T*>(reserve(n * sizeof(T))); }
     void release() {
-        if (p_) cudaFree(p_);
+        if (p_ && owned_) cudaFree(p_);
         p_ = nullptr;
         cap_ = 0;
+        owned_ = true;
+    }
+    // Non-owning view of another buffer's memory (plan clones share the
+    // static mapping arrays of their origin, which outlives them).
+    void alias(const DevBuf& o) {
+        release();
+        p_ = o.p_;
+        cap_ = o.cap_;
+        owned_ = false;
     }
     void* get() const { return p_; }
     size_t capacity() const { return cap_; }
@@ -425,6 +434,7 @@ public:
 private:
     void* p_ = nullptr;
     size_t cap_ = 0;
+    bool owned_ = true;
 };
 
 // A side stream + fork/join events, created on first use (non-blocking, so a

@@ -1,6 +1,7 @@
 // The immutable per-mesh device plan + per-call workspace.
 #pragma once
 
+#include <atomic>
 #include <mutex>
 
 #include "kernels.h"
@@ -50,7 +51,11 @@ struct umcg_plan {
     umcg::DevBuf d_lperm;    // u16 [n]    bucket-local element of node-sorted position
     umcg::DevBuf d_lslot;    // u16 [n]    shared-memory slot of node-sorted position (TMA staging)
     umcg::DevBuf d_bk;       // u32 [2*(B+1)] bucket start (vertex) and first slot
-    // workspace (serialized by mu)
+    // clones (umcg_plan_clone) alias the static arrays above of their origin;
+    // the origin is freed when it and all of its clones are destroyed
+    umcg_plan* origin = nullptr;
+    std::atomic<int> refs{1};
+    // workspace (serialized by mu; a clone has its own)
     std::mutex mu;
     umcg::DevBuf ctl, x1, codes1, codes2, kbuf, enc1, enc2, hdr, scratch_a, scratch_b, scratch_c,
         scratch_d, dx1, dcodes;

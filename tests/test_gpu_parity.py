@@ -420,7 +420,9 @@ def test_host_pipeline_matches_sequential_calls(cuda):
     import torch
     xyz, x = umcg.gen_config(3, 96, 7, device="cuda")
     axes = [np.linspace(0.0, 1.0, 48) for _ in range(3)]
-    pc, pc2, pd, pd2 = (umcg.Plan.build(axes, xyz) for _ in range(4))
+    pc = umcg.Plan.build(axes, xyz)
+    pc2, pd, pd2 = umcg.Plan.build(axes, xyz), pc.clone(), pc.clone()  # a second build and two clones
+    assert pd.digest == pc.digest and pd.n == pc.n
     rng = np.random.default_rng(3)
     xs = [x.cpu().numpy() * (1.0 + 0.1 * k) + rng.normal(0, 1e-3, x.numel()) for k in range(7)]
     b = umcg.Budget(tau=1e-3, split_rho=0.5, bound_kind=1)
@@ -442,6 +444,31 @@ def test_host_pipeline_matches_sequential_calls(cuda):
         umcg.HostPipeline([pc], pc, slots)
     with pytest.raises(ValueError):
         umcg.HostPipeline([pc, pc2], pd, slots[:2])
+
+
+def test_plan_clone_lifetime_and_concurrency(cuda):
+    """umcg_plan_clone: clones share the mapping arrays, outlive their origin,
+    and concurrent calls on different handles give the single-handle bytes."""
+    import threading
+    xyz, x = umcg.gen_config(3, 64, 11, device="cuda")
+    p = umcg.Plan.build([np.linspace(0.0, 1.0, 32) for _ in range(3)], xyz)
+    b = umcg.Budget(tau=1e-4)
+    ref = p.compress(x, b)
+    c1 = p.clone()
+    c2 = c1.clone()  # clone of a clone: same origin
+    del p  # origin handle destroyed first
+    import gc
+    gc.collect()
+    res = {}
+
+    def work(k, h):
+        res[k] = [h.compress(x, b) for _ in range(3)]
+
+    ts = [threading.Thread(target=work, args=(k, h)) for k, h in enumerate((c1, c2))]
+    [t.start() for t in ts]
+    [t.join() for t in ts]
+    assert all(a == ref for v in res.values() for a in v)
+    assert np.array_equal(c2.decompress(ref).cpu().numpy(), c1.decompress(ref).cpu().numpy())
 
 
 @pytest.mark.parametrize("tau", [1e-1, 1e-2, 1e-4, 1e-7])

@@ -14,7 +14,8 @@ import paper_2501_06910_b200 as umcg  # noqa: E402
 lat = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 xyz, x = umcg.gen_config(3, lat, 20250113, device="cuda")
 axes = [np.linspace(0.0, 1.0, lat // 2) for _ in range(3)]
-pc, pc2, pd, pd2 = (umcg.Plan.build(axes, xyz) for _ in range(4))
+pc = umcg.Plan.build(axes, xyz)
+pc2, pd, pd2 = pc.clone(), pc.clone(), pc.clone()
 del xyz
 b = umcg.Budget(tau=1e-4, split_rho=0.5, bound_kind=1)
 cap = pc.compress_bound("f")
