@@ -21,6 +21,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -90,6 +91,29 @@ inline std::map<PlanKey, PlanPtr>& cache() {
     static std::map<PlanKey, PlanPtr> c;
     return c;
 }
+inline std::atomic<std::uint64_t>& cache_generation() {
+    static std::atomic<std::uint64_t> g{0};
+    return g;
+}
+
+// Each host thread works on its own clone of a cached plan (umcg_plan_clone:
+// own workspace, shared mapping arrays), so concurrent calls on one
+// MappingTable run concurrently, as the reference allows.
+inline umcg_plan* thread_handle(umcg_plan* origin) {
+    thread_local std::uint64_t gen = 0;
+    thread_local std::map<umcg_plan*, PlanPtr> clones;
+    const std::uint64_t g = cache_generation().load();
+    if (gen != g) {
+        clones.clear();
+        gen = g;
+    }
+    auto it = clones.find(origin);
+    if (it != clones.end()) return it->second.get();
+    umcg_plan* c = nullptr;
+    check(umcg_plan_clone(origin, &c));
+    clones.emplace(origin, PlanPtr(c));
+    return c;
+}
 
 // Device plan for (map, grid, mesh); coordinates are uploaded only when the
 // caller needs multilinear g.
@@ -98,7 +122,7 @@ inline umcg_plan* plan_for(const MappingTable& map, const RectGrid& grid, const 
                       grid.node_count(), coords};
     std::lock_guard<std::mutex> lock(cache_mutex());
     auto it = cache().find(key);
-    if (it != cache().end()) return it->second.get();
+    if (it != cache().end()) return thread_handle(it->second.get());
     std::vector<std::uint64_t> sizes;
     std::vector<double> axes;
     for (const auto& a : grid.axes) {
@@ -111,14 +135,15 @@ inline umcg_plan* plan_for(const MappingTable& map, const RectGrid& grid, const 
     umcg_plan* p = nullptr;
     check(umcg_plan_create(&g, &m, mesh.dim, coords ? mesh.vertices.data() : nullptr, &p));
     cache().emplace(key, PlanPtr(p));
-    return p;
+    return thread_handle(p);
 }
 
 }  // namespace detail
 
 inline void clear_plan_cache() {
     std::lock_guard<std::mutex> lock(detail::cache_mutex());
-    detail::cache().clear();
+    detail::cache().clear();  // threads drop their clones on their next call
+    detail::cache_generation().fetch_add(1);
 }
 
 /// umc::compress (pipeline.hpp:117-148) on the GPU. Same arguments, same

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "umc/datagen.hpp"
@@ -184,6 +185,43 @@ int main() {
         CHECK(rc.mapping.assignments == gc.mapping.assignments, "grid_coarsen assignments identical");
         CHECK(rc.mapping.visited_nodes == gc.mapping.visited_nodes, "grid_coarsen visited identical");
         CHECK(mapping_digest(rc.mapping) == mapping_digest(gc.mapping), "mapping digest");
+    }
+    {
+        // concurrent calls on one MappingTable from several host threads (each
+        // gets its own plan clone): same archives as one thread
+        Built c = build(2, 2, 4000, MeshStyle::jittered);
+        std::vector<Field> fields;
+        std::vector<std::vector<std::uint8_t>> want;
+        std::vector<std::vector<double>> want_back;  // one-thread drop-in decode (the GPU decode is deterministic)
+        for (int k = 0; k < 4; ++k) {
+            SynthSpec s2;
+            s2.rng_seed = 100 + k;
+            fields.push_back(gen_field(c.mesh, s2));
+            const Archive r = compress(fields.back(), c.map, c.grid, c.mesh, ErrorBudget{});
+            want.push_back(serialize_archive(r));
+            want_back.push_back(b200::decompress(r, c.map, c.grid, c.mesh).values);
+        }
+        std::vector<int> ok(4, 0);
+        std::vector<std::thread> th;
+        for (int k = 0; k < 4; ++k)
+            th.emplace_back([&, k] {
+                for (int r = 0; r < 3; ++r) {
+                    const Archive g = b200::compress(fields[k], c.map, c.grid, c.mesh, ErrorBudget{});
+                    const Field back = b200::decompress(g, c.map, c.grid, c.mesh);
+                    const bool a_ok = serialize_archive(g) == want[k];
+                    const bool d_ok = back.values == want_back[k];
+                    if (!a_ok || !d_ok) std::printf("thread %d round %d: archive %d decode %d\n", k, r, a_ok, d_ok);
+                    ok[k] += a_ok && d_ok;
+                }
+            });
+        for (auto& t : th) t.join();
+        for (int k = 0; k < 4; ++k) {
+            if (ok[k] != 3) std::printf("thread %d: %d of 3 round trips matched\n", k, ok[k]);
+            CHECK(ok[k] == 3, "concurrent drop-in calls match the reference");
+        }
+        b200::clear_plan_cache();
+        CHECK(serialize_archive(b200::compress(fields[0], c.map, c.grid, c.mesh, ErrorBudget{})) == want[0],
+              "after clear_plan_cache");
     }
     std::printf("cases %d exact %d failures %d\n", total, exact, failures);
     return failures ? 1 : 0;
