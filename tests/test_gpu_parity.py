@@ -654,6 +654,19 @@ def test_config5_shell_matches_reference(cuda, ref, oracle, g):
                      f"config5 g={g} tau={tau} rho={rho} mode={s.mode}")
 
 
+def test_config5_error_split_sweep_matches_reference(cuda, ref, oracle):
+    """BASELINE config 5's nine error splits between the grid and residual
+    components (rho 0.1 .. 0.9) at 2^19 vertices, tau 1e-4, dense and seed
+    grids."""
+    xyz, x = umcg.gen_config(5, 1 << 19, 20250115, device="cuda")
+    xh = x.cpu().numpy()
+    for g in (48, 96):
+        plan, s = _bbox_plan(xyz, g)
+        for rho in np.round(np.arange(0.1, 0.95, 0.1), 1):
+            _parity_case(plan, s, x, xh, dict(tau=1e-4, rho=float(rho)), ref, oracle,
+                         f"config5 split g={g} rho={rho} mode={s.mode}")
+
+
 def test_config5_modes_cover_dense_and_seed(cuda):
     """The shell switches the grid builder to seed mode as the grid refines
     (128^3 dense, 256^3 seed at 200M vertices)."""

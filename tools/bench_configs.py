@@ -1,6 +1,7 @@
 """Throughput of the other BASELINE configs (parity cases, not bench lines):
 config 2 (graded annulus), config 4 (5 fp32 variables, one batch call),
-config 5 (clustered shell; seed mode at 256^3). CUDA-event timed, inputs
+config 5 (clustered shell; seed mode at 256^3; the 9-way error split at
+256^3). CUDA-event timed, inputs
 resident in HBM, median of 5 after 2 warm-ups."""
 import json
 import os
@@ -34,8 +35,8 @@ def bbox_plan(xyz, g):
     return umcg.Plan.build([np.linspace(lo[d], hi[d], g) for d in range(xyz.shape[1])], xyz)
 
 
-def run(name, plan, x, tau, n_bytes, extra=None):
-    b = umcg.Budget(tau=tau)
+def run(name, plan, x, tau, n_bytes, extra=None, rho=0.5):
+    b = umcg.Budget(tau=tau, split_rho=rho)
     ar = torch.empty(plan.compress_bound("f"), dtype=torch.uint8, device="cuda")
     out = torch.empty(plan.n, dtype=torch.float64, device="cuda")
     L = [0]
@@ -46,7 +47,7 @@ def run(name, plan, x, tau, n_bytes, extra=None):
     tc = timed(c)
     td = timed(lambda: plan.decompress_into(ar, L[0], out))
     err = (out - x.double()).abs().max().item() / (tau * (x.max() - x.min()).item())
-    r = dict(config=name, tau=tau, n=plan.n, mode=int(plan.info.mode), compress_ms=tc, decompress_ms=td,
+    r = dict(config=name, tau=tau, rho=rho, n=plan.n, mode=int(plan.info.mode), compress_ms=tc, decompress_ms=td,
              compress_gbs=n_bytes / tc / 1e6, decompress_gbs=n_bytes / td / 1e6, archive=L[0],
              max_err_over_tau=err)
     if extra:
@@ -82,4 +83,7 @@ for g in (128, 256, 384):
     plan = bbox_plan(xyz, g)
     for tau in (1e-2, 1e-6):
         run(f"config5 grid{g}^3", plan, x, tau, x.numel() * 8)
+    if g == 256:  # the error-split sweep of the config (9 splits, tau 1e-4)
+        for rho in np.round(np.arange(0.1, 0.95, 0.1), 1):
+            run(f"config5 grid{g}^3 split", plan, x, 1e-4, x.numel() * 8, rho=float(rho))
     del plan
