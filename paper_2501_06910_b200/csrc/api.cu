@@ -1,3 +1,4 @@
+#include <chrono>
 #include <cstdio>
 // C ABI (include/umcg.h): orchestration of the sm_100a kernels for
 // umc::compress / umc::decompress (pipeline.hpp:117-148, 180-210) and the
@@ -729,6 +730,40 @@ __global__ void k_fast_verdict(const DevCtl* c, DecSrc s1, DecSrc s2, uint64_t n
 // synchronization instead of one per step. Returns false (output undefined)
 // whenever the step-by-step path must run; that path also reports the
 // reference's error for malformed payloads.
+// UMCG_DEC_TRACE=1: host / device timestamps of the decompress phases on stderr.
+struct DecTrace {
+    bool on = std::getenv("UMCG_DEC_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point h[8];
+    cudaEvent_t e[8] = {};
+    int nh = 0, ne = 0;
+    const char* hn[8] = {};
+    const char* en[8] = {};
+    DecTrace() {
+        if (on)
+            for (auto& x : e) cudaEventCreate(&x);
+    }
+    void host(const char* n) {
+        if (on && nh < 8) { hn[nh] = n; h[nh++] = std::chrono::steady_clock::now(); }
+    }
+    void dev(const char* n, cudaStream_t st) {
+        if (on && ne < 8) { en[ne] = n; cudaEventRecord(e[ne++], st); }
+    }
+    ~DecTrace() {
+        if (!on) return;
+        cudaDeviceSynchronize();
+        for (int i = 1; i < nh; ++i)
+            std::fprintf(stderr, "[dec trace] host %-12s +%.1f us\n", hn[i],
+                         std::chrono::duration<double, std::micro>(h[i] - h[0]).count());
+        for (int i = 1; i < ne; ++i) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e[0], e[i]);
+            std::fprintf(stderr, "[dec trace] dev  %-12s +%.1f us\n", en[i], 1e3 * ms);
+        }
+        for (auto& x : e) cudaEventDestroy(x);
+    }
+};
+thread_local DecTrace* g_dec_trace = nullptr;
+
 static bool fast_decompress(umcg_plan* p, const uint8_t* d_ar, uint64_t p1, const CompHeader& h1, uint64_t p2,
                             const CompHeader& h2, double* d_out, cudaStream_t st) {
     const int pred1 = (h1.pred == 2 && h1.D == 1) ? 1 : h1.pred;
@@ -741,14 +776,18 @@ static bool fast_decompress(umcg_plan* p, const uint8_t* d_ar, uint64_t p1, cons
     if (!lattice(h1, bin1) || !lattice(h2, bin2) || pred1 == 0 || pred2 != 1 || h2.D != 1) return false;
     const uint64_t n1 = h1.n, n = h2.n;
     auto* c = p->ctl.as<DevCtl>(5);  // token ctl / decode ctl per component + verdict
+    if (g_dec_trace) { g_dec_trace->host("fast begin"); g_dec_trace->dev("fast begin", st); }
     UMCG_CUDA(cudaMemsetAsync(c, 0, 5 * sizeof(DevCtl), st));
     const uint8_t* s1b = d_ar + p1 + h1.stream_off;
     const uint8_t* s2b = d_ar + p2 + h2.stream_off;
     // the residual stream's probe, tile aggregates and scan run on the side
     // stream while the grid component decodes
-    cudaStream_t ss = p->side.get();
+    // grid chain (small, latency-bound kernels) on a high-priority stream so
+    // the residual's tile pass (every SM) does not starve it
+    cudaStream_t ss = p->side.get(), sh = p->side.get_hi();
     p->side.link(st, ss, 0);
-    const Token* t1 = stream_probe(s1b, h1.stream_len, p->dec, &c[0], st);
+    p->side.link(st, sh, 2);
+    const Token* t1 = stream_probe(s1b, h1.stream_len, p->dec, &c[0], sh);
     const Token* t2 = stream_probe(s2b, h2.stream_len, p->dec2, &c[2], ss);
     const DecSrc src1{nullptr, 0, s1b, t1, &c[0]};
     const DecSrc src2{nullptr, 0, s2b, t2, &c[2]};
@@ -757,14 +796,18 @@ static bool fast_decompress(umcg_plan* p, const uint8_t* d_ar, uint64_t p1, cons
     dec_prepare(src2, dec_tiles(h2.stream_len), st2, &c[3], ss);
     int64_t* P = p->kbuf.as<int64_t>(2 * n1);
     int32_t* K1 = p->codes1.as<int32_t>(n1);
-    dec_fused(DEC_P64, src1, dec_tiles(h1.stream_len), n1, st1, &c[1], nullptr, nullptr, 0.0, bin1, nullptr, P, st);
+    dec_fused(DEC_P64, src1, dec_tiles(h1.stream_len), n1, st1, &c[1], nullptr, nullptr, 0.0, bin1, nullptr, P, sh);
     const uint64_t flat[1] = {n1};
     int16_t* K16 = p->dx1.as<int16_t>(n1 + 2);
     nd_from_prefix(P, n1, pred1 == 2 ? make_shape(h1.D, h1.dims) : make_shape(1, flat), P + n1, K1, K16, &c[1],
-                   st);
+                   sh);
+    if (g_dec_trace) g_dec_trace->dev("grid done", sh);
+    p->side.link(sh, st, 3);
     p->side.link(ss, st, 1);
+    if (g_dec_trace) g_dec_trace->dev("resid agg", st);
     dec_fused(DEC_RECOMPOSE, src2, dec_tiles(h2.stream_len), n, st2, &c[3], p->d_node.as<uint32_t>(1), K1, bin1,
               bin2, d_out, nullptr, st, &c[1], K16, true);
+    if (g_dec_trace) { g_dec_trace->dev("dec_out", st); g_dec_trace->host("queued"); }
     auto* verdict = reinterpret_cast<unsigned long long*>(&c[4].aux[0]);
     k_fast_verdict<<<1, 1, 0, st>>>(c, src1, src2, n1, n, k_lim(pred1, pred1 == 2 ? h1.D : 1), k_lim(1, 1),
                                     verdict);
@@ -772,11 +815,17 @@ static bool fast_decompress(umcg_plan* p, const uint8_t* d_ar, uint64_t p1, cons
     auto* hv = static_cast<unsigned long long*>(p->hctl.reserve(sizeof(DevCtl)));
     UMCG_CUDA(cudaMemcpyAsync(hv, verdict, 8, cudaMemcpyDeviceToHost, st));
     UMCG_CUDA(cudaStreamSynchronize(st));
+    if (g_dec_trace) { g_dec_trace->host("verdict"); g_dec_trace->dev("verdict", st); }
     return *hv == 0;
 }
 
+
 void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_out, cudaStream_t st) {
     if (!p || (!d_ar && len)) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
+    DecTrace trace;
+    g_dec_trace = &trace;
+    trace.host("start");
+    trace.dev("start", st);
     std::lock_guard<std::mutex> lock(p->mu);
     UMCG_CUDA(cudaSetDevice(p->device));
     // deserialize_archive (pipeline.hpp:237-267): all truncation -> malformed_file.
@@ -792,7 +841,9 @@ void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_
         k_gather_headers<<<1, 128, 0, st>>>(d_ar, len, dbuf);
         UMCG_LAUNCHED();
         UMCG_CUDA(cudaMemcpyAsync(hb, dbuf, kHeadShort + kTailBytes + 16, cudaMemcpyDeviceToHost, st));
+        trace.dev("headers", st);
         UMCG_CUDA(cudaStreamSynchronize(st));
+        trace.host("headers");
         uint64_t tlen = 0;
         std::memcpy(&tlen, hb + kHeadShort + kTailBytes, 8);
         std::memcpy(&o2_gathered, hb + kHeadShort + kTailBytes + 8, 8);

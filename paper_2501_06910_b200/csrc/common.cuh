@@ -440,11 +440,12 @@ private:
 // A side stream + fork/join events, created on first use (non-blocking, so a
 // caller on the legacy default stream is not serialized against it).
 struct SideStream {
-    cudaStream_t s = nullptr;
+    cudaStream_t s = nullptr, hi = nullptr;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     ~SideStream() {
         for (auto& e : ev) if (e) cudaEventDestroy(e);
         if (s) cudaStreamDestroy(s);
+        if (hi) cudaStreamDestroy(hi);
     }
     cudaStream_t get() {
         if (!s) {
@@ -452,6 +453,18 @@ struct SideStream {
             for (auto& e : ev) UMCG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         }
         return s;
+    }
+    // Highest-priority side stream: a latency-bound chain (few CTAs per
+    // kernel) keeps its SMs while a throughput-bound kernel on a normal
+    // stream fills the rest.
+    cudaStream_t get_hi() {
+        get();
+        if (!hi) {
+            int lo = 0, top = 0;
+            UMCG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &top));
+            UMCG_CUDA(cudaStreamCreateWithPriority(&hi, cudaStreamNonBlocking, top));
+        }
+        return hi;
     }
     // `to` waits for all work queued so far on `from` (event slot k)
     void link(cudaStream_t from, cudaStream_t to, int k) {

@@ -215,7 +215,10 @@ __device__ __forceinline__ CS thread_counts(const uint8_t* sb, int my, bool* bad
 
 // Tile aggregates (count, sum of zigzag values); tiles past the stream end
 // (T is a host-side bound when the stream is resolved on the device) add 0.
-__global__ void __launch_bounds__(RT) k_dec_agg(const DecSrc src, CS* __restrict__ aggs, DevCtl* ctl) {
+// thr: every thread's exclusive (count, sum) inside its tile, so k_dec_out
+// starts its walk without a counting walk + block scan of its own.
+__global__ void __launch_bounds__(RT) k_dec_agg(const DecSrc src, CS* __restrict__ aggs, CS* __restrict__ thr,
+                                               DevCtl* ctl) {
     const uint8_t* U;
     uint64_t ulen;
     resolve_src(src, U, ulen);
@@ -223,8 +226,8 @@ __global__ void __launch_bounds__(RT) k_dec_agg(const DecSrc src, CS* __restrict
         if (threadIdx.x == 0) aggs[blockIdx.x] = CS{0, 0};
         return;
     }
-    using BR = cub::BlockReduce<CS, RT>;
-    __shared__ typename BR::TempStorage tmp;
+    using BS = cub::BlockScan<CS, RT>;
+    __shared__ typename BS::TempStorage tmp;
     __shared__ __align__(16) uint8_t sb[RHALO + RTILE + 16];
     const int64_t base = (int64_t)blockIdx.x * (int64_t)RTILE;
     stage_tile(U, ulen, base, sb);
@@ -233,8 +236,10 @@ __global__ void __launch_bounds__(RT) k_dec_agg(const DecSrc src, CS* __restrict
     const CS mine = thread_counts(sb, RHALO + threadIdx.x * RB, &bad, &wide, base, ulen);
     if (bad) set_err(ctl, DE_CORRUPT_VARINT);
     if (wide) ctl->aux[7] = 1;
-    const CS t = BR(tmp).Reduce(mine, CSAdd());
+    CS excl, t;
+    BS(tmp).ExclusiveScan(mine, excl, CS{0, 0}, CSAdd(), t);
     if (threadIdx.x == 0) aggs[blockIdx.x] = t;
+    thr[blockIdx.x * (uint64_t)RT + threadIdx.x] = excl;
 }
 
 template <int MODE, class KT>
@@ -249,14 +254,15 @@ __global__ void __launch_bounds__(RT, UMCG_DEC_MINB) k_dec_out(const DecSrc src,
                                                const uint32_t* __restrict__ node, const KT* __restrict__ K1,
                                                double bin1, double bin, double* __restrict__ out,
                                                int64_t* __restrict__ P64, const DevCtl* __restrict__ kctl,
-                                               const int16_t* __restrict__ K16) {
-    using BS = cub::BlockScan<CS, RT>;
-    __shared__ typename BS::TempStorage tmp;
+                                               const int16_t* __restrict__ K16, const CS* __restrict__ raw,
+                                               const CS* __restrict__ thr) {
     __shared__ __align__(16) uint8_t sb[RHALO + RTILE + 16];
     // lattice indices of the tile in element order, int16 (the decoded K of
     // a lossy residual stream fits; a tile that does not takes the direct
     // path below)
     __shared__ int16_t kb[MODE == DEC_P64 ? 1 : RTILE];
+    // P64 mode: K - (tile prefix) as int32, written out coalesced afterwards
+    __shared__ int32_t kp[MODE == DEC_P64 ? RTILE : 1];
     // int32 tables: switch to the int16 copy when the grid's max|K1| (known
     // on the device only) allows -- half the L2 footprint of the gather
     const bool use16 = sizeof(KT) == 4 && K16 && kctl && kctl->max_abs_k[0] < 32768;
@@ -268,10 +274,9 @@ __global__ void __launch_bounds__(RT, UMCG_DEC_MINB) k_dec_out(const DecSrc src,
     stage_tile(U, ulen, base, sb);
     __syncthreads();
     const int my = RHALO + threadIdx.x * RB;
-    bool bad = false, wide = false;
-    const CS mine = thread_counts(sb, my, &bad, &wide, base, ulen);
-    CS excl, tot;
-    BS(tmp).ExclusiveScan(mine, excl, CS{0, 0}, CSAdd(), tot);
+    // the thread's prefix inside the tile and the tile's total (k_dec_agg)
+    const CS excl = thr[blockIdx.x * (uint64_t)RT + threadIdx.x];
+    const CS tot = raw[blockIdx.x];
     const CS tp = pre[blockIdx.x];
     const uint64_t e0 = tp.cnt;           // first element of the tile
     uint32_t li = (uint32_t)excl.cnt;     // local element index
@@ -280,13 +285,15 @@ __global__ void __launch_bounds__(RT, UMCG_DEC_MINB) k_dec_out(const DecSrc src,
     bool bad2 = false, wide2 = false;
     const uint32_t li0 = li;
     const int64_t K0 = K;
+    bool ovf = false;  // P64: some K - tp.sum outside int32
     auto f = [&](uint32_t v) {
         K += zz_dec32(v);
         const uint64_t a = (uint64_t)(K < 0 ? -K : K);
         kmax = a > kmax ? a : kmax;
         if (MODE == DEC_P64) {
-            const uint64_t i = e0 + li;
-            if (i < n) P64[i] = K;
+            const int64_t d = K - tp.sum;
+            ovf |= d != (int64_t)(int32_t)d;
+            kp[li] = (int32_t)d;
         } else {
             kb[li] = (int16_t)K;  // exact when kmax < 2^15 (else the direct path)
         }
@@ -298,7 +305,27 @@ __global__ void __launch_bounds__(RT, UMCG_DEC_MINB) k_dec_out(const DecSrc src,
         kmax = b2 > kmax ? b2 : kmax;
     }
     if ((threadIdx.x & 31) == 0 && kmax > ctl->max_abs_k[1]) atomicMax(&ctl->max_abs_k[1], (unsigned long long)kmax);
-    if (MODE == DEC_P64) return;
+    if (MODE == DEC_P64) {
+        if (__syncthreads_or(ovf)) {  // rare: walk again, writing in the walk's order
+            li = li0;
+            K = K0;
+            bool b3 = false, w3 = false;
+            auto g = [&](uint32_t v) {
+                K += zz_dec32(v);
+                const uint64_t i = e0 + li;
+                if (i < n) P64[i] = K;
+                ++li;
+            };
+            if (!thread_walk_fast(sb, my, g)) thread_walk(sb, my, base + (my - RHALO), ulen, &b3, &w3, g);
+            return;
+        }
+        const uint32_t cnt = (uint32_t)tot.cnt;
+        for (uint32_t e = threadIdx.x; e < cnt; e += RT) {
+            const uint64_t i = e0 + e;
+            if (i < n) P64[i] = tp.sum + (int64_t)kp[e];
+        }
+        return;
+    }
     const bool use16t = sizeof(KT) == 2 || use16;
     auto recompose = [&](uint64_t i, int64_t k) {
         const double r = __dmul_rn((double)k, bin);
@@ -524,10 +551,11 @@ __global__ void k_k32_to_f64(const int32_t* __restrict__ K, uint64_t n, double b
 
 }  // namespace
 
-// status: exclusive tile prefixes CS[T + 1] | tile aggregates CS[T]
+// status: exclusive tile prefixes CS[T + 1] | tile aggregates CS[T] |
+// per-thread prefixes CS[T * RT]
 size_t dec_status_bytes(uint64_t ulen) {
     const uint64_t T = cdiv(ulen, RTILE);
-    return (2 * T + 1) * sizeof(CS);
+    return (2 * T + 1 + T * RT) * sizeof(CS);
 }
 uint64_t dec_tiles(uint64_t ulen_bound) { return cdiv(ulen_bound, RTILE); }
 
@@ -538,9 +566,10 @@ void dec_prepare(const DecSrc& src, uint64_t T, void* status, DevCtl* ctl, cudaS
         return;
     }
     CS* raw = aggs + T + 1;
+    CS* thr = raw + T;
     {
         ProfScope ps_a("k_dec_agg", st);
-        k_dec_agg<<<(unsigned)T, RT, 0, st>>>(src, raw, ctl);
+        k_dec_agg<<<(unsigned)T, RT, 0, st>>>(src, raw, thr, ctl);
         UMCG_LAUNCHED();
     }
     static_assert(sizeof(CS) == sizeof(ulonglong2), "CS scans as a pair of 64-bit sums");
@@ -557,19 +586,21 @@ void dec_fused(int mode, const DecSrc& src, uint64_t T, uint64_t n, void* status
     if (!prepared) dec_prepare(src, T, status, ctl, st);
     if (!T) return;
     ProfScope ps_o(mode == DEC_P64 ? "k_dec_out_grid" : "k_dec_out", st);
+    const CS* raw = aggs + T + 1;
+    const CS* thr = raw + T;
     if (mode == DEC_P64)
         k_dec_out<DEC_P64, int32_t><<<(unsigned)T, RT, 0, st>>>(src, n, aggs, ctl, node, K1, bin1, bin, out, P64,
-                                                               nullptr, nullptr);
+                                                               nullptr, nullptr, raw, thr);
     else if (mode == DEC_VALUES)
         k_dec_out<DEC_VALUES, int32_t><<<(unsigned)T, RT, 0, st>>>(src, n, aggs, ctl, node, K1, bin1, bin, out, P64,
-                                                                  nullptr, nullptr);
+                                                                  nullptr, nullptr, raw, thr);
     else if (mode == DEC_RECOMPOSE16)
         k_dec_out<DEC_RECOMPOSE, int16_t><<<(unsigned)T, RT, 0, st>>>(src, n, aggs, ctl, node,
                                                                      reinterpret_cast<const int16_t*>(K1), bin1, bin,
-                                                                     out, P64, nullptr, nullptr);
+                                                                     out, P64, nullptr, nullptr, raw, thr);
     else
         k_dec_out<DEC_RECOMPOSE, int32_t><<<(unsigned)T, RT, 0, st>>>(src, n, aggs, ctl, node, K1, bin1, bin, out, P64,
-                                                                     kctl, K16);
+                                                                     kctl, K16, raw, thr);
     UMCG_LAUNCHED();
 }
 
