@@ -247,7 +247,7 @@ template <int MODE, class KT>
 #define UMCG_DEC_MINB 5
 #endif
 #ifndef UMCG_DEC_UN
-#define UMCG_DEC_UN 12
+#define UMCG_DEC_UN 8
 #endif
 __global__ void __launch_bounds__(RT, UMCG_DEC_MINB) k_dec_out(const DecSrc src, uint64_t n,
                                                const CS* __restrict__ pre, DevCtl* ctl,
