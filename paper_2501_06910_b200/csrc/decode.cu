@@ -204,12 +204,20 @@ __device__ __forceinline__ int64_t zz_dec32(uint32_t v) { return (int64_t)(v >> 
 __device__ __forceinline__ CS thread_counts(const uint8_t* sb, int my, bool* bad, bool* wide, int64_t base,
                                             uint64_t ulen) {
     uint32_t c = 0;
+    // fast path: codes of <= 4 bytes ending in 32 bytes, so |sum| < 8 * 2^27
+    // fits 32-bit accumulation (the emit runs predicated on every byte)
+    int32_t s32 = 0;
+    auto f32 = [&](uint32_t v) {
+        ++c;
+        s32 += (int32_t)(v >> 1) ^ -(int32_t)(v & 1u);
+    };
+    if (thread_walk_fast(sb, my, f32)) return CS{c, (int64_t)s32};
     int64_t s = 0;
     auto f = [&](uint32_t v) {
         ++c;
         s += zz_dec32(v);
     };
-    if (!thread_walk_fast(sb, my, f)) thread_walk(sb, my, base + (my - RHALO), ulen, bad, wide, f);
+    thread_walk(sb, my, base + (my - RHALO), ulen, bad, wide, f);
     return CS{c, s};
 }
 

@@ -529,16 +529,28 @@ __global__ void __launch_bounds__(BTP) k_bucket_tma(const double* __restrict__ x
         if (threadIdx.x <= E) chreg = __ldg(&bct[bn * (uint64_t)(E + 1) + threadIdx.x]);
         if (k + 2 * G < n_regular) b2 = __ldg(&regular[k + 2 * G]);
     }
+    // UMCG_BT_PROF: per-phase clock64 totals of thread 0 (printf, debug builds)
+#ifdef UMCG_BT_PROF
+    long long tp_issue = 0, tp_wait = 0, tp_sum = 0, tp_res = 0, tq = 0;
+    uint32_t nb_prof = 0;
+#define BT_T0() tq = clock64()
+#define BT_ACC(v) do { const long long t_ = clock64(); v += t_ - tq; tq = t_; } while (0)
+#else
+#define BT_T0() do {} while (0)
+#define BT_ACC(v) do {} while (0)
+#endif
     for (uint32_t it = 0; k < n_regular; ++it, k += G) {
         const int st = it & 1;
         const bool has_next = k + G < n_regular;
         if (has_next && threadIdx.x <= E) stage(st ^ 1).ch[threadIdx.x] = chreg;
         __syncthreads();
+        BT_T0();
         Info nn{0, 0, 0, 0};
         uint32_t b3 = 0;
         if (has_next) {
             if (warp == 0)
                 tma_issue(stage(st ^ 1), &bars[st ^ 1], xE, lslot, lnode, nxt.s0, nxt.m, E);
+            BT_ACC(tp_issue);
             if (k + 2 * G < n_regular) {
                 nn = load_info(b2);
                 if (threadIdx.x <= E) chreg = __ldg(&bct[b2 * (uint64_t)(E + 1) + threadIdx.x]);
@@ -556,7 +568,9 @@ __global__ void __launch_bounds__(BTP) k_bucket_tma(const double* __restrict__ x
                 sgr[h][1] = __ldg(&seg[j0 + j + 1]);
             }
         }
+        BT_T0();
         mbar_wait(&bars[st], (it >> 1) & 1u);
+        BT_ACC(tp_wait);
         const TmaStage C = stage(st);
         const uint32_t lo8 = s0 & 7u;
         // interpolate_to_grid (interp.hpp:58-64): 0.0 + x_a + x_b + ... in ascending vertex order
@@ -573,6 +587,7 @@ __global__ void __launch_bounds__(BTP) k_bucket_tma(const double* __restrict__ x
             grid_k(gk, j0 + j, v, ctl);
         }
         __syncthreads();
+        BT_ACC(tp_sum);
         // compute_residuals (interp.hpp:161-170) + lattice index (codec.hpp:307-314)
         for (uint32_t e = warp; KE && e < E; e += BTP / 32) {
             const uint2 c0 = C.ch[e], c1 = C.ch[e + 1];
@@ -585,7 +600,18 @@ __global__ void __launch_bounds__(BTP) k_bucket_tma(const double* __restrict__ x
         nxt = nn;
         b2 = b3;
         __syncthreads();
+        BT_ACC(tp_res);
+#ifdef UMCG_BT_PROF
+        ++nb_prof;
+#endif
     }
+#ifdef UMCG_BT_PROF
+    if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == 150))
+        printf("[bt prof] block %u buckets %u cycles: issue %lld wait %lld sum %lld res %lld\n", blockIdx.x, nb_prof,
+               tp_issue, tp_wait, tp_sum, tp_res);
+#endif
+#undef BT_T0
+#undef BT_ACC
 }
 
 // ---- multilinear g in bucket order -------------------------------------------
