@@ -483,6 +483,13 @@ __device__ __forceinline__ void tma_issue(const TmaStage& S, uint64_t* bar, cons
 }
 
 static_assert(kBucketNodes <= 2 * BTP, "k_bucket_tma keeps <= 2 slots per thread in registers");
+// The warp that issues the next bucket's bulk copies (~100 cycles per copy,
+// E + 2 copies): the last warp, which owns slots only in buckets of more
+// than 480 slots, so the issue overlaps the other warps' ordered sums.
+#ifndef UMCG_BT_ISSUE_WARP
+#define UMCG_BT_ISSUE_WARP (BTP / 32 - 1)
+#endif
+constexpr int BT_ISSUE_WARP = UMCG_BT_ISSUE_WARP;
 
 template <class KT>
 __global__ void __launch_bounds__(BTP) k_bucket_tma(const double* __restrict__ xE, const uint32_t* __restrict__ bk,
@@ -519,7 +526,7 @@ __global__ void __launch_bounds__(BTP) k_bucket_tma(const double* __restrict__ x
     Info cur = load_info(b);
     if (threadIdx.x <= E) stage(0).ch[threadIdx.x] = __ldg(&bct[b * (uint64_t)(E + 1) + threadIdx.x]);
     __syncthreads();
-    if (warp == 0) tma_issue(stage(0), &bars[0], xE, lslot, lnode, cur.s0, cur.m, E);
+    if (warp == BT_ISSUE_WARP) tma_issue(stage(0), &bars[0], xE, lslot, lnode, cur.s0, cur.m, E);
     uint2 chreg = make_uint2(0, 0);
     Info nxt{0, 0, 0, 0};
     uint32_t b2 = 0;
@@ -548,7 +555,7 @@ __global__ void __launch_bounds__(BTP) k_bucket_tma(const double* __restrict__ x
         Info nn{0, 0, 0, 0};
         uint32_t b3 = 0;
         if (has_next) {
-            if (warp == 0)
+            if (warp == BT_ISSUE_WARP)
                 tma_issue(stage(st ^ 1), &bars[st ^ 1], xE, lslot, lnode, nxt.s0, nxt.m, E);
             BT_ACC(tp_issue);
             if (k + 2 * G < n_regular) {
