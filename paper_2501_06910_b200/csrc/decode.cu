@@ -17,6 +17,10 @@
 
 namespace umcg {
 
+#ifndef UMCG_GATHER_LD
+#define UMCG_GATHER_LD __ldcg  // load of the random K1 gathers: L2 only (A/B: __ldg 2 % slower)
+#endif
+
 namespace {
 
 
@@ -377,7 +381,7 @@ __global__ void __launch_bounds__(RT, UMCG_DEC_MINB) k_dec_out(const DecSrc src,
             const uint32_t e = e0 + u * RT + threadIdx.x;
             if (MODE == DEC_RECOMPOSE && e < cnt && tp.cnt + e < n)
                 g1[u] = sizeof(KT) == 2 || use16
-                            ? (int32_t)__ldg((sizeof(KT) == 2 ? reinterpret_cast<const int16_t*>(K1) : K16) + nd[u])
+                            ? (int32_t)UMCG_GATHER_LD((sizeof(KT) == 2 ? reinterpret_cast<const int16_t*>(K1) : K16) + nd[u])
                             : ld_s32_hint(reinterpret_cast<const int32_t*>(K1) + nd[u], pl);
             else
                 g1[u] = 0;

@@ -30,6 +30,10 @@
 
 namespace umcg {
 
+#ifndef UMCG_GATHER_LD
+#define UMCG_GATHER_LD __ldcg  // load of the random gathers: L2 only (A/B: __ldg 2-3 % slower)
+#endif
+
 namespace {
 
 constexpr int PT = 256;
@@ -57,7 +61,7 @@ __global__ void __launch_bounds__(PT) k_gather_fwd(const T* __restrict__ x, uint
 #pragma unroll
     for (int k = 0; k < GI; ++k) {
         const uint64_t p = base + (uint64_t)k * PT;
-        v[k] = p < n ? (double)__ldg(x + s[k]) : 0.0;
+        v[k] = p < n ? (double)UMCG_GATHER_LD(x + s[k]) : 0.0;
     }
 #pragma unroll
     for (int k = 0; k < GI; ++k) {
@@ -702,7 +706,7 @@ __global__ void __launch_bounds__(ENC_THREADS) k_resid_codes(const uint32_t* __r
         }
         int32_t K[ENC_ITEMS];
 #pragma unroll
-        for (int k = 0; k < ENC_ITEMS; ++k) K[k] = first + k < n ? (int32_t)__ldg(&Kp[d[k]]) : 0;
+        for (int k = 0; k < ENC_ITEMS; ++k) K[k] = first + k < n ? (int32_t)UMCG_GATHER_LD(&Kp[d[k]]) : 0;
 #pragma unroll
         for (int k = 0; k < ENC_ITEMS; ++k) {
             if (first + k < n) {
