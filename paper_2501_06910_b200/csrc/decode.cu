@@ -34,15 +34,6 @@ struct CSAdd {
     }
 };
 
-__device__ __forceinline__ uint64_t varint_back(const uint8_t* sb, int e) {
-    int s = e;
-    while (s > 0 && (sb[s - 1] & 0x80) && e - (s - 1) < 10) --s;
-    uint64_t v = 0;
-    int shift = 0;
-    for (int j = s; j <= e; ++j, shift += 7) v |= (uint64_t)(sb[j] & 0x7f) << shift;
-    return v;
-}
-
 // ---- three-phase (reduce, scan, apply) decode: every phase is fully
 // parallel, no inter-CTA waiting. Tiles of 8 KiB of varint bytes.
 constexpr int RT = 256;

@@ -37,7 +37,6 @@ namespace umcg {
 namespace {
 
 constexpr int PT = 256;
-constexpr int PI = 4;  // vertices per thread in the partition pass
 
 // Forward permutation into layout E: xE[p] = x[srcE[p]] (gather inside one
 // epoch's window) + value range / finiteness over the same values.
@@ -126,7 +125,7 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
                                               const uint16_t* __restrict__ lperm, const uint32_t* __restrict__ seg,
                                               DevCtl* ctl, double* __restrict__ x1, KT* __restrict__ KE,
                                               int heavy_only, GridK gk) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     double* xs = reinterpret_cast<double*>(smem);                      // [kBucketCap]
     double* x1s = xs + kBucketCap;                                     // [kBucketNodes]
     uint32_t* sg = reinterpret_cast<uint32_t*>(x1s + kBucketNodes);    // [kBucketNodes + 1]
@@ -265,15 +264,6 @@ __device__ __forceinline__ PipeStage make_stage(unsigned char* p, uint32_t E) {
     return S;
 }
 
-__device__ __forceinline__ uint32_t chunk_of(const uint2* ch, uint32_t E, uint32_t l) {
-    uint32_t lo = 0, hi = E;
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (ch[mid].x <= l) lo = mid; else hi = mid;
-    }
-    return lo;
-}
-
 __device__ __forceinline__ void issue_bucket(const PipeStage& S, const double* __restrict__ xE,
                                              const uint16_t* __restrict__ lperm, const uint16_t* __restrict__ lnode,
                                              const uint32_t* __restrict__ seg, uint32_t s0, uint32_t m, uint32_t j0,
@@ -300,7 +290,7 @@ __global__ void __launch_bounds__(BTP) k_bucket_pipe(const double* __restrict__ 
                                                    const uint16_t* __restrict__ lperm,
                                                    const uint32_t* __restrict__ seg, DevCtl* ctl,
                                                    double* __restrict__ x1, KT* __restrict__ KE, GridK gk) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     // Stage pointers are recomputed from the extern shared array (never kept
     // in a runtime-indexed array) so every access compiles to LDS/STS rather
     // than generic loads.
