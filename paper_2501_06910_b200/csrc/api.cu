@@ -242,11 +242,38 @@ DevCtl verbatim_pass(umcg_plan* p, const umcg_params& prm, const std::string& na
     return read_ctl(p, ctl, st);
 }
 
+// UMCG_COMP_TRACE=1: device timestamps of the compress phases on stderr.
+struct CompTrace {
+    bool on = std::getenv("UMCG_COMP_TRACE") != nullptr;
+    cudaEvent_t e[12] = {};
+    const char* en[12] = {};
+    int ne = 0;
+    CompTrace() {
+        if (on)
+            for (auto& x : e) cudaEventCreate(&x);
+    }
+    void dev(const char* n, cudaStream_t st) {
+        if (on && ne < 12) { en[ne] = n; cudaEventRecord(e[ne++], st); }
+    }
+    ~CompTrace() {
+        if (!on) return;
+        cudaDeviceSynchronize();
+        for (int i = 1; i < ne; ++i) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e[0], e[i]);
+            std::fprintf(stderr, "[comp trace] %-14s +%.1f us\n", en[i], 1e3 * ms);
+        }
+        for (auto& x : e) cudaEventDestroy(x);
+    }
+};
+
 // One pass of the compress pipeline. Returns the device control block.
 DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int x_f32, const std::string& name,
                      uint8_t* d_ar, const CompressMode& m, cudaStream_t st) {
     const uint64_t n = p->n, n1 = p->n_slots;
     auto* ctl = p->ctl.as<DevCtl>(1);
+    CompTrace tr;
+    tr.dev("start", st);
     init_ctl(ctl, st);
     // nearest g: partitioned layout (partition.cu); multilinear: gathers
     // multilinear g on the partitioned layout: means as for nearest, then the
@@ -268,10 +295,12 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
         double* xp = p->scratch_c.as<double>(n + 4);  // + padding: 16-byte bulk copies may overrun
         Kp = p->kbuf.as<int32_t>(std::max<uint64_t>(n, n1) + 1);
         partition_values(d_x, x_f32, p, xp, ctl, st);  // + range / finiteness
+        tr.dev("gather", st);
         budget(BudgetArgs{prm.tau, prm.split_rho, prm.coeff_abs_sum, prm.bound_kind, n}, ctl, st);
         // f: cluster means (interp.hpp:46-93) + residual lattice indices
         bucket_means_residuals(p, xp, ctl, x1, ml_part ? nullptr : Kp, narrow,
                                fuse_k1 ? p->scratch_d.as<int32_t>(n1 ? n1 : 1) : nullptr, p->dim, st);
+        tr.dev("bucket", st);
     } else {
         minmax(d_x, x_f32, n, ctl, st);
         budget(BudgetArgs{prm.tau, prm.split_rho, prm.coeff_abs_sum, prm.bound_kind, n}, ctl, st);
@@ -319,6 +348,8 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     // Common case: the grid component's chain (codes, stream plan, write) runs
     // on a side stream beside the residual's; they share only the layout step.
     const bool overlap = part && !m.serial[0] && !m.serial[1] && !m.lossless[0] && !m.lossless[1];
+    // (normal priority: on the high-priority stream the grid chain finishes
+    // early but k_resid_codes slows by as much -- UMCG_COMP_TRACE)
     cudaStream_t sg = st;
     if (overlap) {
         sg = p->side.get();
@@ -336,6 +367,7 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     } else {
         int32_t* kb = p->scratch_d.as<int32_t>(n1 ? n1 : 1);
         codes_lossy_values(x1, n1, pred1, sh1, ctl, 0, static_cast<uint32_t*>(codes[0]), kb, sg, fuse_k1);
+        tr.dev("grid codes(sg)", sg);
     }
     // residual component
     if (m.serial[1]) {
@@ -360,6 +392,7 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     if (fused_resid) {
         // q = K2_i - K2_{i-1} back in vertex order + RLE tile summaries (partition.cu)
         resid_codes_tiles(p, Kp, codes[1], narrow, es[1], st);
+        tr.dev("resid codes", st);
     } else if (!m.serial[1] && !m.lossless[1]) {
         codes_lossy_residual(rs, n, ctl, static_cast<uint32_t*>(codes[1]), st);
     }
@@ -371,6 +404,8 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
         else if (wide[c]) stream_plan_u64(static_cast<uint64_t*>(codes[c]), ncode[c], es[c], ctl, c, sc);
         else stream_plan_u32(static_cast<uint32_t*>(codes[c]), ncode[c], es[c], ctl, c, sc);
     }
+    tr.dev("plans", st);
+    if (overlap) tr.dev("grid plan(sg)", sg);
     if (overlap) p->side.link(sg, st, 1);  // layout needs both stream lengths
     const HdrArgs h = archive_hdr(p, prm, name, 0, pred1, D1, dims1, st);
     k_layout_archive<<<1, 32, 0, st>>>(h, ctl, d_ar);
@@ -380,7 +415,9 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
         stream_write_u32(static_cast<uint32_t*>(codes[0]), ncode[0], es[0], ctl, 0, d_ar, true, sg);
         if (narrow) stream_write_u16(static_cast<uint16_t*>(codes[1]), ncode[1], es[1], ctl, 1, d_ar, true, st);
         else stream_write_u32(static_cast<uint32_t*>(codes[1]), ncode[1], es[1], ctl, 1, d_ar, true, st);
+        tr.dev("resid write", st);
         p->side.link(sg, st, 3);
+        tr.dev("end", st);
         return read_ctl(p, ctl, st);
     }
     for (int c = 0; c < 2; ++c) {
