@@ -117,14 +117,23 @@ def replica_value(ws: int, n: int, ms: float) -> float:
 
 
 def setup_config3(lattice: int, grid: int, dev, keep_coords=False):
+    """Inputs on the device and the plan (K0: GPU grid_coarsen + layout E).
+    Returns (plan, x, plan build ms: wall clock around umcg_plan_build with
+    the device synchronized on both sides -- it includes the host-side
+    mapping digest -- reported separately from the step)."""
     import torch
     import paper_2501_06910_b200 as umcg
     xyz, x = umcg.gen_config(3, lattice, SEED, device=dev)
     axes = [np.linspace(0.0, 1.0, grid) for _ in range(3)]  # uniform axes over the exact bbox
-    plan = umcg.Plan.build(axes, xyz, keep_coords=keep_coords)
-    del xyz
+    plan = umcg.Plan.build(axes, xyz, keep_coords=keep_coords)  # warm (allocations, attributes)
+    del plan
     torch.cuda.synchronize()
-    return plan, x
+    t0 = time.perf_counter()
+    plan = umcg.Plan.build(axes, xyz, keep_coords=keep_coords)
+    torch.cuda.synchronize()
+    plan_ms = (time.perf_counter() - t0) * 1e3
+    del xyz
+    return plan, x, plan_ms
 
 
 def algorithmic_bytes(n, n1, archive):
@@ -179,69 +188,87 @@ def committed_traffic():
         return {}
 
 
-def cpu_reference_sample(lattice: int, grid: int, threads: int, reps: int, tau: float):
-    """Time the unmodified reference (oracle/_ref) on a bounded sample of the
-    config-3 workload: `threads` concurrent compress+decompress calls."""
-    import torch
-    import paper_2501_06910_b200 as umcg
-    from oracle.bindings import Ref, Setup
-    xyz, x = umcg.gen_config(3, lattice, SEED, device="cuda")
-    axes = [np.linspace(0.0, 1.0, grid) for _ in range(3)]
-    plan = umcg.Plan.build(axes, xyz)
-    mode, gaxes, assign, visited = plan.export()
-    xh = x.cpu().numpy()
-    del xyz, x
-    torch.cuda.empty_cache()
-    R = Ref()
-    s = Setup(dim=3, axes=gaxes, mode=mode, assignments=assign, visited=visited)
-    ctx = R.ctx(s)
-    n = len(xh)
-    results = []
+def workload_config(lattice: int, grid: int, tau: float, ws: int) -> dict:
+    """The `config` both arms print (identical dicts: the reference arm times a
+    block sample of this same workload and says so in cpu_baseline.sample)."""
+    n = lattice ** 3
+    return {"workload": f"config3 lattice{lattice}^3 ({n} vertices) grid{grid}^3 tau_rel {tau} rho 0.5 nearest g",
+            "l2": "inputs larger than L2 (1.07 GB field), no flush", "parallelism": f"replicas x{ws}"}
 
-    def work():
-        tc, td, ab = R.time_roundtrip(ctx, xh, tau, reps=1)
-        results.append((tc, td, ab))
 
-    R.time_roundtrip(ctx, xh, tau, reps=1)  # warm
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        ts = [threading.Thread(target=work) for _ in range(threads)]
-        for t in ts:
-            t.start()
-        for t in ts:
-            t.join()
-    wall = time.perf_counter() - t0
-    tc = float(np.mean([r[0] for r in results]))
-    td = float(np.mean([r[1] for r in results]))
-    gbs = threads * reps * n * 8 / wall / 1e9
-    return dict(value=gbs, unit="GB/s", cores=threads, kind="reference",
-                sample=f"config-3 construction at lattice {lattice}^3 ({n} vertices), grid {grid}^3, "
-                       f"tau_rel {tau}: {threads} concurrent compress+decompress x {reps} rounds "
-                       f"(per call: compress {tc:.3f} s, decompress {td:.3f} s)",
-                compress_s=tc, decompress_s=td, wall_s=wall, n=n)
+REF_BLOCK = 256  # reference-arm sample: the 256^3 lattice block of the 512^3 mesh (16.7M vertices)
+
+
+def cpu_baseline_single_core(tau: float, block: int = REF_BLOCK, reps: int = 3) -> dict:
+    """One pinned core, median of `reps` reference round trips on the block
+    sample (oracle/cpu_bench.py in a subprocess: host-generated inputs, the
+    reference's own grid_coarsen, no product library)."""
+    pin = sorted(os.sched_getaffinity(0))[-1]
+    r = subprocess.run([sys.executable, "-m", "oracle.cpu_bench", "--block", str(block), "--reps", str(reps),
+                        "--tau", str(tau), "--pin", str(pin)], cwd=ROOT, capture_output=True, text=True,
+                       timeout=900)
+    if r.returncode:
+        raise RuntimeError(r.stderr[-300:])
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    out = {"value": d["roundtrip_gbs"], "unit": "GB/s", "cores": 1, "kind": "reference",
+           "sample": f"config-3 lattice block {block}^3 of the 512^3 mesh ({d['vertices']} vertices, "
+                     f"same coordinates/values/vertex order as the full run, grid {d['grid']} after the "
+                     f"reference's grid_coarsen), tau_rel {tau}: median of {reps} compress+decompress "
+                     f"round trips on CPU {pin} (pinned)",
+           "compress_s": d["compress_s"], "decompress_s": d["decompress_s"], "digest_s": d["digest_s"],
+           "value_minus_digest": d["roundtrip_gbs_minus_digest"], "nproc": d["nproc"],
+           "cpu_model": d["cpu_model"]}
+    try:  # committed full-size single-core measurement (tools/cpu_full.sh)
+        with open(os.path.join(ROOT, "profiles", "r02_cpu_full.json")) as f:
+            full = json.load(f)
+        out["full_size"] = {k: full[k] for k in ("vertices", "compress_s", "decompress_s", "digest_s",
+                                                  "roundtrip_gbs", "roundtrip_gbs_minus_digest", "reps",
+                                                  "cpu_model", "nproc") if k in full}
+        out["full_size"]["source"] = "profiles/r02_cpu_full.json"
+    except Exception:
+        pass
+    return out
 
 
 def run_reference(args):
+    """--impl reference: the unmodified reference (oracle/_ref) on the host
+    cores. All host threads run concurrent round trips (the reference is
+    reentrant, each call single-threaded) on the block sample of the same
+    workload; value = field bytes of all calls / step wall time. This process
+    never imports the product package (inputs: oracle/datagen_host.c;
+    mapping: the reference's grid_coarsen)."""
     ws, rank, local = dist_env()
     if rank != 0:
         return 0
-    threads = min(os.cpu_count() or 1, 32)
-    lat, grid = 128, 64
+    from oracle.cpu_bench import Concurrent, host_info
+    threads = len(os.sched_getaffinity(0))
     base = dict(impl="reference", metric=METRIC, unit="GB/s", higher_is_better=True, n_gpus=args.gpus,
                 steps=args.steps, warmup=args.warmup, scaling="weak", vs_baseline=None, dtype="f64",
-                data="synthetic")
+                data="synthetic (host generator, byte-identical to the GPU arm's inputs)",
+                config=workload_config(args.lattice, args.grid, args.tau, args.gpus))
     try:
+        c = Concurrent(REF_BLOCK, threads, args.tau)
         for _ in range(args.warmup):
-            cpu_reference_sample(lat, grid, threads, 1, args.tau)
-        r = cpu_reference_sample(lat, grid, threads, args.steps, args.tau)
+            c.step()
+        c.per_call = []
+        ts = [c.step() for _ in range(args.steps)]
     except Exception as e:
         print(json.dumps(dict(base, unavailable=f"reference CPU run failed: {e}"[:300])))
         return 0
-    out = dict(base, value=r["value"], ms_per_step=1e3 * r["wall_s"] / args.steps,
-               config={"workload": f"config3-sample lattice{lat}^3 grid{grid}^3 tau_rel {args.tau}",
-                       "threads": threads},
-               cpu_baseline={k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
-               e2e={"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+    n = c.x.size
+    wall = float(sum(ts))
+    value = threads * args.steps * n * 8 / wall / 1e9
+    tc = float(np.median([r[0] for r in c.per_call]))
+    td = float(np.median([r[1] for r in c.per_call]))
+    cb = {"value": value, "unit": "GB/s", "cores": threads, "kind": "reference",
+          "sample": f"config-3 lattice block {REF_BLOCK}^3 of the 512^3 mesh ({n} vertices, same coordinates/"
+                    f"values/vertex order as the full run; mapping by the reference's grid_coarsen, grid "
+                    f"{c.info['grid']}): {threads} concurrent compress+decompress round trips per step "
+                    f"(median per call: compress {tc:.3f} s, decompress {td:.3f} s)",
+          **host_info()}
+    out = dict(base, value=value, ms_per_step=1e3 * wall / args.steps, cpu_baseline=cb,
+               e2e={"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+               sample_setup={k: c.info[k] for k in ("gen_s", "grid_coarsen_s", "visited_fraction", "mode")})
     print(json.dumps(out))
     return 0
 
@@ -275,7 +302,7 @@ def main():
             import torch.distributed as dist
             dist.barrier()
 
-    plan, x = setup_config3(args.lattice, args.grid, dev)
+    plan, x, plan_ms = setup_config3(args.lattice, args.grid, dev)
     n, n1 = plan.n, int(plan.info.n_slots)
     budget = umcg.Budget(tau=args.tau, split_rho=0.5, bound_kind=1)
     cap = plan.compress_bound("field")
@@ -394,10 +421,8 @@ def main():
         metric=METRIC, value=value, unit="GB/s", n_gpus=ws, steps=args.steps, warmup=args.warmup,
         ms_per_step=ms, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
         data="synthetic (GPU-generated, SplitMix64-seeded config 3)",
-        config={"workload": f"config3 lattice{args.lattice}^3 ({n} vertices) grid{args.grid}^3 "
-                            f"tau_rel {args.tau} rho 0.5 nearest g",
-                "l2": "inputs larger than L2 (1.07 GB field), no flush", "parallelism": f"replicas x{ws}",
-                "archive_bytes": alen, "mode": "seed" if plan.info.mode else "dense"},
+        config=workload_config(args.lattice, args.grid, args.tau, ws),
+        run={"archive_bytes": alen, "mode": "seed" if plan.info.mode else "dense", "plan_build_ms": plan_ms},
         compress={"ms": tcm, "gbs_field": n * 8 / tcm / 1e6, "algorithmic_bytes": b_c,
                   "roofline_frac": b_c / (tcm * 1e-3) / 1e9 / peak},
         decompress={"ms": tdm, "gbs_field": n * 8 / tdm / 1e6, "algorithmic_bytes": b_d,
@@ -418,8 +443,7 @@ def main():
     )
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
-            cb = cpu_reference_sample(256, 128, 1, 1, args.tau)
-            res["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            res["cpu_baseline"] = cpu_baseline_single_core(args.tau)
         except Exception as e:
             res["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
     if rank == 0:

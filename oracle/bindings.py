@@ -4,6 +4,8 @@
                (header-only C++20 from /root/reference/proj/include) behind
                the extern "C" shim in oracle/ref_shim.cpp.
 * ``Oracle`` -- oracle/liboracle.so: the plain-C restatement (umc_oracle.c).
+* ``HostGen`` -- oracle/libdatagen_host.so: the host generator of the
+               synthetic BASELINE inputs, byte-identical to the device one.
 
 Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg (and
 its ``--impl reference`` arm) may import this module, and only as the checker
@@ -20,6 +22,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 REF_SO = os.path.join(HERE, "_ref", "libumcref.so")
 ORACLE_SO = os.path.join(HERE, "liboracle.so")
+DATAGEN_SO = os.path.join(HERE, "libdatagen_host.so")
 
 u8p = C.POINTER(C.c_uint8)
 u64p = C.POINTER(C.c_uint64)
@@ -436,3 +439,44 @@ class Oracle:
         self._check(self.lib.umco_decompress(C.byref(st), _ptr(buf, u8p), len(archive),
                                              _ptr(out, f64p)))
         return out[: s.n_v]
+
+
+class HostGen:
+    """Host generator of the BASELINE synthetic inputs (oracle/datagen_host.c):
+    the same bytes as umcg_gen_config, without the product library."""
+
+    def __init__(self, path: str = DATAGEN_SO, threads: int | None = None):
+        self.lib = L = C.CDLL(path)
+        L.dgh_gen.argtypes = [C.c_int, C.c_uint64, C.c_uint64, f64p, C.c_void_p, u64p, C.c_int]
+        L.dgh_gen3_block.argtypes = [C.c_uint64, C.c_uint64, u64p, u64p, f64p, f64p, u64p, C.c_int]
+        self.threads = threads or (os.cpu_count() or 1)
+
+    def gen(self, config: int, lattice: int, seed: int, coords=True, values=True):
+        n = C.c_uint64()
+        if self.lib.dgh_gen(config, lattice, seed, None, None, C.byref(n), 1):
+            raise ValueError("bad config / lattice")
+        n = n.value
+        dim = 3 if config in (3, 5) else 2
+        xyz = np.empty((n, dim), np.float64) if coords else None
+        vals = (np.empty((5, n), np.float32) if config == 4 else np.empty(n, np.float64)) if values else None
+        rc = self.lib.dgh_gen(config, lattice, seed, _ptr(xyz, f64p),
+                              None if vals is None else vals.ctypes.data_as(C.c_void_p), C.byref(C.c_uint64()),
+                              self.threads)
+        if rc:
+            raise RuntimeError(f"dgh_gen failed ({rc})")
+        return xyz, vals
+
+    def gen3_block(self, lattice: int, seed: int, lo, hi, coords=True, values=True):
+        """Config 3 restricted to lattice points in [lo, hi) per axis, in the
+        full mesh's (permuted) vertex order."""
+        lo = np.ascontiguousarray(lo, np.uint64)
+        hi = np.ascontiguousarray(hi, np.uint64)
+        n = int(np.prod(hi.astype(np.int64) - lo.astype(np.int64)))
+        xyz = np.empty((n, 3), np.float64) if coords else None
+        vals = np.empty(n, np.float64) if values else None
+        cnt = C.c_uint64()
+        rc = self.lib.dgh_gen3_block(lattice, seed, _ptr(lo, u64p), _ptr(hi, u64p), _ptr(xyz, f64p),
+                                     _ptr(vals, f64p), C.byref(cnt), self.threads)
+        if rc or cnt.value != n:
+            raise RuntimeError(f"dgh_gen3_block failed ({rc})")
+        return xyz, vals

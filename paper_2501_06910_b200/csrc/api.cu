@@ -187,6 +187,7 @@ void host_budget(double tau_abs, double rho, double coeff, double* tc) {
 struct CompressMode {
     bool lossless[2];
     bool serial[2];
+    bool no_narrow;  // a narrow pass saw |K2| > 16383: int32 lattice indices
     bool verbatim;  // codec 1: both components are RLE'd raw fp64 bytes (codec.hpp:240-248)
 };
 
@@ -280,11 +281,13 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     // residuals bucket by bucket (partition.cu k_ml_bucket)
     const bool ml_part = prm.g_kind == 1 && p->n_buckets > 0 && p->has_coords && p->mode == 0 && !m.verbatim;
     const bool part = (prm.g_kind == 0 && p->n_buckets > 0 && !m.verbatim) || ml_part;
-    // Narrow residual path (int16 lattice indices, u16 codes): a residual is
-    // x_i minus the mean of its cluster, so |r| <= range and, for a relative
-    // bound, |K2| <= range / bin2 ~ 1 / (2 (1 - rho) tau): <= 16383 keeps every
-    // code zigzag(K_i - K_{i-1}) < 2^16.
-    const bool narrow = part && !m.serial[1] && !m.lossless[1] && prm.bound_kind == 1 && prm.tau > 0.0 &&
+    // Narrow residual path (int16 lattice indices, u16 codes): for nearest g a
+    // residual is x_i minus the mean of its cluster, so |r| <= range and, for
+    // a relative bound, |K2| <= range / bin2 ~ 1 / (2 (1 - rho) tau): <= 16383
+    // keeps every code zigzag(K_i - K_{i-1}) < 2^16. Multilinear g has no such
+    // bound (unvisited corners hold 0.0), so the bucket kernels check every
+    // |K2| and flag need_wide; the pass then reruns with int32 indices.
+    const bool narrow = part && !m.no_narrow && !m.serial[1] && !m.lossless[1] && prm.bound_kind == 1 && prm.tau > 0.0 &&
                         1.0 / (2.0 * (1.0 - prm.split_rho) * prm.tau) < 16000.0;
     // dense N-D grid: the bucket kernels also write K1 = lattice(x1) (no fill
     // pass may change x1 afterwards)
@@ -482,7 +485,7 @@ void compress_impl(umcg_plan* p, const umcg_params* prm_in, const void* d_x, int
         m.lossless[0] = m.lossless[1] = prm.tau == 0.0;
     }
     m.verbatim = prm.codec_id == 1;
-    for (int iter = 0; iter < 3; ++iter) {
+    for (int iter = 0; iter < 4; ++iter) {
         const DevCtl hc = compress_pass(p, prm, d_x, x_f32, name, d_ar, m, st);
         if (hc.nonfinite) fail(UMCG_NON_FINITE_VALUE, "non-finite field value");
         if (m.verbatim) {
@@ -490,6 +493,7 @@ void compress_impl(umcg_plan* p, const umcg_params* prm_in, const void* d_x, int
             return;
         }
         bool redo = false;
+        if (hc.need_wide && !m.no_narrow) { m.no_narrow = true; redo = true; }
         for (int c = 0; c < 2; ++c) {
             const bool ll = (hc.lossless >> c) & 1;
             if (ll != m.lossless[c]) { m.lossless[c] = ll; m.serial[c] = false; redo = true; }

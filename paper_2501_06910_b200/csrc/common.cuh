@@ -332,6 +332,7 @@ struct DevCtl {
     int lossless;                         // tau_abs == 0
     // per-component fast-path verdicts
     int need_serial[2];                   // escape / regime violation: redo exactly
+    int need_wide;                        // narrow (int16) residual path overflowed: redo in int32
     unsigned long long max_abs_k[2];      // |K| maxima (decode regime check)
     // stream lengths and archive layout
     uint64_t stream_len[2];

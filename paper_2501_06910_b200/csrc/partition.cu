@@ -88,13 +88,22 @@ __device__ __forceinline__ void flag_serial1(DevCtl* ctl) {
 }
 
 // lattice index with the escape / regime checks of codec.hpp:305-314
-// (same as codes.cu lattice_k, 1-D limit 2^30).
-__device__ __forceinline__ int32_t resid_k(double r, double bin, double inv, double tau, DevCtl* ctl) {
+// (same as codes.cu lattice_k, 1-D limit 2^30). KT = int16_t is the narrow
+// path: every |K| <= 16383 keeps each code zigzag(K_i - K_{i-1}) < 2^16. A
+// larger |K| is not an escape, only too wide for int16 (e.g. multilinear g
+// blending the 0.0 of unvisited nodes, interp.hpp:56, 78, 129, into a field
+// far from zero): it flags need_wide and the host reruns the int32 path.
+template <class KT>
+__device__ __forceinline__ KT resid_k(double r, double bin, double inv, double tau, DevCtl* ctl) {
     double err;
     const double K = lattice_round(r, bin, inv, tau, &err);
     const bool bad = !(fabs(K) < 1073741824.0) || !(err <= tau);
     if (bad) flag_serial1(ctl);
-    return bad ? 0 : (int32_t)K;
+    if (sizeof(KT) == 2 && !bad && !(fabs(K) <= 16383.0)) {
+        if (ctl->need_wide == 0) atomicExch(&ctl->need_wide, 1);
+        return 0;
+    }
+    return bad ? 0 : (KT)(int32_t)K;
 }
 
 // Grid lattice index of a cluster mean, fused into the bucket kernels for the
@@ -163,7 +172,7 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
         for (uint32_t e = warp; e < E; e += NW)
             for (uint32_t l = ch[e].x + lane; l < ch[e + 1].x; l += 32) {
                 const uint32_t q = ch[e].y + (l - ch[e].x);
-                KE[q] = (KT)resid_k(__dsub_rn(xE[q], mean), bin, inv, tau, ctl);
+                KE[q] = resid_k<KT>(__dsub_rn(xE[q], mean), bin, inv, tau, ctl);
             }
         return;
     }
@@ -223,7 +232,7 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
             const uint32_t l = threadIdx.x + k * BT;
             if (l < m) {
                 while (l >= ch[e + 1].x) ++e;
-                KE[ch[e].y + (l - ch[e].x)] = (KT)resid_k(__dsub_rn(xs[l], x1s[ln[l]]), bin, inv, tau, ctl);
+                KE[ch[e].y + (l - ch[e].x)] = resid_k<KT>(__dsub_rn(xs[l], x1s[ln[l]]), bin, inv, tau, ctl);
             }
         }
     }
@@ -368,7 +377,7 @@ __global__ void __launch_bounds__(BTP) k_bucket_pipe(const double* __restrict__ 
             for (uint32_t e = warp; e < E; e += BTP / 32) {
                 const uint2 c0 = C.ch[e], c1 = C.ch[e + 1];
                 for (uint32_t l = c0.x + lane; l < c1.x; l += 32)
-                    KE[c0.y + (l - c0.x)] = (KT)resid_k(__dsub_rn(C.xs[l], x1s[C.ln[l + off]]), bin, inv, tau, ctl);
+                    KE[c0.y + (l - c0.x)] = resid_k<KT>(__dsub_rn(C.xs[l], x1s[C.ln[l + off]]), bin, inv, tau, ctl);
             }
         }
         cur = nxt;
@@ -595,7 +604,7 @@ __global__ void __launch_bounds__(BTP, 2) k_bucket_tma(const double* __restrict_
             const uint32_t sbase = c0.x + 2 * e + ((c0.y - c0.x - 2 * e) & 1u);
             for (uint32_t l = c0.x + lane; l < c1.x; l += 32)
                 KE[c0.y + (l - c0.x)] =
-                    (KT)resid_k(__dsub_rn(C.xs[sbase + (l - c0.x)], x1s[C.ln[l + lo8]]), bin, inv, tau, ctl);
+                    resid_k<KT>(__dsub_rn(C.xs[sbase + (l - c0.x)], x1s[C.ln[l + lo8]]), bin, inv, tau, ctl);
         }
         cur = nxt;
         nxt = nn;
@@ -657,7 +666,7 @@ __global__ void __launch_bounds__(256) k_ml_bucket(const double* __restrict__ xE
             double pc[3] = {0, 0, 0};
             for (int d = 0; d < g.D; ++d) pc[d] = __ldcs(&cE[d * n + p]);
             const double gv = multilinear_eval(g.axes, g.axis_off, g.shape, g.D, x1, pc, g.inv_cell, g.scale);
-            if (MODE == 0) KE[p] = (KT)resid_k(__dsub_rn(__ldcs(&xE[p]), gv), bin, inv, tau, ctl);
+            if (MODE == 0) KE[p] = resid_k<KT>(__dsub_rn(__ldcs(&xE[p]), gv), bin, inv, tau, ctl);
             else gE[p] = gv;
         }
     }

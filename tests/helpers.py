@@ -12,6 +12,9 @@ import numpy as np
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
+WINDOW = 1e-6          # rounding-window half width, in bins
+REL_TOL = 1e-12        # decode tolerance relative to max(range, max|x|)
+
 
 def load_cases():
     from oracle.bindings import Setup
@@ -115,3 +118,58 @@ def window_distance(values: np.ndarray, pred: np.ndarray, tau: float) -> np.ndar
     """|frac(t) - 0.5| with t = (v - p_ref)/bin: 0 at a bin boundary."""
     t = (values - pred) / (2.0 * tau)
     return np.abs(t - np.floor(t) - 0.5)
+
+
+def check_component(gp, rp, values, pred_ref, oracle, label):
+    """Byte-exact payload, or code-level diff confined to the rounding window."""
+    if gp == rp:
+        return 0
+    g = parse_payload(gp, oracle.rle_decompress)
+    r = parse_payload(rp, oracle.rle_decompress)
+    for k in ("codec", "pred", "backend", "tau", "n", "dims"):
+        assert g[k] == r[k], (label, k)
+    assert len(g["esc"]) == len(r["esc"]) and np.array_equal(g["esc"], r["esc"]), label
+    assert len(g["codes"]) == len(r["codes"]) == g["n"], label
+    bad = np.flatnonzero(g["codes"] != r["codes"])
+    assert bad.size > 0, f"{label}: payloads differ but codes agree (stream encoder bug)"
+    wd = window_distance(values[bad], pred_ref[bad], r["tau"])
+    assert np.all(wd < WINDOW), (label, bad[:10], wd[:10])
+    return bad.size
+
+
+def check_archive(gpu_ar, ref_ar, s, x, p, oracle, label):
+    """Archive bytes equal, or equal up to codes in the rounding window.
+    Returns the number of differing codes per component."""
+    if gpu_ar == ref_ar:
+        return {"grid": 0, "resid": 0}
+    ga, ra = parse_archive(gpu_ar), parse_archive(ref_ar)
+    for k in ("flags", "name", "digest", "tau", "rho"):
+        assert ga[k] == ra[k], (label, k)
+    # component 1: grid, exact cluster means vs reference Lorenzo prediction
+    x1 = oracle.interpolate_to_grid(s, x, fill=p.get("fill", 0))
+    rec1 = oracle.decode(ra["p1"])
+    if s.mode == 1:
+        pred1 = np.concatenate([[0.0], rec1[:-1]])
+    else:
+        pred1 = lorenzo_pred(rec1, list(s.shape))
+    d1 = check_component(ga["p1"], ra["p1"], x1, pred1, oracle, label + "/grid")
+    # component 2: residuals vs the previous reconstructed residual
+    x2 = oracle.residuals(s, x, fill=p.get("fill", 0), g_kind=p.get("g_kind", 0))
+    rec2 = oracle.decode(ra["p2"])
+    pred2 = np.concatenate([[0.0], rec2[:-1]])
+    d2 = check_component(ga["p2"], ra["p2"], x2, pred2, oracle, label + "/resid")
+    return {"grid": d1, "resid": d2}
+
+
+def check_decode(out, ref_out, x, tau_abs, label):
+    """GPU decode within REL_TOL * max(range, max|x|) of the reference's decode
+    and within the bound of x. Returns (drift / scale, max error / tau_abs)."""
+    scale = max(float(np.ptp(x)) if x.size else 0.0, float(np.abs(x).max()) if x.size else 0.0, 1e-300)
+    if tau_abs == 0.0:
+        assert np.array_equal(out.view(np.uint64), ref_out.view(np.uint64)), label
+        return 0.0, 0.0
+    drift = float(np.max(np.abs(out - ref_out))) if out.size else 0.0
+    err = float(np.max(np.abs(out - x))) if out.size else 0.0
+    assert drift <= REL_TOL * scale, (label, drift)
+    assert err <= tau_abs, (label, err, tau_abs)
+    return drift / scale, err / tau_abs

@@ -13,13 +13,11 @@ import pytest
 
 import paper_2501_06910_b200 as umcg
 from oracle.bindings import Setup
-from helpers import (GOLDEN, load_cases, load_seed7, lorenzo_pred, parse_archive, parse_payload,
-                     window_distance)
+from helpers import (GOLDEN, REL_TOL, WINDOW, check_archive, check_decode, load_cases, load_seed7,
+                     lorenzo_pred, parse_archive, parse_payload, window_distance)
 
 pytestmark = pytest.mark.gpu
 
-WINDOW = 1e-6          # rounding-window half width, in bins
-REL_TOL = 1e-12        # decode tolerance relative to max(range, max|x|)
 
 
 def plan_for(s, coords=True):
@@ -36,53 +34,6 @@ def budget_of(p):
 def dev(x):
     import torch
     return torch.from_numpy(np.ascontiguousarray(x, np.float64)).cuda()
-
-
-def check_component(gp, rp, values, pred_ref, oracle, label):
-    """Byte-exact payload, or code-level diff confined to the rounding window."""
-    if gp == rp:
-        return 0
-    g = parse_payload(gp, oracle.rle_decompress)
-    r = parse_payload(rp, oracle.rle_decompress)
-    for k in ("codec", "pred", "backend", "tau", "n", "dims"):
-        assert g[k] == r[k], (label, k)
-    assert len(g["esc"]) == len(r["esc"]) and np.array_equal(g["esc"], r["esc"]), label
-    assert len(g["codes"]) == len(r["codes"]) == g["n"], label
-    bad = np.flatnonzero(g["codes"] != r["codes"])
-    assert bad.size > 0, f"{label}: payloads differ but codes agree (stream encoder bug)"
-    wd = window_distance(values[bad], pred_ref[bad], r["tau"])
-    assert np.all(wd < WINDOW), (label, bad[:10], wd[:10])
-    return bad.size
-
-
-def check_archive(gpu_ar, ref_ar, s, x, p, oracle, label):
-    if gpu_ar == ref_ar:
-        return
-    ga, ra = parse_archive(gpu_ar), parse_archive(ref_ar)
-    for k in ("flags", "name", "digest", "tau", "rho"):
-        assert ga[k] == ra[k], (label, k)
-    # component 1: grid, exact cluster means vs reference Lorenzo prediction
-    x1 = oracle.interpolate_to_grid(s, x, fill=p.get("fill", 0))
-    rec1 = oracle.decode(ra["p1"])
-    if s.mode == 1:
-        pred1 = np.concatenate([[0.0], rec1[:-1]])
-    else:
-        pred1 = lorenzo_pred(rec1, list(s.shape))
-    check_component(ga["p1"], ra["p1"], x1, pred1, oracle, label + "/grid")
-    # component 2: residuals vs the previous reconstructed residual
-    x2 = oracle.residuals(s, x, fill=p.get("fill", 0), g_kind=p.get("g_kind", 0))
-    rec2 = oracle.decode(ra["p2"])
-    pred2 = np.concatenate([[0.0], rec2[:-1]])
-    check_component(ga["p2"], ra["p2"], x2, pred2, oracle, label + "/resid")
-
-
-def check_decode(out, ref_out, x, tau_abs, label):
-    scale = max(float(np.ptp(x)) if x.size else 0.0, float(np.abs(x).max()) if x.size else 0.0, 1e-300)
-    if tau_abs == 0.0:
-        assert np.array_equal(out.view(np.uint64), ref_out.view(np.uint64)), label
-        return
-    assert np.max(np.abs(out - ref_out)) <= REL_TOL * scale, (label, np.max(np.abs(out - ref_out)))
-    assert np.max(np.abs(out - x)) <= tau_abs, (label, np.max(np.abs(out - x)), tau_abs)
 
 
 # ---------------------------------------------------------------------------
@@ -812,3 +763,46 @@ def test_grid_init_matches_reference(cuda, ref, case):
     assert len(got) == len(want)
     for a, b in zip(got, want):
         assert np.array_equal(a, b), (case, len(a), len(b))
+
+
+@pytest.mark.parametrize("config,fill", [(2, 0), (5, 0), (5, 1)])
+def test_multilinear_offset_field_wide_residuals(cuda, ref, oracle, config, fill):
+    """Multilinear g on a dense grid with unvisited nodes and a field far from
+    zero (x + 1000). Config-2 annulus at 512^2 (the disc inside r = 0.3 holds
+    no vertex) and config-5 cylinder shell at 32^3 (whole rows along the
+    fastest axis inside the cylinder are unvisited, though grid_coarsen keeps
+    their planes). Unvisited nodes hold 0.0 (fill zero, interp.hpp:56) or stay
+    0.0 along whole empty rows (nearest_visited, interp.hpp:78), and
+    multilinear_at blends them in (interp.hpp:129), so |K2| reaches ~10^7:
+    the narrow int16 residual path must detect it and rerun with int32
+    indices (it used to truncate silently). Archive against the reference,
+    both decoders, the bound on every vertex, no serial fallback."""
+    if config == 2:
+        xy, x = umcg.gen_config(2, 1 << 20, 20250102, device="cuda")
+        g = 512
+    else:
+        xy, x = umcg.gen_config(5, 1 << 21, 20250105, device="cuda")
+        g = 32
+    D = xy.shape[1]
+    xy_h = xy.cpu().numpy()
+    lo, hi = xy_h.min(0), xy_h.max(0)
+    axes = [np.linspace(lo[d], hi[d], g) for d in range(D)]
+    plan = umcg.Plan.build(axes, xy, keep_coords=True)
+    mode, gaxes, assign, visited = plan.export()
+    assert mode == 0 and len(visited) < np.prod([len(a) for a in gaxes])
+    s = Setup(dim=D, axes=gaxes, mode=mode, assignments=assign, visited=visited, coords=xy_h)
+    xh = x.cpu().numpy() + 1000.0
+    p = dict(tau=1e-4, rho=0.5, g_kind=1, fill=fill)
+    b = budget_of(p)
+    fb0 = umcg.serial_fallbacks()
+    got = plan.compress(dev(xh), b, name="offset")
+    assert umcg.serial_fallbacks() == fb0
+    want = ref.compress(s, xh, name="offset", tau=1e-4, rho=0.5, g_kind=1, fill=fill)
+    # the residual component really needs more than int16 lattice indices
+    p2 = parse_archive(want)["p2"]
+    rec2 = oracle.decode(p2)
+    assert np.max(np.abs(rec2)) / (2 * parse_payload(p2, oracle.rle_decompress)["tau"]) > 16384
+    check_archive(got, want, s, xh, p, oracle, f"multilinear offset config{config} fill={fill}")
+    tau_abs = 1e-4 * np.ptp(xh)
+    check_decode(plan.decompress(got).cpu().numpy(), ref.decompress(s, got), xh, tau_abs, "own")
+    check_decode(plan.decompress(want).cpu().numpy(), ref.decompress(s, want), xh, tau_abs, "ref")
