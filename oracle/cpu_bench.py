@@ -111,7 +111,7 @@ def single_core(block: int, reps: int, tau: float, pin: int | None = None) -> di
     dig = time_digest(R, ctx)
     mc, md = statistics.median(tc), statistics.median(td)
     nbytes = x.size * 8
-    return dict(info, host_info(), kind="reference", cores=1, reps=reps, tau_rel=tau, archive_bytes=ab,
+    return dict(info, **host_info(), kind="reference", cores=1, reps=reps, tau_rel=tau, archive_bytes=ab,
                 compress_s=mc, decompress_s=md, compress_all_s=tc, decompress_all_s=td, digest_s=dig,
                 compress_gbs=nbytes / mc / 1e9, decompress_gbs=nbytes / md / 1e9,
                 roundtrip_gbs=nbytes / (mc + md) / 1e9,

@@ -184,6 +184,43 @@ void host_budget(double tau_abs, double rho, double coeff, double* tc) {
     tc[1] = t2 * (1.0 - 1e-9);
 }
 
+__global__ void k_set_u64(uint64_t* p, uint64_t v) {
+    if (threadIdx.x | blockIdx.x) return;
+    *p = v;
+}
+
+// Escapes (codec.hpp:305-320) in parallel: the segmented lattice for
+// lorenzo_1d, the exact hyperplane wavefront for 2-/3-D Lorenzo grids. The
+// one-thread replica remains for the non-lattice regime and other ranks
+// (counted, umcg_serial_fallbacks). Same outputs as serial_encode: u64
+// codes, (index, value) records, ctl->n_esc[comp].
+void escape_encode(umcg_plan* p, const double* v, uint64_t n, int pred, const NdShape& sh, double tau,
+                   uint64_t* codes, double* recon_scratch, uint64_t* esc_idx, double* esc_val, DevCtl* ctl, int comp,
+                   cudaStream_t st) {
+    const int epred = (pred == 2 && sh.D == 1) ? 1 : pred;
+    if (n && tau > 0.0 && std::isfinite(2.0 * tau)) {
+        auto* ectl = p->esc_ctl.as<DevCtl>(1);
+        auto* h = static_cast<DevCtl*>(p->hctl.reserve(sizeof(DevCtl)));
+        uint64_t ne = 0;
+        bool ok = false;
+        if (epred == 1) {
+            ok = seg_encode_1d(v, n, tau, codes, esc_idx, esc_val, p->esc_aux.reserve(esc_scratch_bytes(n)), ectl, h,
+                               &ne, st);
+        } else if (epred == 2 && (sh.D == 2 || sh.D == 3)) {
+            auto* F = static_cast<uint8_t*>(p->esc_aux.reserve(esc_scratch_bytes(n)));
+            auto* toff = reinterpret_cast<uint64_t*>(F + ((n + 255) & ~255ull));
+            ok = wave_encode_nd(v, n, sh, tau, codes, recon_scratch, F, st);
+            if (ok) ne = compact_flags(F, v, n, esc_idx, esc_val, toff, &ectl->aux[0], &h->aux[0], st);
+        }
+        if (ok) {
+            k_set_u64<<<1, 1, 0, st>>>(&ctl->n_esc[comp], ne);
+            UMCG_LAUNCHED();
+            return;
+        }
+    }
+    serial_encode(v, n, pred, sh, tau, codes, recon_scratch, esc_idx, esc_val, ctl, comp, st);
+}
+
 struct CompressMode {
     bool lossless[2];
     bool serial[2];
@@ -363,7 +400,7 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
         DevCtl hc = read_ctl(p, ctl, st);  // need the shaved tau on the host for the serial kernel
         esc_idx[0] = p->scratch_a.as<uint64_t>(n1 ? n1 : 1);
         esc_val[0] = p->scratch_b.as<double>(2 * (n1 ? n1 : 1));
-        serial_encode(x1, n1, pred1, sh1, hc.tau_c[0], static_cast<uint64_t*>(codes[0]), esc_val[0] + n1,
+        escape_encode(p, x1, n1, pred1, sh1, hc.tau_c[0], static_cast<uint64_t*>(codes[0]), esc_val[0] + n1,
                       esc_idx[0], esc_val[0], ctl, 0, st);
     } else if (m.lossless[0]) {
         codes_lossless_values(x1, n1, pred1, sh1, static_cast<uint64_t*>(codes[0]), sg);
@@ -381,7 +418,7 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
         esc_val[1] = x2 + n;  // reuse: escapes written after recon? keep separate below
         double* ev = p->dx1.as<double>(2 * (n ? n : 1));
         esc_val[1] = ev;
-        serial_encode(x2, n, 1, make_shape(1, &n), hc.tau_c[1], static_cast<uint64_t*>(codes[1]), ev + n,
+        escape_encode(p, x2, n, 1, make_shape(1, &n), hc.tau_c[1], static_cast<uint64_t*>(codes[1]), ev + n,
                       esc_idx[1], ev, ctl, 1, st);
     } else if (m.lossless[1]) {
         codes_lossless_residual(rs, n, static_cast<uint64_t*>(codes[1]), st);
@@ -666,6 +703,20 @@ void decode_component(umcg_plan* p, const CompHeader& h, const uint8_t* d_payloa
         int64_t* kb = p->kbuf.as<int64_t>(1);
         recon_lossy(codes, h.n, 0, sh, bin, kb, d_out, ctl, st);
         return;
+    }
+    // escapes: segmented lattice (1-D) / exact wavefront (2-, 3-D); the
+    // one-thread replica only outside the lattice regime
+    if (std::isfinite(bin) && h.tau > 0.0 && (pred == 1 || (pred == 2 && (h.D == 2 || h.D == 3)))) {
+        auto* ectl = p->esc_ctl.as<DevCtl>(1);
+        auto* hc = static_cast<DevCtl*>(p->hctl.reserve(sizeof(DevCtl)));
+        if (pred == 1) {
+            int64_t* K = p->kbuf.as<int64_t>(h.n);
+            auto* scr = static_cast<int64_t*>(p->esc_aux.reserve(8 * (cdiv(h.n, 2048) + 2 + h.n_esc)));
+            if (seg_decode_1d(codes, h.n, h.tau, eidx, evals, h.n_esc, K, scr, d_out, ectl, hc, st)) return;
+        } else {
+            auto* eslot = static_cast<int32_t*>(p->esc_aux.reserve(4 * h.n));
+            if (wave_decode_nd(codes, h.n, sh, h.tau, eidx, evals, h.n_esc, eslot, d_out, st)) return;
+        }
     }
     serial_decode(codes, h.n, h.pred, sh, h.tau, eidx, evals, h.n_esc, d_out, st);
 }
@@ -1101,7 +1152,7 @@ void encode_impl(const double* d_v, uint64_t n, int pred, int D, const uint64_t*
         if (serial) {
             eidx = p->scratch_a.as<uint64_t>(n ? n : 1);
             evals = p->scratch_b.as<double>(2 * (n ? n : 1));
-            serial_encode(d_v, n, pred, sh, tau, static_cast<uint64_t*>(codes), evals + n, eidx, evals, ctl, 0, st);
+            escape_encode(p, d_v, n, pred, sh, tau, static_cast<uint64_t*>(codes), evals + n, eidx, evals, ctl, 0, st);
         } else if (lossless) {
             if (epred == 2) {  // N-D lossless codes are parallel (exact prediction from exact values)
                 codes_lossless_values(d_v, n, 2, sh, static_cast<uint64_t*>(codes), st);

@@ -587,7 +587,109 @@ __global__ void __launch_bounds__(THREADS) k_lossless_plane(const uint64_t* __re
     const double p = lorenzo_fp(recon, lin, sh);
     recon[lin] = __longlong_as_double((long long)(codes[lin] ^ (uint64_t)__double_as_longlong(p)));
 }
+
+// Lossy N-D Lorenzo with escapes, exact: the reference loop (codec.hpp:300-326
+// encode, 422-437 decode) per hyperplane, same operations in the same order.
+__global__ void __launch_bounds__(THREADS) k_wave_enc(const double* __restrict__ v, NdShape sh, uint64_t s,
+                                                     uint64_t i_lo, uint64_t cnt, double tau, double bin,
+                                                     double* __restrict__ recon, uint64_t* __restrict__ codes,
+                                                     uint8_t* __restrict__ F) {
+    const uint64_t t = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (t >= cnt) return;
+    uint64_t lin;
+    if (sh.D == 2) {
+        const uint64_t i = i_lo + t, j = s - i;
+        lin = i * sh.dims[1] + j;
+    } else {
+        const uint64_t i = i_lo + t / sh.dims[1], j = t % sh.dims[1];
+        if (i + j > s) return;
+        const uint64_t k = s - i - j;
+        if (k >= sh.dims[2]) return;
+        lin = (i * sh.dims[1] + j) * sh.dims[2] + k;
+    }
+    const double p = lorenzo_fp(recon, lin, sh);
+    const double x = v[lin];
+    const double qd = round(__ddiv_rn(__dsub_rn(x, p), bin));
+    bool escape = !(fabs(qd) <= kQLimit);
+    double r = 0.0;
+    if (!escape) {
+        r = __dadd_rn(p, __dmul_rn(qd, bin));
+        escape = !(fabs(__dsub_rn(x, r)) <= tau);
+    }
+    F[lin] = escape ? 1 : 0;
+    codes[lin] = escape ? 0 : zz_enc((int64_t)qd);
+    recon[lin] = escape ? x : r;
+}
+
+__global__ void __launch_bounds__(THREADS) k_wave_dec(const uint64_t* __restrict__ codes, NdShape sh, uint64_t s,
+                                                     uint64_t i_lo, uint64_t cnt, double bin,
+                                                     const int32_t* __restrict__ eslot,
+                                                     const double* __restrict__ eval, double* __restrict__ recon) {
+    const uint64_t t = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (t >= cnt) return;
+    uint64_t lin;
+    if (sh.D == 2) {
+        const uint64_t i = i_lo + t, j = s - i;
+        lin = i * sh.dims[1] + j;
+    } else {
+        const uint64_t i = i_lo + t / sh.dims[1], j = t % sh.dims[1];
+        if (i + j > s) return;
+        const uint64_t k = s - i - j;
+        if (k >= sh.dims[2]) return;
+        lin = (i * sh.dims[1] + j) * sh.dims[2] + k;
+    }
+    const double p = lorenzo_fp(recon, lin, sh);
+    const int32_t e = eslot[lin];
+    recon[lin] = e >= 0 ? eval[e] : __dadd_rn(p, __dmul_rn((double)zz_dec(codes[lin]), bin));
+}
+
+__global__ void k_esc_slots(const uint64_t* __restrict__ eidx, uint64_t ne, int32_t* __restrict__ eslot) {
+    const uint64_t e = blockIdx.x * 256ull + threadIdx.x;
+    if (e < ne) eslot[eidx[e]] = (int32_t)e;
+}
+
+template <class F>
+void for_planes(const NdShape& sh, F&& f) {
+    uint64_t smax = 0;
+    for (int d = 0; d < sh.D; ++d) smax += sh.dims[d] - 1;
+    const uint64_t d0 = sh.dims[0], rest = smax - (d0 - 1);
+    for (uint64_t s = 0; s <= smax; ++s) {
+        const uint64_t i_lo = s > rest ? s - rest : 0, i_hi = std::min<uint64_t>(d0 - 1, s);
+        const uint64_t rows = i_hi - i_lo + 1;
+        const uint64_t cnt = sh.D == 2 ? rows : rows * sh.dims[1];
+        f(s, i_lo, cnt);
+    }
+}
 }  // namespace
+
+bool wave_encode_nd(const double* v, uint64_t n, const NdShape& sh, double tau, uint64_t* codes, double* recon,
+                    uint8_t* F, cudaStream_t st) {
+    if (sh.D != 2 && sh.D != 3) return false;
+    if (!n) return true;
+    const double bin = 2.0 * tau;
+    for_planes(sh, [&](uint64_t s, uint64_t i_lo, uint64_t cnt) {
+        k_wave_enc<<<(unsigned)cdiv(cnt, THREADS), THREADS, 0, st>>>(v, sh, s, i_lo, cnt, tau, bin, recon, codes, F);
+        UMCG_LAUNCHED();
+    });
+    return true;
+}
+
+bool wave_decode_nd(const uint64_t* codes, uint64_t n, const NdShape& sh, double tau, const uint64_t* esc_idx,
+                    const double* esc_val, uint64_t n_esc, int32_t* eslot, double* out, cudaStream_t st) {
+    if (sh.D != 2 && sh.D != 3) return false;
+    if (!n) return true;
+    const double bin = 2.0 * tau;
+    UMCG_CUDA(cudaMemsetAsync(eslot, 0xff, n * sizeof(int32_t), st));
+    if (n_esc) {
+        k_esc_slots<<<(unsigned)cdiv(n_esc, 256), 256, 0, st>>>(esc_idx, n_esc, eslot);
+        UMCG_LAUNCHED();
+    }
+    for_planes(sh, [&](uint64_t s, uint64_t i_lo, uint64_t cnt) {
+        k_wave_dec<<<(unsigned)cdiv(cnt, THREADS), THREADS, 0, st>>>(codes, sh, s, i_lo, cnt, bin, eslot, esc_val, out);
+        UMCG_LAUNCHED();
+    });
+    return true;
+}
 
 bool lossless_nd_wavefront(const uint64_t* codes, uint64_t n, const NdShape& sh, double* out, cudaStream_t st) {
     if (sh.D != 2 && sh.D != 3) return false;

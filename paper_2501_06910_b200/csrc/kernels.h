@@ -115,6 +115,25 @@ void materialize_residual(const ResidualSrc& src, uint64_t n, double* out, cudaS
 void serial_encode(const double* v, uint64_t n, int pred, const NdShape& sh, double tau,
                    uint64_t* codes, double* recon_scratch, uint64_t* esc_idx, double* esc_val,
                    DevCtl* ctl, int comp, cudaStream_t st);
+// Escapes in parallel (escape.cu). lorenzo_1d: segmented lattice, fixed point
+// over the escape set; false -> the caller takes the serial replica (non-lattice
+// regime / no fixed point). Codes u64 (0 at escapes), records in index order.
+size_t esc_scratch_bytes(uint64_t n);
+bool seg_encode_1d(const double* v, uint64_t n, double tau, uint64_t* codes, uint64_t* esc_idx, double* esc_val,
+                   void* scratch, DevCtl* ectl, DevCtl* hctl, uint64_t* n_esc, cudaStream_t st);
+bool seg_decode_1d(const uint64_t* codes, uint64_t n, double tau, const uint64_t* esc_idx, const double* esc_val,
+                   uint64_t n_esc, int64_t* K, int64_t* scratch, double* out, DevCtl* ectl, DevCtl* hctl,
+                   cudaStream_t st);
+// Stable compaction of flagged elements into (index, value) records; returns
+// the count (host synchronization). tile_off: cdiv(n, 2048) u64 scratch.
+uint64_t compact_flags(const uint8_t* F, const double* v, uint64_t n, uint64_t* idx, double* val, uint64_t* tile_off,
+                       uint64_t* d_total, uint64_t* h_total, cudaStream_t st);
+// N-D Lorenzo (D = 2, 3) with escapes: exact hyperplane wavefront of the
+// reference loop (codes.cu). F: per-element escape flags (encode).
+bool wave_encode_nd(const double* v, uint64_t n, const NdShape& sh, double tau, uint64_t* codes, double* recon,
+                    uint8_t* F, cudaStream_t st);
+bool wave_decode_nd(const uint64_t* codes, uint64_t n, const NdShape& sh, double tau, const uint64_t* esc_idx,
+                    const double* esc_val, uint64_t n_esc, int32_t* eslot, double* out, cudaStream_t st);
 // Exact serial replica of decode (codec.hpp:422-437).
 // N-D lossless decode by hyperplane wavefront (D = 2, 3); false otherwise.
 bool lossless_nd_wavefront(const uint64_t* codes, uint64_t n, const NdShape& sh, double* out, cudaStream_t st);

@@ -58,7 +58,7 @@ struct umcg_plan {
     // workspace (serialized by mu; a clone has its own)
     std::mutex mu;
     umcg::DevBuf ctl, x1, codes1, codes2, kbuf, enc1, enc2, hdr, scratch_a, scratch_b, scratch_c,
-        scratch_d, dx1, dcodes;
+        scratch_d, dx1, dcodes, esc_aux, esc_ctl;
     umcg::StreamDecScratch dec, dec2;
     umcg::SideStream side;  // grid component's chain runs beside the residual's
     umcg::PinnedBuf hctl, hstage;

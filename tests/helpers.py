@@ -120,8 +120,31 @@ def window_distance(values: np.ndarray, pred: np.ndarray, tau: float) -> np.ndar
     return np.abs(t - np.floor(t) - 0.5)
 
 
+def lattice_k(codes: np.ndarray, pred: int, dims) -> np.ndarray:
+    """The lattice index a code stream integrates to: the inclusive prefix of
+    the zigzag-decoded codes along the predictor's axes (lorenzo_1d: one
+    cumsum; lorenzo_nd: one cumsum per axis, codec.hpp:61-80)."""
+    q = zz_dec(codes)
+    if pred == 0:
+        return q
+    if pred == 1 or len(dims) == 1:
+        return np.cumsum(q)
+    k = q.reshape(dims)
+    for ax in range(len(dims)):
+        k = np.cumsum(k, axis=ax)
+    return k.ravel()
+
+
 def check_component(gp, rp, values, pred_ref, oracle, label):
-    """Byte-exact payload, or code-level diff confined to the rounding window."""
+    """Byte-exact payload, or the same lattice up to rounding-window events.
+
+    A code that rounds the other way inside the window (|frac(t) - 1/2| <
+    WINDOW, t = (v - p_ref) / bin) moves that element's lattice index K by one;
+    the following code(s) of the chain compensate, so the integrated lattice
+    agrees again right after. The check is therefore on K (the prefix of the
+    codes along the predictor): every element whose K differs must differ by
+    exactly one and be a window event. Escape records must be identical.
+    Returns the number of differing codes."""
     if gp == rp:
         return 0
     g = parse_payload(gp, oracle.rle_decompress)
@@ -132,8 +155,13 @@ def check_component(gp, rp, values, pred_ref, oracle, label):
     assert len(g["codes"]) == len(r["codes"]) == g["n"], label
     bad = np.flatnonzero(g["codes"] != r["codes"])
     assert bad.size > 0, f"{label}: payloads differ but codes agree (stream encoder bug)"
-    wd = window_distance(values[bad], pred_ref[bad], r["tau"])
-    assert np.all(wd < WINDOW), (label, bad[:10], wd[:10])
+    kg = lattice_k(g["codes"], g["pred"], g["dims"])
+    kr = lattice_k(r["codes"], r["pred"], r["dims"])
+    kd = np.flatnonzero(kg != kr)
+    assert kd.size > 0, (label, "codes differ but integrate to the same lattice", bad[:10])
+    assert np.all(np.abs(kg[kd] - kr[kd]) == 1), (label, kd[:10])
+    wd = window_distance(values[kd], pred_ref[kd], r["tau"])
+    assert np.all(wd < WINDOW), (label, kd[:10], wd[:10])
     return bad.size
 
 
