@@ -162,6 +162,9 @@ def kernel_bytes(n, n1, s2, k1_bytes, narrow=False):
         "k_rle_write": cb * n + s2,              # codes + stream out
         "k_dec_agg": s2,                         # stream in
         "k_dec_out": 12 * n + s2 + k1_bytes * n1,  # node 4 + out 8 + stream + K1 table
+        # multilinear g (layout E): coords 24 + xE 8 + KE, x1 bands staged per bucket (~3 x 1.5 n1 x 8)
+        "k_ml_resid": (32 + kb) * n + 36 * n1,
+        "k_ml_recompose": (24 + 8) * n + 36 * n1 + (4 + 8 + 8 + 8) * n,  # + gather-add: dstE, gE, io r/w
     }
 
 
@@ -188,11 +191,11 @@ def committed_traffic():
         return {}
 
 
-def workload_config(lattice: int, grid: int, tau: float, ws: int) -> dict:
+def workload_config(lattice: int, grid: int, tau: float, ws: int, g: str = "nearest") -> dict:
     """The `config` both arms print (identical dicts: the reference arm times a
     block sample of this same workload and says so in cpu_baseline.sample)."""
     n = lattice ** 3
-    return {"workload": f"config3 lattice{lattice}^3 ({n} vertices) grid{grid}^3 tau_rel {tau} rho 0.5 nearest g",
+    return {"workload": f"config3 lattice{lattice}^3 ({n} vertices) grid{grid}^3 tau_rel {tau} rho 0.5 {g} g",
             "l2": "inputs larger than L2 (1.07 GB field), no flush", "parallelism": f"replicas x{ws}"}
 
 
@@ -245,7 +248,7 @@ def run_reference(args):
     base = dict(impl="reference", metric=METRIC, unit="GB/s", higher_is_better=True, n_gpus=args.gpus,
                 steps=args.steps, warmup=args.warmup, scaling="weak", vs_baseline=None, dtype="f64",
                 data="synthetic (host generator, byte-identical to the GPU arm's inputs)",
-                config=workload_config(args.lattice, args.grid, args.tau, args.gpus))
+                config=workload_config(args.lattice, args.grid, args.tau, args.gpus, args.g))
     try:
         c = Concurrent(REF_BLOCK, threads, args.tau)
         for _ in range(args.warmup):
@@ -282,6 +285,8 @@ def main():
     ap.add_argument("--lattice", type=int, default=512)
     ap.add_argument("--grid", type=int, default=256)
     ap.add_argument("--tau", type=float, default=1e-4)
+    ap.add_argument("--g", default="nearest", choices=["nearest", "multilinear"],
+                    help="back-interpolation g (interp.hpp:140-170); the headline is nearest")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -302,9 +307,10 @@ def main():
             import torch.distributed as dist
             dist.barrier()
 
-    plan, x, plan_ms = setup_config3(args.lattice, args.grid, dev)
+    ml = args.g == "multilinear"
+    plan, x, plan_ms = setup_config3(args.lattice, args.grid, dev, keep_coords=ml)
     n, n1 = plan.n, int(plan.info.n_slots)
-    budget = umcg.Budget(tau=args.tau, split_rho=0.5, bound_kind=1)
+    budget = umcg.Budget(tau=args.tau, split_rho=0.5, bound_kind=1, g_kind=1 if ml else 0)
     cap = plan.compress_bound("field")
     ar = torch.empty(cap, dtype=torch.uint8, device=dev)
     out = torch.empty(n, dtype=torch.float64, device=dev)
@@ -421,7 +427,7 @@ def main():
         metric=METRIC, value=value, unit="GB/s", n_gpus=ws, steps=args.steps, warmup=args.warmup,
         ms_per_step=ms, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
         data="synthetic (GPU-generated, SplitMix64-seeded config 3)",
-        config=workload_config(args.lattice, args.grid, args.tau, ws),
+        config=workload_config(args.lattice, args.grid, args.tau, ws, args.g),
         run={"archive_bytes": alen, "mode": "seed" if plan.info.mode else "dense", "plan_build_ms": plan_ms},
         compress={"ms": tcm, "gbs_field": n * 8 / tcm / 1e6, "algorithmic_bytes": b_c,
                   "roofline_frac": b_c / (tcm * 1e-3) / 1e9 / peak},

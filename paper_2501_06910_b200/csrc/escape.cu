@@ -30,7 +30,10 @@
 // (codes.cu). Elements whose reconstruction leaves the lattice regime
 // (|S| >= 2^30 or |recon| >= 2^30 bin: FP spacing near the bin, the serial
 // chain's drift no longer bounded by the rounding window) still go to the
-// one-thread replica; they are counted (umcg_serial_fallbacks).
+// one-thread replica; they are counted (umcg_serial_fallbacks). The element
+// right after an escape is exempt: its prediction is v_e exactly, so it is
+// bit-exact with the reference at any magnitude (e.g. two equal outliers in a
+// row: the second codes q = 0 against the first).
 #include <cmath>
 
 #include <cub/block/block_reduce.cuh>
@@ -139,7 +142,9 @@ __global__ void __launch_bounds__(ET) k_seg_eval(const double* __restrict__ v, u
         if (esc) {
             codes[i] = 0;
         } else {
-            if (!(fabs(S) < kRegime) || !(fabs(rec) < __dmul_rn(kRegime, bin))) regime = 1;
+            // right after an escape the element is exact (p = v_e, no chain
+            // drift yet), whatever its magnitude
+            if (!(i > 0 && fprev) && (!(fabs(S) < kRegime) || !(fabs(rec) < __dmul_rn(kRegime, bin)))) regime = 1;
             codes[i] = zz_enc((int64_t)q);
         }
         Fout[i] = esc ? 1 : 0;
@@ -295,6 +300,10 @@ __global__ void __launch_bounds__(ET) k_recon_seg(const int64_t* __restrict__ K,
         base = eval[e];
         S = K[i] - Ke[e];
         r = __dadd_rn(base, __dmul_rn((double)S, bin));
+        if (eidx[e] + 1 == i) {  // first element after an escape: exact (p = v_e)
+            out[i] = r;
+            return;
+        }
     } else {
         S = K[i];
         r = __dmul_rn((double)S, bin);

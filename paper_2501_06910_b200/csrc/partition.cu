@@ -647,25 +647,95 @@ struct MlGrid {
     int D;
 };
 
+// Corner staging: a bucket is a contiguous slot range [j0, j1), its vertices
+// map to those slots, and a vertex's cell corners lie within one node of its
+// slot per axis. So every corner lin satisfies lin - j0 in a*s0 + [-w, j1 -
+// j0 + w) for a in {-1, 0, 1} (w = s1 + 1 in 3-D, 1 in 2-D): at most three
+// bands of x1, staged once per bucket in shared memory (where bands
+// overlap they are simply staged twice). The eight (four) corner reads per
+// vertex then hit shared memory instead of one L1 wavefront each.
+constexpr int ML_T = 256;
+constexpr uint32_t ML_STAGE = 6144;  // doubles of staged x1 per bucket (48 KB)
+
+struct MlBands {  // band a = 0, 1, 2 <-> offset (a - 1) * s0; empty bands have lo == hi
+    int64_t lo0, hi0, lo1, hi1, lo2, hi2;
+    uint32_t off1, off2, total;
+};
+
+struct StagedCorners {
+    const double* xs;
+    const double* __restrict__ x1;
+    MlBands bd;
+    __device__ __forceinline__ double operator()(uint64_t lin) const {
+        const int64_t l = (int64_t)lin;
+        if (l >= bd.lo1 && l < bd.hi1) return xs[bd.off1 + (uint32_t)(l - bd.lo1)];
+        if (l >= bd.lo0 && l < bd.hi0) return xs[(uint32_t)(l - bd.lo0)];
+        if (l >= bd.lo2 && l < bd.hi2) return xs[bd.off2 + (uint32_t)(l - bd.lo2)];
+        return x1[lin];  // not reachable for a bucket's own vertices; kept for safety
+    }
+};
+
+__device__ __forceinline__ void ml_band(int64_t lo, int64_t hi, int64_t n1, int64_t& blo, int64_t& bhi) {
+    blo = lo < 0 ? 0 : lo;
+    bhi = hi > n1 ? n1 : hi;
+    if (bhi < blo) bhi = blo;
+}
+
+template <int DD>
+__device__ __forceinline__ MlBands ml_bands(uint32_t j0, uint32_t j1, const MlGrid& g, uint64_t n1) {
+    int64_t s0 = 0, w = 1;
+    if (DD == 3) { s0 = (int64_t)(g.shape[1] * g.shape[2]); w = (int64_t)g.shape[2] + 1; }
+    else if (DD == 2) { s0 = (int64_t)g.shape[1]; }
+    MlBands b;
+    ml_band((int64_t)j0 - s0 - w, (int64_t)j1 - s0 + w, (int64_t)n1, b.lo0, b.hi0);
+    ml_band((int64_t)j0 - w, (int64_t)j1 + w, (int64_t)n1, b.lo1, b.hi1);
+    ml_band((int64_t)j0 + s0 - w, (int64_t)j1 + s0 + w, (int64_t)n1, b.lo2, b.hi2);
+    if (DD == 1) { b.hi0 = b.lo0; b.hi2 = b.lo2; }
+    b.off1 = (uint32_t)(b.hi0 - b.lo0);
+    b.off2 = b.off1 + (uint32_t)(b.hi1 - b.lo1);
+    b.total = b.off2 + (uint32_t)(b.hi2 - b.lo2);
+    return b;
+}
+
+__device__ __forceinline__ void ml_stage(double* xs, const double* __restrict__ x1, int64_t lo, int64_t hi,
+                                         uint32_t off) {
+    const uint32_t len = (uint32_t)(hi - lo);
+    for (uint32_t t = threadIdx.x; t < len; t += ML_T) xs[off + t] = __ldg(&x1[lo + t]);
+}
+
 // MODE 0: KE[p] = lattice(xE[p] - g(p)) (compute_residuals, interp.hpp:161-170)
 // MODE 1: gE[p] = g(p) (back_interpolate for the recomposition, pipeline.hpp:206-208)
-template <int MODE, class KT>
-__global__ void __launch_bounds__(256) k_ml_bucket(const double* __restrict__ xE, const double* __restrict__ cE,
-                                                 uint64_t n, const uint2* __restrict__ bct, uint32_t E, MlGrid g,
-                                                 const double* __restrict__ x1, DevCtl* ctl, KT* __restrict__ KE,
-                                                 double* __restrict__ gE) {
+template <int MODE, int DD, class KT>
+__global__ void __launch_bounds__(ML_T) k_ml_bucket(const double* __restrict__ xE, const double* __restrict__ cE,
+                                                  uint64_t n, const uint2* __restrict__ bct, uint32_t E, MlGrid g,
+                                                  const double* __restrict__ x1, uint64_t n1,
+                                                  const uint32_t* __restrict__ bnode, DevCtl* ctl,
+                                                  KT* __restrict__ KE, double* __restrict__ gE) {
+    __shared__ double xs[ML_STAGE];
     const uint64_t b = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint2* ch = bct + b * (uint64_t)(E + 1);
     double bin = 0, inv = 0, tau = 0;
     if (MODE == 0) { bin = ctl->bin[1]; inv = ctl->inv_bin[1]; tau = ctl->tau_c[1]; }
-    for (uint32_t e = warp; e < E; e += 8) {
+    const MlBands bd = ml_bands<DD>(__ldg(&bnode[b]), __ldg(&bnode[b + 1]), g, n1);
+    const bool staged = bd.total <= ML_STAGE;
+    if (staged) {
+        ml_stage(xs, x1, bd.lo0, bd.hi0, 0);
+        ml_stage(xs, x1, bd.lo1, bd.hi1, bd.off1);
+        ml_stage(xs, x1, bd.lo2, bd.hi2, bd.off2);
+    }
+    __syncthreads();
+    const StagedCorners sc{xs, x1, bd};
+    const GlobalCorners gc{x1};
+    for (uint32_t e = warp; e < E; e += ML_T / 32) {
         const uint2 c0 = __ldg(&ch[e]), c1 = __ldg(&ch[e + 1]);
         for (uint32_t l = c0.x + lane; l < c1.x; l += 32) {
             const uint64_t p = c0.y + (l - c0.x);
             double pc[3] = {0, 0, 0};
-            for (int d = 0; d < g.D; ++d) pc[d] = __ldcs(&cE[d * n + p]);
-            const double gv = multilinear_eval(g.axes, g.axis_off, g.shape, g.D, x1, pc, g.inv_cell, g.scale);
+#pragma unroll
+            for (int d = 0; d < DD; ++d) pc[d] = __ldcs(&cE[d * n + p]);
+            const double gv = staged ? multilinear_eval_c<DD>(g.axes, g.axis_off, g.shape, sc, pc, g.inv_cell, g.scale)
+                                     : multilinear_eval_c<DD>(g.axes, g.axis_off, g.shape, gc, pc, g.inv_cell, g.scale);
             if (MODE == 0) KE[p] = resid_k<KT>(__dsub_rn(__ldcs(&xE[p]), gv), bin, inv, tau, ctl);
             else gE[p] = gv;
         }
@@ -863,30 +933,36 @@ static MlGrid ml_grid(umcg_plan* p) {
     return g;
 }
 
+template <int MODE, class KT>
+static void launch_ml(umcg_plan* p, const double* xE, const double* cE, const double* x1, DevCtl* ctl, KT* KE,
+                      double* gE, cudaStream_t st) {
+    const MlGrid g = ml_grid(p);
+    const uint32_t E = (uint32_t)p->n_epochs;
+    const uint32_t* bnode = p->d_bk.as<uint32_t>(1) + p->n_buckets + 1;
+    auto go = [&](auto kern) {
+        kern<<<(unsigned)p->n_buckets, ML_T, 0, st>>>(xE, cE, p->n, p->d_bct.as<uint2>(1), E, g, x1, p->n_slots,
+                                                     bnode, ctl, KE, gE);
+    };
+    if (g.D == 3) go(k_ml_bucket<MODE, 3, KT>);
+    else if (g.D == 2) go(k_ml_bucket<MODE, 2, KT>);
+    else go(k_ml_bucket<MODE, 1, KT>);
+    UMCG_LAUNCHED();
+}
+
 void ml_residuals(umcg_plan* p, const double* xE, const double* x1, DevCtl* ctl, void* KE, bool narrow,
                   cudaStream_t st) {
     if (!p->n_buckets) return;
     ProfScope ps_("k_ml_resid", st);
     const double* cE = coords_e(p, st);
-    const uint32_t E = (uint32_t)p->n_epochs;
-    if (narrow)
-        k_ml_bucket<0, int16_t><<<(unsigned)p->n_buckets, 256, 0, st>>>(
-            xE, cE, p->n, p->d_bct.as<uint2>(1), E, ml_grid(p), x1, ctl, static_cast<int16_t*>(KE), nullptr);
-    else
-        k_ml_bucket<0, int32_t><<<(unsigned)p->n_buckets, 256, 0, st>>>(
-            xE, cE, p->n, p->d_bct.as<uint2>(1), E, ml_grid(p), x1, ctl, static_cast<int32_t*>(KE), nullptr);
-    UMCG_LAUNCHED();
+    if (narrow) launch_ml<0>(p, xE, cE, x1, ctl, static_cast<int16_t*>(KE), nullptr, st);
+    else launch_ml<0>(p, xE, cE, x1, ctl, static_cast<int32_t*>(KE), nullptr, st);
 }
 
 void ml_recompose(umcg_plan* p, const double* x1, double* gE, double* d_out, cudaStream_t st) {
     if (!p->n) return;
     ProfScope ps_("k_ml_recompose", st);
     const double* cE = coords_e(p, st);
-    if (p->n_buckets) {
-        k_ml_bucket<1, int32_t><<<(unsigned)p->n_buckets, 256, 0, st>>>(
-            nullptr, cE, p->n, p->d_bct.as<uint2>(1), (uint32_t)p->n_epochs, ml_grid(p), x1, nullptr, nullptr, gE);
-        UMCG_LAUNCHED();
-    }
+    if (p->n_buckets) launch_ml<1>(p, nullptr, cE, x1, nullptr, static_cast<int32_t*>(nullptr), gE, st);
     k_add_gathered<<<(unsigned)cdiv(p->n, 256), 256, 0, st>>>(gE, p->d_dstE.as<uint32_t>(1), p->n, d_out);
     UMCG_LAUNCHED();
 }
