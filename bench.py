@@ -150,14 +150,34 @@ def narrow_path(tau, rho=0.5):
 
 
 def kernel_bytes(n, n1, s2, k1_bytes, narrow=False):
-    """Compulsory bytes per launch of each hot kernel:
+    """Per-launch bytes of each hot kernel, two ways:
     s2 = residual stream bytes, k1_bytes = bytes per grid lattice index in
     the decompress gather table (2 when |K1| < 2^15), narrow = int16 KE and
-    u16 codes."""
+    u16 codes.
+
+    "s8d": the SURVEY 8(d) algorithmic terms the kernel accounts for -- perm
+    4n, node ids 4n, seg_off 4 n1, x gathered 8n, x streamed 8n, x1[m] 8n,
+    x1 write + read 16 n1, archive A (compress); node ids 4n, x1' 8 n1,
+    gather 8n, x' 8n, archive A (decompress). Intermediate round trips of
+    this implementation (layout-E xE, KE, codes) earn nothing. Used for
+    `roofline`.
+    "own": every byte the kernel must move in this implementation (its
+    inputs and outputs, intermediates included) -- how close the kernel is
+    to streaming its own traffic."""
     kb, cb = (2, 2) if narrow else (4, 4)
-    return {
+    s8d = {
+        "k_gather_fwd": 12 * n,                  # perm 4 + x gathered 8 (xE write is an intermediate)
+        "k_bucket": 12 * n + 12 * n1,            # node ids 4 + x streamed 8; seg_off 4 + x1 write 8 per slot
+        "k_resid_codes": 4 * n,                  # dstE (the inverse permutation); KE / codes are intermediates
+        "k_rle_write": s2,                       # archive bytes
+        "k_dec_agg": s2,                         # archive bytes
+        "k_dec_out": 20 * n + s2,                # node ids 4 + gather 8 + x' 8 + archive
+        "k_ml_resid": (24 + 8) * n + 16 * n1,    # coords + x streamed, x1 read
+        "k_ml_recompose": (24 + 8 + 8) * n + 8 * n1,
+    }
+    own = {
         "k_gather_fwd": 20 * n,                  # x 8 + srcE 4 -> xE 8
-        "k_bucket": (12 + kb) * n + 12 * n1,     # xE 8 + lperm 2 + lnode 2 + KE; seg 4 + x1 8 per slot
+        "k_bucket": (12 + kb) * n + 12 * n1,     # xE 8 + lslot 2 + lnode 2 + KE; seg 4 + x1 8 per slot
         "k_resid_codes": (4 + kb + cb) * n,      # dstE 4 + KE (gathered once) + codes
         "k_rle_write": cb * n + s2,              # codes + stream out
         "k_dec_agg": s2,                         # stream in
@@ -166,6 +186,7 @@ def kernel_bytes(n, n1, s2, k1_bytes, narrow=False):
         "k_ml_resid": (32 + kb) * n + 36 * n1,
         "k_ml_recompose": (24 + 8) * n + 36 * n1 + (4 + 8 + 8 + 8) * n,  # + gather-add: dstE, gE, io r/w
     }
+    return s8d, own
 
 
 def profiled_pass(plan, x, budget, ar, out, steps=3):
@@ -404,6 +425,19 @@ def main():
                "serial": {"value": ws * n * 8 / te_serial / 1e9, "ms_per_step": te_serial * 1e3,
                           "path": "umcg_compress_host then umcg_decompress_host, one field at a time"}}
 
+    # e2e through the C++ drop-in API (umc::b200::compress / decompress on
+    # std::vector fields; tests/cpp/bench_cpp.cpp, built against the reference
+    # headers), rank 0 at N=1
+    if e2e is not None and ws == 1 and args.g == "nearest":
+        exe = os.path.join(ROOT, "tests", "cpp", "_build", "bench_cpp")
+        try:
+            r = subprocess.run([exe, str(max(3, args.steps // 4)), "2", str(args.lattice), str(args.grid)],
+                               capture_output=True, text=True, timeout=600)
+            e2e["cpp_api"] = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else \
+                {"error": (r.stderr or r.stdout)[-200:]}
+        except Exception as ex:
+            e2e["cpp_api"] = {"error": str(ex)[:200]}
+
     peak, peak_kind = peaks()
     b_c, b_d = algorithmic_bytes(n, n1, alen)
     tcm, tdm = float(np.median(tc)), float(np.median(td))
@@ -417,10 +451,12 @@ def main():
         s2 = alen - (10 + nl + 32 + l1 + 8) - 37  # payload2 minus its 37-byte header
     except Exception:
         pass
-    kb = kernel_bytes(n, n1, s2, 2, narrow_path(args.tau))
+    kb, kown = kernel_bytes(n, n1, s2, 2, narrow_path(args.tau))
     kernels = {k: {"ms": v, "gbs": kb[k] / (v * 1e-3) / 1e9 if k in kb else None,
                    "frac": kb[k] / (v * 1e-3) / 1e9 / peak if k in kb else None,
-                   "algorithmic_bytes": kb.get(k)} for k, v in kms.items()}
+                   "algorithmic_bytes": kb.get(k),
+                   "own_bytes": kown.get(k),
+                   "own_frac": kown[k] / (v * 1e-3) / 1e9 / peak if k in kown else None} for k, v in kms.items()}
     dom = max((k for k in kernels if k in kb), key=lambda k: kernels[k]["ms"], default=None)
     traffic = committed_traffic().get(dom) if dom else None
     res = dict(
@@ -437,6 +473,8 @@ def main():
                   "achieved": kernels[dom]["gbs"] if dom else None, "peak": peak, "unit": "GB/s",
                   "frac": kernels[dom]["frac"] if dom else None, "traffic": traffic,
                   "algorithmic_bytes_per_launch": kb.get(dom) if dom else None,
+                  "bytes_basis": "SURVEY 8(d) algorithmic terms attributed to the kernel (bench.kernel_bytes)",
+                  "own_frac": kernels[dom]["own_frac"] if dom else None,
                   "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
         path_roofline={"achieved": (b_c + b_d) / ((tcm + tdm) * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                        "frac": (b_c + b_d) / ((tcm + tdm) * 1e-3) / 1e9 / peak,

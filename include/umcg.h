@@ -180,6 +180,13 @@ umcg_status umcg_decompress_host(umcg_plan* plan, const uint8_t* archive, uint64
 umcg_status umcg_decompress_host_notify(umcg_plan* plan, const uint8_t* archive, uint64_t len,
                                         double* out, void (*uploaded)(void* ctx), void* ctx);
 
+/* umcg_decompress_host for an archive held in pieces (e.g. the container
+ * header and the two component payloads of an umc::Archive, pipeline.hpp:
+ * 214-235): the pieces are uploaded back to back, so the caller never
+ * concatenates them on the host. */
+umcg_status umcg_decompress_host_parts(umcg_plan* plan, const uint8_t* const* parts, const uint64_t* lens,
+                                       int n_parts, double* out);
+
 /* Single component codec: umc::encode (codec.hpp:220-334) with codec 0 /
  * backend 0, and umc::decode (codec.hpp:364-441). predictor: 0 none,
  * 1 lorenzo_1d, 2 lorenzo_nd; ndims <= 8. tau == 0 selects the lossless

@@ -1542,6 +1542,27 @@ umcg_status umcg_decompress_host_notify(umcg_plan* p, const uint8_t* archive, ui
     });
 }
 
+umcg_status umcg_decompress_host_parts(umcg_plan* p, const uint8_t* const* parts, const uint64_t* lens, int n_parts,
+                                       double* out) {
+    return guarded([&] {
+        if (!p || (n_parts && (!parts || !lens)) || n_parts < 0) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
+        const cudaStream_t hst = host_stream();
+        thread_local DevBuf dar, dy;
+        uint64_t len = 0;
+        for (int k = 0; k < n_parts; ++k) len += lens[k];
+        uint8_t* a = dar.as<uint8_t>(len ? len : 1);
+        double* y = dy.as<double>(p->n ? p->n : 1);
+        uint64_t o = 0;
+        for (int k = 0; k < n_parts; ++k) {
+            if (lens[k]) copy_pieces(a + o, parts[k], lens[k], cudaMemcpyHostToDevice, hst);
+            o += lens[k];
+        }
+        decompress_impl(p, a, len, y, hst);
+        if (p->n) copy_pieces(out, y, p->n * 8, cudaMemcpyDeviceToHost, hst);
+        UMCG_CUDA(cudaStreamSynchronize(hst));
+    });
+}
+
 uint64_t umcg_encode_bound(uint64_t n, int ndims) { return payload_bound(n, ndims); }
 
 umcg_status umcg_encode(const double* d_values, uint64_t n, int predictor, int ndims, const uint64_t* dims,

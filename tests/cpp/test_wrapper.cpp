@@ -48,13 +48,53 @@ static Built build(std::uint64_t seed, int dim, std::uint64_t n, MeshStyle style
     return b;
 }
 
+// A differing archive is dumped (field, mapping, grid, both archives) for
+// tests/test_gpu_cpp.py, which classifies every differing code against the
+// rounding window with the Python helpers (helpers.check_archive).
+static const char* g_dump_dir = nullptr;
+static int g_dumps = 0;
+static void put(std::FILE* f, const void* p, std::size_t n) { std::fwrite(p, 1, n, f); }
+static void dump_case(const Built& b, const Field& field, const ErrorBudget& budget, const CompressOptions& opt,
+                      const std::vector<std::uint8_t>& ref, const std::vector<std::uint8_t>& gpu) {
+    if (!g_dump_dir) return;
+    const std::string path = std::string(g_dump_dir) + "/mismatch_" + std::to_string(g_dumps++) + ".bin";
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) return;
+    const std::uint32_t hdr[6] = {0x4d434d55u, (std::uint32_t)b.grid.dim, (std::uint32_t)b.map.mode,
+                                  (std::uint32_t)(opt.g.kind == BackInterpKind::multilinear),
+                                  (std::uint32_t)(opt.fill == FillPolicy::nearest_visited),
+                                  (std::uint32_t)(budget.bound_kind == BoundKind::relative_to_range)};
+    put(f, hdr, sizeof hdr);
+    const double tr[2] = {budget.tau, budget.split_rho};
+    put(f, tr, sizeof tr);
+    for (const auto& a : b.grid.axes) {
+        const std::uint64_t k = a.size();
+        put(f, &k, 8);
+        put(f, a.data(), 8 * k);
+    }
+    const std::uint64_t n = b.map.assignments.size(), nv = b.map.visited_nodes.size();
+    put(f, &n, 8);
+    put(f, b.map.assignments.data(), 8 * n);
+    put(f, &nv, 8);
+    put(f, b.map.visited_nodes.data(), 8 * nv);
+    put(f, field.values.data(), 8 * n);
+    put(f, b.mesh.vertices.data(), 8 * b.mesh.vertices.size());
+    for (const auto* v : {&ref, &gpu}) {
+        const std::uint64_t k = v->size();
+        put(f, &k, 8);
+        put(f, v->data(), k);
+    }
+    std::fclose(f);
+}
+
 static double max_err(const std::vector<double>& a, const std::vector<double>& b) {
     double m = 0;
     for (std::size_t i = 0; i < a.size(); ++i) m = std::max(m, std::fabs(a[i] - b[i]));
     return m;
 }
 
-int main() {
+int main(int argc, char** argv) {
+    if (argc > 1) g_dump_dir = argv[1];
     int exact = 0, total = 0;
     for (int c = 0; c < 4; ++c) {
         const int dim = c < 2 ? 2 : 3;
@@ -83,9 +123,13 @@ int main() {
                 const Archive ref = compress(field, b.map, b.grid, b.mesh, budget, opt);
                 const Archive gpu = b200::compress(field, b.map, b.grid, b.mesh, budget, opt);
                 ++total;
-                const bool same = serialize_archive(ref) == serialize_archive(gpu);
+                const auto rb = serialize_archive(ref), gb = serialize_archive(gpu);
+                const bool same = rb == gb;
                 exact += same;
-                if (!same) std::printf("MISMATCH case %d tau %g g %d (window flips expected only)\n", c, tau, g);
+                if (!same) {
+                    std::printf("MISMATCH case %d tau %g g %d (dumped for window classification)\n", c, tau, g);
+                    dump_case(b, field, budget, opt, rb, gb);
+                }
                 const Field back = b200::decompress(gpu, b.map, b.grid, b.mesh);
                 const double tau_abs = resolve_tau_abs(budget, field.values);
                 const Field refback = decompress(gpu, b.map, b.grid, b.mesh);  // reference decodes our archive
@@ -222,6 +266,37 @@ int main() {
         b200::clear_plan_cache();
         CHECK(serialize_archive(b200::compress(fields[0], c.map, c.grid, c.mesh, ErrorBudget{})) == want[0],
               "after clear_plan_cache");
+        // the plan cache is keyed by content: an in-place edit of the same
+        // MappingTable object (same address, same sizes) must not reuse the
+        // plan built for the old assignments (the reference recomputes
+        // mapping_digest per call, pipeline.hpp:135)
+        MappingTable& m = c.map;
+        std::size_t i0 = 0, i1 = 1;
+        while (i1 < m.assignments.size() && m.assignments[i1] == m.assignments[i0]) ++i1;
+        std::swap(m.assignments[i0], m.assignments[i1]);
+        const auto edited_ref = serialize_archive(compress(fields[0], m, c.grid, c.mesh, ErrorBudget{}));
+        const auto edited_gpu = serialize_archive(b200::compress(fields[0], m, c.grid, c.mesh, ErrorBudget{}));
+        CHECK(edited_ref != want[0], "the edit changes the archive");
+        CHECK(edited_gpu == edited_ref, "in-place mapping edit: new plan (content-keyed cache)");
+        CHECK(b200::decompress(compress(fields[0], m, c.grid, c.mesh, ErrorBudget{}), m, c.grid, c.mesh).values ==
+                  b200::decompress(b200::compress(fields[0], m, c.grid, c.mesh, ErrorBudget{}), m, c.grid, c.mesh)
+                      .values,
+              "edited mapping decode");
+        std::swap(m.assignments[i0], m.assignments[i1]);
+        CHECK(serialize_archive(b200::compress(fields[0], m, c.grid, c.mesh, ErrorBudget{})) == want[0],
+              "edit undone: the original plan again");
+        // more distinct mappings than the cache holds (LRU eviction, default 4)
+        for (int k = 0; k < 6; ++k) {
+            Built d = build(300 + k, 2, 1500, MeshStyle::jittered);
+            SynthSpec s3;
+            s3.rng_seed = 7;
+            const Field fd = gen_field(d.mesh, s3);
+            CHECK(serialize_archive(b200::compress(fd, d.map, d.grid, d.mesh, ErrorBudget{})) ==
+                      serialize_archive(compress(fd, d.map, d.grid, d.mesh, ErrorBudget{})),
+                  "eviction round");
+        }
+        CHECK(serialize_archive(b200::compress(fields[0], m, c.grid, c.mesh, ErrorBudget{})) == want[0],
+              "after eviction");
     }
     std::printf("cases %d exact %d failures %d\n", total, exact, failures);
     return failures ? 1 : 0;

@@ -70,12 +70,18 @@ def test_1d_outliers_segmented(cuda, ref, oracle, n_out):
 
 
 def test_1d_int32_overflow_escapes(cuda, ref, oracle):
-    """Quanta beyond int32 from a tiny bound on a random walk with jumps."""
+    """Quanta beyond int32 from a tiny bound on a random walk with jumps.
+    |v| / bin reaches 5e9 > 2^30: outside the lattice regime (the serial
+    chain's drift exceeds the rounding window), so the exact replica runs --
+    counted, and the archive is the reference's bit for bit."""
     rng = np.random.default_rng(5)
     n = 300000
     v = np.cumsum(rng.normal(0, 1.0, n))
     v[rng.choice(n, 500, replace=False)] += rng.normal(0, 1e4, 500)
-    _codec_case(ref, oracle, v, 1, [n], 1e-7)
+    fb0 = umcg.serial_fallbacks()
+    _codec_case(ref, oracle, v, 1, [n], 1e-7, expect_parallel=False)
+    assert umcg.serial_fallbacks() > fb0
+    assert umcg.encode(dev(v), predictor=1, dims=[n], tau=1e-7) == ref.encode(v, predictor=1, dims=[n], tau=1e-7)
 
 
 def test_1d_bound_miss_huge_runs(cuda, ref, oracle):
