@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
-                "-Xcompiler", "-O3", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+                "-Xcompiler", "-O3", "-Xcompiler", "-fopenmp", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
 SOURCES = ["encode.cu", "partition.cu", "stream.cu", "codes.cu", "decode.cu", "interp.cu", "plan.cu", "api.cu", "datagen.cu", "gridinit.cu", "escape.cu"]
 
@@ -49,13 +49,30 @@ def _compile(name: str, verbose: bool) -> str:
     return f"[{name}] compiled" + ("\n" + log if verbose else "")
 
 
+def _flags_changed() -> bool:
+    """Objects are rebuilt whenever the compile flags change (mtimes alone
+    would keep objects built with different flags)."""
+    stamp = os.path.join(BUILD, "flags.txt")
+    want = " ".join(FLAGS)
+    have = open(stamp).read() if os.path.exists(stamp) else ""
+    if have != want:
+        for f in os.listdir(BUILD):
+            if f.endswith(".o"):
+                os.remove(os.path.join(BUILD, f))
+        with open(stamp, "w") as fh:
+            fh.write(want)
+        return True
+    return False
+
+
 def build(verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    _flags_changed()
     with cf.ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
         outs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
     objs = [os.path.join(BUILD, s.replace(".cu", ".o")) for s in SOURCES]
     if not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"]
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart", "-lgomp"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

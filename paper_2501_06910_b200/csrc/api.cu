@@ -1395,11 +1395,88 @@ static cudaStream_t host_stream() {
     return hs.s;
 }
 
+// Pageable host memory (a std::vector the caller owns, e.g. umc::Field
+// values): the driver would stage it through its own pinned buffer with one
+// host thread (~10 GB/s). Instead the copy goes through two per-thread pinned
+// 32 MiB buffers, the host side of each piece copied by several threads while
+// the previous piece is on the link.
+static bool host_pinned(const void* h) {
+    cudaPointerAttributes at{};
+    const bool ok = cudaPointerGetAttributes(&at, h) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    cudaGetLastError();  // a pageable pointer is not an error here
+    return ok;
+}
+
+static void par_memcpy(void* d, const void* s, size_t n) {
+    constexpr size_t kSplit = 2u << 20;
+    if (n < 2 * kSplit) {
+        std::memcpy(d, s, n);
+        return;
+    }
+    const int parts = (int)std::min<size_t>(16, n / kSplit);
+#pragma omp parallel for num_threads(parts) schedule(static)
+    for (int k = 0; k < parts; ++k) {
+        const size_t a = n * (size_t)k / parts, b = n * (size_t)(k + 1) / parts;
+        std::memcpy(static_cast<char*>(d) + a, static_cast<const char*>(s) + a, b - a);
+    }
+}
+
+static void staged_copy(void* dst, const void* src, uint64_t bytes, cudaMemcpyKind kind, cudaStream_t st) {
+    constexpr uint64_t kPiece = 32ull << 20;
+    thread_local struct Stg {
+        void* buf[2] = {nullptr, nullptr};
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        ~Stg() {
+            for (int k = 0; k < 2; ++k) {
+                if (buf[k]) cudaFreeHost(buf[k]);
+                if (ev[k]) cudaEventDestroy(ev[k]);
+            }
+        }
+    } g;
+    if (!g.buf[0])
+        for (int k = 0; k < 2; ++k) {
+            UMCG_CUDA(cudaMallocHost(&g.buf[k], kPiece));
+            UMCG_CUDA(cudaEventCreateWithFlags(&g.ev[k], cudaEventDisableTiming));
+        }
+    const uint64_t np = cdiv(bytes, kPiece);
+    auto* d8 = static_cast<uint8_t*>(dst);
+    const auto* s8 = static_cast<const uint8_t*>(src);
+    if (kind == cudaMemcpyHostToDevice) {
+        for (uint64_t i = 0; i < np; ++i) {
+            const int b = (int)(i & 1);
+            const uint64_t o = i * kPiece, len = std::min(kPiece, bytes - o);
+            if (i >= 2) UMCG_CUDA(cudaEventSynchronize(g.ev[b]));  // the buffer's previous piece is on the device
+            par_memcpy(g.buf[b], s8 + o, len);
+            UMCG_CUDA(cudaMemcpyAsync(d8 + o, g.buf[b], len, kind, st));
+            UMCG_CUDA(cudaEventRecord(g.ev[b], st));
+        }
+        return;
+    }
+    auto issue = [&](uint64_t i) {
+        const uint64_t o = i * kPiece, len = std::min(kPiece, bytes - o);
+        UMCG_CUDA(cudaMemcpyAsync(g.buf[i & 1], s8 + o, len, kind, st));
+        UMCG_CUDA(cudaEventRecord(g.ev[i & 1], st));
+    };
+    if (np) issue(0);
+    for (uint64_t i = 0; i < np; ++i) {
+        if (i + 1 < np) issue(i + 1);  // its buffer was drained by the previous iteration
+        UMCG_CUDA(cudaEventSynchronize(g.ev[i & 1]));
+        const uint64_t o = i * kPiece, len = std::min(kPiece, bytes - o);
+        par_memcpy(d8 + o, g.buf[i & 1], len);
+    }
+}
+
 // Large host<->device copies go in 64 MiB pieces with at most two in flight
 // (the host waits on the older one before queueing the next). A copy engine
 // serves queued copies in order, so without the window a concurrent call's
-// small copy (an archive) would wait behind a whole 1 GB field.
+// small copy (an archive) would wait behind a whole 1 GB field. Pageable
+// host memory takes the staged path above.
 static void copy_pieces(void* dst, const void* src, uint64_t bytes, cudaMemcpyKind kind, cudaStream_t st) {
+    const void* host = kind == cudaMemcpyHostToDevice ? src : dst;
+    if (bytes >= (8u << 20) && !host_pinned(host) && !std::getenv("UMCG_NO_STAGING")) {
+        staged_copy(dst, src, bytes, kind, st);
+        return;
+    }
     constexpr uint64_t kPiece = 64ull << 20;
     thread_local struct Ev {
         cudaEvent_t e[2] = {nullptr, nullptr};

@@ -71,11 +71,17 @@ struct GlobalCorners {
 // divide, so the result is RN(num / den) in every case, as the reference's
 // `/` (interp.hpp:118).
 // D is a compile-time rank (1-3) so the per-axis state stays in registers.
+// hint (optional): per axis, the index of the vertex's nearest node (its
+// slot in a dense mapping). The vertex then lies in the cell below or above
+// it, so the cell is one comparison away; it is verified against the axis
+// (axis[l] <= p < axis[l + 1], open at the ends exactly like the clamped
+// upper_bound) and any mapping that does not satisfy it takes the search.
 template <int D, class Corners>
 __device__ __forceinline__ double multilinear_eval_c(const double* __restrict__ axes,
                                                     const uint64_t* __restrict__ axis_off, const uint64_t* shape,
                                                     const Corners& x1, const double* __restrict__ p,
-                                                    const double* __restrict__ inv_cell, const double* scale) {
+                                                    const double* __restrict__ inv_cell, const double* scale,
+                                                    const uint32_t* hint = nullptr) {
     double t[3] = {0, 0, 0}, om[3] = {1, 1, 1};
     uint64_t base = 0, step[3] = {0, 0, 0};
     uint64_t stride = 1;
@@ -86,7 +92,17 @@ __device__ __forceinline__ double multilinear_eval_c(const double* __restrict__ 
         double td = 0.0;
         if (n > 1) {
             const double* axis = axes + axis_off[d];
-            uint64_t h = axis_upper_bound(axis, n, p[d], scale[d]);
+            uint64_t h = 0;
+            bool found = false;
+            if (hint) {
+                const int64_t md = hint[d];
+                int64_t c = (p[d] >= axis[md]) ? md : md - 1;
+                c = c < 0 ? 0 : c;
+                c = c > (int64_t)n - 2 ? (int64_t)n - 2 : c;
+                found = (c == 0 || axis[c] <= p[d]) && (c == (int64_t)n - 2 || p[d] < axis[c + 1]);
+                h = (uint64_t)c + 1;
+            }
+            if (!found) h = axis_upper_bound(axis, n, p[d], scale[d]);
             h = h < 1 ? 1 : h;
             if (h > n - 1) h = n - 1;
             l = h - 1;

@@ -493,6 +493,9 @@ static_assert(kBucketNodes <= 2 * BTP, "k_bucket_tma keeps <= 2 slots per thread
 #define UMCG_BT_ISSUE_WARP (BTP / 32 - 1)
 #endif
 constexpr int BT_ISSUE_WARP = UMCG_BT_ISSUE_WARP;
+#ifndef UMCG_BT3_DEFAULT
+#define UMCG_BT3_DEFAULT 0
+#endif
 
 template <class KT>
 __global__ void __launch_bounds__(BTP, 2) k_bucket_tma(const double* __restrict__ xE, const uint32_t* __restrict__ bk,
@@ -624,6 +627,120 @@ __global__ void __launch_bounds__(BTP, 2) k_bucket_tma(const double* __restrict_
 #undef BT_ACC
 }
 
+// ---- software-pipelined variant (UMCG_BT3=1) ------------------------------------
+// One phase per iteration: the ordered sums of bucket i and the residuals of
+// bucket i-1 run back to back in every warp, with one barrier per bucket
+// instead of two, so the per-phase imbalance (slot sizes, chunk sizes) of the
+// two halves averages out. Three copy stages (bucket i+1 in flight while
+// bucket i is summed and bucket i-1 is read by the residuals) and two cluster
+// mean buffers; one CTA per SM.
+template <class KT>
+__global__ void __launch_bounds__(BTP, 1) k_bucket_tma3(const double* __restrict__ xE, const uint32_t* __restrict__ bk,
+                                                   uint64_t B, uint32_t E, const uint2* __restrict__ bct,
+                                                   const uint32_t* __restrict__ regular, uint32_t n_regular,
+                                                   const uint16_t* __restrict__ lnode,
+                                                   const uint16_t* __restrict__ lslot,
+                                                   const uint32_t* __restrict__ seg, DevCtl* ctl,
+                                                   double* __restrict__ x1, KT* __restrict__ KE, GridK gk) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[3];
+    double* x1b = reinterpret_cast<double*>(smem);  // [2][kBucketNodes]
+    const uint32_t stage_bytes = tma_stage_bytes(E);
+    auto stage = [&](uint32_t st) { return make_tma_stage(smem + 2 * kBucketNodes * 8 + st * stage_bytes, E); };
+    const uint32_t* bstart = bk;
+    const uint32_t* bnode = bk + B + 1;
+    const double bin = ctl->bin[1], inv = ctl->inv_bin[1], tau = ctl->tau_c[1];
+    const uint32_t G = gridDim.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (blockIdx.x >= n_regular) return;
+    const uint32_t K = (n_regular - blockIdx.x + G - 1) / G;  // buckets of this CTA
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 3; ++q) mbar_init(&bars[q], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    struct Info { uint32_t s0, m, j0, nj; };
+    auto load_info = [&](uint32_t i) {
+        const uint32_t bb = __ldg(&regular[blockIdx.x + i * G]);
+        const uint32_t a0 = __ldg(&bstart[bb]), a1 = __ldg(&bstart[bb + 1]);
+        const uint32_t c0 = __ldg(&bnode[bb]), c1 = __ldg(&bnode[bb + 1]);
+        return Info{a0, a1 - a0, c0, c1 - c0};
+    };
+    // the issuing warp stages bucket i's chunk table and issues its copies
+    auto issue = [&](uint32_t i, const Info& inf) {
+        const uint32_t bb = __ldg(&regular[blockIdx.x + i * G]);
+        const TmaStage S = stage(i % 3);
+        for (uint32_t e = lane; e <= E; e += 32) S.ch[e] = __ldg(&bct[bb * (uint64_t)(E + 1) + e]);
+        __syncwarp();
+        tma_issue(S, &bars[i % 3], xE, lslot, lnode, inf.s0, inf.m, E);
+    };
+    __syncthreads();
+    // buckets it - 1 (residuals), it (sums), it + 1 (in flight)
+    Info ip{0, 0, 0, 0}, ic = load_info(0), in1{0, 0, 0, 0};
+    if (K > 1) in1 = load_info(1);
+    if (warp == BT_ISSUE_WARP) {
+        issue(0, ic);
+        if (K > 1) issue(1, in1);
+    }
+    uint32_t sgr[2][2] = {{0, 0}, {0, 0}};
+    auto load_seg = [&](const Info& c) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t j = threadIdx.x + h * BTP;
+            if (j < c.nj) {
+                sgr[h][0] = __ldg(&seg[c.j0 + j]);
+                sgr[h][1] = __ldg(&seg[c.j0 + j + 1]);
+            }
+        }
+    };
+    load_seg(ic);
+    for (uint32_t it = 0; it <= K; ++it) {
+        if (it < K) {
+            const Info c = ic;
+            const TmaStage C = stage(it % 3);
+            double* x1s = x1b + (it & 1) * kBucketNodes;
+            const uint32_t lo8 = c.s0 & 7u;
+            uint32_t sg[2][2] = {{sgr[0][0], sgr[0][1]}, {sgr[1][0], sgr[1][1]}};
+            if (it + 1 < K) load_seg(in1);  // next bucket's offsets in flight
+            mbar_wait(&bars[it % 3], (it / 3) & 1u);
+            // interpolate_to_grid (interp.hpp:58-64): 0.0 + x_a + x_b + ... in ascending vertex order
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t j = threadIdx.x + h * BTP;
+                if (j >= c.nj) break;
+                const uint32_t k0 = sg[h][0] - c.s0, k1 = sg[h][1] - c.s0;
+                double sum = 0.0;
+                for (uint32_t q = k0; q < k1; ++q) sum = __dadd_rn(sum, C.xs[C.ls[q + lo8]]);
+                const double v = k1 > k0 ? __ddiv_rn(sum, (double)(k1 - k0)) : 0.0;
+                x1s[j] = v;
+                x1[c.j0 + j] = v;
+                grid_k(gk, c.j0 + j, v, ctl);
+            }
+        }
+        if (it >= 1 && KE) {
+            // compute_residuals (interp.hpp:161-170) + lattice index of bucket it - 1
+            const Info c = ip;
+            const TmaStage C = stage((it - 1) % 3);
+            const double* x1s = x1b + ((it - 1) & 1) * kBucketNodes;
+            const uint32_t lo8 = c.s0 & 7u;
+            for (uint32_t e = warp; e < E; e += BTP / 32) {
+                const uint2 c0 = C.ch[e], c1 = C.ch[e + 1];
+                const uint32_t sbase = c0.x + 2 * e + ((c0.y - c0.x - 2 * e) & 1u);
+                for (uint32_t l = c0.x + lane; l < c1.x; l += 32)
+                    KE[c0.y + (l - c0.x)] =
+                        resid_k<KT>(__dsub_rn(C.xs[sbase + (l - c0.x)], x1s[C.ln[l + lo8]]), bin, inv, tau, ctl);
+            }
+        }
+        Info in2{0, 0, 0, 0};
+        if (it + 2 < K) in2 = load_info(it + 2);
+        __syncthreads();
+        // stage (it + 2) % 3 == (it - 1) % 3: its last reader (the residuals above) is past the barrier
+        if (warp == BT_ISSUE_WARP && it + 2 < K) issue(it + 2, in2);
+        ip = ic;
+        ic = in1;
+        in1 = in2;
+    }
+}
+
 // ---- multilinear g in bucket order -------------------------------------------
 // A bucket is a contiguous range of grid slots, so the cells around its
 // vertices -- and the 2^D corner values multilinear_at reads -- stay within a
@@ -648,59 +765,158 @@ struct MlGrid {
 };
 
 // Corner staging: a bucket is a contiguous slot range [j0, j1), its vertices
-// map to those slots, and a vertex's cell corners lie within one node of its
-// slot per axis. So every corner lin satisfies lin - j0 in a*s0 + [-w, j1 -
-// j0 + w) for a in {-1, 0, 1} (w = s1 + 1 in 3-D, 1 in 2-D): at most three
-// bands of x1, staged once per bucket in shared memory (where bands
-// overlap they are simply staged twice). The eight (four) corner reads per
-// vertex then hit shared memory instead of one L1 wavefront each.
+// map to those slots (their nearest nodes), and a vertex's cell corners lie
+// within one node of its slot per axis. So every corner lies in one of three
+// bands of x1, a*s0 + [j0 - w, j1 + w) for a in {-1, 0, 1} (s0 the slowest
+// axis' stride, w = s1 + 1 in 3-D, 1 in 2-D), staged once per bucket in
+// shared memory at fixed offsets (a + 1) * Lb, Lb = j1 - j0 + 2w. A corner's
+// band is the offset of its slowest-axis index from the vertex's slot, so
+// its staged index is plain int32 arithmetic from the vertex's bucket-local
+// slot -- no range search. The cell itself comes from the slot too (one
+// comparison per axis, verified against the axis; a vertex whose slot is not
+// its nearest node takes the search and global corner loads).
 constexpr int ML_T = 256;
-constexpr uint32_t ML_STAGE = 6144;  // doubles of staged x1 per bucket (48 KB)
 
-struct MlBands {  // band a = 0, 1, 2 <-> offset (a - 1) * s0; empty bands have lo == hi
-    int64_t lo0, hi0, lo1, hi1, lo2, hi2;
-    uint32_t off1, off2, total;
+struct MlDims {
+    uint32_t s1, s12;      // strides of axes 1 and 0 (3-D), s12 = axis-0 stride
+    float inv_s1, inv_s12; // RN(1 / stride) for the exact division below
+    int32_t w, Lb;
+    int small;             // slots < 2^24: float-reciprocal division, staging
 };
 
-struct StagedCorners {
-    const double* xs;
-    const double* __restrict__ x1;
-    MlBands bd;
-    __device__ __forceinline__ double operator()(uint64_t lin) const {
-        const int64_t l = (int64_t)lin;
-        if (l >= bd.lo1 && l < bd.hi1) return xs[bd.off1 + (uint32_t)(l - bd.lo1)];
-        if (l >= bd.lo0 && l < bd.hi0) return xs[(uint32_t)(l - bd.lo0)];
-        if (l >= bd.lo2 && l < bd.hi2) return xs[bd.off2 + (uint32_t)(l - bd.lo2)];
-        return x1[lin];  // not reachable for a bucket's own vertices; kept for safety
+// x / d for x < 2^24 (exact float conversion; the rounded quotient is within
+// one of the true one and corrected)
+__device__ __forceinline__ uint32_t udiv_small(uint32_t x, uint32_t d, float inv) {
+    uint32_t q = (uint32_t)__fmul_rn((float)x, inv);
+    if (q * d > x) --q;
+    else if ((q + 1) * d <= x) ++q;
+    return q;
+}
+
+__device__ __forceinline__ void ml_stage_band(double* xs, const double* __restrict__ x1, int64_t lo, int64_t hi,
+                                              int64_t n1) {
+    // node v -> xs[v - lo]; nodes outside the grid are never a corner
+    const int64_t a = lo < 0 ? 0 : lo, b = hi > n1 ? n1 : hi;
+    for (int64_t v = a + threadIdx.x; v < b; v += ML_T) xs[v - lo] = __ldg(&x1[v]);
+}
+
+// multilinear_at (interp.hpp:97-132) for a vertex whose slot m = j0 + ln is
+// its nearest node: same operations and order as multilinear_eval_c; corners
+// from the staged bands when `staged`.
+template <int D>
+__device__ __forceinline__ double ml_eval_slot(const MlGrid& g, const double* __restrict__ axes,
+                                               const double* __restrict__ icell, const double* __restrict__ x1,
+                                               const double* xs, bool staged, const MlDims& md, uint32_t m,
+                                               uint32_t ln, const double* p) {
+    uint32_t hint[3] = {0, 0, 0};
+    if (D == 3) {
+        hint[0] = md.small ? udiv_small(m, md.s12, md.inv_s12) : m / md.s12;
+        const uint32_t r = m - hint[0] * md.s12;
+        hint[1] = md.small ? udiv_small(r, md.s1, md.inv_s1) : r / md.s1;
+        hint[2] = r - hint[1] * md.s1;
+    } else if (D == 2) {
+        hint[0] = md.small ? udiv_small(m, md.s12, md.inv_s12) : m / md.s12;
+        hint[1] = m - hint[0] * md.s12;
+    } else {
+        hint[0] = m;
     }
-};
-
-__device__ __forceinline__ void ml_band(int64_t lo, int64_t hi, int64_t n1, int64_t& blo, int64_t& bhi) {
-    blo = lo < 0 ? 0 : lo;
-    bhi = hi > n1 ? n1 : hi;
-    if (bhi < blo) bhi = blo;
-}
-
-template <int DD>
-__device__ __forceinline__ MlBands ml_bands(uint32_t j0, uint32_t j1, const MlGrid& g, uint64_t n1) {
-    int64_t s0 = 0, w = 1;
-    if (DD == 3) { s0 = (int64_t)(g.shape[1] * g.shape[2]); w = (int64_t)g.shape[2] + 1; }
-    else if (DD == 2) { s0 = (int64_t)g.shape[1]; }
-    MlBands b;
-    ml_band((int64_t)j0 - s0 - w, (int64_t)j1 - s0 + w, (int64_t)n1, b.lo0, b.hi0);
-    ml_band((int64_t)j0 - w, (int64_t)j1 + w, (int64_t)n1, b.lo1, b.hi1);
-    ml_band((int64_t)j0 + s0 - w, (int64_t)j1 + s0 + w, (int64_t)n1, b.lo2, b.hi2);
-    if (DD == 1) { b.hi0 = b.lo0; b.hi2 = b.lo2; }
-    b.off1 = (uint32_t)(b.hi0 - b.lo0);
-    b.off2 = b.off1 + (uint32_t)(b.hi1 - b.lo1);
-    b.total = b.off2 + (uint32_t)(b.hi2 - b.lo2);
-    return b;
-}
-
-__device__ __forceinline__ void ml_stage(double* xs, const double* __restrict__ x1, int64_t lo, int64_t hi,
-                                         uint32_t off) {
-    const uint32_t len = (uint32_t)(hi - lo);
-    for (uint32_t t = threadIdx.x; t < len; t += ML_T) xs[off + t] = __ldg(&x1[lo + t]);
+    double t[3] = {0, 0, 0}, om[3] = {1, 1, 1};
+    uint32_t l[3] = {0, 0, 0};
+    bool all = true;
+#pragma unroll
+    for (int d = D - 1; d >= 0; --d) {
+        const uint32_t n = (uint32_t)g.shape[d];
+        double td = 0.0;
+        if (n > 1) {
+            const double* axis = axes + g.axis_off[d];
+            int32_t c = (p[d] >= axis[hint[d]]) ? (int32_t)hint[d] : (int32_t)hint[d] - 1;
+            c = c < 0 ? 0 : c;
+            c = c > (int32_t)n - 2 ? (int32_t)n - 2 : c;
+            const bool found = (c == 0 || axis[c] <= p[d]) && (c == (int32_t)n - 2 || p[d] < axis[c + 1]);
+            if (!found) {
+                all = false;
+                break;
+            }
+            const double num = __dsub_rn(p[d], axis[c]), den = __dsub_rn(axis[c + 1], axis[c]);
+            const double y = icell[g.axis_off[d] + c];
+            const double q0 = __dmul_rn(num, y);
+            double w = __fma_rn(__fma_rn(-q0, den, num), y, q0);
+            if (!(fabs(num) > 0x1p-900) || !(fabs(num) < 0x1p900) || !quotient_certified(num, den, w))
+                w = __ddiv_rn(num, den);
+            td = (w < 0.0) ? 0.0 : ((1.0 < w) ? 1.0 : w);  // std::clamp
+            l[d] = (uint32_t)c;
+        } else {
+            l[d] = 0;
+        }
+        t[d] = td;
+        om[d] = __dsub_rn(1.0, td);
+    }
+    if (!all) return multilinear_eval_c<D>(axes, g.axis_off, g.shape, GlobalCorners{x1}, p, icell, g.scale);
+    // corner value source: staged index or global linear index
+    int32_t ib = 0;
+    uint64_t lb = 0;
+    int32_t so[3] = {0, 0, 0};  // staged offsets per corner bit
+    uint64_t go[3] = {0, 0, 0};  // global offsets per corner bit
+    if (D == 3) {
+        const uint64_t st1 = g.shape[2], st0 = g.shape[1] * g.shape[2];
+        lb = (uint64_t)l[0] * st0 + (uint64_t)l[1] * st1 + l[2];
+        const int32_t a0 = (int32_t)l[0] - (int32_t)hint[0];
+        ib = (a0 + 1) * md.Lb + md.w + (int32_t)ln + ((int32_t)l[1] - (int32_t)hint[1]) * (int32_t)md.s1 +
+             ((int32_t)l[2] - (int32_t)hint[2]);
+        so[0] = g.shape[0] > 1 ? md.Lb : 0;
+        so[1] = g.shape[1] > 1 ? (int32_t)md.s1 : 0;
+        so[2] = g.shape[2] > 1 ? 1 : 0;
+        go[0] = g.shape[0] > 1 ? st0 : 0;
+        go[1] = g.shape[1] > 1 ? st1 : 0;
+        go[2] = g.shape[2] > 1 ? 1 : 0;
+    } else if (D == 2) {
+        lb = (uint64_t)l[0] * g.shape[1] + l[1];
+        const int32_t a0 = (int32_t)l[0] - (int32_t)hint[0];
+        ib = (a0 + 1) * md.Lb + md.w + (int32_t)ln + ((int32_t)l[1] - (int32_t)hint[1]);
+        so[0] = g.shape[0] > 1 ? md.Lb : 0;
+        so[1] = g.shape[1] > 1 ? 1 : 0;
+        go[0] = g.shape[0] > 1 ? g.shape[1] : 0;
+        go[1] = g.shape[1] > 1 ? 1 : 0;
+    } else {
+        lb = l[0];
+        ib = md.w + (int32_t)ln + ((int32_t)l[0] - (int32_t)hint[0]);
+        so[0] = g.shape[0] > 1 ? 1 : 0;
+        go[0] = so[0];
+    }
+    auto val = [&](unsigned corner) {
+        int32_t si = ib;
+        uint64_t gi = lb;
+#pragma unroll
+        for (int d = 0; d < D; ++d)
+            if ((corner >> d) & 1u) { si += so[d]; gi += go[d]; }
+        return staged ? xs[si] : __ldg(&x1[gi]);
+    };
+    double acc = 0.0;
+    if (D == 1) {
+        if (om[0] != 0.0) acc = __dadd_rn(acc, __dmul_rn(om[0], val(0)));
+        if (t[0] != 0.0) acc = __dadd_rn(acc, __dmul_rn(t[0], val(1)));
+        return acc;
+    }
+    if (D == 2) {
+#pragma unroll
+        for (unsigned corner = 0; corner < 4; ++corner) {
+            const double w = __dmul_rn((corner & 1u) ? t[0] : om[0], (corner & 2u) ? t[1] : om[1]);
+            if (w != 0.0) acc = __dadd_rn(acc, __dmul_rn(w, val(corner)));
+        }
+        return acc;
+    }
+    double p01[4];
+#pragma unroll
+    for (unsigned c = 0; c < 4; ++c) p01[c] = __dmul_rn((c & 1u) ? t[0] : om[0], (c & 2u) ? t[1] : om[1]);
+    double v[8];
+#pragma unroll
+    for (unsigned corner = 0; corner < 8; ++corner) v[corner] = val(corner);
+#pragma unroll
+    for (unsigned corner = 0; corner < 8; ++corner) {
+        const double w = __dmul_rn(p01[corner & 3u], (corner & 4u) ? t[2] : om[2]);
+        if (w != 0.0) acc = __dadd_rn(acc, __dmul_rn(w, v[corner]));
+    }
+    return acc;
 }
 
 // MODE 0: KE[p] = lattice(xE[p] - g(p)) (compute_residuals, interp.hpp:161-170)
@@ -709,24 +925,41 @@ template <int MODE, int DD, class KT>
 __global__ void __launch_bounds__(ML_T) k_ml_bucket(const double* __restrict__ xE, const double* __restrict__ cE,
                                                   uint64_t n, const uint2* __restrict__ bct, uint32_t E, MlGrid g,
                                                   const double* __restrict__ x1, uint64_t n1,
-                                                  const uint32_t* __restrict__ bnode, DevCtl* ctl,
-                                                  KT* __restrict__ KE, double* __restrict__ gE) {
-    __shared__ double xs[ML_STAGE];
+                                                  const uint32_t* __restrict__ bk, uint64_t B,
+                                                  const uint16_t* __restrict__ lnode, uint32_t band_cap,
+                                                  uint32_t ax_total, MlDims md, DevCtl* ctl, KT* __restrict__ KE,
+                                                  double* __restrict__ gE) {
+    extern __shared__ __align__(16) double dsm[];
+    double* xs = dsm;                   // [band_cap]   x1 bands
+    double* axs = dsm + band_cap;       // [ax_total]   axes (when staged)
+    double* ics = axs + ax_total;       // [ax_total]   RN(1 / cell width)
     const uint64_t b = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint2* ch = bct + b * (uint64_t)(E + 1);
     double bin = 0, inv = 0, tau = 0;
     if (MODE == 0) { bin = ctl->bin[1]; inv = ctl->inv_bin[1]; tau = ctl->tau_c[1]; }
-    const MlBands bd = ml_bands<DD>(__ldg(&bnode[b]), __ldg(&bnode[b + 1]), g, n1);
-    const bool staged = bd.total <= ML_STAGE;
+    const uint32_t s0 = __ldg(&bk[b]), j0 = __ldg(&bk[B + 1 + b]), j1 = __ldg(&bk[B + 2 + b]);
+    MlDims mdb = md;
+    mdb.Lb = (int32_t)(j1 - j0) + 2 * md.w;
+    const int nbands = DD == 1 ? 1 : 3;
+    const bool staged = (uint32_t)(nbands * mdb.Lb) <= band_cap;
     if (staged) {
-        ml_stage(xs, x1, bd.lo0, bd.hi0, 0);
-        ml_stage(xs, x1, bd.lo1, bd.hi1, bd.off1);
-        ml_stage(xs, x1, bd.lo2, bd.hi2, bd.off2);
+        const int64_t st0 = DD == 1 ? 0 : (int64_t)md.s12;
+        for (int a = (DD == 1 ? 0 : -1); a <= (DD == 1 ? 0 : 1); ++a)
+            ml_stage_band(xs + (DD == 1 ? 0 : (a + 1) * mdb.Lb), x1, (int64_t)j0 + a * st0 - md.w,
+                          (int64_t)j1 + a * st0 + md.w, (int64_t)n1);
+    }
+    const double* axes = g.axes;
+    const double* icell = g.inv_cell;
+    if (ax_total) {  // axes + reciprocals of every axis (small grids): shared memory
+        for (uint32_t t = threadIdx.x; t < ax_total; t += ML_T) {
+            axs[t] = __ldg(&g.axes[t]);
+            ics[t] = __ldg(&g.inv_cell[t]);
+        }
+        axes = axs;
+        icell = ics;
     }
     __syncthreads();
-    const StagedCorners sc{xs, x1, bd};
-    const GlobalCorners gc{x1};
     for (uint32_t e = warp; e < E; e += ML_T / 32) {
         const uint2 c0 = __ldg(&ch[e]), c1 = __ldg(&ch[e + 1]);
         for (uint32_t l = c0.x + lane; l < c1.x; l += 32) {
@@ -734,8 +967,8 @@ __global__ void __launch_bounds__(ML_T) k_ml_bucket(const double* __restrict__ x
             double pc[3] = {0, 0, 0};
 #pragma unroll
             for (int d = 0; d < DD; ++d) pc[d] = __ldcs(&cE[d * n + p]);
-            const double gv = staged ? multilinear_eval_c<DD>(g.axes, g.axis_off, g.shape, sc, pc, g.inv_cell, g.scale)
-                                     : multilinear_eval_c<DD>(g.axes, g.axis_off, g.shape, gc, pc, g.inv_cell, g.scale);
+            const uint32_t ln = __ldg(&lnode[s0 + l]);
+            const double gv = ml_eval_slot<DD>(g, axes, icell, x1, xs, staged, mdb, j0 + ln, ln, pc);
             if (MODE == 0) KE[p] = resid_k<KT>(__dsub_rn(__ldcs(&xE[p]), gv), bin, inv, tau, ctl);
             else gE[p] = gv;
         }
@@ -844,7 +1077,34 @@ void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double*
         tma_configured = true;
     }
     const bool tma = pipe && tma_smem <= 112 * 1024 && !std::getenv("UMCG_NO_TMA");
-    if (tma) {
+    const size_t tma3_smem = 2 * kBucketNodes * 8 + 3 * (size_t)tma_stage_bytes(E);
+    static const bool want3 = [] {
+        const char* e = std::getenv("UMCG_BT3");
+        return e ? std::atoi(e) != 0 : (bool)UMCG_BT3_DEFAULT;
+    }();
+    if (tma && want3 && tma3_smem <= 220 * 1024) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        static bool cfg3 = false;
+        if (!cfg3) {
+            UMCG_CUDA(cudaFuncSetAttribute(k_bucket_tma3<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+            UMCG_CUDA(cudaFuncSetAttribute(k_bucket_tma3<int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+            cfg3 = true;
+        }
+        const unsigned g = (unsigned)std::min<uint64_t>(p->n_regular, (uint64_t)sms);
+        auto launch = [&](auto* ke) {
+            using KT = std::remove_pointer_t<decltype(ke)>;
+            k_bucket_tma3<KT><<<g, BTP, tma3_smem, st>>>(xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E,
+                                                        p->d_bct.as<uint2>(1), p->d_regular.as<uint32_t>(1),
+                                                        (uint32_t)p->n_regular, p->d_lnode.as<uint16_t>(1),
+                                                        p->d_lslot.as<uint16_t>(1), p->d_seg.as<uint32_t>(1), ctl,
+                                                        x1, ke, gk);
+        };
+        if (narrow) launch(static_cast<int16_t*>(KE));
+        else launch(static_cast<int32_t*>(KE));
+        UMCG_LAUNCHED();
+    } else if (tma) {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -938,10 +1198,26 @@ static void launch_ml(umcg_plan* p, const double* xE, const double* cE, const do
                       double* gE, cudaStream_t st) {
     const MlGrid g = ml_grid(p);
     const uint32_t E = (uint32_t)p->n_epochs;
-    const uint32_t* bnode = p->d_bk.as<uint32_t>(1) + p->n_buckets + 1;
+    // x1 bands: three ranges of (bucket slots + one row either side) per bucket
+    MlDims md{};
+    md.w = g.D == 3 ? (int32_t)g.shape[2] + 1 : 1;
+    md.s1 = g.D == 3 ? (uint32_t)g.shape[2] : 1;
+    md.s12 = g.D == 3 ? (uint32_t)(g.shape[1] * g.shape[2]) : g.D == 2 ? (uint32_t)g.shape[1] : 1;
+    md.inv_s1 = 1.0f / (float)md.s1;
+    md.inv_s12 = 1.0f / (float)md.s12;
+    md.small = p->n_slots < (1u << 24) ? 1 : 0;
+    const uint32_t band_cap = md.small ?
+        (uint32_t)std::min<uint64_t>((g.D == 1 ? 1 : 3) * (kBucketNodes + 2 * (uint64_t)md.w), 12288) : 0;
+    uint64_t ax_total = 0;
+    for (int d = 0; d < g.D; ++d) ax_total += g.shape[d];
+    if (ax_total > 2048) ax_total = 0;  // large axes stay in global memory (L1)
+    const size_t smem = 8 * ((size_t)band_cap + 2 * ax_total);
     auto go = [&](auto kern) {
-        kern<<<(unsigned)p->n_buckets, ML_T, 0, st>>>(xE, cE, p->n, p->d_bct.as<uint2>(1), E, g, x1, p->n_slots,
-                                                     bnode, ctl, KE, gE);
+        UMCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<(unsigned)p->n_buckets, ML_T, smem, st>>>(xE, cE, p->n, p->d_bct.as<uint2>(1), E, g, x1, p->n_slots,
+                                                        p->d_bk.as<uint32_t>(1), p->n_buckets,
+                                                        p->d_lnode.as<uint16_t>(1), band_cap, (uint32_t)ax_total, md,
+                                                        ctl, KE, gE);
     };
     if (g.D == 3) go(k_ml_bucket<MODE, 3, KT>);
     else if (g.D == 2) go(k_ml_bucket<MODE, 2, KT>);

@@ -13,8 +13,8 @@ import pytest
 
 import paper_2501_06910_b200 as umcg
 from oracle.bindings import Setup
-from helpers import (GOLDEN, REL_TOL, WINDOW, check_archive, check_decode, load_cases, load_seed7,
-                     lorenzo_pred, parse_archive, parse_payload, window_distance)
+from helpers import (GOLDEN, REL_TOL, WINDOW, check_archive, check_component, check_decode, load_cases,
+                     load_seed7, lorenzo_pred, parse_archive, parse_payload, window_distance)
 
 pytestmark = pytest.mark.gpu
 

@@ -8,10 +8,10 @@ R=$(cd "$(dirname "$0")/.." && pwd)
 B=$R/paper_2501_06910_b200/_build
 mkdir -p $R/variants/$name
 obj=$R/variants/$name/$(basename $src .cu).o
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 --expt-relaxed-constexpr "$@" -c $R/paper_2501_06910_b200/csrc/$src -o $obj
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 -Xcompiler -fopenmp --expt-relaxed-constexpr "$@" -c $R/paper_2501_06910_b200/csrc/$src -o $obj
 objs=""
 for o in $B/*.o; do
   if [ "$(basename $o)" == "$(basename $obj)" ]; then objs="$objs $obj"; else objs="$objs $o"; fi
 done
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $R/variants/$name/libumcg.so $objs -lcudart
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $R/variants/$name/libumcg.so $objs -lcudart -lgomp
 echo built variants/$name
