@@ -27,11 +27,13 @@
  *    Compress/decompress synchronize the stream before returning (they report
  *    lengths and data-dependent errors), so the call is complete on return.
  *  - A plan is immutable after creation apart from its private workspace;
- *    calls on one plan are serialized by an internal mutex. Use one plan per
- *    thread for concurrency (plans can share nothing but are cheap to copy
- *    via umcg_plan_create on the same mapping).
- *  - Unsupported inputs fail loudly: codec_id != 0 or backend_id != 0 give
- *    UMCG_UNKNOWN_CODEC. There is no CPU fallback.
+ *    calls on one plan are serialized by an internal mutex. For concurrency
+ *    use one handle per thread: umcg_plan_clone gives a handle with its own
+ *    workspace that shares the (read-only) mapping arrays of its origin.
+ *  - Plans may live on different devices; every call runs on its plan's
+ *    device (per-device kernel attributes, streams and buffers).
+ *  - Unsupported inputs fail loudly: external codecs (>= 128) and lossless
+ *    backends != 0 give UMCG_UNKNOWN_CODEC. There is no CPU fallback.
  */
 #ifndef UMCG_H
 #define UMCG_H

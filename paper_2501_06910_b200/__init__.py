@@ -354,8 +354,11 @@ class Plan:
         return n.value if out is not None else buf[: n.value].tobytes()
 
     def decompress_host(self, archive, out: np.ndarray | None = None, uploaded=None) -> np.ndarray:
-        """uploaded: optional callable, run once the archive is on the device
-        (umcg_decompress_host_notify)."""
+        """uploaded: optional callable (umcg_decompress_host_notify), run as
+        soon as the next host->device copy can be queued without delaying this
+        archive's upload. It does NOT mean the archive buffer may be reused:
+        a pinned mapped archive is read by the SMs during the call, so the
+        buffer stays in use until this call returns."""
         a = np.frombuffer(archive, np.uint8) if isinstance(archive, (bytes, bytearray)) else archive
         length = len(archive) if isinstance(archive, (bytes, bytearray)) else int(a.size)
         y = out if out is not None else np.empty(self.n, np.float64)

@@ -1091,9 +1091,13 @@ void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_
 
 // Thread-local workspace for the plan-less codec entry points.
 umcg_plan* codec_ws() {
-    thread_local std::unique_ptr<umcg_plan> ws;
-    if (!ws) ws.reset(new umcg_plan);
-    return ws.get();
+    thread_local std::unique_ptr<umcg_plan> ws[kMaxDevices];
+    const int d = current_device();
+    if (!ws[d]) {
+        ws[d].reset(new umcg_plan);
+        ws[d]->device = d;
+    }
+    return ws[d].get();
 }
 
 void encode_impl(const double* d_v, uint64_t n, int pred, int D, const uint64_t* dims, double tau, int codec,
@@ -1386,13 +1390,27 @@ umcg_status umcg_decompress(umcg_plan* p, const uint8_t* d_archive, uint64_t len
 // The host-buffer calls run on a per-thread non-blocking stream: calls from
 // different host threads (on different plans) overlap, e.g. one field's
 // host->device copy with another's device->host copy.
+// One stream per (thread, device); the caller has set the plan's device.
 static cudaStream_t host_stream() {
     thread_local struct S {
-        cudaStream_t s = nullptr;
-        ~S() { if (s) cudaStreamDestroy(s); }
+        cudaStream_t s[kMaxDevices] = {};
+        ~S() {
+            for (auto x : s)
+                if (x) cudaStreamDestroy(x);
+        }
     } hs;
-    if (!hs.s) UMCG_CUDA(cudaStreamCreateWithFlags(&hs.s, cudaStreamNonBlocking));
-    return hs.s;
+    cudaStream_t& s = hs.s[current_device()];
+    if (!s) UMCG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    return s;
+}
+
+// Device work buffers of the host-buffer calls, per (thread, device).
+struct HostBufs {
+    DevBuf in, out;
+};
+static HostBufs& host_bufs(int which) {
+    thread_local HostBufs b[2][kMaxDevices];
+    return b[which][current_device()];
 }
 
 // Pageable host memory (a std::vector the caller owns, e.g. umc::Field
@@ -1424,18 +1442,24 @@ static void par_memcpy(void* d, const void* s, size_t n) {
 static void staged_copy(void* dst, const void* src, uint64_t bytes, cudaMemcpyKind kind, cudaStream_t st) {
     constexpr uint64_t kPiece = 32ull << 20;
     thread_local struct Stg {
-        void* buf[2] = {nullptr, nullptr};
-        cudaEvent_t ev[2] = {nullptr, nullptr};
+        void* buf[kMaxDevices][2] = {};
+        cudaEvent_t ev[kMaxDevices][2] = {};
         ~Stg() {
-            for (int k = 0; k < 2; ++k) {
-                if (buf[k]) cudaFreeHost(buf[k]);
-                if (ev[k]) cudaEventDestroy(ev[k]);
-            }
+            for (int d = 0; d < kMaxDevices; ++d)
+                for (int k = 0; k < 2; ++k) {
+                    if (buf[d][k]) cudaFreeHost(buf[d][k]);
+                    if (ev[d][k]) cudaEventDestroy(ev[d][k]);
+                }
         }
-    } g;
+    } stg;
+    const int dev = current_device();
+    struct View {
+        void** buf;
+        cudaEvent_t* ev;
+    } g{stg.buf[dev], stg.ev[dev]};
     if (!g.buf[0])
         for (int k = 0; k < 2; ++k) {
-            UMCG_CUDA(cudaMallocHost(&g.buf[k], kPiece));
+            UMCG_CUDA(cudaHostAlloc(&g.buf[k], kPiece, cudaHostAllocPortable));
             UMCG_CUDA(cudaEventCreateWithFlags(&g.ev[k], cudaEventDisableTiming));
         }
     const uint64_t np = cdiv(bytes, kPiece);
@@ -1445,7 +1469,8 @@ static void staged_copy(void* dst, const void* src, uint64_t bytes, cudaMemcpyKi
         for (uint64_t i = 0; i < np; ++i) {
             const int b = (int)(i & 1);
             const uint64_t o = i * kPiece, len = std::min(kPiece, bytes - o);
-            if (i >= 2) UMCG_CUDA(cudaEventSynchronize(g.ev[b]));  // the buffer's previous piece is on the device
+            // the buffer's previous piece (this call's or an earlier call's) is on the device
+            UMCG_CUDA(cudaEventSynchronize(g.ev[b]));
             par_memcpy(g.buf[b], s8 + o, len);
             UMCG_CUDA(cudaMemcpyAsync(d8 + o, g.buf[b], len, kind, st));
             UMCG_CUDA(cudaEventRecord(g.ev[b], st));
@@ -1479,14 +1504,18 @@ static void copy_pieces(void* dst, const void* src, uint64_t bytes, cudaMemcpyKi
     }
     constexpr uint64_t kPiece = 64ull << 20;
     thread_local struct Ev {
-        cudaEvent_t e[2] = {nullptr, nullptr};
+        cudaEvent_t e[kMaxDevices][2] = {};
         ~Ev() {
-            for (auto x : e)
-                if (x) cudaEventDestroy(x);
+            for (auto& d : e)
+                for (auto x : d)
+                    if (x) cudaEventDestroy(x);
         }
-    } ev;
+    } evs;
+    struct {
+        cudaEvent_t* e;
+    } ev{evs.e[current_device()]};
     if (!ev.e[0])
-        for (auto& x : ev.e) UMCG_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+        for (int k = 0; k < 2; ++k) UMCG_CUDA(cudaEventCreateWithFlags(&ev.e[k], cudaEventDisableTiming));
     uint64_t i = 0;
     for (uint64_t o = 0; o < bytes; o += kPiece, ++i) {
         if (i >= 2) UMCG_CUDA(cudaEventSynchronize(ev.e[i & 1]));
@@ -1566,8 +1595,10 @@ umcg_status umcg_compress_host(umcg_plan* p, const umcg_params* prm, const doubl
                                uint8_t* archive, uint64_t cap, uint64_t* len) {
     return guarded([&] {
         if (!p || !len) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
+        UMCG_CUDA(cudaSetDevice(p->device));
         const cudaStream_t hst = host_stream();
-        thread_local DevBuf dx, dar;
+        DevBuf& dx = host_bufs(0).in;
+        DevBuf& dar = host_bufs(0).out;
         const uint64_t n = p->n;
         uint64_t bound = 0;
         const int D1 = p->mode == 1 ? 1 : p->dim;
@@ -1596,8 +1627,10 @@ umcg_status umcg_decompress_host_notify(umcg_plan* p, const uint8_t* archive, ui
                                         void (*uploaded)(void*), void* ctx) {
     return guarded([&] {
         if (!p) fail(UMCG_INVALID_ARGUMENT, "NULL plan");
+        UMCG_CUDA(cudaSetDevice(p->device));
         const cudaStream_t hst = host_stream();
-        thread_local DevBuf dar, dy;
+        DevBuf& dar = host_bufs(1).in;
+        DevBuf& dy = host_bufs(1).out;
         uint8_t* a = dar.as<uint8_t>(len ? len : 1);
         double* y = dy.as<double>(p->n ? p->n : 1);
         HostTrace tr;
@@ -1623,8 +1656,10 @@ umcg_status umcg_decompress_host_parts(umcg_plan* p, const uint8_t* const* parts
                                        double* out) {
     return guarded([&] {
         if (!p || (n_parts && (!parts || !lens)) || n_parts < 0) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
+        UMCG_CUDA(cudaSetDevice(p->device));
         const cudaStream_t hst = host_stream();
-        thread_local DevBuf dar, dy;
+        DevBuf& dar = host_bufs(1).in;
+        DevBuf& dy = host_bufs(1).out;
         uint64_t len = 0;
         for (int k = 0; k < n_parts; ++k) len += lens[k];
         uint8_t* a = dar.as<uint8_t>(len ? len : 1);

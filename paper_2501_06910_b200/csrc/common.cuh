@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
@@ -436,6 +437,36 @@ private:
     void* p_ = nullptr;
     size_t cap_ = 0;
     bool owned_ = true;
+};
+
+// Per-device bookkeeping: cudaFuncSetAttribute, streams, events and device
+// buffers belong to one device, so process- or thread-wide "done" flags and
+// thread-local resources are kept per device (plans may live on different
+// devices; calls set the plan's device first).
+constexpr int kMaxDevices = 16;
+inline int current_device() {
+    int d = 0;
+    UMCG_CUDA(cudaGetDevice(&d));
+    if (d < 0 || d >= kMaxDevices) fail(UMCG_ERROR, "device index beyond the per-device tables");
+    return d;
+}
+// Runs f() once per device, serialized (a concurrent first call waits until
+// the attributes are set before it launches).
+class DeviceOnce {
+public:
+    template <class F>
+    void operator()(F&& f) {
+        const int d = current_device();
+        if (done_.load(std::memory_order_acquire) >> d & 1ull) return;
+        std::lock_guard<std::mutex> lock(mu_);
+        if (done_.load(std::memory_order_relaxed) >> d & 1ull) return;
+        f();
+        done_.fetch_or(1ull << d, std::memory_order_release);
+    }
+
+private:
+    std::mutex mu_;
+    std::atomic<uint64_t> done_{0};
 };
 
 // A side stream + fork/join events, created on first use (non-blocking, so a

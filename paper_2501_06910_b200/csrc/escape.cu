@@ -30,10 +30,12 @@
 // (codes.cu). Elements whose reconstruction leaves the lattice regime
 // (|S| >= 2^30 or |recon| >= 2^30 bin: FP spacing near the bin, the serial
 // chain's drift no longer bounded by the rounding window) still go to the
-// one-thread replica; they are counted (umcg_serial_fallbacks). The element
-// right after an escape is exempt: its prediction is v_e exactly, so it is
-// bit-exact with the reference at any magnitude (e.g. two equal outliers in a
-// row: the second codes q = 0 against the first).
+// one-thread replica; they are counted (umcg_serial_fallbacks). Exempt are
+// the element right after an escape (its prediction is v_e exactly, so it is
+// bit-exact with the reference at any magnitude) and every element whose
+// reconstruction fl(v_e + fl(S * bin)) involves no rounding (then the
+// reference's chain reaches the same value exactly, e.g. runs of equal
+// outliers coding q = 0).
 #include <cmath>
 
 #include <cub/block/block_reduce.cuh>
@@ -84,6 +86,19 @@ __global__ void __launch_bounds__(1024) k_scan_last(int64_t* __restrict__ tl, ui
         tl[t] = excl;
         excl = c > excl ? c : excl;
     }
+}
+
+// base + S * bin with no rounding at all (exact product: fma residual 0;
+// exact sum: TwoSum error 0). A segment whose reconstructions are all exact
+// is the reference's chain bit for bit, at any magnitude (e.g. runs of equal
+// huge values coding q = 0 after an escape).
+__device__ __forceinline__ bool seg_exact(double base, double S, double bin) {
+    const double pr = __dmul_rn(S, bin);
+    if (__fma_rn(S, bin, -pr) != 0.0) return false;
+    const double r = __dadd_rn(base, pr);
+    const double bb = __dsub_rn(r, base);
+    const double e = __dadd_rn(__dsub_rn(base, __dsub_rn(r, bb)), __dsub_rn(pr, bb));
+    return e == 0.0;
 }
 
 __device__ __forceinline__ void flag_regime(DevCtl* ctl) {  // ctl->aux[6]: left the lattice regime
@@ -144,7 +159,9 @@ __global__ void __launch_bounds__(ET) k_seg_eval(const double* __restrict__ v, u
         } else {
             // right after an escape the element is exact (p = v_e, no chain
             // drift yet), whatever its magnitude
-            if (!(i > 0 && fprev) && (!(fabs(S) < kRegime) || !(fabs(rec) < __dmul_rn(kRegime, bin)))) regime = 1;
+            if (!(i > 0 && fprev) && (!(fabs(S) < kRegime) || !(fabs(rec) < __dmul_rn(kRegime, bin))) &&
+                !seg_exact(base, S, bin))
+                regime = 1;
             codes[i] = zz_enc((int64_t)q);
         }
         Fout[i] = esc ? 1 : 0;
@@ -309,7 +326,8 @@ __global__ void __launch_bounds__(ET) k_recon_seg(const int64_t* __restrict__ K,
         r = __dmul_rn((double)S, bin);
     }
     const double a = (double)(S < 0 ? -S : S);
-    if (!(a < kRegime) || !(fabs(r) < __dmul_rn(kRegime, bin))) flag_regime(ctl);
+    if ((!(a < kRegime) || !(fabs(r) < __dmul_rn(kRegime, bin))) && !seg_exact(base, (double)S, bin))
+        flag_regime(ctl);
     out[i] = r;
 }
 

@@ -240,157 +240,11 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
 
 constexpr int BTP = 512;  // threads per persistent bucket CTA
 
-// ---- software-pipelined persistent variant ---------------------------------
-// Persistent CTAs walk the regular (<= kBucketCap) buckets round-robin with
-// two shared-memory stages: while bucket k is summed and quantized, the
-// cp.async copies of bucket k+1 (xE chunks, lperm, lnode, segment offsets)
-// are in flight, and the chunk table of bucket k+2 is prefetched to
-// registers. Same arithmetic, same order as k_bucket.
-struct PipeStage {
-    double* xs;     // [kBucketCap]
-    uint16_t* lp;   // [kBucketCap + 2]
-    uint16_t* ln;   // [kBucketCap + 2]
-    uint32_t* sg;   // [kBucketNodes + 2]
-    uint2* ch;      // [E + 1]
-};
-
-__host__ __device__ __forceinline__ uint32_t pipe_stage_bytes(uint32_t E) {
-    const uint32_t b = kBucketCap * 8 + (kBucketNodes + 2) * 4 + (E + 1) * 8 + 2 * (kBucketCap + 4) * 2;
-    return (b + 15) & ~15u;
-}
-
-__device__ __forceinline__ PipeStage make_stage(unsigned char* p, uint32_t E) {
-    PipeStage S;
-    S.xs = reinterpret_cast<double*>(p);
-    p += kBucketCap * 8;
-    S.sg = reinterpret_cast<uint32_t*>(p);
-    p += (kBucketNodes + 2) * 4;
-    S.ch = reinterpret_cast<uint2*>(p);
-    p += (E + 1) * 8;
-    S.lp = reinterpret_cast<uint16_t*>(p);
-    p += (kBucketCap + 4) * 2;
-    S.ln = reinterpret_cast<uint16_t*>(p);
-    return S;
-}
-
-__device__ __forceinline__ void issue_bucket(const PipeStage& S, const double* __restrict__ xE,
-                                             const uint16_t* __restrict__ lperm, const uint16_t* __restrict__ lnode,
-                                             const uint32_t* __restrict__ seg, uint32_t s0, uint32_t m, uint32_t j0,
-                                             uint32_t nj, uint32_t E) {
-    (void)m;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (uint32_t e = warp; e < E; e += BTP / 32) {  // one warp per epoch chunk
-        const uint2 c0 = S.ch[e], c1 = S.ch[e + 1];
-        for (uint32_t l = c0.x + lane; l < c1.x; l += 32) cp_async(&S.xs[l], &xE[c0.y + (l - c0.x)], 8);
-    }
-    const uint32_t a0 = s0 & ~1u, words = (s0 + m - a0 + 1) >> 1;
-    for (uint32_t w = threadIdx.x; w < words; w += BTP) {
-        cp_async(reinterpret_cast<uint32_t*>(S.lp) + w, reinterpret_cast<const uint32_t*>(lperm + a0) + w, 4);
-        cp_async(reinterpret_cast<uint32_t*>(S.ln) + w, reinterpret_cast<const uint32_t*>(lnode + a0) + w, 4);
-    }
-    for (uint32_t j = threadIdx.x; j <= nj; j += BTP) cp_async(&S.sg[j], &seg[j0 + j], 4);
-}
-
-template <class KT>
-__global__ void __launch_bounds__(BTP) k_bucket_pipe(const double* __restrict__ xE, const uint32_t* __restrict__ bk,
-                                                   uint64_t B, uint32_t E, const uint2* __restrict__ bct,
-                                                   const uint32_t* __restrict__ regular, uint32_t n_regular,
-                                                   const uint16_t* __restrict__ lnode,
-                                                   const uint16_t* __restrict__ lperm,
-                                                   const uint32_t* __restrict__ seg, DevCtl* ctl,
-                                                   double* __restrict__ x1, KT* __restrict__ KE, GridK gk) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    // Stage pointers are recomputed from the extern shared array (never kept
-    // in a runtime-indexed array) so every access compiles to LDS/STS rather
-    // than generic loads.
-    double* x1s = reinterpret_cast<double*>(smem);
-    const uint32_t stage_bytes = pipe_stage_bytes(E);
-    auto stage = [&](int st) { return make_stage(smem + kBucketNodes * 8 + st * stage_bytes, E); };
-    const uint32_t* bstart = bk;
-    const uint32_t* bnode = bk + B + 1;
-    const double bin = ctl->bin[1], inv = ctl->inv_bin[1], tau = ctl->tau_c[1];
-    const uint32_t G = gridDim.x;
-    uint32_t k = blockIdx.x;
-    if (k >= n_regular) return;
-    // Per-bucket scalars travel through registers ahead of use so no
-    // dependent global-load chain (regular -> bstart/bnode) sits on the
-    // critical path: info of bucket k+G and the id of bucket k+2G are loaded
-    // one iteration early.
-    struct Info { uint32_t s0, m, j0, nj; };
-    auto load_info = [&](uint32_t bb) {
-        const uint32_t a0 = __ldg(&bstart[bb]), a1 = __ldg(&bstart[bb + 1]);
-        const uint32_t c0 = __ldg(&bnode[bb]), c1 = __ldg(&bnode[bb + 1]);
-        return Info{a0, a1 - a0, c0, c1 - c0};
-    };
-    // prologue: chunk table + copies of the first bucket; chunk table, info
-    // of the second; id of the third
-    uint32_t b = __ldg(&regular[k]);
-    Info cur = load_info(b);
-    if (threadIdx.x <= E) stage(0).ch[threadIdx.x] = __ldg(&bct[b * (uint64_t)(E + 1) + threadIdx.x]);
-    __syncthreads();
-    issue_bucket(stage(0), xE, lperm, lnode, seg, cur.s0, cur.m, cur.j0, cur.nj, E);
-    cp_commit();
-    uint2 chreg = make_uint2(0, 0);
-    Info nxt{0, 0, 0, 0};
-    uint32_t b2 = 0;
-    if (k + G < n_regular) {
-        const uint32_t bn = __ldg(&regular[k + G]);
-        nxt = load_info(bn);
-        if (threadIdx.x <= E) chreg = __ldg(&bct[bn * (uint64_t)(E + 1) + threadIdx.x]);
-        if (k + 2 * G < n_regular) b2 = __ldg(&regular[k + 2 * G]);
-    }
-    for (uint32_t it = 0; k < n_regular; ++it, k += G) {
-        const int st = it & 1;
-        const bool has_next = k + G < n_regular;
-        if (has_next && threadIdx.x <= E) stage(st ^ 1).ch[threadIdx.x] = chreg;
-        __syncthreads();
-        Info nn{0, 0, 0, 0};
-        uint32_t b3 = 0;
-        if (has_next) {
-            issue_bucket(stage(st ^ 1), xE, lperm, lnode, seg, nxt.s0, nxt.m, nxt.j0, nxt.nj, E);
-            if (k + 2 * G < n_regular) {
-                nn = load_info(b2);
-                if (threadIdx.x <= E) chreg = __ldg(&bct[b2 * (uint64_t)(E + 1) + threadIdx.x]);
-                if (k + 3 * G < n_regular) b3 = __ldg(&regular[k + 3 * G]);
-            }
-        }
-        cp_commit();
-        cp_wait<1>();
-        __syncthreads();
-        const PipeStage C = stage(st);
-        const uint32_t s0 = cur.s0, j0 = cur.j0, nj = cur.nj;
-        const uint32_t off = s0 & 1u;
-        // interpolate_to_grid (interp.hpp:58-64): 0.0 + x_a + x_b + ... in ascending vertex order
-        for (uint32_t j = threadIdx.x; j < nj; j += BTP) {
-            const uint32_t k0 = C.sg[j] - s0, k1 = C.sg[j + 1] - s0;
-            double s = 0.0;
-            for (uint32_t q = k0; q < k1; ++q) s = __dadd_rn(s, C.xs[C.lp[q + off]]);
-            const double v = k1 > k0 ? __ddiv_rn(s, (double)(k1 - k0)) : 0.0;
-            x1s[j] = v;
-            x1[j0 + j] = v;
-            grid_k(gk, j0 + j, v, ctl);
-        }
-        __syncthreads();
-        // compute_residuals (interp.hpp:161-170) + lattice index (codec.hpp:307-314)
-        if (KE) {
-            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-            for (uint32_t e = warp; e < E; e += BTP / 32) {
-                const uint2 c0 = C.ch[e], c1 = C.ch[e + 1];
-                for (uint32_t l = c0.x + lane; l < c1.x; l += 32)
-                    KE[c0.y + (l - c0.x)] = resid_k<KT>(__dsub_rn(C.xs[l], x1s[C.ln[l + off]]), bin, inv, tau, ctl);
-            }
-        }
-        cur = nxt;
-        nxt = nn;
-        b2 = b3;
-        __syncthreads();
-    }
-    cp_wait<0>();
-}
-
 // ---- TMA variant ------------------------------------------------------------
-// Same schedule as k_bucket_pipe, but every bucket arrives through bulk
-// asynchronous copies (cp.async.bulk, completion on an mbarrier): one copy
+// Persistent CTAs (two per SM) walk the regular (<= kBucketCap) buckets
+// round-robin with two shared-memory stages: while bucket k is summed and
+// quantized, bucket k+1 arrives through bulk asynchronous copies
+// (cp.async.bulk, completion on an mbarrier): one copy
 // per epoch chunk of xE, one each for the slot map, lnode and the segment
 // offsets, issued by one warp. Chunk e is staged at slot base
 // c0.x + 2e + phase_e (parity of the layout-E position, plan.cu k_lslot) so
@@ -493,9 +347,7 @@ static_assert(kBucketNodes <= 2 * BTP, "k_bucket_tma keeps <= 2 slots per thread
 #define UMCG_BT_ISSUE_WARP (BTP / 32 - 1)
 #endif
 constexpr int BT_ISSUE_WARP = UMCG_BT_ISSUE_WARP;
-#ifndef UMCG_BT3_DEFAULT
-#define UMCG_BT3_DEFAULT 0
-#endif
+
 
 template <class KT>
 __global__ void __launch_bounds__(BTP, 2) k_bucket_tma(const double* __restrict__ xE, const uint32_t* __restrict__ bk,
@@ -625,120 +477,6 @@ __global__ void __launch_bounds__(BTP, 2) k_bucket_tma(const double* __restrict_
 #endif
 #undef BT_T0
 #undef BT_ACC
-}
-
-// ---- software-pipelined variant (UMCG_BT3=1) ------------------------------------
-// One phase per iteration: the ordered sums of bucket i and the residuals of
-// bucket i-1 run back to back in every warp, with one barrier per bucket
-// instead of two, so the per-phase imbalance (slot sizes, chunk sizes) of the
-// two halves averages out. Three copy stages (bucket i+1 in flight while
-// bucket i is summed and bucket i-1 is read by the residuals) and two cluster
-// mean buffers; one CTA per SM.
-template <class KT>
-__global__ void __launch_bounds__(BTP, 1) k_bucket_tma3(const double* __restrict__ xE, const uint32_t* __restrict__ bk,
-                                                   uint64_t B, uint32_t E, const uint2* __restrict__ bct,
-                                                   const uint32_t* __restrict__ regular, uint32_t n_regular,
-                                                   const uint16_t* __restrict__ lnode,
-                                                   const uint16_t* __restrict__ lslot,
-                                                   const uint32_t* __restrict__ seg, DevCtl* ctl,
-                                                   double* __restrict__ x1, KT* __restrict__ KE, GridK gk) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bars[3];
-    double* x1b = reinterpret_cast<double*>(smem);  // [2][kBucketNodes]
-    const uint32_t stage_bytes = tma_stage_bytes(E);
-    auto stage = [&](uint32_t st) { return make_tma_stage(smem + 2 * kBucketNodes * 8 + st * stage_bytes, E); };
-    const uint32_t* bstart = bk;
-    const uint32_t* bnode = bk + B + 1;
-    const double bin = ctl->bin[1], inv = ctl->inv_bin[1], tau = ctl->tau_c[1];
-    const uint32_t G = gridDim.x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (blockIdx.x >= n_regular) return;
-    const uint32_t K = (n_regular - blockIdx.x + G - 1) / G;  // buckets of this CTA
-    if (threadIdx.x == 0) {
-        for (int q = 0; q < 3; ++q) mbar_init(&bars[q], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    struct Info { uint32_t s0, m, j0, nj; };
-    auto load_info = [&](uint32_t i) {
-        const uint32_t bb = __ldg(&regular[blockIdx.x + i * G]);
-        const uint32_t a0 = __ldg(&bstart[bb]), a1 = __ldg(&bstart[bb + 1]);
-        const uint32_t c0 = __ldg(&bnode[bb]), c1 = __ldg(&bnode[bb + 1]);
-        return Info{a0, a1 - a0, c0, c1 - c0};
-    };
-    // the issuing warp stages bucket i's chunk table and issues its copies
-    auto issue = [&](uint32_t i, const Info& inf) {
-        const uint32_t bb = __ldg(&regular[blockIdx.x + i * G]);
-        const TmaStage S = stage(i % 3);
-        for (uint32_t e = lane; e <= E; e += 32) S.ch[e] = __ldg(&bct[bb * (uint64_t)(E + 1) + e]);
-        __syncwarp();
-        tma_issue(S, &bars[i % 3], xE, lslot, lnode, inf.s0, inf.m, E);
-    };
-    __syncthreads();
-    // buckets it - 1 (residuals), it (sums), it + 1 (in flight)
-    Info ip{0, 0, 0, 0}, ic = load_info(0), in1{0, 0, 0, 0};
-    if (K > 1) in1 = load_info(1);
-    if (warp == BT_ISSUE_WARP) {
-        issue(0, ic);
-        if (K > 1) issue(1, in1);
-    }
-    uint32_t sgr[2][2] = {{0, 0}, {0, 0}};
-    auto load_seg = [&](const Info& c) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const uint32_t j = threadIdx.x + h * BTP;
-            if (j < c.nj) {
-                sgr[h][0] = __ldg(&seg[c.j0 + j]);
-                sgr[h][1] = __ldg(&seg[c.j0 + j + 1]);
-            }
-        }
-    };
-    load_seg(ic);
-    for (uint32_t it = 0; it <= K; ++it) {
-        if (it < K) {
-            const Info c = ic;
-            const TmaStage C = stage(it % 3);
-            double* x1s = x1b + (it & 1) * kBucketNodes;
-            const uint32_t lo8 = c.s0 & 7u;
-            uint32_t sg[2][2] = {{sgr[0][0], sgr[0][1]}, {sgr[1][0], sgr[1][1]}};
-            if (it + 1 < K) load_seg(in1);  // next bucket's offsets in flight
-            mbar_wait(&bars[it % 3], (it / 3) & 1u);
-            // interpolate_to_grid (interp.hpp:58-64): 0.0 + x_a + x_b + ... in ascending vertex order
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint32_t j = threadIdx.x + h * BTP;
-                if (j >= c.nj) break;
-                const uint32_t k0 = sg[h][0] - c.s0, k1 = sg[h][1] - c.s0;
-                double sum = 0.0;
-                for (uint32_t q = k0; q < k1; ++q) sum = __dadd_rn(sum, C.xs[C.ls[q + lo8]]);
-                const double v = k1 > k0 ? __ddiv_rn(sum, (double)(k1 - k0)) : 0.0;
-                x1s[j] = v;
-                x1[c.j0 + j] = v;
-                grid_k(gk, c.j0 + j, v, ctl);
-            }
-        }
-        if (it >= 1 && KE) {
-            // compute_residuals (interp.hpp:161-170) + lattice index of bucket it - 1
-            const Info c = ip;
-            const TmaStage C = stage((it - 1) % 3);
-            const double* x1s = x1b + ((it - 1) & 1) * kBucketNodes;
-            const uint32_t lo8 = c.s0 & 7u;
-            for (uint32_t e = warp; e < E; e += BTP / 32) {
-                const uint2 c0 = C.ch[e], c1 = C.ch[e + 1];
-                const uint32_t sbase = c0.x + 2 * e + ((c0.y - c0.x - 2 * e) & 1u);
-                for (uint32_t l = c0.x + lane; l < c1.x; l += 32)
-                    KE[c0.y + (l - c0.x)] =
-                        resid_k<KT>(__dsub_rn(C.xs[sbase + (l - c0.x)], x1s[C.ln[l + lo8]]), bin, inv, tau, ctl);
-            }
-        }
-        Info in2{0, 0, 0, 0};
-        if (it + 2 < K) in2 = load_info(it + 2);
-        __syncthreads();
-        // stage (it + 2) % 3 == (it - 1) % 3: its last reader (the residuals above) is past the barrier
-        if (warp == BT_ISSUE_WARP && it + 2 < K) issue(it + 2, in2);
-        ip = ic;
-        ic = in1;
-        in1 = in2;
-    }
 }
 
 // ---- multilinear g in bucket order -------------------------------------------
@@ -960,17 +698,33 @@ __global__ void __launch_bounds__(ML_T) k_ml_bucket(const double* __restrict__ x
         icell = ics;
     }
     __syncthreads();
+    // two vertices per thread and pass, every load issued before either is
+    // evaluated (the kernel is bound by the latency of these streams)
     for (uint32_t e = warp; e < E; e += ML_T / 32) {
         const uint2 c0 = __ldg(&ch[e]), c1 = __ldg(&ch[e + 1]);
-        for (uint32_t l = c0.x + lane; l < c1.x; l += 32) {
-            const uint64_t p = c0.y + (l - c0.x);
-            double pc[3] = {0, 0, 0};
+        for (uint32_t l = c0.x + lane; l < c1.x; l += 64) {
+            const bool two = l + 32 < c1.x;
+            const uint64_t p0 = c0.y + (l - c0.x), p1 = p0 + 32;
+            double pa[3] = {0, 0, 0}, pb[3] = {0, 0, 0};
 #pragma unroll
-            for (int d = 0; d < DD; ++d) pc[d] = __ldcs(&cE[d * n + p]);
-            const uint32_t ln = __ldg(&lnode[s0 + l]);
-            const double gv = ml_eval_slot<DD>(g, axes, icell, x1, xs, staged, mdb, j0 + ln, ln, pc);
-            if (MODE == 0) KE[p] = resid_k<KT>(__dsub_rn(__ldcs(&xE[p]), gv), bin, inv, tau, ctl);
-            else gE[p] = gv;
+            for (int d = 0; d < DD; ++d) {
+                pa[d] = __ldcs(&cE[d * n + p0]);
+                if (two) pb[d] = __ldcs(&cE[d * n + p1]);
+            }
+            const uint32_t la = __ldg(&lnode[s0 + l]), lb = two ? __ldg(&lnode[s0 + l + 32]) : 0u;
+            double xa = 0.0, xb = 0.0;
+            if (MODE == 0) {
+                xa = __ldcs(&xE[p0]);
+                if (two) xb = __ldcs(&xE[p1]);
+            }
+            const double ga = ml_eval_slot<DD>(g, axes, icell, x1, xs, staged, mdb, j0 + la, la, pa);
+            if (MODE == 0) KE[p0] = resid_k<KT>(__dsub_rn(xa, ga), bin, inv, tau, ctl);
+            else gE[p0] = ga;
+            if (two) {
+                const double gb = ml_eval_slot<DD>(g, axes, icell, x1, xs, staged, mdb, j0 + lb, lb, pb);
+                if (MODE == 0) KE[p1] = resid_k<KT>(__dsub_rn(xb, gb), bin, inv, tau, ctl);
+                else gE[p1] = gb;
+            }
         }
     }
 }
@@ -1060,51 +814,19 @@ void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double*
     if (!p->n_buckets) return;
     ProfScope ps_("k_bucket", st);
     const uint32_t E = (uint32_t)p->n_epochs;
-    static bool configured = false;
-    if (!configured) {
+    static DeviceOnce configured;
+    configured([] {
         UMCG_CUDA(cudaFuncSetAttribute(k_bucket<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         UMCG_CUDA(cudaFuncSetAttribute(k_bucket<int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        UMCG_CUDA(cudaFuncSetAttribute(k_bucket_pipe<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        UMCG_CUDA(cudaFuncSetAttribute(k_bucket_pipe<int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        configured = true;
-    }
-    const bool pipe = E + 1 <= BTP && p->n_regular > 0;
-    const size_t tma_smem = kBucketNodes * 8 + 2 * (size_t)tma_stage_bytes(E);
-    static bool tma_configured = false;
-    if (!tma_configured) {
         UMCG_CUDA(cudaFuncSetAttribute(k_bucket_tma<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         UMCG_CUDA(cudaFuncSetAttribute(k_bucket_tma<int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        tma_configured = true;
-    }
-    const bool tma = pipe && tma_smem <= 112 * 1024 && !std::getenv("UMCG_NO_TMA");
-    const size_t tma3_smem = 2 * kBucketNodes * 8 + 3 * (size_t)tma_stage_bytes(E);
-    static const bool want3 = [] {
-        const char* e = std::getenv("UMCG_BT3");
-        return e ? std::atoi(e) != 0 : (bool)UMCG_BT3_DEFAULT;
-    }();
-    if (tma && want3 && tma3_smem <= 220 * 1024) {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        static bool cfg3 = false;
-        if (!cfg3) {
-            UMCG_CUDA(cudaFuncSetAttribute(k_bucket_tma3<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-            UMCG_CUDA(cudaFuncSetAttribute(k_bucket_tma3<int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-            cfg3 = true;
-        }
-        const unsigned g = (unsigned)std::min<uint64_t>(p->n_regular, (uint64_t)sms);
-        auto launch = [&](auto* ke) {
-            using KT = std::remove_pointer_t<decltype(ke)>;
-            k_bucket_tma3<KT><<<g, BTP, tma3_smem, st>>>(xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E,
-                                                        p->d_bct.as<uint2>(1), p->d_regular.as<uint32_t>(1),
-                                                        (uint32_t)p->n_regular, p->d_lnode.as<uint16_t>(1),
-                                                        p->d_lslot.as<uint16_t>(1), p->d_seg.as<uint32_t>(1), ctl,
-                                                        x1, ke, gk);
-        };
-        if (narrow) launch(static_cast<int16_t*>(KE));
-        else launch(static_cast<int32_t*>(KE));
-        UMCG_LAUNCHED();
-    } else if (tma) {
+    });
+    const size_t tma_smem = kBucketNodes * 8 + 2 * (size_t)tma_stage_bytes(E);
+    // persistent two-stage bulk-copy kernel for the regular buckets; when its
+    // staging does not fit (> 170 epochs, ~700M vertices) every bucket takes
+    // the one-bucket-per-CTA kernel below
+    const bool pipe = E + 1 <= BTP && p->n_regular > 0 && tma_smem <= 112 * 1024;
+    if (pipe) {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1116,23 +838,6 @@ void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double*
                                                       (uint32_t)p->n_regular, p->d_lnode.as<uint16_t>(1),
                                                       p->d_lslot.as<uint16_t>(1), p->d_seg.as<uint32_t>(1), ctl, x1,
                                                       ke, gk);
-        };
-        if (narrow) launch(static_cast<int16_t*>(KE));
-        else launch(static_cast<int32_t*>(KE));
-        UMCG_LAUNCHED();
-    } else if (pipe) {
-        const size_t smem = kBucketNodes * 8 + 2 * (size_t)pipe_stage_bytes(E);
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const unsigned g = (unsigned)std::min<uint64_t>(p->n_regular, (uint64_t)sms * 2);
-        auto launch = [&](auto* ke) {
-            using KT = std::remove_pointer_t<decltype(ke)>;
-            k_bucket_pipe<KT><<<g, BTP, smem, st>>>(xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E,
-                                                   p->d_bct.as<uint2>(1), p->d_regular.as<uint32_t>(1),
-                                                   (uint32_t)p->n_regular, p->d_lnode.as<uint16_t>(1),
-                                                   p->d_lperm.as<uint16_t>(1), p->d_seg.as<uint32_t>(1), ctl, x1, ke,
-                                                   gk);
         };
         if (narrow) launch(static_cast<int16_t*>(KE));
         else launch(static_cast<int32_t*>(KE));

@@ -583,11 +583,8 @@ __global__ void __launch_bounds__(VD_THREADS) k_varint_decode(const uint8_t* __r
 // 8 KiB chunk, without the sub-exit table.
 static bool parallel_tokens(const uint8_t* d_stream, uint64_t len, Token* tok, StreamDecScratch& sc, DevCtl* ctl,
                             cudaStream_t st, uint64_t* ntok, uint64_t* ulen, bool fine) {
-    static bool attr = false;
-    if (!attr) {
-        UMCG_CUDA(cudaFuncSetAttribute(k_tok_jump, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PJ_SMEM));
-        attr = true;
-    }
+    static DeviceOnce attr;
+    attr([] { UMCG_CUDA(cudaFuncSetAttribute(k_tok_jump, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PJ_SMEM)); });
     const int shift = fine ? PJ_SB : 13;  // 2^13 == PJ_C
     static_assert(PJ_C == (1ull << 13), "chunk-level walks use shift 13");
     const uint64_t nc = cdiv(len, PJ_C), ng = cdiv(nc, PJ_G), ns = nc * (PJ_C >> shift);

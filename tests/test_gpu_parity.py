@@ -806,3 +806,23 @@ def test_multilinear_offset_field_wide_residuals(cuda, ref, oracle, config, fill
     tau_abs = 1e-4 * np.ptp(xh)
     check_decode(plan.decompress(got).cpu().numpy(), ref.decompress(s, got), xh, tau_abs, "own")
     check_decode(plan.decompress(want).cpu().numpy(), ref.decompress(s, want), xh, tau_abs, "ref")
+
+
+def test_host_calls_pageable_staging(cuda):
+    """Host-buffer calls on pageable numpy arrays large enough for the staged
+    copy path (pinned 32 MiB pieces, parallel host memcpy; api.cu
+    staged_copy), several pieces per transfer and back-to-back transfers in
+    one call: the same archive and field as the device path."""
+    import torch
+    xyz, x = umcg.gen_config(3, 256, 20250113, device="cuda")
+    plan = umcg.Plan.build([np.linspace(0.0, 1.0, 128) for _ in range(3)], xyz)
+    b = umcg.Budget(tau=1e-4)
+    want = plan.compress(x, b, "f")
+    xh = x.cpu().numpy().copy()  # pageable, 134 MB
+    for _ in range(2):
+        got = plan.compress_host(xh, b, "f")
+        assert got == want
+        out = np.empty(plan.n)
+        plan.decompress_host(got, out=out)
+        assert np.array_equal(out, plan.decompress(want).cpu().numpy())
+    del torch
