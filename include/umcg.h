@@ -161,6 +161,14 @@ umcg_status umcg_compress_batch(umcg_plan* plan, const umcg_params* params, cons
                                 uint8_t* d_archive, uint64_t capacity, uint64_t* archive_lens,
                                 void* stream);
 
+/* Batched decompress (BASELINE config 4): n_fields archives packed back to
+ * back in d_archives (archive_lens[f] each, as umcg_compress_batch writes
+ * them) -> d_out field-major [n_fields][n_vertices]; dtype 0 = fp64 (the
+ * reference's decode), 1 = fp32 (RN of the fp64 decode: the error bound holds
+ * for the fp64 values; the narrowing adds at most half an fp32 ulp). */
+umcg_status umcg_decompress_batch(umcg_plan* plan, const uint8_t* d_archives, const uint64_t* archive_lens,
+                                  int n_fields, int dtype, void* d_out, void* stream);
+
 /* umc::deserialize_archive + umc::decompress (pipeline.hpp:237-267, 180-210)
  * on device memory: d_archive [len] -> d_out [n_vertices] fp64. Baseline
  * archives (flag 8) decode the single component. */

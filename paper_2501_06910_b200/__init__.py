@@ -37,7 +37,8 @@ ERROR_NAMES = {
 EXPORTED = [
     "umcg_plan_create", "umcg_plan_build", "umcg_plan_destroy", "umcg_plan_clone", "umcg_plan_get_info",
     "umcg_plan_export", "umcg_compress_bound", "umcg_compress", "umcg_compress_batch",
-    "umcg_decompress", "umcg_compress_host", "umcg_decompress_host", "umcg_decompress_host_notify",
+    "umcg_decompress", "umcg_decompress_batch", "umcg_compress_host", "umcg_decompress_host",
+    "umcg_decompress_host_notify", "umcg_decompress_host_parts",
     "umcg_encode_bound",
     "umcg_encode", "umcg_decode", "umcg_grid_init", "umcg_baseline_bound", "umcg_compress_baseline", "umcg_rle_bound", "umcg_rle_compress", "umcg_rle_decompress",
     "umcg_gen_config",
@@ -128,6 +129,8 @@ def lib():
     L.umcg_compress_batch.argtypes = [vp, C.POINTER(Params), vp, C.c_int, C.c_int,
                                       C.POINTER(C.c_char_p), vp, C.c_uint64, u64p, vp]
     L.umcg_decompress.argtypes = [vp, vp, C.c_uint64, vp, vp]
+    L.umcg_decompress_batch.argtypes = [vp, vp, u64p, C.c_int, C.c_int, vp, vp]
+    L.umcg_decompress_host_parts.argtypes = [vp, C.POINTER(vp), u64p, C.c_int, vp]
     L.umcg_compress_host.argtypes = [vp, C.POINTER(Params), vp, C.c_char_p, vp, C.c_uint64, u64p]
     L.umcg_decompress_host.argtypes = [vp, vp, C.c_uint64, vp]
     L.umcg_decompress_host_notify.argtypes = [vp, vp, C.c_uint64, vp, vp, vp]
@@ -333,6 +336,28 @@ class Plan:
             out.append(host[o: o + int(ln)])
             o += int(ln)
         return out
+
+    def decompress_batch_into(self, d_archives, lens, d_out, stream=None):
+        """umcg_decompress_batch: archives packed back to back on the device
+        (lens[k] bytes each, as compress_batch_into writes them) -> d_out
+        [V, n] fp64 or fp32 (BASELINE config 4)."""
+        import torch
+        lens = np.ascontiguousarray(lens, np.uint64)
+        V = int(lens.size)
+        if d_out.dtype not in (torch.float32, torch.float64) or tuple(d_out.shape) != (V, self.n):
+            raise TypeError("d_out must be [V, n] fp32 or fp64")
+        dtype = 1 if d_out.dtype == torch.float32 else 0
+        _check(lib().umcg_decompress_batch(self.h, C.c_void_p(d_archives.data_ptr()), _ptr(lens, u64p), V, dtype,
+                                           C.c_void_p(d_out.data_ptr()), _stream_ptr(stream)))
+        return d_out
+
+    def decompress_batch(self, archives: list, dtype=None, device="cuda"):
+        """V archives (bytes) -> [V, n] tensor (fp64 unless dtype=torch.float32)."""
+        import torch
+        lens = np.array([len(a) for a in archives], np.uint64)
+        buf = torch.from_numpy(np.frombuffer(b"".join(archives), np.uint8).copy()).to(device)
+        out = torch.empty((len(archives), self.n), dtype=dtype or torch.float64, device=device)
+        return self.decompress_batch_into(buf, lens, out)
 
     def decompress(self, archive: bytes, device="cuda"):
         import torch

@@ -1383,6 +1383,38 @@ umcg_status umcg_compress_batch(umcg_plan* p, const umcg_params* prm, const void
     });
 }
 
+__global__ void k_f64_to_f32(const double* __restrict__ a, uint64_t n, float* __restrict__ b) {
+    const uint64_t i = blockIdx.x * 256ull + threadIdx.x;
+    if (i < n) b[i] = __double2float_rn(a[i]);
+}
+
+umcg_status umcg_decompress_batch(umcg_plan* p, const uint8_t* d_archives, const uint64_t* lens, int n_fields,
+                                  int dtype, void* d_out, void* stream) {
+    return guarded([&] {
+        if (!p || n_fields < 0 || (n_fields && (!d_archives || !lens || !d_out)) || (dtype != 0 && dtype != 1))
+            fail(UMCG_INVALID_ARGUMENT, "bad argument");
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        uint64_t off = 0;
+        for (int f = 0; f < n_fields; ++f) {
+            if (dtype == 0) {
+                decompress_impl(p, d_archives + off, lens[f], static_cast<double*>(d_out) + (size_t)f * p->n, st);
+            } else {
+                thread_local DevBuf tmp[kMaxDevices];
+                UMCG_CUDA(cudaSetDevice(p->device));
+                double* y = tmp[current_device()].as<double>(p->n ? p->n : 1);
+                decompress_impl(p, d_archives + off, lens[f], y, st);
+                if (p->n) {
+                    k_f64_to_f32<<<(unsigned)cdiv(p->n, 256), 256, 0, st>>>(
+                        y, p->n, static_cast<float*>(d_out) + (size_t)f * p->n);
+                    UMCG_LAUNCHED();
+                }
+            }
+            off += lens[f];
+        }
+        UMCG_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
 umcg_status umcg_decompress(umcg_plan* p, const uint8_t* d_archive, uint64_t len, double* d_out, void* stream) {
     return guarded([&] { decompress_impl(p, d_archive, len, d_out, static_cast<cudaStream_t>(stream)); });
 }

@@ -642,6 +642,14 @@ def test_config4_fp32_batch_matches_reference(cuda, ref, oracle, tau):
         check_archive(archives[k], want, s, xh, dict(tau=tau), oracle, f"config4 var{k} tau={tau}")
         out = plan.decompress(archives[k]).cpu().numpy()
         check_decode(out, ref.decompress(s, archives[k]), xh, tau * np.ptp(xh), f"config4 var{k}")
+    # batched decompress: fp64 equals the single-archive decodes, fp32 is their RN
+    import torch
+    both = plan.decompress_batch(archives)
+    f32 = plan.decompress_batch(archives, dtype=torch.float32)
+    for k in range(5):
+        one = plan.decompress(archives[k])
+        assert torch.equal(both[k], one)
+        assert torch.equal(f32[k], one.float())
 
 
 @pytest.mark.parametrize("g", [128, 256])

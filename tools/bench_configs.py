@@ -70,11 +70,22 @@ xy, vals = umcg.gen_config(4, 5793, 0x250106910 + 4, device="cuda")  # 5793^2 ~ 
 plan = bbox_plan(xy, 2048)
 cap = 5 * plan.compress_bound("f0")
 buf = torch.empty(cap, dtype=torch.uint8, device="cuda")
+out32 = torch.empty_like(vals)
 for tau in (1e-3, 1e-5):
     b = umcg.Budget(tau=tau)
-    t = timed(lambda: plan.compress_batch_into(vals, b, buf))
-    print(json.dumps(dict(config="config4 batch (5 fp32 vars, one umcg_compress_batch call)", tau=tau, n=plan.n,
-                          compress_ms=t, compress_gbs=vals.numel() * 4 / t / 1e6)))
+    lens = [None]
+
+    def cb():
+        lens[0] = plan.compress_batch_into(vals, b, buf)
+
+    t = timed(cb)
+    td = timed(lambda: plan.decompress_batch_into(buf, lens[0], out32))
+    err = max(((out32[k].double() - vals[k].double()).abs().max() / (tau * (vals[k].max() - vals[k].min()))).item()
+              for k in range(5))
+    print(json.dumps(dict(config="config4 batch (5 fp32 vars, umcg_compress_batch / umcg_decompress_batch fp32)",
+                          tau=tau, n=plan.n, compress_ms=t, compress_gbs=vals.numel() * 4 / t / 1e6,
+                          decompress_ms=td, decompress_gbs=vals.numel() * 4 / td / 1e6,
+                          archive=int(np.sum(lens[0])), max_err_over_tau_fp32_out=err)))
 del plan, xy, vals
 torch.cuda.empty_cache()
 # config 5: 200M vertices, grids 128^3 / 256^3 (seed) / 384^3 (seed)
