@@ -25,8 +25,8 @@ int main(int argc, char** argv) {
     // 1 GB Field / 200 MB payload to the kernel (glibc would mmap/munmap them,
     // and each call would page-fault 1.3 GB back in -- the same cost the
     // reference API's value-semantics Field carries; not the compressor's).
-    mallopt(M_MMAP_THRESHOLD, 1 << 30);
-    mallopt(M_TRIM_THRESHOLD, -1);
+    mallopt(M_MMAP_MAX, 0);       // large blocks from the heap (glibc caps M_MMAP_THRESHOLD at 32 MiB)
+    mallopt(M_TRIM_THRESHOLD, -1);  // and never returned
     const int steps = argc > 1 ? std::atoi(argv[1]) : 5;
     const int warmup = argc > 2 ? std::atoi(argv[2]) : 2;
     const std::uint64_t lattice = argc > 3 ? std::strtoull(argv[3], nullptr, 10) : 512;

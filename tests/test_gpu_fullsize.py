@@ -155,3 +155,28 @@ def test_config5_full_size_matches_reference(cuda, ref, oracle, g, tau, rho):
     assert s.mode == (0 if g == 128 else 1)
     _run_cases(plan, s, ref, oracle, [(x.cpu().numpy(), x, tau)],
                f"config5 200M/{g}^3 mode={'seed' if s.mode else 'dense'} rho={rho}", rho=rho)
+
+
+@pytest.mark.parametrize("fill", [0, 1])
+def test_multilinear_verbatim_pins_g_bit_for_bit(cuda, ref, oracle, fill):
+    """Multilinear g at >= 10^7 vertices (config 3, 224^3 = 11.2M vertices,
+    grid 112^3) with the verbatim codec (codec 1: the raw fp64 residuals
+    x - g are stored, codec.hpp:240-248): archive byte-identical to the
+    reference, i.e. g (interp.hpp:97-132) bit for bit on every vertex --
+    the certified Markstein quotient, the slot-hinted cell search and the
+    staged corners included. Decode: bitwise equal to the reference's."""
+    import torch
+    xyz, x = umcg.gen_config(3, 224, 0x250106910 + 3, device="cuda")
+    plan = umcg.Plan.build([np.linspace(0.0, 1.0, 112) for _ in range(3)], xyz, keep_coords=True)
+    s = _setup(plan, coords=xyz.cpu().numpy())
+    del xyz
+    torch.cuda.empty_cache()
+    xh = x.cpu().numpy()
+    b = umcg.Budget(tau=1e-4, g_kind=1, fill=fill, codec_id=1)
+    got = plan.compress(x, b, name="ml")
+    want = ref.compress(s, xh, name="ml", tau=1e-4, g_kind=1, fill=fill, codec_id=1)
+    assert got == want
+    out = plan.decompress(got).cpu().numpy()
+    assert np.array_equal(out.view(np.uint64), ref.decompress(s, want).view(np.uint64))
+    _log(dict(case=f"multilinear verbatim config3 224^3/112^3 fill={fill}", n=int(xh.size), identical=True,
+              archive_bytes=len(got)))
