@@ -30,8 +30,12 @@ struct umcg_plan {
     double axis_scale[3] = {0, 0, 0};  // (m - 1) / (a[m-1] - a[0]): index guess
     umcg::DevBuf d_coords;   // f64 [n*dim] (multilinear g), optional
     bool has_coords = false;
-    umcg::DevBuf d_coordsE;  // f64 [n*dim] coordinates in layout-E order (built on first multilinear use)
-    bool has_coordsE = false;
+    // multilinear g, layout E (built on first multilinear use, partition.cu
+    // ml_prep): the per-axis cell fractions t_d of every vertex (they depend
+    // only on the static coordinates and axes) and its cell bits
+    umcg::DevBuf d_mlT;      // f64 [dim*n] structure of arrays
+    umcg::DevBuf d_mlB;      // u8  [n] bit d: cell lower index = slot index - 1 along d; 0x80: no slot hint
+    bool has_mlprep = false;
     // bucketed layout for the partitioned compress path (partition.cu):
     // buckets are contiguous slot ranges holding <= kBucketCap vertices
     // (a heavier slot gets a bucket of its own).
