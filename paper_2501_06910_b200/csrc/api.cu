@@ -204,9 +204,11 @@ void escape_encode(umcg_plan* p, const double* v, uint64_t n, int pred, const Nd
         uint64_t ne = 0;
         bool ok = false;
         if (epred == 1) {
+            ProfScope ps_("esc_seg_encode", st);
             ok = seg_encode_1d(v, n, tau, codes, esc_idx, esc_val, p->esc_aux.reserve(esc_scratch_bytes(n)), ectl, h,
                                &ne, st);
         } else if (epred == 2 && (sh.D == 2 || sh.D == 3)) {
+            ProfScope ps_("esc_wave_encode", st);
             auto* F = static_cast<uint8_t*>(p->esc_aux.reserve(esc_scratch_bytes(n)));
             auto* toff = reinterpret_cast<uint64_t*>(F + ((n + 255) & ~255ull));
             ok = wave_encode_nd(v, n, sh, tau, codes, recon_scratch, F, st);
@@ -709,6 +711,7 @@ void decode_component(umcg_plan* p, const CompHeader& h, const uint8_t* d_payloa
     if (std::isfinite(bin) && h.tau > 0.0 && (pred == 1 || (pred == 2 && (h.D == 2 || h.D == 3)))) {
         auto* ectl = p->esc_ctl.as<DevCtl>(1);
         auto* hc = static_cast<DevCtl*>(p->hctl.reserve(sizeof(DevCtl)));
+        ProfScope ps_(pred == 1 ? "esc_seg_decode" : "esc_wave_decode", st);
         if (pred == 1) {
             int64_t* K = p->kbuf.as<int64_t>(h.n);
             auto* scr = static_cast<int64_t*>(p->esc_aux.reserve(8 * (cdiv(h.n, 2048) + 2 + h.n_esc)));

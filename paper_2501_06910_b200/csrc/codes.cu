@@ -18,6 +18,9 @@
 // All files compile with --fmad=false: no contraction, IEEE division and
 // round-half-away-from-zero, exactly like the reference build
 // (-ffp-contract=off, proj/CMakeLists.txt:16-17).
+#include <cstdlib>
+
+#include <cooperative_groups.h>
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
@@ -648,6 +651,95 @@ __global__ void k_esc_slots(const uint64_t* __restrict__ eidx, uint64_t ne, int3
     if (e < ne) eslot[eidx[e]] = (int32_t)e;
 }
 
+// One cooperative launch for the whole wavefront: the grid walks the planes
+// in order with a grid-wide barrier between them (instead of one launch per
+// plane: 766 for a 256^3 grid). Same per-node work as k_wave_enc / k_wave_dec.
+__device__ __forceinline__ bool plane_node(const NdShape& sh, uint64_t s, uint64_t i_lo, uint64_t t, uint64_t* lin) {
+    if (sh.D == 2) {
+        const uint64_t i = i_lo + t, j = s - i;
+        *lin = i * sh.dims[1] + j;
+        return true;
+    }
+    const uint64_t i = i_lo + t / sh.dims[1], j = t % sh.dims[1];
+    if (i + j > s) return false;
+    const uint64_t k = s - i - j;
+    if (k >= sh.dims[2]) return false;
+    *lin = (i * sh.dims[1] + j) * sh.dims[2] + k;
+    return true;
+}
+
+// MODE 0: lossy encode with escapes, 1: lossy decode with escapes, 2: lossless
+// decode (codec.hpp:429-430).
+template <int MODE>
+__global__ void __launch_bounds__(THREADS) k_wave_coop(const double* __restrict__ v, const uint64_t* __restrict__ cin,
+                                                      NdShape sh, double tau, double bin, double* __restrict__ recon,
+                                                      uint64_t* __restrict__ cout, uint8_t* __restrict__ F,
+                                                      const int32_t* __restrict__ eslot,
+                                                      const double* __restrict__ eval) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    uint64_t smax = 0;
+    for (int d = 0; d < sh.D; ++d) smax += sh.dims[d] - 1;
+    const uint64_t d0 = sh.dims[0], rest = smax - (d0 - 1);
+    const uint64_t tid = blockIdx.x * (uint64_t)THREADS + threadIdx.x, nth = (uint64_t)gridDim.x * THREADS;
+    for (uint64_t s = 0; s <= smax; ++s) {
+        const uint64_t i_lo = s > rest ? s - rest : 0, i_hi = d0 - 1 < s ? d0 - 1 : s;
+        const uint64_t rows = i_hi - i_lo + 1;
+        const uint64_t cnt = sh.D == 2 ? rows : rows * sh.dims[1];
+        for (uint64_t t = tid; t < cnt; t += nth) {
+            uint64_t lin;
+            if (!plane_node(sh, s, i_lo, t, &lin)) continue;
+            const double p = lorenzo_fp(recon, lin, sh);
+            if (MODE == 2) {
+                recon[lin] = __longlong_as_double((long long)(cin[lin] ^ (uint64_t)__double_as_longlong(p)));
+            } else if (MODE == 0) {
+                const double x = v[lin];
+                const double qd = round(__ddiv_rn(__dsub_rn(x, p), bin));
+                bool escape = !(fabs(qd) <= kQLimit);
+                double r = 0.0;
+                if (!escape) {
+                    r = __dadd_rn(p, __dmul_rn(qd, bin));
+                    escape = !(fabs(__dsub_rn(x, r)) <= tau);
+                }
+                F[lin] = escape ? 1 : 0;
+                cout[lin] = escape ? 0 : zz_enc((int64_t)qd);
+                recon[lin] = escape ? x : r;
+            } else {
+                const int32_t e = eslot[lin];
+                recon[lin] = e >= 0 ? eval[e] : __dadd_rn(p, __dmul_rn((double)zz_dec(cin[lin]), bin));
+            }
+        }
+        __threadfence();
+        grid.sync();
+    }
+}
+
+// Launches the cooperative wavefront; false when the device cannot (the
+// caller then launches plane by plane).
+template <int MODE>
+bool wave_coop(const double* v, const uint64_t* cin, const NdShape& sh, double tau, double bin, double* recon,
+               uint64_t* cout, uint8_t* F, const int32_t* eslot, const double* eval, cudaStream_t st) {
+    if (std::getenv("UMCG_WAVE_LAUNCHES")) return false;
+    int dev = 0, sms = 0, coop = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (!coop || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wave_coop<MODE>, THREADS, 0) != cudaSuccess ||
+        per < 1) {
+        cudaGetLastError();
+        return false;
+    }
+    void* args[] = {(void*)&v, (void*)&cin, (void*)&sh, (void*)&tau, (void*)&bin, (void*)&recon, (void*)&cout,
+                    (void*)&F, (void*)&eslot, (void*)&eval};
+    const dim3 grid((unsigned)(sms * std::min(per, 4)));
+    if (cudaLaunchCooperativeKernel((const void*)k_wave_coop<MODE>, grid, dim3(THREADS), args, 0, st) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    UMCG_LAUNCHED();
+    return true;
+}
+
 template <class F>
 void for_planes(const NdShape& sh, F&& f) {
     uint64_t smax = 0;
@@ -667,6 +759,7 @@ bool wave_encode_nd(const double* v, uint64_t n, const NdShape& sh, double tau, 
     if (sh.D != 2 && sh.D != 3) return false;
     if (!n) return true;
     const double bin = 2.0 * tau;
+    if (wave_coop<0>(v, nullptr, sh, tau, bin, recon, codes, F, nullptr, nullptr, st)) return true;
     for_planes(sh, [&](uint64_t s, uint64_t i_lo, uint64_t cnt) {
         k_wave_enc<<<(unsigned)cdiv(cnt, THREADS), THREADS, 0, st>>>(v, sh, s, i_lo, cnt, tau, bin, recon, codes, F);
         UMCG_LAUNCHED();
@@ -684,6 +777,7 @@ bool wave_decode_nd(const uint64_t* codes, uint64_t n, const NdShape& sh, double
         k_esc_slots<<<(unsigned)cdiv(n_esc, 256), 256, 0, st>>>(esc_idx, n_esc, eslot);
         UMCG_LAUNCHED();
     }
+    if (wave_coop<1>(nullptr, codes, sh, tau, bin, out, nullptr, nullptr, eslot, esc_val, st)) return true;
     for_planes(sh, [&](uint64_t s, uint64_t i_lo, uint64_t cnt) {
         k_wave_dec<<<(unsigned)cdiv(cnt, THREADS), THREADS, 0, st>>>(codes, sh, s, i_lo, cnt, bin, eslot, esc_val, out);
         UMCG_LAUNCHED();
@@ -694,6 +788,7 @@ bool wave_decode_nd(const uint64_t* codes, uint64_t n, const NdShape& sh, double
 bool lossless_nd_wavefront(const uint64_t* codes, uint64_t n, const NdShape& sh, double* out, cudaStream_t st) {
     if (sh.D != 2 && sh.D != 3) return false;
     if (!n) return true;
+    if (wave_coop<2>(nullptr, codes, sh, 0.0, 0.0, out, nullptr, nullptr, nullptr, nullptr, st)) return true;
     uint64_t smax = 0;
     for (int d = 0; d < sh.D; ++d) smax += sh.dims[d] - 1;
     const uint64_t d0 = sh.dims[0], rest = smax - (d0 - 1);  // max of the other coordinates' sum
