@@ -651,23 +651,33 @@ __global__ void k_esc_slots(const uint64_t* __restrict__ eidx, uint64_t ne, int3
     if (e < ne) eslot[eidx[e]] = (int32_t)e;
 }
 
+// lorenzo_predict (codec.hpp:61-80) at node (i, j, k) of a 2-/3-D grid with
+// the neighbours addressed directly: masks 1..2^D-1 in order, bit d = axis d
+// (axis 0 slowest), a mask skipped when it steps off the grid, p accumulated
+// from 0.0 with + for odd and - for even popcounts -- lorenzo_fp's operations
+// without the index arithmetic.
+__device__ __forceinline__ double lorenzo_direct(const double* __restrict__ r, uint64_t c, uint32_t D, bool ai,
+                                                 bool aj, bool ak, uint64_t s0, uint64_t s1) {
+    double p = 0.0;
+    if (D == 2) {  // axes (i, j) = (0, 1); strides s0 = dims[1], 1
+        if (ai) p = __dadd_rn(p, r[c - s0]);
+        if (aj) p = __dadd_rn(p, r[c - 1]);
+        if (ai && aj) p = __dsub_rn(p, r[c - s0 - 1]);
+        return p;
+    }
+    if (ai) p = __dadd_rn(p, r[c - s0]);                       // mask 1
+    if (aj) p = __dadd_rn(p, r[c - s1]);                       // mask 2
+    if (ai && aj) p = __dsub_rn(p, r[c - s0 - s1]);            // mask 3
+    if (ak) p = __dadd_rn(p, r[c - 1]);                        // mask 4
+    if (ai && ak) p = __dsub_rn(p, r[c - s0 - 1]);             // mask 5
+    if (aj && ak) p = __dsub_rn(p, r[c - s1 - 1]);             // mask 6
+    if (ai && aj && ak) p = __dadd_rn(p, r[c - s0 - s1 - 1]);  // mask 7
+    return p;
+}
+
 // One cooperative launch for the whole wavefront: the grid walks the planes
 // in order with a grid-wide barrier between them (instead of one launch per
 // plane: 766 for a 256^3 grid). Same per-node work as k_wave_enc / k_wave_dec.
-__device__ __forceinline__ bool plane_node(const NdShape& sh, uint64_t s, uint64_t i_lo, uint64_t t, uint64_t* lin) {
-    if (sh.D == 2) {
-        const uint64_t i = i_lo + t, j = s - i;
-        *lin = i * sh.dims[1] + j;
-        return true;
-    }
-    const uint64_t i = i_lo + t / sh.dims[1], j = t % sh.dims[1];
-    if (i + j > s) return false;
-    const uint64_t k = s - i - j;
-    if (k >= sh.dims[2]) return false;
-    *lin = (i * sh.dims[1] + j) * sh.dims[2] + k;
-    return true;
-}
-
 // MODE 0: lossy encode with escapes, 1: lossy decode with escapes, 2: lossless
 // decode (codec.hpp:429-430).
 template <int MODE>
@@ -688,8 +698,29 @@ __global__ void __launch_bounds__(THREADS) k_wave_coop(const double* __restrict_
         const uint64_t cnt = sh.D == 2 ? rows : rows * sh.dims[1];
         for (uint64_t t = tid; t < cnt; t += nth) {
             uint64_t lin;
-            if (!plane_node(sh, s, i_lo, t, &lin)) continue;
-            const double p = lorenzo_fp(recon, lin, sh);
+            bool ai, aj, ak = false;
+            uint64_t st0, st1 = 0;
+            if (sh.D == 2) {
+                const uint64_t i = i_lo + t, j = s - i;
+                lin = i * sh.dims[1] + j;
+                ai = i > 0;
+                aj = j > 0;
+                st0 = sh.dims[1];
+            } else {
+                const uint32_t d1 = (uint32_t)sh.dims[1];
+                const uint32_t tq = (uint32_t)(t / d1);
+                const uint64_t i = i_lo + tq, j = t - (uint64_t)tq * d1;
+                if (i + j > s) continue;
+                const uint64_t k = s - i - j;
+                if (k >= sh.dims[2]) continue;
+                lin = (i * sh.dims[1] + j) * sh.dims[2] + k;
+                ai = i > 0;
+                aj = j > 0;
+                ak = k > 0;
+                st1 = sh.dims[2];
+                st0 = sh.dims[1] * sh.dims[2];
+            }
+            const double p = lorenzo_direct(recon, lin, (uint32_t)sh.D, ai, aj, ak, st0, st1);
             if (MODE == 2) {
                 recon[lin] = __longlong_as_double((long long)(cin[lin] ^ (uint64_t)__double_as_longlong(p)));
             } else if (MODE == 0) {
@@ -716,6 +747,9 @@ __global__ void __launch_bounds__(THREADS) k_wave_coop(const double* __restrict_
 
 // Launches the cooperative wavefront; false when the device cannot (the
 // caller then launches plane by plane).
+#ifndef UMCG_WAVE_BPS_DEFAULT
+#define UMCG_WAVE_BPS_DEFAULT 2
+#endif
 template <int MODE>
 bool wave_coop(const double* v, const uint64_t* cin, const NdShape& sh, double tau, double bin, double* recon,
                uint64_t* cout, uint8_t* F, const int32_t* eslot, const double* eval, cudaStream_t st) {
@@ -731,7 +765,12 @@ bool wave_coop(const double* v, const uint64_t* cin, const NdShape& sh, double t
     }
     void* args[] = {(void*)&v, (void*)&cin, (void*)&sh, (void*)&tau, (void*)&bin, (void*)&recon, (void*)&cout,
                     (void*)&F, (void*)&eslot, (void*)&eval};
-    const dim3 grid((unsigned)(sms * std::min(per, 4)));
+    // blocks per SM: the grid barrier's cost grows with the block count (A/B: UMCG_WAVE_BPS)
+    static const int bps = [] {
+        const char* e = std::getenv("UMCG_WAVE_BPS");
+        return e ? std::max(1, std::atoi(e)) : UMCG_WAVE_BPS_DEFAULT;
+    }();
+    const dim3 grid((unsigned)(sms * std::min(per, bps)));
     if (cudaLaunchCooperativeKernel((const void*)k_wave_coop<MODE>, grid, dim3(THREADS), args, 0, st) != cudaSuccess) {
         cudaGetLastError();
         return false;
