@@ -1069,6 +1069,27 @@ void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_
         if (!hc.aux[7] && (double)hc.max_abs_k[1] < k_lim(1, 1)) return;
     }
     if (k1_lattice) k32_to_f64(K1, p->n_slots, bin1, x1, st);
+    // Multilinear g over the lattice residual: g in layout E first (partition.cu
+    // ml_layout_g), then one fused pass decodes the residual and adds g_i
+    // gathered through dstE (DEC_RECOMPOSE_GE) -- no fp64 residual round trip.
+    if (g_kind == 1 && !seed && p->has_coords && p->n_buckets > 0 && h2.codec == 0 && h2.backend == 0 &&
+        h2.D == 1 && pred2 == 1 && h2.tau != 0.0 && !h2.n_esc && std::isfinite(bin2)) {
+        uint64_t* eidx;
+        double* evals;
+        decode_prelude(p, h2, d_ar + p2, &eidx, &evals, st);
+        double* gE = p->dcodes.as<double>(p->n);
+        ml_layout_g(p, x1, gE, st);
+        auto* ctl = p->ctl.as<DevCtl>(1);
+        init_ctl(ctl, st);
+        uint64_t ulen = 0;
+        const uint8_t* U = stream_unpack(d_ar + p2 + h2.stream_off, h2.stream_len, p->dec, ctl, st, &ulen);
+        init_ctl(ctl, st);
+        void* status = p->scratch_c.reserve(dec_status_bytes(ulen));
+        dec_fused(DEC_RECOMPOSE_GE, host_src(U, ulen), dec_tiles(ulen), p->n, status, ctl, p->d_dstE.as<uint32_t>(1),
+                  reinterpret_cast<const int32_t*>(gE), 0.0, bin2, d_out, nullptr, st);
+        const DevCtl hc = check_fused(p, ctl, U, ulen, p->n, st);
+        if (!hc.aux[7] && (double)hc.max_abs_k[1] < k_lim(1, 1)) return;
+    }
     decode_component(p, h2, d_ar + p2, d_out, st);
     if (g_kind == 1 && seed) fail(UMCG_SEED_MODE_UNSUPPORTED, "multilinear back-interpolation needs a dense grid component");
     if (g_kind == 1 && !p->has_coords) fail(UMCG_INVALID_ARGUMENT, "multilinear g needs a plan with vertex coordinates");

@@ -747,6 +747,178 @@ __global__ void __launch_bounds__(THREADS) k_wave_coop(const double* __restrict_
 
 // Launches the cooperative wavefront; false when the device cannot (the
 // caller then launches plane by plane).
+// Tiled wavefront: the grid is cut into T^D tiles; tiles on one tile-plane
+// (I + J [+ K] = S) are independent given the earlier tile-planes, so the
+// grid barrier runs once per tile-plane (46 for 256^3 with T = 16, instead of
+// 766). Each tile is reconstructed in shared memory with its one-node halo
+// from the earlier tiles, plane by plane inside the tile (i + j [+ k] = s,
+// __syncthreads between), with lorenzo_direct on the shared copy -- the
+// reference's operations, in its order -- then written back.
+template <int D>
+struct WaveTile {
+    static constexpr int T = D == 3 ? 16 : 64;
+    static constexpr int P = T + 1;  // tile + one halo node per axis
+    // shared strides padded off multiples of 128 bytes: the nodes of one
+    // plane (stepping +1 / -1 along two axes) then fall into different banks
+    static constexpr int Q1 = D == 3 ? P + 1 : 1;
+    static constexpr int Q0 = D == 3 ? (P + 1) * Q1 : P + 1;
+    static constexpr int SM = P * Q0;
+};
+
+template <int MODE, int D>
+__global__ void __launch_bounds__(THREADS) k_wave_tiled(const double* __restrict__ v, const uint64_t* __restrict__ cin,
+                                                       NdShape sh, double tau, double bin, double* __restrict__ recon,
+                                                       uint64_t* __restrict__ cout, uint8_t* __restrict__ F,
+                                                       const int32_t* __restrict__ eslot,
+                                                       const double* __restrict__ eval) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    constexpr int T = WaveTile<D>::T, P = WaveTile<D>::P;
+    constexpr int TN = D == 3 ? T * T * T : T * T;  // nodes per tile
+    extern __shared__ __align__(16) double wsm[];
+    double* sr = wsm;                                              // [SM] reconstruction + halo
+    uint64_t* sin = reinterpret_cast<uint64_t*>(wsm + WaveTile<D>::SM);  // [TN] the tile's values / codes
+    int32_t* ses = reinterpret_cast<int32_t*>(sin + TN);              // [TN] escape slots (decode)
+    const uint64_t n0 = sh.dims[0], n1 = sh.dims[1], n2 = D == 3 ? sh.dims[2] : 1;
+    const uint32_t tI = (uint32_t)((n0 + T - 1) / T), tJ = (uint32_t)((n1 + T - 1) / T),
+                   tK = D == 3 ? (uint32_t)((n2 + T - 1) / T) : 1;
+    const uint32_t Smax = (tI - 1) + (tJ - 1) + (tK - 1);
+    const uint64_t g0 = D == 3 ? n1 * n2 : n1, g1 = D == 3 ? n2 : 1;  // global strides of axes 0, 1
+    constexpr uint64_t q0 = WaveTile<D>::Q0, q1 = WaveTile<D>::Q1;       // shared strides
+    for (uint32_t S = 0; S <= Smax; ++S) {
+        const uint32_t ntile = D == 3 ? tI * tJ : tI;
+        for (uint32_t t = blockIdx.x; t < ntile; t += gridDim.x) {
+            uint32_t I, J, K = 0;
+            if (D == 3) {
+                I = t / tJ;
+                J = t - I * tJ;
+                if (I + J > S || S - I - J >= tK) continue;
+                K = S - I - J;
+            } else {
+                I = t;
+                if (I > S || S - I >= tJ) continue;
+                J = S - I;
+            }
+            const uint64_t i0 = (uint64_t)I * T, j0 = (uint64_t)J * T, k0 = (uint64_t)K * T;
+            // halo (local index 0 on some axis) from the finished earlier tiles
+            constexpr uint32_t HN = D == 3 ? P * P * P : P * P;
+            for (uint32_t x = threadIdx.x; x < HN; x += THREADS) {
+                const uint32_t a = D == 3 ? x / (P * P) : x / P;
+                const uint32_t b = D == 3 ? (x / P) % P : x % P;
+                const uint32_t c = D == 3 ? x % P : 1;
+                if (a != 0 && b != 0 && (D == 2 || c != 0)) continue;
+                const int64_t gi = (int64_t)i0 + a - 1, gj = (int64_t)j0 + b - 1, gk = D == 3 ? (int64_t)k0 + c - 1 : 0;
+                double val = 0.0;
+                if (gi >= 0 && gj >= 0 && gk >= 0 && (uint64_t)gi < n0 && (uint64_t)gj < n1 && (uint64_t)gk < n2)
+                    val = recon[(uint64_t)gi * g0 + (uint64_t)gj * g1 + (uint64_t)gk];
+                sr[a * q0 + (D == 3 ? b * q1 + c : b)] = val;
+            }
+            // the tile's inputs, once (the plane loop below touches shared memory only)
+            for (uint32_t x = threadIdx.x; x < (uint32_t)TN; x += THREADS) {
+                const uint32_t a = D == 3 ? x / (T * T) : x / T;
+                const uint32_t b = D == 3 ? (x / T) % T : x % T;
+                const uint32_t c = D == 3 ? x % T : 0;
+                const uint64_t gi = i0 + a, gj = j0 + b, gk = k0 + c;
+                if (gi >= n0 || gj >= n1 || gk >= n2) continue;
+                const uint64_t lin = gi * g0 + gj * g1 + gk;
+                sin[x] = MODE == 0 ? (uint64_t)__double_as_longlong(v[lin]) : cin[lin];
+                if (MODE == 1) ses[x] = eslot[lin];
+            }
+            __syncthreads();
+            const int nloc = D == 3 ? 3 * T - 2 : 2 * T - 1;
+            for (int sl = 0; sl < nloc; ++sl) {
+                // nodes (a, b[, c]) of the tile with a + b [+ c] = sl
+                const uint32_t cand = D == 3 ? T * T : T;
+                for (uint32_t x = threadIdx.x; x < cand; x += THREADS) {
+                    uint32_t a, b, c = 0;
+                    if (D == 3) {
+                        a = x / T;
+                        b = x % T;
+                        if ((int)(a + b) > sl || sl - (int)(a + b) >= T) continue;
+                        c = (uint32_t)sl - a - b;
+                    } else {
+                        a = x;
+                        if ((int)a > sl || sl - (int)a >= T) continue;
+                        b = (uint32_t)sl - a;
+                    }
+                    const uint64_t gi = i0 + a, gj = j0 + b, gk = k0 + c;
+                    if (gi >= n0 || gj >= n1 || gk >= n2) continue;
+                    const uint64_t lin = gi * g0 + gj * g1 + gk;
+                    const uint32_t tx = D == 3 ? (a * T + b) * T + c : a * T + b;
+                    const uint64_t pos = (uint64_t)(a + 1) * q0 + (uint64_t)(b + 1) * q1 + (D == 3 ? c + 1 : 0);
+                    const double p = D == 3 ? lorenzo_direct(sr, pos, 3, gi > 0, gj > 0, gk > 0, q0, q1)
+                                            : lorenzo_direct(sr, pos, 2, gi > 0, gj > 0, false, q0, 0);
+                    double r;
+                    if (MODE == 2) {
+                        r = __longlong_as_double((long long)(sin[tx] ^ (uint64_t)__double_as_longlong(p)));
+                    } else if (MODE == 0) {
+                        const double xv = __longlong_as_double((long long)sin[tx]);
+                        const double qd = round(__ddiv_rn(__dsub_rn(xv, p), bin));
+                        bool escape = !(fabs(qd) <= kQLimit);
+                        r = 0.0;
+                        if (!escape) {
+                            r = __dadd_rn(p, __dmul_rn(qd, bin));
+                            escape = !(fabs(__dsub_rn(xv, r)) <= tau);
+                        }
+                        F[lin] = escape ? 1 : 0;
+                        cout[lin] = escape ? 0 : zz_enc((int64_t)qd);
+                        if (escape) r = xv;
+                    } else {
+                        const int32_t e = ses[tx];
+                        r = e >= 0 ? eval[e] : __dadd_rn(p, __dmul_rn((double)zz_dec(sin[tx]), bin));
+                    }
+                    sr[pos] = r;
+                }
+                __syncthreads();
+            }
+            // the tile back to global memory
+            for (uint32_t x = threadIdx.x; x < (uint32_t)(D == 3 ? T * T * T : T * T); x += THREADS) {
+                const uint32_t a = D == 3 ? x / (T * T) : x / T;
+                const uint32_t b = D == 3 ? (x / T) % T : x % T;
+                const uint32_t c = D == 3 ? x % T : 0;
+                const uint64_t gi = i0 + a, gj = j0 + b, gk = k0 + c;
+                if (gi >= n0 || gj >= n1 || gk >= n2) continue;
+                recon[gi * g0 + gj * g1 + gk] = sr[(uint64_t)(a + 1) * q0 + (uint64_t)(b + 1) * q1 + (D == 3 ? c + 1 : 0)];
+            }
+            __syncthreads();
+        }
+        __threadfence();
+        grid.sync();
+    }
+}
+
+template <int MODE>
+bool wave_tiled(const double* v, const uint64_t* cin, const NdShape& sh, double tau, double bin, double* recon,
+                uint64_t* cout, uint8_t* F, const int32_t* eslot, const double* eval, cudaStream_t st) {
+    if (std::getenv("UMCG_WAVE_LAUNCHES") || std::getenv("UMCG_WAVE_UNTILED")) return false;
+    int dev = 0, sms = 0, coop = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const void* fn = sh.D == 3 ? (const void*)k_wave_tiled<MODE, 3> : (const void*)k_wave_tiled<MODE, 2>;
+    const int tn = sh.D == 3 ? WaveTile<3>::T * WaveTile<3>::T * WaveTile<3>::T : WaveTile<2>::T * WaveTile<2>::T;
+    const size_t smem = 8 * (size_t)(sh.D == 3 ? WaveTile<3>::SM : WaveTile<2>::SM) + 12 * (size_t)tn;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    cudaError_t oe = sh.D == 3 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wave_tiled<MODE, 3>, THREADS, smem)
+                               : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wave_tiled<MODE, 2>, THREADS, smem);
+    if (!coop || oe != cudaSuccess || per < 1) {
+        cudaGetLastError();
+        return false;
+    }
+    void* args[] = {(void*)&v, (void*)&cin, (void*)&sh, (void*)&tau, (void*)&bin, (void*)&recon, (void*)&cout,
+                    (void*)&F, (void*)&eslot, (void*)&eval};
+    const dim3 grid((unsigned)(sms * std::min(per, 2)));
+    if (cudaLaunchCooperativeKernel(fn, grid, dim3(THREADS), args, smem, st) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    UMCG_LAUNCHED();
+    return true;
+}
+
 #ifndef UMCG_WAVE_BPS_DEFAULT
 #define UMCG_WAVE_BPS_DEFAULT 2
 #endif
@@ -798,6 +970,7 @@ bool wave_encode_nd(const double* v, uint64_t n, const NdShape& sh, double tau, 
     if (sh.D != 2 && sh.D != 3) return false;
     if (!n) return true;
     const double bin = 2.0 * tau;
+    if (wave_tiled<0>(v, nullptr, sh, tau, bin, recon, codes, F, nullptr, nullptr, st)) return true;
     if (wave_coop<0>(v, nullptr, sh, tau, bin, recon, codes, F, nullptr, nullptr, st)) return true;
     for_planes(sh, [&](uint64_t s, uint64_t i_lo, uint64_t cnt) {
         k_wave_enc<<<(unsigned)cdiv(cnt, THREADS), THREADS, 0, st>>>(v, sh, s, i_lo, cnt, tau, bin, recon, codes, F);
@@ -816,6 +989,7 @@ bool wave_decode_nd(const uint64_t* codes, uint64_t n, const NdShape& sh, double
         k_esc_slots<<<(unsigned)cdiv(n_esc, 256), 256, 0, st>>>(esc_idx, n_esc, eslot);
         UMCG_LAUNCHED();
     }
+    if (wave_tiled<1>(nullptr, codes, sh, tau, bin, out, nullptr, nullptr, eslot, esc_val, st)) return true;
     if (wave_coop<1>(nullptr, codes, sh, tau, bin, out, nullptr, nullptr, eslot, esc_val, st)) return true;
     for_planes(sh, [&](uint64_t s, uint64_t i_lo, uint64_t cnt) {
         k_wave_dec<<<(unsigned)cdiv(cnt, THREADS), THREADS, 0, st>>>(codes, sh, s, i_lo, cnt, bin, eslot, esc_val, out);
@@ -827,6 +1001,7 @@ bool wave_decode_nd(const uint64_t* codes, uint64_t n, const NdShape& sh, double
 bool lossless_nd_wavefront(const uint64_t* codes, uint64_t n, const NdShape& sh, double* out, cudaStream_t st) {
     if (sh.D != 2 && sh.D != 3) return false;
     if (!n) return true;
+    if (wave_tiled<2>(nullptr, codes, sh, 0.0, 0.0, out, nullptr, nullptr, nullptr, nullptr, st)) return true;
     if (wave_coop<2>(nullptr, codes, sh, 0.0, 0.0, out, nullptr, nullptr, nullptr, nullptr, st)) return true;
     uint64_t smax = 0;
     for (int d = 0; d < sh.D; ++d) smax += sh.dims[d] - 1;

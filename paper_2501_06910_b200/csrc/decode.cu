@@ -337,6 +337,8 @@ __global__ void __launch_bounds__(RT, UMCG_DEC_MINB) k_dec_out(const DecSrc src,
         const double r = __dmul_rn((double)k, bin);
         if (MODE == DEC_VALUES) {
             out[i] = r;
+        } else if (MODE == DEC_RECOMPOSE_GE) {
+            out[i] = __dadd_rn(reinterpret_cast<const double*>(K1)[node[i]], r);
         } else {
             const uint32_t nd = node[i];
             const int32_t g = use16t ? (int32_t)__ldg((sizeof(KT) == 2 ? reinterpret_cast<const int16_t*>(K1) : K16) + nd)
@@ -367,12 +369,18 @@ __global__ void __launch_bounds__(RT, UMCG_DEC_MINB) k_dec_out(const DecSrc src,
 #pragma unroll
         for (int u = 0; u < UN; ++u) {
             const uint32_t e = e0 + u * RT + threadIdx.x;
-            nd[u] = (MODE == DEC_RECOMPOSE && e < cnt && tp.cnt + e < n) ? ld_u32_hint(&node[tp.cnt + e], pf) : 0u;
+            nd[u] = ((MODE == DEC_RECOMPOSE || MODE == DEC_RECOMPOSE_GE) && e < cnt && tp.cnt + e < n)
+                        ? ld_u32_hint(&node[tp.cnt + e], pf)
+                        : 0u;
         }
         int32_t g1[UN];
+        double ge[UN];
 #pragma unroll
         for (int u = 0; u < UN; ++u) {
             const uint32_t e = e0 + u * RT + threadIdx.x;
+            ge[u] = (MODE == DEC_RECOMPOSE_GE && e < cnt && tp.cnt + e < n)
+                        ? UMCG_GATHER_LD(reinterpret_cast<const double*>(K1) + nd[u])
+                        : 0.0;
             if (MODE == DEC_RECOMPOSE && e < cnt && tp.cnt + e < n)
                 g1[u] = sizeof(KT) == 2 || use16
                             ? (int32_t)UMCG_GATHER_LD((sizeof(KT) == 2 ? reinterpret_cast<const int16_t*>(K1) : K16) + nd[u])
@@ -387,6 +395,7 @@ __global__ void __launch_bounds__(RT, UMCG_DEC_MINB) k_dec_out(const DecSrc src,
             if (e >= cnt || i >= n) continue;
             const double r = __dmul_rn((double)kb[e], bin);
             if (MODE == DEC_VALUES) st_f64_hint(&out[i], r, pf);
+            else if (MODE == DEC_RECOMPOSE_GE) st_f64_hint(&out[i], __dadd_rn(ge[u], r), pf);  // approx + x2 (pipeline.hpp:208)
             else st_f64_hint(&out[i], __dadd_rn(__dmul_rn((double)g1[u], bin1), r), pf);
         }
     }
@@ -600,6 +609,9 @@ void dec_fused(int mode, const DecSrc& src, uint64_t T, uint64_t n, void* status
     else if (mode == DEC_VALUES)
         k_dec_out<DEC_VALUES, int32_t><<<(unsigned)T, RT, 0, st>>>(src, n, aggs, ctl, node, K1, bin1, bin, out, P64,
                                                                   nullptr, nullptr, raw, thr);
+    else if (mode == DEC_RECOMPOSE_GE)
+        k_dec_out<DEC_RECOMPOSE_GE, int32_t><<<(unsigned)T, RT, 0, st>>>(src, n, aggs, ctl, node, K1, bin1, bin, out,
+                                                                        P64, nullptr, nullptr, raw, thr);
     else if (mode == DEC_RECOMPOSE16)
         k_dec_out<DEC_RECOMPOSE, int16_t><<<(unsigned)T, RT, 0, st>>>(src, n, aggs, ctl, node,
                                                                      reinterpret_cast<const int16_t*>(K1), bin1, bin,

@@ -5,7 +5,9 @@
 
 namespace umcg {
 
-enum DecMode : int { DEC_P64 = 0, DEC_VALUES = 1, DEC_RECOMPOSE = 2, DEC_RECOMPOSE16 = 3 };
+// DEC_RECOMPOSE_GE: x'_i = g_i + fl(K * bin) with g prepared in layout E
+// (multilinear g, partition.cu): node = dstE, K1 = the fp64 gE array.
+enum DecMode : int { DEC_P64 = 0, DEC_VALUES = 1, DEC_RECOMPOSE = 2, DEC_RECOMPOSE16 = 3, DEC_RECOMPOSE_GE = 4 };
 
 // One RLE token (stream.cu): literal data offset, unpacked offset, length
 // (bit 63 set for literal tokens).

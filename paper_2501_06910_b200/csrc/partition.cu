@@ -957,6 +957,12 @@ void ml_residuals(umcg_plan* p, const double* xE, const double* x1, DevCtl* ctl,
     else launch_ml<0>(p, xE, x1, ctl, static_cast<int32_t*>(KE), nullptr, st);
 }
 
+void ml_layout_g(umcg_plan* p, const double* x1, double* gE, cudaStream_t st) {
+    ml_prep(p, st);
+    ProfScope ps_("k_ml_recompose", st);
+    if (p->n_buckets) launch_ml<1>(p, nullptr, x1, nullptr, static_cast<int32_t*>(nullptr), gE, st);
+}
+
 void ml_recompose(umcg_plan* p, const double* x1, double* gE, double* d_out, cudaStream_t st) {
     if (!p->n) return;
     ml_prep(p, st);

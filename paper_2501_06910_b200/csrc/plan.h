@@ -118,4 +118,6 @@ void resid_codes_tiles(umcg_plan* p, const void* Kp, void* codes, bool narrow, c
 void ml_residuals(umcg_plan* p, const double* xE, const double* x1, DevCtl* ctl, void* KE, bool narrow,
                   cudaStream_t st);
 void ml_recompose(umcg_plan* p, const double* x1, double* gE, double* d_out, cudaStream_t st);
+// g in layout E only (the fused residual decode gathers it back, DEC_RECOMPOSE_GE).
+void ml_layout_g(umcg_plan* p, const double* x1, double* gE, cudaStream_t st);
 }  // namespace umcg

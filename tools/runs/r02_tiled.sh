@@ -1,0 +1,3 @@
+python -m pytest tests/test_gpu_escapes.py tests/test_gpu_parity.py -q -k "escape or outlier or wavefront or lossless or nd_ or codec" 2>&1 | tail -3 > gpurun_out/t21.log
+python tools/bench_extra.py escape 2>&1 | tail -1 > gpurun_out/esc21_tiled.jsonl
+UMCG_WAVE_UNTILED=1 python tools/bench_extra.py escape 2>&1 | tail -1 > gpurun_out/esc21_coop.jsonl
