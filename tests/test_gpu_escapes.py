@@ -142,3 +142,23 @@ def test_pipeline_outliers_absolute_bound(cuda, ref, oracle, n_out):
     assert np.all(np.abs(out - xh)[ok] <= tau)
     out_w = plan.decompress(want).cpu().numpy()
     assert np.all(np.abs(out_w - ref.decompress(s, want)) <= tol)
+
+
+@pytest.mark.parametrize("layout", ["edges", "tile_boundaries", "runs"])
+def test_1d_escape_positions(cuda, ref, oracle, layout):
+    """Escapes where the fixed-point scan's carries matter: the first and the
+    last element, both sides of every 2048-element tile boundary and of the
+    8-element thread boundaries, and runs of consecutive outliers crossing
+    them (each run's second element codes q = 0 against the first: the exact
+    segment after an escape)."""
+    rng = np.random.default_rng(hash(layout) % 2**32)
+    n = 5 * 2048 + 3
+    v = np.cumsum(rng.normal(0, 1e-3, n))
+    if layout == "edges":
+        idx = [0, 1, n - 2, n - 1]
+    elif layout == "tile_boundaries":
+        idx = sorted({k + d for k in range(2048, n, 2048) for d in (-1, 0)} | {7, 8, 15, 16})
+    else:
+        idx = [i for k in range(2040, n, 2048) for i in range(k, min(n, k + 12))]
+    v[idx] = 1e300
+    _codec_case(ref, oracle, v, 1, [n], 1e-4)
