@@ -162,3 +162,33 @@ def test_1d_escape_positions(cuda, ref, oracle, layout):
         idx = [i for k in range(2040, n, 2048) for i in range(k, min(n, k + 12))]
     v[idx] = 1e300
     _codec_case(ref, oracle, v, 1, [n], 1e-4)
+
+
+def test_pipeline_outliers_seed_mode(cuda, ref, oracle):
+    """Seed-mode grid (config-5 shell at 2^19 vertices, 96^3: visited fraction
+    under 0.35, the grid component is lorenzo_1d over the visited nodes) with
+    outliers under an absolute bound: escapes in both 1-D components
+    (segmented lattice), against the reference."""
+    xyz, x = umcg.gen_config(5, 1 << 19, 20250115, device="cuda")
+    lo = xyz.min(0).values.cpu().numpy()
+    hi = xyz.max(0).values.cpu().numpy()
+    plan = umcg.Plan.build([np.linspace(lo[d], hi[d], 96) for d in range(3)], xyz)
+    mode, gaxes, assign, visited = plan.export()
+    assert mode == 1
+    s = Setup(dim=3, axes=gaxes, mode=mode, assignments=assign, visited=visited)
+    rng = np.random.default_rng(77)
+    xh = x.cpu().numpy()
+    idx = rng.choice(xh.size, 300, replace=False)
+    xh[idx] = np.where(rng.random(300) < 0.5, 1e300, -1e300)
+    tau = 1e-3
+    fb0 = umcg.serial_fallbacks()
+    got = plan.compress(dev(xh), umcg.Budget(tau=tau, bound_kind=0), name="s")
+    assert umcg.serial_fallbacks() == fb0
+    want = ref.compress(s, xh, name="s", tau=tau, bound_kind=0)
+    check_archive(got, want, s, xh, dict(tau=tau, bound_kind=0), oracle, "seed outliers")
+    out = plan.decompress(got).cpu().numpy()
+    assert umcg.serial_fallbacks() == fb0
+    rd = ref.decompress(s, got)
+    assert np.all(np.abs(out - rd) <= _tol(xh))
+    ok = np.abs(rd - xh) <= tau
+    assert np.all(np.abs(out - xh)[ok] <= tau)
