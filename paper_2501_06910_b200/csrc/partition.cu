@@ -349,6 +349,7 @@ static_assert(kBucketNodes <= 2 * BTP, "k_bucket_tma keeps <= 2 slots per thread
 constexpr int BT_ISSUE_WARP = UMCG_BT_ISSUE_WARP;
 
 
+
 template <class KT>
 __global__ void __launch_bounds__(BTP, 2) k_bucket_tma(const double* __restrict__ xE, const uint32_t* __restrict__ bk,
                                                   uint64_t B, uint32_t E, const uint2* __restrict__ bct,
