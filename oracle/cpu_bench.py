@@ -8,7 +8,9 @@ serialize_archive, deserialize_archive + umc::decompress, pipeline.hpp:117-148,
   the GPU arm's device-generated field;
 * the mapping from the reference's own grid_coarsen (grid_builder.hpp:365)
   over the same uniform 256^3 axes the GPU arm uses;
-* no import of the product package: this process never loads libumcg.so.
+* no import of the product package: this process loads only
+  oracle/_ref/libumcref.so (the reference behind its shim, plus the host
+  generator compiled into the same library).
 
 A sample is a block of the full 512^3 lattice (lattice points with every
 index below `block`, kept in the full mesh's permuted vertex order): exactly
@@ -37,7 +39,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 if os.path.dirname(HERE) not in sys.path:
     sys.path.insert(0, os.path.dirname(HERE))
 
-from oracle.bindings import HostGen, Ref  # noqa: E402
+from oracle.bindings import REF_SO, HostGen, Ref  # noqa: E402
 
 LATTICE, GRID = 512, 256
 SEED = 0x250106910 + 3
@@ -60,8 +62,10 @@ def host_info() -> dict:
 
 
 def build_sample(block: int, gen_threads: int | None = None):
-    """(ref, ctx, setup, x) for the config-3 block sample, host-only."""
-    g = HostGen(threads=gen_threads)
+    """(ref, ctx, setup, x) for the config-3 block sample, host-only (the
+    generator exported by oracle/_ref/libumcref.so itself: this process loads
+    nothing outside oracle/_ref)."""
+    g = HostGen(path=REF_SO, threads=gen_threads)
     t0 = time.perf_counter()
     if block >= LATTICE:
         xyz, x = g.gen(3, LATTICE, SEED)

@@ -37,3 +37,16 @@ def test_host_generator_matches_device(cuda, config, lattice):
     assert dv.dtype == hvals.dtype
     assert np.array_equal(dv.view(np.uint32 if dv.dtype == np.float32 else np.uint64),
                           hvals.view(np.uint32 if hvals.dtype == np.float32 else np.uint64))
+
+
+def test_reference_library_exports_the_same_generator():
+    """The CPU reference arm generates its inputs with the copy of the host
+    generator compiled into oracle/_ref/libumcref.so (that process loads
+    nothing else from the repo): same bytes as the standalone library."""
+    import os
+    from oracle.bindings import REF_SO
+    if not os.path.exists(REF_SO):
+        pytest.skip("oracle/_ref not built")
+    a = HostGen(path=REF_SO).gen3_block(64, 9, [0, 0, 0], [32, 32, 32])
+    b = HostGen().gen3_block(64, 9, [0, 0, 0], [32, 32, 32])
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
