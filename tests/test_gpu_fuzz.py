@@ -1,0 +1,86 @@
+"""Randomised parity sweep: small random meshes and budgets through the GPU
+pipeline against the unmodified reference (oracle/_ref). Each case draws the
+rank, the vertex count and layout (jittered lattice in random order, or a
+clustered point cloud), the grid size (dense or seed mode after
+grid_coarsen), the field (smooth, noisy, offset far from zero, with
+outliers), the bound kind, tau over seven decades, the error split, g
+(nearest / multilinear), the fill policy and the codec. The archive must be
+the reference's up to rounding-window codes, errors must be the reference's
+exception kinds, both decoders must agree and the bound must hold wherever
+the reference's own decode meets it."""
+import numpy as np
+import pytest
+
+import paper_2501_06910_b200 as umcg
+from helpers import check_archive
+from oracle.bindings import OracleError, Setup
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    dim = int(rng.choice([2, 3]))
+    if rng.random() < 0.6:
+        m = int(rng.integers(20, 120 if dim == 2 else 40))
+        idx = np.stack(np.meshgrid(*[np.arange(m)] * dim, indexing="ij"), -1).reshape(-1, dim)
+        xyz = (idx + rng.uniform(-0.3, 0.3, idx.shape)) / (m - 1)
+    else:
+        n = int(rng.integers(2000, 40000))
+        centres = rng.uniform(0, 1, (5, dim))
+        xyz = centres[rng.integers(0, 5, n)] + rng.normal(0, 0.05, (n, dim))
+    xyz = xyz[rng.permutation(len(xyz))]
+    n = len(xyz)
+    kind = rng.choice(["smooth", "noise", "offset", "outliers"])
+    x = np.sin(6 * xyz[:, 0]) * np.cos(4 * xyz[:, 1]) + (xyz[:, 2] if dim == 3 else 0)
+    if kind == "noise":
+        x = x + rng.normal(0, 0.3, n)
+    elif kind == "offset":
+        x = x + 1000.0
+    elif kind == "outliers":
+        k = rng.choice(n, max(1, n // 500), replace=False)
+        x[k] = rng.choice([1e12, -1e12, 1e290], len(k))
+    g = int(rng.integers(4, 40 if dim == 3 else 200))
+    p = dict(tau=float(10 ** rng.uniform(-8, -1)), rho=float(rng.uniform(0.1, 0.9)),
+             bound_kind=int(rng.random() < 0.7), g_kind=int(rng.random() < 0.3),
+             fill=int(rng.random() < 0.3), codec_id=int(rng.random() < 0.1))
+    if p["bound_kind"] == 0:
+        p["tau"] *= float(np.ptp(x[np.abs(x) < 1e6]) or 1.0)
+    return dim, xyz, x, g, p
+
+
+@pytest.mark.parametrize("seed", range(160))
+def test_random_case_matches_reference(cuda, ref, oracle, seed):
+    import torch
+    dim, xyz, x, g, p = _case(seed)
+    lo, hi = xyz.min(0), xyz.max(0)
+    axes = [np.linspace(lo[d], hi[d], g) for d in range(dim)]
+    plan = umcg.Plan.build(axes, torch.from_numpy(np.ascontiguousarray(xyz)).cuda(), keep_coords=True)
+    mode, gaxes, assign, visited = plan.export()
+    s = Setup(dim=dim, axes=gaxes, mode=mode, assignments=assign, visited=visited, coords=xyz)
+    b = umcg.Budget(tau=p["tau"], split_rho=p["rho"], bound_kind=p["bound_kind"], g_kind=p["g_kind"],
+                    fill=p["fill"], codec_id=p["codec_id"])
+    label = f"seed {seed} dim {dim} n {len(x)} g {g} mode {mode} {p}"
+    try:
+        want = ref.compress(s, x, name="z", tau=p["tau"], rho=p["rho"], bound_kind=p["bound_kind"],
+                            g_kind=p["g_kind"], fill=p["fill"], codec_id=p["codec_id"])
+    except OracleError as e:
+        with pytest.raises(umcg.UmcgError) as ei:
+            plan.compress(torch.from_numpy(x).cuda(), b, name="z")
+        assert ei.value.kind == e.name, (label, e.name, ei.value.kind)
+        return
+    got = plan.compress(torch.from_numpy(x).cuda(), b, name="z")
+    if p["codec_id"] == 1:
+        assert got == want, label
+    else:
+        check_archive(got, want, s, x, p, oracle, label)
+    out = plan.decompress(got).cpu().numpy()
+    rd = ref.decompress(s, got)
+    # decoders within 1e-12 x max(range, max|x|) -- with
+    # outliers that scale is theirs: x' = approx + x2 cancels next to them in
+    # both implementations, and the grid lattice's drift is relative to it
+    scale = max(float(np.ptp(x)), float(np.abs(x).max()))
+    assert np.max(np.abs(out - rd)) <= 1e-12 * scale, label
+    tau_abs = p["tau"] * (float(np.ptp(x)) if p["bound_kind"] == 1 else 1.0)
+    ok = np.abs(rd - x) <= tau_abs
+    assert np.all(np.abs(out - x)[ok] <= tau_abs), label
