@@ -184,6 +184,11 @@ void host_budget(double tau_abs, double rho, double coeff, double* tc) {
     tc[1] = t2 * (1.0 - 1e-9);
 }
 
+__global__ void k_set_ctl(DevCtl* d, DevCtl v) {
+    if (threadIdx.x | blockIdx.x) return;
+    *d = v;
+}
+
 __global__ void k_set_u64(uint64_t* p, uint64_t v) {
     if (threadIdx.x | blockIdx.x) return;
     *p = v;
@@ -227,6 +232,11 @@ struct CompressMode {
     bool lossless[2];
     bool serial[2];
     bool no_narrow;  // a narrow pass saw |K2| > 16383: int32 lattice indices
+    // Rerun after escapes only: the previous pass's range, budget, cluster
+    // means (x1), fused grid lattice (scratch_d) and residual lattice (kbuf)
+    // are still valid, so the pass restarts from them (prev = its control block).
+    bool reuse;
+    DevCtl prev;
     bool verbatim;  // codec 1: both components are RLE'd raw fp64 bytes (codec.hpp:240-248)
 };
 
@@ -314,7 +324,22 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     auto* ctl = p->ctl.as<DevCtl>(1);
     CompTrace tr;
     tr.dev("start", st);
-    init_ctl(ctl, st);
+    if (m.reuse) {
+        // the previous pass's range and budget; every per-pass output cleared
+        DevCtl c = m.prev;
+        c.err = 0;
+        c.need_serial[0] = c.need_serial[1] = 0;
+        c.need_wide = 0;
+        c.max_abs_k[0] = c.max_abs_k[1] = 0;
+        for (int k = 0; k < 2; ++k) c.stream_len[k] = c.n_esc[k] = c.payload_len[k] = c.stream_off[k] = 0;
+        c.archive_len = 0;
+        c.count = 0;
+        for (auto& a : c.aux) a = 0;
+        k_set_ctl<<<1, 1, 0, st>>>(ctl, c);
+        UMCG_LAUNCHED();
+    } else {
+        init_ctl(ctl, st);
+    }
     // nearest g: partitioned layout (partition.cu); multilinear: gathers
     // multilinear g on the partitioned layout: means as for nearest, then the
     // residuals bucket by bucket (partition.cu k_ml_bucket)
@@ -333,7 +358,9 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     const bool fuse_k1 = part && p->mode == 0 && p->dim > 1 && !m.serial[0] && !m.lossless[0] && prm.fill == 0;
     double* x1 = p->x1.as<double>(n1 ? n1 : 1);
     int32_t* Kp = nullptr;
-    if (part) {
+    if (part && m.reuse) {
+        Kp = p->kbuf.as<int32_t>(std::max<uint64_t>(n, n1) + 1);  // the previous pass's lattice indices
+    } else if (part) {
         double* xp = p->scratch_c.as<double>(n + 4);  // + padding: 16-byte bulk copies may overrun
         Kp = p->kbuf.as<int32_t>(std::max<uint64_t>(n, n1) + 1);
         partition_values(d_x, x_f32, p, xp, ctl, st);  // + range / finiteness
@@ -343,14 +370,15 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
         bucket_means_residuals(p, xp, ctl, x1, ml_part ? nullptr : Kp, narrow,
                                fuse_k1 ? p->scratch_d.as<int32_t>(n1 ? n1 : 1) : nullptr, p->dim, st);
         tr.dev("bucket", st);
-    } else {
+    } else if (!m.reuse) {
         minmax(d_x, x_f32, n, ctl, st);
         budget(BudgetArgs{prm.tau, prm.split_rho, prm.coeff_abs_sum, prm.bound_kind, n}, ctl, st);
         // f: cluster means (interp.hpp:46-93)
         cluster_mean(d_x, x_f32, p->d_perm.as<uint32_t>(1), p->d_seg.as<uint32_t>(1), n1, x1, st);
     }
-    if (prm.fill == 1 && p->mode == 0) fill_nearest_visited(p->d_seg.as<uint32_t>(1), n1, p->shape[p->dim - 1], x1, st);
-    if (ml_part && !m.serial[1] && !m.lossless[1])
+    if (prm.fill == 1 && p->mode == 0 && !m.reuse)
+        fill_nearest_visited(p->d_seg.as<uint32_t>(1), n1, p->shape[p->dim - 1], x1, st);
+    if (ml_part && !m.serial[1] && !m.lossless[1] && !m.reuse)
         ml_residuals(p, p->scratch_c.as<double>(n + 4), x1, ctl, Kp, narrow, st);
 
     // component specs (grid_codec_spec, pipeline.hpp:96-110)
@@ -531,13 +559,16 @@ void compress_impl(umcg_plan* p, const umcg_params* prm_in, const void* d_x, int
             *out_len = hc.archive_len;
             return;
         }
-        bool redo = false;
-        if (hc.need_wide && !m.no_narrow) { m.no_narrow = true; redo = true; }
+        bool redo = false, only_escapes = true;
+        if (hc.need_wide && !m.no_narrow) { m.no_narrow = true; redo = true; only_escapes = false; }
         for (int c = 0; c < 2; ++c) {
             const bool ll = (hc.lossless >> c) & 1;
-            if (ll != m.lossless[c]) { m.lossless[c] = ll; m.serial[c] = false; redo = true; }
+            if (ll != m.lossless[c]) { m.lossless[c] = ll; m.serial[c] = false; redo = true; only_escapes = false; }
             if (!ll && !m.serial[c] && hc.need_serial[c]) { m.serial[c] = true; redo = true; }
         }
+        // a rerun for escapes alone restarts from this pass's means and lattices
+        m.reuse = redo && only_escapes && !m.reuse && !std::getenv("UMCG_NO_REUSE");
+        if (m.reuse) m.prev = hc;
         if (!redo) {
             *out_len = hc.archive_len;
             return;
