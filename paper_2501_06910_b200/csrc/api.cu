@@ -417,7 +417,8 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     double* esc_val[2] = {nullptr, nullptr};
     // Common case: the grid component's chain (codes, stream plan, write) runs
     // on a side stream beside the residual's; they share only the layout step.
-    const bool overlap = part && !m.serial[0] && !m.serial[1] && !m.lossless[0] && !m.lossless[1];
+    const bool overlap = part && !m.serial[0] && !m.serial[1] && !m.lossless[0] && !m.lossless[1] &&
+                         !std::getenv("UMCG_NO_OVERLAP");  // (A/B knob)
     // (normal priority: on the high-priority stream the grid chain finishes
     // early but k_resid_codes slows by as much -- UMCG_COMP_TRACE)
     cudaStream_t sg = st;
@@ -458,10 +459,10 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
         DevBuf& eb = c == 0 ? p->enc1 : p->enc2;
         es[c] = stream_enc_carve(eb.reserve(stream_enc_scratch_bytes(ncode[c])), ncode[c]);
     }
-    const bool fused_resid = part && !m.serial[1] && !m.lossless[1];
+    bool fused_resid = part && !m.serial[1] && !m.lossless[1];
     if (fused_resid) {
-        // q = K2_i - K2_{i-1} back in vertex order + RLE tile summaries (partition.cu)
-        resid_codes_tiles(p, Kp, codes[1], narrow, es[1], st);
+        // q = K2_i - K2_{i-1} back in vertex order (+ RLE tile summaries, partition.cu)
+        fused_resid = resid_codes_tiles(p, Kp, codes[1], narrow, es[1], st);
         tr.dev("resid codes", st);
     } else if (!m.serial[1] && !m.lossless[1]) {
         codes_lossy_residual(rs, n, ctl, static_cast<uint32_t*>(codes[1]), st);
@@ -471,6 +472,7 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     for (int c = 0; c < 2; ++c) {
         cudaStream_t sc = c == 0 ? sg : st;
         if (c == 1 && fused_resid) stream_plan_from_sums(ncode[c], es[c], ctl, c, sc);
+        else if (c == 1 && narrow) stream_plan_u16(static_cast<uint16_t*>(codes[c]), ncode[c], es[c], ctl, c, sc);
         else if (wide[c]) stream_plan_u64(static_cast<uint64_t*>(codes[c]), ncode[c], es[c], ctl, c, sc);
         else stream_plan_u32(static_cast<uint32_t*>(codes[c]), ncode[c], es[c], ctl, c, sc);
     }
@@ -1367,7 +1369,7 @@ umcg_status umcg_plan_clone(const umcg_plan* src, umcg_plan** out) {
                        &umcg_plan::d_axes, &umcg_plan::d_axis_off, &umcg_plan::d_inv_cell, &umcg_plan::d_coords,
                        &umcg_plan::d_srcE, &umcg_plan::d_dstE, &umcg_plan::d_ech, &umcg_plan::d_bct,
                        &umcg_plan::d_regular, &umcg_plan::d_lnode, &umcg_plan::d_lperm, &umcg_plan::d_lslot,
-                       &umcg_plan::d_bk})
+                       &umcg_plan::d_rPt, &umcg_plan::d_rLt, &umcg_plan::d_bk})
             ((*c).*m).alias((*o).*m);
         o->refs.fetch_add(1);
         c->origin = o;

@@ -40,6 +40,150 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_tiles(const T* __restrict__
     if (threadIdx.x == 0) sums[tile] = tot;
 }
 
+// Phase 1 with the fast tile summary: a tile with no zero run of >=
+// kMinZeroRun codes strictly inside has the summary {lz, tz, fb = code bytes
+// from its first to its last nonzero} (the composition of its thread
+// summaries has no interior pieces, common.cuh rle_compose), which three warp
+// reductions give. Such a run either fills one thread's ENC_ITEMS codes or
+// ends at a thread's first nonzero after lz >= 1 zeros that continue >= 8 - lz
+// codes into the previous thread; tiles with either (and the partial last
+// tile) take the exact RleSum block reduction of k_rle_tiles.
+constexpr int FT = 4;  // tiles per CTA of k_rle_tiles_fast: every code load in flight up front
+template <class T>
+__global__ void __launch_bounds__(ENC_THREADS) k_rle_tiles_fast(const T* __restrict__ codes, uint64_t n,
+                                                                RleSum* __restrict__ sums,
+                                                                uint32_t* __restrict__ redo,
+                                                                uint32_t* __restrict__ n_redo) {
+    static_assert(ENC_ITEMS == 8, "8-bit zero masks");
+    constexpr int NW = ENC_THREADS / 32;
+    __shared__ uint32_t wpart[FT][NW][4];  // per warp: code bytes, first / last nonzero, any bad
+    const uint64_t T_ = (n + ENC_TILE - 1) / ENC_TILE;
+    const uint64_t tile0 = (uint64_t)blockIdx.x * FT;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // u16 codes of a full thread stay packed: SIMD halfword compares give the
+    // zero mask and the varint byte count (clen: 1 + (v >= 0x80) + (v >= 0x4000))
+    constexpr bool P16 = sizeof(T) == 2;
+    T v[FT][P16 ? 1 : ENC_ITEMS];
+    uint4 pw[FT];
+    int cnt[FT];
+#pragma unroll
+    for (int t = 0; t < FT; ++t) {
+        cnt[t] = 0;
+        const uint64_t first = (tile0 + t) * ENC_TILE + (uint64_t)threadIdx.x * ENC_ITEMS;
+        if (tile0 + t >= T_) continue;
+        if constexpr (P16) {
+            if (first + ENC_ITEMS <= n) {
+                pw[t] = __ldg(reinterpret_cast<const uint4*>(codes + first));
+                cnt[t] = ENC_ITEMS;
+            } else {
+                uint32_t w[4] = {0, 0, 0, 0};
+                for (int k = 0; k < ENC_ITEMS; ++k)
+                    if (first + k < n) {
+                        w[k >> 1] |= (uint32_t)codes[first + k] << (16 * (k & 1));
+                        cnt[t] = k + 1;
+                    }
+                pw[t] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+        } else {
+            cnt[t] = load_items(codes, n, first, v[t]);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < FT; ++t) {
+        const uint64_t tile = tile0 + t;
+        if (tile >= T_) break;
+        uint32_t zm = 0, bytes = 0;
+        if constexpr (P16) {
+            const uint32_t w[4] = {pw[t].x, pw[t].y, pw[t].z, pw[t].w};
+            uint32_t g = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t e = __vcmpeq2(w[i], 0u);
+                zm |= ((e & 1u) | ((e >> 15) & 2u)) << (2 * i);
+                g += __popc(__vcmpgeu2(w[i], 0x00800080u)) + __popc(__vcmpgeu2(w[i], 0x40004000u));
+            }
+            const uint32_t valid = (1u << cnt[t]) - 1u;
+            zm &= valid;  // (padding halfwords of a partial thread are 0: excluded here, and bad below)
+            bytes = (uint32_t)cnt[t] + g / 16;
+        } else {
+#pragma unroll
+            for (int k = 0; k < ENC_ITEMS; ++k) {
+                zm |= (k < cnt[t] && v[t][k] == 0) ? 1u << k : 0u;
+                bytes += k < cnt[t] ? clen(v[t][k]) : 0u;
+            }
+        }
+        const uint32_t lz = zm == 0xffu ? 8u : (uint32_t)(__ffs(~zm) - 1);
+        const uint32_t tzr = (zm & 0x80u) ? (uint32_t)__clz(~(zm << 24)) : 0u;
+        uint32_t tz_prev = __shfl_up_sync(0xffffffffu, tzr, 1);
+        if (lane == 0 && threadIdx.x > 0 && lz > 0 && lz < 8 && cnt[t] == ENC_ITEMS) {
+            // the previous thread's codes (previous warp): trailing zeros
+            const T* pc = codes + tile * ENC_TILE + (uint64_t)threadIdx.x * ENC_ITEMS - ENC_ITEMS;
+            tz_prev = 0;
+            for (int k = ENC_ITEMS - 1; k >= 0 && pc[k] == 0; --k) ++tz_prev;
+        }
+        const bool bad = cnt[t] < ENC_ITEMS || zm == 0xffu ||
+                         (threadIdx.x > 0 && lz > 0 && tz_prev + lz >= kMinZeroRun) || tile == T_ - 1;
+        const uint32_t fnz = zm != 0xffu ? threadIdx.x * ENC_ITEMS + lz : 0xffffffffu;
+        const uint32_t lnz = zm != 0xffu ? threadIdx.x * ENC_ITEMS + 7u - tzr : 0u;
+        const uint32_t wb = __reduce_add_sync(0xffffffffu, bytes);
+        const uint32_t wf = __reduce_min_sync(0xffffffffu, fnz);
+        const uint32_t wl = __reduce_max_sync(0xffffffffu, lnz);
+        const uint32_t wx = __any_sync(0xffffffffu, bad);
+        if (lane == 0) {
+            wpart[t][warp][0] = wb;
+            wpart[t][warp][1] = wf;
+            wpart[t][warp][2] = wl;
+            wpart[t][warp][3] = wx;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < FT && tile0 + threadIdx.x < T_) {
+        const int t = threadIdx.x;
+        const uint64_t tile = tile0 + t;
+        uint32_t tb = 0, f = 0xffffffffu, l = 0, bad = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            tb += wpart[t][w][0];
+            f = min(f, wpart[t][w][1]);
+            l = max(l, wpart[t][w][2]);
+            bad |= wpart[t][w][3];
+        }
+        if (bad) {
+            redo[atomicAdd(n_redo, 1u)] = (uint32_t)tile;
+        } else {
+            RleSum S;
+            S.lz = f;
+            S.tz = (uint64_t)(ENC_TILE - 1 - l);
+            S.fb = (uint64_t)(tb - f - (ENC_TILE - 1 - l));
+            S.lb = S.mid = 0;
+            S.origin = (uint32_t)tile;
+            S.flags = 0u;
+            sums[tile] = S;
+        }
+    }
+}
+
+// The exact summaries of the listed tiles (grid-stride: the count is on the device).
+template <class T>
+__global__ void __launch_bounds__(ENC_THREADS) k_rle_tiles_redo(const T* __restrict__ codes, uint64_t n,
+                                                                RleSum* __restrict__ sums,
+                                                                const uint32_t* __restrict__ redo,
+                                                                const uint32_t* __restrict__ n_redo) {
+    using BR = cub::BlockReduce<RleSum, ENC_THREADS>;
+    __shared__ typename BR::TempStorage tmp;
+    const uint32_t cnt = *n_redo;
+    for (uint32_t i = blockIdx.x; i < cnt; i += gridDim.x) {
+        const uint64_t tile = redo[i];
+        const uint64_t first = tile * ENC_TILE + (uint64_t)threadIdx.x * ENC_ITEMS;
+        T v[ENC_ITEMS];
+        const int c = load_items(codes, n, first, v);
+        const RleSum s = thread_summary(v, c, (uint32_t)tile);
+        const RleSum tot = BR(tmp).Reduce(s, RleComposeOp());
+        if (threadIdx.x == 0) sums[tile] = tot;
+        __syncthreads();
+    }
+}
+
 constexpr int CH = 256;  // tiles per chunk
 
 // Phase 2: chunk aggregates of CH tile summaries.
@@ -287,13 +431,11 @@ __global__ void __launch_bounds__(ENC_THREADS, UMCG_WF_MINB) k_rle_write_fast(co
 //   4. prefix of unit bytes U_j              -> output positions
 // (literals still open at the tile end take T from lit_total[tile]).
 template <class T>
-__global__ void __launch_bounds__(ENC_THREADS, 6) k_rle_write_general(const T* __restrict__ codes, uint64_t n,
-                                                           const RleState* __restrict__ states,
-                                                           const RleSum* __restrict__ sums,
-                                                           const uint64_t* __restrict__ lit_total,
-                                                           const DevCtl* __restrict__ ctl, int comp, const uint32_t* __restrict__ glist,
-                                                           const uint64_t* __restrict__ tpos,
-                                                           uint8_t* __restrict__ dst, int off_from_ctl) {
+__device__ __forceinline__ void general_tile(const uint64_t tile, const T* __restrict__ codes, uint64_t n,
+                                             const RleState* __restrict__ states, const RleSum* __restrict__ sums,
+                                             const uint64_t* __restrict__ lit_total, const DevCtl* __restrict__ ctl,
+                                             int comp, const uint64_t* __restrict__ tpos, uint8_t* __restrict__ dst,
+                                             int off_from_ctl) {
     constexpr uint32_t CAP = ENC_TILE * (sizeof(T) == 8 ? 10 : 5) + 96;
     constexpr int NONE = 0x7fffffff;
     using BSi = cub::BlockScan<int, ENC_THREADS>;
@@ -306,8 +448,6 @@ __global__ void __launch_bounds__(ENC_THREADS, 6) k_rle_write_general(const T* _
     __shared__ int sfx[ENC_THREADS];
     __shared__ __align__(16) uint8_t out[CAP];
 
-    if (blockIdx.x >= (uint32_t)ctl->aux[4 + comp]) return;
-    const uint64_t tile = glist[blockIdx.x];
     const uint64_t T_ = (n + ENC_TILE - 1) / ENC_TILE;
     const bool last = tile == T_ - 1;
     const RleState E = states[tile];
@@ -439,6 +579,24 @@ __global__ void __launch_bounds__(ENC_THREADS, 6) k_rle_write_general(const T* _
     copy_out16(out, ao, len, d);
 }
 
+// Grid-stride over the general tiles (their count is on the device): a
+// launch per tile of the stream would start and retire a CTA for every
+// fast tile as well (~36 us at config 3).
+template <class T>
+__global__ void __launch_bounds__(ENC_THREADS, 6) k_rle_write_general(const T* __restrict__ codes, uint64_t n,
+                                                           const RleState* __restrict__ states,
+                                                           const RleSum* __restrict__ sums,
+                                                           const uint64_t* __restrict__ lit_total,
+                                                           const DevCtl* __restrict__ ctl, int comp, const uint32_t* __restrict__ glist,
+                                                           const uint64_t* __restrict__ tpos,
+                                                           uint8_t* __restrict__ dst, int off_from_ctl) {
+    const uint32_t cnt = (uint32_t)ctl->aux[4 + comp];
+    for (uint32_t i = blockIdx.x; i < cnt; i += gridDim.x) {
+        general_tile<T>(glist[i], codes, n, states, sums, lit_total, ctl, comp, tpos, dst, off_from_ctl);
+        __syncthreads();
+    }
+}
+
 }  // namespace
 
 size_t stream_enc_scratch_bytes(uint64_t n) {
@@ -461,6 +619,8 @@ StreamEncScratch stream_enc_carve(void* base, uint64_t n) {
     s.pos = reinterpret_cast<uint64_t*>(p);
     p += T * sizeof(uint64_t);
     s.glist = reinterpret_cast<uint32_t*>(p);
+    p += T * sizeof(uint32_t);
+    s.n_redo = reinterpret_cast<uint32_t*>(p);  // inside the scratch's 4096-byte slack
     return s;
 }
 
@@ -473,7 +633,21 @@ static void plan_impl(const T* codes, uint64_t n, const StreamEncScratch& s, Dev
     }
     const uint64_t C = cdiv(T_, CH);
     UMCG_CUDA(cudaMemsetAsync(&ctl->aux[4 + comp], 0, 8, st));
+#ifdef UMCG_RLE_TILES_EXACT  // (A/B: the exact RleSum reduction on every tile)
     k_rle_tiles<T><<<(unsigned)T_, ENC_THREADS, 0, st>>>(codes, n, s.sums);
+#else
+    // the tile list doubles as the redo list (k_rle_states fills it afterwards)
+    UMCG_CUDA(cudaMemsetAsync(s.n_redo, 0, 4, st));
+    k_rle_tiles_fast<T><<<(unsigned)cdiv(T_, (uint64_t)FT), ENC_THREADS, 0, st>>>(codes, n, s.sums, s.glist, s.n_redo);
+    UMCG_LAUNCHED();
+    {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        k_rle_tiles_redo<T><<<(unsigned)std::min<uint64_t>(T_, (uint64_t)sms * 4), ENC_THREADS, 0, st>>>(
+            codes, n, s.sums, s.glist, s.n_redo);
+    }
+#endif
     UMCG_LAUNCHED();
     k_rle_chunks<<<(unsigned)C, CH, 0, st>>>(s.sums, T_, s.csum);
     UMCG_LAUNCHED();
@@ -510,7 +684,11 @@ static void write_impl(const T* codes, uint64_t n, const StreamEncScratch& s, De
     k_rle_write_fast<T><<<(unsigned)T_, ENC_THREADS, 0, st>>>(codes, n, s.states, s.sums, s.lit_total, s.pos, ctl,
                                                               comp, dst, off_ctl ? 1 : 0);
     UMCG_LAUNCHED();
-    k_rle_write_general<T><<<(unsigned)T_, ENC_THREADS, 0, st>>>(codes, n, s.states, s.sums, s.lit_total, ctl,
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned gg = (unsigned)std::min<uint64_t>(T_, (uint64_t)sms * 6);
+    k_rle_write_general<T><<<gg, ENC_THREADS, 0, st>>>(codes, n, s.states, s.sums, s.lit_total, ctl,
                                                                  comp, s.glist, s.pos, dst, off_ctl ? 1 : 0);
     UMCG_LAUNCHED();
 }
@@ -518,6 +696,8 @@ static void write_impl(const T* codes, uint64_t n, const StreamEncScratch& s, De
 void stream_plan_u32(const uint32_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
                      cudaStream_t st) { plan_impl(c, n, s, ctl, comp, st); }
 void stream_plan_u64(const uint64_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
+                     cudaStream_t st) { plan_impl(c, n, s, ctl, comp, st); }
+void stream_plan_u16(const uint16_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
                      cudaStream_t st) { plan_impl(c, n, s, ctl, comp, st); }
 void stream_write_u32(const uint32_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
                       uint8_t* dst, bool o, cudaStream_t st) { write_impl(c, n, s, ctl, comp, dst, o, st); }

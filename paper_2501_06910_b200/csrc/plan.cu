@@ -138,6 +138,11 @@ __global__ void k_dstE(const uint32_t* __restrict__ L, uint64_t n, uint32_t* __r
     if (p < n) dstE[L[p]] = (uint32_t)p;
 }
 
+__global__ void k_rlt(const uint32_t* __restrict__ keys, uint64_t n, uint16_t* __restrict__ rLt) {
+    const uint64_t k = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (k < n) rLt[k] = (uint16_t)(keys[k] & (kRTile - 1));
+}
+
 // per-epoch exclusive scan of bucket counts (one thread per epoch; E*B small)
 __global__ void k_epoch_offsets(const uint32_t* __restrict__ cnt, uint64_t E, uint64_t B, uint32_t* __restrict__ ech) {
     const uint64_t e = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
@@ -356,6 +361,21 @@ void plan_build_buckets(umcg_plan* p, cudaStream_t st) {
     UMCG_CUDA(cub::DeviceRadixSort::SortPairs(t, tb, kk, ks, io, srcE, (int)n, 0, end_bit, st));
     k_dstE<<<blocks(n), THREADS, 0, st>>>(srcE, n, p->d_dstE.as<uint32_t>(n));
     UMCG_LAUNCHED();
+    // vertex tiles: stable sort of the layout-E positions by the tile of their
+    // vertex (bits kRTileBits.. of srcE) keeps each tile's positions ascending
+    {
+        k_iota<<<blocks(n), THREADS, 0, st>>>(io, n);
+        UMCG_LAUNCHED();
+        int hi = kRTileBits + 1;
+        while (hi < 32 && (1ull << hi) < n) ++hi;
+        uint32_t* rPt = p->d_rPt.as<uint32_t>(n);
+        tb = 0;
+        UMCG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, srcE, ks, io, rPt, (int)n, (int)kRTileBits, hi, st));
+        t = scratch.reserve(std::max(tb, scratch.capacity()));
+        UMCG_CUDA(cub::DeviceRadixSort::SortPairs(t, tb, srcE, ks, io, rPt, (int)n, (int)kRTileBits, hi, st));
+        k_rlt<<<blocks(n), THREADS, 0, st>>>(ks, n, p->d_rLt.as<uint16_t>(n));
+        UMCG_LAUNCHED();
+    }
     k_epoch_offsets<<<blocks(E), THREADS, 0, st>>>(ec, E, B, p->d_ech.as<uint32_t>(E * (B + 1)));
     UMCG_LAUNCHED();
     k_bucket_chunks<<<blocks(B), THREADS, 0, st>>>(p->d_ech.as<uint32_t>(1), E, B, p->d_bct.as<uint2>(B * (E + 1)));

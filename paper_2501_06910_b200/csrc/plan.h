@@ -55,6 +55,12 @@ struct umcg_plan {
     umcg::DevBuf d_lperm;    // u16 [n]    bucket-local element of node-sorted position
     umcg::DevBuf d_lslot;    // u16 [n]    shared-memory slot of node-sorted position (TMA staging)
     umcg::DevBuf d_bk;       // u32 [2*(B+1)] bucket start (vertex) and first slot
+    // vertex tiles of kRTile consecutive vertices (k_resid_codes): the
+    // layout-E positions of a tile's vertices in ascending order -- runs of
+    // consecutive positions, one per bucket chunk the tile meets -- and the
+    // tile-local vertex of each
+    umcg::DevBuf d_rPt;      // u32 [n]
+    umcg::DevBuf d_rLt;      // u16 [n]
     // clones (umcg_plan_clone) alias the static arrays above of their origin;
     // the origin is freed when it and all of its clones are destroyed
     umcg_plan* origin = nullptr;
@@ -84,6 +90,11 @@ constexpr uint32_t kBucketCap = 4096;   // vertices per bucket (smem staging)
 constexpr uint64_t kEpoch = 1ull << 22;  // vertices per epoch of layout E
 constexpr uint32_t kMaxEpochs = 2048;    // k_bucket stages per-epoch chunk prefixes
 constexpr uint32_t kBucketNodes = 1016; // slots per bucket
+#ifndef UMCG_RTILE_BITS
+#define UMCG_RTILE_BITS 15
+#endif
+constexpr uint32_t kRTileBits = UMCG_RTILE_BITS;
+constexpr uint32_t kRTile = 1u << kRTileBits;  // vertices per k_resid_codes tile (a multiple of ENC_TILE)
 void plan_build_buckets(umcg_plan* p, cudaStream_t st);
 
 // Component payload decode (codec.hpp:364-441) of a payload in device memory
@@ -111,7 +122,9 @@ void partition_values(const void* x, int x_f32, umcg_plan* p, double* xp, DevCtl
 // fused (D1 = grid rank).
 void bucket_means_residuals(umcg_plan* p, const double* xp, DevCtl* ctl, double* x1, void* Kp, bool narrow,
                             int32_t* K1, int D1, cudaStream_t st);
-void resid_codes_tiles(umcg_plan* p, const void* Kp, void* codes, bool narrow, const StreamEncScratch& s,
+// Returns whether the RLE tile summaries were written too (else the caller
+// runs the stream plan over the codes).
+bool resid_codes_tiles(umcg_plan* p, const void* Kp, void* codes, bool narrow, const StreamEncScratch& s,
                        cudaStream_t st);
 // Multilinear g in bucket order (layout E): residual lattice indices KE
 // (compress) and the recomposition x' = g + x2' (decompress, gE [n] scratch).

@@ -7,10 +7,10 @@ R=$(cd "$(dirname "$0")/.." && pwd)
 O=$R/variants/$name
 mkdir -p $O
 objs=""
-for src in encode partition stream codes decode interp plan api datagen gridinit; do
-  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 --expt-relaxed-constexpr "$@" -c $R/paper_2501_06910_b200/csrc/$src.cu -o $O/$src.o &
+for src in $(cd $R/paper_2501_06910_b200/csrc && ls *.cu | sed 's/\.cu$//'); do
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 -Xcompiler -fopenmp --expt-relaxed-constexpr "$@" -c $R/paper_2501_06910_b200/csrc/$src.cu -o $O/$src.o &
   objs="$objs $O/$src.o"
 done
 wait
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $O/libumcg.so $objs -lcudart
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $O/libumcg.so $objs -lcudart -lgomp
 echo built variants/$name
