@@ -90,13 +90,12 @@ __device__ __forceinline__ void stage_tile(const uint8_t* __restrict__ U, uint64
 // codes are zigzag(int32) < 2^32 (codec.hpp:305, 322), so values are
 // accumulated in 32 bits; a longer varint sets *wide and the caller falls
 // back to the general decoder.
+// W: the thread's 48-byte window, 16 halo bytes then its 32 bytes, as words.
 template <class F>
-__device__ __forceinline__ void thread_walk(const uint8_t* sb, int my, int64_t gbase, uint64_t ulen, bool* bad,
+__device__ __forceinline__ void thread_walk(const uint32_t (&W)[12], int64_t gbase, uint64_t ulen, bool* bad,
                                             bool* wide, F&& emit) {
-    const uint4* p = reinterpret_cast<const uint4*>(sb + my - 16);
-    const uint4 h = p[0], a = p[1], b = p[2];
-    const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
-    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    const uint32_t hw[4] = {W[0], W[1], W[2], W[3]};
+    const uint32_t w[8] = {W[4], W[5], W[6], W[7], W[8], W[9], W[10], W[11]};
     // continuation bytes immediately before my first byte
     int hlen = 0;
     bool run = true;
@@ -158,18 +157,11 @@ __device__ __forceinline__ uint32_t ends4(uint32_t x) {
 // code rather than per byte. Returns false -- having emitted nothing -- when
 // the general walk must run instead (long codes, end padding, corruption).
 template <class F>
-__device__ __forceinline__ bool thread_walk_fast(const uint8_t* sb, int my, F&& emit) {
-    const uint4* p = reinterpret_cast<const uint4*>(sb + my - 16);
-    const uint32_t h3 = p[0].w;  // the 4 bytes before mine
+__device__ __forceinline__ bool thread_walk_fast(const uint32_t (&W)[12], F&& emit) {
+    const uint32_t h3 = W[3];  // the 4 bytes before mine
     uint32_t w[RB / 4];
 #pragma unroll
-    for (int q = 0; q < RB / 16; ++q) {
-        const uint4 a = p[1 + q];
-        w[4 * q] = a.x;
-        w[4 * q + 1] = a.y;
-        w[4 * q + 2] = a.z;
-        w[4 * q + 3] = a.w;
-    }
+    for (int q = 0; q < RB / 4; ++q) w[q] = W[4 + q];
     uint64_t E = ends4(h3);  // bit i: byte i - 4 ends a code
 #pragma unroll
     for (int q = 0; q < RB / 4; ++q) E |= (uint64_t)ends4(w[q]) << (4 + 4 * q);
@@ -194,6 +186,60 @@ __device__ __forceinline__ bool thread_walk_fast(const uint8_t* sb, int my, F&& 
     return true;
 }
 
+__device__ __forceinline__ void smem_window(const uint8_t* sb, int my, uint32_t (&W)[12]) {
+    const uint4* p = reinterpret_cast<const uint4*>(sb + my - 16);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const uint4 a = p[q];
+        W[4 * q] = a.x;
+        W[4 * q + 1] = a.y;
+        W[4 * q + 2] = a.z;
+        W[4 * q + 3] = a.w;
+    }
+}
+
+// The same window straight from global memory (no shared-memory staging: the
+// L1 it leaves serves the random K1 gathers of k_dec_out): stream bytes
+// [g - 16, g + 32) from 16-byte aligned loads realigned with funnel shifts,
+// then the padding of stage_tile (before the stream 0x00, past its end 0x80).
+__device__ __forceinline__ void global_window(const uint8_t* __restrict__ U, uint64_t ulen, int64_t g,
+                                              uint64_t pol, uint32_t (&W)[12]) {
+    const intptr_t A = (intptr_t)U + g - 16;
+    const intptr_t a0 = A & ~(intptr_t)15;
+    const int sh = (int)(A - a0);
+    const intptr_t g_lo = (intptr_t)U & ~(intptr_t)15;
+    const intptr_t g_hi = ((intptr_t)U + (intptr_t)ulen + 15) & ~(intptr_t)15;
+    uint32_t r[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const intptr_t c = a0 + 16 * q;
+        uint4 x = make_uint4(0, 0, 0, 0);
+        if ((q < 3 || sh) && c >= g_lo && c < g_hi) x = ld_v4_hint(reinterpret_cast<const void*>(c), pol);
+        r[4 * q] = x.x;
+        r[4 * q + 1] = x.y;
+        r[4 * q + 2] = x.z;
+        r[4 * q + 3] = x.w;
+    }
+    const int ws = sh >> 2, bs = 8 * (sh & 3);
+#pragma unroll
+    for (int m = 0; m < 12; ++m) {
+        uint32_t l = r[m], h = r[m + 1];
+#pragma unroll
+        for (int q = 1; q < 4; ++q)
+            if (ws == q) { l = r[m + q]; h = r[m + q + 1]; }
+        W[m] = __funnelshift_r(l, h, bs);
+    }
+    if (g - 16 < 0 || g + 32 > (int64_t)ulen) {  // first / last thread windows only
+#pragma unroll
+        for (int k = 0; k < 48; ++k) {
+            const int64_t off = g - 16 + k;
+            const uint32_t b = off < 0 ? 0x00u : 0x80u;
+            if (off < 0 || off >= (int64_t)ulen)
+                W[k >> 2] = (W[k >> 2] & ~(0xffu << (8 * (k & 3)))) | (b << (8 * (k & 3)));
+        }
+    }
+}
+
 __device__ __forceinline__ int64_t zz_dec32(uint32_t v) { return (int64_t)(v >> 1) ^ -(int64_t)(v & 1u); }
 
 __device__ __forceinline__ CS thread_counts(const uint8_t* sb, int my, bool* bad, bool* wide, int64_t base,
@@ -206,13 +252,15 @@ __device__ __forceinline__ CS thread_counts(const uint8_t* sb, int my, bool* bad
         ++c;
         s32 += (int32_t)(v >> 1) ^ -(int32_t)(v & 1u);
     };
-    if (thread_walk_fast(sb, my, f32)) return CS{c, (int64_t)s32};
+    uint32_t W[12];
+    smem_window(sb, my, W);
+    if (thread_walk_fast(W, f32)) return CS{c, (int64_t)s32};
     int64_t s = 0;
     auto f = [&](uint32_t v) {
         ++c;
         s += zz_dec32(v);
     };
-    thread_walk(sb, my, base + (my - RHALO), ulen, bad, wide, f);
+    thread_walk(W, base + (my - RHALO), ulen, bad, wide, f);
     return CS{c, s};
 }
 
@@ -262,13 +310,16 @@ __global__ void __launch_bounds__(RT, UMCG_DEC_MINB) k_dec_out(const DecSrc src,
                                                int64_t* __restrict__ P64, const DevCtl* __restrict__ kctl,
                                                const int16_t* __restrict__ K16, const CS* __restrict__ raw,
                                                const CS* __restrict__ thr) {
-    __shared__ __align__(16) uint8_t sb[RHALO + RTILE + 16];
     // lattice indices of the tile in element order, int16 (the decoded K of
     // a lossy residual stream fits; a tile that does not takes the direct
     // path below)
     __shared__ int16_t kb[MODE == DEC_P64 ? 1 : RTILE];
     // P64 mode: K - (tile prefix) as int32, written out coalesced afterwards
     __shared__ int32_t kp[MODE == DEC_P64 ? RTILE : 1];
+#ifdef UMCG_DEC_PAD  // (A/B: shared-memory footprint vs the L1 left for the K1 gathers)
+    __shared__ volatile uint8_t pad_[MODE == DEC_P64 ? 1 : UMCG_DEC_PAD];
+    if (threadIdx.x == 0) pad_[0] = 0;
+#endif
     // int32 tables: switch to the int16 copy when the grid's max|K1| (known
     // on the device only) allows -- half the L2 footprint of the gather
     const bool use16 = sizeof(KT) == 4 && K16 && kctl && kctl->max_abs_k[0] < 32768;
@@ -277,9 +328,9 @@ __global__ void __launch_bounds__(RT, UMCG_DEC_MINB) k_dec_out(const DecSrc src,
     resolve_src(src, U, ulen);
     if ((uint64_t)blockIdx.x * RTILE >= ulen) return;
     const int64_t base = (int64_t)blockIdx.x * (int64_t)RTILE;
-    stage_tile(U, ulen, base, sb);
-    __syncthreads();
     const int my = RHALO + threadIdx.x * RB;
+    uint32_t W[12];
+    global_window(U, ulen, base + threadIdx.x * RB, l2_evict_first(), W);
     // the thread's prefix inside the tile and the tile's total (k_dec_agg)
     const CS excl = thr[blockIdx.x * (uint64_t)RT + threadIdx.x];
     const CS tot = raw[blockIdx.x];
@@ -305,7 +356,7 @@ __global__ void __launch_bounds__(RT, UMCG_DEC_MINB) k_dec_out(const DecSrc src,
         }
         ++li;
     };
-    if (!thread_walk_fast(sb, my, f)) thread_walk(sb, my, base + (my - RHALO), ulen, &bad2, &wide2, f);
+    if (!thread_walk_fast(W, f)) thread_walk(W, base + (my - RHALO), ulen, &bad2, &wide2, f);
     for (int o = 16; o; o >>= 1) {
         const uint64_t b2 = __shfl_xor_sync(0xffffffffu, kmax, o);
         kmax = b2 > kmax ? b2 : kmax;
@@ -322,7 +373,7 @@ __global__ void __launch_bounds__(RT, UMCG_DEC_MINB) k_dec_out(const DecSrc src,
                 if (i < n) P64[i] = K;
                 ++li;
             };
-            if (!thread_walk_fast(sb, my, g)) thread_walk(sb, my, base + (my - RHALO), ulen, &b3, &w3, g);
+            if (!thread_walk_fast(W, g)) thread_walk(W, base + (my - RHALO), ulen, &b3, &w3, g);
             return;
         }
         const uint32_t cnt = (uint32_t)tot.cnt;
@@ -358,7 +409,7 @@ __global__ void __launch_bounds__(RT, UMCG_DEC_MINB) k_dec_out(const DecSrc src,
             if (i < n) recompose(i, K);
             ++li;
         };
-        if (!thread_walk_fast(sb, my, g)) thread_walk(sb, my, base + (my - RHALO), ulen, &b3, &w3, g);
+        if (!thread_walk_fast(W, g)) thread_walk(W, base + (my - RHALO), ulen, &b3, &w3, g);
         return;
     }
     const uint32_t cnt = (uint32_t)tot.cnt;

@@ -23,7 +23,6 @@
 
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
-#include <cub/warp/warp_reduce.cuh>
 
 #include "encode_dev.cuh"
 #include "multilinear.cuh"
@@ -813,34 +812,25 @@ __global__ void __launch_bounds__(ENC_THREADS) k_resid_codes(const uint32_t* __r
 // are gathered in ascending layout-E order (plan rPt: a tile meets each
 // bucket chunk in a run of consecutive positions, so a warp's 32 loads share
 // sectors), scattered into shared memory by tile-local vertex (rLt), and the
-// codes q_i = K_i - K_{i-1} leave in vertex order with the RLE summary of
-// every ENC_TILE codes -- the same codes and summaries as k_resid_codes.
-// (A/B, tools/microbench_paths.cu: 2-byte gathers through dstE 0.59 ms,
-// run-sorted 0.42 ms per 134M vertices.)
-template <class KT, class CT, int NT, int MINB, bool SUMS>
-__global__ void __launch_bounds__(NT, MINB) k_resid_codes_sr(const uint32_t* __restrict__ rPt,
+// codes q_i = K_i - K_{i-1} leave in vertex order, coalesced. The RLE tile
+// summaries follow from the codes (k_rle_tiles_fast, stream_plan_u16).
+// A/B (tools/microbench_paths.cu, config 3): 2-byte gathers through dstE
+// 0.59 ms per 134M vertices, run-sorted 0.42 ms; one CTA of 1024 threads per
+// SM -- the gathers in flight are bounded by the L1 left beside the shared-
+// memory carve-out (3 x 256 threads with 192 KB of shared memory: 0.69 ms);
+// 4 loads in flight per thread (8: 0.62 ms). With the RLE summaries fused
+// into this kernel (no overlap of the two phases at one CTA per SM) 0.70 ms.
+template <class KT, class CT, int NT>
+__global__ void __launch_bounds__(NT, 1) k_resid_codes_sr(const uint32_t* __restrict__ rPt,
                                                           const uint16_t* __restrict__ rLt,
                                                           const uint32_t* __restrict__ dst,
                                                           const KT* __restrict__ Kp, uint64_t n,
-                                                          CT* __restrict__ codes, RleSum* __restrict__ sums) {
-    static_assert(NT % ENC_THREADS == 0, "ENC tiles of ENC_THREADS threads");
+                                                          CT* __restrict__ codes) {
     extern __shared__ __align__(16) unsigned char smem[];
     KT* ks = reinterpret_cast<KT*>(smem);
-    constexpr int NWARP = NT / 32, WPT = ENC_THREADS / 32;  // warps per CTA / per ENC tile
-    using WR = cub::WarpReduce<RleSum>;
-    __shared__ typename WR::TempStorage wtmp[NWARP];
-    __shared__ RleSum wsum[NWARP];
-    __shared__ uint32_t wpart[2][NWARP][3];  // per warp: code bytes, first / last nonzero (round parity)
     const uint64_t t0 = (uint64_t)blockIdx.x * kRTile;
     const uint32_t cnt = (uint32_t)min((uint64_t)kRTile, n - t0);
-    // Phase 1. One CTA per SM and little shared memory: the gathers in flight
-    // are bounded by the L1 left beside the shared-memory carve-out (A/B,
-    // tools/microbench_paths.cu: 1024 threads x 4 loads 0.43 ms; 3 x 256
-    // threads x 8 loads with 192 KB of shared memory 0.69 ms; U = 8 0.62 ms).
-#ifndef UMCG_RSR_U
-#define UMCG_RSR_U 4
-#endif
-    constexpr int U = UMCG_RSR_U;
+    constexpr int U = 4;
     for (uint32_t k0 = threadIdx.x; k0 < cnt; k0 += NT * U) {
         uint32_t pp[U];
         uint32_t ll[U];
@@ -859,113 +849,29 @@ __global__ void __launch_bounds__(NT, MINB) k_resid_codes_sr(const uint32_t* __r
     }
     const int32_t prev0 = t0 ? (int32_t)UMCG_GATHER_LD(Kp + __ldg(dst + t0 - 1)) : 0;
     __syncthreads();
-    // Phase 2: codes in vertex order; ENC tile g of a round = threads
-    // [g * ENC_THREADS, (g + 1) * ENC_THREADS), 8 codes each.
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t gt = threadIdx.x % ENC_THREADS;  // thread within its ENC tile
-    const uint64_t last_tile = (n - 1) / ENC_TILE;
-    for (uint32_t base = 0, r = 0; base < cnt; base += NT * ENC_ITEMS, ++r) {
-        const uint32_t i0 = base + threadIdx.x * ENC_ITEMS;
+    for (uint32_t i0 = threadIdx.x * ENC_ITEMS; i0 < cnt; i0 += NT * ENC_ITEMS) {
         const uint64_t first = t0 + i0;
-        const uint64_t tile = first / ENC_TILE;
+        const int c = (int)min((uint32_t)ENC_ITEMS, cnt - i0);
+        int32_t prev = i0 ? (int32_t)ks[i0 - 1] : prev0;
         CT v[ENC_ITEMS];
-        int c = 0;
-        uint32_t zm = 0, bytes = 0;
-        if (i0 < cnt) {
-            c = (int)min((uint32_t)ENC_ITEMS, cnt - i0);
-            int32_t prev = i0 ? (int32_t)ks[i0 - 1] : prev0;
 #pragma unroll
-            for (int k = 0; k < ENC_ITEMS; ++k) {
-                if (k < c) {
-                    const int32_t K = (int32_t)ks[i0 + k];
-                    v[k] = (CT)zz_enc((int64_t)K - prev);
-                    prev = K;
-                    zm |= v[k] == 0 ? 1u << k : 0u;
-                    bytes += clen(v[k]);
-                } else {
-                    v[k] = 0;
-                }
-            }
-            if (c == ENC_ITEMS) {
-                if (sizeof(CT) == 4) {
-                    uint4* o = reinterpret_cast<uint4*>(codes + first);
-                    o[0] = make_uint4(v[0], v[1], v[2], v[3]);
-                    o[1] = make_uint4(v[4], v[5], v[6], v[7]);
-                } else {
-                    *reinterpret_cast<uint4*>(codes + first) = make_uint4(
-                        (uint32_t)v[0] | ((uint32_t)v[1] << 16), (uint32_t)v[2] | ((uint32_t)v[3] << 16),
-                        (uint32_t)v[4] | ((uint32_t)v[5] << 16), (uint32_t)v[6] | ((uint32_t)v[7] << 16));
-                }
+        for (int k = 0; k < ENC_ITEMS; ++k) {
+            const int32_t K = k < c ? (int32_t)ks[i0 + k] : prev;
+            v[k] = (CT)zz_enc((int64_t)K - prev);
+            prev = K;
+        }
+        if (c == ENC_ITEMS) {
+            if (sizeof(CT) == 4) {
+                uint4* o = reinterpret_cast<uint4*>(codes + first);
+                o[0] = make_uint4(v[0], v[1], v[2], v[3]);
+                o[1] = make_uint4(v[4], v[5], v[6], v[7]);
             } else {
-                for (int k = 0; k < c; ++k) codes[first + k] = v[k];
+                *reinterpret_cast<uint4*>(codes + first) = make_uint4(
+                    (uint32_t)v[0] | ((uint32_t)v[1] << 16), (uint32_t)v[2] | ((uint32_t)v[3] << 16),
+                    (uint32_t)v[4] | ((uint32_t)v[5] << 16), (uint32_t)v[6] | ((uint32_t)v[7] << 16));
             }
         } else {
-#pragma unroll
-            for (int k = 0; k < ENC_ITEMS; ++k) v[k] = 0;
-        }
-        if (!SUMS) continue;  // summaries by k_rle_tiles over the coalesced codes (stream_plan_u16)
-        // Fast tile summary: with no zero run of >= kMinZeroRun codes strictly
-        // inside the tile, its RleSum is {lz, tz, fb = code bytes from the
-        // first to the last nonzero} -- the composition of the thread
-        // summaries (common.cuh rle_compose) has no interior pieces. Such a run
-        // either fills one thread's 8 codes or ends at a thread's first
-        // nonzero after lz >= 1 zeros that continue >= 8 - lz codes into the
-        // previous thread; either case (and the stream's last, possibly
-        // partial, tile) takes the exact RleSum reduction.
-        const uint32_t lz = zm == 0xffu ? 8u : (uint32_t)(__ffs(~zm) - 1);
-        const uint32_t tzr = (zm & 0x80u) ? (uint32_t)__clz(~(zm << 24)) : 0u;  // trailing zero codes
-        uint32_t tz_prev = __shfl_up_sync(0xffffffffu, tzr, 1);
-        if (lane == 0 && gt > 0 && i0 < cnt && lz > 0 && lz < 8) {
-            // the previous thread is in the previous warp: count from shared memory
-            tz_prev = 0;
-            int32_t b = (int32_t)ks[i0 - 1];
-            for (uint32_t k = 1; k <= 8; ++k) {
-                const int32_t a = (int32_t)ks[i0 - 1 - k];  // i0 >= ENC_ITEMS * 32 here
-                if (a != b) break;
-                ++tz_prev;
-                b = a;
-            }
-        }
-        const bool bad = (c > 0 && c < ENC_ITEMS) || (i0 < cnt && zm == 0xffu) ||
-                         (gt > 0 && i0 < cnt && lz > 0 && tz_prev + lz >= kMinZeroRun) || tile == last_tile;
-        const uint32_t fnz = (i0 < cnt && zm != 0xffu) ? gt * ENC_ITEMS + lz : 0xffffffffu;
-        const uint32_t lnz = (i0 < cnt && zm != 0xffu) ? gt * ENC_ITEMS + 7u - tzr : 0u;
-        const uint32_t wb = __reduce_add_sync(0xffffffffu, bytes);
-        const uint32_t wf = __reduce_min_sync(0xffffffffu, fnz);
-        const uint32_t wl = __reduce_max_sync(0xffffffffu, lnz);
-        if (lane == 0) {
-            wpart[r & 1][warp][0] = wb;
-            wpart[r & 1][warp][1] = wf;
-            wpart[r & 1][warp][2] = wl;
-        }
-        const bool lead = gt == 0 && i0 < cnt;
-        if (__syncthreads_or(bad)) {
-            const RleSum s = thread_summary(v, c, (uint32_t)tile);
-            const RleSum w = WR(wtmp[warp]).Reduce(s, RleComposeOp());
-            if (lane == 0) wsum[warp] = w;
-            __syncthreads();
-            if (lead) {
-                RleSum tot = wsum[warp];
-#pragma unroll
-                for (int q = 1; q < WPT; ++q) tot = rle_compose(tot, wsum[warp + q]);
-                sums[tile] = tot;
-            }
-        } else if (lead) {
-            uint32_t tb = 0, f = 0xffffffffu, l = 0;
-#pragma unroll
-            for (int q = 0; q < WPT; ++q) {
-                tb += wpart[r & 1][warp + q][0];
-                f = min(f, wpart[r & 1][warp + q][1]);
-                l = max(l, wpart[r & 1][warp + q][2]);
-            }
-            RleSum S;
-            S.lz = f;
-            S.tz = (uint64_t)(ENC_TILE - 1 - l);
-            S.fb = (uint64_t)(tb - f - (ENC_TILE - 1 - l));
-            S.lb = S.mid = 0;
-            S.origin = (uint32_t)tile;
-            S.flags = 0u;
-            sums[tile] = S;
+            for (int k = 0; k < c; ++k) codes[first + k] = v[k];
         }
     }
 }
@@ -1035,40 +941,28 @@ void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double*
         UMCG_LAUNCHED();
     }
 }
-#ifndef UMCG_RSR_NT
-#define UMCG_RSR_NT 1024
-#endif
-#ifndef UMCG_RSR_MINB
-#define UMCG_RSR_MINB 1
-#endif
-#ifndef UMCG_RSR_SUMS
-#define UMCG_RSR_SUMS false
-#endif
 bool resid_codes_tiles(umcg_plan* p, const void* KE, void* codes, bool narrow, const StreamEncScratch& s,
                        cudaStream_t st) {
     const uint64_t T = cdiv(p->n, ENC_TILE);
     if (!T) return true;
     ProfScope ps_("k_resid_codes", st);
 #ifndef UMCG_RSR_OFF  // (A/B: the dstE gather kernel below)
-    if (p->d_rPt.capacity() >= p->n * 4 && p->d_rLt.capacity() >= p->n * 2) {
+    // narrow (int16) lattice indices only: with int32 indices the tile takes 128 KB of shared
+    // memory and the dstE kernel below (summaries fused) is faster (A/B: absolute-bound
+    // config 3, compress 2.69 -> 2.56 ms)
+    if (narrow && p->d_rPt.capacity() >= p->n * 4 && p->d_rLt.capacity() >= p->n * 2) {
+        constexpr int NT = 1024;
         static DeviceOnce configured;
         configured([] {
-            UMCG_CUDA(cudaFuncSetAttribute(k_resid_codes_sr<int16_t, uint16_t, UMCG_RSR_NT, UMCG_RSR_MINB, UMCG_RSR_SUMS>,
+            UMCG_CUDA(cudaFuncSetAttribute(k_resid_codes_sr<int16_t, uint16_t, NT>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, kRTile * 2));
-            UMCG_CUDA(cudaFuncSetAttribute(k_resid_codes_sr<int32_t, uint32_t, 1024, 1, UMCG_RSR_SUMS>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kRTile * 4));
         });
         const unsigned g = (unsigned)cdiv(p->n, (uint64_t)kRTile);
-        if (narrow)
-            k_resid_codes_sr<int16_t, uint16_t, UMCG_RSR_NT, UMCG_RSR_MINB, UMCG_RSR_SUMS><<<g, UMCG_RSR_NT, kRTile * 2, st>>>(
-                p->d_rPt.as<uint32_t>(1), p->d_rLt.as<uint16_t>(1), p->d_dstE.as<uint32_t>(1),
-                static_cast<const int16_t*>(KE), p->n, static_cast<uint16_t*>(codes), s.sums);
-        else
-            k_resid_codes_sr<int32_t, uint32_t, 1024, 1, UMCG_RSR_SUMS><<<g, 1024, kRTile * 4, st>>>(
-                p->d_rPt.as<uint32_t>(1), p->d_rLt.as<uint16_t>(1), p->d_dstE.as<uint32_t>(1),
-                static_cast<const int32_t*>(KE), p->n, static_cast<uint32_t*>(codes), s.sums);
+        k_resid_codes_sr<int16_t, uint16_t, NT><<<g, NT, kRTile * 2, st>>>(
+            p->d_rPt.as<uint32_t>(1), p->d_rLt.as<uint16_t>(1), p->d_dstE.as<uint32_t>(1),
+            static_cast<const int16_t*>(KE), p->n, static_cast<uint16_t*>(codes));
         UMCG_LAUNCHED();
-        return UMCG_RSR_SUMS;
+        return false;
     }
 #endif
     if (narrow)
