@@ -60,8 +60,9 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_tiles_fast(const T* __restr
     const uint64_t T_ = (n + ENC_TILE - 1) / ENC_TILE;
     const uint64_t tile0 = (uint64_t)blockIdx.x * FT;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // u16 codes of a full thread stay packed: SIMD halfword compares give the
-    // zero mask and the varint byte count (clen: 1 + (v >= 0x80) + (v >= 0x4000))
+    // u16 codes of a full thread stay packed: halfword compares give the zero
+    // mask and the varint byte count (clen: 1 + (v >= 0x80) + (v >= 0x4000);
+    // the __vcmp*2 SIMD intrinsics are emulated and cost ~3x more)
     constexpr bool P16 = sizeof(T) == 2;
     T v[FT][P16 ? 1 : ENC_ITEMS];
     uint4 pw[FT];
@@ -98,13 +99,13 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_tiles_fast(const T* __restr
             uint32_t g = 0;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const uint32_t e = __vcmpeq2(w[i], 0u);
-                zm |= ((e & 1u) | ((e >> 15) & 2u)) << (2 * i);
-                g += __popc(__vcmpgeu2(w[i], 0x00800080u)) + __popc(__vcmpgeu2(w[i], 0x40004000u));
+                const uint32_t lo = w[i] & 0xffffu, hi = w[i] >> 16;
+                zm |= ((uint32_t)(lo == 0) | ((uint32_t)(hi == 0) << 1)) << (2 * i);
+                g += (lo >= 0x80u) + (lo >= 0x4000u) + (hi >= 0x80u) + (hi >= 0x4000u);
             }
             const uint32_t valid = (1u << cnt[t]) - 1u;
             zm &= valid;  // (padding halfwords of a partial thread are 0: excluded here, and bad below)
-            bytes = (uint32_t)cnt[t] + g / 16;
+            bytes = (uint32_t)cnt[t] + g;
         } else {
 #pragma unroll
             for (int k = 0; k < ENC_ITEMS; ++k) {
