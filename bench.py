@@ -168,7 +168,7 @@ def kernel_bytes(n, n1, s2, k1_bytes, narrow=False):
     s8d = {
         "k_gather_fwd": 12 * n,                  # perm 4 + x gathered 8 (xE write is an intermediate)
         "k_bucket": 12 * n + 12 * n1,            # node ids 4 + x streamed 8; seg_off 4 + x1 write 8 per slot
-        "k_resid_codes": 4 * n,                  # dstE (the inverse permutation); KE / codes are intermediates
+        "k_resid_codes": 4 * n,                  # rPt / dstE (the inverse permutation); KE / codes are intermediates
         "k_rle_write": s2,                       # archive bytes
         "k_dec_agg": s2,                         # archive bytes
         "k_dec_out": 20 * n + s2,                # node ids 4 + gather 8 + x' 8 + archive
@@ -178,7 +178,8 @@ def kernel_bytes(n, n1, s2, k1_bytes, narrow=False):
     own = {
         "k_gather_fwd": 20 * n,                  # x 8 + srcE 4 -> xE 8
         "k_bucket": (12 + kb) * n + 12 * n1,     # xE 8 + lslot 2 + lnode 2 + KE; seg 4 + x1 8 per slot
-        "k_resid_codes": (4 + kb + cb) * n,      # dstE 4 + KE (gathered once) + codes
+        # narrow: run-sorted gather, rPt 4 + rLt 2 + KE (gathered once) + codes; wide: dstE 4 + KE + codes
+        "k_resid_codes": ((6 if narrow else 4) + kb + cb) * n,
         "k_rle_write": cb * n + s2,              # codes + stream out
         "k_dec_agg": s2,                         # stream in
         "k_dec_out": 12 * n + s2 + k1_bytes * n1,  # node 4 + out 8 + stream + K1 table

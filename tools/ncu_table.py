@@ -21,7 +21,7 @@ def g(r, k):
 def short(nm, rd):
     m = re.search(r"(k_\w+)(<[^>(]*>)?", nm)
     base, targs = m.group(1), m.group(2) or ""
-    if base == "k_rle_write_fast":
+    if base in ("k_rle_write_fast", "k_rle_tiles_fast"):
         return base + ("<u16> (residual)" if "short" in targs else "<u32> (grid)")
     if base == "k_dec_out":
         return base + ("<P64> (grid)" if targs.startswith("<0") else "<RECOMPOSE> (residual)")
@@ -45,7 +45,7 @@ md = ["| kernel | ncu us | DRAM read GB | DRAM write GB | L2 hit % | issue activ
 for s, t, rd, wr, hit, iss, l1 in lines:
     md.append(f"| {s} | {t:.1f} | {rd / 1e9:.3f} | {wr / 1e9:.3f} | {hit:.1f} | {iss:.1f} | {l1:.1f} |")
 open(out_md, "w").write("\n".join(md) + "\n")
-names = {"k_gather_fwd": "k_gather_fwd", "k_bucket_tma": "k_bucket", "k_resid_codes": "k_resid_codes",
+names = {"k_gather_fwd": "k_gather_fwd", "k_bucket_tma": "k_bucket", "k_resid_codes": "k_resid_codes", "k_resid_codes_sr": "k_resid_codes",
          "k_dec_agg (residual)": "k_dec_agg", "k_dec_out<RECOMPOSE> (residual)": "k_dec_out",
          "k_dec_out<P64> (grid)": "k_dec_out_grid"}
 d = {names[s]: rd + wr for s, t, rd, wr, *_ in lines if s in names}
