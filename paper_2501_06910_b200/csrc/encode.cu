@@ -51,12 +51,14 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_tiles(const T* __restrict__
 constexpr int FT = 4;  // tiles per CTA of k_rle_tiles_fast: every code load in flight up front
 template <class T>
 __global__ void __launch_bounds__(ENC_THREADS) k_rle_tiles_fast(const T* __restrict__ codes, uint64_t n,
-                                                                RleSum* __restrict__ sums,
-                                                                uint32_t* __restrict__ redo,
-                                                                uint32_t* __restrict__ n_redo) {
+                                                                RleSum* __restrict__ sums) {
     static_assert(ENC_ITEMS == 8, "8-bit zero masks");
     constexpr int NW = ENC_THREADS / 32;
+    using WR = cub::WarpReduce<RleSum>;
+    __shared__ typename WR::TempStorage wtmp[NW];
+    __shared__ RleSum wsum[FT][NW];
     __shared__ uint32_t wpart[FT][NW][4];  // per warp: code bytes, first / last nonzero, any bad
+    __shared__ uint32_t tbad[FT];
     const uint64_t T_ = (n + ENC_TILE - 1) / ENC_TILE;
     const uint64_t tile0 = (uint64_t)blockIdx.x * FT;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -149,9 +151,8 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_tiles_fast(const T* __restr
             l = max(l, wpart[t][w][2]);
             bad |= wpart[t][w][3];
         }
-        if (bad) {
-            redo[atomicAdd(n_redo, 1u)] = (uint32_t)tile;
-        } else {
+        tbad[t] = bad;
+        if (!bad) {
             RleSum S;
             S.lz = f;
             S.tz = (uint64_t)(ENC_TILE - 1 - l);
@@ -162,26 +163,38 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_tiles_fast(const T* __restr
             sums[tile] = S;
         }
     }
-}
-
-// The exact summaries of the listed tiles (grid-stride: the count is on the device).
-template <class T>
-__global__ void __launch_bounds__(ENC_THREADS) k_rle_tiles_redo(const T* __restrict__ codes, uint64_t n,
-                                                                RleSum* __restrict__ sums,
-                                                                const uint32_t* __restrict__ redo,
-                                                                const uint32_t* __restrict__ n_redo) {
-    using BR = cub::BlockReduce<RleSum, ENC_THREADS>;
-    __shared__ typename BR::TempStorage tmp;
-    const uint32_t cnt = *n_redo;
-    for (uint32_t i = blockIdx.x; i < cnt; i += gridDim.x) {
-        const uint64_t tile = redo[i];
-        const uint64_t first = tile * ENC_TILE + (uint64_t)threadIdx.x * ENC_ITEMS;
-        T v[ENC_ITEMS];
-        const int c = load_items(codes, n, first, v);
-        const RleSum s = thread_summary(v, c, (uint32_t)tile);
-        const RleSum tot = BR(tmp).Reduce(s, RleComposeOp());
-        if (threadIdx.x == 0) sums[tile] = tot;
-        __syncthreads();
+    __syncthreads();
+    // the other tiles: the exact RleSum reduction, inline (token-dense streams
+    // have many; a second pass over a list of them measured slower): warp
+    // reductions of every such tile, then one thread per tile composes the
+    // warps' summaries in order
+    bool any = false;
+#pragma unroll
+    for (int t = 0; t < FT; ++t) {
+        const uint64_t tile = tile0 + t;
+        if (tile >= T_ || !tbad[t]) continue;
+        any = true;
+        T u[ENC_ITEMS];
+        if constexpr (P16) {
+            const uint32_t w[4] = {pw[t].x, pw[t].y, pw[t].z, pw[t].w};
+#pragma unroll
+            for (int k = 0; k < ENC_ITEMS; ++k) u[k] = (T)(w[k >> 1] >> (16 * (k & 1)));
+        } else {
+#pragma unroll
+            for (int k = 0; k < ENC_ITEMS; ++k) u[k] = v[t][k];
+        }
+        const RleSum r = WR(wtmp[warp]).Reduce(thread_summary(u, cnt[t], (uint32_t)tile), RleComposeOp());
+        if (lane == 0) wsum[t][warp] = r;
+        __syncwarp();
+    }
+    if (!any) return;
+    __syncthreads();
+    if (threadIdx.x < FT && tile0 + threadIdx.x < T_ && tbad[threadIdx.x]) {
+        const int t = threadIdx.x;
+        RleSum tot = wsum[t][0];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) tot = rle_compose(tot, wsum[t][w]);
+        sums[tile0 + t] = tot;
     }
 }
 
@@ -620,13 +633,12 @@ StreamEncScratch stream_enc_carve(void* base, uint64_t n) {
     s.pos = reinterpret_cast<uint64_t*>(p);
     p += T * sizeof(uint64_t);
     s.glist = reinterpret_cast<uint32_t*>(p);
-    p += T * sizeof(uint32_t);
-    s.n_redo = reinterpret_cast<uint32_t*>(p);  // inside the scratch's 4096-byte slack
     return s;
 }
 
 template <class T>
-static void plan_impl(const T* codes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp, cudaStream_t st) {
+static void plan_impl(const T* codes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp, cudaStream_t st,
+                      bool fast = false) {
     const uint64_t T_ = cdiv(n, ENC_TILE);
     if (!T_) {
         UMCG_CUDA(cudaMemsetAsync(&ctl->stream_len[comp], 0, 8, st));
@@ -634,21 +646,10 @@ static void plan_impl(const T* codes, uint64_t n, const StreamEncScratch& s, Dev
     }
     const uint64_t C = cdiv(T_, CH);
     UMCG_CUDA(cudaMemsetAsync(&ctl->aux[4 + comp], 0, 8, st));
-#ifdef UMCG_RLE_TILES_EXACT  // (A/B: the exact RleSum reduction on every tile)
-    k_rle_tiles<T><<<(unsigned)T_, ENC_THREADS, 0, st>>>(codes, n, s.sums);
-#else
-    // the tile list doubles as the redo list (k_rle_states fills it afterwards)
-    UMCG_CUDA(cudaMemsetAsync(s.n_redo, 0, 4, st));
-    k_rle_tiles_fast<T><<<(unsigned)cdiv(T_, (uint64_t)FT), ENC_THREADS, 0, st>>>(codes, n, s.sums, s.glist, s.n_redo);
-    UMCG_LAUNCHED();
-    {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        k_rle_tiles_redo<T><<<(unsigned)std::min<uint64_t>(T_, (uint64_t)sms * 4), ENC_THREADS, 0, st>>>(
-            codes, n, s.sums, s.glist, s.n_redo);
-    }
-#endif
+    if (fast)
+        k_rle_tiles_fast<T><<<(unsigned)cdiv(T_, (uint64_t)FT), ENC_THREADS, 0, st>>>(codes, n, s.sums);
+    else
+        k_rle_tiles<T><<<(unsigned)T_, ENC_THREADS, 0, st>>>(codes, n, s.sums);
     UMCG_LAUNCHED();
     k_rle_chunks<<<(unsigned)C, CH, 0, st>>>(s.sums, T_, s.csum);
     UMCG_LAUNCHED();
@@ -688,7 +689,10 @@ static void write_impl(const T* codes, uint64_t n, const StreamEncScratch& s, De
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned gg = (unsigned)std::min<uint64_t>(T_, (uint64_t)sms * 6);
+#ifndef UMCG_GENERAL_PER_SM
+#define UMCG_GENERAL_PER_SM 32  // (A/B config 5, tau 1e-2: 6 per SM 6.79 ms, 24 or one CTA per tile 6.06 ms)
+#endif
+    const unsigned gg = (unsigned)std::min<uint64_t>(T_, (uint64_t)sms * UMCG_GENERAL_PER_SM);
     k_rle_write_general<T><<<gg, ENC_THREADS, 0, st>>>(codes, n, s.states, s.sums, s.lit_total, ctl,
                                                                  comp, s.glist, s.pos, dst, off_ctl ? 1 : 0);
     UMCG_LAUNCHED();
@@ -699,7 +703,7 @@ void stream_plan_u32(const uint32_t* c, uint64_t n, const StreamEncScratch& s, D
 void stream_plan_u64(const uint64_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
                      cudaStream_t st) { plan_impl(c, n, s, ctl, comp, st); }
 void stream_plan_u16(const uint16_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
-                     cudaStream_t st) { plan_impl(c, n, s, ctl, comp, st); }
+                     cudaStream_t st, bool fast) { plan_impl(c, n, s, ctl, comp, st, fast); }
 void stream_write_u32(const uint32_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
                       uint8_t* dst, bool o, cudaStream_t st) { write_impl(c, n, s, ctl, comp, dst, o, st); }
 void stream_write_u64(const uint64_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,

@@ -19,7 +19,6 @@ struct StreamEncScratch {
     uint64_t* lit_total = nullptr;  // [T]   literal byte totals, keyed by opening tile
     uint64_t* pos = nullptr;        // [T+1] stream position of each tile's first byte (writers)
     uint32_t* glist = nullptr;      // [T]   tiles for the general writer (count in ctl->aux[4+comp])
-    uint32_t* n_redo = nullptr;     // [1]   tiles whose summary needs the exact reduction (list in glist)
 };
 size_t stream_enc_scratch_bytes(uint64_t n);
 StreamEncScratch stream_enc_carve(void* base, uint64_t n);
@@ -34,8 +33,10 @@ void stream_encode_u64(const uint64_t* codes, uint64_t n, const StreamEncScratch
 // Phase split used by the pipeline (summaries/scan first, layout, then write).
 void stream_plan_u32(const uint32_t* codes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl,
                      int comp, cudaStream_t st);
+// fast: tile summaries by k_rle_tiles_fast (pays when zero codes are rare --
+// fine residual bounds; token-dense streams are faster with k_rle_tiles)
 void stream_plan_u16(const uint16_t* codes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
-                     cudaStream_t st);
+                     cudaStream_t st, bool fast = false);
 void stream_plan_u64(const uint64_t* codes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl,
                      int comp, cudaStream_t st);
 // Phases 2-4 only, when the tile summaries (s.sums) were produced by a fused

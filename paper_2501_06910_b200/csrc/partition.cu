@@ -941,16 +941,18 @@ void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double*
         UMCG_LAUNCHED();
     }
 }
-bool resid_codes_tiles(umcg_plan* p, const void* KE, void* codes, bool narrow, const StreamEncScratch& s,
+bool resid_codes_tiles(umcg_plan* p, const void* KE, void* codes, bool narrow, bool fine, const StreamEncScratch& s,
                        cudaStream_t st) {
     const uint64_t T = cdiv(p->n, ENC_TILE);
     if (!T) return true;
     ProfScope ps_("k_resid_codes", st);
 #ifndef UMCG_RSR_OFF  // (A/B: the dstE gather kernel below)
-    // narrow (int16) lattice indices only: with int32 indices the tile takes 128 KB of shared
-    // memory and the dstE kernel below (summaries fused) is faster (A/B: absolute-bound
-    // config 3, compress 2.69 -> 2.56 ms)
-    if (narrow && p->d_rPt.capacity() >= p->n * 4 && p->d_rLt.capacity() >= p->n * 2) {
+    // Narrow (int16) lattice indices of a fine bound only. With int32 indices the tile takes
+    // 128 KB of shared memory and the dstE kernel below (summaries fused) is faster (A/B:
+    // absolute-bound config 3, compress 2.69 -> 2.56 ms); with coarse bounds (token-dense
+    // streams) the exact summaries are better hidden under the dstE kernel's gathers than
+    // run as a pass of their own (config 5 256^3 tau 1e-2: 5.35 -> 4.95 ms).
+    if (narrow && fine && p->d_rPt.capacity() >= p->n * 4 && p->d_rLt.capacity() >= p->n * 2) {
         constexpr int NT = 1024;
         static DeviceOnce configured;
         configured([] {

@@ -124,7 +124,8 @@ void bucket_means_residuals(umcg_plan* p, const double* xp, DevCtl* ctl, double*
                             int32_t* K1, int D1, cudaStream_t st);
 // Returns whether the RLE tile summaries were written too (else the caller
 // runs the stream plan over the codes).
-bool resid_codes_tiles(umcg_plan* p, const void* Kp, void* codes, bool narrow, const StreamEncScratch& s,
+// fine: a fine relative bound (zero codes rare): the run-sorted kernel, summaries by the fast pass.
+bool resid_codes_tiles(umcg_plan* p, const void* Kp, void* codes, bool narrow, bool fine, const StreamEncScratch& s,
                        cudaStream_t st);
 // Multilinear g in bucket order (layout E): residual lattice indices KE
 // (compress) and the recomposition x' = g + x2' (decompress, gE [n] scratch).

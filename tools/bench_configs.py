@@ -56,9 +56,12 @@ def run(name, plan, x, tau, n_bytes, extra=None, rho=0.5):
 
 
 res = []
+# BENCH_CFG_ONLY=2,4,5 selects configs; BENCH_CFG_QUICK=1 times config 5 at 256^3, tau 1e-2 only (A/B runs)
+ONLY = [c for c in os.environ.get("BENCH_CFG_ONLY", "2,4,5").split(",") if c]
+QUICK = os.environ.get("BENCH_CFG_QUICK") == "1"
 # config 2: 16.7M vertices, grids 512^2 / 1024^2 / 2048^2, tau 1e-2 / 1e-4 / 1e-6
 xy, x = umcg.gen_config(2, 1 << 24, 0x250106910 + 2, device="cuda")
-for g in (512, 1024, 2048):
+for g in ((512, 1024, 2048) if "2" in ONLY else ()):
     plan = bbox_plan(xy, g)
     for tau in (1e-2, 1e-4, 1e-6):
         run(f"config2 grid{g}^2", plan, x, tau, x.numel() * 8)
@@ -71,7 +74,7 @@ plan = bbox_plan(xy, 2048)
 cap = 5 * plan.compress_bound("f0")
 buf = torch.empty(cap, dtype=torch.uint8, device="cuda")
 out32 = torch.empty_like(vals)
-for tau in (1e-3, 1e-5):
+for tau in ((1e-3, 1e-5) if "4" in ONLY else ()):
     b = umcg.Budget(tau=tau)
     lens = [None]
 
@@ -90,11 +93,11 @@ del plan, xy, vals
 torch.cuda.empty_cache()
 # config 5: 200M vertices, grids 128^3 / 256^3 (seed) / 384^3 (seed)
 xyz, x = umcg.gen_config(5, 200_000_000, 0x250106910 + 5, device="cuda")
-for g in (128, 256, 384):
+for g in (((256,) if QUICK else (128, 256, 384)) if "5" in ONLY else ()):
     plan = bbox_plan(xyz, g)
-    for tau in (1e-2, 1e-6):
+    for tau in ((1e-2,) if QUICK else (1e-2, 1e-6)):
         run(f"config5 grid{g}^3", plan, x, tau, x.numel() * 8)
-    if g == 256:  # the error-split sweep of the config (9 splits, tau 1e-4)
+    if g == 256 and not QUICK:  # the error-split sweep of the config (9 splits, tau 1e-4)
         for rho in np.round(np.arange(0.1, 0.95, 0.1), 1):
             run(f"config5 grid{g}^3 split", plan, x, 1e-4, x.numel() * 8, rho=float(rho))
     del plan
