@@ -834,3 +834,48 @@ def test_host_calls_pageable_staging(cuda):
         plan.decompress_host(got, out=out)
         assert np.array_equal(out, plan.decompress(want).cpu().numpy())
     del torch
+
+
+def test_fine_bound_zero_runs_at_tile_warp_and_thread_boundaries(cuda, ref, oracle):
+    """The fine-bound residual path (tau_rel <= 2.5e-4: run-sorted codes,
+    k_rle_tiles_fast summaries with the exact fallback) on zero-code runs
+    placed across the summary's seams: runs of 7 / 9 / 17 zeros straddling
+    thread (8 codes), warp (256) and ENC tile (2048) boundaries, all-zero
+    threads and whole zero tiles, and a partial last tile. Two vertices per
+    node in vertex order, so a node whose two values are equal has K2 = 0 on
+    both and a stretch of such nodes is a run of 2 m - 1 zero codes after
+    the stretch's first (nonzero) code."""
+    rng = np.random.default_rng(20251020)
+    n = (1 << 20) - 6
+    nodes = n // 2
+    x = rng.normal(0.0, 1.0, n)
+
+    def zero_run(start, length):  # `length` (odd) zero codes starting at code `start` (odd)
+        assert start % 2 == 1 and length % 2 == 1
+        a = (start - 1) // 2
+        m = (length + 1) // 2
+        for k in range(a, a + m):
+            x[2 * k + 1] = x[2 * k]
+
+    starts = []
+    for w in range(1, 60):  # warp boundaries: runs of 7 / 9 / 17 across 256 w
+        b = 256 * w
+        ln = (7, 9, 17)[w % 3]
+        starts.append((b - ln // 2 - (1 if (b - ln // 2) % 2 == 0 else 0), ln))
+    for t in range(64, 160, 3):  # thread boundaries inside warps: 7 / 9 zeros across 8 t
+        b = 8 * t + 2048 * 40
+        ln = 7 if t % 2 else 9
+        starts.append((b - 3 if (b - 3) % 2 else b - 4, ln))
+    for tile in (100, 101, 300):  # tile boundaries
+        starts.append((2048 * tile - 5, 9))
+    starts.append((2048 * 200 + 1, 2 * 2048 + 1))  # whole zero tiles (all-zero threads)
+    starts.append((n - 2000 + 1, 1999 - 2))  # a long run into the partial last tile
+    for s0, ln in starts:
+        zero_run(s0, ln)
+    axes = [np.linspace(0.0, 1.0, 5), np.linspace(0.0, 1.0, nodes // 5)]
+    assert 5 * (nodes // 5) == nodes
+    assign = (np.arange(n, dtype=np.uint64) // np.uint64(2))
+    s = Setup(dim=2, axes=axes, mode=0, assignments=assign)
+    plan = plan_for(s, coords=False)
+    for tau in (1e-4, 2e-4):
+        _parity_case(plan, s, dev(x), x, dict(tau=tau), ref, oracle, f"zero-run seams tau={tau}")

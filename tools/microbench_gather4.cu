@@ -176,5 +176,48 @@ int main(int argc, char** argv) {
     G4(1024, 3, 8, 2)
     G4(1024, 2, 8, 4)
     G4(512, 4, 8, 4)
+    // Mixed: LDG on the first f*n elements (stream s1) beside TMA gather4 on the
+    // rest (stream s2) -- is TMA a second path to L2 next to L1TEX?
+    {
+        cudaStream_t s1, s2;
+        CK(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        auto k = k_g4<1024, 2, 8>;
+        const int smem = 1024 * 2 * 32;
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        for (double f : {1.0, 0.85, 0.75, 0.65}) {
+            for (int bps : {1, 2}) {
+                const uint64_t n1s = (uint64_t)(f * n) & ~2047ull, n2s = n - n1s;
+                CK(cudaMemset(o2, 0, n * 2));
+                auto launch = [&] {
+                    CK(cudaEventRecord(a, 0));
+                    CK(cudaStreamWaitEvent(s1, a));
+                    CK(cudaStreamWaitEvent(s2, a));
+                    k_ldg<<<(unsigned)((n1s + 2047) / 2048), 256, 0, s1>>>(tab, idx, n1s, o2);
+                    if (n2s) k<<<sms * bps, 256, smem, s2>>>(tm, idx + n1s, n2s, o2 + n1s);
+                    cudaEvent_t e1, e2;
+                    cudaEventCreate(&e1); cudaEventCreate(&e2);
+                    cudaEventRecord(e1, s1); cudaEventRecord(e2, s2);
+                    cudaStreamWaitEvent(0, e1); cudaStreamWaitEvent(0, e2);
+                    cudaEventDestroy(e1); cudaEventDestroy(e2);
+                };
+                for (int w = 0; w < 3; ++w) launch();
+                CK(cudaDeviceSynchronize());
+                cudaEvent_t t0, t1;
+                cudaEventCreate(&t0); cudaEventCreate(&t1);
+                cudaEventRecord(t0, 0);
+                for (int w = 0; w < 10; ++w) launch();
+                cudaEventRecord(t1, 0);
+                CK(cudaEventSynchronize(t1));
+                float ms = 0;
+                cudaEventElapsedTime(&ms, t0, t1);
+                CK(cudaMemcpy(r2.data(), o2, n * 2, cudaMemcpyDeviceToHost));
+                uint64_t bad = 0;
+                for (uint64_t i = 0; i < n; ++i) bad += r1[i] != r2[i];
+                std::printf("mixed ldg %.2f + g4 bps%d        %.3f ms  (mismatches %llu)\n", f, bps, ms / 10,
+                            (unsigned long long)bad);
+            }
+        }
+    }
     return 0;
 }
