@@ -1371,6 +1371,8 @@ umcg_status umcg_plan_clone(const umcg_plan* src, umcg_plan** out) {
         c->n_buckets = o->n_buckets;
         c->n_epochs = o->n_epochs;
         c->n_regular = o->n_regular;
+        c->bucket_cap = o->bucket_cap;
+        c->bucket_nodes = o->bucket_nodes;
         for (auto m : {&umcg_plan::d_node, &umcg_plan::d_perm, &umcg_plan::d_seg, &umcg_plan::d_visited,
                        &umcg_plan::d_axes, &umcg_plan::d_axis_off, &umcg_plan::d_inv_cell, &umcg_plan::d_coords,
                        &umcg_plan::d_srcE, &umcg_plan::d_dstE, &umcg_plan::d_ech, &umcg_plan::d_bct,

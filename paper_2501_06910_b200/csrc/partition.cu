@@ -125,9 +125,8 @@ __device__ __forceinline__ void grid_k(const GridK& g, uint64_t j, double v, Dev
 // Bucket b's elements, in bucket order l = 0..m-1, live in layout E as one
 // chunk per epoch: pre[e] = first l of epoch e's chunk, cbase[e] = its
 // layout-E position. Each warp moves whole chunks (coalesced).
-constexpr int PER = kBucketCap / BT;  // elements per thread in a bucket
 
-template <class KT>
+template <class KT, uint32_t CAP, uint32_t NODES>
 __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, const uint32_t* __restrict__ bk,
                                               uint64_t B, uint32_t E, const uint2* __restrict__ bct,
                                               const uint16_t* __restrict__ lnode,
@@ -135,12 +134,13 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
                                               DevCtl* ctl, double* __restrict__ x1, KT* __restrict__ KE,
                                               int heavy_only, GridK gk) {
     extern __shared__ __align__(128) unsigned char smem[];
-    double* xs = reinterpret_cast<double*>(smem);                      // [kBucketCap]
-    double* x1s = xs + kBucketCap;                                     // [kBucketNodes]
-    uint32_t* sg = reinterpret_cast<uint32_t*>(x1s + kBucketNodes);    // [kBucketNodes + 1]
-    uint2* ch = reinterpret_cast<uint2*>(sg + kBucketNodes + 2);       // [E+1]
-    uint16_t* lp = reinterpret_cast<uint16_t*>(ch + (E + 1));          // [kBucketCap]
-    uint16_t* ln = lp + kBucketCap;                                    // [kBucketCap]
+    constexpr int PER = CAP / BT;  // elements per thread in a bucket
+    double* xs = reinterpret_cast<double*>(smem);                      // [CAP]
+    double* x1s = xs + CAP;                                            // [NODES]
+    uint32_t* sg = reinterpret_cast<uint32_t*>(x1s + NODES);           // [NODES + 1]
+    uint2* ch = reinterpret_cast<uint2*>(sg + NODES + 2);              // [E+1]
+    uint16_t* lp = reinterpret_cast<uint16_t*>(ch + (E + 1));          // [CAP]
+    uint16_t* ln = lp + CAP;                                           // [CAP]
     const uint32_t* bstart = bk;
     const uint32_t* bnode = bk + B + 1;
     const uint64_t b = blockIdx.x;
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
     constexpr int NW = BT / 32;
     // chunk table (one chunk per epoch, bucket-major) + segment offsets
     for (uint32_t e = threadIdx.x; e <= E; e += BT) ch[e] = __ldg(&bct[b * (uint64_t)(E + 1) + e]);
-    const bool heavy = m > kBucketCap;
+    const bool heavy = m > CAP;
     if (heavy_only && !heavy) return;
     if (!heavy)
         for (uint32_t j = threadIdx.x; j <= nj; j += BT) sg[j] = __ldg(&seg[j0 + j]) - s0;
@@ -238,10 +238,9 @@ __global__ void __launch_bounds__(BT) k_bucket(const double* __restrict__ xE, co
     }
 }
 
-constexpr int BTP = 512;  // threads per persistent bucket CTA
 
 // ---- TMA variant ------------------------------------------------------------
-// Persistent CTAs (two per SM) walk the regular (<= kBucketCap) buckets
+// Persistent CTAs walk the regular (<= CAP vertices) buckets
 // round-robin with two shared-memory stages: while bucket k is summed and
 // quantized, bucket k+1 arrives through bulk asynchronous copies
 // (cp.async.bulk, completion on an mbarrier): one copy
@@ -276,26 +275,28 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 struct TmaStage {
-    double* xs;     // [kBucketCap + 2E + 4] slots
-    uint16_t* ls;   // [kBucketCap + 16]   slot map (node-sorted), phase s0 & 7
-    uint16_t* ln;   // [kBucketCap + 16]   lnode (bucket order),    phase s0 & 7
+    double* xs;     // [CAP + 2E + 4] slots
+    uint16_t* ls;   // [CAP + 16]   slot map (node-sorted), phase s0 & 7
+    uint16_t* ln;   // [CAP + 16]   lnode (bucket order),    phase s0 & 7
     uint2* ch;      // [E + 1]
 };
 
 // (segment offsets go straight to registers: two CTAs fit per SM)
+template <uint32_t CAP>
 __host__ __device__ __forceinline__ uint32_t tma_stage_bytes(uint32_t E) {
-    const uint32_t b = (kBucketCap + 2 * E + 4) * 8 + 2 * (kBucketCap + 16) * 2 + (E + 1) * 8;
+    const uint32_t b = (CAP + 2 * E + 4) * 8 + 2 * (CAP + 16) * 2 + (E + 1) * 8;
     return (b + 127) & ~127u;
 }
 
+template <uint32_t CAP>
 __device__ __forceinline__ TmaStage make_tma_stage(unsigned char* p, uint32_t E) {
     TmaStage S;
     S.xs = reinterpret_cast<double*>(p);
-    p += (kBucketCap + 2 * E + 4) * 8;
+    p += (CAP + 2 * E + 4) * 8;
     S.ls = reinterpret_cast<uint16_t*>(p);
-    p += (kBucketCap + 16) * 2;
+    p += (CAP + 16) * 2;
     S.ln = reinterpret_cast<uint16_t*>(p);
-    p += (kBucketCap + 16) * 2;
+    p += (CAP + 16) * 2;
     S.ch = reinterpret_cast<uint2*>(p);
     return S;
 }
@@ -339,19 +340,16 @@ __device__ __forceinline__ void tma_issue(const TmaStage& S, uint64_t* bar, cons
     }
 }
 
-static_assert(kBucketNodes <= 2 * BTP, "k_bucket_tma keeps <= 2 slots per thread in registers");
+
 // The warp that issues the next bucket's bulk copies (~100 cycles per copy,
 // E + 2 copies): the last warp, which owns slots only in buckets of more
 // than 480 slots, so the issue overlaps the other warps' ordered sums.
-#ifndef UMCG_BT_ISSUE_WARP
-#define UMCG_BT_ISSUE_WARP (BTP / 32 - 1)
-#endif
-constexpr int BT_ISSUE_WARP = UMCG_BT_ISSUE_WARP;
 
 
 
-template <class KT>
-__global__ void __launch_bounds__(BTP, 2) k_bucket_tma(const double* __restrict__ xE, const uint32_t* __restrict__ bk,
+// CAP vertices / NODES slots per bucket, BTP threads, MINB CTAs per SM.
+template <class KT, uint32_t CAP, uint32_t NODES, int BTP, int MINB>
+__global__ void __launch_bounds__(BTP, MINB) k_bucket_tma(const double* __restrict__ xE, const uint32_t* __restrict__ bk,
                                                   uint64_t B, uint32_t E, const uint2* __restrict__ bct,
                                                   const uint32_t* __restrict__ regular, uint32_t n_regular,
                                                   const uint16_t* __restrict__ lnode,
@@ -361,8 +359,10 @@ __global__ void __launch_bounds__(BTP, 2) k_bucket_tma(const double* __restrict_
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bars[2];
     double* x1s = reinterpret_cast<double*>(smem);
-    const uint32_t stage_bytes = tma_stage_bytes(E);
-    auto stage = [&](int st) { return make_tma_stage(smem + kBucketNodes * 8 + st * stage_bytes, E); };
+    static_assert(NODES <= 2 * BTP, "k_bucket_tma keeps <= 2 slots per thread in registers");
+    constexpr int BT_ISSUE_WARP = BTP / 32 - 1;
+    const uint32_t stage_bytes = tma_stage_bytes<CAP>(E);
+    auto stage = [&](int st) { return make_tma_stage<CAP>(smem + NODES * 8 + st * stage_bytes, E); };
     const uint32_t* bstart = bk;
     const uint32_t* bnode = bk + B + 1;
     const double bin = ctl->bin[1], inv = ctl->inv_bin[1], tau = ctl->tau_c[1];
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(BTP, 2) k_bucket_tma(const double* __restrict_
             }
         }
         const uint32_t s0 = cur.s0, j0 = cur.j0, nj = cur.nj;
-        // segment offsets of this thread's slots (kBucketNodes <= 2 * BTP), in flight during the wait
+        // segment offsets of this thread's slots (NODES <= 2 * BTP), in flight during the wait
         uint32_t sgr[2][2] = {{0, 0}, {0, 0}};
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -889,36 +889,39 @@ void partition_values(const void* x, int x_f32, umcg_plan* p, double* xE, DevCtl
     UMCG_LAUNCHED();
 }
 
-void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double* x1, void* KE, bool narrow,
-                            int32_t* K1, int D1, cudaStream_t st) {
-    const GridK gk{K1, std::ldexp(1.0, 31 - (D1 < 1 ? 1 : D1))};
-    if (!p->n_buckets) return;
-    ProfScope ps_("k_bucket", st);
+// Buckets of CAP vertices / NODES slots: persistent BTP-thread CTAs, MINB per SM.
+template <uint32_t CAP, uint32_t NODES, int BTP, int MINB>
+static void run_buckets(umcg_plan* p, const double* xE, DevCtl* ctl, double* x1, void* KE, bool narrow,
+                        const GridK& gk, cudaStream_t st) {
     const uint32_t E = (uint32_t)p->n_epochs;
     static DeviceOnce configured;
     configured([] {
-        UMCG_CUDA(cudaFuncSetAttribute(k_bucket<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        UMCG_CUDA(cudaFuncSetAttribute(k_bucket<int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        UMCG_CUDA(cudaFuncSetAttribute(k_bucket_tma<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        UMCG_CUDA(cudaFuncSetAttribute(k_bucket_tma<int16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        constexpr int kMaxDyn = MINB == 1 ? 224 * 1024 : 112 * 1024;
+        UMCG_CUDA(cudaFuncSetAttribute(k_bucket<int32_t, CAP, NODES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       200 * 1024));
+        UMCG_CUDA(cudaFuncSetAttribute(k_bucket<int16_t, CAP, NODES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       200 * 1024));
+        UMCG_CUDA(cudaFuncSetAttribute(k_bucket_tma<int32_t, CAP, NODES, BTP, MINB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDyn));
+        UMCG_CUDA(cudaFuncSetAttribute(k_bucket_tma<int16_t, CAP, NODES, BTP, MINB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDyn));
     });
-    const size_t tma_smem = kBucketNodes * 8 + 2 * (size_t)tma_stage_bytes(E);
+    const size_t tma_smem = NODES * 8 + 2 * (size_t)tma_stage_bytes<CAP>(E);
     // persistent two-stage bulk-copy kernel for the regular buckets; when its
-    // staging does not fit (> 170 epochs, ~700M vertices) every bucket takes
+    // staging does not fit (many epochs, ~700M vertices) every bucket takes
     // the one-bucket-per-CTA kernel below
-    const bool pipe = E + 1 <= BTP && p->n_regular > 0 && tma_smem <= 112 * 1024;
+    const bool pipe = E + 1 <= BTP && p->n_regular > 0 && tma_smem <= (MINB == 1 ? 224 : 112) * 1024;
     if (pipe) {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const unsigned g = (unsigned)std::min<uint64_t>(p->n_regular, (uint64_t)sms * 2);
+        const unsigned g = (unsigned)std::min<uint64_t>(p->n_regular, (uint64_t)sms * MINB);
         auto launch = [&](auto* ke) {
             using KT = std::remove_pointer_t<decltype(ke)>;
-            k_bucket_tma<KT><<<g, BTP, tma_smem, st>>>(xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E,
-                                                      p->d_bct.as<uint2>(1), p->d_regular.as<uint32_t>(1),
-                                                      (uint32_t)p->n_regular, p->d_lnode.as<uint16_t>(1),
-                                                      p->d_lslot.as<uint16_t>(1), p->d_seg.as<uint32_t>(1), ctl, x1,
-                                                      ke, gk);
+            k_bucket_tma<KT, CAP, NODES, BTP, MINB><<<g, BTP, tma_smem, st>>>(
+                xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E, p->d_bct.as<uint2>(1), p->d_regular.as<uint32_t>(1),
+                (uint32_t)p->n_regular, p->d_lnode.as<uint16_t>(1), p->d_lslot.as<uint16_t>(1),
+                p->d_seg.as<uint32_t>(1), ctl, x1, ke, gk);
         };
         if (narrow) launch(static_cast<int16_t*>(KE));
         else launch(static_cast<int32_t*>(KE));
@@ -926,20 +929,28 @@ void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double*
     }
     if (!pipe || p->n_regular < p->n_buckets) {
         // all buckets (no pipeline possible) or the heavy single-slot buckets
-        const size_t smem = kBucketCap * 8 + kBucketNodes * 8 + (kBucketNodes + 2) * 4 + ((size_t)E + 1) * 8 +
-                            kBucketCap * 4 + 16;
+        const size_t smem = CAP * 8 + NODES * 8 + (NODES + 2) * 4 + ((size_t)E + 1) * 8 + CAP * 4 + 16;
         auto launch = [&](auto* ke) {
             using KT = std::remove_pointer_t<decltype(ke)>;
-            k_bucket<KT><<<(unsigned)p->n_buckets, BT, smem, st>>>(xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E,
-                                                                   p->d_bct.as<uint2>(1), p->d_lnode.as<uint16_t>(1),
-                                                                   p->d_lperm.as<uint16_t>(1),
-                                                                   p->d_seg.as<uint32_t>(1), ctl, x1, ke, pipe ? 1 : 0,
-                                                                   gk);
+            k_bucket<KT, CAP, NODES><<<(unsigned)p->n_buckets, BT, smem, st>>>(
+                xE, p->d_bk.as<uint32_t>(1), p->n_buckets, E, p->d_bct.as<uint2>(1), p->d_lnode.as<uint16_t>(1),
+                p->d_lperm.as<uint16_t>(1), p->d_seg.as<uint32_t>(1), ctl, x1, ke, pipe ? 1 : 0, gk);
         };
         if (narrow) launch(static_cast<int16_t*>(KE));
         else launch(static_cast<int32_t*>(KE));
         UMCG_LAUNCHED();
     }
+}
+
+void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double* x1, void* KE, bool narrow,
+                            int32_t* K1, int D1, cudaStream_t st) {
+    const GridK gk{K1, std::ldexp(1.0, 31 - (D1 < 1 ? 1 : D1))};
+    if (!p->n_buckets) return;
+    ProfScope ps_("k_bucket", st);
+    if (p->bucket_cap == kBucketCapL)
+        run_buckets<kBucketCapL, kBucketNodesL, 1024, 1>(p, xE, ctl, x1, KE, narrow, gk, st);
+    else
+        run_buckets<kBucketCap, kBucketNodes, 512, 2>(p, xE, ctl, x1, KE, narrow, gk, st);
 }
 bool resid_codes_tiles(umcg_plan* p, const void* KE, void* codes, bool narrow, bool fine, const StreamEncScratch& s,
                        cudaStream_t st) {
@@ -1021,7 +1032,7 @@ static void launch_ml(umcg_plan* p, const double* xE, const double* x1, DevCtl* 
     md.s1 = g.D == 3 ? (uint32_t)g.shape[2] : 1;
     md.s12 = g.D == 3 ? (uint32_t)(g.shape[1] * g.shape[2]) : g.D == 2 ? (uint32_t)g.shape[1] : 1;
     const uint32_t band_cap =
-        p->n_slots < (1u << 30) ? (uint32_t)std::min<uint64_t>((g.D == 1 ? 1 : 3) * (kBucketNodes + 2 * (uint64_t)md.w), 12288)
+        p->n_slots < (1u << 30) ? (uint32_t)std::min<uint64_t>((g.D == 1 ? 1 : 3) * (p->bucket_nodes + 2 * (uint64_t)md.w), 12288)
                                 : 0;
     const size_t smem = 8 * (size_t)band_cap;
     const double* tE = p->d_mlT.as<double>(1);

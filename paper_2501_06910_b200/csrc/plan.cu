@@ -283,14 +283,21 @@ void plan_build_buckets(umcg_plan* p, cudaStream_t st) {
     std::vector<uint32_t> seg(ns + 1);
     UMCG_CUDA(cudaMemcpyAsync(seg.data(), p->d_seg.get(), (ns + 1) * 4, cudaMemcpyDeviceToHost, st));
     UMCG_CUDA(cudaStreamSynchronize(st));
+    // bucket size (plan.h kBucketCapL): large buckets for big fields without heavy clusters
+    uint32_t max_slot = 0;
+    for (uint64_t k = 0; k < ns; ++k) max_slot = std::max(max_slot, seg[k + 1] - seg[k]);
+    const bool large = n >= (1ull << 26) && !p->has_coords && max_slot <= 64;
+    p->bucket_cap = large ? kBucketCapL : kBucketCap;
+    p->bucket_nodes = large ? kBucketNodesL : kBucketNodes;
+    const uint32_t cap = p->bucket_cap, cap_nodes = p->bucket_nodes;
     std::vector<uint32_t> bnode;
     uint64_t j = 0;
     while (j < ns) {
         const uint64_t j0 = j;
         bnode.push_back((uint32_t)j0);
-        if (seg[j0 + 1] - seg[j0] > kBucketCap) { j = j0 + 1; continue; }
+        if (seg[j0 + 1] - seg[j0] > cap) { j = j0 + 1; continue; }
         ++j;
-        while (j < ns && j - j0 < kBucketNodes && seg[j + 1] - seg[j0] <= kBucketCap) ++j;
+        while (j < ns && j - j0 < cap_nodes && seg[j + 1] - seg[j0] <= cap) ++j;
     }
     const uint64_t B = bnode.size();
     bnode.push_back((uint32_t)ns);
@@ -303,7 +310,7 @@ void plan_build_buckets(umcg_plan* p, cudaStream_t st) {
     {
         std::vector<uint32_t> reg;
         for (uint64_t b = 0; b < B; ++b)
-            if (tab[b + 1] - tab[b] <= kBucketCap) reg.push_back((uint32_t)b);
+            if (tab[b + 1] - tab[b] <= cap) reg.push_back((uint32_t)b);
         p->n_regular = reg.size();
         uint32_t* dr = p->d_regular.as<uint32_t>(reg.size() + 1);
         if (!reg.empty()) UMCG_CUDA(cudaMemcpyAsync(dr, reg.data(), reg.size() * 4, cudaMemcpyHostToDevice, st));

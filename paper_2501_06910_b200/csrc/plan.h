@@ -45,6 +45,7 @@ struct umcg_plan {
     // epoch's window (L2 resident).
     uint64_t n_buckets = 0;
     uint64_t n_epochs = 0;
+    uint32_t bucket_cap = 4096, bucket_nodes = 1016;  // kBucketCap / kBucketCapL (and slots)
     umcg::DevBuf d_srcE;     // u32 [n]    vertex at layout-E position p
     umcg::DevBuf d_dstE;     // u32 [n]    layout-E position of vertex i
     umcg::DevBuf d_ech;      // u32 [E*(B+1)] offset of bucket b inside epoch e's block
@@ -86,10 +87,19 @@ uint64_t mapping_digest_host32(int mode, uint64_t n, const uint32_t* assign, uin
 // Build perm / seg_off from d_node on the plan (stable radix sort by slot),
 // then the bucketed layout (plan_build_buckets).
 void plan_build_segments(umcg_plan* p, cudaStream_t st);
-constexpr uint32_t kBucketCap = 4096;   // vertices per bucket (smem staging)
+constexpr uint32_t kBucketCap = 4096;   // vertices per bucket (smem staging; two 512-thread CTAs per SM)
 constexpr uint64_t kEpoch = 1ull << 22;  // vertices per epoch of layout E
 constexpr uint32_t kMaxEpochs = 2048;    // k_bucket stages per-epoch chunk prefixes
 constexpr uint32_t kBucketNodes = 1016; // slots per bucket
+// Large buckets for big uniform meshes: 8192 vertices / 2032 slots, one
+// 1024-thread CTA per SM (A/B, config 3: k_bucket_tma 0.696 -> 0.665 ms and,
+// through the longer runs of a vertex tile in a bucket chunk,
+// k_resid_codes_sr 0.455 -> 0.387 ms; compress 2.415 -> 2.328 ms). Meshes
+// with heavy clusters lose with one CTA per SM (a long ordered sum stalls the
+// whole CTA: config 2 0.48 -> 0.57 ms), and so do smaller fields and
+// multilinear plans (wider x1 bands per bucket): plan_build_buckets picks.
+constexpr uint32_t kBucketCapL = 8192;
+constexpr uint32_t kBucketNodesL = 2032;
 #ifndef UMCG_RTILE_BITS
 #define UMCG_RTILE_BITS 15
 #endif
