@@ -88,7 +88,10 @@ uint64_t mapping_digest_host32(int mode, uint64_t n, const uint32_t* assign, uin
 // then the bucketed layout (plan_build_buckets).
 void plan_build_segments(umcg_plan* p, cudaStream_t st);
 constexpr uint32_t kBucketCap = 4096;   // vertices per bucket (smem staging; two 512-thread CTAs per SM)
-constexpr uint64_t kEpoch = 1ull << 22;  // vertices per epoch of layout E
+#ifndef UMCG_EPOCH_BITS
+#define UMCG_EPOCH_BITS 22
+#endif
+constexpr uint64_t kEpoch = 1ull << UMCG_EPOCH_BITS;  // vertices per epoch of layout E
 constexpr uint32_t kMaxEpochs = 2048;    // k_bucket stages per-epoch chunk prefixes
 constexpr uint32_t kBucketNodes = 1016; // slots per bucket
 // Large buckets for big uniform meshes: 8192 vertices / 2032 slots, one
