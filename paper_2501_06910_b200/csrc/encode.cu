@@ -51,14 +51,12 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_tiles(const T* __restrict__
 constexpr int FT = 4;  // tiles per CTA of k_rle_tiles_fast: every code load in flight up front
 template <class T>
 __global__ void __launch_bounds__(ENC_THREADS) k_rle_tiles_fast(const T* __restrict__ codes, uint64_t n,
-                                                                RleSum* __restrict__ sums) {
+                                                                RleSum* __restrict__ sums,
+                                                                uint32_t* __restrict__ redo,
+                                                                uint32_t* __restrict__ n_redo) {
     static_assert(ENC_ITEMS == 8, "8-bit zero masks");
     constexpr int NW = ENC_THREADS / 32;
-    using WR = cub::WarpReduce<RleSum>;
-    __shared__ typename WR::TempStorage wtmp[NW];
-    __shared__ RleSum wsum[FT][NW];
     __shared__ uint32_t wpart[FT][NW][4];  // per warp: code bytes, first / last nonzero, any bad
-    __shared__ uint32_t tbad[FT];
     const uint64_t T_ = (n + ENC_TILE - 1) / ENC_TILE;
     const uint64_t tile0 = (uint64_t)blockIdx.x * FT;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -151,8 +149,9 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_tiles_fast(const T* __restr
             l = max(l, wpart[t][w][2]);
             bad |= wpart[t][w][3];
         }
-        tbad[t] = bad;
-        if (!bad) {
+        if (bad) {
+            redo[atomicAdd(n_redo, 1u)] = (uint32_t)tile;
+        } else {
             RleSum S;
             S.lz = f;
             S.tz = (uint64_t)(ENC_TILE - 1 - l);
@@ -163,38 +162,26 @@ __global__ void __launch_bounds__(ENC_THREADS) k_rle_tiles_fast(const T* __restr
             sums[tile] = S;
         }
     }
-    __syncthreads();
-    // the other tiles: the exact RleSum reduction, inline (token-dense streams
-    // have many; a second pass over a list of them measured slower): warp
-    // reductions of every such tile, then one thread per tile composes the
-    // warps' summaries in order
-    bool any = false;
-#pragma unroll
-    for (int t = 0; t < FT; ++t) {
-        const uint64_t tile = tile0 + t;
-        if (tile >= T_ || !tbad[t]) continue;
-        any = true;
-        T u[ENC_ITEMS];
-        if constexpr (P16) {
-            const uint32_t w[4] = {pw[t].x, pw[t].y, pw[t].z, pw[t].w};
-#pragma unroll
-            for (int k = 0; k < ENC_ITEMS; ++k) u[k] = (T)(w[k >> 1] >> (16 * (k & 1)));
-        } else {
-#pragma unroll
-            for (int k = 0; k < ENC_ITEMS; ++k) u[k] = v[t][k];
-        }
-        const RleSum r = WR(wtmp[warp]).Reduce(thread_summary(u, cnt[t], (uint32_t)tile), RleComposeOp());
-        if (lane == 0) wsum[t][warp] = r;
-        __syncwarp();
-    }
-    if (!any) return;
-    __syncthreads();
-    if (threadIdx.x < FT && tile0 + threadIdx.x < T_ && tbad[threadIdx.x]) {
-        const int t = threadIdx.x;
-        RleSum tot = wsum[t][0];
-#pragma unroll
-        for (int w = 1; w < NW; ++w) tot = rle_compose(tot, wsum[t][w]);
-        sums[tile0 + t] = tot;
+}
+
+// The exact summaries of the listed tiles (grid-stride: the count is on the device).
+template <class T>
+__global__ void __launch_bounds__(ENC_THREADS) k_rle_tiles_redo(const T* __restrict__ codes, uint64_t n,
+                                                                RleSum* __restrict__ sums,
+                                                                const uint32_t* __restrict__ redo,
+                                                                const uint32_t* __restrict__ n_redo) {
+    using BR = cub::BlockReduce<RleSum, ENC_THREADS>;
+    __shared__ typename BR::TempStorage tmp;
+    const uint32_t cnt = *n_redo;
+    for (uint32_t i = blockIdx.x; i < cnt; i += gridDim.x) {
+        const uint64_t tile = redo[i];
+        const uint64_t first = tile * ENC_TILE + (uint64_t)threadIdx.x * ENC_ITEMS;
+        T v[ENC_ITEMS];
+        const int c = load_items(codes, n, first, v);
+        const RleSum s = thread_summary(v, c, (uint32_t)tile);
+        const RleSum tot = BR(tmp).Reduce(s, RleComposeOp());
+        if (threadIdx.x == 0) sums[tile] = tot;
+        __syncthreads();
     }
 }
 
@@ -633,6 +620,8 @@ StreamEncScratch stream_enc_carve(void* base, uint64_t n) {
     s.pos = reinterpret_cast<uint64_t*>(p);
     p += T * sizeof(uint64_t);
     s.glist = reinterpret_cast<uint32_t*>(p);
+    p += T * sizeof(uint32_t);
+    s.n_redo = reinterpret_cast<uint32_t*>(p);  // inside the scratch's 4096-byte slack
     return s;
 }
 
@@ -646,10 +635,20 @@ static void plan_impl(const T* codes, uint64_t n, const StreamEncScratch& s, Dev
     }
     const uint64_t C = cdiv(T_, CH);
     UMCG_CUDA(cudaMemsetAsync(&ctl->aux[4 + comp], 0, 8, st));
-    if (fast)
-        k_rle_tiles_fast<T><<<(unsigned)cdiv(T_, (uint64_t)FT), ENC_THREADS, 0, st>>>(codes, n, s.sums);
-    else
+    if (fast) {
+        // the tile list doubles as the redo list (k_rle_states fills it afterwards)
+        UMCG_CUDA(cudaMemsetAsync(s.n_redo, 0, 4, st));
+        k_rle_tiles_fast<T><<<(unsigned)cdiv(T_, (uint64_t)FT), ENC_THREADS, 0, st>>>(codes, n, s.sums, s.glist,
+                                                                                    s.n_redo);
+        UMCG_LAUNCHED();
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        k_rle_tiles_redo<T><<<(unsigned)std::min<uint64_t>(T_, (uint64_t)sms * 8), ENC_THREADS, 0, st>>>(
+            codes, n, s.sums, s.glist, s.n_redo);
+    } else {
         k_rle_tiles<T><<<(unsigned)T_, ENC_THREADS, 0, st>>>(codes, n, s.sums);
+    }
     UMCG_LAUNCHED();
     k_rle_chunks<<<(unsigned)C, CH, 0, st>>>(s.sums, T_, s.csum);
     UMCG_LAUNCHED();

@@ -19,6 +19,7 @@ struct StreamEncScratch {
     uint64_t* lit_total = nullptr;  // [T]   literal byte totals, keyed by opening tile
     uint64_t* pos = nullptr;        // [T+1] stream position of each tile's first byte (writers)
     uint32_t* glist = nullptr;      // [T]   tiles for the general writer (count in ctl->aux[4+comp])
+    uint32_t* n_redo = nullptr;     // [1]   tiles whose summary needs the exact reduction (list in glist)
 };
 size_t stream_enc_scratch_bytes(uint64_t n);
 StreamEncScratch stream_enc_carve(void* base, uint64_t n);
