@@ -594,48 +594,77 @@ __global__ void k_ml_prep(const double* __restrict__ coords, const uint32_t* __r
 // bucket-local slot ln sits at (1 - c_0 + b_0) Lb + w + ln + (b_1 - c_1) s1 +
 // (b_2 - c_2) (3-D; c_d the cell bits), or at the global index m - sum c_d
 // s_d + sum b_d s_d.
+// Per-bucket constants of ml_eval_prepared (hoisted out of the element loop:
+// the strides and band offsets would otherwise be reloaded from the kernel
+// parameters for every element).
+struct MlEvalC {
+    int32_t so[3];   // corner offsets in the staged bands per axis
+    uint64_t go[3];  // corner offsets in x1 per axis
+    int32_t Lb, w;
+    int32_t s1;      // axis-1 stride (3-D) / axis-0 cell step
+    uint64_t st0, st1;
+};
 template <int D>
-__device__ __forceinline__ double ml_eval_prepared(const MlGrid& g, const double* __restrict__ x1, const double* xs,
-                                                   bool staged, const MlDims& md, uint32_t m, uint32_t ln,
-                                                   const double* t, uint32_t cb) {
+__device__ __forceinline__ MlEvalC ml_eval_const(const MlGrid& g, const MlDims& md) {
+    MlEvalC c{};
+    c.Lb = md.Lb;
+    c.w = md.w;
+    if (D == 3) {
+        c.st1 = g.shape[2];
+        c.st0 = g.shape[1] * g.shape[2];
+        c.s1 = (int32_t)c.st1;
+        c.so[0] = g.shape[0] > 1 ? md.Lb : 0;
+        c.so[1] = g.shape[1] > 1 ? (int32_t)c.st1 : 0;
+        c.so[2] = g.shape[2] > 1 ? 1 : 0;
+        c.go[0] = g.shape[0] > 1 ? c.st0 : 0;
+        c.go[1] = g.shape[1] > 1 ? c.st1 : 0;
+        c.go[2] = g.shape[2] > 1 ? 1 : 0;
+    } else if (D == 2) {
+        c.st0 = g.shape[1];
+        c.so[0] = g.shape[0] > 1 ? md.Lb : 0;
+        c.so[1] = g.shape[1] > 1 ? 1 : 0;
+        c.go[0] = g.shape[0] > 1 ? g.shape[1] : 0;
+        c.go[1] = g.shape[1] > 1 ? 1 : 0;
+    } else {
+        c.so[0] = g.shape[0] > 1 ? 1 : 0;
+        c.go[0] = (uint64_t)c.so[0];
+    }
+    return c;
+}
+
+template <int D, bool STAGED>
+__device__ __forceinline__ double ml_eval_prepared(const MlEvalC& k, const double* __restrict__ x1, const double* xs,
+                                                   uint32_t m, uint32_t ln, const double* t, uint32_t cb) {
     double om[3] = {1, 1, 1};
 #pragma unroll
     for (int d = 0; d < D; ++d) om[d] = __dsub_rn(1.0, t[d]);
-    int32_t so[3] = {0, 0, 0};
-    uint64_t go[3] = {0, 0, 0};
     int32_t ib;
     uint64_t lb;
     const int c0 = cb & 1, c1 = (cb >> 1) & 1, c2 = (cb >> 2) & 1;
     if (D == 3) {
-        const uint64_t st1 = g.shape[2], st0 = g.shape[1] * g.shape[2];
-        so[0] = g.shape[0] > 1 ? md.Lb : 0;
-        so[1] = g.shape[1] > 1 ? (int32_t)st1 : 0;
-        so[2] = g.shape[2] > 1 ? 1 : 0;
-        go[0] = g.shape[0] > 1 ? st0 : 0;
-        go[1] = g.shape[1] > 1 ? st1 : 0;
-        go[2] = g.shape[2] > 1 ? 1 : 0;
-        ib = (1 - c0) * md.Lb + md.w + (int32_t)ln - c1 * (int32_t)st1 - c2;
-        lb = (uint64_t)m - c0 * st0 - c1 * st1 - c2;
+        ib = (1 - c0) * k.Lb + k.w + (int32_t)ln - c1 * k.s1 - c2;
+        lb = (uint64_t)m - c0 * k.st0 - c1 * k.st1 - c2;
     } else if (D == 2) {
-        so[0] = g.shape[0] > 1 ? md.Lb : 0;
-        so[1] = g.shape[1] > 1 ? 1 : 0;
-        go[0] = g.shape[0] > 1 ? g.shape[1] : 0;
-        go[1] = g.shape[1] > 1 ? 1 : 0;
-        ib = (1 - c0) * md.Lb + md.w + (int32_t)ln - c1;
-        lb = (uint64_t)m - c0 * g.shape[1] - c1;
+        ib = (1 - c0) * k.Lb + k.w + (int32_t)ln - c1;
+        lb = (uint64_t)m - c0 * k.st0 - c1;
     } else {
-        so[0] = g.shape[0] > 1 ? 1 : 0;
-        go[0] = so[0];
-        ib = md.w + (int32_t)ln - c0;
+        ib = k.w + (int32_t)ln - c0;
         lb = (uint64_t)m - c0;
     }
     auto val = [&](unsigned corner) {
-        int32_t si = ib;
-        uint64_t gi = lb;
+        if (STAGED) {
+            int32_t si = ib;
 #pragma unroll
-        for (int d = 0; d < D; ++d)
-            if ((corner >> d) & 1u) { si += so[d]; gi += go[d]; }
-        return staged ? xs[si] : __ldg(&x1[gi]);
+            for (int d = 0; d < D; ++d)
+                if ((corner >> d) & 1u) si += k.so[d];
+            return xs[si];
+        } else {
+            uint64_t gi = lb;
+#pragma unroll
+            for (int d = 0; d < D; ++d)
+                if ((corner >> d) & 1u) gi += k.go[d];
+            return __ldg(&x1[gi]);
+        }
     };
     double acc = 0.0;
     if (D == 1) {
@@ -663,6 +692,16 @@ __device__ __forceinline__ double ml_eval_prepared(const MlGrid& g, const double
         if (w != 0.0) acc = __dadd_rn(acc, __dmul_rn(w, v[corner]));
     }
     return acc;
+}
+
+// The generic evaluation from the coordinates, for a vertex whose slot is not
+// a cell hint (out of line: it would crowd the hot loop's registers).
+template <int D>
+__device__ __noinline__ double ml_eval_generic(const MlGrid& g, const double* __restrict__ x1,
+                                               const double* __restrict__ coords, uint32_t v) {
+    double pc[3] = {0, 0, 0};
+    for (int d = 0; d < D; ++d) pc[d] = __ldg(&coords[(uint64_t)v * D + d]);
+    return multilinear_eval_c<D>(g.axes, g.axis_off, g.shape, GlobalCorners{x1}, pc, g.inv_cell, g.scale);
 }
 
 // MODE 0: KE[p] = lattice(xE[p] - g(p)) (compute_residuals, interp.hpp:161-170)
@@ -704,42 +743,41 @@ __global__ void __launch_bounds__(ML_T, UMCG_ML_MINB) k_ml_bucket(const double* 
     // U vertices per thread and pass, every load issued before any is
     // evaluated (the kernel is bound by the latency of these streams)
     constexpr int U = UMCG_ML_U;
-    for (uint32_t e = warp; e < E; e += ML_T / 32) {
-        const uint2 c0 = __ldg(&ch[e]), c1 = __ldg(&ch[e + 1]);
-        for (uint32_t l0 = c0.x + lane; l0 < c1.x; l0 += 32 * U) {
-            double t[U][3], xv[U];
-            uint32_t ln[U], cb[U];
+    const MlEvalC kc = ml_eval_const<DD>(g, mdb);
+    auto run = [&](auto staged_tag) {
+        constexpr bool STAGED = decltype(staged_tag)::value;
+        for (uint32_t e = warp; e < E; e += ML_T / 32) {
+            const uint2 c0 = __ldg(&ch[e]), c1 = __ldg(&ch[e + 1]);
+            for (uint32_t l0 = c0.x + lane; l0 < c1.x; l0 += 32 * U) {
+                double t[U][3], xv[U];
+                uint32_t ln[U], cb[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t l = l0 + 32 * u;
-                const bool ok = l < c1.x;
-                const uint64_t p = c0.y + (l - c0.x);
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t l = l0 + 32 * u;
+                    const bool ok = l < c1.x;
+                    const uint64_t p = c0.y + (l - c0.x);
 #pragma unroll
-                for (int d = 0; d < 3; ++d) t[u][d] = (d < DD && ok) ? __ldcs(&tE[d * n + p]) : 0.0;
-                ln[u] = ok ? __ldg(&lnode[s0 + l]) : 0u;
-                cb[u] = ok ? __ldcs(&bE[p]) : 0u;
-                xv[u] = (MODE == 0 && ok) ? __ldcs(&xE[p]) : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t l = l0 + 32 * u;
-                if (l >= c1.x) break;
-                const uint64_t p = c0.y + (l - c0.x);
-                double gv;
-                if (cb[u] & 0x80u) {  // slot is not a cell hint: the generic evaluation from the coordinates
-                    const uint32_t v = __ldg(&srcE[p]);
-                    double pc[3] = {0, 0, 0};
-                    for (int d = 0; d < DD; ++d) pc[d] = __ldg(&coords[(uint64_t)v * DD + d]);
-                    gv = multilinear_eval_c<DD>(g.axes, g.axis_off, g.shape, GlobalCorners{x1}, pc, g.inv_cell,
-                                                g.scale);
-                } else {
-                    gv = ml_eval_prepared<DD>(g, x1, xs, staged, mdb, j0 + ln[u], ln[u], t[u], cb[u]);
+                    for (int d = 0; d < 3; ++d) t[u][d] = (d < DD && ok) ? __ldcs(&tE[d * n + p]) : 0.0;
+                    ln[u] = ok ? __ldg(&lnode[s0 + l]) : 0u;
+                    cb[u] = ok ? __ldcs(&bE[p]) : 0u;
+                    xv[u] = (MODE == 0 && ok) ? __ldcs(&xE[p]) : 0.0;
                 }
-                if (MODE == 0) KE[p] = resid_k<KT>(__dsub_rn(xv[u], gv), bin, inv, tau, ctl);
-                else gE[p] = gv;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t l = l0 + 32 * u;
+                    if (l >= c1.x) break;
+                    const uint64_t p = c0.y + (l - c0.x);
+                    const double gv = (cb[u] & 0x80u)  // slot is not a cell hint: from the coordinates
+                                          ? ml_eval_generic<DD>(g, x1, coords, __ldg(&srcE[p]))
+                                          : ml_eval_prepared<DD, STAGED>(kc, x1, xs, j0 + ln[u], ln[u], t[u], cb[u]);
+                    if (MODE == 0) KE[p] = resid_k<KT>(__dsub_rn(xv[u], gv), bin, inv, tau, ctl);
+                    else gE[p] = gv;
+                }
             }
         }
-    }
+    };
+    if (staged) run(std::true_type{});
+    else run(std::false_type{});
 }
 
 // x'_i = approx_i + x2'_i (pipeline.hpp:206-208) with approx gathered from
