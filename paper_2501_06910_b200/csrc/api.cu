@@ -480,7 +480,7 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
             // the exact reduction and k_rle_tiles is faster: config 5 256^3 5.80 -> 5.36 ms)
             stream_plan_u16(static_cast<uint16_t*>(codes[c]), ncode[c], es[c], ctl, c, sc, fine);
         else if (wide[c]) stream_plan_u64(static_cast<uint64_t*>(codes[c]), ncode[c], es[c], ctl, c, sc);
-        else stream_plan_u32(static_cast<uint32_t*>(codes[c]), ncode[c], es[c], ctl, c, sc);
+        else stream_plan_u32(static_cast<uint32_t*>(codes[c]), ncode[c], es[c], ctl, c, sc, fine && c == 0);
     }
     tr.dev("plans", st);
     if (overlap) tr.dev("grid plan(sg)", sg);

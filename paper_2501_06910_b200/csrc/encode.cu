@@ -698,7 +698,7 @@ static void write_impl(const T* codes, uint64_t n, const StreamEncScratch& s, De
 }
 
 void stream_plan_u32(const uint32_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
-                     cudaStream_t st) { plan_impl(c, n, s, ctl, comp, st); }
+                     cudaStream_t st, bool fast) { plan_impl(c, n, s, ctl, comp, st, fast); }
 void stream_plan_u64(const uint64_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
                      cudaStream_t st) { plan_impl(c, n, s, ctl, comp, st); }
 void stream_plan_u16(const uint16_t* c, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,

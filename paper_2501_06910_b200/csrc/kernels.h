@@ -33,7 +33,7 @@ void stream_encode_u64(const uint64_t* codes, uint64_t n, const StreamEncScratch
                        int comp, uint8_t* dst, bool dst_off_from_ctl, cudaStream_t st);
 // Phase split used by the pipeline (summaries/scan first, layout, then write).
 void stream_plan_u32(const uint32_t* codes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl,
-                     int comp, cudaStream_t st);
+                     int comp, cudaStream_t st, bool fast = false);
 // fast: tile summaries by k_rle_tiles_fast (pays when zero codes are rare --
 // fine residual bounds; token-dense streams are faster with k_rle_tiles)
 void stream_plan_u16(const uint16_t* codes, uint64_t n, const StreamEncScratch& s, DevCtl* ctl, int comp,
