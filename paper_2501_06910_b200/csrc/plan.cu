@@ -232,6 +232,8 @@ uint64_t mapping_digest_host32(int mode, uint64_t n, const uint32_t* assign, uin
 }
 
 void plan_build_segments(umcg_plan* p, cudaStream_t st) {
+    // the device sorts (cub, int item counts) and u32 layout positions bound a plan's size
+    if (p->n > (uint64_t)INT32_MAX) fail(UMCG_INVALID_ARGUMENT, "more than 2^31-1 vertices per plan");
     const uint64_t n = p->n, ns = p->n_slots;
     uint32_t* node = p->d_node.as<uint32_t>(n ? n : 1);
     uint32_t* perm = p->d_perm.as<uint32_t>(n ? n : 1);
@@ -441,7 +443,7 @@ umcg_plan* plan_create_host(const umcg_grid_desc* g, const umcg_mapping_desc* m,
         upload_grid(p, g);
         p->mode = m->mode ? 1 : 0;
         p->n = m->n_vertices;
-        if (p->n >= (1ull << 32)) fail(UMCG_INVALID_ARGUMENT, "more than 2^32-1 vertices per plan");
+        if (p->n > (uint64_t)INT32_MAX) fail(UMCG_INVALID_ARGUMENT, "more than 2^31-1 vertices per plan");
         if (p->mode == 1) {
             p->n_slots = m->n_visited;
             p->n_visited = m->n_visited;
@@ -489,7 +491,7 @@ umcg_plan* plan_build_gpu(const umcg_grid_desc* g0, uint64_t n, const double* d_
                           int keep_coords) {
     if (!g0 || !d_coords) fail(UMCG_INVALID_ARGUMENT, "NULL argument");
     if (!(thr > 0.0) || thr > 1.0) fail(UMCG_ERROR, "seed mode threshold must be in (0, 1]");
-    if (n >= (1ull << 32)) fail(UMCG_INVALID_ARGUMENT, "more than 2^32-1 vertices per plan");
+    if (n > (uint64_t)INT32_MAX) fail(UMCG_INVALID_ARGUMENT, "more than 2^31-1 vertices per plan");
     const int D = g0->dim;
     if (D != 2 && D != 3) fail(UMCG_MALFORMED_FILE, "grid dimension must be 2 or 3");
     cudaStream_t st = 0;
