@@ -90,6 +90,7 @@ __device__ uint64_t write_comp_header(uint8_t* a, uint64_t o, int codec, int pre
 // Computes stream offsets (consumed by the stream writers) and writes every
 // header byte of the UMCZ archive.
 __global__ void k_layout_archive(HdrArgs h, DevCtl* ctl, uint8_t* a) {
+    if (pass_skipped(ctl)) return;
     if (threadIdx.x | blockIdx.x) return;
     uint64_t o = 0;
     a[0] = 'U'; a[1] = 'M'; a[2] = 'C'; a[3] = 'Z';
@@ -167,6 +168,15 @@ DevCtl read_ctl(umcg_plan* p, DevCtl* d, cudaStream_t st) {
     UMCG_CUDA(cudaMemcpyAsync(h, d, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
     UMCG_CUDA(cudaStreamSynchronize(st));
     return *h;
+}
+
+// After the bucket pass: ctl->skip = a rerun is certain -- an escape or
+// regime verdict for a component on its fast path (mask bits 0 / 1), or the
+// int16 residual path overflowing (bit 2). The kernels of the rest of the pass
+// then return at once (common.cuh pass_skipped).
+__global__ void k_gate(DevCtl* ctl, int mask) {
+    ctl->skip = ((mask & 1) && ctl->need_serial[0]) || ((mask & 2) && ctl->need_serial[1]) ||
+                ((mask & 4) && ctl->need_wide);
 }
 
 void init_ctl(DevCtl* d, cudaStream_t st) {
@@ -330,6 +340,7 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
         c.err = 0;
         c.need_serial[0] = c.need_serial[1] = 0;
         c.need_wide = 0;
+        c.skip = 0;
         c.max_abs_k[0] = c.max_abs_k[1] = 0;
         for (int k = 0; k < 2; ++k) c.stream_len[k] = c.n_esc[k] = c.payload_len[k] = c.stream_off[k] = 0;
         c.archive_len = 0;
@@ -380,6 +391,13 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
         fill_nearest_visited(p->d_seg.as<uint32_t>(1), n1, p->shape[p->dim - 1], x1, st);
     if (ml_part && !m.serial[1] && !m.lossless[1] && !m.reuse)
         ml_residuals(p, p->scratch_c.as<double>(n + 4), x1, ctl, Kp, narrow, st);
+    if (part && !m.reuse) {
+        // a rerun already certain after the bucket pass skips the rest of this one
+        const int mask = (!m.serial[0] && !m.lossless[0] ? 1 : 0) | (!m.serial[1] && !m.lossless[1] ? 2 : 0) |
+                         (narrow ? 4 : 0);
+        k_gate<<<1, 1, 0, st>>>(ctl, mask);
+        UMCG_LAUNCHED();
+    }
 
     // component specs (grid_codec_spec, pipeline.hpp:96-110)
     const int pred1 = p->mode == 1 ? 1 : 2;
@@ -464,7 +482,7 @@ DevCtl compress_pass(umcg_plan* p, const umcg_params& prm, const void* d_x, int 
     bool fused_resid = part && !m.serial[1] && !m.lossless[1];
     if (fused_resid) {
         // q = K2_i - K2_{i-1} back in vertex order (+ RLE tile summaries, partition.cu)
-        fused_resid = resid_codes_tiles(p, Kp, codes[1], narrow, fine, es[1], st);
+        fused_resid = resid_codes_tiles(p, Kp, codes[1], narrow, fine, es[1], ctl, st);
         tr.dev("resid codes", st);
     } else if (!m.serial[1] && !m.lossless[1]) {
         codes_lossy_residual(rs, n, ctl, static_cast<uint32_t*>(codes[1]), st);

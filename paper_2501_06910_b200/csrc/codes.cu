@@ -121,7 +121,8 @@ __global__ void __launch_bounds__(THREADS) k_stencil_nd(const int32_t* __restric
 // division per element). Missing neighbours (index -1) contribute 0, which
 // is exactly the reference's skipped masks (codec.hpp:70-75).
 __global__ void __launch_bounds__(THREADS) k_stencil_3d(const int32_t* __restrict__ K, uint64_t d0, uint64_t d1,
-                                                       uint64_t d2, uint32_t* __restrict__ codes) {
+                                                       uint64_t d2, uint32_t* __restrict__ codes, const DevCtl* ctl) {
+    if (pass_skipped(ctl)) return;
     const uint64_t k = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
     if (k >= d2) return;
     const uint64_t j = blockIdx.y, i = blockIdx.z;
@@ -512,7 +513,7 @@ void codes_lossy_values(const double* v, uint64_t n, int pred, const NdShape& sh
             const uint64_t d0 = sh.D == 3 ? sh.dims[0] : 1, d1 = sh.D == 3 ? sh.dims[1] : sh.dims[0];
             const uint64_t d2 = sh.dims[sh.D - 1];
             dim3 g((unsigned)cdiv(d2, THREADS), (unsigned)d1, (unsigned)d0);
-            k_stencil_3d<<<g, THREADS, 0, st>>>(kbuf, d0, d1, d2, codes);
+            k_stencil_3d<<<g, THREADS, 0, st>>>(kbuf, d0, d1, d2, codes, ctl);
         } else {
             k_stencil_nd<<<blocks(n), THREADS, 0, st>>>(kbuf, n, sh, codes);
         }

@@ -334,6 +334,7 @@ struct DevCtl {
     // per-component fast-path verdicts
     int need_serial[2];                   // escape / regime violation: redo exactly
     int need_wide;                        // narrow (int16) residual path overflowed: redo in int32
+    int skip;                             // a rerun is certain: the rest of this pass returns at once
     unsigned long long max_abs_k[2];      // |K| maxima (decode regime check)
     // stream lengths and archive layout
     uint64_t stream_len[2];
@@ -346,6 +347,10 @@ struct DevCtl {
 };
 
 __device__ __forceinline__ void set_err(DevCtl* c, int e) { atomicCAS(&c->err, 0, e); }
+// The kernels after the bucket pass return at once when its verdicts make a
+// rerun certain (api.cu k_gate; escapes, int16 overflow): nothing they would
+// write is used, and their inputs may be incomplete.
+__device__ __forceinline__ bool pass_skipped(const DevCtl* c) { return c && c->skip; }
 
 // Lattice index + bound check in one step (codec.hpp:305-314 on the
 // lattice): K = round(fl(r / bin)) and err = |r - K*bin|, bin = 2*tau.

@@ -28,7 +28,8 @@ namespace {
 // Phase 1: tile summaries (independent tiles).
 template <class T>
 __global__ void __launch_bounds__(ENC_THREADS) k_rle_tiles(const T* __restrict__ codes, uint64_t n,
-                                                           RleSum* __restrict__ sums) {
+                                                           RleSum* __restrict__ sums, const DevCtl* ctl) {
+    if (pass_skipped(ctl)) return;
     using BR = cub::BlockReduce<RleSum, ENC_THREADS>;
     __shared__ typename BR::TempStorage tmp;
     const uint64_t tile = blockIdx.x;
@@ -53,8 +54,9 @@ template <class T>
 __global__ void __launch_bounds__(ENC_THREADS) k_rle_tiles_fast(const T* __restrict__ codes, uint64_t n,
                                                                 RleSum* __restrict__ sums,
                                                                 uint32_t* __restrict__ redo,
-                                                                uint32_t* __restrict__ n_redo) {
+                                                                uint32_t* __restrict__ n_redo, const DevCtl* ctl) {
     static_assert(ENC_ITEMS == 8, "8-bit zero masks");
+    if (pass_skipped(ctl)) return;
     constexpr int NW = ENC_THREADS / 32;
     __shared__ uint32_t wpart[FT][NW][4];  // per warp: code bytes, first / last nonzero, any bad
     const uint64_t T_ = (n + ENC_TILE - 1) / ENC_TILE;
@@ -222,6 +224,7 @@ __global__ void __launch_bounds__(CH) k_rle_states(const RleSum* __restrict__ su
                                                    const RleSum* __restrict__ csum, RleState* __restrict__ states,
                                                    uint64_t* __restrict__ lit_total, uint32_t* __restrict__ glist,
                                                    DevCtl* ctl, int comp) {
+    if (pass_skipped(ctl)) return;
     using BS = cub::BlockScan<RleSum, CH>;
     __shared__ typename BS::TempStorage tmp;
     const uint64_t t = blockIdx.x * (uint64_t)CH + threadIdx.x;
@@ -256,6 +259,7 @@ __device__ __forceinline__ uint64_t state_pos(const RleState& s, const uint64_t*
 // the writers start from one load instead of a chain of dependent ones.
 __global__ void k_rle_pos(const RleState* __restrict__ states, const uint64_t* __restrict__ lit_total, uint64_t T,
                           const DevCtl* __restrict__ ctl, int comp, uint64_t* __restrict__ pos) {
+    if (pass_skipped(ctl)) return;
     const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (t < T) pos[t] = state_pos(states[t], lit_total);
     else if (t == T) pos[t] = ctl->stream_len[comp];
@@ -324,6 +328,7 @@ __global__ void __launch_bounds__(ENC_THREADS, UMCG_WF_MINB) k_rle_write_fast(co
                                                                const uint64_t* __restrict__ tpos,
                                                                const DevCtl* __restrict__ ctl, int comp,
                                                                uint8_t* __restrict__ dst, int off_from_ctl) {
+    if (pass_skipped(ctl)) return;
     constexpr uint32_t CAP = ENC_TILE * (sizeof(T) == 8 ? 10 : 5) + 96;
     using BS32 = cub::BlockScan<uint32_t, ENC_THREADS>;
     __shared__ typename BS32::TempStorage tmp;
@@ -591,6 +596,7 @@ __global__ void __launch_bounds__(ENC_THREADS, 6) k_rle_write_general(const T* _
                                                            const DevCtl* __restrict__ ctl, int comp, const uint32_t* __restrict__ glist,
                                                            const uint64_t* __restrict__ tpos,
                                                            uint8_t* __restrict__ dst, int off_from_ctl) {
+    if (pass_skipped(ctl)) return;
     const uint32_t cnt = (uint32_t)ctl->aux[4 + comp];
     for (uint32_t i = blockIdx.x; i < cnt; i += gridDim.x) {
         general_tile<T>(glist[i], codes, n, states, sums, lit_total, ctl, comp, tpos, dst, off_from_ctl);
@@ -639,7 +645,7 @@ static void plan_impl(const T* codes, uint64_t n, const StreamEncScratch& s, Dev
         // the tile list doubles as the redo list (k_rle_states fills it afterwards)
         UMCG_CUDA(cudaMemsetAsync(s.n_redo, 0, 4, st));
         k_rle_tiles_fast<T><<<(unsigned)cdiv(T_, (uint64_t)FT), ENC_THREADS, 0, st>>>(codes, n, s.sums, s.glist,
-                                                                                    s.n_redo);
+                                                                                    s.n_redo, ctl);
         UMCG_LAUNCHED();
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
@@ -647,7 +653,7 @@ static void plan_impl(const T* codes, uint64_t n, const StreamEncScratch& s, Dev
         k_rle_tiles_redo<T><<<(unsigned)std::min<uint64_t>(T_, (uint64_t)sms * 8), ENC_THREADS, 0, st>>>(
             codes, n, s.sums, s.glist, s.n_redo);
     } else {
-        k_rle_tiles<T><<<(unsigned)T_, ENC_THREADS, 0, st>>>(codes, n, s.sums);
+        k_rle_tiles<T><<<(unsigned)T_, ENC_THREADS, 0, st>>>(codes, n, s.sums, ctl);
     }
     UMCG_LAUNCHED();
     k_rle_chunks<<<(unsigned)C, CH, 0, st>>>(s.sums, T_, s.csum);

@@ -793,7 +793,9 @@ __global__ void k_add_gathered(const double* __restrict__ gE, const uint32_t* __
 template <class KT, class CT>
 __global__ void __launch_bounds__(ENC_THREADS) k_resid_codes(const uint32_t* __restrict__ dst,
                                                             const KT* __restrict__ Kp, uint64_t n,
-                                                            CT* __restrict__ codes, RleSum* __restrict__ sums) {
+                                                            CT* __restrict__ codes, RleSum* __restrict__ sums,
+                                                            const DevCtl* ctl) {
+    if (pass_skipped(ctl)) return;
     using BR = cub::BlockReduce<RleSum, ENC_THREADS>;
     __shared__ typename BR::TempStorage tmp;
     const uint64_t tile = blockIdx.x;
@@ -863,7 +865,8 @@ __global__ void __launch_bounds__(NT, 1) k_resid_codes_sr(const uint32_t* __rest
                                                           const uint16_t* __restrict__ rLt,
                                                           const uint32_t* __restrict__ dst,
                                                           const KT* __restrict__ Kp, uint64_t n,
-                                                          CT* __restrict__ codes) {
+                                                          CT* __restrict__ codes, const DevCtl* ctl) {
+    if (pass_skipped(ctl)) return;
     extern __shared__ __align__(16) unsigned char smem[];
     KT* ks = reinterpret_cast<KT*>(smem);
     const uint64_t t0 = (uint64_t)blockIdx.x * kRTile;
@@ -991,7 +994,7 @@ void bucket_means_residuals(umcg_plan* p, const double* xE, DevCtl* ctl, double*
         run_buckets<kBucketCap, kBucketNodes, 512, 2>(p, xE, ctl, x1, KE, narrow, gk, st);
 }
 bool resid_codes_tiles(umcg_plan* p, const void* KE, void* codes, bool narrow, bool fine, const StreamEncScratch& s,
-                       cudaStream_t st) {
+                       const DevCtl* ctl, cudaStream_t st) {
     const uint64_t T = cdiv(p->n, ENC_TILE);
     if (!T) return true;
     ProfScope ps_("k_resid_codes", st);
@@ -1011,17 +1014,19 @@ bool resid_codes_tiles(umcg_plan* p, const void* KE, void* codes, bool narrow, b
         const unsigned g = (unsigned)cdiv(p->n, (uint64_t)kRTile);
         k_resid_codes_sr<int16_t, uint16_t, NT><<<g, NT, kRTile * 2, st>>>(
             p->d_rPt.as<uint32_t>(1), p->d_rLt.as<uint16_t>(1), p->d_dstE.as<uint32_t>(1),
-            static_cast<const int16_t*>(KE), p->n, static_cast<uint16_t*>(codes));
+            static_cast<const int16_t*>(KE), p->n, static_cast<uint16_t*>(codes), ctl);
         UMCG_LAUNCHED();
         return false;
     }
 #endif
     if (narrow)
         k_resid_codes<int16_t, uint16_t><<<(unsigned)T, ENC_THREADS, 0, st>>>(
-            p->d_dstE.as<uint32_t>(1), static_cast<const int16_t*>(KE), p->n, static_cast<uint16_t*>(codes), s.sums);
+            p->d_dstE.as<uint32_t>(1), static_cast<const int16_t*>(KE), p->n, static_cast<uint16_t*>(codes), s.sums,
+            ctl);
     else
         k_resid_codes<int32_t, uint32_t><<<(unsigned)T, ENC_THREADS, 0, st>>>(
-            p->d_dstE.as<uint32_t>(1), static_cast<const int32_t*>(KE), p->n, static_cast<uint32_t*>(codes), s.sums);
+            p->d_dstE.as<uint32_t>(1), static_cast<const int32_t*>(KE), p->n, static_cast<uint32_t*>(codes), s.sums,
+            ctl);
     UMCG_LAUNCHED();
     return true;
 }

@@ -139,7 +139,7 @@ void bucket_means_residuals(umcg_plan* p, const double* xp, DevCtl* ctl, double*
 // runs the stream plan over the codes).
 // fine: a fine relative bound (zero codes rare): the run-sorted kernel, summaries by the fast pass.
 bool resid_codes_tiles(umcg_plan* p, const void* Kp, void* codes, bool narrow, bool fine, const StreamEncScratch& s,
-                       cudaStream_t st);
+                       const DevCtl* ctl, cudaStream_t st);
 // Multilinear g in bucket order (layout E): residual lattice indices KE
 // (compress) and the recomposition x' = g + x2' (decompress, gE [n] scratch).
 void ml_residuals(umcg_plan* p, const double* xE, const double* x1, DevCtl* ctl, void* KE, bool narrow,
