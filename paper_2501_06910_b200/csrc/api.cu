@@ -948,11 +948,21 @@ static bool fast_decompress(umcg_plan* p, const uint8_t* d_ar, uint64_t p1, cons
     dec_prepare(src2, dec_tiles(h2.stream_len), st2, &c[3], ss);
     int64_t* P = p->kbuf.as<int64_t>(2 * n1);
     int32_t* K1 = p->codes1.as<int32_t>(n1);
-    dec_fused(DEC_P64, src1, dec_tiles(h1.stream_len), n1, st1, &c[1], nullptr, nullptr, 0.0, bin1, nullptr, P, sh);
     const uint64_t flat[1] = {n1};
+    const NdShape shape1 = pred1 == 2 ? make_shape(h1.D, h1.dims) : make_shape(1, flat);
     int16_t* K16 = p->dx1.as<int16_t>(n1 + 2);
-    nd_from_prefix(P, n1, pred1 == 2 ? make_shape(h1.D, h1.dims) : make_shape(1, flat), P + n1, K1, K16, &c[1],
-                   sh);
+    static const bool nd3_off = std::getenv("UMCG_ND3_OFF") != nullptr;  // (A/B knob)
+    if (nd3_supported(shape1) && !nd3_off) {
+        // 3-D grid: codes as int32 -> per-plane 2-D prefix -> outer scan
+        auto* Q = reinterpret_cast<int32_t*>(P);
+        dec_fused(DEC_Q32, src1, dec_tiles(h1.stream_len), n1, st1, &c[1], nullptr, nullptr, 0.0, bin1, nullptr, P,
+                  sh);
+        nd3_from_codes(Q, shape1, Q + n1, K1, K16, &c[1], sh);
+    } else {
+        dec_fused(DEC_P64, src1, dec_tiles(h1.stream_len), n1, st1, &c[1], nullptr, nullptr, 0.0, bin1, nullptr, P,
+                  sh);
+        nd_from_prefix(P, n1, shape1, P + n1, K1, K16, &c[1], sh);
+    }
     if (g_dec_trace) g_dec_trace->dev("grid done", sh);
     p->side.link(sh, st, 3);
     p->side.link(ss, st, 1);

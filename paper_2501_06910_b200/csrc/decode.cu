@@ -242,8 +242,64 @@ __device__ __forceinline__ void global_window(const uint8_t* __restrict__ U, uin
 
 __device__ __forceinline__ int64_t zz_dec32(uint32_t v) { return (int64_t)(v >> 1) ^ -(int64_t)(v & 1u); }
 
+// Byte-parallel (count, sum of zigzag values) of the codes that end in the
+// thread's 32 bytes, for the common case of codes of at most 2 bytes (the
+// thread's window) -- no per-byte walk. With per-byte flag words (bit 7 of
+// each byte): t = code ends here, s0 = code starts here (previous byte ends
+// one), s1 = second byte of a code. A code c = p0 + 128 p1 (7-bit payloads)
+// decodes to unzigzag(c) = +((p0 >> 1) + 64 p1) when p0 is even and
+// -((p0 >> 1) + 64 p1) - 1 when odd, so the sum is four byte-masked dot
+// products (dp4a against 0/1 byte masks) per word:
+//   sum = A0 - 2 A0odd + 64 (A1 - 2 A1odd) - n_odd.
+// Included bytes: the partial code entering from the halo (bytes of W[3]
+// after its last end) and every byte of the thread up to its last end.
+// Returns false (nothing computed) when a code of 3+ bytes touches the
+// thread, or its first or last word has no code end: the walk then runs.
+__device__ __forceinline__ bool thread_counts_swar(const uint32_t (&W)[12], uint32_t& cnt, int64_t& sum) {
+    constexpr uint32_t M7 = 0x80808080u;
+    const uint32_t t3 = ~W[3] & M7, t11 = ~W[11] & M7;
+    if (!t3 || !t11) return false;
+    const uint32_t keepH = (t3 & 0x80000000u) ? 0u : (0xffffffffu << (32 - __clz(t3)));
+    const uint32_t keepL = (t11 & 0x80000000u) ? 0xffffffffu : (0xffffffffu >> __clz(t11));
+    uint32_t tp = M7, s0p = 0, s1p = 0, wp = 0, more = 0;
+    uint32_t a0 = 0, a0o = 0, a1 = 0, a1o = 0, no = 0, c = 0;
+#pragma unroll
+    for (int q = 3; q < 12; ++q) {
+        const uint32_t w = W[q];
+        const uint32_t t = ~w & M7;
+        const uint32_t s0 = __funnelshift_l(tp, t, 8);
+        const uint32_t s1 = __funnelshift_l(s0p, s0, 8) & ~s0;
+        const uint32_t keep = q == 3 ? keepH : (q == 11 ? keepL : 0xffffffffu);
+        more |= __funnelshift_l(s1p, s1, 8) & ~s0 & keep;  // third byte of a code
+        const uint32_t sel0 = (s0 & keep) >> 7, sel1 = (s1 & keep) >> 7;
+        const uint32_t odd0 = sel0 & w, odd1 = sel1 & __funnelshift_l(wp, w, 8);
+        const uint32_t p0 = (w >> 1) & 0x3f3f3f3fu, p = w & 0x7f7f7f7fu;
+        a0 = __dp4a(p0, sel0, a0);
+        a0o = __dp4a(p0, odd0, a0o);
+        a1 = __dp4a(p, sel1, a1);
+        a1o = __dp4a(p, odd1, a1o);
+        no = __dp4a(odd0, 0x01010101u, no);
+        if (q >= 4) c += __popc(t);
+        tp = t;
+        s0p = s0;
+        s1p = s1;
+        wp = w;
+    }
+    if (more) return false;
+    cnt = c;
+    sum = (int64_t)a0 - 2 * (int64_t)a0o + 64 * ((int64_t)a1 - 2 * (int64_t)a1o) - (int64_t)no;
+    return true;
+}
+
 __device__ __forceinline__ CS thread_counts(const uint8_t* sb, int my, bool* bad, bool* wide, int64_t base,
                                             uint64_t ulen) {
+    uint32_t W[12];
+    smem_window(sb, my, W);
+    {
+        uint32_t c2;
+        int64_t s2;
+        if (thread_counts_swar(W, c2, s2)) return CS{c2, s2};
+    }
     uint32_t c = 0;
     // fast path: codes of <= 4 bytes ending in 32 bytes, so |sum| < 8 * 2^27
     // fits 32-bit accumulation (the emit runs predicated on every byte)
@@ -252,8 +308,6 @@ __device__ __forceinline__ CS thread_counts(const uint8_t* sb, int my, bool* bad
         ++c;
         s32 += (int32_t)(v >> 1) ^ -(int32_t)(v & 1u);
     };
-    uint32_t W[12];
-    smem_window(sb, my, W);
     if (thread_walk_fast(W, f32)) return CS{c, (int64_t)s32};
     int64_t s = 0;
     auto f = [&](uint32_t v) {
@@ -264,6 +318,12 @@ __device__ __forceinline__ CS thread_counts(const uint8_t* sb, int my, bool* bad
     return CS{c, s};
 }
 
+// Per-thread prefix inside a tile, packed into one int64: sum * 2^16 + count
+// (count <= 8192 codes per 8 KiB tile, |sum| < 2^44), so the block scan and
+// the hand-off to k_dec_out move 8 bytes per thread instead of 16.
+__device__ __forceinline__ int64_t cs_pack(const CS& a) { return (int64_t)((uint64_t)a.sum << 16) + (int64_t)a.cnt; }
+__device__ __forceinline__ CS cs_unpack(int64_t v) { return CS{(uint64_t)(v & 0xffff), v >> 16}; }
+
 // Tile aggregates (count, sum of zigzag values); tiles past the stream end
 // (T is a host-side bound when the stream is resolved on the device) add 0.
 // thr: every thread's exclusive (count, sum) inside its tile, so k_dec_out
@@ -271,8 +331,8 @@ __device__ __forceinline__ CS thread_counts(const uint8_t* sb, int my, bool* bad
 #ifndef UMCG_AGG_MINB
 #define UMCG_AGG_MINB 6  // 6 CTAs per SM (A/B: 1 -> 0.178 ms, 6 or 8 -> 0.168 ms; 8 spills)
 #endif
-__global__ void __launch_bounds__(RT, UMCG_AGG_MINB) k_dec_agg(const DecSrc src, CS* __restrict__ aggs, CS* __restrict__ thr,
-                                               DevCtl* ctl) {
+__global__ void __launch_bounds__(RT, UMCG_AGG_MINB) k_dec_agg(const DecSrc src, CS* __restrict__ aggs,
+                                                               int64_t* __restrict__ thr, DevCtl* ctl) {
     const uint8_t* U;
     uint64_t ulen;
     resolve_src(src, U, ulen);
@@ -280,7 +340,7 @@ __global__ void __launch_bounds__(RT, UMCG_AGG_MINB) k_dec_agg(const DecSrc src,
         if (threadIdx.x == 0) aggs[blockIdx.x] = CS{0, 0};
         return;
     }
-    using BS = cub::BlockScan<CS, RT>;
+    using BS = cub::BlockScan<int64_t, RT>;
     __shared__ typename BS::TempStorage tmp;
     __shared__ __align__(16) uint8_t sb[RHALO + RTILE + 16];
     const int64_t base = (int64_t)blockIdx.x * (int64_t)RTILE;
@@ -290,9 +350,9 @@ __global__ void __launch_bounds__(RT, UMCG_AGG_MINB) k_dec_agg(const DecSrc src,
     const CS mine = thread_counts(sb, RHALO + threadIdx.x * RB, &bad, &wide, base, ulen);
     if (bad) set_err(ctl, DE_CORRUPT_VARINT);
     if (wide) ctl->aux[7] = 1;
-    CS excl, t;
-    BS(tmp).ExclusiveScan(mine, excl, CS{0, 0}, CSAdd(), t);
-    if (threadIdx.x == 0) aggs[blockIdx.x] = t;
+    int64_t excl, t;
+    BS(tmp).ExclusiveSum(cs_pack(mine), excl, t);
+    if (threadIdx.x == 0) aggs[blockIdx.x] = cs_unpack(t);
     thr[blockIdx.x * (uint64_t)RT + threadIdx.x] = excl;
 }
 
@@ -309,15 +369,17 @@ __global__ void __launch_bounds__(RT, UMCG_DEC_MINB) k_dec_out(const DecSrc src,
                                                double bin1, double bin, double* __restrict__ out,
                                                int64_t* __restrict__ P64, const DevCtl* __restrict__ kctl,
                                                const int16_t* __restrict__ K16, const CS* __restrict__ raw,
-                                               const CS* __restrict__ thr) {
+                                               const int64_t* __restrict__ thr) {
     // lattice indices of the tile in element order, int16 (the decoded K of
     // a lossy residual stream fits; a tile that does not takes the direct
     // path below)
-    __shared__ int16_t kb[MODE == DEC_P64 ? 1 : RTILE];
-    // P64 mode: K - (tile prefix) as int32, written out coalesced afterwards
-    __shared__ int32_t kp[MODE == DEC_P64 ? RTILE : 1];
+    constexpr bool PREFIX = MODE == DEC_P64 || MODE == DEC_Q32;
+    __shared__ int16_t kb[PREFIX ? 1 : RTILE];
+    // P64 mode: K - (tile prefix) as int32, written out coalesced afterwards;
+    // Q32 mode: the zigzag-decoded code itself
+    __shared__ int32_t kp[PREFIX ? RTILE : 1];
 #ifdef UMCG_DEC_PAD  // (A/B: shared-memory footprint vs the L1 left for the K1 gathers)
-    __shared__ volatile uint8_t pad_[MODE == DEC_P64 ? 1 : UMCG_DEC_PAD];
+    __shared__ volatile uint8_t pad_[PREFIX ? 1 : UMCG_DEC_PAD];
     if (threadIdx.x == 0) pad_[0] = 0;
 #endif
     // int32 tables: switch to the int16 copy when the grid's max|K1| (known
@@ -332,7 +394,7 @@ __global__ void __launch_bounds__(RT, UMCG_DEC_MINB) k_dec_out(const DecSrc src,
     uint32_t W[12];
     global_window(U, ulen, base + threadIdx.x * RB, l2_evict_first(), W);
     // the thread's prefix inside the tile and the tile's total (k_dec_agg)
-    const CS excl = thr[blockIdx.x * (uint64_t)RT + threadIdx.x];
+    const CS excl = cs_unpack(thr[blockIdx.x * (uint64_t)RT + threadIdx.x]);
     const CS tot = raw[blockIdx.x];
     const CS tp = pre[blockIdx.x];
     const uint64_t e0 = tp.cnt;           // first element of the tile
@@ -347,7 +409,9 @@ __global__ void __launch_bounds__(RT, UMCG_DEC_MINB) k_dec_out(const DecSrc src,
         K += zz_dec32(v);
         const uint64_t a = (uint64_t)(K < 0 ? -K : K);
         kmax = a > kmax ? a : kmax;
-        if (MODE == DEC_P64) {
+        if (MODE == DEC_Q32) {
+            kp[li] = (int32_t)zz_dec32(v);  // exact: |q| <= 2^31 for a u32 code
+        } else if (MODE == DEC_P64) {
             const int64_t d = K - tp.sum;
             ovf |= d != (int64_t)(int32_t)d;
             kp[li] = (int32_t)d;
@@ -362,6 +426,16 @@ __global__ void __launch_bounds__(RT, UMCG_DEC_MINB) k_dec_out(const DecSrc src,
         kmax = b2 > kmax ? b2 : kmax;
     }
     if ((threadIdx.x & 31) == 0 && kmax > ctl->max_abs_k[1]) atomicMax(&ctl->max_abs_k[1], (unsigned long long)kmax);
+    if (MODE == DEC_Q32) {
+        __syncthreads();
+        int32_t* Q = reinterpret_cast<int32_t*>(P64);
+        const uint32_t cnt = (uint32_t)tot.cnt;
+        for (uint32_t e = threadIdx.x; e < cnt; e += RT) {
+            const uint64_t i = e0 + e;
+            if (i < n) Q[i] = kp[e];
+        }
+        return;
+    }
     if (MODE == DEC_P64) {
         if (__syncthreads_or(ovf)) {  // rare: walk again, writing in the walk's order
             li = li0;
@@ -593,6 +667,132 @@ __global__ void __launch_bounds__(256) k_nd_outer(const int64_t* __restrict__ Kw
     if ((threadIdx.x & 31) == 0 && amax > ctl->max_abs_k[0]) atomicMax(&ctl->max_abs_k[0], (unsigned long long)amax);
 }
 
+// 3-D inverse Lorenzo from the decoded codes q (int32, row-major d0 x d1 x d2,
+// d2 <= 256), first stage: per plane i, the 2-D inclusive prefix over (j, k),
+//   S[i, j, k] = sum_{j' <= j, k' <= k} q[i, j', k'] = K[i] - K[i - 1].
+// One CTA per plane, thread = column k. The plane is walked in tiles of 32
+// rows whose 32 loads per thread are all in flight (the next tile's loads are
+// issued before the current tile is processed), so a plane costs d1 / 32
+// memory round trips instead of one per row: column prefix in registers,
+// row prefix by a shared-memory transpose (lane = 8 consecutive columns,
+// in-lane prefix + one warp scan), S stored coalesced.
+// Arithmetic is int32 modulo 2^32; it is exact when sum over the plane of |q|
+// < 2^31 (then no partial sum leaves int32), which every plane checks -- a
+// plane that does not fails the fast decompress's verdict (max|K| := ~0).
+constexpr int ND3_T = 256;
+constexpr int ND3_R = 32;
+__global__ void __launch_bounds__(ND3_T) k_nd3_plane(const int32_t* __restrict__ Q, uint32_t d1, uint32_t d2,
+                                                     int32_t* __restrict__ S, DevCtl* ctl) {
+    __shared__ __align__(16) int32_t tile[ND3_R][ND3_T];
+    const uint64_t plane = (uint64_t)d1 * d2;
+    const int32_t* q = Q + (uint64_t)blockIdx.x * plane;
+    int32_t* s = S + (uint64_t)blockIdx.x * plane;
+    const uint32_t k = threadIdx.x;
+    const bool col = k < d2;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int32_t nx[ND3_R];
+    auto load = [&](uint32_t j0) {
+#pragma unroll
+        for (int r = 0; r < ND3_R; ++r) nx[r] = (col && j0 + r < d1) ? __ldcs(&q[(uint64_t)(j0 + r) * d2 + k]) : 0;
+    };
+    load(0);
+    uint64_t asum = 0;
+    int32_t carry = 0;
+    for (uint32_t j0 = 0; j0 < d1; j0 += ND3_R) {
+        int32_t v[ND3_R];
+#pragma unroll
+        for (int r = 0; r < ND3_R; ++r) v[r] = nx[r];
+        if (j0 + ND3_R < d1) load(j0 + ND3_R);
+#pragma unroll
+        for (int r = 0; r < ND3_R; ++r) {
+            asum += (uint32_t)(v[r] < 0 ? -v[r] : v[r]);
+            carry += v[r];  // column prefix (mod 2^32)
+            tile[r][k] = carry;
+        }
+        __syncthreads();
+        // row prefix of rows warp, warp + 8, ...: lane owns columns 8 lane .. 8 lane + 7
+#pragma unroll
+        for (int rr = 0; rr < ND3_R / (ND3_T / 32); ++rr) {
+            const int r = warp + rr * (ND3_T / 32);
+            const uint32_t j = j0 + r;
+            const int4 a = *reinterpret_cast<const int4*>(&tile[r][8 * lane]);
+            const int4 b = *reinterpret_cast<const int4*>(&tile[r][8 * lane + 4]);
+            int32_t x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int u = 1; u < 8; ++u) x[u] += x[u - 1];
+            int32_t p = x[7];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(0xffffffffu, p, o);
+                if (lane >= o) p += y;
+            }
+            const int32_t off = p - x[7];  // exclusive prefix of the lane totals
+            if (j < d1) {
+                int32_t* row = s + (uint64_t)j * d2;
+                const uint32_t kb = 8 * lane;
+                if ((d2 & 7) == 0 && kb + 8 <= d2) {
+                    int4 o0 = make_int4(x[0] + off, x[1] + off, x[2] + off, x[3] + off);
+                    int4 o1 = make_int4(x[4] + off, x[5] + off, x[6] + off, x[7] + off);
+                    if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
+                        *reinterpret_cast<int4*>(row + kb) = o0;
+                        *reinterpret_cast<int4*>(row + kb + 4) = o1;
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) row[kb + u] = x[u] + off;
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (kb + u < d2) row[kb + u] = x[u] + off;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // exactness: with sum |q| < 2^31 over the plane no partial sum wrapped
+    if (__syncthreads_or(asum >= 0x80000000ull) && threadIdx.x == 0) atomicMax(&ctl->max_abs_k[0], ~0ull);
+}
+
+// Second stage: K[i] = sum_{i' <= i} S[i'] along the outer axis (exact int64
+// accumulation of the exact S), threads own (j, k) columns; planes in tiles
+// of 32 with all loads of the next tile in flight. int32 + int16 tables and
+// max|K|.
+__global__ void __launch_bounds__(256) k_nd3_outer(const int32_t* __restrict__ S, uint32_t d0, uint64_t plane,
+                                                  int32_t* __restrict__ K32, int16_t* __restrict__ K16,
+                                                  DevCtl* ctl) {
+    const uint64_t c = blockIdx.x * 256ull + threadIdx.x;
+    uint64_t amax = 0;
+    if (c < plane) {
+        int32_t nx[ND3_R];
+        auto load = [&](uint32_t i0) {
+#pragma unroll
+            for (int u = 0; u < ND3_R; ++u) nx[u] = i0 + u < d0 ? __ldcs(&S[(i0 + u) * plane + c]) : 0;
+        };
+        load(0);
+        int64_t acc = 0;
+        for (uint32_t i0 = 0; i0 < d0; i0 += ND3_R) {
+            int32_t v[ND3_R];
+#pragma unroll
+            for (int u = 0; u < ND3_R; ++u) v[u] = nx[u];
+            if (i0 + ND3_R < d0) load(i0 + ND3_R);
+#pragma unroll
+            for (int u = 0; u < ND3_R; ++u) {
+                if (i0 + u >= d0) break;
+                acc += v[u];
+                K32[(i0 + u) * plane + c] = (int32_t)acc;
+                if (K16) K16[(i0 + u) * plane + c] = (int16_t)acc;
+                const uint64_t a = (uint64_t)(acc < 0 ? -acc : acc);
+                amax = a > amax ? a : amax;
+            }
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        const uint64_t b = __shfl_xor_sync(0xffffffffu, amax, o);
+        amax = b > amax ? b : amax;
+    }
+    if ((threadIdx.x & 31) == 0 && amax > ctl->max_abs_k[0]) atomicMax(&ctl->max_abs_k[0], (unsigned long long)amax);
+}
+
 __global__ void k_k32(const int64_t* __restrict__ K, uint64_t n, int32_t* __restrict__ K32,
                       int16_t* __restrict__ K16, DevCtl* ctl) {
     const uint64_t i = blockIdx.x * 256ull + threadIdx.x;
@@ -632,7 +832,7 @@ void dec_prepare(const DecSrc& src, uint64_t T, void* status, DevCtl* ctl, cudaS
         return;
     }
     CS* raw = aggs + T + 1;
-    CS* thr = raw + T;
+    auto* thr = reinterpret_cast<int64_t*>(raw + T);
     {
         ProfScope ps_a("k_dec_agg", st);
         k_dec_agg<<<(unsigned)T, RT, 0, st>>>(src, raw, thr, ctl);
@@ -651,10 +851,13 @@ void dec_fused(int mode, const DecSrc& src, uint64_t T, uint64_t n, void* status
     auto* aggs = static_cast<CS*>(status);
     if (!prepared) dec_prepare(src, T, status, ctl, st);
     if (!T) return;
-    ProfScope ps_o(mode == DEC_P64 ? "k_dec_out_grid" : "k_dec_out", st);
+    ProfScope ps_o(mode == DEC_P64 || mode == DEC_Q32 ? "k_dec_out_grid" : "k_dec_out", st);
     const CS* raw = aggs + T + 1;
-    const CS* thr = raw + T;
-    if (mode == DEC_P64)
+    const auto* thr = reinterpret_cast<const int64_t*>(raw + T);
+    if (mode == DEC_Q32)
+        k_dec_out<DEC_Q32, int32_t><<<(unsigned)T, RT, 0, st>>>(src, n, aggs, ctl, node, K1, bin1, bin, out, P64,
+                                                               nullptr, nullptr, raw, thr);
+    else if (mode == DEC_P64)
         k_dec_out<DEC_P64, int32_t><<<(unsigned)T, RT, 0, st>>>(src, n, aggs, ctl, node, K1, bin1, bin, out, P64,
                                                                nullptr, nullptr, raw, thr);
     else if (mode == DEC_VALUES)
@@ -717,6 +920,21 @@ void nd_from_prefix(const int64_t* P, uint64_t n, const NdShape& sh, int64_t* Kw
         src = Kw;
     }
     k_k32<<<g, 256, 0, st>>>(src, n, K32, K16, ctl);
+    UMCG_LAUNCHED();
+}
+
+bool nd3_supported(const NdShape& sh) {
+    return sh.D == 3 && sh.dims[2] >= 1 && sh.dims[2] <= (uint64_t)ND3_T && sh.dims[1] < (1ull << 31) &&
+           sh.dims[0] < (1ull << 31);
+}
+
+void nd3_from_codes(const int32_t* Q, const NdShape& sh, int32_t* S, int32_t* K32, int16_t* K16, DevCtl* ctl,
+                    cudaStream_t st) {
+    const uint64_t d0 = sh.dims[0], d1 = sh.dims[1], d2 = sh.dims[2];
+    if (!d0 || !d1 || !d2) return;
+    k_nd3_plane<<<(unsigned)d0, ND3_T, 0, st>>>(Q, (uint32_t)d1, (uint32_t)d2, S, ctl);
+    UMCG_LAUNCHED();
+    k_nd3_outer<<<(unsigned)cdiv(d1 * d2, 256), 256, 0, st>>>(S, (uint32_t)d0, d1 * d2, K32, K16, ctl);
     UMCG_LAUNCHED();
 }
 

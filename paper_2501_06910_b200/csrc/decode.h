@@ -7,7 +7,8 @@ namespace umcg {
 
 // DEC_RECOMPOSE_GE: x'_i = g_i + fl(K * bin) with g prepared in layout E
 // (multilinear g, partition.cu): node = dstE, K1 = the fp64 gE array.
-enum DecMode : int { DEC_P64 = 0, DEC_VALUES = 1, DEC_RECOMPOSE = 2, DEC_RECOMPOSE16 = 3, DEC_RECOMPOSE_GE = 4 };
+enum DecMode : int { DEC_P64 = 0, DEC_VALUES = 1, DEC_RECOMPOSE = 2, DEC_RECOMPOSE16 = 3, DEC_RECOMPOSE_GE = 4,
+                     DEC_Q32 = 5 };  // Q32: the zigzag-decoded codes as int32 (P64 points to them)
 
 // One RLE token (stream.cu): literal data offset, unpacked offset, length
 // (bit 63 set for literal tokens).
@@ -64,6 +65,11 @@ void dec_prepare(const DecSrc& src, uint64_t t_tiles, void* status, DevCtl* ctl,
 // max|K| -> ctl->max_abs_k[0]. Kw is int64 scratch [n] (unused when D == 1).
 void nd_from_prefix(const int64_t* P, uint64_t n, const NdShape& sh, int64_t* Kw, int32_t* K32, int16_t* K16,
                     DevCtl* ctl,
+                    cudaStream_t st);
+// 3-D grids with d2 <= 1024: N-D inclusive prefix straight from the decoded
+// codes Q (DEC_Q32), int32 plane prefixes S [n] as scratch.
+bool nd3_supported(const NdShape& sh);
+void nd3_from_codes(const int32_t* Q, const NdShape& sh, int32_t* S, int32_t* K32, int16_t* K16, DevCtl* ctl,
                     cudaStream_t st);
 void k32_to_f64(const int32_t* K, uint64_t n, double bin, double* x, cudaStream_t st);
 
