@@ -302,26 +302,59 @@ __device__ __forceinline__ uint32_t put_code(uint8_t* o, T v) {
 
 // Staged bytes out[ao, ao+len) -> d[0, len) where ao = d & 15: 16-byte
 // stores for the aligned middle, bytes at the two ends.
+template <uint32_t NT = ENC_THREADS>
 __device__ __forceinline__ void copy_out16(const uint8_t* out, uint32_t ao, uint32_t len, uint8_t* d) {
     uint8_t* g = d - ao;  // 16-byte aligned
     const uint32_t end = ao + len;
     const uint32_t w0 = (ao + 15) / 16, w1 = end / 16;  // full words [w0, w1)
     if (w0 >= w1) {
-        for (uint32_t k = ao + threadIdx.x; k < end; k += ENC_THREADS) g[k] = out[k];
+        for (uint32_t k = ao + threadIdx.x; k < end; k += NT) g[k] = out[k];
         return;
     }
-    for (uint32_t k = ao + threadIdx.x; k < 16 * w0; k += ENC_THREADS) g[k] = out[k];
-    for (uint32_t k = 16 * w1 + threadIdx.x; k < end; k += ENC_THREADS) g[k] = out[k];
+    for (uint32_t k = ao + threadIdx.x; k < 16 * w0; k += NT) g[k] = out[k];
+    for (uint32_t k = 16 * w1 + threadIdx.x; k < end; k += NT) g[k] = out[k];
     const uint4* s4 = reinterpret_cast<const uint4*>(out);
     uint4* g4 = reinterpret_cast<uint4*>(g);
-    for (uint32_t w = w0 + threadIdx.x; w < w1; w += ENC_THREADS) g4[w] = s4[w];
+    for (uint32_t w = w0 + threadIdx.x; w < w1; w += NT) g4[w] = s4[w];
 }
 
-template <class T>
+// ITEMS consecutive codes of one thread (vector loads when whole and aligned).
+template <class T, int ITEMS>
+__device__ __forceinline__ int load_items_n(const T* codes, uint64_t n, uint64_t first, T (&v)[ITEMS]) {
+    if (first + ITEMS <= n && sizeof(T) == 2 && (first % 8) == 0 && ITEMS % 8 == 0) {
+#pragma unroll
+        for (int h = 0; h < ITEMS / 8; ++h) {
+            const uint4 a = __ldg(reinterpret_cast<const uint4*>(codes + first) + h);
+            const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[8 * h + k] = (T)(w[k >> 1] >> (16 * (k & 1)));
+        }
+        return ITEMS;
+    }
+    if (first + ITEMS <= n && sizeof(T) == 4 && (first % 4) == 0 && ITEMS % 4 == 0) {
+#pragma unroll
+        for (int h = 0; h < ITEMS / 4; ++h) {
+            const uint4 a = __ldg(reinterpret_cast<const uint4*>(codes + first) + h);
+            v[4 * h] = (T)a.x, v[4 * h + 1] = (T)a.y, v[4 * h + 2] = (T)a.z, v[4 * h + 3] = (T)a.w;
+        }
+        return ITEMS;
+    }
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const uint64_t i = first + k;
+        if (i < n) { v[k] = codes[i]; cnt = k + 1; } else { v[k] = 0; }
+    }
+    return cnt;
+}
+
 #ifndef UMCG_WF_MINB
 #define UMCG_WF_MINB 8  // 8 CTAs per SM (A/B: 6 -> 0.333 ms, 8 -> 0.303 ms for both writers' fast path)
 #endif
-__global__ void __launch_bounds__(ENC_THREADS, UMCG_WF_MINB) k_rle_write_fast(const T* __restrict__ codes, uint64_t n,
+// ITEMS codes per thread, ENC_TILE / ITEMS threads: the per-thread costs (block
+// scan, tile state, head arithmetic) are shared by ITEMS codes.
+template <class T, int ITEMS, int MINB>
+__global__ void __launch_bounds__(ENC_TILE / ITEMS, MINB) k_rle_write_fast(const T* __restrict__ codes, uint64_t n,
                                                                const RleState* __restrict__ states,
                                                                const RleSum* __restrict__ sums,
                                                                const uint64_t* __restrict__ lit_total,
@@ -329,16 +362,17 @@ __global__ void __launch_bounds__(ENC_THREADS, UMCG_WF_MINB) k_rle_write_fast(co
                                                                const DevCtl* __restrict__ ctl, int comp,
                                                                uint8_t* __restrict__ dst, int off_from_ctl) {
     if (pass_skipped(ctl)) return;
-    constexpr uint32_t CAP = ENC_TILE * (sizeof(T) == 8 ? 10 : 5) + 96;
-    using BS32 = cub::BlockScan<uint32_t, ENC_THREADS>;
+    constexpr uint32_t CAP = ENC_TILE * (sizeof(T) == 8 ? 10 : sizeof(T) == 2 ? 3 : 5) + 96;  // u16: <= 3 bytes per code
+    constexpr int NT = ENC_TILE / ITEMS;
+    using BS32 = cub::BlockScan<uint32_t, NT>;
     __shared__ typename BS32::TempStorage tmp;
     __shared__ __align__(16) uint8_t out[CAP];
 
     const uint64_t tile = blockIdx.x;
     // every load up front (codes too: they do not depend on the tile's kind)
-    const uint64_t first = tile * ENC_TILE + (uint64_t)threadIdx.x * ENC_ITEMS;
-    T v[ENC_ITEMS];
-    const int cnt = load_items(codes, n, first, v);
+    const uint64_t first = tile * ENC_TILE + (uint64_t)threadIdx.x * ITEMS;
+    T v[ITEMS];
+    const int cnt = load_items_n<T, ITEMS>(codes, n, first, v);
     const RleSum S = sums[tile];
     const RleState entry = states[tile];
     const uint64_t P0 = tpos[tile], P1 = tpos[tile + 1];
@@ -353,16 +387,16 @@ __global__ void __launch_bounds__(ENC_THREADS, UMCG_WF_MINB) k_rle_write_fast(co
     // the core [lz, tile_cnt - tz) is one literal segment
     const uint32_t tile_cnt = (uint32_t)min((uint64_t)ENC_TILE, n - tile * ENC_TILE);
     const uint32_t core_lo = (uint32_t)S.lz, core_hi = tile_cnt - (uint32_t)S.tz;
-    const uint32_t r0 = threadIdx.x * ENC_ITEMS;
+    const uint32_t r0 = threadIdx.x * ITEMS;
     // common case: all of the thread's items are in the core (no per-item checks)
-    const bool inner = cnt == ENC_ITEMS && r0 >= core_lo && r0 + ENC_ITEMS <= core_hi;
+    const bool inner = cnt == ITEMS && r0 >= core_lo && r0 + ITEMS <= core_hi;
     uint32_t w = 0;
     if (inner) {
 #pragma unroll
-        for (int k = 0; k < ENC_ITEMS; ++k) w += clen(v[k]);
+        for (int k = 0; k < ITEMS; ++k) w += clen(v[k]);
     } else {
 #pragma unroll
-        for (int k = 0; k < ENC_ITEMS; ++k) {
+        for (int k = 0; k < ITEMS; ++k) {
             const uint32_t r = r0 + k;
             if (k < cnt && r >= core_lo && r < core_hi) w += clen(v[k]);
         }
@@ -414,16 +448,16 @@ __global__ void __launch_bounds__(ENC_THREADS, UMCG_WF_MINB) k_rle_write_fast(co
     uint32_t pos = (uint32_t)(data_base - P0) + off;
     if (inner) {
 #pragma unroll
-        for (int k = 0; k < ENC_ITEMS; ++k) pos += put_code(o + pos, v[k]);
+        for (int k = 0; k < ITEMS; ++k) pos += put_code(o + pos, v[k]);
     } else {
 #pragma unroll
-        for (int k = 0; k < ENC_ITEMS; ++k) {
+        for (int k = 0; k < ITEMS; ++k) {
             const uint32_t r = r0 + k;
             if (k < cnt && r >= core_lo && r < core_hi) pos += put_code(o + pos, v[k]);
         }
     }
     __syncthreads();
-    copy_out16(out, ao, len, d);
+    copy_out16<NT>(out, ao, len, d);
 }
 
 // General writer: tiles with a zero run >= 8 strictly inside, and the last
@@ -688,8 +722,18 @@ static void write_impl(const T* codes, uint64_t n, const StreamEncScratch& s, De
     ProfScope ps_("k_rle_write", st);
     k_rle_pos<<<(unsigned)cdiv(T_ + 1, 256), 256, 0, st>>>(s.states, s.lit_total, T_, ctl, comp, s.pos);
     UMCG_LAUNCHED();
-    k_rle_write_fast<T><<<(unsigned)T_, ENC_THREADS, 0, st>>>(codes, n, s.states, s.sums, s.lit_total, s.pos, ctl,
-                                                              comp, dst, off_ctl ? 1 : 0);
+#ifndef UMCG_WF_ITEMS16
+#define UMCG_WF_ITEMS16 8  // codes per thread of the u16 fast writer
+#endif
+#ifndef UMCG_WF_MINB16
+#define UMCG_WF_MINB16 UMCG_WF_MINB
+#endif
+    if (sizeof(T) == 2)
+        k_rle_write_fast<T, UMCG_WF_ITEMS16, UMCG_WF_MINB16><<<(unsigned)T_, ENC_TILE / UMCG_WF_ITEMS16, 0, st>>>(
+            codes, n, s.states, s.sums, s.lit_total, s.pos, ctl, comp, dst, off_ctl ? 1 : 0);
+    else
+        k_rle_write_fast<T, ENC_ITEMS, UMCG_WF_MINB><<<(unsigned)T_, ENC_THREADS, 0, st>>>(
+            codes, n, s.states, s.sums, s.lit_total, s.pos, ctl, comp, dst, off_ctl ? 1 : 0);
     UMCG_LAUNCHED();
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

@@ -24,7 +24,11 @@ def short(nm, rd):
     if base in ("k_rle_write_fast", "k_rle_tiles_fast"):
         return base + ("<u16> (residual)" if "short" in targs else "<u32> (grid)")
     if base == "k_dec_out":
-        return base + ("<P64> (grid)" if targs.startswith("<0") else "<RECOMPOSE> (residual)")
+        if targs.startswith("<0"):
+            return base + "<P64> (grid)"
+        if targs.startswith("<5"):
+            return base + "<Q32> (grid)"
+        return base + "<RECOMPOSE> (residual)"
     if base == "k_dec_agg":
         return base + (" (residual)" if rd > 1e8 else " (grid)")
     return base
@@ -47,7 +51,7 @@ for s, t, rd, wr, hit, iss, l1 in lines:
 open(out_md, "w").write("\n".join(md) + "\n")
 names = {"k_gather_fwd": "k_gather_fwd", "k_bucket_tma": "k_bucket", "k_resid_codes": "k_resid_codes", "k_resid_codes_sr": "k_resid_codes",
          "k_dec_agg (residual)": "k_dec_agg", "k_dec_out<RECOMPOSE> (residual)": "k_dec_out",
-         "k_dec_out<P64> (grid)": "k_dec_out_grid"}
+         "k_dec_out<P64> (grid)": "k_dec_out_grid", "k_dec_out<Q32> (grid)": "k_dec_out_grid"}
 d = {names[s]: rd + wr for s, t, rd, wr, *_ in lines if s in names}
 d["k_rle_write"] = sum(rd + wr for s, t, rd, wr, *_ in lines if s.startswith("k_rle_write_fast"))
 json.dump(d, open(out_json, "w"), indent=1)
