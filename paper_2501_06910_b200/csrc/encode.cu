@@ -723,12 +723,12 @@ static void write_impl(const T* codes, uint64_t n, const StreamEncScratch& s, De
     k_rle_pos<<<(unsigned)cdiv(T_ + 1, 256), 256, 0, st>>>(s.states, s.lit_total, T_, ctl, comp, s.pos);
     UMCG_LAUNCHED();
 #ifndef UMCG_WF_ITEMS16
-#define UMCG_WF_ITEMS16 8  // codes per thread of the u16 fast writer
+#define UMCG_WF_ITEMS16 16  // codes per thread of the u16 fast writer (A/B config 3, k_rle_write scope:
+#endif                      // 8 x 256 threads 0.278 ms; 16 x 128, 8 / 12 / 16 CTAs per SM 0.257 / 0.234 / 0.233;
+#ifndef UMCG_WF_MINB16      // 32 x 64, 16 / 24 CTAs per SM 0.228 / 0.244)
+#define UMCG_WF_MINB16 16
 #endif
-#ifndef UMCG_WF_MINB16
-#define UMCG_WF_MINB16 UMCG_WF_MINB
-#endif
-    if (sizeof(T) == 2)
+    if constexpr (sizeof(T) == 2)
         k_rle_write_fast<T, UMCG_WF_ITEMS16, UMCG_WF_MINB16><<<(unsigned)T_, ENC_TILE / UMCG_WF_ITEMS16, 0, st>>>(
             codes, n, s.states, s.sums, s.lit_total, s.pos, ctl, comp, dst, off_ctl ? 1 : 0);
     else
