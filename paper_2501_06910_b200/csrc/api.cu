@@ -163,7 +163,19 @@ uint64_t archive_bound(uint64_t n, uint64_t n1, int D, uint64_t name_len) {
     return 34 + name_len + 16 + payload_bound(n1, D) + payload_bound(n, 1) + 64;
 }
 
+__global__ void k_post_ctl(const DevCtl* d, DevCtl* h, volatile uint64_t* ticket, uint64_t seq) {
+    *h = *d;
+    mailbox_post(ticket, seq);
+}
+
 DevCtl read_ctl(umcg_plan* p, DevCtl* d, cudaStream_t st) {
+    if (Mailbox::enabled()) {
+        auto* h = reinterpret_cast<DevCtl*>(p->mail.data(sizeof(DevCtl)));
+        k_post_ctl<<<1, 1, 0, st>>>(d, h, p->mail.ticket(), p->mail.next());
+        UMCG_LAUNCHED();
+        p->mail.wait(st);
+        return *h;
+    }
     auto* h = static_cast<DevCtl*>(p->hctl.reserve(sizeof(DevCtl)));
     UMCG_CUDA(cudaMemcpyAsync(h, d, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
     UMCG_CUDA(cudaStreamSynchronize(st));
@@ -821,7 +833,8 @@ constexpr uint64_t kTailBytes = 8 + 29 + 64 + 8;   // component-2 length + heade
 // Container header + component 1 header -> out[0, kHeadShort); component 2's
 // length + header -> out[kHeadShort, +kTailBytes) with its byte count at
 // out[kHeadShort + kTailBytes] (0 when it could not be located).
-__global__ void k_gather_headers(const uint8_t* __restrict__ a, uint64_t len, uint8_t* __restrict__ out) {
+__global__ void k_gather_headers(const uint8_t* __restrict__ a, uint64_t len, uint8_t* __restrict__ out,
+                                 volatile uint64_t* ticket, uint64_t seq) {
     const uint64_t head = len < kHeadShort ? len : kHeadShort;
     for (uint64_t i = threadIdx.x; i < kHeadShort; i += blockDim.x) out[i] = i < head ? a[i] : 0;
     __shared__ uint64_t o2s;
@@ -847,6 +860,11 @@ __global__ void k_gather_headers(const uint8_t* __restrict__ a, uint64_t len, ui
             out[kHeadShort + kTailBytes + k] = (uint8_t)(tl >> (8 * k));
             out[kHeadShort + kTailBytes + 8 + k] = (uint8_t)(o2 >> (8 * k));
         }
+    if (ticket) {  // out is host memory (Mailbox): every writer fences, then one thread posts
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) mailbox_post(ticket, seq);
+    }
 }
 
 // Verdict of the speculative decompress: every check the step-by-step path
@@ -854,7 +872,8 @@ __global__ void k_gather_headers(const uint8_t* __restrict__ a, uint64_t len, ui
 // stream, no malformed varint, exact code counts, no dangling varint, no wide
 // code, lattice regimes. 0 = accept.
 __global__ void k_fast_verdict(const DevCtl* c, DecSrc s1, DecSrc s2, uint64_t n1, uint64_t n2, double lim1,
-                               double lim2, unsigned long long* verdict) {
+                               double lim2, unsigned long long* verdict, volatile uint64_t* ticket,
+                               uint64_t seq) {
     if (threadIdx.x | blockIdx.x) return;
     unsigned long long v = 0;
     const DecSrc s[2] = {s1, s2};
@@ -874,6 +893,7 @@ __global__ void k_fast_verdict(const DevCtl* c, DecSrc s1, DecSrc s2, uint64_t n
     if (!((double)c[1].max_abs_k[0] < lim1)) v |= 1ull << 16;
     if (!((double)c[3].max_abs_k[1] < lim2)) v |= 1ull << 17;
     *verdict = v;
+    if (ticket) mailbox_post(ticket, seq);  // verdict is host memory (Mailbox)
 }
 
 // Speculative nearest-g decompress (the common case): both token probes, the
@@ -970,13 +990,22 @@ static bool fast_decompress(umcg_plan* p, const uint8_t* d_ar, uint64_t p1, cons
     dec_fused(DEC_RECOMPOSE, src2, dec_tiles(h2.stream_len), n, st2, &c[3], p->d_node.as<uint32_t>(1), K1, bin1,
               bin2, d_out, nullptr, st, &c[1], K16, true);
     if (g_dec_trace) { g_dec_trace->dev("dec_out", st); g_dec_trace->host("queued"); }
-    auto* verdict = reinterpret_cast<unsigned long long*>(&c[4].aux[0]);
-    k_fast_verdict<<<1, 1, 0, st>>>(c, src1, src2, n1, n, k_lim(pred1, pred1 == 2 ? h1.D : 1), k_lim(1, 1),
-                                    verdict);
-    UMCG_LAUNCHED();
-    auto* hv = static_cast<unsigned long long*>(p->hctl.reserve(sizeof(DevCtl)));
-    UMCG_CUDA(cudaMemcpyAsync(hv, verdict, 8, cudaMemcpyDeviceToHost, st));
-    UMCG_CUDA(cudaStreamSynchronize(st));
+    unsigned long long* hv;
+    if (Mailbox::enabled()) {
+        hv = reinterpret_cast<unsigned long long*>(p->mail.data(8));
+        k_fast_verdict<<<1, 1, 0, st>>>(c, src1, src2, n1, n, k_lim(pred1, pred1 == 2 ? h1.D : 1), k_lim(1, 1), hv,
+                                        p->mail.ticket(), p->mail.next());
+        UMCG_LAUNCHED();
+        p->mail.wait(st);
+    } else {
+        auto* verdict = reinterpret_cast<unsigned long long*>(&c[4].aux[0]);
+        k_fast_verdict<<<1, 1, 0, st>>>(c, src1, src2, n1, n, k_lim(pred1, pred1 == 2 ? h1.D : 1), k_lim(1, 1),
+                                        verdict, nullptr, 0);
+        UMCG_LAUNCHED();
+        hv = static_cast<unsigned long long*>(p->hctl.reserve(sizeof(DevCtl)));
+        UMCG_CUDA(cudaMemcpyAsync(hv, verdict, 8, cudaMemcpyDeviceToHost, st));
+        UMCG_CUDA(cudaStreamSynchronize(st));
+    }
     if (g_dec_trace) { g_dec_trace->host("verdict"); g_dec_trace->dev("verdict", st); }
     return *hv == 0;
 }
@@ -999,12 +1028,22 @@ void decompress_impl(umcg_plan* p, const uint8_t* d_ar, uint64_t len, double* d_
     uint8_t tail[kTailBytes];
     uint64_t tl_gathered = 0, o2_gathered = 0;
     {
-        auto* dbuf = p->hdr.as<uint8_t>(kHeadShort + kTailBytes + 16);
-        k_gather_headers<<<1, 128, 0, st>>>(d_ar, len, dbuf);
-        UMCG_LAUNCHED();
-        UMCG_CUDA(cudaMemcpyAsync(hb, dbuf, kHeadShort + kTailBytes + 16, cudaMemcpyDeviceToHost, st));
-        trace.dev("headers", st);
-        UMCG_CUDA(cudaStreamSynchronize(st));
+        if (Mailbox::enabled()) {
+            // the gather writes straight into pinned host memory and posts a ticket
+            uint8_t* mb = p->mail.data(kHeadShort + kTailBytes + 16);
+            k_gather_headers<<<1, 128, 0, st>>>(d_ar, len, mb, p->mail.ticket(), p->mail.next());
+            UMCG_LAUNCHED();
+            trace.dev("headers", st);
+            p->mail.wait(st);
+            std::memcpy(hb, mb, kHeadShort + kTailBytes + 16);
+        } else {
+            auto* dbuf = p->hdr.as<uint8_t>(kHeadShort + kTailBytes + 16);
+            k_gather_headers<<<1, 128, 0, st>>>(d_ar, len, dbuf, nullptr, 0);
+            UMCG_LAUNCHED();
+            UMCG_CUDA(cudaMemcpyAsync(hb, dbuf, kHeadShort + kTailBytes + 16, cudaMemcpyDeviceToHost, st));
+            trace.dev("headers", st);
+            UMCG_CUDA(cudaStreamSynchronize(st));
+        }
         trace.host("headers");
         uint64_t tlen = 0;
         std::memcpy(&tlen, hb + kHeadShort + kTailBytes, 8);

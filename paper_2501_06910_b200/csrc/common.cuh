@@ -7,6 +7,7 @@
 #include <atomic>
 #include <mutex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -524,5 +525,61 @@ struct PinnedBuf {
         return p;
     }
 };
+
+// Device -> host hand-off without a copy operation or a stream
+// synchronization: the last kernel of a phase writes its small result into
+// pinned host memory (unified addressing: the same pointer on the device),
+// then a ticket; the host polls the ticket. A posted PCIe write reaches the
+// host in ~1-2 us, against ~10 us for cudaMemcpyAsync + cudaStreamSynchronize
+// (UMCG_DEC_TRACE: headers on the device at +13 us, on the host at +24 us).
+// UMCG_NO_MAILBOX=1 keeps the copy + synchronize hand-off (A/B knob).
+struct Mailbox {
+    static constexpr size_t kData = 64;  // payload offset: the ticket has its own cache line
+    PinnedBuf buf;
+    uint64_t seq = 0;
+    uint8_t* base = nullptr;
+    // payload of >= bytes; call before every use (the buffer only grows)
+    uint8_t* data(size_t bytes) {
+        if (!base || bytes + kData > buf.cap) {
+            base = static_cast<uint8_t*>(buf.reserve(bytes + kData < 4096 ? 4096 : bytes + kData));
+            *reinterpret_cast<volatile uint64_t*>(base) = 0;
+            seq = 0;
+        }
+        return base + kData;
+    }
+    volatile uint64_t* ticket() { return reinterpret_cast<volatile uint64_t*>(base); }
+    uint64_t next() { return ++seq; }
+    static bool enabled() {
+        static const bool on = std::getenv("UMCG_NO_MAILBOX") == nullptr;
+        return on;
+    }
+    // Poll until the ticket shows seq. Every ~1k polls the stream is queried,
+    // so a failed launch or a faulted kernel surfaces as its CUDA error
+    // instead of an endless wait.
+    void wait(cudaStream_t st) {
+        const volatile uint64_t* t = ticket();
+        for (uint32_t spins = 1;; ++spins) {
+            if (*t == seq) break;
+            if ((spins & 0x3ffu) == 0) {
+                const cudaError_t q = cudaStreamQuery(st);
+                if (q == cudaSuccess) {
+                    if (*t == seq) break;
+                    throw umcg::Error(UMCG_INTERNAL_INCONSISTENCY, "mailbox ticket missing after the stream finished");
+                }
+                if (q != cudaErrorNotReady) UMCG_CUDA(q);
+            }
+        }
+        std::atomic_thread_fence(std::memory_order_acquire);
+    }
+};
+
+#ifdef __CUDACC__
+// Post a ticket after the payload stores of this thread (and, after a
+// __syncthreads(), of its CTA: each writer fences first).
+__device__ __forceinline__ void mailbox_post(volatile uint64_t* ticket, uint64_t seq) {
+    __threadfence_system();
+    *ticket = seq;
+}
+#endif
 
 }  // namespace umcg

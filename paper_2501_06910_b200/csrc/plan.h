@@ -73,6 +73,7 @@ struct umcg_plan {
     umcg::StreamDecScratch dec, dec2;
     umcg::SideStream side;  // grid component's chain runs beside the residual's
     umcg::PinnedBuf hctl, hstage;
+    umcg::Mailbox mail;  // small device -> host results (control block, headers, verdict)
 };
 
 namespace umcg {
