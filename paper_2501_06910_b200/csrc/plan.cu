@@ -478,7 +478,17 @@ umcg_plan* plan_create_host(const umcg_grid_desc* g, const umcg_mapping_desc* m,
             p->has_coords = true;
         }
         plan_build_segments(p, 0);
-        p->digest = mapping_digest_host(p->mode, p->n, m->assignments, m->n_visited, m->visited_nodes);
+        static const bool dig_host = std::getenv("UMCG_DIGEST_HOST") != nullptr;
+        static const bool dig_check = std::getenv("UMCG_DIGEST_CHECK") != nullptr;
+        if (dig_host) {
+            p->digest = mapping_digest_host(p->mode, p->n, m->assignments, m->n_visited, m->visited_nodes);
+        } else {
+            p->digest = mapping_digest_device(p->mode, p->n, dn, m->n_visited,
+                                              p->mode == 1 ? p->d_visited.as<uint64_t>(1) : nullptr, p->scratch_a, 0);
+            if (dig_check &&
+                p->digest != mapping_digest_host(p->mode, p->n, m->assignments, m->n_visited, m->visited_nodes))
+                fail(UMCG_INTERNAL_INCONSISTENCY, "device mapping digest differs from the host digest");
+        }
     } catch (...) {
         delete p;
         throw;
@@ -598,9 +608,19 @@ umcg_plan* plan_build_gpu(const umcg_grid_desc* g0, uint64_t n, const double* d_
             p->has_coords = true;
         }
         plan_build_segments(p, st);
-        std::vector<uint32_t> h32(n);
-        if (n) UMCG_CUDA(cudaMemcpy(h32.data(), dn, n * 4, cudaMemcpyDeviceToHost));
-        p->digest = mapping_digest_host32(p->mode, n, h32.data(), nv, hvis.data());
+        static const bool dig_host = std::getenv("UMCG_DIGEST_HOST") != nullptr;
+        static const bool dig_check = std::getenv("UMCG_DIGEST_CHECK") != nullptr;
+        if (!dig_host)
+            p->digest = mapping_digest_device(p->mode, n, dn, nv, p->mode == 1 ? p->d_visited.as<uint64_t>(1) : nullptr,
+                                              p->scratch_a, st);
+        if (dig_host || dig_check) {
+            std::vector<uint32_t> h32(n);
+            if (n) UMCG_CUDA(cudaMemcpy(h32.data(), dn, n * 4, cudaMemcpyDeviceToHost));
+            const uint64_t hd = mapping_digest_host32(p->mode, n, h32.data(), nv, hvis.data());
+            if (dig_check && !dig_host && hd != p->digest)
+                fail(UMCG_INTERNAL_INCONSISTENCY, "device mapping digest differs from the host digest");
+            p->digest = hd;
+        }
         if (p->mode == 0) {
             p->n_visited = nv;
             p->visited_fraction = frac;

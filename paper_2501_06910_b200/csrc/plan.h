@@ -81,6 +81,12 @@ namespace umcg {
 // Host-side FNV-1a-64 of serialize_mapping bytes (serialize.hpp:255-267, 300-303).
 uint64_t mapping_digest_host(int mode, uint64_t n, const uint64_t* assign, uint64_t n_visited,
                              const uint64_t* visited);
+// The same digest from the device-resident mapping (digest.cu: FNV-1a chained
+// in parallel through per-chunk affine maps keyed by the hash's low byte).
+// UMCG_DIGEST_HOST=1 keeps the byte-serial host loop; UMCG_DIGEST_CHECK=1
+// computes both and fails on a difference.
+uint64_t mapping_digest_device(int mode, uint64_t n, const uint32_t* d_assign, uint64_t n_visited,
+                               const uint64_t* d_visited, umcg::DevBuf& scratch, cudaStream_t st);
 // Same digest with u32 assignments (widened to u64 LE bytes as the reference writes them).
 uint64_t mapping_digest_host32(int mode, uint64_t n, const uint32_t* assign, uint64_t n_visited,
                                const uint64_t* visited);

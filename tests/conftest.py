@@ -3,6 +3,10 @@ import sys
 
 import pytest
 
+# every plan built by the GPU tests cross-checks the parallel device digest
+# (csrc/digest.cu) against the byte-serial host loop
+os.environ.setdefault("UMCG_DIGEST_CHECK", "1")
+
 ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -53,6 +53,30 @@ def test_plan_digest_matches_reference(cuda, ref):
     assert plan_for(s).digest == ref.mapping_digest(s) == parse_archive(ar)["digest"]
 
 
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("n", [1, 255, 16383, 16384, 16385, 50001])
+def test_parallel_digest_matches_reference(cuda, ref, mode, n):
+    """mapping_digest (serialize.hpp:255-267, 300-303): the device FNV-1a (chunk
+    maps keyed by the low byte, digest.cu) on chunk-boundary sizes, ids with
+    1-3 significant bytes and zero ids, and a seed-mode mapping (assignments
+    into a visited list, the list hashed after them)."""
+    rng = np.random.default_rng(1000 * mode + n)
+    g = 300  # 90000 nodes: ids up to 3 bytes
+    axes = [np.linspace(0.0, 1.0, g), np.linspace(0.0, 1.0, g)]
+    if mode == 0:
+        a = rng.integers(0, g * g, n).astype(np.uint64)
+        a[rng.random(n) < 0.2] = 0
+        small = rng.random(n) < 0.2
+        a[small] = rng.integers(0, 256, int(small.sum())).astype(np.uint64)
+        s = Setup(2, axes, 0, a)
+    else:
+        nv = min(n, 977)
+        vis = np.sort(rng.choice(g * g, nv, replace=False)).astype(np.uint64)
+        a = rng.integers(0, nv, n).astype(np.uint64)
+        s = Setup(2, axes, 1, a, vis)
+    assert plan_for(s, coords=False).digest == ref.mapping_digest(s)
+
+
 @pytest.mark.parametrize("case_idx", range(7))
 def test_fixture_cases(cuda, case_idx, ref, oracle):
     params, cases = load_cases()
