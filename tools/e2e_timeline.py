@@ -43,7 +43,14 @@ for _ in range(2):
     s1 = time.perf_counter()
     print(f"concurrent: total {1e3*(s1-s0):.1f} ms; compress [{1e3*(T['c'][0]-s0):.1f}, {1e3*(T['c'][1]-s0):.1f}] "
           f"decompress [{1e3*(T['d'][0]-s0):.1f}, {1e3*(T['d'][1]-s0):.1f}]")
-for plans, pds in (([pc], [pd]), ([pc, pc2], [pd]), ([pc, pc2], [pd, pd2])):
+more = int(os.environ.get("E2E_MORE", "0"))  # extra workers per direction (E2E_MORE=1: 3c/3d, 2: 4c/4d)
+extra_c = [pc.clone() for _ in range(more)]
+extra_d = [pc.clone() for _ in range(more)]
+slots += [torch.empty(cap, dtype=torch.uint8, pin_memory=True).numpy() for _ in range(2 * more)]
+combos = [([pc], [pd]), ([pc, pc2], [pd]), ([pc, pc2], [pd, pd2])]
+if more:
+    combos = [([pc, pc2] + extra_c, [pd, pd2] + extra_d)]
+for plans, pds in combos:
     pipe = umcg.HostPipeline(plans, pds, slots)
     pipe.run([xa] * 2, b, [ya] * 2, "f")
     for kp in (4, 8, 16):
