@@ -22,7 +22,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
                 "-Xcompiler", "-O3", "-Xcompiler", "-fopenmp", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
-SOURCES = ["encode.cu", "partition.cu", "stream.cu", "codes.cu", "decode.cu", "interp.cu", "plan.cu", "api.cu", "datagen.cu", "gridinit.cu", "escape.cu", "digest.cu"]
+SOURCES = ["encode.cu", "partition.cu", "stream.cu", "codes.cu", "decode.cu", "interp.cu", "plan.cu", "api.cu", "datagen.cu", "gridinit.cu", "escape.cu", "digest.cu", "radix.cu"]
 
 
 def _needs(src: str, obj: str) -> bool:

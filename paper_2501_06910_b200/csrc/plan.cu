@@ -238,7 +238,7 @@ void plan_build_segments(umcg_plan* p, cudaStream_t st) {
     uint32_t* node = p->d_node.as<uint32_t>(n ? n : 1);
     uint32_t* perm = p->d_perm.as<uint32_t>(n ? n : 1);
     uint32_t* seg = p->d_seg.as<uint32_t>(ns + 8);  // + padding for 16-byte bulk copies
-    DevBuf tmp_keys, tmp_vals, cnt, scratch;
+    DevBuf tmp_keys, tmp_vals, cnt, scratch, rs_hist, rs_scan;
     uint32_t* keys_out = tmp_keys.as<uint32_t>(n ? n : 1);
     uint32_t* iota = tmp_vals.as<uint32_t>(n ? n : 1);
     uint32_t* c = cnt.as<uint32_t>(ns + 1);
@@ -250,15 +250,12 @@ void plan_build_segments(umcg_plan* p, cudaStream_t st) {
         UMCG_LAUNCHED();
         int end_bit = 1;
         while (end_bit < 32 && (1ull << end_bit) < ns) ++end_bit;
-        size_t tb = 0;
-        UMCG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, node, keys_out, iota, perm, (int)n, 0, end_bit, st));
-        void* t = scratch.reserve(tb);
-        UMCG_CUDA(cub::DeviceRadixSort::SortPairs(t, tb, node, keys_out, iota, perm, (int)n, 0, end_bit, st));
+        // K0: vertices stably sorted by slot (radix.cu)
+        radix_sort_pairs_u32(node, keys_out, iota, perm, n, 0, end_bit, scratch, rs_hist, rs_scan, st);
     }
-    size_t tb = 0;
-    UMCG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, c, seg, (int)(ns + 1), st));
-    void* t = scratch.reserve(std::max<size_t>(tb, scratch.capacity()));
-    UMCG_CUDA(cub::DeviceScan::ExclusiveSum(t, tb, c, seg, (int)(ns + 1), st));
+    // seg = exclusive scan of the slot counts
+    UMCG_CUDA(cudaMemcpyAsync(seg, c, (ns + 1) * 4, cudaMemcpyDeviceToDevice, st));
+    exclusive_scan_u32(seg, ns + 1, rs_scan, st);
     // visited count (dense info)
     DevBuf vc;
     auto* v = vc.as<unsigned long long>(1);
@@ -341,10 +338,8 @@ void plan_build_buckets(umcg_plan* p, cudaStream_t st) {
     UMCG_LAUNCHED();
     int end_bit = 1;
     while (end_bit < 32 && (1ull << end_bit) < B) ++end_bit;
-    size_t tb = 0;
-    UMCG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kk, ks, io, Lv, (int)n, 0, end_bit, st));
-    void* t = scratch.reserve(tb);
-    UMCG_CUDA(cub::DeviceRadixSort::SortPairs(t, tb, kk, ks, io, Lv, (int)n, 0, end_bit, st));
+    DevBuf rs_hist, rs_scan;
+    radix_sort_pairs_u32(kk, ks, io, Lv, n, 0, end_bit, scratch, rs_hist, rs_scan, st);
     k_dst_lnode<<<blocks(n), THREADS, 0, st>>>(Lv, ks, n, p->d_node.as<uint32_t>(1), dbn, dst, lnode);
     UMCG_LAUNCHED();
     k_lperm<<<blocks(n), THREADS, 0, st>>>(p->d_perm.as<uint32_t>(1), n, dst, p->d_node.as<uint32_t>(1), sb,
@@ -364,10 +359,7 @@ void plan_build_buckets(umcg_plan* p, cudaStream_t st) {
     uint32_t* srcE = p->d_srcE.as<uint32_t>(n);
     end_bit = 1;
     while (end_bit < 32 && (1ull << end_bit) < E * B) ++end_bit;
-    tb = 0;
-    UMCG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kk, ks, io, srcE, (int)n, 0, end_bit, st));
-    t = scratch.reserve(std::max(tb, scratch.capacity()));
-    UMCG_CUDA(cub::DeviceRadixSort::SortPairs(t, tb, kk, ks, io, srcE, (int)n, 0, end_bit, st));
+    radix_sort_pairs_u32(kk, ks, io, srcE, n, 0, end_bit, scratch, rs_hist, rs_scan, st);
     k_dstE<<<blocks(n), THREADS, 0, st>>>(srcE, n, p->d_dstE.as<uint32_t>(n));
     UMCG_LAUNCHED();
     // vertex tiles: stable sort of the layout-E positions by the tile of their
@@ -378,10 +370,7 @@ void plan_build_buckets(umcg_plan* p, cudaStream_t st) {
         int hi = kRTileBits + 1;
         while (hi < 32 && (1ull << hi) < n) ++hi;
         uint32_t* rPt = p->d_rPt.as<uint32_t>(n);
-        tb = 0;
-        UMCG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, srcE, ks, io, rPt, (int)n, (int)kRTileBits, hi, st));
-        t = scratch.reserve(std::max(tb, scratch.capacity()));
-        UMCG_CUDA(cub::DeviceRadixSort::SortPairs(t, tb, srcE, ks, io, rPt, (int)n, (int)kRTileBits, hi, st));
+        radix_sort_pairs_u32(srcE, ks, io, rPt, n, (int)kRTileBits, hi, scratch, rs_hist, rs_scan, st);
         k_rlt<<<blocks(n), THREADS, 0, st>>>(ks, n, p->d_rLt.as<uint16_t>(n));
         UMCG_LAUNCHED();
     }

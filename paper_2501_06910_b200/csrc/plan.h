@@ -91,6 +91,15 @@ uint64_t mapping_digest_device(int mode, uint64_t n, const uint32_t* d_assign, u
 uint64_t mapping_digest_host32(int mode, uint64_t n, const uint32_t* assign, uint64_t n_visited,
                                const uint64_t* visited);
 
+// Stable LSD radix sort of (u32 key, u32 value) pairs on key bits
+// [begin_bit, end_bit) and an in-place exclusive u32 scan (radix.cu; plan-time).
+// vals_in == nullptr sorts the indices 0..n-1. keys_in / vals_in are not
+// modified and must not alias the outputs.
+void radix_sort_pairs_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
+                          uint64_t n, int begin_bit, int end_bit, umcg::DevBuf& tmp_pairs, umcg::DevBuf& tmp_hist,
+                          umcg::DevBuf& tmp_scan, cudaStream_t st);
+void exclusive_scan_u32(uint32_t* d_a, uint64_t n, umcg::DevBuf& scratch, cudaStream_t st);
+
 // Build perm / seg_off from d_node on the plan (stable radix sort by slot),
 // then the bucketed layout (plan_build_buckets).
 void plan_build_segments(umcg_plan* p, cudaStream_t st);
