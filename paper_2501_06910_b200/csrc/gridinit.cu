@@ -14,11 +14,9 @@
 #include <limits>
 #include <vector>
 
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_reduce.cuh>
-#include <cub/device/device_scan.cuh>
 
 #include "kernels.h"
+#include "plan.h"
 
 namespace umcg {
 
@@ -139,6 +137,21 @@ __global__ void k_knn(const double* __restrict__ xyz, uint64_t n_v, KnnGrid g, c
         deltas[d * n_v + v] = best_idx < n_v ? fabs(__dsub_rn(xyz[best_idx * D + d], pv[d])) : 0.0;
 }
 
+// IEEE doubles as u64 keys of the same order (sign bit flipped for positive
+// values, all bits for negative ones), and back in place.
+__global__ void k_double_keys(const double* __restrict__ v, uint64_t n, uint64_t* __restrict__ k) {
+    const uint64_t i = blockIdx.x * (uint64_t)GT + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t u = (uint64_t)__double_as_longlong(v[i]);
+    k[i] = (u >> 63) ? ~u : u | 0x8000000000000000ull;
+}
+__global__ void k_keys_double(uint64_t* __restrict__ k, uint64_t n) {
+    const uint64_t i = blockIdx.x * (uint64_t)GT + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t u = k[i];
+    k[i] = (u >> 63) ? u & 0x7fffffffffffffffull : ~u;
+}
+
 __global__ void k_count_zero(const double* __restrict__ s, uint64_t n, unsigned long long* z) {
     const uint64_t i = blockIdx.x * (uint64_t)GT + threadIdx.x;
     if (i < n && s[i] == 0.0) atomicAdd(z, 1ull);
@@ -162,10 +175,14 @@ void sort_axis(double* in, uint64_t n, SortedAxis& out, cudaStream_t st) {
     out.total = n;
     double* o = out.keys.as<double>(n ? n : 1);
     if (n) {
-        DevBuf tmp;
-        size_t tb = 0;
-        UMCG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, in, o, (int)n, 0, 64, st));
-        UMCG_CUDA(cub::DeviceRadixSort::SortKeys(tmp.reserve(tb), tb, in, o, (int)n, 0, 64, st));
+        // ascending doubles = ascending order-preserving u64 keys (radix.cu)
+        DevBuf kb, tmp, rs_hist, rs_scan;
+        uint64_t* k = kb.as<uint64_t>(n);
+        k_double_keys<<<gblocks(n), GT, 0, st>>>(in, n, k);
+        UMCG_LAUNCHED();
+        radix_sort_u64(k, reinterpret_cast<uint64_t*>(o), nullptr, nullptr, n, 0, 64, tmp, rs_hist, rs_scan, st);
+        k_keys_double<<<gblocks(n), GT, 0, st>>>(reinterpret_cast<uint64_t*>(o), n);
+        UMCG_LAUNCHED();
     }
     DevBuf zb;
     auto* z = zb.as<unsigned long long>(1);
@@ -260,17 +277,14 @@ void grid_init_gpu(int D, uint64_t n_v, const double* xyz, int arity, uint64_t n
         UMCG_CUDA(cudaMemsetAsync(cnt, 0, (nb + 1) * 4, st));
         k_knn_keys<<<gblocks(n_v), GT, 0, st>>>(xyz, n_v, g, key, idx, cnt);
         UMCG_LAUNCHED();
-        size_t tb = 0;
-        UMCG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, start, (int)(nb + 1), st));
-        UMCG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.reserve(tb), tb, cnt, start, (int)(nb + 1), st));
+        DevBuf rs_hist, rs_scan;
+        UMCG_CUDA(cudaMemcpyAsync(start, cnt, (nb + 1) * 4, cudaMemcpyDeviceToDevice, st));
+        exclusive_scan_u32(start, nb + 1, rs_scan, st);
         auto* ks = sk.as<uint64_t>(n_v);
         auto* is = si.as<uint32_t>(n_v);
         int end_bit = 1;
         while (end_bit < 64 && (1ull << end_bit) < nb) ++end_bit;
-        size_t tb2 = 0;
-        UMCG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, key, ks, idx, is, (int)n_v, 0, end_bit, st));
-        DevBuf tmp2;
-        UMCG_CUDA(cub::DeviceRadixSort::SortPairs(tmp2.reserve(tb2), tb2, key, ks, idx, is, (int)n_v, 0, end_bit, st));
+        radix_sort_u64(key, ks, idx, is, n_v, 0, end_bit, tmp, rs_hist, rs_scan, st);
         double* buf = dl.as<double>(n_v * D);
         k_knn<<<gblocks(n_v), GT, 0, st>>>(xyz, n_v, g, start, is, buf);
         UMCG_LAUNCHED();

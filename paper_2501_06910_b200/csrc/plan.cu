@@ -1,8 +1,5 @@
 // Plan construction: device-resident mapping, stable slot sort, digest, and
 // the GPU grid_coarsen (grid_builder.hpp:286-421).
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
-#include <cub/device/device_select.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -201,6 +198,21 @@ __global__ void k_lslot(const uint32_t* __restrict__ perm, uint64_t n, const uin
     lslot[q] = (uint16_t)(l + 2 * e + phase);
 }
 
+// Run heads of a sorted key array (1 where a new key starts), and the
+// compaction of the heads through the exclusive scan of those flags.
+__global__ void k_run_heads(const uint64_t* __restrict__ s, uint64_t n, uint32_t* __restrict__ f) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i < n) f[i] = (i == 0 || s[i] != s[i - 1]) ? 1u : 0u;
+}
+__global__ void k_unique_out(const uint64_t* __restrict__ s, uint64_t n, const uint32_t* __restrict__ pos,
+                             uint64_t* __restrict__ out, unsigned long long* __restrict__ count) {
+    const uint64_t i = blockIdx.x * (uint64_t)THREADS + threadIdx.x;
+    if (i >= n) return;
+    const bool head = i == 0 || s[i] != s[i - 1];
+    if (head) out[pos[i]] = s[i];
+    if (i == n - 1) *count = (unsigned long long)pos[i] + (head ? 1u : 0u);
+}
+
 }  // namespace
 
 uint64_t mapping_digest_host(int mode, uint64_t n, const uint64_t* assign, uint64_t nv, const uint64_t* vis) {
@@ -232,7 +244,7 @@ uint64_t mapping_digest_host32(int mode, uint64_t n, const uint32_t* assign, uin
 }
 
 void plan_build_segments(umcg_plan* p, cudaStream_t st) {
-    // the device sorts (cub, int item counts) and u32 layout positions bound a plan's size
+    // u32 layout positions (and the sorts' u32 ranks) bound a plan's size
     if (p->n > (uint64_t)INT32_MAX) fail(UMCG_INVALID_ARGUMENT, "more than 2^31-1 vertices per plan");
     const uint64_t n = p->n, ns = p->n_slots;
     uint32_t* node = p->d_node.as<uint32_t>(n ? n : 1);
@@ -545,14 +557,20 @@ umcg_plan* plan_build_gpu(const umcg_grid_desc* g0, uint64_t n, const double* d_
     auto* dnu = nuniq.as<unsigned long long>(1);
     uint64_t nv = 0;
     if (n) {
-        size_t tb = 0;
-        UMCG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, dlin, dsorted, (int)n, 0, 64, st));
-        void* t = scratch.reserve(tb);
-        UMCG_CUDA(cub::DeviceRadixSort::SortKeys(t, tb, dlin, dsorted, (int)n, 0, 64, st));
-        size_t tb2 = 0;
-        UMCG_CUDA(cub::DeviceSelect::Unique(nullptr, tb2, dsorted, duniq, dnu, (int)n, st));
-        t = scratch.reserve(std::max(tb, tb2));
-        UMCG_CUDA(cub::DeviceSelect::Unique(t, tb2, dsorted, duniq, dnu, (int)n, st));
+        // (radix.cu) keys below the coarse grid's node count; then the heads
+        // of the runs of equal keys, compacted through a scan of their flags
+        uint64_t nodes = 1;
+        for (int d = 0; d < D; ++d) nodes *= std::max<uint64_t>(csizes[d], 1);
+        int end_bit = 1;
+        while (end_bit < 64 && (1ull << end_bit) < nodes) ++end_bit;
+        DevBuf rs_hist, rs_scan, heads;
+        radix_sort_u64(dlin, dsorted, nullptr, nullptr, n, 0, end_bit, scratch, rs_hist, rs_scan, st);
+        uint32_t* hp = heads.as<uint32_t>(n);
+        k_run_heads<<<blocks(n), THREADS, 0, st>>>(dsorted, n, hp);
+        UMCG_LAUNCHED();
+        exclusive_scan_u32(hp, n, rs_scan, st);
+        k_unique_out<<<blocks(n), THREADS, 0, st>>>(dsorted, n, hp, duniq, dnu);
+        UMCG_LAUNCHED();
         unsigned long long h = 0;
         UMCG_CUDA(cudaMemcpy(&h, dnu, 8, cudaMemcpyDeviceToHost));
         nv = h;

@@ -98,6 +98,10 @@ uint64_t mapping_digest_host32(int mode, uint64_t n, const uint32_t* assign, uin
 void radix_sort_pairs_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
                           uint64_t n, int begin_bit, int end_bit, umcg::DevBuf& tmp_pairs, umcg::DevBuf& tmp_hist,
                           umcg::DevBuf& tmp_scan, cudaStream_t st);
+// u64 keys; vals_out == nullptr sorts the keys alone.
+void radix_sort_u64(const uint64_t* keys_in, uint64_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
+                    uint64_t n, int begin_bit, int end_bit, umcg::DevBuf& tmp_pairs, umcg::DevBuf& tmp_hist,
+                    umcg::DevBuf& tmp_scan, cudaStream_t st);
 void exclusive_scan_u32(uint32_t* d_a, uint64_t n, umcg::DevBuf& scratch, cudaStream_t st);
 
 // Build perm / seg_off from d_node on the plan (stable radix sort by slot),

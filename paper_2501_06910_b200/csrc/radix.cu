@@ -27,7 +27,8 @@ constexpr int RS_TILE = RS_T * RS_ITEMS;   // 4096 pairs per tile
 constexpr int RS_W = RS_T / 32;            // warps
 constexpr int RS_RUN = RS_TILE / RS_W;     // 512 consecutive pairs per warp
 
-__global__ void __launch_bounds__(RS_T) k_rs_hist(const uint32_t* __restrict__ keys, uint64_t n, int shift,
+template <class K>
+__global__ void __launch_bounds__(RS_T) k_rs_hist(const K* __restrict__ keys, uint64_t n, int shift,
                                                   uint32_t mask, uint64_t T, uint32_t* __restrict__ hist) {
     __shared__ uint32_t h[256];
     h[threadIdx.x] = 0;
@@ -39,7 +40,7 @@ __global__ void __launch_bounds__(RS_T) k_rs_hist(const uint32_t* __restrict__ k
         const uint64_t i = base + (uint64_t)j * RS_T + threadIdx.x;
         // one atomic per group of equal digits in the warp (clustered keys
         // would otherwise serialize on one counter)
-        const uint32_t d = i < n ? (keys[i] >> shift) & mask : 0x100u + (threadIdx.x & 31);
+        const uint32_t d = i < n ? (uint32_t)(keys[i] >> shift) & mask : 0x100u + (threadIdx.x & 31);
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
         if (i < n && (peers & lt) == 0) atomicAdd(&h[d], (uint32_t)__popc(peers));
     }
@@ -47,10 +48,12 @@ __global__ void __launch_bounds__(RS_T) k_rs_hist(const uint32_t* __restrict__ k
     hist[(uint64_t)threadIdx.x * T + blockIdx.x] = h[threadIdx.x];
 }
 
-__global__ void __launch_bounds__(RS_T) k_rs_scatter(const uint32_t* __restrict__ keys,
+// vals_out == nullptr: keys only; vals == nullptr: the values are the indices
+template <class K>
+__global__ void __launch_bounds__(RS_T) k_rs_scatter(const K* __restrict__ keys,
                                                      const uint32_t* __restrict__ vals, uint64_t n, int shift,
                                                      uint32_t mask, uint64_t T, const uint32_t* __restrict__ offs,
-                                                     uint32_t* __restrict__ keys_out,
+                                                     K* __restrict__ keys_out,
                                                      uint32_t* __restrict__ vals_out) {
     __shared__ uint32_t wc[RS_W][256];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -58,20 +61,21 @@ __global__ void __launch_bounds__(RS_T) k_rs_scatter(const uint32_t* __restrict_
     for (int k = 0; k < RS_W; ++k) wc[k][threadIdx.x] = 0;
     __syncthreads();
     const uint64_t first = (uint64_t)blockIdx.x * RS_TILE + (uint64_t)w * RS_RUN;
-    uint32_t key[RS_ITEMS], val[RS_ITEMS], rank[RS_ITEMS];
+    K key[RS_ITEMS];
+    uint32_t val[RS_ITEMS], rank[RS_ITEMS];
 #pragma unroll
     for (int j = 0; j < RS_ITEMS; ++j) {
         const uint64_t i = first + (uint64_t)j * 32 + lane;
         const bool ok = i < n;
-        key[j] = ok ? keys[i] : 0u;
-        val[j] = ok ? (vals ? vals[i] : (uint32_t)i) : 0u;
+        key[j] = ok ? keys[i] : (K)0;
+        val[j] = ok && vals_out ? (vals ? vals[i] : (uint32_t)i) : 0u;
     }
     const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
     for (int j = 0; j < RS_ITEMS; ++j) {
         const bool ok = first + (uint64_t)j * 32 + lane < n;
         // lanes past the end form groups of their own and count nothing
-        const uint32_t d = ok ? (key[j] >> shift) & mask : 0x100u + (uint32_t)lane;
+        const uint32_t d = ok ? (uint32_t)(key[j] >> shift) & mask : 0x100u + (uint32_t)lane;
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
         const uint32_t before = ok ? wc[w][d] : 0u;
         rank[j] = before + __popc(peers & lt);
@@ -93,9 +97,9 @@ __global__ void __launch_bounds__(RS_T) k_rs_scatter(const uint32_t* __restrict_
 #pragma unroll
     for (int j = 0; j < RS_ITEMS; ++j) {
         if (first + (uint64_t)j * 32 + lane >= n) continue;
-        const uint32_t o = wc[w][(key[j] >> shift) & mask] + rank[j];
+        const uint32_t o = wc[w][(uint32_t)(key[j] >> shift) & mask] + rank[j];
         keys_out[o] = key[j];
-        vals_out[o] = val[j];
+        if (vals_out) vals_out[o] = val[j];
     }
 }
 
@@ -187,35 +191,55 @@ void exclusive_scan_u32(uint32_t* d_a, uint64_t n, DevBuf& scratch, cudaStream_t
     UMCG_LAUNCHED();
 }
 
-void radix_sort_pairs_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
-                          uint64_t n, int begin_bit, int end_bit, DevBuf& tmp_pairs, DevBuf& tmp_hist,
-                          DevBuf& tmp_scan, cudaStream_t st) {
+namespace {
+template <class K>
+void radix_sort_impl(const K* keys_in, K* keys_out, const uint32_t* vals_in, uint32_t* vals_out, uint64_t n,
+                     int begin_bit, int end_bit, DevBuf& tmp_pairs, DevBuf& tmp_hist, DevBuf& tmp_scan,
+                     cudaStream_t st) {
     if (!n) return;
-    if (n >= (1ull << 32)) fail(UMCG_INVALID_ARGUMENT, "radix sort: more than 2^32-1 pairs");
+    if (n >= (1ull << 32)) fail(UMCG_INVALID_ARGUMENT, "radix sort: more than 2^32-1 items");
     const int bits = end_bit - begin_bit;
     const int passes = bits <= 0 ? 1 : (bits + 7) / 8;
     const uint64_t T = cdiv(n, (uint64_t)RS_TILE);
     uint32_t* hist = tmp_hist.as<uint32_t>(256 * T);
-    uint32_t* tk = passes > 1 ? tmp_pairs.as<uint32_t>(2 * n) : nullptr;
-    uint32_t* tv = tk ? tk + n : nullptr;
-    const uint32_t* sk = keys_in;
+    K* tk = nullptr;
+    uint32_t* tv = nullptr;
+    if (passes > 1) {
+        auto* raw = tmp_pairs.as<uint8_t>(n * (sizeof(K) + 4) + 16);
+        tk = reinterpret_cast<K*>(raw);
+        tv = vals_out ? reinterpret_cast<uint32_t*>(raw + n * sizeof(K)) : nullptr;
+    }
+    const K* sk = keys_in;
     const uint32_t* sv = vals_in;  // nullptr: the values are 0..n-1
     for (int p = 0; p < passes; ++p) {
         // the last pass lands in the caller's arrays
         const bool to_out = ((passes - 1 - p) & 1) == 0;
-        uint32_t* dk = to_out ? keys_out : tk;
+        K* dk = to_out ? keys_out : tk;
         uint32_t* dv = to_out ? vals_out : tv;
         const int shift = begin_bit + 8 * p;
         const int nb = bits <= 0 ? 0 : std::min(8, end_bit - shift);
         const uint32_t mask = (1u << nb) - 1u;
-        k_rs_hist<<<(unsigned)T, RS_T, 0, st>>>(sk, n, shift, mask, T, hist);
+        k_rs_hist<K><<<(unsigned)T, RS_T, 0, st>>>(sk, n, shift, mask, T, hist);
         UMCG_LAUNCHED();
         exclusive_scan_u32(hist, 256 * T, tmp_scan, st);
-        k_rs_scatter<<<(unsigned)T, RS_T, 0, st>>>(sk, sv, n, shift, mask, T, hist, dk, dv);
+        k_rs_scatter<K><<<(unsigned)T, RS_T, 0, st>>>(sk, sv, n, shift, mask, T, hist, dk, dv);
         UMCG_LAUNCHED();
         sk = dk;
         sv = dv;
     }
+}
+}  // namespace
+
+void radix_sort_pairs_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
+                          uint64_t n, int begin_bit, int end_bit, DevBuf& tmp_pairs, DevBuf& tmp_hist,
+                          DevBuf& tmp_scan, cudaStream_t st) {
+    radix_sort_impl(keys_in, keys_out, vals_in, vals_out, n, begin_bit, end_bit, tmp_pairs, tmp_hist, tmp_scan, st);
+}
+
+void radix_sort_u64(const uint64_t* keys_in, uint64_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
+                    uint64_t n, int begin_bit, int end_bit, DevBuf& tmp_pairs, DevBuf& tmp_hist, DevBuf& tmp_scan,
+                    cudaStream_t st) {
+    radix_sort_impl(keys_in, keys_out, vals_in, vals_out, n, begin_bit, end_bit, tmp_pairs, tmp_hist, tmp_scan, st);
 }
 
 }  // namespace umcg
