@@ -24,8 +24,12 @@
  *    plan's device. Host pointers are plain. Sizes are bytes or elements as
  *    named.
  *  - stream: a cudaStream_t passed as void* (NULL = legacy default stream).
- *    Compress/decompress synchronize the stream before returning (they report
- *    lengths and data-dependent errors), so the call is complete on return.
+ *    Compress/decompress wait for their device work before returning (they
+ *    report lengths and data-dependent errors), so the call is complete on
+ *    return: the last kernel of the call posts a completion ticket into
+ *    pinned host memory after everything queued before it has finished, and
+ *    the host waits for that ticket (UMCG_NO_MAILBOX=1: a plain
+ *    cudaStreamSynchronize).
  *  - A plan is immutable after creation apart from its private workspace;
  *    calls on one plan are serialized by an internal mutex. For concurrency
  *    use one handle per thread: umcg_plan_clone gives a handle with its own
