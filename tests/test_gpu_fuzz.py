@@ -8,6 +8,8 @@ outliers), the bound kind, tau over seven decades, the error split, g
 the reference's up to rounding-window codes, errors must be the reference's
 exception kinds, both decoders must agree and the bound must hold wherever
 the reference's own decode meets it."""
+import os
+
 import numpy as np
 import pytest
 
@@ -49,10 +51,14 @@ def _case(seed):
     return dim, xyz, x, g, p
 
 
+# UMCG_FUZZ_BASE=N shifts every seed by N (one-off wider sweeps of the same tests)
+FUZZ_BASE = int(os.environ.get("UMCG_FUZZ_BASE", "0"))
+
+
 @pytest.mark.parametrize("seed", range(160))
 def test_random_case_matches_reference(cuda, ref, oracle, seed):
     import torch
-    dim, xyz, x, g, p = _case(seed)
+    dim, xyz, x, g, p = _case(seed + FUZZ_BASE)
     lo, hi = xyz.min(0), xyz.max(0)
     axes = [np.linspace(lo[d], hi[d], g) for d in range(dim)]
     plan = umcg.Plan.build(axes, torch.from_numpy(np.ascontiguousarray(xyz)).cuda(), keep_coords=True)
@@ -96,7 +102,7 @@ def test_random_codec_matches_reference(cuda, ref, oracle, seed):
     and the bound holds."""
     import torch
     from helpers import check_component, lorenzo_pred
-    rng = np.random.default_rng(5000 + seed)
+    rng = np.random.default_rng(5000 + seed + FUZZ_BASE)
     D = int(rng.integers(1, 4))
     dims = [int(rng.integers(2, {1: 20000, 2: 200, 3: 40}[D])) for _ in range(D)]
     n = int(np.prod(dims))
