@@ -553,14 +553,18 @@ struct Mailbox {
         static const bool on = std::getenv("UMCG_NO_MAILBOX") == nullptr;
         return on;
     }
-    // Poll until the ticket shows seq. Every ~1k polls the stream is queried,
-    // so a failed launch or a faulted kernel surfaces as its CUDA error
-    // instead of an endless wait.
+    // Poll until the ticket shows seq (a pause per poll: the sibling
+    // hyperthread and the other host threads' driver calls are not starved).
+    // Every 16k polls (~1 ms) the stream is queried, so a failed launch or a
+    // faulted kernel surfaces as its CUDA error instead of an endless wait.
     void wait(cudaStream_t st) {
         const volatile uint64_t* t = ticket();
         for (uint32_t spins = 1;; ++spins) {
             if (*t == seq) break;
-            if ((spins & 0x3ffu) == 0) {
+#if defined(__x86_64__) || defined(__i386__)
+            __builtin_ia32_pause();
+#endif
+            if ((spins & 0x3fffu) == 0) {
                 const cudaError_t q = cudaStreamQuery(st);
                 if (q == cudaSuccess) {
                     if (*t == seq) break;
